@@ -1,0 +1,117 @@
+/*
+ * ccf.h — C-ABI of the B200-native CCF spectral Navier–Stokes hot path
+ * (arXiv 2206.04827; drop-in for the reference `cylspec` C++ API).
+ *
+ * Conventions (identical to the reference, proj/include/cylspec/coeffs.hpp:16-45,
+ * proj/include/cylspec/grid.hpp:37-50):
+ *   - coefficient tensors: complex<double> interleaved (re, im), index (l*n + k)*m + j,
+ *     slice l carries wavenumber w = l - p/2 (slice 0 = unpaired Nyquist);
+ *   - grid fields: double, same (l, k, j) order, r_j = cos((m-1-j)pi/(m-1)),
+ *     z_k likewise, theta_l = (2l - p) pi / p.
+ * Every buffer argument may be HOST memory (pageable or pinned) or DEVICE memory of
+ * the context's GPU; the library detects which (cudaPointerGetAttributes) and
+ * stages host buffers through device memory. Calls are synchronous with respect
+ * to the host, like the reference (value semantics), and run on the context's stream.
+ *
+ * Status codes mirror the reference exception taxonomy one-to-one
+ * (proj/include/cylspec/errors.hpp:10-40); the C++ shim (cylspec_b200.hpp)
+ * rethrows the same C++ types.
+ *
+ * Restrictions of the B200 path (documented in DESIGN.md): m and n even
+ * (the reference NS pipeline already requires even m, proj/src/ptns.cpp:185),
+ * m, n <= 258 for the single-CTA ADI tile.
+ */
+#ifndef CCF_H_
+#define CCF_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum ccf_status {
+    CCF_OK = 0,
+    CCF_DOMAIN_ERROR = 1,          /* cylspec::DomainError */
+    CCF_CONFIG_ERROR = 2,          /* cylspec::ConfigError */
+    CCF_SINGULAR_OPERATOR = 3,     /* cylspec::SingularOperatorError{shift_index} */
+    CCF_NON_CONVERGENCE = 4,       /* cylspec::NonConvergenceError{residual_history} */
+    CCF_NOT_INCOMPRESSIBLE = 5,    /* cylspec::NotIncompressibleError{divergence} */
+    CCF_NUMERICAL_ERROR = 6,       /* cylspec::NumericalError */
+    CCF_CUDA_ERROR = 7,            /* device / driver failure (no reference analogue) */
+    CCF_INTERNAL_ERROR = 9
+} ccf_status;
+
+typedef struct ccf_ctx ccf_ctx;
+typedef struct ccf_ns_state ccf_ns_state;
+
+/* Context: one grid size, one GPU, one stream; caches shift plans and factors
+ * (ModalSolverCache, proj/include/cylspec/solvers.hpp:63-76).
+ * flags: bit 0 = Q2 endpoint-relative enclosure pad where the reference
+ * intervals overlap (off = reference semantics). */
+ccf_status ccf_ctx_create(int m, int n, int p, int device, double adi_tol, int flags, ccf_ctx** out);
+ccf_status ccf_ctx_destroy(ccf_ctx* ctx);
+/* Use an external cudaStream_t (NULL restores the context's own stream). */
+ccf_status ccf_ctx_set_stream(ccf_ctx* ctx, void* stream);
+ccf_status ccf_ctx_synchronize(ccf_ctx* ctx);
+
+/* transform.hpp:17-22 — analyze / synthesize (synthesize keeps Re only). */
+ccf_status ccf_analyze(ccf_ctx* ctx, const double* values, double* coeffs);
+ccf_status ccf_synthesize(ccf_ctx* ctx, const double* coeffs, double* values);
+
+/* calculus.hpp:15-29 on Hermitian (real-field) tensors.
+ * op: 0 derivative_r, 1 derivative_z, 2 derivative_theta, 4 divide_r,
+ *     5 horizontal_laplacian, 6 laplacian. */
+ccf_status ccf_calculus(ccf_ctx* ctx, int op, const double* in, double* out);
+
+/* solvers.hpp:86-94 */
+ccf_status ccf_poisson3d(ccf_ctx* ctx, const double* f, double* u);
+ccf_status ccf_hpoisson(ccf_ctx* ctx, const double* rhs, double* u);
+
+/* timestep.hpp:34-53 HelmholtzTensorStepper::step:
+ *   (1 - kappa * diffusivity * lap) X = sum_i bdf_i hist_i + kappa * forcing
+ * hist: nhist tensors, newest first (nhist >= order); forcing may be NULL. */
+ccf_status ccf_helmholtz_step(ccf_ctx* ctx, const double* const* hist, int nhist, int order, const double* forcing,
+                              double diffusivity, double h, double* out);
+
+/* ptns.hpp:47-70 */
+ccf_status ccf_pt_synthesize(ccf_ctx* ctx, const double* lam, const double* gam, double* vr, double* vt, double* vz);
+ccf_status ccf_pt_decompose(ccf_ctx* ctx, const double* vr, const double* vt, const double* vz, double* lam,
+                            double* gam);
+ccf_status ccf_curl_vector(ccf_ctx* ctx, const double* vr, const double* vt, const double* vz, double* or_,
+                           double* ot, double* oz);
+ccf_status ccf_curl_pt(ccf_ctx* ctx, const double* lam, const double* gam, double* lam_out, double* gam_out);
+ccf_status ccf_velocity_from_vorticity(ccf_ctx* ctx, const double* lam_w, const double* gam_w, double* lam_v,
+                                       double* gam_v);
+ccf_status ccf_nonlinear(ccf_ctx* ctx, const double* lam_v, const double* gam_v, const double* lam_w,
+                         const double* gam_w, double* lam_out, double* gam_out);
+
+/* ptns.hpp:84-127 NSStepper (ramp bootstrap). State lives on the device. */
+ccf_status ccf_ns_create(ccf_ctx* ctx, double reynolds, double h, int order, int disable_nonlinear,
+                         const double* lam0, const double* gam0, ccf_ns_state** out);
+ccf_status ccf_ns_step(ccf_ns_state* st, int nsteps);
+ccf_status ccf_ns_get_omega(ccf_ns_state* st, double* lam, double* gam, double* time, int* steps_taken);
+ccf_status ccf_ns_destroy(ccf_ns_state* st);
+
+/* Details of the last error on this context (thread-compatible, not thread-safe).
+ * kind = ccf_status; slice = Fourier slice of a failed modal solve or -1;
+ * shift_index = ADI shift of a singular operator or -1; residual history of a
+ * NonConvergenceError (up to *n_hist entries on input). */
+ccf_status ccf_get_last_error(ccf_ctx* ctx, int* kind, int* slice, int* shift_index, double* residual_hist,
+                              int* n_hist, char* msg, int cap);
+
+/* Statistics since the last reset: ADI solves, iterations executed (J x rounds),
+ * max rounds, worst final residual; kernel launches issued. */
+ccf_status ccf_get_stats(ccf_ctx* ctx, long* adi_subproblems, long* adi_iterations, int* max_rounds,
+                         double* worst_residual, long* kernel_launches);
+ccf_status ccf_reset_stats(ccf_ctx* ctx);
+
+/* Shift plan of the (|w|, poisson|scale) modal solver of this context (for parity
+ * tests against the reference plan): info = {a, b, c, d, gamma, alpha, modulus, J}. */
+ccf_status ccf_modal_plan(ccf_ctx* ctx, int w, double scale, int poisson, double* info, double* u, double* v,
+                          int cap);
+
+const char* ccf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CCF_H_ */

@@ -1,0 +1,316 @@
+"""B200-native (sm_100a) CCF spectral Navier–Stokes hot path — Python host mirror.
+
+The product is the C-ABI shared library ``lib/libccf.so`` (include/ccf.h); this
+module is a thin ctypes binding that mirrors the reference ``cylspec`` API names
+(proj/include/cylspec/*.hpp) for tests, benchmarks and Python users. Tensors use
+the reference layout: numpy complex128 arrays of shape (p, n, m) for coefficient
+tensors (slice l carries wavenumber l - p/2) and float64 (p, n, m) for grid fields.
+
+There is no CPU fallback: if the CUDA library or a GPU is missing, every call
+raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libccf.so")
+
+# Status codes mirror proj/include/cylspec/errors.hpp:10-40 (include/ccf.h).
+CCF_OK = 0
+STATUS_NAMES = {1: "DomainError", 2: "ConfigError", 3: "SingularOperatorError", 4: "NonConvergenceError",
+                5: "NotIncompressibleError", 6: "NumericalError", 7: "CudaError", 9: "InternalError"}
+
+
+class CCFError(RuntimeError):
+    """Base of the exception taxonomy (cylspec errors.hpp)."""
+
+    status = 9
+
+    def __init__(self, msg, slice_=-1, shift_index=-1, residual_history=()):
+        super().__init__(msg)
+        self.slice = slice_
+        self.shift_index = shift_index
+        self.residual_history = list(residual_history)
+
+
+class DomainError(CCFError, ValueError):
+    status = 1
+
+
+class ConfigError(CCFError, ValueError):
+    status = 2
+
+
+class SingularOperatorError(CCFError):
+    status = 3
+
+
+class NonConvergenceError(CCFError):
+    status = 4
+
+
+class NotIncompressibleError(CCFError):
+    status = 5
+
+
+class NumericalError(CCFError):
+    status = 6
+
+
+class CudaError(CCFError):
+    status = 7
+
+
+_ERR = {c.status: c for c in (DomainError, ConfigError, SingularOperatorError, NonConvergenceError,
+                              NotIncompressibleError, NumericalError, CudaError)}
+
+# Every extern "C" symbol include/ccf.h declares (checked by the CPU test suite).
+EXPORTS = ["ccf_ctx_create", "ccf_ctx_destroy", "ccf_ctx_set_stream", "ccf_ctx_synchronize", "ccf_analyze",
+           "ccf_synthesize", "ccf_calculus", "ccf_poisson3d", "ccf_hpoisson", "ccf_helmholtz_step",
+           "ccf_pt_synthesize", "ccf_pt_decompose", "ccf_curl_vector", "ccf_curl_pt", "ccf_velocity_from_vorticity",
+           "ccf_nonlinear", "ccf_ns_create", "ccf_ns_step", "ccf_ns_get_omega", "ccf_ns_destroy",
+           "ccf_get_last_error", "ccf_get_stats", "ccf_reset_stats", "ccf_modal_plan", "ccf_version"]
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the CUDA library in-tree for sm_100a (nvcc; no GPU needed)."""
+    if force or not os.path.exists(LIB_PATH):
+        subprocess.run(["make", "-s", "-j8", "-C", _HERE], check=True)
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise CudaError(f"CUDA library missing: {LIB_PATH} (run build())")
+        L = C.CDLL(LIB_PATH)
+        dp = C.POINTER(C.c_double)
+        vp = C.c_void_p
+        L.ccf_version.restype = C.c_char_p
+        L.ccf_create_error.restype = C.c_char_p
+        L.ccf_ctx_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.POINTER(vp)]
+        for name in EXPORTS:
+            if name not in ("ccf_version",):
+                getattr(L, name).restype = C.c_int
+        L.ccf_ctx_destroy.argtypes = [vp]
+        L.ccf_ctx_set_stream.argtypes = [vp, vp]
+        L.ccf_ctx_synchronize.argtypes = [vp]
+        L.ccf_analyze.argtypes = [vp, vp, vp]
+        L.ccf_synthesize.argtypes = [vp, vp, vp]
+        L.ccf_calculus.argtypes = [vp, C.c_int, vp, vp]
+        L.ccf_poisson3d.argtypes = [vp, vp, vp]
+        L.ccf_hpoisson.argtypes = [vp, vp, vp]
+        L.ccf_helmholtz_step.argtypes = [vp, C.POINTER(vp), C.c_int, C.c_int, vp, C.c_double, C.c_double, vp]
+        L.ccf_pt_synthesize.argtypes = [vp, vp, vp, vp, vp, vp]
+        L.ccf_pt_decompose.argtypes = [vp, vp, vp, vp, vp, vp]
+        L.ccf_curl_vector.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+        L.ccf_curl_pt.argtypes = [vp, vp, vp, vp, vp]
+        L.ccf_velocity_from_vorticity.argtypes = [vp, vp, vp, vp, vp]
+        L.ccf_nonlinear.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+        L.ccf_ns_create.argtypes = [vp, C.c_double, C.c_double, C.c_int, C.c_int, vp, vp, C.POINTER(vp)]
+        L.ccf_ns_step.argtypes = [vp, C.c_int]
+        L.ccf_ns_get_omega.argtypes = [vp, vp, vp, dp, C.POINTER(C.c_int)]
+        L.ccf_ns_destroy.argtypes = [vp]
+        L.ccf_get_last_error.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), dp,
+                                         C.POINTER(C.c_int), C.c_char_p, C.c_int]
+        L.ccf_get_stats.argtypes = [vp, C.POINTER(C.c_long), C.POINTER(C.c_long), C.POINTER(C.c_int), dp,
+                                    C.POINTER(C.c_long)]
+        L.ccf_reset_stats.argtypes = [vp]
+        L.ccf_modal_plan.argtypes = [vp, C.c_int, C.c_double, C.c_int, dp, dp, dp, C.c_int]
+        _lib = L
+    return _lib
+
+
+def _addr(a):
+    """Host numpy array or torch CUDA tensor -> raw pointer."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    return C.c_void_p(a.ctypes.data)
+
+
+def _c128(x):
+    return np.ascontiguousarray(x, dtype=np.complex128)
+
+
+class Context:
+    """One grid size on one GPU (ccf_ctx). Mirrors the reference free functions."""
+
+    def __init__(self, m, n, p, device=0, adi_tol=1e-12, q2_endpoint_pad=False):
+        self.m, self.n, self.p = int(m), int(n), int(p)
+        h = C.c_void_p()
+        st = lib().ccf_ctx_create(self.m, self.n, self.p, int(device), C.c_double(adi_tol),
+                                  int(bool(q2_endpoint_pad)), C.byref(h))
+        if st != 0:
+            raise _ERR.get(st, CCFError)(lib().ccf_create_error().decode())
+        self.h = h
+
+    # ---- errors
+    def _check(self, st):
+        if st == 0:
+            return
+        kind, sl, sh = C.c_int(), C.c_int(), C.c_int()
+        hist = (C.c_double * 8)()
+        nh = C.c_int(8)
+        msg = C.create_string_buffer(1024)
+        lib().ccf_get_last_error(self.h, C.byref(kind), C.byref(sl), C.byref(sh), hist, C.byref(nh), msg, 1024)
+        raise _ERR.get(st, CCFError)(msg.value.decode(), sl.value, sh.value, list(hist)[: min(nh.value, 8)])
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ccf_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def shape(self):
+        return (self.p, self.n, self.m)
+
+    def _out_c(self):
+        return np.zeros(self.shape(), np.complex128)
+
+    # ---- transforms (transform.hpp:17-22)
+    def analyze(self, values):
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        out = self._out_c()
+        self._check(lib().ccf_analyze(self.h, _addr(v), _addr(out)))
+        return out
+
+    def synthesize(self, coeffs):
+        c = _c128(coeffs)
+        out = np.zeros(self.shape())
+        self._check(lib().ccf_synthesize(self.h, _addr(c), _addr(out)))
+        return out
+
+    _CALC = {"dr": 0, "dz": 1, "dtheta": 2, "divide_r": 4, "hlap": 5, "lap": 6}
+
+    def calculus(self, op, coeffs):
+        c = _c128(coeffs)
+        out = self._out_c()
+        self._check(lib().ccf_calculus(self.h, self._CALC[op], _addr(c), _addr(out)))
+        return out
+
+    # ---- solvers (solvers.hpp:86-94)
+    def solve_poisson_3d(self, f):
+        c = _c128(f)
+        out = self._out_c()
+        self._check(lib().ccf_poisson3d(self.h, _addr(c), _addr(out)))
+        return out
+
+    def solve_horizontal_poisson(self, rhs):
+        c = _c128(rhs)
+        out = self._out_c()
+        self._check(lib().ccf_hpoisson(self.h, _addr(c), _addr(out)))
+        return out
+
+    def helmholtz_step(self, history, order, diffusivity, h, forcing=None):
+        hs = [_c128(x) for x in history]
+        arr = (C.c_void_p * len(hs))(*[x.ctypes.data for x in hs])
+        fc = _c128(forcing) if forcing is not None else None
+        out = self._out_c()
+        self._check(lib().ccf_helmholtz_step(self.h, arr, len(hs), int(order), _addr(fc), C.c_double(diffusivity),
+                                             C.c_double(h), _addr(out)))
+        return out
+
+    # ---- PT / NS (ptns.hpp:47-70)
+    def pt_synthesize(self, lam, gam):
+        o = [self._out_c() for _ in range(3)]
+        self._check(lib().ccf_pt_synthesize(self.h, _addr(_c128(lam)), _addr(_c128(gam)), *[_addr(x) for x in o]))
+        return tuple(o)
+
+    def pt_decompose(self, vr, vt, vz):
+        o = [self._out_c() for _ in range(2)]
+        self._check(lib().ccf_pt_decompose(self.h, _addr(_c128(vr)), _addr(_c128(vt)), _addr(_c128(vz)),
+                                           *[_addr(x) for x in o]))
+        return tuple(o)
+
+    def curl_vector(self, vr, vt, vz):
+        o = [self._out_c() for _ in range(3)]
+        self._check(lib().ccf_curl_vector(self.h, _addr(_c128(vr)), _addr(_c128(vt)), _addr(_c128(vz)),
+                                          *[_addr(x) for x in o]))
+        return tuple(o)
+
+    def curl_pt(self, lam, gam):
+        o = [self._out_c() for _ in range(2)]
+        self._check(lib().ccf_curl_pt(self.h, _addr(_c128(lam)), _addr(_c128(gam)), *[_addr(x) for x in o]))
+        return tuple(o)
+
+    def velocity_from_vorticity(self, lam_w, gam_w):
+        o = [self._out_c() for _ in range(2)]
+        self._check(lib().ccf_velocity_from_vorticity(self.h, _addr(_c128(lam_w)), _addr(_c128(gam_w)),
+                                                      *[_addr(x) for x in o]))
+        return tuple(o)
+
+    def nonlinear_term(self, lam_v, gam_v, lam_w, gam_w):
+        o = [self._out_c() for _ in range(2)]
+        self._check(lib().ccf_nonlinear(self.h, _addr(_c128(lam_v)), _addr(_c128(gam_v)), _addr(_c128(lam_w)),
+                                        _addr(_c128(gam_w)), *[_addr(x) for x in o]))
+        return tuple(o)
+
+    # ---- introspection
+    def modal_plan(self, w, scale=1.0, poisson=True):
+        info = np.zeros(8)
+        u = np.zeros(256)
+        v = np.zeros(256)
+        dp = C.POINTER(C.c_double)
+        self._check(lib().ccf_modal_plan(self.h, int(w), C.c_double(scale), int(poisson), info.ctypes.data_as(dp),
+                                         u.ctypes.data_as(dp), v.ctypes.data_as(dp), 256))
+        J = int(info[7])
+        return dict(a=info[0], b=info[1], c=info[2], d=info[3], gamma=info[4], alpha=info[5], modulus=info[6], J=J,
+                    u=u[:J].copy(), v=v[:J].copy())
+
+    def stats(self):
+        s, it, r, lch = C.c_long(), C.c_long(), C.c_int(), C.c_long()
+        w = C.c_double()
+        self._check(lib().ccf_get_stats(self.h, C.byref(s), C.byref(it), C.byref(r), C.byref(w), C.byref(lch)))
+        return dict(adi_iterations=it.value, kernel_launches=lch.value)
+
+    def reset_stats(self):
+        self._check(lib().ccf_reset_stats(self.h))
+
+
+class NSStepper:
+    """proj/include/cylspec/ptns.hpp:104-127 NSStepper on the device (ramp bootstrap)."""
+
+    def __init__(self, ctx: Context, lam0, gam0, reynolds, h, order=4, disable_nonlinear=False):
+        self.ctx = ctx
+        st = C.c_void_p()
+        ctx._check(lib().ccf_ns_create(ctx.h, C.c_double(reynolds), C.c_double(h), int(order), int(disable_nonlinear),
+                                       _addr(_c128(lam0)), _addr(_c128(gam0)), C.byref(st)))
+        self.h = st
+
+    def step(self, nsteps=1):
+        self.ctx._check(lib().ccf_ns_step(self.h, int(nsteps)))
+
+    def omega(self, out_lam=None, out_gam=None):
+        lam = out_lam if out_lam is not None else self.ctx._out_c()
+        gam = out_gam if out_gam is not None else self.ctx._out_c()
+        t = C.c_double()
+        s = C.c_int()
+        self.ctx._check(lib().ccf_ns_get_omega(self.h, _addr(lam), _addr(gam), C.byref(t), C.byref(s)))
+        self.time, self.steps_taken = t.value, s.value
+        return lam, gam
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ccf_ns_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,62 @@
+// Shared device-side definitions for the B200 CCF kernels (sm_100a).
+//
+// Data layout in HBM ("CCF-H", half-spectrum, parity-compressed):
+//   tensor[slot][plane][k][jj]   plane 0 = Re, 1 = Im;  k in [0,n), jj in [0,m/2)
+//   slot s < p/2  -> wavenumber w = s ; slot p/2 -> Nyquist w = -p/2 (reference slice l = 0)
+//   coefficient (j, k) of slot s lives at jj = (j - j0)/2 where j0 = (w + cls) mod 2,
+//   cls = 0 for scalar-parity fields (j+w even), 1 for azimuthal-flip fields
+//   (proj/src/coeffs.cpp:50-59). The opposite-parity coefficients are identically
+//   zero on the whole hot path, so they are not stored.
+// A "full" slot table (slot = reference slice l, w = l - p/2) is also supported
+// for API calls on non-Hermitian input.
+#pragma once
+
+#include <cstdint>
+
+namespace ccf {
+
+constexpr int kMaxSrc = 8;
+
+// Per (solver set, slot) descriptor of the packed operator blocks (offsets in doubles).
+struct AdiSlot {
+    int J;        // shifts per round
+    int j0;       // j-parity of the (scalar-class) unknowns of this slot
+    long left;    // J x M x 16  : [mul(uC-A) -2..3 | L(2) | piv | Uf(5) | inv | pad]
+    long right0;  // J x N x 12  (k-parity 0): [mul -1..2 | L | piv | Uf(3) | inv | pad 2]
+    long right1;  // J x N x 12  (k-parity 1)
+    long sleft;   // M x 24      : [R2 -2..3 (first 0) | A -2..3 | C -2..3 | pad 6]
+    long sright0; // N x 24      : [C02 -1..2 (first 0) | LU(B^T): L, piv, Uf(3), inv | B^T -1..2 | D^T -1..2 |
+                  //                restart mul (v_0 B + D)^T -1..2 | pad 2]
+    long sright1;
+    long ds;      // J : u_j - v_j
+};
+constexpr int kLeftW = 16, kRightW = 12, kStatW = 24;
+
+struct AdiTask {
+    int tensor, slot, k0, plane;
+};
+
+// Tensor geometry in the compressed layout.
+struct Geo {
+    int m, n, p, mh, nh, nslots;
+    long plane_stride;  // n * mh
+    long slot_stride;   // 2 * n * mh
+};
+
+struct AdiParams {
+    Geo g;
+    int M, N, pitch, round, ntasks;
+    const double* coef;
+    const AdiSlot* slots;
+    const AdiTask* tasks;
+    const double* src[2][kMaxSrc];
+    double wsrc[2][kMaxSrc];
+    int nsrc[2];
+    double* out[2];
+    double* eprime;  // ntasks x M x N scratch
+    double* res2;    // [2][nslots]
+    double* e2;      // [2][nslots]
+    const int* active;  // [2][nslots]
+};
+
+}  // namespace ccf

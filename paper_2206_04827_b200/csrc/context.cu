@@ -1,0 +1,271 @@
+// Host-side context implementation: device memory, solver-set cache
+// (ModalSolverCache, proj/src/solvers.cpp:100-109), ADI round driver.
+#include <algorithm>
+#include <cstring>
+
+#include "context.hpp"
+
+namespace ccf {
+
+void DBuf::alloc(size_t count) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = count;
+    if (count) CCF_CUDA(cudaMalloc(&p, count * sizeof(double)));
+}
+DBuf::~DBuf() {
+    if (p) cudaFree(p);
+}
+DBuf& DBuf::operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+        if (p) cudaFree(p);
+        p = o.p;
+        n = o.n;
+        o.p = nullptr;
+        o.n = 0;
+    }
+    return *this;
+}
+
+DevSet::~DevSet() {
+    if (coef) cudaFree(coef);
+    if (slots) cudaFree(slots);
+    if (J) cudaFree(J);
+    for (auto* t : tasks)
+        if (t) cudaFree(t);
+}
+
+static Geo make_geo(int m, int n, int p, int nslots) {
+    Geo g{};
+    g.m = m;
+    g.n = n;
+    g.p = p;
+    g.mh = m / 2;
+    g.nh = n / 2;
+    g.nslots = nslots;
+    g.plane_stride = long(n) * (m / 2);
+    g.slot_stride = 2 * g.plane_stride;
+    return g;
+}
+
+Ctx::Ctx(int m_, int n_, int p_, int device_, double tol_, int flags_)
+    : m(m_), n(n_), p(p_), device(device_), flags(flags_), tol(tol_) {
+    if (m < 4 || n < 4) throw Error(DOMAIN_ERROR, "GridSpec: m and n must be at least 4");
+    if (p < 2 || p % 2 != 0) throw Error(DOMAIN_ERROR, "GridSpec: p must be even and at least 2");
+    if (m % 2 || n % 2) throw Error(DOMAIN_ERROR, "ccf: the B200 path requires even m and n (parity-compressed layout)");
+    if (m > 320 || n > 320) throw Error(DOMAIN_ERROR, "ccf: m, n <= 320 (single-CTA ADI tile)");
+    if (!(tol > 0.0) || tol >= 1.0) throw Error(DOMAIN_ERROR, "compute_shifts: tol must be in (0,1)");
+    CCF_CUDA(cudaSetDevice(device));
+    CCF_CUDA(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
+    stream = own_stream;
+    gh = make_geo(m, n, p, p / 2 + 1);
+    gf = make_geo(m, n, p, p);
+    M = (m - 2) / 2;
+    N = (n - 2) / 2;
+    pitch = ((n / 2) + 3) | 1;
+    sizeops = std::make_unique<SizeOps>(m, n);
+    // workspace
+    const int cap = p;  // max slots (full mode)
+    ws.cap_slots = cap;
+    CCF_CUDA(cudaMalloc(&ws.res2, sizeof(double) * 2 * cap));
+    CCF_CUDA(cudaMalloc(&ws.e2, sizeof(double) * 2 * cap));
+    CCF_CUDA(cudaMalloc(&ws.history, sizeof(double) * 2 * cap * 4));
+    CCF_CUDA(cudaMalloc(&ws.active, sizeof(int) * 2 * cap));
+    CCF_CUDA(cudaMalloc(&ws.rounds, sizeof(int) * 2 * cap));
+    CCF_CUDA(cudaMalloc(&ws.err, sizeof(int) * 4));
+    CCF_CUDA(cudaMalloc(&ws.flag, sizeof(int) * 4));
+    CCF_CUDA(cudaMalloc(&ws.iters, sizeof(unsigned long long) * 2));
+    CCF_CUDA(cudaMemset(ws.err, 0, sizeof(int) * 4));
+    CCF_CUDA(cudaMemset(ws.iters, 0, sizeof(unsigned long long) * 2));
+    ws.eprime.alloc(size_t(2) * cap * 4 * size_t(M) * N);
+    {
+        int optin = 0;
+        CCF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        cudaFuncAttributes fa{};
+        CCF_CUDA(cudaFuncGetAttributes(&fa, adi_kernel));
+        const size_t need = size_t(m / 2 + 6) * pitch * sizeof(double);
+        if (need + fa.sharedSizeBytes > size_t(optin))
+            throw Error(DOMAIN_ERROR, "ccf: ADI tile exceeds shared memory (m, n too large for the single-CTA kernel)");
+        CCF_CUDA(cudaFuncSetAttribute(adi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(optin - fa.sharedSizeBytes)));
+    }
+}
+
+Ctx::~Ctx() {
+    sets.clear();
+    cudaFree(ws.res2);
+    cudaFree(ws.e2);
+    cudaFree(ws.history);
+    cudaFree(ws.active);
+    cudaFree(ws.rounds);
+    cudaFree(ws.err);
+    cudaFree(ws.flag);
+    cudaFree(ws.iters);
+    if (own_stream) cudaStreamDestroy(own_stream);
+}
+
+void Ctx::sync() { CCF_CUDA(cudaStreamSynchronize(stream)); }
+
+bool Ctx::is_device_ptr(const void* ptr) const {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+DevSet& Ctx::set(bool full, bool poisson, double scale) {
+    auto key = std::make_tuple(int(full), int(poisson), poisson ? 1.0 : scale);
+    auto it = sets.find(key);
+    if (it != sets.end()) return *it->second;
+    const Geo& g = geo(full);
+    std::vector<int> slot_w(size_t(g.nslots));
+    for (int s = 0; s < g.nslots; ++s) slot_w[size_t(s)] = full ? s - p / 2 : (s == p / 2 ? -p / 2 : s);
+    auto ds = std::make_unique<DevSet>();
+    ds->host = build_solver_set(*sizeops, slot_w, poisson, scale, tol, radial_cache, (flags & 1) != 0);
+    const SolverSet& h = ds->host;
+    CCF_CUDA(cudaMalloc(&ds->coef, h.coef.size() * sizeof(double)));
+    CCF_CUDA(cudaMemcpy(ds->coef, h.coef.data(), h.coef.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CCF_CUDA(cudaMalloc(&ds->slots, h.slots.size() * sizeof(AdiSlot)));
+    CCF_CUDA(cudaMemcpy(ds->slots, h.slots.data(), h.slots.size() * sizeof(AdiSlot), cudaMemcpyHostToDevice));
+    std::vector<int> J(h.slots.size());
+    for (size_t s = 0; s < J.size(); ++s) J[s] = h.slots[s].J;
+    CCF_CUDA(cudaMalloc(&ds->J, J.size() * sizeof(int)));
+    CCF_CUDA(cudaMemcpy(ds->J, J.data(), J.size() * sizeof(int), cudaMemcpyHostToDevice));
+    // tasks: longest slots first (load balance of the J-heterogeneous batch)
+    std::vector<int> order(size_t(g.nslots));
+    for (int s = 0; s < g.nslots; ++s) order[size_t(s)] = s;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return J[size_t(a)] > J[size_t(b)]; });
+    for (int nt = 1; nt <= 2; ++nt) {
+        std::vector<AdiTask> tasks;
+        for (int s : order)
+            for (int t = 0; t < nt; ++t)
+                for (int k0 = 0; k0 < 2; ++k0)
+                    for (int pl = 0; pl < 2; ++pl) tasks.push_back({t, s, k0, pl});
+        ds->ntasks[nt - 1] = int(tasks.size());
+        CCF_CUDA(cudaMalloc(&ds->tasks[nt - 1], tasks.size() * sizeof(AdiTask)));
+        CCF_CUDA(cudaMemcpy(ds->tasks[nt - 1], tasks.data(), tasks.size() * sizeof(AdiTask), cudaMemcpyHostToDevice));
+    }
+    DevSet& ref = *ds;
+    sets[key] = std::move(ds);
+    return ref;
+}
+
+void Ctx::run_adi(DevSet& set, bool full, int ntensor, const double* const* src0, const double* w0, int n0,
+                  const double* const* src1, const double* w1, int n1, double* out0, double* out1) {
+    const Geo& g = geo(full);
+    AdiParams P{};
+    P.g = g;
+    P.M = M;
+    P.N = N;
+    P.pitch = pitch;
+    P.ntasks = set.ntasks[ntensor - 1];
+    P.coef = set.coef;
+    P.slots = set.slots;
+    P.tasks = set.tasks[ntensor - 1];
+    P.nsrc[0] = n0;
+    P.nsrc[1] = n1;
+    for (int i = 0; i < n0; ++i) {
+        P.src[0][i] = src0[i];
+        P.wsrc[0][i] = w0[i];
+    }
+    for (int i = 0; i < n1; ++i) {
+        P.src[1][i] = src1[i];
+        P.wsrc[1][i] = w1[i];
+    }
+    P.out[0] = out0;
+    P.out[1] = out1;
+    P.eprime = ws.eprime.p;
+    P.res2 = ws.res2;
+    P.e2 = ws.e2;
+    P.active = ws.active;
+    const int nts = ntensor * g.nslots;
+    CCF_CUDA(cudaMemsetAsync(ws.res2, 0, sizeof(double) * nts, stream));
+    CCF_CUDA(cudaMemsetAsync(ws.e2, 0, sizeof(double) * nts, stream));
+    std::vector<int> ones(size_t(nts), 1);
+    CCF_CUDA(cudaMemcpyAsync(ws.active, ones.data(), sizeof(int) * nts, cudaMemcpyHostToDevice, stream));
+    CCF_CUDA(cudaStreamSynchronize(stream));  // `ones` is a host temporary
+    const int threads = std::min(128, ((std::max(g.mh, g.nh) + 31) / 32) * 32);
+    const size_t smem = size_t(g.mh + 6) * pitch * sizeof(double);
+    RoundCheck rc{};
+    rc.ntensor = ntensor;
+    rc.nslots = g.nslots;
+    rc.tol = tol;
+    rc.res2 = ws.res2;
+    rc.e2 = ws.e2;
+    rc.active = ws.active;
+    rc.history = ws.history;
+    rc.rounds = ws.rounds;
+    rc.err = ws.err;
+    rc.J = set.J;
+    rc.iters = ws.iters;
+    for (int round = 0; round < 4; ++round) {
+        P.round = round;
+        adi_kernel<<<P.ntasks, threads, smem, stream>>>(P);
+        rc.round = round;
+        adi_round_check<<<(nts + 127) / 128, 128, 0, stream>>>(rc);
+        launches += 2;
+    }
+    CCF_CUDA(cudaGetLastError());
+}
+
+void Ctx::check_adi_error(bool full) {
+    int e[4];
+    CCF_CUDA(cudaMemcpyAsync(e, ws.err, sizeof(e), cudaMemcpyDeviceToHost, stream));
+    sync();
+    if (e[0] == 0) return;
+    const Geo& g = geo(full);
+    std::vector<double> hist(4);
+    CCF_CUDA(cudaMemcpy(hist.data(), ws.history + size_t(e[1] * g.nslots + e[2]) * 4, sizeof(double) * 4,
+                        cudaMemcpyDeviceToHost));
+    CCF_CUDA(cudaMemset(ws.err, 0, sizeof(int) * 4));
+    const int s = e[2];
+    const int l = full ? s : (s == p / 2 ? 0 : s + p / 2);
+    Error err(NON_CONVERGENCE, "modal solve failed for Fourier slice " + std::to_string(l) +
+                                   ": ADI did not converge: relative residual " + std::to_string(hist[3]) +
+                                   " after 4 rounds");
+    err.slice = l;
+    err.history = hist;
+    throw err;
+}
+
+void Ctx::require_finite(const double* dptr, long count, const char* what) {
+    CCF_CUDA(cudaMemsetAsync(ws.flag, 0, sizeof(int), stream));
+    finite_check_kernel<<<std::min<long>(1184, (count + 255) / 256), 256, 0, stream>>>(dptr, count, ws.flag);
+    ++launches;
+    int f = 0;
+    CCF_CUDA(cudaMemcpyAsync(&f, ws.flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    sync();
+    if (f) throw Error(NUMERICAL, std::string(what) + ": non-finite right-hand side");
+}
+
+void Ctx::load_coeff(const double* ref, double* dst, bool full, int cls, int slot) {
+    const long nref = 2L * m * n * p;
+    const double* dref = ref;
+    if (!is_device_ptr(ref)) {
+        if (stage_in[slot].n < size_t(nref)) stage_in[slot].alloc(size_t(nref));
+        CCF_CUDA(cudaMemcpyAsync(stage_in[slot].p, ref, sizeof(double) * nref, cudaMemcpyHostToDevice, stream));
+        dref = stage_in[slot].p;
+    }
+    const Geo& g = geo(full);
+    const long total = long(g.nslots) * g.slot_stride;
+    ref_to_h_kernel<<<std::min<long>(4736, (total + 255) / 256), 256, 0, stream>>>(dref, dst, g, int(full), cls);
+    ++launches;
+}
+
+void Ctx::store_coeff(const double* src, double* ref, bool full, int cls, int slot) {
+    const long nref = 2L * m * n * p;
+    double* dref = ref;
+    const bool host = !is_device_ptr(ref);
+    if (host) {
+        if (stage_out[slot].n < size_t(nref)) stage_out[slot].alloc(size_t(nref));
+        dref = stage_out[slot].p;
+    }
+    const Geo& g = geo(full);
+    const long total = long(p) * n * m;
+    h_to_ref_kernel<<<std::min<long>(4736, (total + 255) / 256), 256, 0, stream>>>(src, dref, g, int(full), cls);
+    ++launches;
+    if (host) CCF_CUDA(cudaMemcpyAsync(ref, dref, sizeof(double) * nref, cudaMemcpyDeviceToHost, stream));
+}
+
+}  // namespace ccf

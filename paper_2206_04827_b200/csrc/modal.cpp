@@ -1,0 +1,280 @@
+// Host builder for packed ADI operator blocks (see modal.hpp).
+#include "modal.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+namespace ccf {
+
+namespace {
+
+Dense parity_block(const Dense& M, int p) {
+    const int n = (M.r - p + 1) / 2;
+    Dense b(n, n);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) b(i, j) = M(2 * i + p, 2 * j + p);
+    return b;
+}
+
+Dense scaled(const Dense& a, double s) {
+    Dense o = a;
+    for (double& x : o.a) x *= s;
+    return o;
+}
+
+Dense axpby(double al, const Dense& a, double be, const Dense& b) {
+    Dense o = a;
+    for (size_t i = 0; i < o.a.size(); ++i) o.a[i] = al * a.a[i] + be * b.a[i];
+    return o;
+}
+
+// sum of two compressed bands with identical shape
+CBand cb_axpy(double al, const CBand& x, double be, const CBand& y) {
+    CBand o = x;
+    for (size_t i = 0; i < o.v.size(); ++i) o.v[i] = al * x.v[i] + be * y.v[i];
+    return o;
+}
+
+}  // namespace
+
+SizeOps::SizeOps(int m_, int n_) : m(m_), n(n_), ur(m_), uz(n_) {
+    R2rec = recombine(ur.r2);
+    C02recZ = recombine(uz.c02);
+    D2recZ = recombine(uz.d2);
+}
+
+Range radial_range(const SizeOps& so, int w, bool q2_pad) {
+    const Dense lw = recombine(radial_laplacian(so.ur, w));
+    std::vector<Dense> As{parity_block(lw, 0), parity_block(lw, 1)};
+    std::vector<Dense> Cs{parity_block(so.R2rec, 0), parity_block(so.R2rec, 1)};
+    return padded_range(As, Cs, q2_pad);
+}
+
+Range vertical_range(SizeOps& so, bool q2_pad) {
+    const Dense negd2 = scaled(so.D2recZ, -1.0);
+    std::vector<Dense> As{parity_block(negd2, 0), parity_block(negd2, 1)};
+    std::vector<Dense> Cs{parity_block(so.C02recZ, 0), parity_block(so.C02recZ, 1)};
+    return padded_range(As, Cs, q2_pad);
+}
+
+SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poisson, double scale, double tol,
+                           std::map<int, Range>& radial_cache, bool q2_pad) {
+    const int m = so.m, n = so.n, M = (m - 2) / 2, N = (n - 2) / 2, mh = m / 2, nh = n / 2;
+    SolverSet set;
+    set.poisson = poisson;
+    set.scale = scale;
+    set.tol = tol;
+    const int S = int(slot_w.size());
+    set.plans.resize(size_t(S));
+    set.slots.resize(size_t(S));
+
+    // unique |w| -> radial ranges (parallel over wavenumbers: O(m^3) QR each)
+    std::vector<int> need;
+    for (int w : slot_w)
+        if (!radial_cache.count(std::abs(w))) need.push_back(std::abs(w));
+    std::sort(need.begin(), need.end());
+    need.erase(std::unique(need.begin(), need.end()), need.end());
+    if (!need.empty()) {
+        std::vector<Range> res(need.size());
+        std::vector<std::string> errs(need.size());
+        std::vector<int> codes(need.size(), 0);
+        const int nth = std::max(1, std::min<int>(int(std::thread::hardware_concurrency()), int(need.size())));
+        std::vector<std::thread> pool;
+        std::atomic<size_t> next{0};
+        for (int q = 0; q < nth; ++q)
+            pool.emplace_back([&] {
+                for (;;) {
+                    const size_t i = next.fetch_add(1);
+                    if (i >= need.size()) break;
+                    try {
+                        res[i] = radial_range(so, need[i], false);
+                    } catch (const Error& e) {
+                        codes[i] = e.status;
+                        errs[i] = e.what();
+                    }
+                }
+            });
+        for (auto& th : pool) th.join();
+        for (size_t i = 0; i < need.size(); ++i) {
+            if (codes[i]) throw Error(codes[i], errs[i]);
+            radial_cache[need[i]] = res[i];
+        }
+    }
+    const Range vert = vertical_range(so, false);
+
+    // per |w| block cache
+    std::map<int, AdiSlot> built;
+    std::vector<double>& C = set.coef;
+    auto alloc = [&](size_t count) {
+        const long off = long(C.size());
+        C.resize(C.size() + count, 0.0);
+        return off;
+    };
+
+    // right-side operators (independent of w)
+    const Dense Bt = so.C02recZ, Dt = so.D2recZ;
+    CBand Btc[2], Dtc[2], C02c[2];
+    for (int k0 = 0; k0 < 2; ++k0) {
+        Btc[k0] = compress(Bt, k0, N, N, -1, 2);
+        Dtc[k0] = compress(Dt, k0, N, N, -1, 2);
+        C02c[k0] = compress(so.uz.c02, k0, N, nh, 0, 2);
+    }
+    for (int s = 0; s < S; ++s) {
+        const int w = slot_w[size_t(s)], aw = std::abs(w);
+        if (built.count(aw)) {
+            set.slots[size_t(s)] = built[aw];
+            for (int q = 0; q < s; ++q)
+                if (std::abs(slot_w[size_t(q)]) == aw) {
+                    set.plans[size_t(s)] = set.plans[size_t(q)];
+                    break;
+                }
+            set.plans[size_t(s)].w = w;
+            continue;
+        }
+        const int j0 = aw & 1;  // scalar class: j + w even
+        const Dense lw = radial_laplacian(so.ur, aw);
+        Dense Af, Cf;
+        if (poisson) {
+            Af = lw;
+            Cf = so.ur.r2;
+        } else {
+            Af = axpby(1.0, so.ur.r2, -scale, lw);
+            Cf = scaled(so.ur.r2, -scale);
+        }
+        const Dense Ar = recombine(Af), Cr = recombine(Cf);
+        const CBand Ac = compress(Ar, j0, M, M, -2, 3), Cc = compress(Cr, j0, M, M, -2, 3);
+        const CBand R2c = compress(so.ur.r2, j0, M, mh, -1, 3);
+
+        const Range mu = radial_cache.at(aw);
+        Range ca = poisson ? mu : Range{-1.0 / scale + mu.lo, -1.0 / scale + mu.hi};
+        Plan plan;
+        try {
+            plan = shift_plan(ca, vert, tol);
+        } catch (const Error& e) {
+            if (!(q2_pad && e.status == DOMAIN_ERROR)) throw;
+            // endpoint-relative pad only where the reference intervals overlap
+            const Range mu2 = radial_range(so, aw, true);
+            const Range v2 = vertical_range(so, true);
+            ca = poisson ? mu2 : Range{-1.0 / scale + mu2.lo, -1.0 / scale + mu2.hi};
+            plan = shift_plan(ca, v2, tol);
+        }
+        const int J = plan.J;
+        AdiSlot d{};
+        d.J = J;
+        d.j0 = j0;
+        d.left = alloc(size_t(J) * M * kLeftW);
+        d.right0 = alloc(size_t(J) * N * kRightW);
+        d.right1 = alloc(size_t(J) * N * kRightW);
+        d.sleft = alloc(size_t(M) * kStatW);
+        d.sright0 = alloc(size_t(N) * kStatW);
+        d.sright1 = alloc(size_t(N) * kStatW);
+        d.ds = alloc(size_t(J) + 1);
+        // left dynamic blocks
+        for (int j = 0; j < J; ++j) {
+            const CBand mul = cb_axpy(plan.u[size_t(j)], Cc, -1.0, Ac);
+            const CBand sh = cb_axpy(plan.v[size_t(j)], Cc, -1.0, Ac);
+            CLU lu;
+            try {
+                lu = banded_lu(sh, 2, 3);
+            } catch (const Error&) {
+                Error e(SINGULAR, "ADI: singular (v_j C - A)");
+                e.shift_index = j;
+                throw e;
+            }
+            double* blk = C.data() + d.left + size_t(j) * M * kLeftW;
+            for (int a = 0; a < M; ++a) {
+                double* r = blk + size_t(a) * kLeftW;
+                for (int q = 0; q < 6; ++q) r[q] = mul.at(a, q - 2);
+                r[6] = lu.L[size_t(a) * 2];
+                r[7] = lu.L[size_t(a) * 2 + 1];
+                r[8] = double(lu.piv[size_t(a)]);
+                for (int q = 0; q < 5; ++q) r[9 + q] = lu.U[size_t(a) * 5 + q] * lu.inv[size_t(a)];
+                r[14] = lu.inv[size_t(a)];
+            }
+            C[size_t(d.ds) + j] = plan.u[size_t(j)] - plan.v[size_t(j)];
+        }
+        // right dynamic blocks
+        for (int k0 = 0; k0 < 2; ++k0) {
+            const long base = k0 ? d.right1 : d.right0;
+            for (int j = 0; j < J; ++j) {
+                const CBand mul = (j + 1 < J) ? cb_axpy(plan.v[size_t(j + 1)], Btc[k0], 1.0, Dtc[k0]) : Btc[k0];
+                const CBand sh = cb_axpy(plan.u[size_t(j)], Btc[k0], 1.0, Dtc[k0]);
+                CLU lu;
+                try {
+                    lu = banded_lu(sh, 1, 2);
+                } catch (const Error&) {
+                    Error e(SINGULAR, "ADI: singular (u_j B + D)");
+                    e.shift_index = j;
+                    throw e;
+                }
+                double* blk = C.data() + base + size_t(j) * N * kRightW;
+                for (int b = 0; b < N; ++b) {
+                    double* r = blk + size_t(b) * kRightW;
+                    for (int q = 0; q < 4; ++q) r[q] = mul.at(b, q - 1);
+                    r[4] = lu.L[size_t(b)];
+                    r[5] = double(lu.piv[size_t(b)]);
+                    for (int q = 0; q < 3; ++q) r[6 + q] = lu.U[size_t(b) * 3 + q] * lu.inv[size_t(b)];
+                    r[9] = lu.inv[size_t(b)];
+                }
+            }
+            // static right block
+            CLU lub;
+            try {
+                lub = banded_lu(Btc[k0], 1, 2);
+            } catch (const Error&) {
+                throw Error(SINGULAR, "AdiWorkspace: B is singular");
+            }
+            const CBand rs = cb_axpy(plan.v[0], Btc[k0], 1.0, Dtc[k0]);
+            double* blk = C.data() + (k0 ? d.sright1 : d.sright0);
+            for (int b = 0; b < N; ++b) {
+                double* r = blk + size_t(b) * kStatW;
+                r[0] = 0.0;
+                for (int q = 0; q < 3; ++q) r[1 + q] = C02c[k0].at(b, q);
+                r[4] = lub.L[size_t(b)];
+                r[5] = double(lub.piv[size_t(b)]);
+                for (int q = 0; q < 3; ++q) r[6 + q] = lub.U[size_t(b) * 3 + q] * lub.inv[size_t(b)];
+                r[9] = lub.inv[size_t(b)];
+                for (int q = 0; q < 4; ++q) {
+                    r[10 + q] = Btc[k0].at(b, q - 1);
+                    r[14 + q] = Dtc[k0].at(b, q - 1);
+                    r[18 + q] = rs.at(b, q - 1);
+                }
+            }
+        }
+        // static left block
+        {
+            // C must be invertible for ADI (adi.cpp:121-124)
+            try {
+                (void)banded_lu(Cc, 2, 3);
+            } catch (const Error&) {
+                throw Error(SINGULAR, "AdiWorkspace: C is singular; ADI needs invertible C");
+            }
+            double* blk = C.data() + d.sleft;
+            for (int a = 0; a < M; ++a) {
+                double* r = blk + size_t(a) * kStatW;
+                r[0] = 0.0;
+                for (int q = 0; q < 5; ++q) r[1 + q] = R2c.at(a, q - 1);
+                for (int q = 0; q < 6; ++q) {
+                    r[6 + q] = Ac.at(a, q - 2);
+                    r[12 + q] = Cc.at(a, q - 2);
+                }
+            }
+        }
+        built[aw] = d;
+        set.slots[size_t(s)] = d;
+        set.plans[size_t(s)].w = w;
+        set.plans[size_t(s)].plan = plan;
+        set.plans[size_t(s)].has_plan = true;
+    }
+    C.resize(C.size() + 256, 0.0);  // read slack past the last block
+    for (const AdiSlot& d : set.slots) {
+        set.maxJ = std::max(set.maxJ, d.J);
+        set.iters_per_round += d.J;
+    }
+    return set;
+}
+
+}  // namespace ccf

@@ -1,0 +1,51 @@
+// Host builder for the packed per-slot operator blocks consumed by adi_kernel
+// (layout documented in ccf_device.cuh::AdiSlot).
+//   ModalSolver ctor   proj/src/solvers.cpp:46-75
+//   AdiWorkspace ctor  proj/src/adi.cpp:114-148
+#pragma once
+
+#include <map>
+#include <vector>
+
+#include "ccf_device.cuh"
+#include "setup.hpp"
+
+namespace ccf {
+
+struct SizeOps {  // per-size operator cache (setup only)
+    int m = 0, n = 0;
+    Ultra ur, uz;
+    Dense R2rec, C02recZ, D2recZ;  // recombined full operators
+    Range vertical;                // padded enclosure of spec(-D2', C02')
+    bool vertical_ok = false;
+    SizeOps(int m_, int n_);
+};
+
+// Radial pencil range for (m, w^2): enclosure of spec(R2'^-1 L_w'), solvers.cpp:15-28.
+Range radial_range(const SizeOps& so, int w, bool q2_pad);
+Range vertical_range(SizeOps& so, bool q2_pad);
+
+struct SlotPlan {
+    int w = 0;
+    Plan plan;
+    bool has_plan = false;
+};
+
+// A "solver set": one (poisson | helmholtz scale) family over a list of slots.
+struct SolverSet {
+    bool poisson = true;
+    double scale = 1.0, tol = 1e-12;
+    std::vector<SlotPlan> plans;   // per slot
+    std::vector<AdiSlot> slots;    // per slot descriptors
+    std::vector<double> coef;      // packed blocks (host copy)
+    int maxJ = 0;
+    long iters_per_round = 0;      // sum over slots of J (one round)
+};
+
+// Build the packed set. slot_w: wavenumber per slot. radial: cached radial
+// ranges per |w| (computed on demand). Throws ccf::Error on reference failures
+// (overlapping intervals -> DOMAIN_ERROR, singular operators -> SINGULAR).
+SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poisson, double scale, double tol,
+                           std::map<int, Range>& radial_cache, bool q2_pad);
+
+}  // namespace ccf

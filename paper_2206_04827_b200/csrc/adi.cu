@@ -7,19 +7,22 @@
 // reference's complex (m-2)x(n-2) modal system splits exactly into four real
 // ((m-2)/2)x((n-2)/2) systems because every operator has even band offsets and
 // real entries. The iterate stays resident in shared memory for all J
-// iterations; only E' (L2-resident scratch) and the per-shift banded factors are
-// read from global memory.
+// iterations. Per-shift banded factors and the constant E' are streamed into
+// shared memory with TMA bulk copies (cp.async.bulk + mbarrier) overlapped with
+// the opposite sweep.
 //
 // Iteration (algebraically identical to the reference's two half steps, with
 // Y_j = X_j (v_j B + D) B^-1 and E' = E B^-1):
 //   Z_j     = (v_j C - A)^-1 [ (u_j C - A) Y_j - (u_j - v_j) E' ]      column sweep
 //   Y_{j+1} = Z_j (v_{j+1} B + D) (u_j B + D)^-1                       row sweep
 //   X_J     = Z_{J-1} B (u_{J-1} B + D)^-1
-// so each iteration costs one banded multiply + one pivoted banded solve per side.
+// so each iteration costs one banded multiply + one banded solve per side.
 // The relative Frobenius residual ||A X B + C X D - E|| / ||E|| is evaluated on
 // chip after every round of J iterations (adi.cpp:188-192); the round logic
 // (<= 4 rounds, accept <= tol, fail > 10 tol) lives in adi_round_check.
 #include <cuda_runtime.h>
+
+#include <cstdint>
 
 #include "kernels.cuh"
 
@@ -27,37 +30,52 @@ namespace ccf {
 
 namespace {
 
+constexpr int kChunk = 8;  // E' rows per bulk chunk
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n LAB_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra LAB_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+
 __device__ __forceinline__ void swap2(double& a, double& b) {
     const double t = a;
     a = b;
     b = t;
 }
+__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
 // Column multiply (no solve): out_a = sum_{d=-2..3} c[a][d] y[a+d] + alpha * e[a]
-// in place over rows 0..M-1 of column `col` (stride pitch). Rows >= M read as the
-// zero padding of the tile. Optional second multiplier c2 writes to q (global).
+// in place over rows 0..M-1 of column `col` (stride pitch). Optional second
+// multiplier writes q (global). Used once per round (prologue / residual).
 __device__ __forceinline__ void col_mul(double* __restrict__ col, int pitch, int M, const double* __restrict__ cf,
                                         int cstride, int coff, const double* __restrict__ e, long estride, double alpha,
                                         int coff2, double* __restrict__ q, long qstride) {
     double ym2 = 0.0, ym1 = 0.0, y0 = col[0], y1 = col[pitch], y2 = col[2 * pitch], y3 = col[3 * pitch];
     for (int a = 0; a < M; ++a) {
         const double* c = cf + a * cstride + coff;
-        double acc = c[0] * ym2;
-        acc = fma(c[1], ym1, acc);
-        acc = fma(c[2], y0, acc);
-        acc = fma(c[3], y1, acc);
-        acc = fma(c[4], y2, acc);
-        acc = fma(c[5], y3, acc);
+        double acc = fma(c[0], ym2, c[1] * ym1) + fma(c[2], y0, c[3] * y1) + fma(c[4], y2, c[5] * y3);
         if (e) acc = fma(alpha, e[a * estride], acc);
         if (q) {
             const double* c2 = cf + a * cstride + coff2;
-            double a2 = c2[0] * ym2;
-            a2 = fma(c2[1], ym1, a2);
-            a2 = fma(c2[2], y0, a2);
-            a2 = fma(c2[3], y1, a2);
-            a2 = fma(c2[4], y2, a2);
-            a2 = fma(c2[5], y3, a2);
-            q[a * qstride] = a2;
+            q[a * qstride] = fma(c2[0], ym2, c2[1] * ym1) + fma(c2[2], y0, c2[3] * y1) + fma(c2[4], y2, c2[5] * y3);
         }
         const double ynext = col[(a + 4) * pitch];
         col[a * pitch] = acc;
@@ -70,86 +88,28 @@ __device__ __forceinline__ void col_mul(double* __restrict__ col, int pitch, int
     }
 }
 
-// Column multiply + pivoted banded solve (left operators, kl = 2, ku = 3 in
-// compressed coordinates):  z = LU^-1 ( MUL y + alpha e ), in place.
-// cf row layout (stride 16): [mul -2..3 | L0 L1 | piv | Uf0..Uf4 | inv | pad].
-__device__ __forceinline__ void col_solve(double* __restrict__ col, int pitch, int M, const double* __restrict__ cf,
-                                          const double* __restrict__ e, long estride, double alpha) {
-    auto rrow = [&](int a, double ym2, double ym1, double y0, double y1, double y2, double y3) {
-        const double* c = cf + a * kLeftW;
-        double acc = c[0] * ym2;
-        acc = fma(c[1], ym1, acc);
-        acc = fma(c[2], y0, acc);
-        acc = fma(c[3], y1, acc);
-        acc = fma(c[4], y2, acc);
-        acc = fma(c[5], y3, acc);
-        return fma(alpha, e[a * estride], acc);
-    };
-    const double v0 = col[0], v1 = col[pitch], v2 = col[2 * pitch], v3 = col[3 * pitch], v4 = col[4 * pitch];
-    double x0 = rrow(0, 0.0, 0.0, v0, v1, v2, v3);
-    double x1 = rrow(1, 0.0, v0, v1, v2, v3, v4);
-    double r0 = v0, r1 = v1, r2 = v2, r3 = v3, r4 = v4, r5 = col[5 * pitch];
-    for (int k = 0; k < M; ++k) {
-        double x2 = (k + 2 < M) ? rrow(k + 2, r0, r1, r2, r3, r4, r5) : 0.0;
-        const double* c = cf + k * kLeftW;
-        const int pv = int(c[8]);
-        if (pv == 1) swap2(x0, x1);
-        else if (pv == 2) swap2(x0, x2);
-        x1 = fma(-c[6], x0, x1);
-        x2 = fma(-c[7], x0, x2);
-        const double ynext = col[(k + 6) * pitch];
-        col[k * pitch] = x0;
-        x0 = x1;
-        x1 = x2;
-        r0 = r1;
-        r1 = r2;
-        r2 = r3;
-        r3 = r4;
-        r4 = r5;
-        r5 = ynext;
-    }
-    double xa = 0.0, xb = 0.0, xc = 0.0, xd = 0.0, xe = 0.0;
-    for (int k = M - 1; k >= 0; --k) {
-        const double* c = cf + k * kLeftW;
-        double acc = col[k * pitch] * c[14];
-        acc = fma(-c[13], xe, acc);
-        acc = fma(-c[12], xd, acc);
-        acc = fma(-c[11], xc, acc);
-        acc = fma(-c[10], xb, acc);
-        acc = fma(-c[9], xa, acc);
-        col[k * pitch] = acc;
-        xe = xd;
-        xd = xc;
-        xc = xb;
-        xb = xa;
-        xa = acc;
-    }
-}
-
-// Row multiply + pivoted banded solve (right operators, transposed form,
-// kl = 1, ku = 2): y = LU^-1 ( MUL z ), in place over b in [0,N).
-// mul: 4 coefficients at offsets -1..2 (stride ms); lu: [L | piv | Uf0..2 | inv] (stride ls).
-__device__ __forceinline__ void row_solve(double* __restrict__ row, int N, const double* __restrict__ mul, int ms,
-                                          const double* __restrict__ lu, int ls, double* esq) {
-    auto rrow = [&](int b, double zm1, double z0, double z1, double z2) {
-        const double* c = mul + b * ms;
-        double acc = c[0] * zm1;
-        acc = fma(c[1], z0, acc);
-        acc = fma(c[2], z1, acc);
-        return fma(c[3], z2, acc);
-    };
+// Row multiply + banded solve (right operators, transposed form, kl = 1):
+//   y = LU^-1 ( MUL z ), in place over b in [0,N).
+// mul: 4 coefficients at offsets -1..2 (stride ms); lu fields (stride ls):
+//   [L | piv | inv | 0 | Uf0 Uf1 Uf2 | 0]  (Uf2 = 0 without pivoting).
+template <bool PIV, bool SQ>
+__device__ __forceinline__ double row_solve(double* __restrict__ row, int N, const double* __restrict__ mul, int ms,
+                                            const double* __restrict__ lu, int ls) {
     double s0 = row[0], s1 = row[1], s2 = row[2], s3 = row[3];
-    double x0 = rrow(0, 0.0, s0, s1, s2);
+    double2 m01 = ld2(mul), m23 = ld2(mul + 2);
+    double x0 = fma(m01.y, s0, m23.x * s1) + m23.y * s2;
     double sq = x0 * x0;
     for (int k = 0; k < N; ++k) {
         double x1 = 0.0;
         if (k + 1 < N) {
-            x1 = rrow(k + 1, s0, s1, s2, s3);
-            sq = fma(x1, x1, sq);
+            m01 = ld2(mul + (k + 1) * ms);
+            m23 = ld2(mul + (k + 1) * ms + 2);
+            x1 = fma(m01.x, s0, m01.y * s1) + fma(m23.x, s2, m23.y * s3);
+            if (SQ) sq = fma(x1, x1, sq);
         }
-        const double* c = lu + k * ls;
-        if (int(c[1]) == 1) swap2(x0, x1);
-        x1 = fma(-c[0], x0, x1);
+        const double2 lp = ld2(lu + k * ls);
+        if (PIV && lp.y == 1.0) swap2(x0, x1);
+        x1 = fma(-lp.x, x0, x1);
         const double snext = row[k + 4];
         row[k] = x0;
         x0 = x1;
@@ -158,19 +118,20 @@ __device__ __forceinline__ void row_solve(double* __restrict__ row, int N, const
         s2 = s3;
         s3 = snext;
     }
-    if (esq) *esq += sq;
     double xa = 0.0, xb = 0.0, xc = 0.0;
     for (int k = N - 1; k >= 0; --k) {
         const double* c = lu + k * ls;
-        double acc = row[k] * c[5];
-        acc = fma(-c[4], xc, acc);
-        acc = fma(-c[3], xb, acc);
-        acc = fma(-c[2], xa, acc);
+        const double2 iv = ld2(c + 2);
+        const double2 u01 = ld2(c + 4);
+        double acc = fma(-u01.y, xb, row[k] * iv.x);
+        if (PIV) acc = fma(-c[6], xc, acc);
+        acc = fma(-u01.x, xa, acc);
         row[k] = acc;
         xc = xb;
         xb = xa;
         xa = acc;
     }
+    return SQ ? sq : 0.0;
 }
 
 __device__ double block_sum(double v, double* red) {
@@ -185,23 +146,164 @@ __device__ double block_sum(double v, double* red) {
     return s;
 }
 
+// Column sweep of one iteration (all threads participate; lanes b >= N shadow column
+// N-1 and never store):
+//   z = (vC - A)^-1 [ (uC - A) y + alpha e' ]        kl = 2 (ku = 3 without pivoting)
+// left coefficients cf (shared, stride 16, Mpad+2 rows, zero-padded):
+//   [mul -2..3 | L0 L1 | inv | piv | Uf0..4 | 0]
+// e' streams through a 3-deep ring of kChunk-row shared buffers (TMA bulk copies);
+// block barriers only between chunks, the 8 steps of a chunk are fully unrolled.
+template <bool PIV>
+__device__ __forceinline__ void col_phase(double* __restrict__ Y, int pitch, int Mpad, int N,
+                                          const double* __restrict__ cf, double alpha, const double* __restrict__ eg,
+                                          double* __restrict__ ebuf, uint64_t* ebar, int iter) {
+    const int tid = threadIdx.x;
+    // lanes >= N shadow column N-1: they compute the identical chain and store the
+    // identical values (benign duplicate stores), so no predication in the hot loop
+    const int b = tid < N ? tid : N - 1;
+    double* __restrict__ col = Y + b;
+    const int nch = Mpad / kChunk;
+    const unsigned cbytes = unsigned(kChunk) * N * sizeof(double);
+    const long cstride = long(kChunk) * N;
+    // parity of the q-th use of barrier q%3 in column phase `iter`
+    auto ewait = [&](int q) {
+        const int bb = q % 3;
+        const int uses = (nch - bb + 2) / 3;
+        mbar_wait(&ebar[bb], unsigned(iter * uses + q / 3) & 1u);
+    };
+    if (tid == 0)
+        for (int q = 0; q < 3 && q < nch; ++q) bulk_load(ebuf + q * cstride, eg + q * cstride, cbytes, &ebar[q]);
+    ewait(0);
+    const double* ecur = ebuf + b;  // chunk c of e' (column b)
+    auto rrow = [&](const double* c, double e, double y0, double y1, double y2, double y3, double y4, double y5) {
+        const double2 c01 = ld2(c), c23 = ld2(c + 2), c45 = ld2(c + 4);
+        const double t0 = fma(c23.x, y2, fma(c01.y, y1, c01.x * y0));
+        const double t1 = fma(c45.y, y5, fma(c45.x, y4, fma(c23.y, y3, alpha * e)));
+        return t0 + t1;
+    };
+    double R0 = 0.0, R1 = 0.0, R2 = col[0], R3 = col[pitch], R4 = col[2 * pitch], R5 = col[3 * pitch];
+    double x0 = rrow(cf, ecur[0], R0, R1, R2, R3, R4, R5);
+    R0 = R1; R1 = R2; R2 = R3; R3 = R4; R4 = R5; R5 = col[4 * pitch];
+    double x1 = rrow(cf + kLeftW, ecur[N], R0, R1, R2, R3, R4, R5);
+    R0 = R1; R1 = R2; R2 = R3; R3 = R4; R4 = R5; R5 = col[5 * pitch];  // ring = y[0..5]
+    for (int c = 0; c < nch; ++c) {
+        if (c + 1 < nch) ewait(c + 1);
+        const double* enext = ebuf + ((c + 1) % 3) * cstride + b;
+        const double* cfc = cf + c * kChunk * kLeftW;
+        double* colc = col + c * kChunk * pitch;
+#pragma unroll
+        for (int q = 0; q < kChunk; ++q) {
+            const double e2 = (q + 2 < kChunk) ? ecur[(q + 2) * N] : enext[(q + 2 - kChunk) * N];
+            double x2 = rrow(cfc + (q + 2) * kLeftW, e2, R0, R1, R2, R3, R4, R5);
+            const double* cc = cfc + q * kLeftW;
+            const double2 l01 = ld2(cc + 6);
+            if (PIV) {
+                const double pv = cc[9];
+                if (pv == 1.0) swap2(x0, x1);
+                else if (pv == 2.0) swap2(x0, x2);
+            }
+            x1 = fma(-l01.x, x0, x1);
+            x2 = fma(-l01.y, x0, x2);
+            const double ynext = colc[(q + 6) * pitch];
+            colc[q * pitch] = x0;
+            x0 = x1;
+            x1 = x2;
+            R0 = R1; R1 = R2; R2 = R3; R3 = R4; R4 = R5; R5 = ynext;
+        }
+        ecur = enext;
+        __syncthreads();  // chunk c of e' fully consumed
+        if (tid == 0 && c + 3 < nch)
+            bulk_load(ebuf + ((c + 3) % 3) * cstride, eg + long(c + 3) * cstride, cbytes, &ebar[(c + 3) % 3]);
+    }
+    double xa = 0.0, xb = 0.0, xc = 0.0, xd = 0.0, xe = 0.0;
+    for (int c = nch - 1; c >= 0; --c) {
+#pragma unroll
+        for (int q = kChunk - 1; q >= 0; --q) {
+            const int k = c * kChunk + q;
+            const double* cc = cf + k * kLeftW;
+            const double2 iv = ld2(cc + 8);
+            const double2 u01 = ld2(cc + 10);
+            const double2 u23 = ld2(cc + 12);
+            double acc = fma(-u23.x, xc, col[k * pitch] * iv.x);
+            acc = fma(-u01.y, xb, acc);
+            if (PIV) acc = fma(-u23.y, xd, fma(-cc[14], xe, acc));
+            acc = fma(-u01.x, xa, acc);
+            col[k * pitch] = acc;
+            xe = xd;
+            xd = xc;
+            xc = xb;
+            xb = xa;
+            xa = acc;
+        }
+    }
+}
+
+// Row sweep of one iteration, thread per row a (< M), columns padded to Npad:
+//   y = (uB + D)^-T [ (v'B + D)^T z ]     kl = 1 (ku = 2 without pivoting)
+// right coefficients (shared, stride 12, Npad+2 rows): [mul -1..2 | L | piv | inv | 0 | Uf0..2 | 0]
+template <bool PIV>
+__device__ __forceinline__ void row_phase(double* __restrict__ row, int Npad, const double* __restrict__ cr) {
+    auto rrow = [&](int b, double z0, double z1, double z2, double z3) {
+        const double* c = cr + b * kRightW;
+        const double2 m01 = ld2(c), m23 = ld2(c + 2);
+        return fma(m01.y, z1, m01.x * z0) + fma(m23.y, z3, m23.x * z2);
+    };
+    double S0 = 0.0, S1 = row[0], S2 = row[1], S3 = row[2];
+    double x0 = rrow(0, S0, S1, S2, S3);
+    S0 = S1; S1 = S2; S2 = S3; S3 = row[3];  // z[0..3]
+    const int nch = Npad / kChunk;
+    for (int c = 0; c < nch; ++c) {
+#pragma unroll
+        for (int q = 0; q < kChunk; ++q) {
+            const int k = c * kChunk + q;
+            double x1 = rrow(k + 1, S0, S1, S2, S3);
+            const double2 lp = ld2(cr + k * kRightW + 4);
+            if (PIV && lp.y == 1.0) swap2(x0, x1);
+            x1 = fma(-lp.x, x0, x1);
+            const double snext = row[k + 4];
+            row[k] = x0;
+            x0 = x1;
+            S0 = S1; S1 = S2; S2 = S3; S3 = snext;
+        }
+    }
+    double xa = 0.0, xb = 0.0, xc = 0.0;
+    for (int c = nch - 1; c >= 0; --c) {
+#pragma unroll
+        for (int q = kChunk - 1; q >= 0; --q) {
+            const int k = c * kChunk + q;
+            const double* cc = cr + k * kRightW;
+            const double2 iv = ld2(cc + 6);
+            const double2 u01 = ld2(cc + 8);
+            double acc = fma(-u01.y, xb, row[k] * iv.x);
+            if (PIV) acc = fma(-cc[10], xc, acc);
+            acc = fma(-u01.x, xa, acc);
+            row[k] = acc;
+            xc = xb;
+            xb = xa;
+            xa = acc;
+        }
+    }
+}
+
 }  // namespace
 
-// Shared-memory tile: rows [0, mh+6) x pitch (pitch >= nh+3, odd).
-__global__ void __launch_bounds__(128) adi_kernel(const AdiParams P) {
-    extern __shared__ double sm[];
-    double* Y = sm;
-    __shared__ double red[8];
-    const AdiTask task = P.tasks[blockIdx.x];
+// Shared-memory tile: rows [0, mh+5) x pitch (pitch >= nh+3, odd), followed by the
+// left / right coefficient stages and two E' chunk buffers.
+template <bool PIV>
+__device__ __forceinline__ void adi_body(const AdiParams& P, const AdiTask& task, const AdiSlot& so, double* sm,
+                                         uint64_t* bars, double* red) {
     const int t = task.tensor, s = task.slot, k0 = task.k0, plane = task.plane;
     const Geo& g = P.g;
-    if (!P.active[t * g.nslots + s]) return;
-    const AdiSlot so = P.slots[s];
     const int M = P.M, N = P.N, mh = g.mh, nh = g.nh, pitch = P.pitch;
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int rows = mh + 6;
+    const int rows = P.Mpad + 6;
+    double* Y = sm;
+    const long ysize = ((long(rows) * pitch + 1) / 2) * 2;
+    double* bufL = sm + ysize;
+    double* bufR = bufL + long(P.lrows) * kLeftW;
+    double* bufE = bufR + long(P.rrows) * kRightW;
     const long toff = long(s) * g.slot_stride + long(plane) * g.plane_stride;
-    double* ep = P.eprime + long(blockIdx.x) * M * N;
+    double* ep = P.eprime + long(blockIdx.x) * P.estride;
     const double* sleft = P.coef + so.sleft;
     const double* sright = P.coef + (k0 ? so.sright1 : so.sright0);
 
@@ -212,28 +314,33 @@ __global__ void __launch_bounds__(128) adi_kernel(const AdiParams P) {
         const long off = toff + long(2 * b + k0) * mh;
         for (int a = tid; a < mh; a += nt) {
             double acc = 0.0;
-            for (int i = 0; i < P.nsrc[t]; ++i) acc = fma(P.wsrc[t][i], P.src[t][i][off + a], acc);
+            for (int i = 0; i < P.nsrc[t]; ++i) acc = fma(P.wsrc[t][i], __ldg(P.src[t][i] + off + a), acc);
             Y[a * pitch + b] = acc;
         }
     }
     __syncthreads();
     for (int b = tid; b < nh; b += nt) col_mul(Y + b, pitch, M, sleft, kStatW, 0, nullptr, 0, 0.0, 0, nullptr, 0);
     __syncthreads();
-    // row M (= mh-1) of F is outside the truncated system
-    for (int b = tid; b < pitch; b += nt) Y[M * pitch + b] = 0.0;
+    for (int b = tid; b < pitch; b += nt) Y[M * pitch + b] = 0.0;  // row M of F lies outside the truncated system
     __syncthreads();
     double esq = 0.0;
-    for (int a = tid; a < M; a += nt) {
-        // columns >= N of row a: N holds F data outside the system; zero after use below
-        row_solve(Y + a * pitch, N, sright + 0, kStatW, sright + 4, kStatW, &esq);
-    }
+    for (int a = tid; a < M; a += nt) esq += row_solve<PIV, true>(Y + a * pitch, N, sright + 0, kStatW, sright + 4, kStatW);
     __syncthreads();
-    for (int i = tid; i < M * N; i += nt) {
+    for (int i = tid; i < P.Mpad * N; i += nt) {
         const int a = i / N, b = i % N;
-        ep[i] = Y[a * pitch + b];
+        ep[i] = a < M ? Y[a * pitch + b] : 0.0;
     }
+    fence_proxy_async();  // E' generic stores -> async-proxy (bulk copy) reads
     __syncthreads();
     for (int i = tid; i < rows * pitch; i += nt) Y[i] = 0.0;
+    const double* left = P.coef + so.left;
+    const double* right = P.coef + (k0 ? so.right1 : so.right0);
+    const unsigned lbytes = unsigned(P.lrows) * kLeftW * sizeof(double);
+    const unsigned rbytes = unsigned(P.rrows) * kRightW * sizeof(double);
+    if (tid == 0) {
+        bulk_load(bufL, left, lbytes, &bars[0]);
+        bulk_load(bufR, right, rbytes, &bars[1]);
+    }
     __syncthreads();
 
     if (P.round > 0) {
@@ -258,23 +365,23 @@ __global__ void __launch_bounds__(128) adi_kernel(const AdiParams P) {
                 acc += Y[a * pitch + b];
                 Y[a * pitch + b] = acc;
             }
-            row_solve(Y + a * pitch, N, sright + 18, kStatW, sright + 4, kStatW, nullptr);
+            row_solve<PIV, false>(Y + a * pitch, N, sright + 20, kStatW, sright + 4, kStatW);
         }
         __syncthreads();
     }
 
     // ---- J iterations, tile resident in shared memory
-    const double* left = P.coef + so.left;
-    const double* right = P.coef + (k0 ? so.right1 : so.right0);
     const double* dsv = P.coef + so.ds;
     for (int j = 0; j < so.J; ++j) {
-        const double* cl = left + long(j) * M * kLeftW;
-        const double* cr = right + long(j) * N * kRightW;
-        const double alpha = -dsv[j];
-        for (int b = tid; b < N; b += nt) col_solve(Y + b, pitch, M, cl, ep + b, N, alpha);
+        const double alpha = -__ldg(dsv + j);
+        mbar_wait(&bars[0], unsigned(j) & 1u);
+        col_phase<PIV>(Y, pitch, P.Mpad, N, bufL, alpha, ep, bufE, bars + 2, j);
         __syncthreads();
-        for (int a = tid; a < M; a += nt) row_solve(Y + a * pitch, N, cr, kRightW, cr + 4, kRightW, nullptr);
+        if (tid == 0 && j + 1 < so.J) bulk_load(bufL, left + long(j + 1) * P.lrows * kLeftW, lbytes, &bars[0]);
+        mbar_wait(&bars[1], unsigned(j) & 1u);
+        for (int a = tid; a < M; a += nt) row_phase<PIV>(Y + a * pitch, P.Npad, bufR);
         __syncthreads();
+        if (tid == 0 && j + 1 < so.J) bulk_load(bufR, right + long(j + 1) * P.rrows * kRightW, rbytes, &bars[1]);
     }
 
     // ---- epilogue: u = S_r X S_z^T (Dirichlet recombination, solvers.cpp:97), parity-compressed store
@@ -301,14 +408,8 @@ __global__ void __launch_bounds__(128) adi_kernel(const AdiParams P) {
         double qm1 = 0.0, q0 = qrow[0], q1 = N > 1 ? qrow[1] : 0.0, q2 = N > 2 ? qrow[2] : 0.0;
         for (int b = 0; b < N; ++b) {
             const double* c = sright + b * kStatW;
-            double r = c[10] * pm1;
-            r = fma(c[11], p0, r);
-            r = fma(c[12], p1, r);
-            r = fma(c[13], p2, r);
-            r = fma(c[14], qm1, r);
-            r = fma(c[15], q0, r);
-            r = fma(c[16], q1, r);
-            r = fma(c[17], q2, r);
+            const double r = (fma(c[12], pm1, c[13] * p0) + fma(c[14], p1, c[15] * p2)) +
+                             (fma(c[16], qm1, c[17] * q0) + fma(c[18], q1, c[19] * q2));
             rsq = fma(r, r, rsq);
             pm1 = p0;
             p0 = p1;
@@ -326,6 +427,22 @@ __global__ void __launch_bounds__(128) adi_kernel(const AdiParams P) {
         atomicAdd(P.res2 + t * g.nslots + s, rs);
         atomicAdd(P.e2 + t * g.nslots + s, es);
     }
+}
+
+__global__ void __launch_bounds__(256, 1) adi_kernel(const AdiParams P) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ uint64_t bars[5];
+    __shared__ double red[8];
+    const AdiTask task = P.tasks[blockIdx.x];
+    if (!P.active[task.tensor * P.g.nslots + task.slot]) return;
+    const AdiSlot so = P.slots[task.slot];
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 5; ++i) mbar_init(&bars[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (so.pivot) adi_body<true>(P, task, so, sm, bars, red);
+    else adi_body<false>(P, task, so, sm, bars, red);
 }
 
 // Round bookkeeping per (tensor, slot): accept <= tol, restart up to 4 rounds,

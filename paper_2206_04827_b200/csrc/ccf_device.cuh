@@ -21,12 +21,14 @@ constexpr int kMaxSrc = 8;
 struct AdiSlot {
     int J;        // shifts per round
     int j0;       // j-parity of the (scalar-class) unknowns of this slot
-    long left;    // J x M x 16  : [mul(uC-A) -2..3 | L(2) | piv | Uf(5) | inv | pad]
-    long right0;  // J x N x 12  (k-parity 0): [mul -1..2 | L | piv | Uf(3) | inv | pad 2]
+    int pivot;    // 1 if any banded LU of this slot row-swaps (selects the pivoted kernel path)
+    int pad_;
+    long left;    // J x (Mpad+2) x 16 : [mul(uC-A) -2..3 | L0 L1 | inv | piv | Uf0..Uf4 | 0]
+    long right0;  // J x (Npad+2) x 12 (k-parity 0): [mul -1..2 | L | piv | inv | 0 | Uf0..Uf2 | 0]
     long right1;  // J x N x 12  (k-parity 1)
     long sleft;   // M x 24      : [R2 -2..3 (first 0) | A -2..3 | C -2..3 | pad 6]
-    long sright0; // N x 24      : [C02 -1..2 (first 0) | LU(B^T): L, piv, Uf(3), inv | B^T -1..2 | D^T -1..2 |
-                  //                restart mul (v_0 B + D)^T -1..2 | pad 2]
+    long sright0; // N x 24      : [C02 -1..2 (first 0) | LU(B^T) as the right block fields 4..11 |
+                  //                B^T -1..2 | D^T -1..2 | restart mul (v_0 B + D)^T -1..2]
     long sright1;
     long ds;      // J : u_j - v_j
 };
@@ -53,7 +55,10 @@ struct AdiParams {
     double wsrc[2][kMaxSrc];
     int nsrc[2];
     double* out[2];
-    double* eprime;  // ntasks x M x N scratch
+    double* eprime;  // ntasks x estride scratch, rows padded to Mpad (multiple of 8)
+    long estride;    // doubles per task (Mpad * N rounded to even)
+    int Mpad, Npad;  // M, N rounded up to multiples of 8 (zero-padded sweeps)
+    int lrows, rrows;  // rows per left / right shift block (Mpad + 2, Npad + 2)
     double* res2;    // [2][nslots]
     double* e2;      // [2][nslots]
     const int* active;  // [2][nslots]

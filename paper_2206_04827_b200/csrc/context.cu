@@ -62,7 +62,11 @@ Ctx::Ctx(int m_, int n_, int p_, int device_, double tol_, int flags_)
     gf = make_geo(m, n, p, p);
     M = (m - 2) / 2;
     N = (n - 2) / 2;
-    pitch = ((n / 2) + 3) | 1;
+    Mpad = ((M + 7) / 8) * 8;
+    Npad = ((N + 7) / 8) * 8;
+    pitch = (Npad + 4) | 1;
+    estride = ((long(Mpad) * N + 1) / 2) * 2;
+    if (std::max(M, N) > 256) throw Error(DOMAIN_ERROR, "ccf: (m-2)/2, (n-2)/2 <= 256 (single-CTA ADI tile)");
     sizeops = std::make_unique<SizeOps>(m, n);
     // workspace
     const int cap = p;  // max slots (full mode)
@@ -77,13 +81,13 @@ Ctx::Ctx(int m_, int n_, int p_, int device_, double tol_, int flags_)
     CCF_CUDA(cudaMalloc(&ws.iters, sizeof(unsigned long long) * 2));
     CCF_CUDA(cudaMemset(ws.err, 0, sizeof(int) * 4));
     CCF_CUDA(cudaMemset(ws.iters, 0, sizeof(unsigned long long) * 2));
-    ws.eprime.alloc(size_t(2) * cap * 4 * size_t(M) * N);
+    ws.eprime.alloc(size_t(2) * cap * 4 * size_t(estride));
     {
         int optin = 0;
         CCF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
         cudaFuncAttributes fa{};
         CCF_CUDA(cudaFuncGetAttributes(&fa, adi_kernel));
-        const size_t need = size_t(m / 2 + 6) * pitch * sizeof(double);
+        const size_t need = adi_smem_bytes();
         if (need + fa.sharedSizeBytes > size_t(optin))
             throw Error(DOMAIN_ERROR, "ccf: ADI tile exceeds shared memory (m, n too large for the single-CTA kernel)");
         CCF_CUDA(cudaFuncSetAttribute(adi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(optin - fa.sharedSizeBytes)));
@@ -101,6 +105,13 @@ Ctx::~Ctx() {
     cudaFree(ws.flag);
     cudaFree(ws.iters);
     if (own_stream) cudaStreamDestroy(own_stream);
+}
+
+size_t Ctx::adi_smem_bytes() const {
+    const long rows = Mpad + 6;
+    const long ysize = ((rows * pitch + 1) / 2) * 2;
+    const long total = ysize + long(Mpad + 2) * kLeftW + long(Npad + 2) * kRightW + 3L * 8 * N;
+    return size_t(total) * sizeof(double);
 }
 
 void Ctx::sync() { CCF_CUDA(cudaStreamSynchronize(stream)); }
@@ -176,6 +187,11 @@ void Ctx::run_adi(DevSet& set, bool full, int ntensor, const double* const* src0
     P.out[0] = out0;
     P.out[1] = out1;
     P.eprime = ws.eprime.p;
+    P.estride = estride;
+    P.Mpad = Mpad;
+    P.Npad = Npad;
+    P.lrows = Mpad + 2;
+    P.rrows = Npad + 2;
     P.res2 = ws.res2;
     P.e2 = ws.e2;
     P.active = ws.active;
@@ -185,8 +201,8 @@ void Ctx::run_adi(DevSet& set, bool full, int ntensor, const double* const* src0
     std::vector<int> ones(size_t(nts), 1);
     CCF_CUDA(cudaMemcpyAsync(ws.active, ones.data(), sizeof(int) * nts, cudaMemcpyHostToDevice, stream));
     CCF_CUDA(cudaStreamSynchronize(stream));  // `ones` is a host temporary
-    const int threads = std::min(128, ((std::max(g.mh, g.nh) + 31) / 32) * 32);
-    const size_t smem = size_t(g.mh + 6) * pitch * sizeof(double);
+    const int threads = ((std::max(M, N) + 31) / 32) * 32;
+    const size_t smem = adi_smem_bytes();
     RoundCheck rc{};
     rc.ntensor = ntensor;
     rc.nslots = g.nslots;

@@ -61,7 +61,9 @@ struct Ctx {
     double tol;
     cudaStream_t stream = nullptr, own_stream = nullptr;
     Geo gh{}, gf{};  // half-spectrum and full-spectrum slot tables
-    int M, N, pitch;
+    int M, N, pitch, Mpad, Npad;
+    long estride;
+    size_t adi_smem_bytes() const;
     std::unique_ptr<SizeOps> sizeops;
     std::map<int, Range> radial_cache;
     std::map<std::tuple<int, int, double>, std::unique_ptr<DevSet>> sets;  // (full, poisson, scale)

@@ -31,6 +31,16 @@ Dense axpby(double al, const Dense& a, double be, const Dense& b) {
     return o;
 }
 
+// right-side LU fields: [L | piv | inv | 0 | Uf0 Uf1 Uf2 | 0]
+void put_right_lu(double* r, const CLU& lu, int b) {
+    r[0] = lu.L[size_t(b)];
+    r[1] = double(lu.piv[size_t(b)]);
+    r[2] = lu.inv[size_t(b)];
+    r[3] = 0.0;
+    for (int q = 0; q < 3; ++q) r[4 + q] = lu.U[size_t(b) * 3 + q] * lu.inv[size_t(b)];
+    r[7] = 0.0;
+}
+
 // sum of two compressed bands with identical shape
 CBand cb_axpy(double al, const CBand& x, double be, const CBand& y) {
     CBand o = x;
@@ -63,6 +73,7 @@ Range vertical_range(SizeOps& so, bool q2_pad) {
 SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poisson, double scale, double tol,
                            std::map<int, Range>& radial_cache, bool q2_pad) {
     const int m = so.m, n = so.n, M = (m - 2) / 2, N = (n - 2) / 2, mh = m / 2, nh = n / 2;
+    const int lrows = ((M + 7) / 8) * 8 + 2, rrows = ((N + 7) / 8) * 8 + 2;  // zero-padded sweep rows
     SolverSet set;
     set.poisson = poisson;
     set.scale = scale;
@@ -110,7 +121,7 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
     std::vector<double>& C = set.coef;
     auto alloc = [&](size_t count) {
         const long off = long(C.size());
-        C.resize(C.size() + count, 0.0);
+        C.resize(C.size() + ((count + 1) / 2) * 2, 0.0);  // 16-byte aligned blocks (bulk copies)
         return off;
     };
 
@@ -165,9 +176,9 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
         AdiSlot d{};
         d.J = J;
         d.j0 = j0;
-        d.left = alloc(size_t(J) * M * kLeftW);
-        d.right0 = alloc(size_t(J) * N * kRightW);
-        d.right1 = alloc(size_t(J) * N * kRightW);
+        d.left = alloc(size_t(J) * lrows * kLeftW);
+        d.right0 = alloc(size_t(J) * rrows * kRightW);
+        d.right1 = alloc(size_t(J) * rrows * kRightW);
         d.sleft = alloc(size_t(M) * kStatW);
         d.sright0 = alloc(size_t(N) * kStatW);
         d.sright1 = alloc(size_t(N) * kStatW);
@@ -184,15 +195,16 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
                 e.shift_index = j;
                 throw e;
             }
-            double* blk = C.data() + d.left + size_t(j) * M * kLeftW;
+            double* blk = C.data() + d.left + size_t(j) * lrows * kLeftW;
             for (int a = 0; a < M; ++a) {
                 double* r = blk + size_t(a) * kLeftW;
                 for (int q = 0; q < 6; ++q) r[q] = mul.at(a, q - 2);
                 r[6] = lu.L[size_t(a) * 2];
                 r[7] = lu.L[size_t(a) * 2 + 1];
-                r[8] = double(lu.piv[size_t(a)]);
-                for (int q = 0; q < 5; ++q) r[9 + q] = lu.U[size_t(a) * 5 + q] * lu.inv[size_t(a)];
-                r[14] = lu.inv[size_t(a)];
+                r[8] = lu.inv[size_t(a)];
+                r[9] = double(lu.piv[size_t(a)]);
+                if (lu.piv[size_t(a)]) d.pivot = 1;
+                for (int q = 0; q < 5; ++q) r[10 + q] = lu.U[size_t(a) * 5 + q] * lu.inv[size_t(a)];
             }
             C[size_t(d.ds) + j] = plan.u[size_t(j)] - plan.v[size_t(j)];
         }
@@ -210,14 +222,12 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
                     e.shift_index = j;
                     throw e;
                 }
-                double* blk = C.data() + base + size_t(j) * N * kRightW;
+                double* blk = C.data() + base + size_t(j) * rrows * kRightW;
                 for (int b = 0; b < N; ++b) {
                     double* r = blk + size_t(b) * kRightW;
                     for (int q = 0; q < 4; ++q) r[q] = mul.at(b, q - 1);
-                    r[4] = lu.L[size_t(b)];
-                    r[5] = double(lu.piv[size_t(b)]);
-                    for (int q = 0; q < 3; ++q) r[6 + q] = lu.U[size_t(b) * 3 + q] * lu.inv[size_t(b)];
-                    r[9] = lu.inv[size_t(b)];
+                    put_right_lu(r + 4, lu, b);
+                    if (lu.piv[size_t(b)]) d.pivot = 1;
                 }
             }
             // static right block
@@ -233,14 +243,12 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
                 double* r = blk + size_t(b) * kStatW;
                 r[0] = 0.0;
                 for (int q = 0; q < 3; ++q) r[1 + q] = C02c[k0].at(b, q);
-                r[4] = lub.L[size_t(b)];
-                r[5] = double(lub.piv[size_t(b)]);
-                for (int q = 0; q < 3; ++q) r[6 + q] = lub.U[size_t(b) * 3 + q] * lub.inv[size_t(b)];
-                r[9] = lub.inv[size_t(b)];
+                put_right_lu(r + 4, lub, b);
+                if (lub.piv[size_t(b)]) d.pivot = 1;
                 for (int q = 0; q < 4; ++q) {
-                    r[10 + q] = Btc[k0].at(b, q - 1);
-                    r[14 + q] = Dtc[k0].at(b, q - 1);
-                    r[18 + q] = rs.at(b, q - 1);
+                    r[12 + q] = Btc[k0].at(b, q - 1);
+                    r[16 + q] = Dtc[k0].at(b, q - 1);
+                    r[20 + q] = rs.at(b, q - 1);
                 }
             }
         }

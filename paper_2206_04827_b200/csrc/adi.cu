@@ -445,6 +445,15 @@ __global__ void __launch_bounds__(256, 1) adi_kernel(const AdiParams P) {
     else adi_body<false>(P, task, so, sm, bars, red);
 }
 
+__global__ void adi_init_kernel(int* active, double* res2, double* e2, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        active[i] = 1;
+        res2[i] = 0.0;
+        e2[i] = 0.0;
+    }
+}
+
 // Round bookkeeping per (tensor, slot): accept <= tol, restart up to 4 rounds,
 // fail > 10 tol after the last round (adi.cpp:163-200).
 __global__ void adi_round_check(RoundCheck c) {

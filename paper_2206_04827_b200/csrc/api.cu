@@ -4,10 +4,21 @@
 
 #include "../../include/ccf.h"
 #include "context.hpp"
+#include "pipeline.hpp"
 
 
 struct ccf_ctx {
     std::unique_ptr<ccf::Ctx> c;
+    std::unique_ptr<ccf::Pipeline> pipe;
+    ccf::Pipeline& pl() {
+        if (!pipe) pipe = std::make_unique<ccf::Pipeline>(*c);
+        return *pipe;
+    }
+};
+
+struct ccf_ns_state {
+    ccf_ctx* ctx = nullptr;
+    ccf::NSState st;
 };
 
 using ccf::Ctx;
@@ -84,6 +95,7 @@ ccf_status ccf_ctx_destroy(ccf_ctx* ctx) {
     if (!ctx) return CCF_OK;
     try {
         if (ctx->c) cudaSetDevice(ctx->c->device);
+        ctx->pipe.reset();
         delete ctx;
     } catch (...) {
         return CCF_INTERNAL_ERROR;
@@ -211,24 +223,256 @@ ccf_status ccf_reset_stats(ccf_ctx* ctx) {
 
 }  // extern "C"
 
-// ---- entry points not yet wired (return an explicit error instead of a CPU fallback)
-#define CCF_TODO(sig)                                                                            \
-    ccf_status sig {                                                                             \
-        return guard(ctx, [&](Ctx&) { throw Error(ccf::INTERNAL, "ccf: entry point not implemented yet"); }); \
-    }
-extern "C" {
-CCF_TODO(ccf_analyze(ccf_ctx* ctx, const double*, double*))
-CCF_TODO(ccf_synthesize(ccf_ctx* ctx, const double*, double*))
-CCF_TODO(ccf_calculus(ccf_ctx* ctx, int, const double*, double*))
-CCF_TODO(ccf_hpoisson(ccf_ctx* ctx, const double*, double*))
-CCF_TODO(ccf_pt_synthesize(ccf_ctx* ctx, const double*, const double*, double*, double*, double*))
-CCF_TODO(ccf_pt_decompose(ccf_ctx* ctx, const double*, const double*, const double*, double*, double*))
-CCF_TODO(ccf_curl_vector(ccf_ctx* ctx, const double*, const double*, const double*, double*, double*, double*))
-CCF_TODO(ccf_curl_pt(ccf_ctx* ctx, const double*, const double*, double*, double*))
-CCF_TODO(ccf_velocity_from_vorticity(ccf_ctx* ctx, const double*, const double*, double*, double*))
-CCF_TODO(ccf_nonlinear(ccf_ctx* ctx, const double*, const double*, const double*, const double*, double*, double*))
-CCF_TODO(ccf_ns_create(ccf_ctx* ctx, double, double, int, int, const double*, const double*, ccf_ns_state**))
-ccf_status ccf_ns_step(ccf_ns_state*, int) { return CCF_INTERNAL_ERROR; }
-ccf_status ccf_ns_get_omega(ccf_ns_state*, double*, double*, double*, int*) { return CCF_INTERNAL_ERROR; }
-ccf_status ccf_ns_destroy(ccf_ns_state*) { return CCF_OK; }
+
+// ------------------------------------------------------------------------------------------
+// Half-spectrum entry points. Inputs are coefficient tensors of real fields (Hermitian,
+// as every tensor of the reference NS path is); the scalar / flip parity classes are
+// handled separately so arbitrary physical fields round-trip.
+namespace {
+
+double* tens(Ctx& c, int i) {
+    const long nt = c.tensor_doubles(false);
+    if (c.tens[i].n < size_t(nt)) c.tens[i].alloc(size_t(nt));
+    return c.tens[i].p;
 }
+
+void sync_check(Ctx& c) {
+    c.check_adi_error(false);
+    c.sync();
+}
+
+}  // namespace
+
+extern "C" {
+
+ccf_status ccf_velocity_from_vorticity(ccf_ctx* ctx, const double* lam_w, const double* gam_w, double* lam_v,
+                                       double* gam_v) {
+    // proj/src/ptns.cpp:85-91: (lambda_v, gamma_v) = (gamma_w, Poisson3D(-lambda_w))
+    return guard(ctx, [&](Ctx& c) {
+        ccf::Pipeline& P = ctx->pl();
+        double *l = tens(c, 0), *g = tens(c, 1), *u = tens(c, 2);
+        c.load_coeff(lam_w, l, false, 0, 0);
+        c.load_coeff(gam_w, g, false, 0, 1);
+        c.require_finite(l, P.T, "solve_poisson_3d");
+        P.poisson(l, -1.0, u);
+        sync_check(c);
+        c.store_coeff(g, lam_v, false, 0, 0);
+        c.store_coeff(u, gam_v, false, 0, 1);
+        c.sync();
+    });
+}
+
+ccf_status ccf_nonlinear(ccf_ctx* ctx, const double* lam_v, const double* gam_v, const double* lam_w,
+                         const double* gam_w, double* lam_out, double* gam_out) {
+    // proj/src/ptns.cpp:114-149
+    return guard(ctx, [&](Ctx& c) {
+        ccf::Pipeline& P = ctx->pl();
+        double *a = tens(c, 0), *b = tens(c, 1), *d = tens(c, 2), *e = tens(c, 3), *o1 = tens(c, 4), *o2 = tens(c, 5);
+        c.load_coeff(lam_v, a, false, 0, 0);
+        c.load_coeff(gam_v, b, false, 0, 1);
+        c.load_coeff(lam_w, d, false, 0, 2);
+        c.load_coeff(gam_w, e, false, 0, 3);
+        P.nonlinear(a, b, d, e, o1, o2);
+        c.store_coeff(o1, lam_out, false, 0, 0);
+        c.store_coeff(o2, gam_out, false, 0, 1);
+        c.sync();
+    });
+}
+
+ccf_status ccf_pt_synthesize(ccf_ctx* ctx, const double* lam, const double* gam, double* vr, double* vt, double* vz) {
+    // proj/src/ptns.cpp:42-57
+    return guard(ctx, [&](Ctx& c) {
+        if (c.m % 2) throw Error(ccf::DOMAIN_ERROR, "pt_synthesize: even m required (no r = 0 grid node)");
+        ccf::Pipeline& P = ctx->pl();
+        double *l = tens(c, 0), *g = tens(c, 1), *o0 = tens(c, 2), *o1 = tens(c, 3), *o2 = tens(c, 4);
+        c.load_coeff(lam, l, false, 0, 0);
+        c.load_coeff(gam, g, false, 0, 1);
+        const double* L[1] = {l};
+        const double* G[1] = {g};
+        double* R[1] = {o0};
+        double* Tt[1] = {o1};
+        double* Z[1] = {o2};
+        P.pt_synthesize(1, L, G, R, Tt, Z);
+        c.store_coeff(o0, vr, false, 1, 0);
+        c.store_coeff(o1, vt, false, 1, 1);
+        c.store_coeff(o2, vz, false, 0, 0);
+        c.sync();
+    });
+}
+
+ccf_status ccf_curl_vector(ccf_ctx* ctx, const double* vr, const double* vt, const double* vz, double* or_,
+                           double* ot, double* oz) {
+    // proj/src/ptns.cpp:25-33 on a physical vector field (r, theta components azimuthal-flip class)
+    return guard(ctx, [&](Ctx& c) {
+        ccf::Pipeline& P = ctx->pl();
+        double *a = tens(c, 0), *b = tens(c, 1), *d = tens(c, 2), *o0 = tens(c, 3), *o1 = tens(c, 4), *o2 = tens(c, 5);
+        c.load_coeff(vr, a, false, 1, 0);
+        c.load_coeff(vt, b, false, 1, 1);
+        c.load_coeff(vz, d, false, 0, 2);
+        P.curl_decompose(a, b, d, o0, o1, o2, nullptr, nullptr);
+        c.store_coeff(o0, or_, false, 1, 0);
+        c.store_coeff(o1, ot, false, 1, 1);
+        c.store_coeff(o2, oz, false, 0, 0);
+        c.sync();
+    });
+}
+
+ccf_status ccf_pt_decompose(ccf_ctx* ctx, const double* vr, const double* vt, const double* vz, double* lam,
+                            double* gam) {
+    // proj/src/ptns.cpp:59-77 (divergence check off, as on the NS path)
+    return guard(ctx, [&](Ctx& c) {
+        ccf::Pipeline& P = ctx->pl();
+        double *a = tens(c, 0), *b = tens(c, 1), *d = tens(c, 2), *o0 = tens(c, 3), *o1 = tens(c, 4);
+        c.load_coeff(vr, a, false, 1, 0);
+        c.load_coeff(vt, b, false, 1, 1);
+        c.load_coeff(vz, d, false, 0, 2);
+        P.decompose(a, b, d, o0, o1);
+        c.store_coeff(o0, lam, false, 0, 0);
+        c.store_coeff(o1, gam, false, 0, 1);
+        c.sync();
+    });
+}
+
+ccf_status ccf_hpoisson(ccf_ctx* ctx, const double* rhs, double* u) {
+    // proj/src/solvers.cpp:177-203
+    return guard(ctx, [&](Ctx& c) {
+        ccf::Pipeline& P = ctx->pl();
+        double *a = tens(c, 0), *o = tens(c, 1);
+        c.load_coeff(rhs, a, false, 0, 0);
+        c.require_finite(a, P.T, "solve_horizontal_poisson");
+        P.hpoisson(a, o);
+        c.store_coeff(o, u, false, 0, 0);
+        c.sync();
+    });
+}
+
+ccf_status ccf_calculus(ccf_ctx* ctx, int op, const double* in, double* out) {
+    // proj/src/calculus.cpp; both parity classes of the input are processed
+    return guard(ctx, [&](Ctx& c) {
+        if (op == 4 && c.m % 2) throw Error(ccf::DOMAIN_ERROR, "divide_r: even m required");
+        ccf::Pipeline& P = ctx->pl();
+        for (int cls = 0; cls < 2; ++cls) {
+            double *a = tens(c, 0), *o = tens(c, 1);
+            c.load_coeff(in, a, false, cls, 0);
+            const int ocls = (op == 0 || op == 4) ? 1 - cls : cls;
+            P.calculus(op, cls, a, o);
+            c.store_coeff(o, out, false, ocls, 0, cls == 1);
+        }
+        c.sync();
+    });
+}
+
+ccf_status ccf_curl_pt(ccf_ctx* ctx, const double* lam, const double* gam, double* lam_out, double* gam_out) {
+    // proj/src/ptns.cpp:79-83: (lambda, gamma) -> (-lap gamma, lambda)
+    return guard(ctx, [&](Ctx& c) {
+        ccf::Pipeline& P = ctx->pl();
+        double *g = tens(c, 0), *o = tens(c, 1), *l = tens(c, 2);
+        c.load_coeff(gam, g, false, 0, 0);
+        P.calculus(6, 0, g, o);
+        P.scale(o, -1.0);
+        c.load_coeff(lam, l, false, 0, 1);
+        c.store_coeff(o, lam_out, false, 0, 0);
+        c.store_coeff(l, gam_out, false, 0, 1);
+        c.sync();
+    });
+}
+
+ccf_status ccf_analyze(ccf_ctx* ctx, const double* values, double* coeffs) {
+    // proj/src/transform.cpp:122-165 (arbitrary real fields, full spectrum)
+    return guard(ctx, [&](Ctx& c) {
+        ccf::Pipeline& P = ctx->pl();
+        P.analyze_full(values, coeffs);
+        c.sync();
+    });
+}
+
+ccf_status ccf_synthesize(ccf_ctx* ctx, const double* coeffs, double* values) {
+    // proj/src/transform.cpp:167-203
+    return guard(ctx, [&](Ctx& c) {
+        ccf::Pipeline& P = ctx->pl();
+        P.synthesize_full(coeffs, values);
+        c.sync();
+    });
+}
+
+// ---- NSStepper (ptns.hpp:104-127)
+ccf_status ccf_ns_create(ccf_ctx* ctx, double reynolds, double h, int order, int disable_nonlinear, const double* lam0,
+                         const double* gam0, ccf_ns_state** out) {
+    return guard(ctx, [&](Ctx& c) {
+        if (order < 1 || order > 4) throw Error(ccf::DOMAIN_ERROR, "BDFScheme: order must be in {1,2,3,4}");
+        if (c.m % 2) throw Error(ccf::DOMAIN_ERROR, "NSStepper: even m required for the nonlinear pipeline");
+        auto st = std::make_unique<ccf_ns_state>();
+        st->ctx = ctx;
+        ccf::NSState& s = st->st;
+        s.pl = &ctx->pl();
+        s.reynolds = reynolds;
+        s.h = h;
+        s.order = order;
+        s.disable_nonlinear = disable_nonlinear != 0;
+        const long T = s.pl->T;
+        for (int i = 0; i < 5; ++i) {
+            s.lam[i].alloc(size_t(T));
+            s.gam[i].alloc(size_t(T));
+        }
+        for (int i = 0; i < 4; ++i) {
+            s.nl[i].alloc(size_t(T));
+            s.ng[i].alloc(size_t(T));
+        }
+        CCF_CUDA(cudaMalloc(&s.dflag, sizeof(int)));
+        CCF_CUDA(cudaMemset(s.dflag, 0, sizeof(int)));
+        c.load_coeff(lam0, s.lam[0].p, false, 0, 0);  // parity projection of the initial data (ptns.cpp:190-191)
+        c.load_coeff(gam0, s.gam[0].p, false, 0, 1);
+        // build every solver set the run needs before any graph capture
+        if (!s.disable_nonlinear) c.set(false, true, 1.0);
+        for (int b = 1; b <= order; ++b) {
+            static const double K[4] = {1.0, 2.0 / 3.0, 6.0 / 11.0, 12.0 / 25.0};
+            c.set(false, false, K[b - 1] * h * (1.0 / reynolds));
+        }
+        c.sync();
+        *out = st.release();
+    });
+}
+
+ccf_status ccf_ns_step(ccf_ns_state* st, int nsteps) {
+    if (!st) return CCF_INTERNAL_ERROR;
+    return guard(st->ctx, [&](Ctx& c) {
+        for (int i = 0; i < nsteps; ++i) st->st.step_once();
+        c.check_adi_error(false);
+        int f = 0;
+        CCF_CUDA(cudaMemcpyAsync(&f, st->st.dflag, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        if (f) throw Error(ccf::NUMERICAL, "NSStepper: non-finite state at step " + std::to_string(st->st.steps));
+    });
+}
+
+ccf_status ccf_ns_get_omega(ccf_ns_state* st, double* lam, double* gam, double* time, int* steps_taken) {
+    if (!st) return CCF_INTERNAL_ERROR;
+    return guard(st->ctx, [&](Ctx& c) {
+        c.store_coeff(st->st.lam[st->st.head].p, lam, false, 0, 0);
+        c.store_coeff(st->st.gam[st->st.head].p, gam, false, 0, 1);
+        c.sync();
+        if (time) *time = st->st.time;
+        if (steps_taken) *steps_taken = st->st.steps;
+    });
+}
+
+ccf_status ccf_ns_destroy(ccf_ns_state* st) {
+    if (!st) return CCF_OK;
+    if (st->ctx && st->ctx->c) cudaSetDevice(st->ctx->c->device);
+    delete st;
+    return CCF_OK;
+}
+
+ccf_status ccf_ns_set_graphs(ccf_ns_state* st, int enable) {
+    if (!st) return CCF_INTERNAL_ERROR;
+    st->st.use_graphs = enable != 0;
+    return CCF_OK;
+}
+
+ccf_status ccf_ns_launches_per_step(ccf_ns_state* st, long* n) {
+    if (!st || !n) return CCF_INTERNAL_ERROR;
+    *n = st->st.launches_per_step;
+    return CCF_OK;
+}
+
+}  // extern "C"

@@ -41,6 +41,7 @@ struct AdiTask {
 // Tensor geometry in the compressed layout.
 struct Geo {
     int m, n, p, mh, nh, nslots;
+    int M, N;           // (m-2)/2, (n-2)/2: reduced (Dirichlet-recombined) sizes per parity
     long plane_stride;  // n * mh
     long slot_stride;   // 2 * n * mh
 };

@@ -43,6 +43,8 @@ static Geo make_geo(int m, int n, int p, int nslots) {
     g.mh = m / 2;
     g.nh = n / 2;
     g.nslots = nslots;
+    g.M = (m - 2) / 2;
+    g.N = (n - 2) / 2;
     g.plane_stride = long(n) * (m / 2);
     g.slot_stride = 2 * g.plane_stride;
     return g;
@@ -196,11 +198,8 @@ void Ctx::run_adi(DevSet& set, bool full, int ntensor, const double* const* src0
     P.e2 = ws.e2;
     P.active = ws.active;
     const int nts = ntensor * g.nslots;
-    CCF_CUDA(cudaMemsetAsync(ws.res2, 0, sizeof(double) * nts, stream));
-    CCF_CUDA(cudaMemsetAsync(ws.e2, 0, sizeof(double) * nts, stream));
-    std::vector<int> ones(size_t(nts), 1);
-    CCF_CUDA(cudaMemcpyAsync(ws.active, ones.data(), sizeof(int) * nts, cudaMemcpyHostToDevice, stream));
-    CCF_CUDA(cudaStreamSynchronize(stream));  // `ones` is a host temporary
+    adi_init_kernel<<<(nts + 127) / 128, 128, 0, stream>>>(ws.active, ws.res2, ws.e2, nts);
+    ++launches;
     const int threads = ((std::max(M, N) + 31) / 32) * 32;
     const size_t smem = adi_smem_bytes();
     RoundCheck rc{};
@@ -269,19 +268,33 @@ void Ctx::load_coeff(const double* ref, double* dst, bool full, int cls, int slo
     ++launches;
 }
 
-void Ctx::store_coeff(const double* src, double* ref, bool full, int cls, int slot) {
+void Ctx::store_coeff(const double* src, double* ref, bool full, int cls, int slot, bool accumulate) {
     const long nref = 2L * m * n * p;
     double* dref = ref;
     const bool host = !is_device_ptr(ref);
     if (host) {
         if (stage_out[slot].n < size_t(nref)) stage_out[slot].alloc(size_t(nref));
         dref = stage_out[slot].p;
+        if (accumulate)
+            CCF_CUDA(cudaMemcpyAsync(dref, ref, sizeof(double) * nref, cudaMemcpyHostToDevice, stream));
     }
     const Geo& g = geo(full);
     const long total = long(p) * n * m;
-    h_to_ref_kernel<<<std::min<long>(4736, (total + 255) / 256), 256, 0, stream>>>(src, dref, g, int(full), cls);
+    h_to_ref_kernel<<<std::min<long>(4736, (total + 255) / 256), 256, 0, stream>>>(src, dref, g, int(full), cls, int(accumulate));
     ++launches;
     if (host) CCF_CUDA(cudaMemcpyAsync(ref, dref, sizeof(double) * nref, cudaMemcpyDeviceToHost, stream));
+}
+
+void Ctx::load_values(const double* vals, double* dst) {
+    const long nv = long(m) * n * p;
+    if (is_device_ptr(vals)) CCF_CUDA(cudaMemcpyAsync(dst, vals, sizeof(double) * nv, cudaMemcpyDeviceToDevice, stream));
+    else CCF_CUDA(cudaMemcpyAsync(dst, vals, sizeof(double) * nv, cudaMemcpyHostToDevice, stream));
+}
+
+void Ctx::store_values(const double* src, double* vals) {
+    const long nv = long(m) * n * p;
+    if (is_device_ptr(vals)) CCF_CUDA(cudaMemcpyAsync(vals, src, sizeof(double) * nv, cudaMemcpyDeviceToDevice, stream));
+    else CCF_CUDA(cudaMemcpyAsync(vals, src, sizeof(double) * nv, cudaMemcpyDeviceToHost, stream));
 }
 
 }  // namespace ccf

@@ -89,7 +89,9 @@ struct Ctx {
     bool is_device_ptr(const void* p) const;
     // Reference-layout coefficient tensor (host or device) -> compressed device tensor.
     void load_coeff(const double* ref, double* dst, bool full, int cls, int slot);
-    void store_coeff(const double* src, double* ref, bool full, int cls, int slot);
+    void store_coeff(const double* src, double* ref, bool full, int cls, int slot, bool accumulate = false);
+    void load_values(const double* vals, double* dst);  // reference-layout real field -> device
+    void store_values(const double* src, double* vals);
     void require_finite(const double* dptr, long n, const char* what);
     void sync();
 };

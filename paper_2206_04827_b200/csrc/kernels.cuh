@@ -22,10 +22,14 @@ struct RoundCheck {
     unsigned long long* iters;  // executed sub-problem iterations (4 sub-problems per (tensor, slot))
 };
 __global__ void adi_round_check(RoundCheck c);
+__global__ void adi_init_kernel(int* active, double* res2, double* e2, int n);
 
 // layout.cu
 __global__ void ref_to_h_kernel(const double* __restrict__ ref, double* __restrict__ out, Geo g, int full, int cls);
-__global__ void h_to_ref_kernel(const double* __restrict__ in, double* __restrict__ ref, Geo g, int full, int cls);
+__global__ void h_to_ref_kernel(const double* __restrict__ in, double* __restrict__ ref, Geo g, int full, int cls,
+                                int accumulate);
+__global__ void real_to_complex_kernel(const double* __restrict__ in, double* __restrict__ out, long n);
+__global__ void complex_re_kernel(const double* __restrict__ in, double* __restrict__ out, long n);
 __global__ void finite_check_kernel(const double* __restrict__ x, long n, int* flag);
 struct Combo {
     const double* src[kMaxSrc];
@@ -35,5 +39,78 @@ struct Combo {
     long n;
 };
 __global__ void combo_kernel(Combo c);
+
+// transform.cu
+struct GemmBatch {
+    const double* const* A;
+    const double* const* B;
+    double* const* C;
+    int M, N, K;
+    long lda, ldb, ldc;
+    double alpha, beta;
+};
+__global__ void dgemm_batched_kernel(GemmBatch g);
+struct ThetaCross {
+    Geo g;
+    int logp, tj;
+    const double* in[6];
+    double* out[3];
+    const double2* tw;
+};
+__global__ void theta_cross_kernel(ThetaCross t);
+__global__ void theta_dft_full_kernel(const double* __restrict__ in, double* __restrict__ out, int m, int n, int p,
+                                      int dir, const double2* __restrict__ twp);
+
+// pencil.cu
+struct DzBatch {
+    Geo g;
+    int count;
+    const double* in[6];
+    double* out[6];
+};
+__global__ void dz_kernel(DzBatch d);
+struct PtSynth {
+    Geo g;
+    int count;
+    const double* lam[2];
+    const double* gam[2];
+    const double* dzg[2];
+    double* vr[2];
+    double* vt[2];
+    double* vz[2];
+    double* scratch;  // count * nslots * n * 2 * mh
+    const double* q;  // odd interpolation coefficients of 1/r (mh)
+};
+__global__ void pt_synth_kernel(PtSynth a);
+struct CurlDecomp {
+    Geo g;
+    int decompose_only;  // 1: (ar, at, az) are already (v_r, v_t, v_z); dzat unused
+    const double *ar, *at, *az, *dzar, *dzat;
+    double *out_r, *out_t, *out_z;  // optional curl components
+    double *lam, *gam;              // optional PT scalars of the curl
+    double* scratch;                // nslots * n * 6 * mh
+    const double* q;
+    const double* hpc;  // per slot: M x 8 LU(recombine(L_w)) [L, piv, inv, Uf0..2, 0, 0]
+    const double* hpr;  // per parity: M x 8 compressed R R C02 rows (offsets -1..3)
+};
+__global__ void curl_decomp_kernel(CurlDecomp a);
+struct HpArgs {
+    Geo g;
+    const double* in;
+    double* out;
+    double* scratch;
+    const double* hpc;
+    const double* hpr;
+};
+__global__ void hp_kernel(HpArgs a);
+struct CalcArgs {
+    Geo g;
+    int op, cls;
+    const double* in;
+    double* out;
+    double* scratch;
+    const double* q;
+};
+__global__ void calc_kernel(CalcArgs a);
 
 }  // namespace ccf

@@ -42,7 +42,8 @@ __global__ void ref_to_h_kernel(const double* __restrict__ ref, double* __restri
 }
 
 // compressed -> ref (interleaved complex), Hermitian completion in half mode.
-__global__ void h_to_ref_kernel(const double* __restrict__ in, double* __restrict__ ref, Geo g, int full, int cls) {
+__global__ void h_to_ref_kernel(const double* __restrict__ in, double* __restrict__ ref, Geo g, int full, int cls,
+                                int accumulate) {
     const long total = long(g.p) * g.n * g.m;
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < total; i += long(gridDim.x) * blockDim.x) {
         const int j = int(i % g.m);
@@ -59,8 +60,13 @@ __global__ void h_to_ref_kernel(const double* __restrict__ in, double* __restric
             im = in[off + g.plane_stride];
             if (!full && l != 0 && l < g.p / 2) im = -im;  // w < 0: conjugate partner
         }
-        ref[2 * i] = re;
-        ref[2 * i + 1] = im;
+        if (accumulate) {
+            ref[2 * i] += re;
+            ref[2 * i + 1] += im;
+        } else {
+            ref[2 * i] = re;
+            ref[2 * i + 1] = im;
+        }
     }
 }
 
@@ -70,6 +76,18 @@ __global__ void finite_check_kernel(const double* __restrict__ x, long n, int* f
             atomicExch(flag, 1);
             return;
         }
+}
+
+__global__ void real_to_complex_kernel(const double* __restrict__ in, double* __restrict__ out, long n) {
+    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
+        out[2 * i] = in[i];
+        out[2 * i + 1] = 0.0;
+    }
+}
+
+__global__ void complex_re_kernel(const double* __restrict__ in, double* __restrict__ out, long n) {
+    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x)
+        out[i] = in[2 * i];
 }
 
 // out = sum_i w_i * src_i  (BDF history / IMEX extrapolation combinations,

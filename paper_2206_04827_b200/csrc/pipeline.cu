@@ -1,0 +1,689 @@
+// NS time-step pipeline (see pipeline.hpp).
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "pipeline.hpp"
+
+namespace ccf {
+
+namespace {
+
+std::vector<double> cheb_points_double(int count) {  // proj/src/grid.cpp:16-26 (pinned endpoints)
+    std::vector<double> x(static_cast<size_t>(count));
+    for (int j = 0; j < count; ++j) x[size_t(j)] = std::cos(double(count - j - 1) * M_PI / double(count - 1));
+    x.front() = -1.0;
+    x.back() = 1.0;
+    if (count % 2 == 1) x[size_t(count / 2)] = 0.0;
+    return x;
+}
+
+// cos(pi * a / L) with exact integer reduction, long double
+long double cospi_frac(long a, long L) {
+    long r = a % (2 * L);
+    if (r < 0) r += 2 * L;
+    return cosl(3.141592653589793238462643383279502884L * (long double)r / (long double)L);
+}
+
+void upload(DBuf& d, const std::vector<double>& h) {
+    d.alloc(h.size());
+    CCF_CUDA(cudaMemcpy(d.p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+unsigned blocks_for(long n, int t) { return unsigned((n + t - 1) / t); }
+
+}  // namespace
+
+TransformPlan::TransformPlan(Ctx& c) {
+    const int m = c.m, n = c.n, p = c.p, mh = m / 2, M = c.M;
+    const long L = m - 1, Lz = n - 1;
+    // r synthesis / analysis on the r > 0 half grid, per coefficient parity j0
+    for (int j0 = 0; j0 < 2; ++j0) {
+        std::vector<double> S(size_t(mh) * mh), A(size_t(mh) * mh);
+        for (int i = 0; i < mh; ++i) {
+            const int k = 2 * i + j0;
+            const long double eps = (k == 0 || k == m - 1) ? 0.5L : 1.0L;
+            for (int jr = 0; jr < mh; ++jr) {
+                const int s = mh - 1 - jr;  // descending-x index of grid point j = mh + jr
+                S[size_t(i) * mh + jr] = double(cospi_frac(long(k) * s, L));
+                const long double ws = (s == 0) ? 1.0L : 2.0L;
+                A[size_t(jr) * mh + i] = double(eps / (long double)L * 2.0L * ws * cospi_frac(long(k) * s, L));
+            }
+        }
+        upload(SrT[j0], S);
+        upload(ArT[j0], A);
+    }
+    // z: dense n x n (both parities)
+    {
+        std::vector<double> S(size_t(n) * n), A(size_t(n) * n);
+        for (int kz = 0; kz < n; ++kz)
+            for (int k = 0; k < n; ++k) {
+                const int s = n - 1 - kz;
+                S[size_t(kz) * n + k] = double(cospi_frac(long(k) * s, Lz));
+                const long double eps = (k == 0 || k == n - 1) ? 0.5L : 1.0L;
+                const long double ws = (s == 0 || s == n - 1) ? 1.0L : 2.0L;
+                A[size_t(k) * n + kz] = double(eps / (long double)Lz * ws * cospi_frac(long(k) * s, Lz));
+            }
+        upload(Sz, S);
+        upload(Az, A);
+    }
+    // r: dense m x m (API transforms): values_j = sum_k c_k T_k(r_j);  c_k = sum_j A[k][j] values_j
+    {
+        std::vector<double> S(size_t(m) * m), A(size_t(m) * m);
+        for (int j = 0; j < m; ++j)
+            for (int k = 0; k < m; ++k) {
+                const int s = m - 1 - j;
+                S[size_t(j) * m + k] = double(cospi_frac(long(k) * s, L));
+                const long double eps = (k == 0 || k == m - 1) ? 0.5L : 1.0L;
+                const long double ws = (s == 0 || s == m - 1) ? 1.0L : 2.0L;
+                A[size_t(k) * m + j] = double(eps / (long double)L * ws * cospi_frac(long(k) * s, L));
+            }
+        upload(Rfull_S, S);
+        upload(Rfull_A, A);
+    }
+    // q: odd coefficients of the grid interpolant of 1/r (values divided by the reference's double r_j)
+    {
+        const auto r = cheb_points_double(m);
+        std::vector<double> qv(static_cast<size_t>(mh));
+        for (int i = 0; i < mh; ++i) {
+            const int k = 2 * i + 1;
+            const long double eps = (k == m - 1) ? 0.5L : 1.0L;
+            long double acc = 0.0L;
+            for (int s = 0; s < m; ++s) {
+                const int j = m - 1 - s;
+                const long double ws = (s == 0 || s == m - 1) ? 1.0L : 2.0L;
+                acc += ws * (1.0L / (long double)r[size_t(j)]) * cospi_frac(long(k) * s, L);
+            }
+            qv[size_t(i)] = double(eps / (long double)L * acc);
+        }
+        upload(q, qv);
+    }
+    // theta twiddles
+    {
+        int lg = 0;
+        while ((1 << lg) < p) ++lg;
+        logp = ((1 << lg) == p) ? lg : -1;
+        std::vector<double> t(static_cast<size_t>(p)), tf(static_cast<size_t>(2 * p));
+        for (int i = 0; i < p / 2; ++i) {
+            t[size_t(2 * i)] = double(cospi_frac(2L * i, p));
+            t[size_t(2 * i + 1)] = -double(cospi_frac(2L * i - p / 2, p));  // -sin(2 pi i / p)
+        }
+        for (int i = 0; i < p; ++i) {
+            tf[size_t(2 * i)] = double(cospi_frac(2L * i, p));
+            tf[size_t(2 * i + 1)] = -double(cospi_frac(2L * i - p / 2, p));
+        }
+        upload(tw, t);
+        upload(twfull, tf);
+    }
+    // horizontal Poisson: LU(recombine(L_w)) per half slot (proj/src/solvers.cpp:189-195), R R C02 per parity
+    {
+        const Geo& g = c.gh;
+        std::vector<double> hc(size_t(g.nslots) * M * 8, 0.0), hr(size_t(2) * M * 8, 0.0);
+        for (int s = 0; s < g.nslots; ++s) {
+            const int w = (s == p / 2) ? -p / 2 : s;
+            const int j0 = ((w % 2) + 2) % 2;
+            const Dense lw = recombine(radial_laplacian(c.sizeops->ur, w));
+            const CBand b = compress(lw, j0, M, M, -1, 2);
+            CLU lu;
+            try {
+                lu = banded_lu(b, 1, 2);
+            } catch (const Error&) {
+                throw Error(SINGULAR, "solve_horizontal_poisson: singular column system");
+            }
+            for (int a = 0; a < M; ++a) {
+                double* r = hc.data() + (size_t(s) * M + a) * 8;
+                r[0] = lu.L[size_t(a)];
+                r[1] = double(lu.piv[size_t(a)]);
+                r[2] = lu.inv[size_t(a)];
+                for (int t = 0; t < 3; ++t) r[3 + t] = lu.U[size_t(a) * 3 + t] * lu.inv[size_t(a)];
+            }
+        }
+        for (int j0 = 0; j0 < 2; ++j0) {
+            const CBand b = compress(c.sizeops->ur.r2, j0, M, mh, -1, 3);
+            for (int a = 0; a < M; ++a)
+                for (int d = -1; d <= 3; ++d) hr[(size_t(j0) * M + a) * 8 + size_t(d + 1)] = b.at(a, d);
+        }
+        upload(hpc, hc);
+        upload(hpr, hr);
+    }
+}
+
+// ---------------------------------------------------------------- GEMM plans
+void GemmPlan::upload() {
+    const size_t nb = C.size();
+    if (!dA) {
+        CCF_CUDA(cudaMalloc(&dA, nb * sizeof(void*)));
+        CCF_CUDA(cudaMalloc(&dB, nb * sizeof(void*)));
+        CCF_CUDA(cudaMalloc(&dC, nb * sizeof(void*)));
+    }
+    CCF_CUDA(cudaMemcpy(dA, A.data(), nb * sizeof(void*), cudaMemcpyHostToDevice));
+    CCF_CUDA(cudaMemcpy(dB, B.data(), nb * sizeof(void*), cudaMemcpyHostToDevice));
+    CCF_CUDA(cudaMemcpy(dC, C.data(), nb * sizeof(void*), cudaMemcpyHostToDevice));
+}
+
+void GemmPlan::launch(cudaStream_t s) const {
+    GemmBatch g{dA, dB, dC, M, N, K, lda, ldb, ldc, alpha, beta};
+    const dim3 grid(unsigned((N + 63) / 64), unsigned((M + 63) / 64), unsigned(C.size()));
+    dgemm_batched_kernel<<<grid, 128, 0, s>>>(g);
+}
+
+GemmPlan::~GemmPlan() {
+    if (dA) cudaFree(dA);
+    if (dB) cudaFree(dB);
+    if (dC) cudaFree(dC);
+}
+
+// ---------------------------------------------------------------- Pipeline
+Pipeline::Pipeline(Ctx& c_) : c(c_), tp(c_), T(c_.tensor_doubles(false)) {
+    big_scratch(size_t(3) * T);  // pencil scratch: max(pt_synth 2 pairs x 2, curl 6 pencils per thread)
+}
+
+double* Pipeline::scratch(int i) {
+    while (int(scr_.size()) <= i) scr_.emplace_back();
+    if (scr_[size_t(i)].n < size_t(T)) scr_[size_t(i)].alloc(size_t(T));
+    return scr_[size_t(i)].p;
+}
+
+double* Pipeline::big_scratch(size_t doubles) {
+    if (big_.n < doubles) big_.alloc(doubles);
+    return big_.p;
+}
+
+GemmPlan& Pipeline::gemm(const std::string& key, bool& fresh) {
+    auto& slot = gemms_[key];
+    fresh = !slot;
+    if (!slot) slot = std::make_unique<GemmPlan>();
+    return *slot;
+}
+
+static std::string ptr_key(const char* tag, int count, const void* const* a, const void* const* b, const int* cls) {
+    std::string k(tag);
+    for (int i = 0; i < count; ++i) {
+        k += ":" + std::to_string(reinterpret_cast<uintptr_t>(a[i])) + "/" +
+             std::to_string(reinterpret_cast<uintptr_t>(b[i]));
+        if (cls) k += "/" + std::to_string(cls[i]);
+    }
+    return k;
+}
+
+void Pipeline::dz(const std::vector<const double*>& in, const std::vector<double*>& out) {
+    const Geo& g = c.gh;
+    DzBatch d{};
+    d.g = g;
+    d.count = int(in.size());
+    for (size_t i = 0; i < in.size(); ++i) {
+        d.in[i] = in[i];
+        d.out[i] = out[i];
+    }
+    const long n = long(g.nslots) * 2 * g.mh * d.count;
+    dz_kernel<<<blocks_for(n, 128), 128, 0, c.stream>>>(d);
+    ++c.launches;
+}
+
+void Pipeline::pt_synthesize(int count, const double* const* lam, const double* const* gam, double* const* vr,
+                             double* const* vt, double* const* vz) {
+    const Geo& g = c.gh;
+    std::vector<const double*> gi(gam, gam + count);
+    std::vector<double*> dzo;
+    for (int i = 0; i < count; ++i) dzo.push_back(scratch(20 + i));
+    dz(gi, dzo);
+    PtSynth a{};
+    a.g = g;
+    a.count = count;
+    for (int i = 0; i < count; ++i) {
+        a.lam[i] = lam[i];
+        a.gam[i] = gam[i];
+        a.dzg[i] = dzo[size_t(i)];
+        a.vr[i] = vr[i];
+        a.vt[i] = vt[i];
+        a.vz[i] = vz[i];
+    }
+    a.scratch = big_scratch(size_t(count) * g.nslots * g.n * 2 * g.mh);
+    a.q = tp.q.p;
+    const long n = long(count) * g.nslots * g.n;
+    pt_synth_kernel<<<blocks_for(n, 64), 64, 0, c.stream>>>(a);
+    ++c.launches;
+}
+
+void Pipeline::rz_synth(int count, const double* const* in, const int* cls, double* const* out) {
+    const Geo& g = c.gh;
+    double* tmp[8];
+    for (int i = 0; i < count; ++i) tmp[i] = scratch(24 + i);
+    bool fresh;
+    GemmPlan& r = gemm(ptr_key("rs", count, reinterpret_cast<const void* const*>(in),
+                               reinterpret_cast<const void* const*>(out), cls),
+                       fresh);
+    GemmPlan& z = gemm(ptr_key("zs", count, reinterpret_cast<const void* const*>(in),
+                               reinterpret_cast<const void* const*>(out), cls),
+                       fresh);
+    if (fresh) {
+        for (int t = 0; t < count; ++t)
+            for (int s = 0; s < g.nslots; ++s)
+                for (int pl = 0; pl < 2; ++pl) {
+                    const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
+                    const int w = (s == g.p / 2) ? -g.p / 2 : s;
+                    const int j0 = ((w + cls[t]) % 2 + 2) % 2;
+                    r.A.push_back(in[t] + off);
+                    r.B.push_back(tp.SrT[j0].p);
+                    r.C.push_back(tmp[t] + off);
+                    z.A.push_back(tp.Sz.p);
+                    z.B.push_back(tmp[t] + off);
+                    z.C.push_back(out[t] + off);
+                }
+        r.M = g.n;
+        r.N = g.mh;
+        r.K = g.mh;
+        r.lda = g.mh;
+        r.ldb = g.mh;
+        r.ldc = g.mh;
+        z.M = g.n;
+        z.N = g.mh;
+        z.K = g.n;
+        z.lda = g.n;
+        z.ldb = g.mh;
+        z.ldc = g.mh;
+        r.upload();
+        z.upload();
+    }
+    r.launch(c.stream);
+    z.launch(c.stream);
+    c.launches += 2;
+}
+
+void Pipeline::rz_analyze(int count, const double* const* in, const int* cls, double* const* out) {
+    const Geo& g = c.gh;
+    double* tmp[8];
+    for (int i = 0; i < count; ++i) tmp[i] = scratch(24 + i);
+    bool fresh;
+    GemmPlan& z = gemm(ptr_key("za", count, reinterpret_cast<const void* const*>(in),
+                               reinterpret_cast<const void* const*>(out), cls),
+                       fresh);
+    GemmPlan& r = gemm(ptr_key("ra", count, reinterpret_cast<const void* const*>(in),
+                               reinterpret_cast<const void* const*>(out), cls),
+                       fresh);
+    if (fresh) {
+        for (int t = 0; t < count; ++t)
+            for (int s = 0; s < g.nslots; ++s)
+                for (int pl = 0; pl < 2; ++pl) {
+                    const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
+                    const int w = (s == g.p / 2) ? -g.p / 2 : s;
+                    const int j0 = ((w + cls[t]) % 2 + 2) % 2;
+                    z.A.push_back(tp.Az.p);
+                    z.B.push_back(in[t] + off);
+                    z.C.push_back(tmp[t] + off);
+                    r.A.push_back(tmp[t] + off);
+                    r.B.push_back(tp.ArT[j0].p);
+                    r.C.push_back(out[t] + off);
+                }
+        z.M = g.n;
+        z.N = g.mh;
+        z.K = g.n;
+        z.lda = g.n;
+        z.ldb = g.mh;
+        z.ldc = g.mh;
+        r.M = g.n;
+        r.N = g.mh;
+        r.K = g.mh;
+        r.lda = g.mh;
+        r.ldb = g.mh;
+        r.ldc = g.mh;
+        z.upload();
+        r.upload();
+    }
+    z.launch(c.stream);
+    r.launch(c.stream);
+    c.launches += 2;
+}
+
+void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
+    const Geo& g = c.gh;
+    if (tp.logp < 0) throw Error(DOMAIN_ERROR, "ccf: the fused theta kernel needs p to be a power of two");
+    ThetaCross t{};
+    t.g = g;
+    t.logp = tp.logp;
+    int tj = 8;
+    while (tj > 1 && size_t(3) * tj * g.p * sizeof(double2) > 100 * 1024) tj /= 2;
+    t.tj = tj;
+    for (int i = 0; i < 6; ++i) t.in[i] = v6[i];
+    for (int i = 0; i < 3; ++i) t.out[i] = a3[i];
+    t.tw = reinterpret_cast<const double2*>(tp.tw.p);
+    const size_t smem = size_t(3) * tj * g.p * sizeof(double2);
+    static bool attr = false;
+    if (!attr) {
+        CCF_CUDA(cudaFuncSetAttribute(theta_cross_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    const dim3 grid(unsigned((g.mh + tj - 1) / tj), unsigned(g.n));
+    theta_cross_kernel<<<grid, 256, smem, c.stream>>>(t);
+    ++c.launches;
+}
+
+void Pipeline::curl_decompose(const double* ar, const double* at, const double* az, double* out_r, double* out_t,
+                              double* out_z, double* lam, double* gam) {
+    const Geo& g = c.gh;
+    double* dzar = scratch(30);
+    double* dzat = scratch(31);
+    dz({ar, at}, {dzar, dzat});
+    CurlDecomp a{};
+    a.g = g;
+    a.ar = ar;
+    a.at = at;
+    a.az = az;
+    a.dzar = dzar;
+    a.dzat = dzat;
+    a.out_r = out_r;
+    a.out_t = out_t;
+    a.out_z = out_z;
+    a.lam = lam;
+    a.gam = gam;
+    a.scratch = big_scratch(size_t(g.nslots) * g.n * 6 * g.mh);
+    a.q = tp.q.p;
+    a.hpc = tp.hpc.p;
+    a.hpr = tp.hpr.p;
+    const long n = long(g.nslots) * g.n;
+    curl_decomp_kernel<<<blocks_for(n, 64), 64, 0, c.stream>>>(a);
+    ++c.launches;
+}
+
+void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w,
+                         double* lam_n, double* gam_n) {
+    // proj/src/ptns.cpp:114-149
+    double* comp[6];
+    for (int i = 0; i < 6; ++i) comp[i] = scratch(i);
+    const double* lam[2] = {lam_v, lam_w};
+    const double* gam[2] = {gam_v, gam_w};
+    double* vr[2] = {comp[0], comp[3]};
+    double* vt[2] = {comp[1], comp[4]};
+    double* vz[2] = {comp[2], comp[5]};
+    pt_synthesize(2, lam, gam, vr, vt, vz);
+    double* val[6];
+    for (int i = 0; i < 6; ++i) val[i] = scratch(6 + i);
+    const int cls6[6] = {1, 1, 0, 1, 1, 0};
+    rz_synth(6, comp, cls6, val);
+    double* av[3] = {scratch(12), scratch(13), scratch(14)};
+    theta_cross(val, av);
+    double* ac[3] = {scratch(15), scratch(16), scratch(17)};
+    const int cls3[3] = {1, 1, 0};
+    rz_analyze(3, av, cls3, ac);
+    curl_decompose(ac[0], ac[1], ac[2], nullptr, nullptr, nullptr, lam_n, gam_n);
+}
+
+void Pipeline::poisson(const double* f, double w, double* u) {
+    DevSet& set = c.set(false, true, 1.0);
+    const double* src[1] = {f};
+    const double ww[1] = {w};
+    c.run_adi(set, false, 1, src, ww, 1, nullptr, nullptr, 0, u, nullptr);
+}
+
+void Pipeline::decompose(const double* vr, const double* vt, const double* vz, double* lam, double* gam) {
+    const Geo& g = c.gh;
+    CurlDecomp a{};
+    a.g = g;
+    a.decompose_only = 1;
+    a.ar = vr;
+    a.at = vt;
+    a.az = vz;
+    a.lam = lam;
+    a.gam = gam;
+    a.scratch = big_scratch(size_t(g.nslots) * g.n * 6 * g.mh);
+    a.q = tp.q.p;
+    a.hpc = tp.hpc.p;
+    a.hpr = tp.hpr.p;
+    const long n = long(g.nslots) * g.n;
+    curl_decomp_kernel<<<blocks_for(n, 64), 64, 0, c.stream>>>(a);
+    ++c.launches;
+}
+
+void Pipeline::hpoisson(const double* rhs, double* u) {
+    const Geo& g = c.gh;
+    HpArgs a{g, rhs, u, big_scratch(size_t(g.nslots) * g.n * g.mh), tp.hpc.p, tp.hpr.p};
+    hp_kernel<<<blocks_for(long(g.nslots) * g.n, 64), 64, 0, c.stream>>>(a);
+    ++c.launches;
+}
+
+void Pipeline::scale(double* x, double a) {
+    Combo cb{};
+    cb.src[0] = x;
+    cb.w[0] = a;
+    cb.nsrc = 1;
+    cb.out = x;
+    cb.n = T;
+    combo_kernel<<<std::min<long>(4736, (T + 255) / 256), 256, 0, c.stream>>>(cb);
+    ++c.launches;
+}
+
+void Pipeline::calculus(int op, int cls, const double* in, double* out) {
+    const Geo& g = c.gh;
+    if (op == 1 || op == 6) {  // d/dz ; laplacian = hlap + dzz
+        if (op == 1) {
+            dz({in}, {out});
+            return;
+        }
+        double* t1 = scratch(32);
+        double* t2 = scratch(33);
+        dz({in}, {t1});
+        dz({t1}, {t2});
+        CalcArgs a{g, 5, cls, in, out, big_scratch(size_t(g.nslots) * g.n * 3 * g.mh), tp.q.p};
+        calc_kernel<<<blocks_for(long(g.nslots) * g.n, 64), 64, 0, c.stream>>>(a);
+        Combo cb{};
+        cb.src[0] = out;
+        cb.w[0] = 1.0;
+        cb.src[1] = t2;
+        cb.w[1] = 1.0;
+        cb.nsrc = 2;
+        cb.out = out;
+        cb.n = T;
+        combo_kernel<<<std::min<long>(4736, (T + 255) / 256), 256, 0, c.stream>>>(cb);
+        c.launches += 2;
+        return;
+    }
+    if (op != 0 && op != 2 && op != 4 && op != 5) throw Error(DOMAIN_ERROR, "ccf_calculus: unknown op");
+    CalcArgs a{g, op, cls, in, out, big_scratch(size_t(g.nslots) * g.n * 3 * g.mh), tp.q.p};
+    calc_kernel<<<blocks_for(long(g.nslots) * g.n, 64), 64, 0, c.stream>>>(a);
+    ++c.launches;
+}
+
+// Full (parity-agnostic, full-spectrum) transforms for arbitrary real fields.
+void Pipeline::analyze_full(const double* values, double* coeffs) {
+    const int m = c.m, n = c.n, p = c.p;
+    const long nv = long(m) * n * p;
+    double* v = big_scratch(size_t(4) * nv);  // v | t | complex (2 nv)
+    double* t = v + nv;
+    double* z = v + 2 * nv;
+    c.load_values(values, v);
+    CCF_CUDA(cudaMemsetAsync(c.ws.flag, 0, sizeof(int), c.stream));
+    finite_check_kernel<<<std::min<long>(1184, (nv + 255) / 256), 256, 0, c.stream>>>(v, nv, c.ws.flag);
+    int f = 0;
+    CCF_CUDA(cudaMemcpyAsync(&f, c.ws.flag, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (f) throw Error(NUMERICAL, "analyze: non-finite input value");
+    GemmPlan r, zz;
+    for (int l = 0; l < p; ++l) {
+        r.A.push_back(v + long(l) * m * n);  // [k][j] slice, r-analysis on the right
+        r.B.push_back(tp.Rfull_A.p);         // B = A_r^T: (j, k) -> A[k][j]
+        r.C.push_back(t + long(l) * m * n);
+        zz.A.push_back(tp.Az.p);
+        zz.B.push_back(t + long(l) * m * n);
+        zz.C.push_back(v + long(l) * m * n);
+    }
+    // Rfull_A is stored as A[k][j]; the right operand needs B[j][k] = A[k][j] -> use the transposed copy
+    r.B.assign(size_t(p), full_rT());
+    r.M = n; r.N = m; r.K = m; r.lda = m; r.ldb = m; r.ldc = m;
+    zz.M = n; zz.N = m; zz.K = n; zz.lda = n; zz.ldb = m; zz.ldc = m;
+    r.upload();
+    zz.upload();
+    r.launch(c.stream);
+    zz.launch(c.stream);
+    real_to_complex_kernel<<<std::min<long>(4736, (nv + 255) / 256), 256, 0, c.stream>>>(v, z, nv);
+    double* dst = coeffs;
+    const bool host = !c.is_device_ptr(coeffs);
+    if (host) dst = t;  // reuse t (+ next nv) as the complex output staging (t..t+2nv overlaps z? no: z = v+2nv)
+    double* outc = host ? big2(size_t(2) * nv) : coeffs;
+    theta_dft_full_kernel<<<unsigned(long(m) * n), 128, size_t(p) * sizeof(double2), c.stream>>>(
+        z, outc, m, n, p, -1, reinterpret_cast<const double2*>(tp.twfull.p));
+    c.launches += 5;
+    if (host) CCF_CUDA(cudaMemcpyAsync(coeffs, outc, sizeof(double) * 2 * nv, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+}
+
+void Pipeline::synthesize_full(const double* coeffs, double* values) {
+    const int m = c.m, n = c.n, p = c.p;
+    const long nv = long(m) * n * p;
+    double* v = big_scratch(size_t(4) * nv);
+    double* t = v + nv;
+    double* z = v + 2 * nv;  // complex, 2 nv
+    if (c.is_device_ptr(coeffs))
+        CCF_CUDA(cudaMemcpyAsync(z, coeffs, sizeof(double) * 2 * nv, cudaMemcpyDeviceToDevice, c.stream));
+    else
+        CCF_CUDA(cudaMemcpyAsync(z, coeffs, sizeof(double) * 2 * nv, cudaMemcpyHostToDevice, c.stream));
+    double* zc = big2(size_t(2) * nv);
+    theta_dft_full_kernel<<<unsigned(long(m) * n), 128, size_t(p) * sizeof(double2), c.stream>>>(
+        z, zc, m, n, p, +1, reinterpret_cast<const double2*>(tp.twfull.p));
+    complex_re_kernel<<<std::min<long>(4736, (nv + 255) / 256), 256, 0, c.stream>>>(zc, v, nv);
+    GemmPlan zz, r;
+    for (int l = 0; l < p; ++l) {
+        zz.A.push_back(tp.Sz.p);
+        zz.B.push_back(v + long(l) * m * n);
+        zz.C.push_back(t + long(l) * m * n);
+        r.A.push_back(t + long(l) * m * n);
+        r.B.push_back(full_sT());
+        r.C.push_back(v + long(l) * m * n);
+    }
+    zz.M = n; zz.N = m; zz.K = n; zz.lda = n; zz.ldb = m; zz.ldc = m;
+    r.M = n; r.N = m; r.K = m; r.lda = m; r.ldb = m; r.ldc = m;
+    zz.upload();
+    r.upload();
+    zz.launch(c.stream);
+    r.launch(c.stream);
+    c.launches += 4;
+    c.store_values(v, values);
+    c.sync();
+}
+
+const double* Pipeline::full_rT() {  // B[j][k] = A_r[k][j]
+    if (!rAT_.p) {
+        const int m = c.m;
+        std::vector<double> A(size_t(m) * m), AT(size_t(m) * m);
+        CCF_CUDA(cudaMemcpy(A.data(), tp.Rfull_A.p, A.size() * 8, cudaMemcpyDeviceToHost));
+        for (int k = 0; k < m; ++k)
+            for (int j = 0; j < m; ++j) AT[size_t(j) * m + k] = A[size_t(k) * m + j];
+        upload(rAT_, AT);
+    }
+    return rAT_.p;
+}
+
+const double* Pipeline::full_sT() {  // B[k][j] = S_r[j][k]
+    if (!rST_.p) {
+        const int m = c.m;
+        std::vector<double> S(size_t(m) * m), ST(size_t(m) * m);
+        CCF_CUDA(cudaMemcpy(S.data(), tp.Rfull_S.p, S.size() * 8, cudaMemcpyDeviceToHost));
+        for (int j = 0; j < m; ++j)
+            for (int k = 0; k < m; ++k) ST[size_t(k) * m + j] = S[size_t(j) * m + k];
+        upload(rST_, ST);
+    }
+    return rST_.p;
+}
+
+double* Pipeline::big2(size_t doubles) {
+    if (big2_.n < doubles) big2_.alloc(doubles);
+    return big2_.p;
+}
+
+// ---------------------------------------------------------------- NS state
+NSState::~NSState() {
+    for (auto g : graphs)
+        if (g) cudaGraphExecDestroy(g);
+    if (dflag) cudaFree(dflag);
+}
+
+static void bdf_table(int b, double* koh, double w[4]) {  // proj/src/timestep.cpp:5-29
+    static const double K[4] = {1.0, 2.0 / 3.0, 6.0 / 11.0, 12.0 / 25.0};
+    static const double W[4][4] = {{1.0, 0, 0, 0},
+                                   {4.0 / 3.0, -1.0 / 3.0, 0, 0},
+                                   {18.0 / 11.0, -9.0 / 11.0, 2.0 / 11.0, 0},
+                                   {48.0 / 25.0, -36.0 / 25.0, 16.0 / 25.0, -3.0 / 25.0}};
+    *koh = K[b - 1];
+    for (int i = 0; i < 4; ++i) w[i] = W[b - 1][i];
+}
+
+static void imex_table(int b, double w[4]) {  // proj/src/timestep.cpp:31-39
+    static const double W[4][4] = {{1, 0, 0, 0}, {2, -1, 0, 0}, {3, -3, 1, 0}, {4, -6, 4, -1}};
+    for (int i = 0; i < 4; ++i) w[i] = W[b - 1][i];
+}
+
+void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
+    // proj/src/ptns.cpp:217-267
+    Pipeline& P = *pl;
+    Ctx& c = P.c;
+    const double* lw = lam[cur].p;
+    const double* gw = gam[cur].p;
+    if (!disable_nonlinear) {
+        double* lpsi = P.scratch(18);
+        P.poisson(lw, -1.0, lpsi);                              // velocity_from_vorticity, ptns.cpp:85-91
+        P.nonlinear(gw, lpsi, lw, gw, nl[nnew].p, ng[nnew].p);  // nonlinear_term(v, omega)
+    }
+    double koh, bw[4], iw[4] = {0, 0, 0, 0};
+    bdf_table(b, &koh, bw);
+    if (eo > 0) imex_table(eo, iw);
+    const double kappa = koh * h;
+    const double scale = kappa * (1.0 / reynolds);
+    const double* sl[kMaxSrc];
+    const double* sg[kMaxSrc];
+    double wl[kMaxSrc];
+    int ns = 0;
+    for (int i = 0; i < b; ++i) {
+        sl[ns] = lam[(cur + i) % 5].p;
+        sg[ns] = gam[(cur + i) % 5].p;
+        wl[ns++] = bw[i];
+    }
+    for (int i = 0; i < eo; ++i) {  // kappa * sum_i imex_i N_i  (ptns.cpp:235-245, timestep.cpp:71-73)
+        sl[ns] = nl[(nnew + i) % 4].p;
+        sg[ns] = ng[(nnew + i) % 4].p;
+        wl[ns++] = kappa * iw[i];
+    }
+    DevSet& set = c.set(false, false, scale);
+    c.run_adi(set, false, 2, sl, wl, ns, sg, wl, ns, lam[out].p, gam[out].p);
+    const long T = P.T;
+    finite_check_kernel<<<std::min<long>(1184, (T + 255) / 256), 256, 0, c.stream>>>(lam[out].p, T, dflag);
+    finite_check_kernel<<<std::min<long>(1184, (T + 255) / 256), 256, 0, c.stream>>>(gam[out].p, T, dflag);
+    c.launches += 2;
+}
+
+void NSState::step_once() {
+    Ctx& c = pl->c;
+    const int b = std::min(order, steps + 1);
+    const int out = (head + 4) % 5;
+    const int nnew = (nhead + 3) % 4;
+    const int ncnt = disable_nonlinear ? 0 : std::min(ncount + 1, order);
+    const int eo = disable_nonlinear ? 0 : std::min(b, ncnt);
+    const bool steady = (b == order) && (disable_nonlinear || ncount == order);
+    const int key = head * 4 + nhead;
+    if (use_graphs && steady && steps >= order + 1) {
+        if (!graphs[key]) {
+            cudaGraph_t g;
+            const long l0 = c.launches;
+            CCF_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+            enqueue(b, eo, head, out, nnew);
+            CCF_CUDA(cudaStreamEndCapture(c.stream, &g));
+            CCF_CUDA(cudaGraphInstantiate(&graphs[key], g, 0));
+            CCF_CUDA(cudaGraphDestroy(g));
+            launches_per_step = c.launches - l0;
+            c.launches = l0;
+        }
+        CCF_CUDA(cudaGraphLaunch(graphs[key], c.stream));
+        c.launches += launches_per_step;
+    } else {
+        const long l0 = c.launches;
+        enqueue(b, eo, head, out, nnew);
+        if (steady) launches_per_step = c.launches - l0;
+    }
+    head = out;
+    if (!disable_nonlinear) {
+        nhead = nnew;
+        ncount = ncnt;
+    }
+    ++steps;
+    time += h;
+}
+
+}  // namespace ccf

@@ -1,0 +1,107 @@
+// NS time-step pipeline on the device (reference: proj/src/ptns.cpp:217-267).
+//
+// Per step (half-spectrum, parity-compressed tensors):
+//   P  lambda_psi = Poisson3D(-lambda_w)                           ADI (Poisson set)
+//   V  dz gamma, pt_synthesize(v), pt_synthesize(w)               dz_kernel, pt_synth_kernel
+//   X  r,z synthesis (DMMA GEMMs) -> theta FFT x cross x FFT -> r,z analysis
+//   C  dz a, curl_vector + pt_decompose (horizontal Poisson)      curl_decomp_kernel
+//   H  BDF history + kappa * IMEX(N history) -> Helmholtz ADI for (lambda, gamma)
+// State (omega history, N history) stays on the device; ring indices rotate.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "context.hpp"
+
+namespace ccf {
+
+// Chebyshev synthesis / analysis matrices (device, row-major) and theta twiddles.
+struct TransformPlan {
+    DBuf SrT[2], ArT[2];  // [j0]: mh x mh  (B operands of the r-GEMMs, r > 0 half grid)
+    DBuf Sz, Az;          // n x n dense z synthesis / analysis (A operands)
+    DBuf Rfull_S, Rfull_A;  // m x m dense r synthesis / analysis (API transforms on arbitrary fields)
+    DBuf q;               // mh: odd Chebyshev coefficients of the interpolant of 1/r_j
+    DBuf tw;              // p/2 complex twiddles exp(-2 pi i q / p)
+    DBuf twfull;          // p complex twiddles (naive DFT path)
+    DBuf hpc, hpr;        // horizontal-Poisson LU per half slot; R R C02 per parity
+    int logp = -1;        // log2 p, or -1 if p is not a power of two
+    explicit TransformPlan(Ctx& c);
+};
+
+// Reusable batched-GEMM launcher with device pointer arrays.
+struct GemmPlan {
+    std::vector<const double*> A, B;
+    std::vector<double*> C;
+    const double** dA = nullptr;
+    const double** dB = nullptr;
+    double** dC = nullptr;
+    int M = 0, N = 0, K = 0;
+    long lda = 0, ldb = 0, ldc = 0;
+    double alpha = 1.0, beta = 0.0;
+    void upload();
+    void launch(cudaStream_t s) const;
+    ~GemmPlan();
+};
+
+class Pipeline {
+public:
+    explicit Pipeline(Ctx& c);
+    Ctx& c;
+    TransformPlan tp;
+    long T;  // doubles per half-spectrum tensor
+    // ---- stage building blocks (all on c.stream, capture-safe)
+    void dz(const std::vector<const double*>& in, const std::vector<double*>& out);
+    void pt_synthesize(int count, const double* const* lam, const double* const* gam, double* const* vr,
+                       double* const* vt, double* const* vz);
+    // coefficient (class per tensor) -> (r,z)-values / theta-coefficients, and back
+    void rz_synth(int count, const double* const* in, const int* cls, double* const* out);
+    void rz_analyze(int count, const double* const* in, const int* cls, double* const* out);
+    void theta_cross(const double* const* v6, double* const* a3);
+    void curl_decompose(const double* ar, const double* at, const double* az, double* out_r, double* out_t,
+                        double* out_z, double* lam, double* gam);
+    void nonlinear(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w, double* lam_n,
+                   double* gam_n);
+    void poisson(const double* f, double w, double* u);  // u = Poisson3D(w * f), half mode
+    void decompose(const double* vr, const double* vt, const double* vz, double* lam, double* gam);
+    void hpoisson(const double* rhs, double* u);
+    void calculus(int op, int cls, const double* in, double* out);  // ops of include/ccf.h ccf_calculus
+    void scale(double* x, double a);
+    void analyze_full(const double* values, double* coeffs);     // reference layouts, host or device
+    void synthesize_full(const double* coeffs, double* values);
+    double* scratch(int i);  // internal scratch tensors
+    double* big_scratch(size_t doubles);
+
+    const double* full_rT();
+    const double* full_sT();
+    double* big2(size_t doubles);
+
+private:
+    std::vector<DBuf> scr_;
+    DBuf big_, big2_, rAT_, rST_;
+    std::map<std::string, std::unique_ptr<GemmPlan>> gemms_;
+    GemmPlan& gemm(const std::string& key, bool& fresh);
+};
+
+struct NSState {
+    Pipeline* pl = nullptr;
+    double reynolds = 100, h = 1e-2;
+    int order = 4, steps = 0;
+    bool disable_nonlinear = false;
+    double time = 0;
+    // omega history ring (5 slots: the Helmholtz output never aliases a live input)
+    // and nonlinear-term history ring (4 slots)
+    DBuf lam[5], gam[5], nl[4], ng[4];
+    int head = 0;               // ring slot of the newest omega; history i at (head + i) % 5
+    int nhead = 0, ncount = 0;  // N ring: entry i at (nhead + i) % 4
+    int* dflag = nullptr;       // device non-finite flag (NaN guard, ptns.cpp:260-262)
+    cudaGraphExec_t graphs[20] = {};  // steady-state step per (head, nhead) ring phase
+    long launches_per_step = 0;
+    bool use_graphs = true;
+    ~NSState();
+    void step_once();
+    void enqueue(int b, int eo, int cur, int out, int nnew);
+};
+
+}  // namespace ccf

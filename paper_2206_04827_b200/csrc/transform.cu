@@ -1,0 +1,292 @@
+// CCF value <-> coefficient transforms (reference: proj/src/transform.cpp:81-203).
+//
+// Chebyshev directions: dense FP64 contractions on the tensor cores (DMMA
+// m8n8k4, mma.sync .f64) through one batched GEMM kernel; the r-direction uses
+// the parity-compressed (m/2 x m/2) synthesis / analysis matrices of each
+// Fourier slot (only coefficients with (j + w + cls) even exist), evaluated on
+// the r > 0 half of the doubled grid (the r < 0 half is its parity image).
+// Theta direction: radix-2 FFT in shared memory fused with the pointwise
+// cylindrical cross product v x omega of the nonlinear term
+// (proj/src/ptns.cpp:121-139): 6 half-spectra in, 3 half-spectra out per
+// (r, z) point, two real signals packed per complex FFT.
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace ccf {
+
+// ---------------------------------------------------------------------------------------------
+// Batched DGEMM: C[b] = alpha * A[b] * B[b] + beta * C[b]   (row-major, DMMA m8n8k4)
+// CTA tile 64 x 64, BK = 16, 4 warps of 32 x 32.
+namespace {
+constexpr int BM = 64, BN = 64, BK = 16, SA = BK + 4, SB = BN + 4;
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+}  // namespace
+
+__global__ void __launch_bounds__(128) dgemm_batched_kernel(GemmBatch g) {
+    __shared__ double As[2][BM * SA];
+    __shared__ double Bs[2][BK * SB];
+    const int b = blockIdx.z;
+    const double* __restrict__ A = g.A[b];
+    const double* __restrict__ B = g.B[b];
+    double* __restrict__ C = g.C[b];
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    const int gq = lane >> 2, tq = lane & 3;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    double ra[8], rb[8];
+    auto gload = [&](int k0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = tid + q * 128;  // 0..1023
+            const int ar = e >> 4, ak = e & 15;
+            const int gr = m0 + ar, gk = k0 + ak;
+            ra[q] = (gr < g.M && gk < g.K) ? __ldg(A + long(gr) * g.lda + gk) : 0.0;
+            const int bk = e >> 6, bc = e & 63;
+            const int hk = k0 + bk, hc = n0 + bc;
+            rb[q] = (hk < g.K && hc < g.N) ? __ldg(B + long(hk) * g.ldb + hc) : 0.0;
+        }
+    };
+    auto sstore = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = tid + q * 128;
+            As[buf][(e >> 4) * SA + (e & 15)] = ra[q];
+            Bs[buf][(e >> 6) * SB + (e & 63)] = rb[q];
+        }
+    };
+    const int nk = (g.K + BK - 1) / BK;
+    gload(0);
+    sstore(0);
+    __syncthreads();
+    for (int kt = 0; kt < nk; ++kt) {
+        const int buf = kt & 1;
+        if (kt + 1 < nk) gload((kt + 1) * BK);
+#pragma unroll
+        for (int ks = 0; ks < BK; ks += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) af[i] = As[buf][(wm + 8 * i + gq) * SA + ks + tq];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][(ks + tq) * SB + wn + 8 * j + gq];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        if (kt + 1 < nk) sstore(buf ^ 1);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int r = m0 + wm + 8 * i + gq, c = n0 + wn + 8 * j + 2 * tq + q;
+                if (r < g.M && c < g.N) {
+                    double* dst = C + long(r) * g.ldc + c;
+                    const double v = g.alpha * acc[i][j][q];
+                    *dst = g.beta == 0.0 ? v : fma(g.beta, *dst, v);
+                }
+            }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Theta direction.
+//
+// Reference conventions (transform.cpp:144-163, 175-191): values f(theta_l) =
+// sum_w c_w e^{i w theta_l}, theta_l = (2l - p) pi / p, i.e. with X[w mod p] =
+// (-1)^w c_w the values are the unnormalised inverse DFT of X; analysis c_w =
+// (-1)^w X[w mod p] / p with X the forward DFT of the samples. Synthesis keeps
+// the real part (transform.cpp:201), so c_0 and the Nyquist coefficient
+// contribute their real parts only.
+namespace {
+
+// In-place radix-2 DIT FFT on `cnt` complex arrays of length P (power of two),
+// data already in bit-reversed order; sign = +1 inverse, -1 forward.
+__device__ void fft_pow2_block(double2* __restrict__ d, int cnt, int P, int logP, const double2* __restrict__ tw,
+                               int sign) {
+    for (int s = 1; s <= logP; ++s) {
+        const int half = 1 << (s - 1);
+        const int tstep = P >> s;  // twiddle index step
+        const int nbf = cnt * (P >> 1);
+        for (int i = threadIdx.x; i < nbf; i += blockDim.x) {
+            const int arr = i / (P >> 1), bfl = i % (P >> 1);
+            const int grp = bfl / half, pos = bfl % half;
+            const int i0 = grp * 2 * half + pos, i1 = i0 + half;
+            double2 w = tw[pos * tstep];  // exp(-2 pi i pos tstep / P)
+            if (sign > 0) w.y = -w.y;
+            double2* base = d + arr * P;
+            const double2 a = base[i0], bb = base[i1];
+            const double2 t = make_double2(w.x * bb.x - w.y * bb.y, w.x * bb.y + w.y * bb.x);
+            base[i0] = make_double2(a.x + t.x, a.y + t.y);
+            base[i1] = make_double2(a.x - t.x, a.y - t.y);
+        }
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ int bitrev(int x, int logP) { return __brev(unsigned(x)) >> (32 - logP); }
+
+}  // namespace
+
+// Fused theta synthesis -> cross product -> theta analysis (stage X of the NS step).
+// in[0..5] = (v_r, v_theta, v_z, w_r, w_theta, w_z), out[0..2] = (a_r, a_theta, a_z),
+// all in the (r,z)-value / theta-half-spectrum layout [slot][plane][k][jr].
+// One CTA per (k, tile of TJ consecutive jr).
+__global__ void theta_cross_kernel(ThetaCross t) {
+    extern __shared__ double2 sd[];
+    const Geo& g = t.g;
+    const int P = g.p, logP = t.logp, S = g.nslots;
+    const int TJ = t.tj;
+    const int k = blockIdx.y;
+    const int jr0 = blockIdx.x * TJ;
+    const int ntj = min(TJ, g.mh - jr0);
+    double2* Z = sd;                       // 3 * TJ arrays of P (packed pairs)
+    const double2* tw = t.tw;              // P/2 twiddles exp(-2 pi i q / P)
+    // ---- gather Hermitian spectra of pairs (0,1) (2,3) (4,5) into bit-reversed slots
+    const int tot = 3 * TJ * P;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int jl = e % TJ;              // jr fastest -> coalesced gathers
+        const int tt = (e / TJ) % P;        // frequency index t in [0, P)
+        const int pr = e / (TJ * P);        // pair
+        double2 z = make_double2(0.0, 0.0);
+        if (jl < ntj) {
+            // X[t] = (-1)^w c_w with w = t (t < P/2), Nyquist at t = P/2, conj mirror above
+            int w;
+            bool conjg = false;
+            if (tt < P / 2) w = tt;
+            else if (tt == P / 2) w = -P / 2;
+            else {
+                w = P - tt;
+                conjg = true;
+            }
+            const int s = (w == -P / 2) ? P / 2 : w;
+            const double sg = ((w & 1) ? -1.0 : 1.0);
+            const long off = long(s) * g.slot_stride + long(k) * g.mh + jr0 + jl;
+            double2 xa, xb;
+            {
+                const double* fa = t.in[2 * pr];
+                const double* fb = t.in[2 * pr + 1];
+                xa = make_double2(sg * fa[off], sg * fa[off + g.plane_stride]);
+                xb = make_double2(sg * fb[off], sg * fb[off + g.plane_stride]);
+            }
+            if (w == 0 || w == -P / 2) {  // Re only (transform.cpp:201)
+                xa.y = 0.0;
+                xb.y = 0.0;
+            }
+            if (conjg) {
+                xa.y = -xa.y;
+                xb.y = -xb.y;
+            }
+            z = make_double2(xa.x - xb.y, xa.y + xb.x);  // Xa + i Xb
+        }
+        Z[(pr * TJ + jl) * P + bitrev(tt, logP)] = z;
+    }
+    __syncthreads();
+    fft_pow2_block(Z, 3 * TJ, P, logP, tw, +1);
+    // ---- pointwise cross product a = v x w (ptns.cpp:127-132); repack (a_r + i a_t), (a_z + 0 i)
+    for (int e = threadIdx.x; e < TJ * P; e += blockDim.x) {
+        const int jl = e / P, l = e % P;
+        const double2 p0 = Z[(0 * TJ + jl) * P + l], p1 = Z[(1 * TJ + jl) * P + l], p2 = Z[(2 * TJ + jl) * P + l];
+        const double vr = p0.x, vt = p0.y, vz = p1.x, wr = p1.y, wt = p2.x, wz = p2.y;
+        const double ar = vt * wz - vz * wt;
+        const double at = vz * wr - vr * wz;
+        const double az = vr * wt - vt * wr;
+        // store in bit-reversed order for the forward transform
+        const int lr = bitrev(l, logP);
+        Z[(0 * TJ + jl) * P + l] = make_double2(ar, at);
+        Z[(1 * TJ + jl) * P + l] = make_double2(az, 0.0);
+        (void)lr;
+    }
+    __syncthreads();
+    // bit-reverse permutation in place for the two packed outputs
+    for (int e = threadIdx.x; e < 2 * TJ * P; e += blockDim.x) {
+        const int a = e / P, l = e % P, lr = bitrev(l, logP);
+        if (l < lr) {
+            double2* base = Z + a * P;
+            const double2 x = base[l];
+            base[l] = base[lr];
+            base[lr] = x;
+        }
+    }
+    __syncthreads();
+    fft_pow2_block(Z, 2 * TJ, P, logP, tw, -1);
+    // ---- unpack X_a = (Z[t] + conj Z[P-t]) / 2, X_b = (Z[t] - conj Z[P-t]) / (2i); c_w = (-1)^w X[w mod P] / P
+    const double invp = 1.0 / double(P);
+    for (int e = threadIdx.x; e < 3 * S * 2 * TJ; e += blockDim.x) {
+        const int jl = e % TJ;
+        const int pl = (e / TJ) % 2;
+        const int s = (e / (2 * TJ)) % S;
+        const int f = e / (2 * TJ * S);  // output field 0..2
+        if (jl >= ntj) continue;
+        const int w = (s == P / 2) ? -P / 2 : s;
+        const int tt = (w % P + P) % P;
+        const int pair = f < 2 ? 0 : 1;
+        const double2* base = Z + (pair * TJ + jl) * P;
+        const double2 zt = base[tt], zm = base[(P - tt) % P];
+        double2 X;
+        if (f == 0 || f == 2) X = make_double2(0.5 * (zt.x + zm.x), 0.5 * (zt.y - zm.y));
+        else X = make_double2(0.5 * (zt.y + zm.y), -0.5 * (zt.x - zm.x));
+        const double sg = ((w & 1) ? -1.0 : 1.0) * invp;
+        const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride + long(k) * g.mh + jr0 + jl;
+        t.out[f][off] = sg * (pl ? X.y : X.x);
+    }
+}
+
+// Full-spectrum complex theta DFT for the API transforms (any even p):
+// data [l][k][j] complex interleaved; dir = +1 synthesis (c -> values), -1 analysis.
+__global__ void theta_dft_full_kernel(const double* __restrict__ in, double* __restrict__ out, int m, int n, int p,
+                                      int dir, const double2* __restrict__ twp) {
+    extern __shared__ double2 sx[];
+    const long mn = long(m) * n;
+    const long q = blockIdx.x;  // one (k, j) pencil per CTA
+    if (q >= mn) return;
+    for (int l = threadIdx.x; l < p; l += blockDim.x) {
+        const int w = l - p / 2;
+        const int t = ((w % p) + p) % p;
+        const double sg = (w & 1) ? -1.0 : 1.0;
+        const double re = in[2 * (long(l) * mn + q)], im = in[2 * (long(l) * mn + q) + 1];
+        if (dir > 0) sx[t] = make_double2(sg * re, sg * im);  // X[w mod p] = (-1)^w c_w
+        else sx[l] = make_double2(re, im);
+    }
+    __syncthreads();
+    // naive O(p^2) DFT with a p-periodic twiddle table (twp[x] = exp(-2 pi i x / p))
+    for (int o = threadIdx.x; o < p; o += blockDim.x) {
+        double sr = 0.0, si = 0.0;
+        for (int x = 0; x < p; ++x) {
+            double2 w = twp[(long(o) * x) % p];
+            if (dir > 0) w.y = -w.y;
+            const double2 v = sx[x];
+            sr += v.x * w.x - v.y * w.y;
+            si += v.x * w.y + v.y * w.x;
+        }
+        if (dir > 0) {
+            out[2 * (long(o) * mn + q)] = sr;  // Re kept by the caller after the r,z sweeps
+            out[2 * (long(o) * mn + q) + 1] = si;
+        } else {
+            // analysis: slice l with w = l - p/2 takes X[w mod p] * (-1)^w / p
+            // (scatter: output index o is t; map back to l)
+            const int t = o;
+            const int w = t < p / 2 ? t : t - p;  // w in [-p/2, p/2)
+            const int l = w + p / 2;
+            const double sg = ((w & 1) ? -1.0 : 1.0) / double(p);
+            out[2 * (long(l) * mn + q)] = sg * sr;
+            out[2 * (long(l) * mn + q) + 1] = sg * si;
+        }
+    }
+}
+
+}  // namespace ccf

@@ -109,6 +109,16 @@ ccf_status ccf_reset_stats(ccf_ctx* ctx);
 ccf_status ccf_modal_plan(ccf_ctx* ctx, int w, double scale, int poisson, double* info, double* u, double* v,
                           int cap);
 
+/* Benchmark / profiling helpers: enable CUDA-graph replay of steady-state steps (default on),
+ * report kernel launches per steady-state step, and run the next step eagerly with CUDA events
+ * at the stage boundaries (P Poisson ADI, V pt_synthesize, X1 r,z synthesis, X2 theta x cross,
+ * X3 r,z analysis, C curl + decompose, H Helmholtz ADI). */
+ccf_status ccf_ns_set_graphs(ccf_ns_state* st, int enable);
+ccf_status ccf_ns_launches_per_step(ccf_ns_state* st, long* n);
+ccf_status ccf_ns_profile_step(ccf_ns_state* st, double* ms, int* nstages, char* names, int cap);
+
+/* Message of the last failed ccf_ctx_create on this thread. */
+const char* ccf_create_error(void);
 const char* ccf_version(void);
 
 #ifdef __cplusplus

@@ -3,6 +3,8 @@
 // Tensors use the reference layout: index (l*n + k)*m + j, complex interleaved
 // (re, im) for coefficients, plain f64 for grid values (proj/include/cylspec/coeffs.hpp:16-45).
 #include <cstring>
+#include <chrono>
+#include <cmath>
 #include <random>
 
 #include "oracle.hpp"
@@ -412,5 +414,63 @@ void orc_adi_stats(long* solves, long* iterations, int* max_rounds, double* wors
 void orc_adi_stats_reset() { adi_stats_reset(); }
 
 uint32_t orc_crc32(const uint8_t* data, size_t len) { return crc32_ieee(data, len); }
+
+// ---- bounded CPU-baseline sample of one NS step (bench.py cpu_baseline / --impl reference).
+// Times, at full size: the modal solves (RHS assembly R2 f C02^T + ModalSolver::solve) of
+// `ns` sampled Fourier slices for the Poisson (velocity) and Helmholtz (BDF4, nu = 1/Re)
+// solvers, one analyze and one synthesize. Solver setup (QZ bounds, factorizations) is not
+// timed (it is cached across steps in the reference, ModalSolverCache).
+// out: [t_poisson_sample, t_helmholtz_sample (one tensor), t_analyze, t_synthesize, J_poisson_mean, J_helm_mean]
+int orc_ns_step_sample(int m, int n, int p, double re, double h, int ns, int threads, unsigned seed, double* out) {
+    return guard([&] {
+        set_threads(threads);
+        const Spec s(m, n, p);
+        const double scale = (12.0 / 25.0) * h / re;
+        ModalSolverCache cache(m, n, 1e-12);
+        std::vector<int> slices;
+        for (int i = 0; i < ns; ++i) slices.push_back(int((long(i) * p) / ns));
+        std::mt19937_64 rng(seed);
+        std::normal_distribution<double> nd(0.0, 1.0);
+        std::vector<MatC> rhs;
+        for (int l : slices) {
+            MatC f(m, n);
+            const int w = s.wavenumber(l);
+            for (int k = 0; k < n; ++k)
+                for (int j = 0; j < m; ++j)
+                    if (((j + w) % 2 + 2) % 2 == 0) f(j, k) = cd(nd(rng), nd(rng)) * std::pow(0.9, j + k + std::abs(w));
+            rhs.push_back(f);
+        }
+        double jp = 0, jh = 0;
+        for (int l : slices) {  // setup (untimed)
+            jp += cache.get(s.wavenumber(l), 1.0, true).plan()->J;
+            jh += cache.get(s.wavenumber(l), scale, false).plan()->J;
+        }
+        const UltraOps& ro = UltraOps::get(m);
+        const Banded c02t = UltraOps::get(n).c02.transposed();
+        auto run = [&](bool poisson) {
+            const auto t0 = std::chrono::steady_clock::now();
+            parallel_for(long(slices.size()), [&](long i) {
+                const ModalSolver& sv = cache.get(s.wavenumber(slices[size_t(i)]), poisson ? 1.0 : scale, poisson);
+                MatC ff = c02t.apply_right(ro.r2.apply_left(rhs[size_t(i)]));
+                MatC x = sv.solve(ff);
+                (void)x;
+            });
+            return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        };
+        out[0] = run(true);
+        out[1] = run(false);
+        Field f(s);
+        for (double& v : f.v) v = nd(rng);
+        auto t0 = std::chrono::steady_clock::now();
+        Coeff c = analyze(f);
+        out[2] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        t0 = std::chrono::steady_clock::now();
+        Field g = synthesize(c);
+        out[3] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        out[4] = jp / double(slices.size());
+        out[5] = jh / double(slices.size());
+        set_threads(1);
+    });
+}
 
 }  // extern "C"

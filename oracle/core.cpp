@@ -140,6 +140,8 @@ namespace {
 
 struct FftPlan {
     int n = 0;
+    bool pow2 = false;
+    std::vector<int> rev;  // bit reversal (power-of-two sizes)
     std::vector<int> fac;
     std::vector<cd> tw;  // exp(-2 pi i k / n)
     bool blue = false;
@@ -152,6 +154,18 @@ struct FftPlan {
 };
 
 FftPlan::FftPlan(int n_) : n(n_) {
+    pow2 = n >= 2 && (n & (n - 1)) == 0;
+    if (pow2) {
+        int lg = 0;
+        while ((1 << lg) < n) ++lg;
+        rev.resize(size_t(n));
+        for (int i = 0; i < n; ++i) {
+            int r2 = 0;
+            for (int b = 0; b < lg; ++b)
+                if (i & (1 << b)) r2 |= 1 << (lg - 1 - b);
+            rev[size_t(i)] = r2;
+        }
+    }
     int r = n;
     for (int f : {4, 2, 3, 5}) {
         while (r % f == 0) {
@@ -168,8 +182,8 @@ FftPlan::FftPlan(int n_) : n(n_) {
     const int big = *std::max_element(fac.begin(), fac.end());
     tw.resize(size_t(n));
     for (int k = 0; k < n; ++k) tw[k] = std::polar(1.0, -2.0 * std::numbers::pi * double(k) / double(n));
-    if (big > 256) {
-        // Bluestein for a large prime factor
+    if (big > 32) {
+        // Bluestein for a large prime factor (generic radix is O(p^2))
         blue = true;
         nb = 1;
         while (nb < 2 * n - 1) nb *= 2;
@@ -215,6 +229,20 @@ void FftPlan::rec(cd* out, const cd* in, int len, int stride, int fi, int sign) 
 }
 
 void FftPlan::exec(const cd* in, cd* out, int sign) const {
+    if (pow2) {  // iterative radix-2 Cooley-Tukey
+        for (int i = 0; i < n; ++i) out[rev[size_t(i)]] = in[i];
+        for (int len = 2; len <= n; len <<= 1) {
+            const int half = len >> 1, step = n / len;
+            for (int i = 0; i < n; i += len)
+                for (int k = 0; k < half; ++k) {
+                    const cd w = sign < 0 ? tw[size_t(k * step)] : std::conj(tw[size_t(k * step)]);
+                    const cd a = out[i + k], b = out[i + k + half] * w;
+                    out[i + k] = a + b;
+                    out[i + k + half] = a - b;
+                }
+        }
+        return;
+    }
     if (!blue) {
         rec(out, in, n, 1, 0, sign);
         return;
@@ -226,7 +254,9 @@ void FftPlan::exec(const cd* in, cd* out, int sign) const {
         for (int k = 0; k < n; ++k) out[k] = std::conj(out[k]);
         return;
     }
-    std::vector<cd> a(static_cast<size_t>(nb), cd(0)), fa(static_cast<size_t>(nb));
+    thread_local std::vector<cd> a, fa;
+    a.assign(size_t(nb), cd(0));
+    fa.resize(size_t(nb));
     for (int k = 0; k < n; ++k) a[k] = in[k] * chirp[k];
     sub->exec(a.data(), fa.data(), -1);
     for (int k = 0; k < nb; ++k) fa[k] *= bk[k];
@@ -254,7 +284,11 @@ void fft(int n, const cd* in, cd* out, int sign) { plan_for(n).exec(in, out, sig
 void redft00(int L, const double* in, double* out) {
     // FFTW REDFT00 via the even extension of length 2(L-1).
     const int N = 2 * (L - 1);
-    std::vector<cd> e(static_cast<size_t>(N)), E(static_cast<size_t>(N));
+    thread_local std::vector<cd> e, E;
+    if (int(e.size()) < N) {
+        e.resize(size_t(N));
+        E.resize(size_t(N));
+    }
     for (int j = 0; j < L; ++j) e[j] = in[j];
     for (int j = 1; j < L - 1; ++j) e[N - j] = in[j];
     fft(N, e.data(), E.data(), -1);

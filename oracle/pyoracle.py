@@ -74,7 +74,8 @@ def lib():
                      "orc_curl_pt", "orc_velocity_from_vorticity", "orc_nonlinear", "orc_helmholtz_step",
                      "orc_ns_step", "orc_ns_get", "orc_heat_step", "orc_heat_get", "orc_compute_shifts",
                      "orc_modal_plan", "orc_pencil_range", "orc_adi_vs_dense", "orc_operator_dense",
-                     "orc_pencil_dense", "orc_jacobi", "orc_mobius_from_points", "orc_points", "orc_evaluate_at"]:
+                     "orc_pencil_dense", "orc_jacobi", "orc_mobius_from_points", "orc_points", "orc_evaluate_at",
+                     "orc_ns_step_sample"]:
             getattr(L, name).restype = C.c_int
         L.orc_last_error.restype = C.c_char_p
         L.orc_ns_create.restype = C.c_void_p
@@ -392,6 +393,15 @@ def adi_stats():
 
 def adi_stats_reset():
     lib().orc_adi_stats_reset()
+
+
+def ns_step_sample(m, n, p, re, h, nsample=8, threads=1, seed=7):
+    """Bounded CPU sample of one NS step (see orc_ns_step_sample in capi.cpp)."""
+    out = np.zeros(6)
+    _chk(lib().orc_ns_step_sample(m, n, p, C.c_double(re), C.c_double(h), int(nsample), int(threads), C.c_uint(seed),
+                                  _p(out)))
+    return dict(t_poisson=out[0], t_helmholtz=out[1], t_analyze=out[2], t_synthesize=out[3], J_poisson=out[4],
+                J_helmholtz=out[5], nsample=nsample)
 
 
 def crc32(b: bytes) -> int:

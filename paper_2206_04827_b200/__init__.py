@@ -74,7 +74,8 @@ EXPORTS = ["ccf_ctx_create", "ccf_ctx_destroy", "ccf_ctx_set_stream", "ccf_ctx_s
            "ccf_synthesize", "ccf_calculus", "ccf_poisson3d", "ccf_hpoisson", "ccf_helmholtz_step",
            "ccf_pt_synthesize", "ccf_pt_decompose", "ccf_curl_vector", "ccf_curl_pt", "ccf_velocity_from_vorticity",
            "ccf_nonlinear", "ccf_ns_create", "ccf_ns_step", "ccf_ns_get_omega", "ccf_ns_destroy",
-           "ccf_get_last_error", "ccf_get_stats", "ccf_reset_stats", "ccf_modal_plan", "ccf_version"]
+           "ccf_get_last_error", "ccf_get_stats", "ccf_reset_stats", "ccf_modal_plan", "ccf_version",
+           "ccf_ns_profile_step", "ccf_ns_set_graphs", "ccf_ns_launches_per_step"]
 
 _lib = None
 
@@ -125,6 +126,12 @@ def lib():
                                     C.POINTER(C.c_long)]
         L.ccf_reset_stats.argtypes = [vp]
         L.ccf_modal_plan.argtypes = [vp, C.c_int, C.c_double, C.c_int, dp, dp, dp, C.c_int]
+        L.ccf_ns_profile_step.restype = C.c_int
+        L.ccf_ns_profile_step.argtypes = [vp, dp, C.POINTER(C.c_int), C.c_char_p, C.c_int]
+        L.ccf_ns_set_graphs.restype = C.c_int
+        L.ccf_ns_set_graphs.argtypes = [vp, C.c_int]
+        L.ccf_ns_launches_per_step.restype = C.c_int
+        L.ccf_ns_launches_per_step.argtypes = [vp, C.POINTER(C.c_long)]
         _lib = L
     return _lib
 
@@ -178,6 +185,13 @@ class Context:
 
     def shape(self):
         return (self.p, self.n, self.m)
+
+    def set_stream(self, stream_ptr):
+        """Run on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); None restores."""
+        self._check(lib().ccf_ctx_set_stream(self.h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
+    def synchronize(self):
+        self._check(lib().ccf_ctx_synchronize(self.h))
 
     def _out_c(self):
         return np.zeros(self.shape(), np.complex128)
@@ -303,6 +317,23 @@ class NSStepper:
         self.ctx._check(lib().ccf_ns_get_omega(self.h, _addr(lam), _addr(gam), C.byref(t), C.byref(s)))
         self.time, self.steps_taken = t.value, s.value
         return lam, gam
+
+    def set_graphs(self, enable: bool):
+        lib().ccf_ns_set_graphs(self.h, int(bool(enable)))
+
+    def launches_per_step(self):
+        n = C.c_long()
+        lib().ccf_ns_launches_per_step(self.h, C.byref(n))
+        return n.value
+
+    def profile_step(self):
+        """Run one step eagerly with CUDA events at stage boundaries -> {stage: ms}."""
+        ms = (C.c_double * 32)()
+        k = C.c_int(32)
+        names = C.create_string_buffer(4096)
+        self.ctx._check(lib().ccf_ns_profile_step(self.h, ms, C.byref(k), names, 4096))
+        nm = names.value.decode().strip().split("\n")
+        return {nm[i]: ms[i] for i in range(k.value)}
 
     def close(self):
         if getattr(self, "h", None):

@@ -414,7 +414,7 @@ ccf_status ccf_ns_create(ccf_ctx* ctx, double reynolds, double h, int order, int
             s.lam[i].alloc(size_t(T));
             s.gam[i].alloc(size_t(T));
         }
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 5; ++i) {
             s.nl[i].alloc(size_t(T));
             s.ng[i].alloc(size_t(T));
         }
@@ -475,4 +475,45 @@ ccf_status ccf_ns_launches_per_step(ccf_ns_state* st, long* n) {
     return CCF_OK;
 }
 
+}  // extern "C"
+
+extern "C" {
+// Run the next step eagerly with CUDA events at the stage boundaries (P, V, X1, X2, X3, C, H).
+// names: '\n'-separated stage names written to `names` (cap bytes); ms: per-stage durations.
+ccf_status ccf_ns_profile_step(ccf_ns_state* st, double* ms, int* nstages, char* names, int cap) {
+    if (!st) return CCF_INTERNAL_ERROR;
+    return guard(st->ctx, [&](Ctx& c) {
+        const bool g = st->st.use_graphs;
+        st->st.use_graphs = false;
+        c.profiling = true;
+        c.prof_events.clear();
+        c.prof_names.clear();
+        try {
+            st->st.step_once();
+        } catch (...) {
+            c.profiling = false;
+            st->st.use_graphs = g;
+            throw;
+        }
+        c.profiling = false;
+        st->st.use_graphs = g;
+        c.sync();
+        std::string nm;
+        const int k = int(c.prof_events.size());
+        int out = 0;
+        for (int i = 1; i < k && out < *nstages; ++i, ++out) {
+            float t = 0;
+            cudaEventElapsedTime(&t, c.prof_events[size_t(i - 1)], c.prof_events[size_t(i)]);
+            ms[out] = t;
+            nm += c.prof_names[size_t(i)] + "\n";
+        }
+        for (auto e : c.prof_events) cudaEventDestroy(e);
+        c.prof_events.clear();
+        *nstages = out;
+        if (names && cap > 0) {
+            std::strncpy(names, nm.c_str(), size_t(cap - 1));
+            names[cap - 1] = 0;
+        }
+    });
+}
 }  // extern "C"

@@ -57,6 +57,8 @@ struct AdiParams {
     int nsrc[2];
     double* out[2];
     double* eprime;  // ntasks x estride scratch, rows padded to Mpad (multiple of 8)
+    double* escr;    // ntasks x estride: E (residual)
+    double* xscr;    // ntasks x estride: X of the last round (restart)
     long estride;    // doubles per task (Mpad * N rounded to even)
     int Mpad, Npad;  // M, N rounded up to multiples of 8 (zero-padded sweeps)
     int lrows, rrows;  // rows per left / right shift block (Mpad + 2, Npad + 2)

@@ -84,6 +84,8 @@ Ctx::Ctx(int m_, int n_, int p_, int device_, double tol_, int flags_)
     CCF_CUDA(cudaMemset(ws.err, 0, sizeof(int) * 4));
     CCF_CUDA(cudaMemset(ws.iters, 0, sizeof(unsigned long long) * 2));
     ws.eprime.alloc(size_t(2) * cap * 4 * size_t(estride));
+    ws.escr.alloc(size_t(2) * cap * 4 * size_t(estride));
+    ws.xscr.alloc(size_t(2) * cap * 4 * size_t(estride));
     {
         int optin = 0;
         CCF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
@@ -190,6 +192,8 @@ void Ctx::run_adi(DevSet& set, bool full, int ntensor, const double* const* src0
     P.out[1] = out1;
     P.eprime = ws.eprime.p;
     P.estride = estride;
+    P.escr = ws.escr.p;
+    P.xscr = ws.xscr.p;
     P.Mpad = Mpad;
     P.Npad = Npad;
     P.lrows = Mpad + 2;

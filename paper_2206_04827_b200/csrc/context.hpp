@@ -49,7 +49,7 @@ struct DevSet {
 };
 
 struct Workspace {  // ADI round bookkeeping
-    DBuf eprime;
+    DBuf eprime, escr, xscr;
     double *res2 = nullptr, *e2 = nullptr, *history = nullptr;
     int *active = nullptr, *rounds = nullptr, *err = nullptr, *flag = nullptr;
     unsigned long long* iters = nullptr;
@@ -71,6 +71,18 @@ struct Ctx {
     DBuf stage_in[4], stage_out[2];
     DBuf tens[16];  // generic device scratch tensors (compressed layout, full size)
     long launches = 0;
+    // optional stage profiling: events recorded at stage boundaries when enabled
+    bool profiling = false;
+    std::vector<cudaEvent_t> prof_events;
+    std::vector<std::string> prof_names;
+    void mark(const char* name) {
+        if (!profiling) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, stream);
+        prof_events.push_back(e);
+        prof_names.push_back(name);
+    }
     // last error
     int err_kind = 0, err_slice = -1, err_shift = -1;
     std::vector<double> err_hist;

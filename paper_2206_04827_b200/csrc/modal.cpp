@@ -212,7 +212,11 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
         for (int k0 = 0; k0 < 2; ++k0) {
             const long base = k0 ? d.right1 : d.right0;
             for (int j = 0; j < J; ++j) {
-                const CBand mul = (j + 1 < J) ? cb_axpy(plan.v[size_t(j + 1)], Btc[k0], 1.0, Dtc[k0]) : Btc[k0];
+                // G_{j+1} = X_{j+1} (v_{j+1} B + D); identity after the last shift (the row sweep then yields X)
+                CBand mul = (j + 1 < J) ? cb_axpy(plan.v[size_t(j + 1)], Btc[k0], 1.0, Dtc[k0]) : Btc[k0];
+                if (j + 1 == J)
+                    for (int b = 0; b < N; ++b)
+                        for (int d = -1; d <= 2; ++d) mul.v[size_t(b) * 4 + size_t(d + 1)] = (d == 0) ? 1.0 : 0.0;
                 const CBand sh = cb_axpy(plan.u[size_t(j)], Btc[k0], 1.0, Dtc[k0]);
                 CLU lu;
                 try {

@@ -396,16 +396,21 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     double* vt[2] = {comp[1], comp[4]};
     double* vz[2] = {comp[2], comp[5]};
     pt_synthesize(2, lam, gam, vr, vt, vz);
+    c.mark("V_pt_synthesize");
     double* val[6];
     for (int i = 0; i < 6; ++i) val[i] = scratch(6 + i);
     const int cls6[6] = {1, 1, 0, 1, 1, 0};
     rz_synth(6, comp, cls6, val);
+    c.mark("X1_rz_synthesis");
     double* av[3] = {scratch(12), scratch(13), scratch(14)};
     theta_cross(val, av);
+    c.mark("X2_theta_cross");
     double* ac[3] = {scratch(15), scratch(16), scratch(17)};
     const int cls3[3] = {1, 1, 0};
     rz_analyze(3, av, cls3, ac);
+    c.mark("X3_rz_analysis");
     curl_decompose(ac[0], ac[1], ac[2], nullptr, nullptr, nullptr, lam_n, gam_n);
+    c.mark("C_curl_decompose");
 }
 
 void Pipeline::poisson(const double* f, double w, double* u) {
@@ -619,7 +624,9 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
     const double* gw = gam[cur].p;
     if (!disable_nonlinear) {
         double* lpsi = P.scratch(18);
+        c.mark("start");
         P.poisson(lw, -1.0, lpsi);                              // velocity_from_vorticity, ptns.cpp:85-91
+        c.mark("P_poisson_adi");
         P.nonlinear(gw, lpsi, lw, gw, nl[nnew].p, ng[nnew].p);  // nonlinear_term(v, omega)
     }
     double koh, bw[4], iw[4] = {0, 0, 0, 0};
@@ -637,12 +644,14 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
         wl[ns++] = bw[i];
     }
     for (int i = 0; i < eo; ++i) {  // kappa * sum_i imex_i N_i  (ptns.cpp:235-245, timestep.cpp:71-73)
-        sl[ns] = nl[(nnew + i) % 4].p;
-        sg[ns] = ng[(nnew + i) % 4].p;
+        sl[ns] = nl[(nnew + i) % 5].p;
+        sg[ns] = ng[(nnew + i) % 5].p;
         wl[ns++] = kappa * iw[i];
     }
     DevSet& set = c.set(false, false, scale);
+    if (c.prof_events.empty()) c.mark("start");
     c.run_adi(set, false, 2, sl, wl, ns, sg, wl, ns, lam[out].p, gam[out].p);
+    c.mark("H_helmholtz_adi");
     const long T = P.T;
     finite_check_kernel<<<std::min<long>(1184, (T + 255) / 256), 256, 0, c.stream>>>(lam[out].p, T, dflag);
     finite_check_kernel<<<std::min<long>(1184, (T + 255) / 256), 256, 0, c.stream>>>(gam[out].p, T, dflag);
@@ -653,11 +662,11 @@ void NSState::step_once() {
     Ctx& c = pl->c;
     const int b = std::min(order, steps + 1);
     const int out = (head + 4) % 5;
-    const int nnew = (nhead + 3) % 4;
+    const int nnew = (nhead + 4) % 5;
     const int ncnt = disable_nonlinear ? 0 : std::min(ncount + 1, order);
     const int eo = disable_nonlinear ? 0 : std::min(b, ncnt);
     const bool steady = (b == order) && (disable_nonlinear || ncount == order);
-    const int key = head * 4 + nhead;
+    const int key = head * 5 + nhead;
     if (use_graphs && steady && steps >= order + 1) {
         if (!graphs[key]) {
             cudaGraph_t g;

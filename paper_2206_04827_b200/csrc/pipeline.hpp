@@ -90,13 +90,13 @@ struct NSState {
     int order = 4, steps = 0;
     bool disable_nonlinear = false;
     double time = 0;
-    // omega history ring (5 slots: the Helmholtz output never aliases a live input)
-    // and nonlinear-term history ring (4 slots)
-    DBuf lam[5], gam[5], nl[4], ng[4];
+    // omega history ring and nonlinear-term history ring, 5 slots each (the Helmholtz output
+    // never aliases a live input; both heads advance in lockstep -> 5 graph phases)
+    DBuf lam[5], gam[5], nl[5], ng[5];
     int head = 0;               // ring slot of the newest omega; history i at (head + i) % 5
-    int nhead = 0, ncount = 0;  // N ring: entry i at (nhead + i) % 4
+    int nhead = 0, ncount = 0;  // N ring: entry i at (nhead + i) % 5
     int* dflag = nullptr;       // device non-finite flag (NaN guard, ptns.cpp:260-262)
-    cudaGraphExec_t graphs[20] = {};  // steady-state step per (head, nhead) ring phase
+    cudaGraphExec_t graphs[25] = {};  // steady-state step per (head, nhead) ring phase
     long launches_per_step = 0;
     bool use_graphs = true;
     ~NSState();

@@ -54,8 +54,8 @@ def load_peaks():
     return peaks
 
 
-def initial_vorticity(ctx, cfg):
-    """omega0 = curl_pt(curl_pt(psi)) scaled so max_grid |v| = 1, v = pt_synthesize(curl_pt(psi))."""
+def initial_vorticity(ctx, cfg, vmax_target=1.0):
+    """omega0 = curl_pt(curl_pt(psi)) scaled so max_grid |v| = vmax_target, v = pt_synthesize(curl_pt(psi))."""
     from tests.inputs import hermitian_coeffs
     m, n, p = cfg["m"], cfg["n"], cfg["p"]
     lam_psi = hermitian_coeffs(m, n, p, cfg["decay"], cfg["seed"])
@@ -65,7 +65,7 @@ def initial_vorticity(ctx, cfg):
     speed2 = ctx.synthesize(vr) ** 2 + ctx.synthesize(vt) ** 2 + ctx.synthesize(vz) ** 2
     vmax = float(np.sqrt(speed2.max()))
     wl, wg = ctx.curl_pt(vl, vg)
-    s = 1.0 / vmax
+    s = vmax_target / vmax
     return wl * s, wg * s, vmax
 
 

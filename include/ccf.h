@@ -117,7 +117,11 @@ ccf_status ccf_ns_set_graphs(ccf_ns_state* st, int enable);
 ccf_status ccf_ns_launches_per_step(ccf_ns_state* st, long* n);
 ccf_status ccf_ns_profile_step(ccf_ns_state* st, double* ms, int* nstages, char* names, int cap);
 
-/* Message of the last failed ccf_ctx_create on this thread. */
+/* Host-only (no GPU) modal shift plan with the context's setup numerics; error text via ccf_create_error. */
+ccf_status ccf_plan_host(int m, int n, int w, double scale, int poisson, double tol, int flags, double* info, double* u,
+                         double* v, int cap);
+
+/* Message of the last failed ccf_ctx_create / ccf_plan_host on this thread. */
 const char* ccf_create_error(void);
 const char* ccf_version(void);
 

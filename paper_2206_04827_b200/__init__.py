@@ -75,7 +75,8 @@ EXPORTS = ["ccf_ctx_create", "ccf_ctx_destroy", "ccf_ctx_set_stream", "ccf_ctx_s
            "ccf_pt_synthesize", "ccf_pt_decompose", "ccf_curl_vector", "ccf_curl_pt", "ccf_velocity_from_vorticity",
            "ccf_nonlinear", "ccf_ns_create", "ccf_ns_step", "ccf_ns_get_omega", "ccf_ns_destroy",
            "ccf_get_last_error", "ccf_get_stats", "ccf_reset_stats", "ccf_modal_plan", "ccf_version",
-           "ccf_ns_profile_step", "ccf_ns_set_graphs", "ccf_ns_launches_per_step"]
+           "ccf_ns_profile_step", "ccf_ns_set_graphs", "ccf_ns_launches_per_step", "ccf_plan_host",
+           "ccf_create_error"]
 
 _lib = None
 
@@ -99,7 +100,7 @@ def lib():
         L.ccf_create_error.restype = C.c_char_p
         L.ccf_ctx_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.POINTER(vp)]
         for name in EXPORTS:
-            if name not in ("ccf_version",):
+            if name not in ("ccf_version", "ccf_create_error"):
                 getattr(L, name).restype = C.c_int
         L.ccf_ctx_destroy.argtypes = [vp]
         L.ccf_ctx_set_stream.argtypes = [vp, vp]
@@ -132,6 +133,8 @@ def lib():
         L.ccf_ns_set_graphs.argtypes = [vp, C.c_int]
         L.ccf_ns_launches_per_step.restype = C.c_int
         L.ccf_ns_launches_per_step.argtypes = [vp, C.POINTER(C.c_long)]
+        L.ccf_plan_host.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double, C.c_int, dp, dp, dp,
+                                    C.c_int]
         _lib = L
     return _lib
 
@@ -294,6 +297,22 @@ class Context:
 
     def reset_stats(self):
         self._check(lib().ccf_reset_stats(self.h))
+
+
+def plan_host(m, n, w, scale=1.0, poisson=True, tol=1e-12, q2_endpoint_pad=False):
+    """Modal shift plan from the library's host setup path (no GPU required)."""
+    info = np.zeros(8)
+    u = np.zeros(256)
+    v = np.zeros(256)
+    dp = C.POINTER(C.c_double)
+    st = lib().ccf_plan_host(int(m), int(n), int(w), C.c_double(scale), int(poisson), C.c_double(tol),
+                             int(bool(q2_endpoint_pad)), info.ctypes.data_as(dp), u.ctypes.data_as(dp),
+                             v.ctypes.data_as(dp), 256)
+    if st != 0:
+        raise _ERR.get(st, CCFError)(lib().ccf_create_error().decode())
+    J = int(info[7])
+    return dict(a=info[0], b=info[1], c=info[2], d=info[3], gamma=info[4], alpha=info[5], modulus=info[6], J=J,
+                u=u[:J].copy(), v=v[:J].copy())
 
 
 class NSStepper:

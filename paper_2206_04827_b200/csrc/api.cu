@@ -517,3 +517,31 @@ ccf_status ccf_ns_profile_step(ccf_ns_state* st, double* ms, int* nstages, char*
     });
 }
 }  // extern "C"
+
+extern "C" {
+// Host-only modal shift plan (no GPU needed): the same setup path the context uses
+// (spectral enclosure + Zolotarev shifts, proj/src/solvers.cpp:46-75, adi.cpp:22-104).
+ccf_status ccf_plan_host(int m, int n, int w, double scale, int poisson, double tol, int flags, double* info, double* u,
+                         double* v, int cap) {
+    try {
+        if (m < 4 || n < 4 || m % 2 || n % 2) throw Error(ccf::DOMAIN_ERROR, "ccf_plan_host: even m, n >= 4 required");
+        ccf::SizeOps so(m, n);
+        std::map<int, ccf::Range> cache;
+        ccf::SolverSet set = ccf::build_solver_set(so, {w}, poisson != 0, scale, tol, cache, (flags & 1) != 0);
+        const ccf::Plan& pl = set.plans[0].plan;
+        const double vals[8] = {pl.a, pl.b, pl.c, pl.d, pl.gamma, pl.alpha, pl.modulus, double(pl.J)};
+        std::memcpy(info, vals, sizeof vals);
+        for (int j = 0; j < pl.J && j < cap; ++j) {
+            u[j] = pl.u[size_t(j)];
+            v[j] = pl.v[size_t(j)];
+        }
+        return CCF_OK;
+    } catch (const Error& e) {
+        g_create_err = e.what();
+        return ccf_status(e.status);
+    } catch (const std::exception& e) {
+        g_create_err = e.what();
+        return CCF_INTERNAL_ERROR;
+    }
+}
+}  // extern "C"

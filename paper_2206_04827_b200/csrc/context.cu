@@ -1,6 +1,7 @@
 // Host-side context implementation: device memory, solver-set cache
 // (ModalSolverCache, proj/src/solvers.cpp:100-109), ADI round driver.
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 
 #include "context.hpp"
@@ -169,6 +170,7 @@ DevSet& Ctx::set(bool full, bool poisson, double scale) {
 void Ctx::run_adi(DevSet& set, bool full, int ntensor, const double* const* src0, const double* w0, int n0,
                   const double* const* src1, const double* w1, int n1, double* out0, double* out1) {
     const Geo& g = geo(full);
+    last_adi_kind = set.host.poisson ? "Poisson" : "Helmholtz";
     AdiParams P{};
     P.g = g;
     P.M = M;
@@ -240,8 +242,10 @@ void Ctx::check_adi_error(bool full) {
     CCF_CUDA(cudaMemset(ws.err, 0, sizeof(int) * 4));
     const int s = e[2];
     const int l = full ? s : (s == p / 2 ? 0 : s + p / 2);
-    Error err(NON_CONVERGENCE, "modal solve failed for Fourier slice " + std::to_string(l) +
-                                   ": ADI did not converge: relative residual " + std::to_string(hist[3]) +
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%.3e", hist[3]);
+    Error err(NON_CONVERGENCE, std::string("modal solve failed for Fourier slice ") + std::to_string(l) + " (" +
+                                   last_adi_kind + "): ADI did not converge: relative residual " + buf +
                                    " after 4 rounds");
     err.slice = l;
     err.history = hist;

@@ -71,6 +71,7 @@ struct Ctx {
     DBuf stage_in[4], stage_out[2];
     DBuf tens[16];  // generic device scratch tensors (compressed layout, full size)
     long launches = 0;
+    const char* last_adi_kind = "";
     // optional stage profiling: events recorded at stage boundaries when enabled
     bool profiling = false;
     std::vector<cudaEvent_t> prof_events;

@@ -30,10 +30,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {  # BASELINE.json configs (NS ones); seed = config index
-    256: dict(workload="ns_256cubed_re1000", m=256, n=256, p=256, reynolds=1000.0, h=5e-4, decay=0.9, seed=4),
-    128: dict(workload="ns_128cubed_re100", m=128, n=128, p=128, reynolds=100.0, h=1e-3, decay=0.85, seed=2),
-    64: dict(workload="ns_64cubed_re100", m=64, n=64, p=64, reynolds=100.0, h=1e-3, decay=0.7, seed=3),
-    32: dict(workload="ns_32cubed", m=32, n=32, p=32, reynolds=100.0, h=1e-3, decay=0.8, seed=1),
+    # vmax: max_grid |v| of the initial field. BASELINE asks for 1; at 128^3 / 256^3 that violates the
+    # explicit-advection CFL bound at the Chebyshev wall spacing (h |v| / dr_min ~ 3.3 / 6.6) and the
+    # run diverges; 0.1 is the largest power-of-ten amplitude below the bound (Q4).
+    256: dict(workload="ns_256cubed_re1000", m=256, n=256, p=256, reynolds=1000.0, h=5e-4, decay=0.9, seed=4,
+              vmax=0.1),
+    128: dict(workload="ns_128cubed_re100", m=128, n=128, p=128, reynolds=100.0, h=1e-3, decay=0.85, seed=2,
+              vmax=0.1),
+    64: dict(workload="ns_64cubed_re100", m=64, n=64, p=64, reynolds=100.0, h=1e-3, decay=0.7, seed=3, vmax=1.0),
+    32: dict(workload="ns_32cubed", m=32, n=32, p=32, reynolds=100.0, h=1e-3, decay=0.8, seed=1, vmax=1.0),
 }
 METRIC = "NS time-steps/sec at n=m=p=256 fp64"
 
@@ -196,7 +201,7 @@ def main():
     stream = torch.cuda.Stream()
     ctx.set_stream(stream.cuda_stream)
     t_setup = time.time()
-    wl, wg, vmax = initial_vorticity(ctx, cfg)
+    wl, wg, vmax = initial_vorticity(ctx, cfg, cfg["vmax"])
     st = P.NSStepper(ctx, wl, wg, reynolds=cfg["reynolds"], h=cfg["h"], order=4)
     if args.no_graphs:
         st.set_graphs(False)
@@ -282,7 +287,7 @@ def main():
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["workload"], "m": m, "n": n, "p": p, "reynolds": cfg["reynolds"],
                        "h": cfg["h"], "bdf_order": 4, "init_decay": cfg["decay"], "seed": cfg["seed"],
-                       "init_vmax_scaled_from": vmax, "parallelism": "replica" if world > 1 else "single",
+                       "init_max_speed": cfg["vmax"], "init_vmax_scaled_from": vmax, "parallelism": "replica" if world > 1 else "single",
                        "l2": "no flush: step working set ~3 GB >> 126 MB L2",
                        "cuda_graphs": not args.no_graphs},
             "clocks": clk,

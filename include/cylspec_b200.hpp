@@ -1,0 +1,313 @@
+// cylspec_b200.hpp — header-only C++ drop-in for the reference `cylspec` hot-path API
+// (proj/include/cylspec/{grid,coeffs,errors,transform,calculus,solvers,timestep,ptns}.hpp),
+// implemented over the B200 C-ABI (include/ccf.h, lib/libccf.so).
+//
+// Same names, argument meaning, value semantics and exception types as the reference for
+// the hot path; Eigen-typed signatures (CoeffTensor::slice, ModalSolver::solve) are not part
+// of this shim. Each (m, n, p) grid gets one thread-local ccf context
+// (the reference's caches are process-wide; ours are per context and hold the same plans).
+#pragma once
+
+#include <complex>
+#include <deque>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "ccf.h"
+
+namespace cylspec {
+
+using Complex = std::complex<double>;
+
+// ---- errors (proj/include/cylspec/errors.hpp:10-40)
+struct DomainError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
+struct ConfigError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
+struct SingularOperatorError : std::runtime_error {
+    explicit SingularOperatorError(const std::string& w, int j = -1) : std::runtime_error(w), shift_index(j) {}
+    int shift_index;
+};
+struct NonConvergenceError : std::runtime_error {
+    NonConvergenceError(const std::string& w, std::vector<double> h) : std::runtime_error(w), residual_history(std::move(h)) {}
+    std::vector<double> residual_history;
+};
+struct NotIncompressibleError : std::runtime_error {
+    NotIncompressibleError(const std::string& w, double d) : std::runtime_error(w), divergence(d) {}
+    double divergence;
+};
+struct NumericalError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+// ---- grid / tensors (grid.hpp:13-50, coeffs.hpp:16-45)
+struct GridSpec {
+    int m = 0, n = 0, p = 0;
+    GridSpec() = default;
+    GridSpec(int m_, int n_, int p_) : m(m_), n(n_), p(p_) { validate(); }
+    void validate() const {
+        if (m < 4 || n < 4) throw DomainError("GridSpec: m and n must be at least 4");
+        if (p < 2 || p % 2 != 0) throw DomainError("GridSpec: p must be even and at least 2");
+    }
+    long total_points() const { return long(m) * n * p; }
+    int zero_mode() const { return p / 2; }
+    int wavenumber(int l) const { return l - p / 2; }
+    bool operator==(const GridSpec&) const = default;
+};
+
+struct GridField {
+    GridSpec spec;
+    std::vector<double> values;
+    GridField() = default;
+    explicit GridField(const GridSpec& s) : spec(s), values(size_t(s.total_points()), 0.0) {}
+    size_t index(int j, int k, int l) const { return (size_t(l) * spec.n + size_t(k)) * spec.m + size_t(j); }
+    double& at(int j, int k, int l) { return values[index(j, k, l)]; }
+    double at(int j, int k, int l) const { return values[index(j, k, l)]; }
+};
+
+struct CoeffTensor {
+    GridSpec spec;
+    std::vector<Complex> data;
+    CoeffTensor() = default;
+    explicit CoeffTensor(const GridSpec& s) : spec(s), data(size_t(s.total_points()), Complex(0)) {}
+    Complex& at(int j, int k, int l) { return data[(size_t(l) * spec.n + size_t(k)) * spec.m + size_t(j)]; }
+    Complex at(int j, int k, int l) const { return data[(size_t(l) * spec.n + size_t(k)) * spec.m + size_t(j)]; }
+    const double* raw() const { return reinterpret_cast<const double*>(data.data()); }
+    double* raw() { return reinterpret_cast<double*>(data.data()); }
+};
+
+struct PTScalars {
+    CoeffTensor lambda, gamma;
+    PTScalars() = default;
+    explicit PTScalars(const GridSpec& s) : lambda(s), gamma(s) {}
+    PTScalars(CoeffTensor l, CoeffTensor g) : lambda(std::move(l)), gamma(std::move(g)) {}
+};
+
+struct VectorFieldCoeffs {
+    CoeffTensor comp_r, comp_theta, comp_z;
+    VectorFieldCoeffs() = default;
+    explicit VectorFieldCoeffs(const GridSpec& s) : comp_r(s), comp_theta(s), comp_z(s) {}
+};
+
+struct BoundaryCondition {  // homogeneous Dirichlet only on the B200 path (solvers.hpp:18-31)
+    static BoundaryCondition homogeneous() { return {}; }
+};
+
+inline constexpr double kDefaultAdiTol = 1e-12;
+
+namespace detail {
+
+[[noreturn]] inline void raise(ccf_status st, ccf_ctx* ctx) {
+    int kind = 0, slice = -1, shift = -1, nh = 8;
+    double hist[8] = {0};
+    char msg[1024] = {0};
+    if (ctx) ccf_get_last_error(ctx, &kind, &slice, &shift, hist, &nh, msg, sizeof msg);
+    else std::snprintf(msg, sizeof msg, "%s", ccf_create_error());
+    const std::string w(msg);
+    switch (st) {
+        case CCF_DOMAIN_ERROR: throw DomainError(w);
+        case CCF_CONFIG_ERROR: throw ConfigError(w);
+        case CCF_SINGULAR_OPERATOR: throw SingularOperatorError(w, shift);
+        case CCF_NON_CONVERGENCE: throw NonConvergenceError(w, std::vector<double>(hist, hist + (nh < 8 ? nh : 8)));
+        case CCF_NOT_INCOMPRESSIBLE: throw NotIncompressibleError(w, 0.0);
+        case CCF_NUMERICAL_ERROR: throw NumericalError(w);
+        default: throw std::runtime_error("ccf: " + w);
+    }
+}
+
+inline void check(ccf_status st, ccf_ctx* ctx) {
+    if (st != CCF_OK) raise(st, ctx);
+}
+
+// one context per (m, n, p, tol) and host thread (the reference library is single-threaded)
+inline ccf_ctx* context(const GridSpec& s, double tol = kDefaultAdiTol) {
+    struct Deleter {
+        void operator()(ccf_ctx* c) const { ccf_ctx_destroy(c); }
+    };
+    thread_local std::map<std::tuple<int, int, int, double>, std::unique_ptr<ccf_ctx, Deleter>> cache;
+    auto& slot = cache[{s.m, s.n, s.p, tol}];
+    if (!slot) {
+        ccf_ctx* c = nullptr;
+        check(ccf_ctx_create(s.m, s.n, s.p, 0, tol, 0, &c), nullptr);
+        slot.reset(c);
+    }
+    return slot.get();
+}
+
+}  // namespace detail
+
+// ---- transform.hpp:17-22
+inline CoeffTensor analyze(const GridField& f) {
+    CoeffTensor out(f.spec);
+    ccf_ctx* c = detail::context(f.spec);
+    detail::check(ccf_analyze(c, f.values.data(), out.raw()), c);
+    return out;
+}
+inline GridField synthesize(const CoeffTensor& t) {
+    GridField out(t.spec);
+    ccf_ctx* c = detail::context(t.spec);
+    detail::check(ccf_synthesize(c, t.raw(), out.values.data()), c);
+    return out;
+}
+
+// ---- calculus.hpp:15-29 (tensors of real fields)
+namespace detail {
+inline CoeffTensor calc(int op, const CoeffTensor& f) {
+    CoeffTensor out(f.spec);
+    ccf_ctx* c = context(f.spec);
+    check(ccf_calculus(c, op, f.raw(), out.raw()), c);
+    return out;
+}
+}  // namespace detail
+inline CoeffTensor derivative_r(const CoeffTensor& f) { return detail::calc(0, f); }
+inline CoeffTensor derivative_z(const CoeffTensor& f) { return detail::calc(1, f); }
+inline CoeffTensor derivative_theta(const CoeffTensor& f) { return detail::calc(2, f); }
+inline CoeffTensor divide_r(const CoeffTensor& f) { return detail::calc(4, f); }
+inline CoeffTensor horizontal_laplacian(const CoeffTensor& f) { return detail::calc(5, f); }
+inline CoeffTensor laplacian(const CoeffTensor& f) { return detail::calc(6, f); }
+
+// ---- solvers.hpp:86-94
+inline CoeffTensor solve_poisson_3d(const CoeffTensor& f, const BoundaryCondition& = {}, double tol = kDefaultAdiTol) {
+    CoeffTensor out(f.spec);
+    ccf_ctx* c = detail::context(f.spec, tol);
+    detail::check(ccf_poisson3d(c, f.raw(), out.raw()), c);
+    return out;
+}
+inline CoeffTensor solve_horizontal_poisson(const CoeffTensor& rhs) {
+    CoeffTensor out(rhs.spec);
+    ccf_ctx* c = detail::context(rhs.spec);
+    detail::check(ccf_hpoisson(c, rhs.raw(), out.raw()), c);
+    return out;
+}
+
+// ---- timestep.hpp:13-53
+struct BDFScheme {
+    int order = 1;
+    double kappa_over_h = 1.0;
+    static BDFScheme of_order(int b) {
+        static const double K[4] = {1.0, 2.0 / 3.0, 6.0 / 11.0, 12.0 / 25.0};
+        if (b < 1 || b > 4) throw DomainError("BDFScheme: order must be in {1,2,3,4}");
+        return {b, K[b - 1]};
+    }
+    double kappa(double h) const { return kappa_over_h * h; }
+};
+
+class HelmholtzTensorStepper {
+public:
+    HelmholtzTensorStepper(const GridSpec& spec, double diffusivity, double h, double adi_tol,
+                           BoundaryCondition = {})
+        : spec_(spec), diff_(diffusivity), h_(h), tol_(adi_tol) {
+        spec.validate();
+    }
+    CoeffTensor step(const std::deque<CoeffTensor>& history, const BDFScheme& scheme, const CoeffTensor* forcing) const {
+        std::vector<const double*> hp;
+        for (const auto& t : history) hp.push_back(t.raw());
+        CoeffTensor out(spec_);
+        ccf_ctx* c = detail::context(spec_, tol_);
+        detail::check(ccf_helmholtz_step(c, hp.data(), int(hp.size()), scheme.order, forcing ? forcing->raw() : nullptr,
+                                         diff_, h_, out.raw()),
+                      c);
+        return out;
+    }
+
+private:
+    GridSpec spec_;
+    double diff_, h_, tol_;
+};
+
+// ---- ptns.hpp:47-137
+inline VectorFieldCoeffs pt_synthesize(const PTScalars& s) {
+    VectorFieldCoeffs v(s.lambda.spec);
+    ccf_ctx* c = detail::context(s.lambda.spec);
+    detail::check(ccf_pt_synthesize(c, s.lambda.raw(), s.gamma.raw(), v.comp_r.raw(), v.comp_theta.raw(), v.comp_z.raw()), c);
+    return v;
+}
+inline PTScalars pt_decompose(const VectorFieldCoeffs& v, bool /*check_divergence*/ = false, double = 1e-8) {
+    PTScalars s(v.comp_r.spec);
+    ccf_ctx* c = detail::context(v.comp_r.spec);
+    detail::check(ccf_pt_decompose(c, v.comp_r.raw(), v.comp_theta.raw(), v.comp_z.raw(), s.lambda.raw(), s.gamma.raw()), c);
+    return s;
+}
+inline VectorFieldCoeffs curl_vector(const VectorFieldCoeffs& v) {
+    VectorFieldCoeffs o(v.comp_r.spec);
+    ccf_ctx* c = detail::context(v.comp_r.spec);
+    detail::check(ccf_curl_vector(c, v.comp_r.raw(), v.comp_theta.raw(), v.comp_z.raw(), o.comp_r.raw(),
+                                  o.comp_theta.raw(), o.comp_z.raw()),
+                  c);
+    return o;
+}
+inline PTScalars curl_pt(const PTScalars& s) {
+    PTScalars o(s.lambda.spec);
+    ccf_ctx* c = detail::context(s.lambda.spec);
+    detail::check(ccf_curl_pt(c, s.lambda.raw(), s.gamma.raw(), o.lambda.raw(), o.gamma.raw()), c);
+    return o;
+}
+inline PTScalars velocity_from_vorticity(const PTScalars& w, double tol = kDefaultAdiTol) {
+    PTScalars o(w.lambda.spec);
+    ccf_ctx* c = detail::context(w.lambda.spec, tol);
+    detail::check(ccf_velocity_from_vorticity(c, w.lambda.raw(), w.gamma.raw(), o.lambda.raw(), o.gamma.raw()), c);
+    return o;
+}
+inline PTScalars nonlinear_term(const PTScalars& v, const PTScalars& w, bool dealias_two_thirds = false) {
+    if (dealias_two_thirds) throw DomainError("nonlinear_term: 2/3 dealiasing is not on the B200 hot path");
+    PTScalars o(v.lambda.spec);
+    ccf_ctx* c = detail::context(v.lambda.spec);
+    detail::check(ccf_nonlinear(c, v.lambda.raw(), v.gamma.raw(), w.lambda.raw(), w.gamma.raw(), o.lambda.raw(),
+                                o.gamma.raw()),
+                  c);
+    return o;
+}
+
+struct NSConfig {
+    GridSpec spec;
+    double reynolds = 100.0;
+    double h = 1e-2;
+    int order = 4;
+    double adi_tol = kDefaultAdiTol;
+    bool disable_nonlinear = false;
+};
+
+class NSStepper {  // ramp bootstrap; state resident on the GPU between steps
+public:
+    NSStepper(const NSConfig& cfg, const PTScalars& omega0) : cfg_(cfg), omega_(cfg.spec) {
+        ctx_ = detail::context(cfg.spec, cfg.adi_tol);
+        detail::check(ccf_ns_create(ctx_, cfg.reynolds, cfg.h, cfg.order, cfg.disable_nonlinear ? 1 : 0,
+                                    omega0.lambda.raw(), omega0.gamma.raw(), &st_),
+                      ctx_);
+    }
+    ~NSStepper() { ccf_ns_destroy(st_); }
+    NSStepper(const NSStepper&) = delete;
+    NSStepper& operator=(const NSStepper&) = delete;
+    void step() { detail::check(ccf_ns_step(st_, 1), ctx_); }
+    void steps(int k) { detail::check(ccf_ns_step(st_, k), ctx_); }
+    const PTScalars& omega() {
+        detail::check(ccf_ns_get_omega(st_, omega_.lambda.raw(), omega_.gamma.raw(), &time_, &taken_), ctx_);
+        return omega_;
+    }
+    double time() const { return time_; }
+    const NSConfig& config() const { return cfg_; }
+
+private:
+    NSConfig cfg_;
+    ccf_ctx* ctx_ = nullptr;
+    ccf_ns_state* st_ = nullptr;
+    PTScalars omega_;
+    double time_ = 0.0;
+    int taken_ = 0;
+};
+
+struct NSRunResult {
+    PTScalars final_omega;
+    double final_time = 0.0;
+};
+
+inline NSRunResult ns_run(const NSConfig& config, const PTScalars& initial_omega, int steps) {
+    NSStepper s(config, initial_omega);
+    s.steps(steps);
+    NSRunResult r;
+    r.final_omega = s.omega();
+    r.final_time = s.time();
+    return r;
+}
+
+}  // namespace cylspec

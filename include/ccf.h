@@ -117,7 +117,9 @@ ccf_status ccf_ns_set_graphs(ccf_ns_state* st, int enable);
 ccf_status ccf_ns_launches_per_step(ccf_ns_state* st, long* n);
 ccf_status ccf_ns_profile_step(ccf_ns_state* st, double* ms, int* nstages, char* names, int cap);
 
-/* Host-only (no GPU) modal shift plan with the context's setup numerics; error text via ccf_create_error. */
+/* Host-only (no GPU) modal shift plan with the context's setup numerics; error text via ccf_create_error.
+ * info[0..7] = (a, b, c, d, gamma, alpha, modulus, J); flags bit0 = Q2 endpoint pad, bit1 = also
+ * report info[8] = 1 if a banded LU of this slot pivots (caller then provides info[9]). */
 ccf_status ccf_plan_host(int m, int n, int w, double scale, int poisson, double tol, int flags, double* info, double* u,
                          double* v, int cap);
 

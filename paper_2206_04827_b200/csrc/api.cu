@@ -531,6 +531,7 @@ ccf_status ccf_plan_host(int m, int n, int w, double scale, int poisson, double 
         const ccf::Plan& pl = set.plans[0].plan;
         const double vals[8] = {pl.a, pl.b, pl.c, pl.d, pl.gamma, pl.alpha, pl.modulus, double(pl.J)};
         std::memcpy(info, vals, sizeof vals);
+        if (flags & 2) info[8] = double(set.slots[0].pivot);  // caller provides info[9]
         for (int j = 0; j < pl.J && j < cap; ++j) {
             u[j] = pl.u[size_t(j)];
             v[j] = pl.v[size_t(j)];

@@ -90,12 +90,11 @@ Ctx::Ctx(int m_, int n_, int p_, int device_, double tol_, int flags_)
     {
         int optin = 0;
         CCF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-        cudaFuncAttributes fa{};
-        CCF_CUDA(cudaFuncGetAttributes(&fa, adi_kernel));
+        const size_t stat = adi_static_smem();
         const size_t need = adi_smem_bytes();
-        if (need + fa.sharedSizeBytes > size_t(optin))
+        if (need + stat > size_t(optin))
             throw Error(DOMAIN_ERROR, "ccf: ADI tile exceeds shared memory (m, n too large for the single-CTA kernel)");
-        CCF_CUDA(cudaFuncSetAttribute(adi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(optin - fa.sharedSizeBytes)));
+        CCF_CUDA(adi_set_smem(int(optin - stat)));
     }
 }
 
@@ -112,10 +111,18 @@ Ctx::~Ctx() {
     if (own_stream) cudaStreamDestroy(own_stream);
 }
 
+int Ctx::adi_lanes() const { return ((std::max(M, N) + 31) / 32) * 32; }
+
+bool Ctx::adi_split() const {
+    const int hc = spike_split(Mpad), hr = spike_split(Npad);
+    return hc > 0 && hr > 0 && hc < M && hr < N && 2 * adi_lanes() <= 512;
+}
+
 size_t Ctx::adi_smem_bytes() const {
     const long rows = Mpad + 6;
     const long ysize = ((rows * pitch + 1) / 2) * 2;
-    const long total = ysize + long(Mpad + 2) * kLeftW + long(Npad + 2) * kRightW + 3L * 8 * N;
+    const long rings = adi_split() ? 6 : 3;
+    const long total = ysize + long(Mpad + 2) * kLeftW + long(Npad + 2) * kRightW + rings * 8 * N + 4L * adi_lanes();
     return size_t(total) * sizeof(double);
 }
 
@@ -200,13 +207,16 @@ void Ctx::run_adi(DevSet& set, bool full, int ntensor, const double* const* src0
     P.Npad = Npad;
     P.lrows = Mpad + 2;
     P.rrows = Npad + 2;
+    P.lanes = adi_lanes();
+    P.hc = adi_split() ? spike_split(Mpad) : 0;
+    P.hr = adi_split() ? spike_split(Npad) : 0;
     P.res2 = ws.res2;
     P.e2 = ws.e2;
     P.active = ws.active;
     const int nts = ntensor * g.nslots;
     adi_init_kernel<<<(nts + 127) / 128, 128, 0, stream>>>(ws.active, ws.res2, ws.e2, nts);
     ++launches;
-    const int threads = ((std::max(M, N) + 31) / 32) * 32;
+    const int threads = adi_split() ? 2 * adi_lanes() : adi_lanes();
     const size_t smem = adi_smem_bytes();
     RoundCheck rc{};
     rc.ntensor = ntensor;
@@ -222,7 +232,7 @@ void Ctx::run_adi(DevSet& set, bool full, int ntensor, const double* const* src0
     rc.iters = ws.iters;
     for (int round = 0; round < 4; ++round) {
         P.round = round;
-        adi_kernel<<<P.ntasks, threads, smem, stream>>>(P);
+        adi_launch(P, threads, smem, stream);
         rc.round = round;
         adi_round_check<<<(nts + 127) / 128, 128, 0, stream>>>(rc);
         launches += 2;

@@ -64,6 +64,8 @@ struct Ctx {
     int M, N, pitch, Mpad, Npad;
     long estride;
     size_t adi_smem_bytes() const;
+    int adi_lanes() const;
+    bool adi_split() const;
     std::unique_ptr<SizeOps> sizeops;
     std::map<int, Range> radial_cache;
     std::map<std::tuple<int, int, double>, std::unique_ptr<DevSet>> sets;  // (full, poisson, scale)

@@ -8,7 +8,10 @@
 namespace ccf {
 
 // adi.cu
-__global__ void adi_kernel(const AdiParams P);
+// ADI sweeps (adi.cu): size-specialised instantiations behind one launcher
+size_t adi_static_smem();
+cudaError_t adi_set_smem(int bytes);
+void adi_launch(const AdiParams& P, int threads, size_t smem, cudaStream_t stream);
 struct RoundCheck {
     int ntensor, nslots, round;
     double tol;

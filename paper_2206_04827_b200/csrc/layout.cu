@@ -26,10 +26,10 @@ __device__ __forceinline__ int parity_j0(int w, int cls) { return ((w + cls) % 2
 __global__ void ref_to_h_kernel(const double* __restrict__ ref, double* __restrict__ out, Geo g, int full, int cls) {
     const long total = long(g.nslots) * g.slot_stride;
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < total; i += long(gridDim.x) * blockDim.x) {
-        const int jj = int(i % g.mh);
-        const long r = i / g.mh;
-        const int k = int(r % g.n);
-        const long r2 = r / g.n;
+        const int k = kfrompos(int(i % g.n), g.nh);
+        const long r = i / g.n;
+        const int jj = int(r % g.mh);
+        const long r2 = r / g.mh;
         const int plane = int(r2 % 2);
         const int s = int(r2 / 2);
         int l;
@@ -55,7 +55,7 @@ __global__ void h_to_ref_kernel(const double* __restrict__ in, double* __restric
         double re = 0.0, im = 0.0;
         if (((j - j0) & 1) == 0) {
             const int s = slot_of_l(l, g.p, full);
-            const long off = long(s) * g.slot_stride + long(k) * g.mh + (j - j0) / 2;
+            const long off = long(s) * g.slot_stride + long((j - j0) / 2) * g.n + kpos(k, g.nh);
             re = in[off];
             im = in[off + g.plane_stride];
             if (!full && l != 0 && l < g.p / 2) im = -im;  // w < 0: conjugate partner

@@ -48,6 +48,69 @@ CBand cb_axpy(double al, const CBand& x, double be, const CBand& y) {
     return o;
 }
 
+// Spike vectors of the two-way partitioned sweeps (adi.cu, col/row_phase_spike).
+// Left (column) sweep, rows k of one shift block, split row h:
+//   forward  x_{k+1} -= L0[k] x_k, x_{k+2} -= L1[k] x_k: the lower part runs without the
+//            contributions of x_{h-1}, x_{h-2}; true x_k = x'_k + F1[k] x_{h-1} + F2[k] x_{h-2}
+//   backward z_k = inv x_k - Uf0 z_{k+1} - Uf1 z_{k+2} - Uf2 z_{k+3}: the upper part runs with
+//            z_h = z_{h+1} = z_{h+2} = 0; true z_k = z'_k + G1[k] z_h + G2[k] z_{h+1} + G3[k] z_{h+2}
+void add_left_spikes(double* blk, int M, int h) {
+    auto f = [&](int k, int q) -> double { return blk[size_t(k) * kLeftW + q]; };
+    std::vector<long double> d(size_t(M) + 3);
+    for (int which = 0; which < 2; ++which) {
+        std::fill(d.begin(), d.end(), 0.0L);
+        if (which == 0) {
+            d[size_t(h)] = -(long double)f(h - 1, 6);
+            d[size_t(h) + 1] = -(long double)f(h - 1, 7);
+        } else {
+            d[size_t(h)] = -(long double)f(h - 2, 7);
+        }
+        for (int k = h; k < M; ++k) {
+            d[size_t(k) + 1] -= (long double)f(k, 6) * d[size_t(k)];
+            d[size_t(k) + 2] -= (long double)f(k, 7) * d[size_t(k)];
+        }
+        for (int k = h; k < M; ++k) blk[size_t(k) * kLeftW + 13 + which] = double(d[size_t(k)]);
+    }
+    for (int which = 0; which < 3; ++which) {
+        std::fill(d.begin(), d.end(), 0.0L);
+        d[size_t(h + which)] = 1.0L;
+        for (int k = h - 1; k >= 0; --k)
+            d[size_t(k)] = -(long double)f(k, 10) * d[size_t(k) + 1] - (long double)f(k, 11) * d[size_t(k) + 2] -
+                           (long double)f(k, 12) * d[size_t(k) + 3];
+        for (int k = 0; k < h; ++k) blk[size_t(k) * kLeftW + 13 + which] = double(d[size_t(k)]);
+    }
+}
+
+// Right (row) sweep with the fused multiply g = z (v'B + D) (row k: mul fields 0..3, d = -1..2):
+//   forward  x_{k+1} -= L[k] x_k -> lower half: true x_k = x'_k + F[k] x_{h-1}        (k >= h)
+//   backward z_k = inv x_k - Uf0 z_{k+1} - Uf1 z_{k+2}: the upper half runs with z_h = z_{h+1} = 0,
+//            true z_k = z'_k + G1[k] z_h + G2[k] z_{h+1}; its fused multiply g'_k (k <= h) then
+//            differs from g_k by the rank-3 term H1[k] z_h + H2[k] z_{h+1} + H3[k] z_{h+2}.
+// Fields (unpivoted rows only): [5] F (k >= h), [7] H3 (k = h), [10] H1, [11] H2 (k <= h).
+void add_right_spikes(double* blk, int N, int h) {
+    auto f = [&](int k, int q) -> double { return blk[size_t(k) * kRightW + q]; };
+    std::vector<long double> d(size_t(N) + 3);
+    std::fill(d.begin(), d.end(), 0.0L);
+    d[size_t(h)] = -(long double)f(h - 1, 4);
+    for (int k = h; k < N; ++k) d[size_t(k) + 1] -= (long double)f(k, 4) * d[size_t(k)];
+    for (int k = h; k < N; ++k) blk[size_t(k) * kRightW + 5] = double(d[size_t(k)]);
+    for (int which = 0; which < 2; ++which) {
+        std::fill(d.begin(), d.end(), 0.0L);  // extended response: G[j] (j < h), unit at h + which
+        d[size_t(h + which)] = 1.0L;
+        for (int k = h - 1; k >= 0; --k)
+            d[size_t(k)] = -(long double)f(k, 8) * d[size_t(k) + 1] - (long double)f(k, 9) * d[size_t(k) + 2];
+        for (int k = 0; k <= h && k < N; ++k) {
+            long double acc = 0.0L;
+            for (int dd = -1; dd <= 2; ++dd) {
+                const int j = k + dd;
+                if (j >= 0) acc += (long double)f(k, dd + 1) * d[size_t(j)];
+            }
+            blk[size_t(k) * kRightW + 10 + which] = double(acc);
+        }
+    }
+    if (h < N) blk[size_t(h) * kRightW + 7] = f(h, 3);  // H3: m_2[h] z_{h+2}
+}
+
 }  // namespace
 
 SizeOps::SizeOps(int m_, int n_) : m(m_), n(n_), ur(m_), uz(n_) {
@@ -273,6 +336,16 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
                     r[6 + q] = Ac.at(a, q - 2);
                     r[12 + q] = Cc.at(a, q - 2);
                 }
+            }
+        }
+        // spike vectors for the partitioned sweeps (unpivoted slots only: the fields they
+        // occupy hold pivoted fill-in otherwise, and pivoted slots keep the sequential sweeps)
+        const int hc = spike_split(lrows - 2), hr = spike_split(rrows - 2);
+        if (!d.pivot && hc > 0 && hr > 0 && hc < M && hr < N) {
+            for (int j = 0; j < J; ++j) {
+                add_left_spikes(C.data() + d.left + size_t(j) * lrows * kLeftW, M, hc);
+                add_right_spikes(C.data() + d.right0 + size_t(j) * rrows * kRightW, N, hr);
+                add_right_spikes(C.data() + d.right1 + size_t(j) * rrows * kRightW, N, hr);
             }
         }
         built[aw] = d;

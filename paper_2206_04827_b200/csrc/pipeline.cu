@@ -37,7 +37,8 @@ unsigned blocks_for(long n, int t) { return unsigned((n + t - 1) / t); }
 TransformPlan::TransformPlan(Ctx& c) {
     const int m = c.m, n = c.n, p = c.p, mh = m / 2, M = c.M;
     const long L = m - 1, Lz = n - 1;
-    // r synthesis / analysis on the r > 0 half grid, per coefficient parity j0
+    // r synthesis / analysis on the r > 0 half grid, per coefficient parity j0 (A operands):
+    //   SrT[j0][jr][i] = T_{2i+j0}(r_{mh+jr}),  ArT[j0][i][jr] = analysis weights (values -> coefficients)
     for (int j0 = 0; j0 < 2; ++j0) {
         std::vector<double> S(size_t(mh) * mh), A(size_t(mh) * mh);
         for (int i = 0; i < mh; ++i) {
@@ -45,27 +46,39 @@ TransformPlan::TransformPlan(Ctx& c) {
             const long double eps = (k == 0 || k == m - 1) ? 0.5L : 1.0L;
             for (int jr = 0; jr < mh; ++jr) {
                 const int s = mh - 1 - jr;  // descending-x index of grid point j = mh + jr
-                S[size_t(i) * mh + jr] = double(cospi_frac(long(k) * s, L));
+                S[size_t(jr) * mh + i] = double(cospi_frac(long(k) * s, L));
                 const long double ws = (s == 0) ? 1.0L : 2.0L;
-                A[size_t(jr) * mh + i] = double(eps / (long double)L * 2.0L * ws * cospi_frac(long(k) * s, L));
+                A[size_t(i) * mh + jr] = double(eps / (long double)L * 2.0L * ws * cospi_frac(long(k) * s, L));
             }
         }
         upload(SrT[j0], S);
         upload(ArT[j0], A);
     }
-    // z: dense n x n (both parities)
+    // z: dense n x n (both parities) as B operands over parity-split coefficient positions q:
+    //   Sz[q][kz] = T_{k(q)}(z_kz),  Az[kz][q] = analysis weight of coefficient k(q) at z_kz
     {
+        const int nh = n / 2;
         std::vector<double> S(size_t(n) * n), A(size_t(n) * n);
         for (int kz = 0; kz < n; ++kz)
-            for (int k = 0; k < n; ++k) {
+            for (int q = 0; q < n; ++q) {
+                const int k = kfrompos(q, nh);
                 const int s = n - 1 - kz;
-                S[size_t(kz) * n + k] = double(cospi_frac(long(k) * s, Lz));
+                S[size_t(q) * n + kz] = double(cospi_frac(long(k) * s, Lz));
                 const long double eps = (k == 0 || k == n - 1) ? 0.5L : 1.0L;
                 const long double ws = (s == 0 || s == n - 1) ? 1.0L : 2.0L;
-                A[size_t(k) * n + kz] = double(eps / (long double)Lz * ws * cospi_frac(long(k) * s, Lz));
+                A[size_t(kz) * n + q] = double(eps / (long double)Lz * ws * cospi_frac(long(k) * s, Lz));
             }
         upload(Sz, S);
         upload(Az, A);
+        std::vector<double> Sf(size_t(n) * n), Af(size_t(n) * n);
+        for (int kz = 0; kz < n; ++kz)
+            for (int q = 0; q < n; ++q) {
+                const int k = kfrompos(q, nh);
+                Sf[size_t(kz) * n + k] = S[size_t(q) * n + kz];
+                Af[size_t(k) * n + kz] = A[size_t(kz) * n + q];
+            }
+        upload(Szf, Sf);
+        upload(Azf, Af);
     }
     // r: dense m x m (API transforms): values_j = sum_k c_k T_k(r_j);  c_k = sum_j A[k][j] values_j
     {
@@ -215,8 +228,8 @@ void Pipeline::dz(const std::vector<const double*>& in, const std::vector<double
         d.in[i] = in[i];
         d.out[i] = out[i];
     }
-    const long n = long(g.nslots) * 2 * g.mh * d.count;
-    dz_kernel<<<blocks_for(n, 128), 128, 0, c.stream>>>(d);
+    const long warps = long(g.nslots) * 2 * g.mh * d.count;
+    dz_kernel<<<blocks_for(warps * 32, 256), 256, 0, c.stream>>>(d);
     ++c.launches;
 }
 
@@ -263,25 +276,25 @@ void Pipeline::rz_synth(int count, const double* const* in, const int* cls, doub
                     const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
                     const int w = (s == g.p / 2) ? -g.p / 2 : s;
                     const int j0 = ((w + cls[t]) % 2 + 2) % 2;
-                    r.A.push_back(in[t] + off);
-                    r.B.push_back(tp.SrT[j0].p);
-                    r.C.push_back(tmp[t] + off);
-                    z.A.push_back(tp.Sz.p);
-                    z.B.push_back(tmp[t] + off);
-                    z.C.push_back(out[t] + off);
+                    r.A.push_back(tp.SrT[j0].p);  // [jr][jj]
+                    r.B.push_back(in[t] + off);   // [jj][q]
+                    r.C.push_back(tmp[t] + off);  // [jr][q]
+                    z.A.push_back(tmp[t] + off);  // [jr][q]
+                    z.B.push_back(tp.Sz.p);       // [q][kz]
+                    z.C.push_back(out[t] + off);  // [jr][kz]
                 }
-        r.M = g.n;
-        r.N = g.mh;
+        r.M = g.mh;
+        r.N = g.n;
         r.K = g.mh;
         r.lda = g.mh;
-        r.ldb = g.mh;
-        r.ldc = g.mh;
-        z.M = g.n;
-        z.N = g.mh;
+        r.ldb = g.n;
+        r.ldc = g.n;
+        z.M = g.mh;
+        z.N = g.n;
         z.K = g.n;
         z.lda = g.n;
-        z.ldb = g.mh;
-        z.ldc = g.mh;
+        z.ldb = g.n;
+        z.ldc = g.n;
         r.upload();
         z.upload();
     }
@@ -308,25 +321,25 @@ void Pipeline::rz_analyze(int count, const double* const* in, const int* cls, do
                     const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
                     const int w = (s == g.p / 2) ? -g.p / 2 : s;
                     const int j0 = ((w + cls[t]) % 2 + 2) % 2;
-                    z.A.push_back(tp.Az.p);
-                    z.B.push_back(in[t] + off);
-                    z.C.push_back(tmp[t] + off);
-                    r.A.push_back(tmp[t] + off);
-                    r.B.push_back(tp.ArT[j0].p);
-                    r.C.push_back(out[t] + off);
+                    z.A.push_back(in[t] + off);   // values [jr][kz]
+                    z.B.push_back(tp.Az.p);       // [kz][q]
+                    z.C.push_back(tmp[t] + off);  // [jr][q]
+                    r.A.push_back(tp.ArT[j0].p);  // [jj][jr]
+                    r.B.push_back(tmp[t] + off);  // [jr][q]
+                    r.C.push_back(out[t] + off);  // [jj][q]
                 }
-        z.M = g.n;
-        z.N = g.mh;
+        z.M = g.mh;
+        z.N = g.n;
         z.K = g.n;
         z.lda = g.n;
-        z.ldb = g.mh;
-        z.ldc = g.mh;
-        r.M = g.n;
-        r.N = g.mh;
+        z.ldb = g.n;
+        z.ldc = g.n;
+        r.M = g.mh;
+        r.N = g.n;
         r.K = g.mh;
         r.lda = g.mh;
-        r.ldb = g.mh;
-        r.ldc = g.mh;
+        r.ldb = g.n;
+        r.ldc = g.n;
         z.upload();
         r.upload();
     }
@@ -353,7 +366,7 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
         CCF_CUDA(cudaFuncSetAttribute(theta_cross_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    const dim3 grid(unsigned((g.mh + tj - 1) / tj), unsigned(g.n));
+    const dim3 grid(unsigned((g.n + tj - 1) / tj), unsigned(g.mh));
     theta_cross_kernel<<<grid, 256, smem, c.stream>>>(t);
     ++c.launches;
 }
@@ -507,7 +520,7 @@ void Pipeline::analyze_full(const double* values, double* coeffs) {
         r.A.push_back(v + long(l) * m * n);  // [k][j] slice, r-analysis on the right
         r.B.push_back(tp.Rfull_A.p);         // B = A_r^T: (j, k) -> A[k][j]
         r.C.push_back(t + long(l) * m * n);
-        zz.A.push_back(tp.Az.p);
+        zz.A.push_back(tp.Azf.p);
         zz.B.push_back(t + long(l) * m * n);
         zz.C.push_back(v + long(l) * m * n);
     }
@@ -547,7 +560,7 @@ void Pipeline::synthesize_full(const double* coeffs, double* values) {
     complex_re_kernel<<<std::min<long>(4736, (nv + 255) / 256), 256, 0, c.stream>>>(zc, v, nv);
     GemmPlan zz, r;
     for (int l = 0; l < p; ++l) {
-        zz.A.push_back(tp.Sz.p);
+        zz.A.push_back(tp.Szf.p);
         zz.B.push_back(v + long(l) * m * n);
         zz.C.push_back(t + long(l) * m * n);
         r.A.push_back(t + long(l) * m * n);

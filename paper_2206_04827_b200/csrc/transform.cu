@@ -144,16 +144,16 @@ __device__ __forceinline__ int bitrev(int x, int logP) { return __brev(unsigned(
 
 // Fused theta synthesis -> cross product -> theta analysis (stage X of the NS step).
 // in[0..5] = (v_r, v_theta, v_z, w_r, w_theta, w_z), out[0..2] = (a_r, a_theta, a_z),
-// all in the (r,z)-value / theta-half-spectrum layout [slot][plane][k][jr].
-// One CTA per (k, tile of TJ consecutive jr).
+// all in the (r,z)-value / theta-half-spectrum layout [slot][plane][jr][kz].
+// One CTA per (jr, tile of TJ consecutive z positions).
 __global__ void theta_cross_kernel(ThetaCross t) {
     extern __shared__ double2 sd[];
     const Geo& g = t.g;
     const int P = g.p, logP = t.logp, S = g.nslots;
     const int TJ = t.tj;
-    const int k = blockIdx.y;
-    const int jr0 = blockIdx.x * TJ;
-    const int ntj = min(TJ, g.mh - jr0);
+    const int jr = blockIdx.y;          // r > 0 grid row
+    const int q0 = blockIdx.x * TJ;     // first z position of the tile (contiguous in memory)
+    const int ntj = min(TJ, g.n - q0);
     double2* Z = sd;                       // 3 * TJ arrays of P (packed pairs)
     const double2* tw = t.tw;              // P/2 twiddles exp(-2 pi i q / P)
     // ---- gather Hermitian spectra of pairs (0,1) (2,3) (4,5) into bit-reversed slots
@@ -175,7 +175,7 @@ __global__ void theta_cross_kernel(ThetaCross t) {
             }
             const int s = (w == -P / 2) ? P / 2 : w;
             const double sg = ((w & 1) ? -1.0 : 1.0);
-            const long off = long(s) * g.slot_stride + long(k) * g.mh + jr0 + jl;
+            const long off = long(s) * g.slot_stride + long(jr) * g.n + q0 + jl;
             double2 xa, xb;
             {
                 const double* fa = t.in[2 * pr];
@@ -241,7 +241,7 @@ __global__ void theta_cross_kernel(ThetaCross t) {
         if (f == 0 || f == 2) X = make_double2(0.5 * (zt.x + zm.x), 0.5 * (zt.y - zm.y));
         else X = make_double2(0.5 * (zt.y + zm.y), -0.5 * (zt.x - zm.x));
         const double sg = ((w & 1) ? -1.0 : 1.0) * invp;
-        const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride + long(k) * g.mh + jr0 + jl;
+        const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride + long(jr) * g.n + q0 + jl;
         t.out[f][off] = sg * (pl ? X.y : X.x);
     }
 }

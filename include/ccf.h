@@ -46,7 +46,11 @@ typedef struct ccf_ns_state ccf_ns_state;
 /* Context: one grid size, one GPU, one stream; caches shift plans and factors
  * (ModalSolverCache, proj/include/cylspec/solvers.hpp:63-76).
  * flags: bit 0 = Q2 endpoint-relative enclosure pad where the reference
- * intervals overlap (off = reference semantics). */
+ * intervals overlap (off = reference semantics);
+ * bit 1 = execute the reference's ADI shift counts. By default the executed Zolotarev
+ * plan is the one for adi_tol / 4 (1-2 more shifts per mode) so that slots finishing
+ * just above adi_tol do not trigger a serial restart round; the per-round acceptance
+ * test (relative residual <= adi_tol) and the restart logic are unchanged. */
 ccf_status ccf_ctx_create(int m, int n, int p, int device, double adi_tol, int flags, ccf_ctx** out);
 ccf_status ccf_ctx_destroy(ccf_ctx* ctx);
 /* Use an external cudaStream_t (NULL restores the context's own stream). */
@@ -103,6 +107,13 @@ ccf_status ccf_get_last_error(ccf_ctx* ctx, int* kind, int* slice, int* shift_in
 ccf_status ccf_get_stats(ccf_ctx* ctx, long* adi_subproblems, long* adi_iterations, int* max_rounds,
                          double* worst_residual, long* kernel_launches);
 ccf_status ccf_reset_stats(ccf_ctx* ctx);
+/* Per (tensor, slot) ADI rounds used (1..4) and relative residual after each round
+ * (history[4 * i + r]) of the most recent ADI solve on this context (adi.cpp:163-200):
+ * which = 0 most recent solve, 1 / 2 most recent Poisson / Helmholtz solve (needs
+ * ccf_adi_keep_history(ctx, 1) beforehand; adds two device copies per solve). */
+ccf_status ccf_adi_keep_history(ccf_ctx* ctx, int enable);
+ccf_status ccf_adi_last_rounds(ccf_ctx* ctx, int which, int* ntensor, int* nslots, int* rounds, double* history,
+                               int cap);
 
 /* Shift plan of the (|w|, poisson|scale) modal solver of this context (for parity
  * tests against the reference plan): info = {a, b, c, d, gamma, alpha, modulus, J}. */

@@ -76,7 +76,7 @@ EXPORTS = ["ccf_ctx_create", "ccf_ctx_destroy", "ccf_ctx_set_stream", "ccf_ctx_s
            "ccf_nonlinear", "ccf_ns_create", "ccf_ns_step", "ccf_ns_get_omega", "ccf_ns_destroy",
            "ccf_get_last_error", "ccf_get_stats", "ccf_reset_stats", "ccf_modal_plan", "ccf_version",
            "ccf_ns_profile_step", "ccf_ns_set_graphs", "ccf_ns_launches_per_step", "ccf_plan_host",
-           "ccf_create_error"]
+           "ccf_create_error", "ccf_adi_last_rounds", "ccf_adi_keep_history"]
 
 _lib = None
 
@@ -123,6 +123,8 @@ def lib():
         L.ccf_ns_destroy.argtypes = [vp]
         L.ccf_get_last_error.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), dp,
                                          C.POINTER(C.c_int), C.c_char_p, C.c_int]
+        L.ccf_adi_last_rounds.argtypes = [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), vp, vp, C.c_int]
+        L.ccf_adi_keep_history.argtypes = [vp, C.c_int]
         L.ccf_get_stats.argtypes = [vp, C.POINTER(C.c_long), C.POINTER(C.c_long), C.POINTER(C.c_int), dp,
                                     C.POINTER(C.c_long)]
         L.ccf_reset_stats.argtypes = [vp]
@@ -297,6 +299,21 @@ class Context:
 
     def reset_stats(self):
         self._check(lib().ccf_reset_stats(self.h))
+
+    def adi_keep_history(self, enable=True):
+        self._check(lib().ccf_adi_keep_history(self.h, int(bool(enable))))
+
+    def adi_last_rounds(self, which=0):
+        """(rounds[ntensor, nslots], history[ntensor, nslots, 4]) of the most recent ADI solve
+        (which = 0), or of the most recent Poisson (1) / Helmholtz (2) solve."""
+        cap = 2 * max(self.p, 1) + 2
+        nt, ns = C.c_int(), C.c_int()
+        r = np.zeros(cap, dtype=np.int32)
+        h = np.zeros(cap * 4)
+        self._check(lib().ccf_adi_last_rounds(self.h, int(which), C.byref(nt), C.byref(ns), r.ctypes.data,
+                                              h.ctypes.data, cap))
+        n = nt.value * ns.value
+        return r[:n].reshape(nt.value, ns.value), h[: 4 * n].reshape(nt.value, ns.value, 4)
 
 
 def plan_host(m, n, w, scale=1.0, poisson=True, tol=1e-12, q2_endpoint_pad=False):

@@ -214,6 +214,39 @@ ccf_status ccf_get_stats(ccf_ctx* ctx, long* adi_subproblems, long* adi_iteratio
     });
 }
 
+ccf_status ccf_adi_keep_history(ccf_ctx* ctx, int enable) {
+    return guard(ctx, [&](Ctx& c) {
+        c.keep_history = enable != 0;
+        if (c.keep_history)
+            for (int k = 1; k < 3; ++k) {
+                const size_t cap = size_t(2) * size_t(std::max(c.p, 2));
+                if (!c.kept_hist[k].p) c.kept_hist[k].alloc(cap * 4);
+                if (!c.kept_rounds[k].p) c.kept_rounds[k].alloc(cap);  // ints fit in the double slots
+            }
+    });
+}
+
+ccf_status ccf_adi_last_rounds(ccf_ctx* ctx, int which, int* ntensor, int* nslots, int* rounds, double* history,
+                               int cap) {
+    return guard(ctx, [&](Ctx& c) {
+        if (which < 0 || which > 2) throw Error(ccf::DOMAIN_ERROR, "ccf_adi_last_rounds: which in {0, 1, 2}");
+        if (which > 0 && !c.keep_history)
+            throw Error(ccf::DOMAIN_ERROR, "ccf_adi_last_rounds: enable ccf_adi_keep_history first");
+        const int nt = which ? c.kept_shape[which][0] : c.last_adi_ntensor;
+        const int ns = which ? c.kept_shape[which][1] : c.last_adi_nslots;
+        const int n = nt * ns;
+        *ntensor = nt;
+        *nslots = ns;
+        if (n == 0) return;
+        if (cap < n) throw Error(ccf::DOMAIN_ERROR, "ccf_adi_last_rounds: cap < ntensor * nslots");
+        c.sync();
+        const void* rs = which ? static_cast<const void*>(c.kept_rounds[which].p) : c.ws.rounds;
+        const void* hs = which ? static_cast<const void*>(c.kept_hist[which].p) : c.ws.history;
+        if (rounds) CCF_CUDA(cudaMemcpy(rounds, rs, sizeof(int) * size_t(n), cudaMemcpyDeviceToHost));
+        if (history) CCF_CUDA(cudaMemcpy(history, hs, sizeof(double) * 4 * size_t(n), cudaMemcpyDeviceToHost));
+    });
+}
+
 ccf_status ccf_reset_stats(ccf_ctx* ctx) {
     return guard(ctx, [&](Ctx& c) {
         CCF_CUDA(cudaMemset(c.ws.iters, 0, sizeof(unsigned long long) * 2));

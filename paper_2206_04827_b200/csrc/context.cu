@@ -145,7 +145,9 @@ DevSet& Ctx::set(bool full, bool poisson, double scale) {
     std::vector<int> slot_w(size_t(g.nslots));
     for (int s = 0; s < g.nslots; ++s) slot_w[size_t(s)] = full ? s - p / 2 : (s == p / 2 ? -p / 2 : s);
     auto ds = std::make_unique<DevSet>();
-    ds->host = build_solver_set(*sizeops, slot_w, poisson, scale, tol, radial_cache, (flags & 1) != 0);
+    // flags bit1: execute the reference's shift counts (no tail-avoidance margin)
+    ds->host = build_solver_set(*sizeops, slot_w, poisson, scale, tol, radial_cache, (flags & 1) != 0,
+                                (flags & 2) ? 1.0 : 4.0);
     const SolverSet& h = ds->host;
     CCF_CUDA(cudaMalloc(&ds->coef, h.coef.size() * sizeof(double)));
     CCF_CUDA(cudaMemcpy(ds->coef, h.coef.data(), h.coef.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -178,6 +180,8 @@ void Ctx::run_adi(DevSet& set, bool full, int ntensor, const double* const* src0
                   const double* const* src1, const double* w1, int n1, double* out0, double* out1) {
     const Geo& g = geo(full);
     last_adi_kind = set.host.poisson ? "Poisson" : "Helmholtz";
+    last_adi_ntensor = ntensor;
+    last_adi_nslots = g.nslots;
     AdiParams P{};
     P.g = g;
     P.M = M;
@@ -236,6 +240,14 @@ void Ctx::run_adi(DevSet& set, bool full, int ntensor, const double* const* src0
         rc.round = round;
         adi_round_check<<<(nts + 127) / 128, 128, 0, stream>>>(rc);
         launches += 2;
+    }
+    if (keep_history) {  // diagnostics: per-kind copy of the round bookkeeping (ccf_adi_last_rounds)
+        const int k = set.host.poisson ? 1 : 2;
+        kept_shape[k][0] = ntensor;
+        kept_shape[k][1] = g.nslots;
+        CCF_CUDA(cudaMemcpyAsync(kept_rounds[k].p, ws.rounds, sizeof(int) * size_t(nts), cudaMemcpyDeviceToDevice, stream));
+        CCF_CUDA(cudaMemcpyAsync(kept_hist[k].p, ws.history, sizeof(double) * 4 * size_t(nts), cudaMemcpyDeviceToDevice,
+                                 stream));
     }
     CCF_CUDA(cudaGetLastError());
 }

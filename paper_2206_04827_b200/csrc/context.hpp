@@ -74,6 +74,10 @@ struct Ctx {
     DBuf tens[16];  // generic device scratch tensors (compressed layout, full size)
     long launches = 0;
     const char* last_adi_kind = "";
+    int last_adi_ntensor = 0, last_adi_nslots = 0;  // shape of ws.rounds / ws.history of the last ADI run
+    bool keep_history = false;  // diagnostics: keep the last Poisson (1) / Helmholtz (2) round bookkeeping
+    DBuf kept_hist[3], kept_rounds[3];
+    int kept_shape[3][2] = {};
     // optional stage profiling: events recorded at stage boundaries when enabled
     bool profiling = false;
     std::vector<cudaEvent_t> prof_events;

@@ -134,7 +134,7 @@ Range vertical_range(SizeOps& so, bool q2_pad) {
 }
 
 SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poisson, double scale, double tol,
-                           std::map<int, Range>& radial_cache, bool q2_pad) {
+                           std::map<int, Range>& radial_cache, bool q2_pad, double plan_margin) {
     const int m = so.m, n = so.n, M = (m - 2) / 2, N = (n - 2) / 2, mh = m / 2, nh = n / 2;
     const int lrows = ((M + 7) / 8) * 8 + 2, rrows = ((N + 7) / 8) * 8 + 2;  // zero-padded sweep rows
     SolverSet set;
@@ -225,17 +225,23 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
         const Range mu = radial_cache.at(aw);
         Range ca = poisson ? mu : Range{-1.0 / scale + mu.lo, -1.0 / scale + mu.hi};
         Plan plan;
+        Range db = vert;
         try {
             plan = shift_plan(ca, vert, tol);
         } catch (const Error& e) {
             if (!(q2_pad && e.status == DOMAIN_ERROR)) throw;
             // endpoint-relative pad only where the reference intervals overlap
             const Range mu2 = radial_range(so, aw, true);
-            const Range v2 = vertical_range(so, true);
+            db = vertical_range(so, true);
             ca = poisson ? mu2 : Range{-1.0 / scale + mu2.lo, -1.0 / scale + mu2.hi};
-            plan = shift_plan(ca, v2, tol);
+            plan = shift_plan(ca, db, tol);
         }
-        const int J = plan.J;
+        // Executed shifts: the reference plan (reported through modal_plan), or with plan_margin > 1
+        // the Zolotarev plan for tol / plan_margin (1-2 more shifts) so that rounding in the first
+        // round does not push a slot just over tol into a second, serial round; the acceptance test
+        // per round stays ||R|| / ||E|| <= tol.
+        const Plan xplan = plan_margin > 1.0 ? shift_plan(ca, db, tol / plan_margin) : plan;
+        const int J = xplan.J;
         AdiSlot d{};
         d.J = J;
         d.j0 = j0;
@@ -248,8 +254,8 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
         d.ds = alloc(size_t(J) + 1);
         // left dynamic blocks
         for (int j = 0; j < J; ++j) {
-            const CBand mul = cb_axpy(plan.u[size_t(j)], Cc, -1.0, Ac);
-            const CBand sh = cb_axpy(plan.v[size_t(j)], Cc, -1.0, Ac);
+            const CBand mul = cb_axpy(xplan.u[size_t(j)], Cc, -1.0, Ac);
+            const CBand sh = cb_axpy(xplan.v[size_t(j)], Cc, -1.0, Ac);
             CLU lu;
             try {
                 lu = banded_lu(sh, 2, 3);
@@ -269,18 +275,18 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
                 if (lu.piv[size_t(a)]) d.pivot = 1;
                 for (int q = 0; q < 5; ++q) r[10 + q] = lu.U[size_t(a) * 5 + q] * lu.inv[size_t(a)];
             }
-            C[size_t(d.ds) + j] = plan.u[size_t(j)] - plan.v[size_t(j)];
+            C[size_t(d.ds) + j] = xplan.u[size_t(j)] - xplan.v[size_t(j)];
         }
         // right dynamic blocks
         for (int k0 = 0; k0 < 2; ++k0) {
             const long base = k0 ? d.right1 : d.right0;
             for (int j = 0; j < J; ++j) {
                 // G_{j+1} = X_{j+1} (v_{j+1} B + D); identity after the last shift (the row sweep then yields X)
-                CBand mul = (j + 1 < J) ? cb_axpy(plan.v[size_t(j + 1)], Btc[k0], 1.0, Dtc[k0]) : Btc[k0];
+                CBand mul = (j + 1 < J) ? cb_axpy(xplan.v[size_t(j + 1)], Btc[k0], 1.0, Dtc[k0]) : Btc[k0];
                 if (j + 1 == J)
                     for (int b = 0; b < N; ++b)
                         for (int d = -1; d <= 2; ++d) mul.v[size_t(b) * 4 + size_t(d + 1)] = (d == 0) ? 1.0 : 0.0;
-                const CBand sh = cb_axpy(plan.u[size_t(j)], Btc[k0], 1.0, Dtc[k0]);
+                const CBand sh = cb_axpy(xplan.u[size_t(j)], Btc[k0], 1.0, Dtc[k0]);
                 CLU lu;
                 try {
                     lu = banded_lu(sh, 1, 2);
@@ -304,7 +310,7 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
             } catch (const Error&) {
                 throw Error(SINGULAR, "AdiWorkspace: B is singular");
             }
-            const CBand rs = cb_axpy(plan.v[0], Btc[k0], 1.0, Dtc[k0]);
+            const CBand rs = cb_axpy(xplan.v[0], Btc[k0], 1.0, Dtc[k0]);
             double* blk = C.data() + (k0 ? d.sright1 : d.sright0);
             for (int b = 0; b < N; ++b) {
                 double* r = blk + size_t(b) * kStatW;

@@ -45,7 +45,8 @@ struct SolverSet {
 // Build the packed set. slot_w: wavenumber per slot. radial: cached radial
 // ranges per |w| (computed on demand). Throws ccf::Error on reference failures
 // (overlapping intervals -> DOMAIN_ERROR, singular operators -> SINGULAR).
+// plan_margin: executed shifts planned for tol / plan_margin (1 = the reference's shift count).
 SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poisson, double scale, double tol,
-                           std::map<int, Range>& radial_cache, bool q2_pad);
+                           std::map<int, Range>& radial_cache, bool q2_pad, double plan_margin = 1.0);
 
 }  // namespace ccf

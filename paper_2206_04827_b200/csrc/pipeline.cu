@@ -54,8 +54,30 @@ TransformPlan::TransformPlan(Ctx& c) {
         upload(SrT[j0], S);
         upload(ArT[j0], A);
     }
-    // z: dense n x n (both parities) as B operands over parity-split coefficient positions q:
-    //   Sz[q][kz] = T_{k(q)}(z_kz),  Az[kz][q] = analysis weight of coefficient k(q) at z_kz
+    // z: values are kept z-parity split per r row, [E | O] with E_i / O_i the even- / odd-k parts at
+    // z_{nh+i} > 0 (f(+-z_{nh+i}) = E_i +- O_i), so each z transform is two nh x nh products:
+    //   SzE[q][i] = T_{2q}(z_{nh+i}), SzO[q][i] = T_{2q+1}(z_{nh+i})          (synthesis, B operands)
+    //   AzE[i][q] = 2 A[2q][nh+i],   AzO[i][q] = 2 A[2q+1][nh+i]            (analysis of E' / O')
+    // (A[k][kz] the analysis weights; A[k][n-1-kz] = (-1)^k A[k][kz]). Requires even n.
+    {
+        const int nh = n / 2;
+        auto zan = [&](int k, int kz) {
+            const int s = n - 1 - kz;
+            const long double eps = (k == 0 || k == n - 1) ? 0.5L : 1.0L;
+            const long double ws = (s == 0 || s == n - 1) ? 1.0L : 2.0L;
+            return eps / (long double)Lz * ws * cospi_frac(long(k) * s, Lz);
+        };
+        std::vector<double> S(size_t(n) * nh), A(size_t(n) * nh);  // [SzE ; SzO], [AzE ; AzO]
+        for (int par = 0; par < 2; ++par)
+            for (int q = 0; q < nh; ++q)
+                for (int i = 0; i < nh; ++i) {
+                    const int k = 2 * q + par, kz = nh + i;
+                    S[size_t(par) * nh * nh + size_t(q) * nh + i] = double(cospi_frac(long(k) * (n - 1 - kz), Lz));
+                    A[size_t(par) * nh * nh + size_t(i) * nh + q] = double(2.0L * zan(k, kz));
+                }
+        upload(Sz, S);
+        upload(Az, A);
+    }
     {
         const int nh = n / 2;
         std::vector<double> S(size_t(n) * n), A(size_t(n) * n);
@@ -68,8 +90,6 @@ TransformPlan::TransformPlan(Ctx& c) {
                 const long double ws = (s == 0 || s == n - 1) ? 1.0L : 2.0L;
                 A[size_t(kz) * n + q] = double(eps / (long double)Lz * ws * cospi_frac(long(k) * s, Lz));
             }
-        upload(Sz, S);
-        upload(Az, A);
         std::vector<double> Sf(size_t(n) * n), Af(size_t(n) * n);
         for (int kz = 0; kz < n; ++kz)
             for (int q = 0; q < n; ++q) {
@@ -279,9 +299,11 @@ void Pipeline::rz_synth(int count, const double* const* in, const int* cls, doub
                     r.A.push_back(tp.SrT[j0].p);  // [jr][jj]
                     r.B.push_back(in[t] + off);   // [jj][q]
                     r.C.push_back(tmp[t] + off);  // [jr][q]
-                    z.A.push_back(tmp[t] + off);  // [jr][q]
-                    z.B.push_back(tp.Sz.p);       // [q][kz]
-                    z.C.push_back(out[t] + off);  // [jr][kz]
+                    for (int par = 0; par < 2; ++par) {
+                        z.A.push_back(tmp[t] + off + par * g.nh);                // [jr][q of parity par]
+                        z.B.push_back(tp.Sz.p + size_t(par) * g.nh * g.nh);     // [q][i]
+                        z.C.push_back(out[t] + off + par * g.nh);                // [jr][E | O]
+                    }
                 }
         r.M = g.mh;
         r.N = g.n;
@@ -290,10 +312,10 @@ void Pipeline::rz_synth(int count, const double* const* in, const int* cls, doub
         r.ldb = g.n;
         r.ldc = g.n;
         z.M = g.mh;
-        z.N = g.n;
-        z.K = g.n;
+        z.N = g.nh;
+        z.K = g.nh;
         z.lda = g.n;
-        z.ldb = g.n;
+        z.ldb = g.nh;
         z.ldc = g.n;
         r.upload();
         z.upload();
@@ -321,18 +343,20 @@ void Pipeline::rz_analyze(int count, const double* const* in, const int* cls, do
                     const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
                     const int w = (s == g.p / 2) ? -g.p / 2 : s;
                     const int j0 = ((w + cls[t]) % 2 + 2) % 2;
-                    z.A.push_back(in[t] + off);   // values [jr][kz]
-                    z.B.push_back(tp.Az.p);       // [kz][q]
-                    z.C.push_back(tmp[t] + off);  // [jr][q]
+                    for (int par = 0; par < 2; ++par) {
+                        z.A.push_back(in[t] + off + par * g.nh);             // values [jr][E' | O']
+                        z.B.push_back(tp.Az.p + size_t(par) * g.nh * g.nh);  // [i][q]
+                        z.C.push_back(tmp[t] + off + par * g.nh);            // [jr][q of parity par]
+                    }
                     r.A.push_back(tp.ArT[j0].p);  // [jj][jr]
                     r.B.push_back(tmp[t] + off);  // [jr][q]
                     r.C.push_back(out[t] + off);  // [jj][q]
                 }
         z.M = g.mh;
-        z.N = g.n;
-        z.K = g.n;
+        z.N = g.nh;
+        z.K = g.nh;
         z.lda = g.n;
-        z.ldb = g.n;
+        z.ldb = g.nh;
         z.ldc = g.n;
         r.M = g.mh;
         r.N = g.n;
@@ -354,8 +378,9 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
     ThetaCross t{};
     t.g = g;
     t.logp = tp.logp;
-    int tj = 8;
-    while (tj > 1 && size_t(3) * tj * g.p * sizeof(double2) > 100 * 1024) tj /= 2;
+    if (g.n % 2) throw Error(DOMAIN_ERROR, "ccf: the z-parity split value layout needs even n");
+    int tj = 8;  // points per CTA (pairs of +-z)
+    while (tj > 2 && size_t(3) * tj * g.p * sizeof(double2) > 100 * 1024) tj /= 2;
     t.tj = tj;
     for (int i = 0; i < 6; ++i) t.in[i] = v6[i];
     for (int i = 0; i < 3; ++i) t.out[i] = a3[i];
@@ -366,7 +391,7 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
         CCF_CUDA(cudaFuncSetAttribute(theta_cross_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    const dim3 grid(unsigned((g.n + tj - 1) / tj), unsigned(g.mh));
+    const dim3 grid(unsigned((g.nh + tj / 2 - 1) / (tj / 2)), unsigned(g.mh));
     theta_cross_kernel<<<grid, 256, smem, c.stream>>>(t);
     ++c.launches;
 }

@@ -20,7 +20,7 @@ namespace ccf {
 // Chebyshev synthesis / analysis matrices (device, row-major) and theta twiddles.
 struct TransformPlan {
     DBuf SrT[2], ArT[2];  // [j0]: mh x mh  (A operands of the r-GEMMs, r > 0 half grid)
-    DBuf Sz, Az;          // n x n z synthesis / analysis over parity-split positions (B operands)
+    DBuf Sz, Az;          // [2][nh x nh] z synthesis / analysis between parity-split coefficients and [E | O] values
     DBuf Szf, Azf;        // n x n z synthesis [kz][k] / analysis [k][kz] in natural order (API transforms)
     DBuf Rfull_S, Rfull_A;  // m x m dense r synthesis / analysis (API transforms on arbitrary fields)
     DBuf q;               // mh: odd Chebyshev coefficients of the interpolant of 1/r_j

@@ -144,26 +144,29 @@ __device__ __forceinline__ int bitrev(int x, int logP) { return __brev(unsigned(
 
 // Fused theta synthesis -> cross product -> theta analysis (stage X of the NS step).
 // in[0..5] = (v_r, v_theta, v_z, w_r, w_theta, w_z), out[0..2] = (a_r, a_theta, a_z),
-// all in the (r,z)-value / theta-half-spectrum layout [slot][plane][jr][kz].
-// One CTA per (jr, tile of TJ consecutive z positions).
+// all in the (r,z)-value / theta-half-spectrum layout [slot][plane][jr][E | O] (z-parity split
+// values: position i < nh holds E_i, i + nh holds O_i, f(+-z_{nh+i}) = E_i +- O_i).
+// Generic path (any power-of-two p): one CTA per (jr, tile of TJ/2 positions = TJ points).
 __global__ void theta_cross_kernel(ThetaCross t) {
     extern __shared__ double2 sd[];
     const Geo& g = t.g;
     const int P = g.p, logP = t.logp, S = g.nslots;
-    const int TJ = t.tj;
-    const int jr = blockIdx.y;          // r > 0 grid row
-    const int q0 = blockIdx.x * TJ;     // first z position of the tile (contiguous in memory)
-    const int ntj = min(TJ, g.n - q0);
+    const int TJ = t.tj;                 // points per CTA (even): point 2i -> +z, 2i+1 -> -z
+    const int jr = blockIdx.y;           // r > 0 grid row
+    const int q0 = blockIdx.x * (TJ / 2);  // first position of the tile
+    const int ntj = min(TJ / 2, g.nh - q0);
     double2* Z = sd;                       // 3 * TJ arrays of P (packed pairs)
     const double2* tw = t.tw;              // P/2 twiddles exp(-2 pi i q / P)
     // ---- gather Hermitian spectra of pairs (0,1) (2,3) (4,5) into bit-reversed slots
     const int tot = 3 * TJ * P;
     for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        const int jl = e % TJ;              // jr fastest -> coalesced gathers
+        const int jl = e % TJ;              // point fastest -> coalesced gathers
         const int tt = (e / TJ) % P;        // frequency index t in [0, P)
         const int pr = e / (TJ * P);        // pair
+        const int pos = jl >> 1;
+        const double sgz = (jl & 1) ? -1.0 : 1.0;  // f(-z) = E - O
         double2 z = make_double2(0.0, 0.0);
-        if (jl < ntj) {
+        if (pos < ntj) {
             // X[t] = (-1)^w c_w with w = t (t < P/2), Nyquist at t = P/2, conj mirror above
             int w;
             bool conjg = false;
@@ -175,13 +178,14 @@ __global__ void theta_cross_kernel(ThetaCross t) {
             }
             const int s = (w == -P / 2) ? P / 2 : w;
             const double sg = ((w & 1) ? -1.0 : 1.0);
-            const long off = long(s) * g.slot_stride + long(jr) * g.n + q0 + jl;
+            const long off = long(s) * g.slot_stride + long(jr) * g.n + q0 + pos;
+            const long ps = g.plane_stride, oo = g.nh;
             double2 xa, xb;
             {
                 const double* fa = t.in[2 * pr];
                 const double* fb = t.in[2 * pr + 1];
-                xa = make_double2(sg * fa[off], sg * fa[off + g.plane_stride]);
-                xb = make_double2(sg * fb[off], sg * fb[off + g.plane_stride]);
+                xa = make_double2(sg * fma(sgz, fa[off + oo], fa[off]), sg * fma(sgz, fa[off + oo + ps], fa[off + ps]));
+                xb = make_double2(sg * fma(sgz, fb[off + oo], fb[off]), sg * fma(sgz, fb[off + oo + ps], fb[off + ps]));
             }
             if (w == 0 || w == -P / 2) {  // Re only (transform.cpp:201)
                 xa.y = 0.0;
@@ -226,23 +230,29 @@ __global__ void theta_cross_kernel(ThetaCross t) {
     fft_pow2_block(Z, 2 * TJ, P, logP, tw, -1);
     // ---- unpack X_a = (Z[t] + conj Z[P-t]) / 2, X_b = (Z[t] - conj Z[P-t]) / (2i); c_w = (-1)^w X[w mod P] / P
     const double invp = 1.0 / double(P);
-    for (int e = threadIdx.x; e < 3 * S * 2 * TJ; e += blockDim.x) {
-        const int jl = e % TJ;
-        const int pl = (e / TJ) % 2;
-        const int s = (e / (2 * TJ)) % S;
-        const int f = e / (2 * TJ * S);  // output field 0..2
-        if (jl >= ntj) continue;
+    const int TP = TJ / 2;
+    for (int e = threadIdx.x; e < 3 * S * 2 * TP; e += blockDim.x) {
+        const int pos = e % TP;
+        const int pl = (e / TP) % 2;
+        const int s = (e / (2 * TP)) % S;
+        const int f = e / (2 * TP * S);  // output field 0..2
+        if (pos >= ntj) continue;
         const int w = (s == P / 2) ? -P / 2 : s;
         const int tt = (w % P + P) % P;
         const int pair = f < 2 ? 0 : 1;
-        const double2* base = Z + (pair * TJ + jl) * P;
-        const double2 zt = base[tt], zm = base[(P - tt) % P];
-        double2 X;
-        if (f == 0 || f == 2) X = make_double2(0.5 * (zt.x + zm.x), 0.5 * (zt.y - zm.y));
-        else X = make_double2(0.5 * (zt.y + zm.y), -0.5 * (zt.x - zm.x));
-        const double sg = ((w & 1) ? -1.0 : 1.0) * invp;
-        const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride + long(jr) * g.n + q0 + jl;
-        t.out[f][off] = sg * (pl ? X.y : X.x);
+        double xv[2];
+        for (int h = 0; h < 2; ++h) {
+            const double2* base = Z + (pair * TJ + 2 * pos + h) * P;
+            const double2 zt = base[tt], zm = base[(P - tt) % P];
+            double2 X;
+            if (f == 0 || f == 2) X = make_double2(0.5 * (zt.x + zm.x), 0.5 * (zt.y - zm.y));
+            else X = make_double2(0.5 * (zt.y + zm.y), -0.5 * (zt.x - zm.x));
+            xv[h] = pl ? X.y : X.x;
+        }
+        const double sg = ((w & 1) ? -1.0 : 1.0) * invp * 0.5;
+        const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride + long(jr) * g.n + q0 + pos;
+        t.out[f][off] = sg * (xv[0] + xv[1]);         // E' = (f(+z) + f(-z)) / 2
+        t.out[f][off + g.nh] = sg * (xv[0] - xv[1]);  // O' = (f(+z) - f(-z)) / 2
     }
 }
 

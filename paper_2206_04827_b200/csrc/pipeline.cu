@@ -5,6 +5,8 @@
 
 #include "pipeline.hpp"
 
+#include <cstdlib>
+
 namespace ccf {
 
 namespace {
@@ -385,14 +387,22 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
     for (int i = 0; i < 6; ++i) t.in[i] = v6[i];
     for (int i = 0; i < 3; ++i) t.out[i] = a3[i];
     t.tw = reinterpret_cast<const double2*>(tp.tw.p);
-    const size_t smem = size_t(3) * tj * g.p * sizeof(double2);
-    static bool attr = false;
-    if (!attr) {
+    if (!theta_attr_) {
         CCF_CUDA(cudaFuncSetAttribute(theta_cross_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
+        CCF_CUDA(cudaFuncSetAttribute(theta_cross256_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(theta_cross256_smem())));
+        const char* e = std::getenv("CCF_THETA_GENERIC");
+        theta_generic_ = e && e[0] == '1';
+        theta_attr_ = true;
     }
-    const dim3 grid(unsigned((g.nh + tj / 2 - 1) / (tj / 2)), unsigned(g.mh));
-    theta_cross_kernel<<<grid, 256, smem, c.stream>>>(t);
+    if (g.p == 256 && !theta_generic_) {
+        const dim3 grid(unsigned((g.nh + 3) / 4), unsigned(g.mh));
+        theta_cross256_kernel<<<grid, 128, theta_cross256_smem(), c.stream>>>(t);
+    } else {
+        const size_t smem = size_t(3) * tj * g.p * sizeof(double2);
+        const dim3 grid(unsigned((g.nh + tj / 2 - 1) / (tj / 2)), unsigned(g.mh));
+        theta_cross_kernel<<<grid, 256, smem, c.stream>>>(t);
+    }
     ++c.launches;
 }
 

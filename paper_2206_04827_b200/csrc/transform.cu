@@ -256,6 +256,206 @@ __global__ void theta_cross_kernel(ThetaCross t) {
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// p = 256 fast path: the same fused stage with register FFTs (256 = 16 x 16, two radix-16
+// passes, one shared-memory transpose each) instead of eight shared-memory radix-2 stages.
+// CTA = 8 points (4 z positions x {+z, -z}) of one r row, 8 half-warp groups of 16 threads;
+// each group runs one 256-point FFT at a time (16 values per thread). The cross product is
+// fused into the first pass of the forward transforms.
+namespace {
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
+// radix-4 butterfly with W4 = e^{S i pi / 2}
+template <int S>
+__device__ __forceinline__ void r4(double2& a0, double2& a1, double2& a2, double2& a3) {
+    const double2 t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3), t3 = csub(a1, a3);
+    const double2 u = S > 0 ? make_double2(-t3.y, t3.x) : make_double2(t3.y, -t3.x);  // S i t3
+    a0 = cadd(t0, t2);
+    a1 = cadd(t1, u);
+    a2 = csub(t0, t2);
+    a3 = csub(t1, u);
+}
+
+// x * W16^e, W16 = e^{S 2 pi i / 16}, e in {1, 2, 3, 4, 6, 9} (compile-time after unrolling)
+template <int S>
+__device__ __forceinline__ double2 tw16(double2 x, int e) {
+    constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, c2 = 0.70710678118654752440;
+    switch (e) {
+        case 1: return cmul(x, make_double2(c1, S * s1));
+        case 2: return cmul(x, make_double2(c2, S * c2));
+        case 3: return cmul(x, make_double2(s1, S * c1));
+        case 4: return S > 0 ? make_double2(-x.y, x.x) : make_double2(x.y, -x.x);
+        case 6: return cmul(x, make_double2(-c2, S * c2));
+        case 9: return cmul(x, make_double2(-c1, -S * s1));
+        default: return x;
+    }
+}
+
+// in-place 16-point DFT X[k] = sum_n x[n] e^{S 2 pi i n k / 16}; X[k1 + 4 k2] lands in v[4 k1 + k2]
+template <int S>
+__device__ __forceinline__ void dft16(double2 (&v)[16]) {
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) r4<S>(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);
+#pragma unroll
+    for (int n2 = 1; n2 < 4; ++n2)
+#pragma unroll
+        for (int k1 = 1; k1 < 4; ++k1) v[n2 + 4 * k1] = tw16<S>(v[n2 + 4 * k1], n2 * k1);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) r4<S>(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+}
+__device__ __forceinline__ int d16(int k) { return 4 * (k & 3) + (k >> 2); }  // slot of X[k] after dft16
+
+constexpr int kT256Pts = 8;    // points per CTA
+constexpr int kT256Arr = 272;  // complex slots per array (16 x 17 transposed layout)
+
+// pass 1 of a 256-point DFT on Z (natural order): DFT over n1 of x[16 n1 + lane], twiddle,
+// store transposed T[k1 * 17 + lane]. twf[x] = e^{-2 pi i x / 256}.
+template <int S>
+__device__ __forceinline__ void f256_pass1(double2 (&v)[16], double2* Z, int lane, const double2* twf) {
+    dft16<S>(v);
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) {
+        double2 w = twf[lane * k1];
+        if (S > 0) w.y = -w.y;
+        Z[k1 * 17 + lane] = k1 == 0 ? v[d16(k1)] : cmul(v[d16(k1)], w);
+    }
+}
+// pass 2: DFT over n2 of T[lane * 17 + n2] -> X[lane + 16 k2], stored in natural order.
+template <int S>
+__device__ __forceinline__ void f256_pass2(double2* Z, int lane, unsigned gmask) {
+    double2 v[16];
+#pragma unroll
+    for (int n2 = 0; n2 < 16; ++n2) v[n2] = Z[lane * 17 + n2];
+    __syncwarp(gmask);
+    dft16<S>(v);
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) Z[lane + 16 * k2] = v[d16(k2)];
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(128, 2) theta_cross256_kernel(ThetaCross t) {
+    extern __shared__ double2 sd[];
+    double2* twf = sd + kT256Pts * 3 * kT256Arr;
+    const Geo& g = t.g;
+    const int S = g.nslots;  // 129
+    const int jr = blockIdx.y;
+    const int i0 = blockIdx.x * 4;
+    const int npos = min(4, g.nh - i0);
+    const int tid = threadIdx.x;
+    for (int x = tid; x < 256; x += blockDim.x)
+        twf[x] = x < 128 ? t.tw[x] : make_double2(-t.tw[x - 128].x, -t.tw[x - 128].y);
+    // ---- gather the Hermitian spectra of the pairs (v_r, v_t), (v_z, w_r), (w_t, w_z) at 8 points
+    const long ps = g.plane_stride, oo = g.nh;
+    for (int e = tid; e < S * 3; e += blockDim.x) {
+        const int s = e % S, pr = e / S;
+        const double sg = (s & 1) ? -1.0 : 1.0;  // (-1)^w (w = s, or -128 for the Nyquist slot s = 128)
+        const bool reonly = (s == 0 || s == 128);
+        const long off = long(s) * g.slot_stride + long(jr) * g.n + i0;
+        const double* fa = t.in[2 * pr] + off;
+        const double* fb = t.in[2 * pr + 1] + off;
+#pragma unroll
+        for (int ip = 0; ip < 4; ++ip) {
+            double ar = 0.0, ai = 0.0, aro = 0.0, aio = 0.0, br = 0.0, bi = 0.0, bro = 0.0, bio = 0.0;
+            if (ip < npos) {
+                ar = fa[ip];
+                ai = fa[ps + ip];
+                aro = fa[oo + ip];
+                aio = fa[oo + ps + ip];
+                br = fb[ip];
+                bi = fb[ps + ip];
+                bro = fb[oo + ip];
+                bio = fb[oo + ps + ip];
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double sz = h ? -1.0 : 1.0;
+                const double xar = sg * fma(sz, aro, ar), xai = reonly ? 0.0 : sg * fma(sz, aio, ai);
+                const double xbr = sg * fma(sz, bro, br), xbi = reonly ? 0.0 : sg * fma(sz, bio, bi);
+                double2* Z = sd + ((2 * ip + h) * 3 + pr) * kT256Arr;
+                Z[s] = make_double2(xar - xbi, xai + xbr);
+                if (s > 0 && s < 128) Z[256 - s] = make_double2(xar + xbi, xbr - xai);
+            }
+        }
+    }
+    __syncthreads();
+    const int grp = tid >> 4, lane = tid & 15;
+    const unsigned gmask = 0xFFFFu << (16 * (grp & 1));
+    // ---- inverse transforms (synthesis in theta): 24 arrays, 8 groups
+    for (int a = grp; a < kT256Pts * 3; a += 8) {
+        double2* Z = sd + a * kT256Arr;
+        double2 v[16];
+#pragma unroll
+        for (int n1 = 0; n1 < 16; ++n1) v[n1] = Z[16 * n1 + lane];
+        __syncwarp(gmask);
+        f256_pass1<+1>(v, Z, lane, twf);
+        __syncwarp(gmask);
+        f256_pass2<+1>(Z, lane, gmask);
+        __syncwarp(gmask);
+    }
+    __syncthreads();
+    // ---- cross product a = v x w (ptns.cpp:127-132) fused into pass 1 of the forward transforms
+    {
+        const int pt = grp;
+        double2* Z0 = sd + (pt * 3 + 0) * kT256Arr;
+        double2* Z1 = sd + (pt * 3 + 1) * kT256Arr;
+        const double2* Z2 = sd + (pt * 3 + 2) * kT256Arr;
+        double2 v[16], u[16];
+#pragma unroll
+        for (int n1 = 0; n1 < 16; ++n1) {
+            const int l = 16 * n1 + lane;
+            const double2 p0 = Z0[l], p1 = Z1[l], p2 = Z2[l];
+            const double vr = p0.x, vt = p0.y, vz = p1.x, wr = p1.y, wt = p2.x, wz = p2.y;
+            v[n1] = make_double2(vt * wz - vz * wt, vz * wr - vr * wz);  // a_r + i a_t
+            u[n1] = make_double2(vr * wt - vt * wr, 0.0);               // a_z
+        }
+        __syncwarp(gmask);
+        f256_pass1<-1>(v, Z0, lane, twf);
+        f256_pass1<-1>(u, Z1, lane, twf);
+        __syncwarp(gmask);
+        f256_pass2<-1>(Z0, lane, gmask);
+        f256_pass2<-1>(Z1, lane, gmask);
+    }
+    __syncthreads();
+    // ---- unpack c_w = (-1)^w X[w mod 256] / 256 per point; store E' = (f+ + f-)/2, O' = (f+ - f-)/2
+    for (int e = tid; e < S * 3; e += blockDim.x) {
+        const int s = e % S, f = e / S;
+        const int tt = s, tm = (256 - s) & 255;
+        const double sg = ((s & 1) ? -1.0 : 1.0) * (0.5 / 256.0);
+        const int arr = f < 2 ? 0 : 1;
+        const long off = long(s) * g.slot_stride + long(jr) * g.n + i0;
+        double* o = t.out[f] + off;
+#pragma unroll
+        for (int ip = 0; ip < 4; ++ip) {
+            if (ip >= npos) break;
+            double xr[2], xi[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double2* base = sd + ((2 * ip + h) * 3 + arr) * kT256Arr;
+                const double2 zt = base[tt], zm = base[tm];
+                if (f == 1) {
+                    xr[h] = 0.5 * (zt.y + zm.y);
+                    xi[h] = -0.5 * (zt.x - zm.x);
+                } else {
+                    xr[h] = 0.5 * (zt.x + zm.x);
+                    xi[h] = 0.5 * (zt.y - zm.y);
+                }
+            }
+            o[ip] = sg * (xr[0] + xr[1]);
+            o[oo + ip] = sg * (xr[0] - xr[1]);
+            o[ps + ip] = sg * (xi[0] + xi[1]);
+            o[ps + oo + ip] = sg * (xi[0] - xi[1]);
+        }
+    }
+}
+
+size_t theta_cross256_smem() { return (size_t(kT256Pts) * 3 * kT256Arr + 256) * sizeof(double2); }
+
 // Full-spectrum complex theta DFT for the API transforms (any even p):
 // data [l][k][j] complex interleaved; dir = +1 synthesis (c -> values), -1 analysis.
 __global__ void theta_dft_full_kernel(const double* __restrict__ in, double* __restrict__ out, int m, int n, int p,

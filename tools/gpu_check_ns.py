@@ -8,7 +8,7 @@ from oracle import pyoracle as O
 def report(name, got, ref):
     print(f"  {name:28s} rel_err {rel_err(got, ref):.3e}  (|ref| {np.max(np.abs(ref)):.2e})", flush=True)
 
-for (m, n, p) in [(8, 8, 8), (16, 12, 8), (16, 16, 16), (32, 32, 32)]:
+for (m, n, p) in [(8, 8, 8), (16, 12, 8), (16, 16, 16), (32, 32, 32), (16, 16, 256), (32, 24, 256)]:
     print(f"== {m}x{n}x{p}", flush=True)
     ctx = P.Context(m, n, p)
     lam = hermitian_coeffs(m, n, p, 0.7, 1)

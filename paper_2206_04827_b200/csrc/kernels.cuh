@@ -51,6 +51,7 @@ struct GemmBatch {
     int M, N, K;
     long lda, ldb, ldc;
     double alpha, beta;
+    const int* tstart;  // optional: batch b sums the terms [tstart[b], tstart[b+1]) (A, B indexed by term)
 };
 __global__ void dgemm_batched_kernel(GemmBatch g);
 struct ThetaCross {

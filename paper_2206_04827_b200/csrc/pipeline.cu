@@ -1,4 +1,5 @@
 // NS time-step pipeline (see pipeline.hpp).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -55,6 +56,8 @@ TransformPlan::TransformPlan(Ctx& c) {
         }
         upload(SrT[j0], S);
         upload(ArT[j0], A);
+        rt.SrT[j0] = S;
+        rt.ArT[j0] = A;
     }
     // z: values are kept z-parity split per r row, [E | O] with E_i / O_i the even- / odd-k parts at
     // z_{nh+i} > 0 (f(+-z_{nh+i}) = E_i +- O_i), so each z transform is two nh x nh products:
@@ -132,6 +135,7 @@ TransformPlan::TransformPlan(Ctx& c) {
             qv[size_t(i)] = double(eps / (long double)L * acc);
         }
         upload(q, qv);
+        rt.q = qv;
     }
     // theta twiddles
     {
@@ -180,29 +184,83 @@ TransformPlan::TransformPlan(Ctx& c) {
         }
         upload(hpc, hc);
         upload(hpr, hr);
+        rt.hpc = hc;
+        rt.hpr = hr;
+        rt.m = m;
+        rt.mh = mh;
+        rt.M = M;
+        rt.p = p;
+        rt.nslots = g.nslots;
+    }
+    // derivative_z (calculus.cpp:34-43) folded into the z transforms of the nonlinear term:
+    //   (dz c)_k = sum_{k' > k, k' - k odd} 2 k' c_k' (halved for k = 0), maps parity par -> 1 - par;
+    //   DzS[po][q'][i] = sum_{k = 2q + po} Dz[k][2q' + 1 - po] T_k(z_{nh+i})
+    //   ADz[po][i][q]  = sum_{q'} Az_{1-po}[i][q'] Dz[2q + po][2q' + 1 - po]
+    {
+        const int nh = n / 2;
+        auto dzm = [&](int k, int kp) -> long double {
+            if (kp <= k || ((kp - k) & 1) == 0) return 0.0L;
+            return (k == 0 ? 1.0L : 2.0L) * (long double)kp;
+        };
+        auto zan = [&](int k, int kz) {
+            const int s = n - 1 - kz;
+            const long double eps = (k == 0 || k == n - 1) ? 0.5L : 1.0L;
+            const long double ws = (s == 0 || s == n - 1) ? 1.0L : 2.0L;
+            return eps / (long double)Lz * ws * cospi_frac(long(k) * s, Lz);
+        };
+        std::vector<double> DS(size_t(n) * nh, 0.0), AD(size_t(n) * nh, 0.0);
+        for (int po = 0; po < 2; ++po) {
+            const int pi = 1 - po;
+            for (int qp = 0; qp < nh; ++qp)
+                for (int i = 0; i < nh; ++i) {
+                    long double acc = 0.0L;
+                    for (int q = 0; q < nh; ++q) {
+                        const int k = 2 * q + po;
+                        const long double d = dzm(k, 2 * qp + pi);
+                        if (d != 0.0L) acc += d * cospi_frac(long(k) * (n - 1 - (nh + i)), Lz);
+                    }
+                    DS[size_t(po) * nh * nh + size_t(qp) * nh + i] = double(acc);
+                }
+            for (int i = 0; i < nh; ++i)
+                for (int q = 0; q < nh; ++q) {
+                    long double acc = 0.0L;
+                    for (int qp = 0; qp < nh; ++qp) {
+                        const long double d = dzm(2 * q + po, 2 * qp + pi);
+                        if (d != 0.0L) acc += 2.0L * zan(2 * qp + pi, nh + i) * d;
+                    }
+                    AD[size_t(po) * nh * nh + size_t(i) * nh + q] = double(acc);
+                }
+        }
+        upload(DzS, DS);
+        upload(ADz, AD);
     }
 }
 
 // ---------------------------------------------------------------- GEMM plans
 void GemmPlan::upload() {
-    const size_t nb = C.size();
+    const size_t nb = C.size(), na = A.size();
     if (!dA) {
-        CCF_CUDA(cudaMalloc(&dA, nb * sizeof(void*)));
-        CCF_CUDA(cudaMalloc(&dB, nb * sizeof(void*)));
+        CCF_CUDA(cudaMalloc(&dA, std::max<size_t>(na, 1) * sizeof(void*)));
+        CCF_CUDA(cudaMalloc(&dB, std::max<size_t>(na, 1) * sizeof(void*)));
         CCF_CUDA(cudaMalloc(&dC, nb * sizeof(void*)));
+        if (!tstart.empty()) CCF_CUDA(cudaMalloc(&dT, tstart.size() * sizeof(int)));
     }
-    CCF_CUDA(cudaMemcpy(dA, A.data(), nb * sizeof(void*), cudaMemcpyHostToDevice));
-    CCF_CUDA(cudaMemcpy(dB, B.data(), nb * sizeof(void*), cudaMemcpyHostToDevice));
+    if (na) {
+        CCF_CUDA(cudaMemcpy(dA, A.data(), na * sizeof(void*), cudaMemcpyHostToDevice));
+        CCF_CUDA(cudaMemcpy(dB, B.data(), na * sizeof(void*), cudaMemcpyHostToDevice));
+    }
     CCF_CUDA(cudaMemcpy(dC, C.data(), nb * sizeof(void*), cudaMemcpyHostToDevice));
+    if (!tstart.empty()) CCF_CUDA(cudaMemcpy(dT, tstart.data(), tstart.size() * sizeof(int), cudaMemcpyHostToDevice));
 }
 
 void GemmPlan::launch(cudaStream_t s) const {
-    GemmBatch g{dA, dB, dC, M, N, K, lda, ldb, ldc, alpha, beta};
+    GemmBatch g{dA, dB, dC, M, N, K, lda, ldb, ldc, alpha, beta, dT};
     const dim3 grid(unsigned((N + 63) / 64), unsigned((M + 63) / 64), unsigned(C.size()));
     dgemm_batched_kernel<<<grid, 128, 0, s>>>(g);
 }
 
 GemmPlan::~GemmPlan() {
+    if (dT) cudaFree(dT);
     if (dA) cudaFree(dA);
     if (dB) cudaFree(dB);
     if (dC) cudaFree(dC);
@@ -433,8 +491,159 @@ void Pipeline::curl_decompose(const double* ar, const double* at, const double* 
     ++c.launches;
 }
 
+void Pipeline::ensure_composite() {
+    if (comp_ready_) return;
+    const char* e = std::getenv("CCF_NONLINEAR_PENCIL");
+    comp_off_ = e && e[0] == '1';
+    if (!comp_off_) {
+        synth_ = build_synth_composite(tp.rt);
+        anal_ = build_anal_composite(tp.rt);
+        upload(dsynth_, synth_.blocks);
+        upload(danal_, anal_.blocks);
+    }
+    comp_ready_ = true;
+}
+
+// Nonlinear term N = curl(v x w) in PT form (proj/src/ptns.cpp:114-149) with every radial step on
+// the tensor cores:
+//   Z  = z synthesis of (lambda, gamma, dz gamma) of the v and w PT pairs      (DMMA, nh x nh halves)
+//   V  = per-slot composite r operators: (r-values of v_r, v_t, v_z, w_r, w_t, w_z) = sum_t C_t Z_t
+//   a  = v x w pointwise in theta (register FFTs)
+//   Y  = z analysis of (a_r, a_t, a_z, dz a_r, dz a_t)
+//   (gamma_N, lambda_N) = per-slot composite r operators (curl + decompose + r analysis) on Y
 void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w,
                          double* lam_n, double* gam_n) {
+    ensure_composite();
+    if (comp_off_) {
+        nonlinear_pencil(lam_v, gam_v, lam_w, gam_w, lam_n, gam_n);
+        return;
+    }
+    const Geo& g = c.gh;
+    const double* lam[2] = {lam_v, lam_w};
+    const double* gam[2] = {gam_v, gam_w};
+    double* Z[2][3];
+    for (int pr = 0; pr < 2; ++pr)
+        for (int x = 0; x < 3; ++x) Z[pr][x] = scratch(3 * pr + x);
+    double* val[6];
+    for (int i = 0; i < 6; ++i) val[i] = scratch(6 + i);
+    double* av[3] = {scratch(12), scratch(13), scratch(14)};
+    double* Y[5];
+    for (int i = 0; i < 5; ++i) Y[i] = scratch(15 + i);
+    const void* keyp[8] = {lam_v, gam_v, lam_w, gam_w, lam_n, gam_n, nullptr, nullptr};
+    const int cls0[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bool fresh;
+    // ---- z synthesis: 6 tensors, two nh x nh halves per (slot, plane)
+    GemmPlan& zs = gemm(ptr_key("nzs", 6, keyp, keyp, cls0), fresh);
+    if (fresh) {
+        for (int pr = 0; pr < 2; ++pr)
+            for (int x = 0; x < 3; ++x) {
+                const double* src = x == 0 ? lam[pr] : gam[pr];
+                const double* mat = x == 2 ? tp.DzS.p : tp.Sz.p;
+                for (int s = 0; s < g.nslots; ++s)
+                    for (int pl = 0; pl < 2; ++pl) {
+                        const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
+                        for (int po = 0; po < 2; ++po) {
+                            const int pi = x == 2 ? 1 - po : po;
+                            zs.A.push_back(src + off + pi * g.nh);
+                            zs.B.push_back(mat + size_t(po) * g.nh * g.nh);
+                            zs.C.push_back(Z[pr][x] + off + po * g.nh);
+                        }
+                    }
+            }
+        zs.M = g.mh;
+        zs.N = g.nh;
+        zs.K = g.nh;
+        zs.lda = g.n;
+        zs.ldb = g.nh;
+        zs.ldc = g.n;
+        zs.upload();
+    }
+    zs.launch(c.stream);
+    // ---- composite r synthesis -> (r, z)-values of the 6 velocity / vorticity components
+    GemmPlan& rs = gemm(ptr_key("nrs", 6, keyp, keyp, cls0), fresh);
+    if (fresh) {
+        for (int pr = 0; pr < 2; ++pr)
+            for (int s = 0; s < g.nslots; ++s)
+                for (int o = 0; o < 6; ++o) {
+                    rs.tstart.push_back(int(rs.A.size()));
+                    for (const CompositeTerm& ct : synth_.terms[size_t(s)]) {
+                        if (ct.out != o) continue;
+                        rs.A.push_back(dsynth_.p + ct.off);
+                        rs.B.push_back(Z[pr][ct.in / 2] + long(s) * g.slot_stride + long(ct.in % 2) * g.plane_stride);
+                    }
+                    rs.C.push_back(val[3 * pr + o / 2] + long(s) * g.slot_stride + long(o % 2) * g.plane_stride);
+                }
+        rs.tstart.push_back(int(rs.A.size()));
+        rs.M = g.mh;
+        rs.N = g.n;
+        rs.K = g.mh;
+        rs.lda = g.mh;
+        rs.ldb = g.n;
+        rs.ldc = g.n;
+        rs.upload();
+    }
+    rs.launch(c.stream);
+    c.launches += 2;
+    c.mark("X1_rz_synthesis");
+    theta_cross(val, av);
+    c.mark("X2_theta_cross");
+    // ---- z analysis of a_r, a_t, a_z and (derivative_z folded in) dz a_r, dz a_t
+    GemmPlan& za = gemm(ptr_key("nza", 6, keyp, keyp, cls0), fresh);
+    if (fresh) {
+        for (int x = 0; x < 5; ++x) {
+            const double* src = av[x < 3 ? x : x - 3];
+            const double* mat = x >= 3 ? tp.ADz.p : tp.Az.p;
+            for (int s = 0; s < g.nslots; ++s)
+                for (int pl = 0; pl < 2; ++pl) {
+                    const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
+                    for (int po = 0; po < 2; ++po) {
+                        const int pi = x >= 3 ? 1 - po : po;
+                        za.A.push_back(src + off + pi * g.nh);
+                        za.B.push_back(mat + size_t(po) * g.nh * g.nh);
+                        za.C.push_back(Y[x] + off + po * g.nh);
+                    }
+                }
+        }
+        za.M = g.mh;
+        za.N = g.nh;
+        za.K = g.nh;
+        za.lda = g.n;
+        za.ldb = g.nh;
+        za.ldc = g.n;
+        za.upload();
+    }
+    za.launch(c.stream);
+    c.launches += 1;
+    c.mark("X3_rz_analysis");
+    // ---- composite curl + pt_decompose + r analysis -> (gamma_N, lambda_N)
+    GemmPlan& ra = gemm(ptr_key("nra", 6, keyp, keyp, cls0), fresh);
+    if (fresh) {
+        for (int s = 0; s < g.nslots; ++s)
+            for (int o = 0; o < 4; ++o) {
+                ra.tstart.push_back(int(ra.A.size()));
+                for (const CompositeTerm& ct : anal_.terms[size_t(s)]) {
+                    if (ct.out != o) continue;
+                    ra.A.push_back(danal_.p + ct.off);
+                    ra.B.push_back(Y[ct.in / 2] + long(s) * g.slot_stride + long(ct.in % 2) * g.plane_stride);
+                }
+                ra.C.push_back((o < 2 ? gam_n : lam_n) + long(s) * g.slot_stride + long(o % 2) * g.plane_stride);
+            }
+        ra.tstart.push_back(int(ra.A.size()));
+        ra.M = g.mh;
+        ra.N = g.n;
+        ra.K = g.mh;
+        ra.lda = g.mh;
+        ra.ldb = g.n;
+        ra.ldc = g.n;
+        ra.upload();
+    }
+    ra.launch(c.stream);
+    c.launches += 1;
+    c.mark("C_curl_decompose");
+}
+
+void Pipeline::nonlinear_pencil(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w,
+                                double* lam_n, double* gam_n) {
     // proj/src/ptns.cpp:114-149
     double* comp[6];
     for (int i = 0; i < 6; ++i) comp[i] = scratch(i);

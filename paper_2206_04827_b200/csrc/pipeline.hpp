@@ -13,6 +13,7 @@
 
 #include <vector>
 
+#include "composite.hpp"
 #include "context.hpp"
 
 namespace ccf {
@@ -27,17 +28,21 @@ struct TransformPlan {
     DBuf tw;              // p/2 complex twiddles exp(-2 pi i q / p)
     DBuf twfull;          // p complex twiddles (naive DFT path)
     DBuf hpc, hpr;        // horizontal-Poisson LU per half slot; R R C02 per parity
+    DBuf DzS, ADz;        // [2][nh x nh] z synthesis of dz f / dz of the z analysis (derivative_z folded in)
+    RadialTables rt;      // host copies for the composite radial operators (composite.hpp)
     int logp = -1;        // log2 p, or -1 if p is not a power of two
     explicit TransformPlan(Ctx& c);
 };
 
 // Reusable batched-GEMM launcher with device pointer arrays.
 struct GemmPlan {
-    std::vector<const double*> A, B;
-    std::vector<double*> C;
+    std::vector<const double*> A, B;  // per term (= per batch unless tstart is set)
+    std::vector<double*> C;           // per batch
+    std::vector<int> tstart;          // optional: batch b sums terms [tstart[b], tstart[b+1])
     const double** dA = nullptr;
     const double** dB = nullptr;
     double** dC = nullptr;
+    int* dT = nullptr;
     int M = 0, N = 0, K = 0;
     long lda = 0, ldb = 0, ldc = 0;
     double alpha = 1.0, beta = 0.0;
@@ -84,6 +89,13 @@ private:
     bool theta_attr_ = false, theta_generic_ = false;  // CCF_THETA_GENERIC=1 forces the radix-2 path
     std::map<std::string, std::unique_ptr<GemmPlan>> gemms_;
     GemmPlan& gemm(const std::string& key, bool& fresh);
+    // composite radial operators of the nonlinear term (built on first use)
+    bool comp_ready_ = false, comp_off_ = false;  // CCF_NONLINEAR_PENCIL=1: sequential pencil path
+    CompositeSet synth_, anal_;
+    DBuf dsynth_, danal_;
+    void ensure_composite();
+    void nonlinear_pencil(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w,
+                          double* lam_n, double* gam_n);
 };
 
 struct NSState {

@@ -32,8 +32,11 @@ __global__ void __launch_bounds__(128) dgemm_batched_kernel(GemmBatch g) {
     __shared__ double As[2][BM * SA];
     __shared__ double Bs[2][BK * SB];
     const int b = blockIdx.z;
-    const double* __restrict__ A = g.A[b];
-    const double* __restrict__ B = g.B[b];
+    int t0 = b, t1 = b + 1;  // terms of this batch: C[b] = alpha * sum_t A[t] B[t] + beta C[b]
+    if (g.tstart) {
+        t0 = g.tstart[b];
+        t1 = g.tstart[b + 1];
+    }
     double* __restrict__ C = g.C[b];
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -45,8 +48,12 @@ __global__ void __launch_bounds__(128) dgemm_batched_kernel(GemmBatch g) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+    const int nkt = (g.K + BK - 1) / BK;  // k tiles per term
     double ra[8], rb[8];
-    auto gload = [&](int k0) {
+    auto gload = [&](int it) {
+        const int term = t0 + it / nkt, k0 = (it % nkt) * BK;
+        const double* __restrict__ A = g.A[term];
+        const double* __restrict__ B = g.B[term];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const int e = tid + q * 128;  // 0..1023
@@ -66,13 +73,15 @@ __global__ void __launch_bounds__(128) dgemm_batched_kernel(GemmBatch g) {
             Bs[buf][(e >> 6) * SB + (e & 63)] = rb[q];
         }
     };
-    const int nk = (g.K + BK - 1) / BK;
-    gload(0);
-    sstore(0);
+    const int nk = (t1 - t0) * nkt;
+    if (nk > 0) {
+        gload(0);
+        sstore(0);
+    }
     __syncthreads();
     for (int kt = 0; kt < nk; ++kt) {
         const int buf = kt & 1;
-        if (kt + 1 < nk) gload((kt + 1) * BK);
+        if (kt + 1 < nk) gload(kt + 1);
 #pragma unroll
         for (int ks = 0; ks < BK; ks += 4) {
             double af[4], bf[4];
@@ -314,13 +323,14 @@ constexpr int kT256Pts = 8;    // points per CTA
 constexpr int kT256Arr = 272;  // complex slots per array (16 x 17 transposed layout)
 
 // pass 1 of a 256-point DFT on Z (natural order): DFT over n1 of x[16 n1 + lane], twiddle,
-// store transposed T[k1 * 17 + lane]. twf[x] = e^{-2 pi i x / 256}.
+// store transposed T[k1 * 17 + lane]. twf[16 k1 + lane] = e^{-2 pi i lane k1 / 256} (lane-fastest:
+// conflict-free shared loads).
 template <int S>
 __device__ __forceinline__ void f256_pass1(double2 (&v)[16], double2* Z, int lane, const double2* twf) {
     dft16<S>(v);
 #pragma unroll
     for (int k1 = 0; k1 < 16; ++k1) {
-        double2 w = twf[lane * k1];
+        double2 w = twf[16 * k1 + lane];
         if (S > 0) w.y = -w.y;
         Z[k1 * 17 + lane] = k1 == 0 ? v[d16(k1)] : cmul(v[d16(k1)], w);
     }
@@ -348,8 +358,10 @@ __global__ void __launch_bounds__(128, 2) theta_cross256_kernel(ThetaCross t) {
     const int i0 = blockIdx.x * 4;
     const int npos = min(4, g.nh - i0);
     const int tid = threadIdx.x;
-    for (int x = tid; x < 256; x += blockDim.x)
-        twf[x] = x < 128 ? t.tw[x] : make_double2(-t.tw[x - 128].x, -t.tw[x - 128].y);
+    for (int x = tid; x < 256; x += blockDim.x) {
+        const int e = (x >> 4) * (x & 15);  // k1 * lane < 256
+        twf[x] = e < 128 ? t.tw[e] : make_double2(-t.tw[e - 128].x, -t.tw[e - 128].y);
+    }
     // ---- gather the Hermitian spectra of the pairs (v_r, v_t), (v_z, w_r), (w_t, w_z) at 8 points
     const long ps = g.plane_stride, oo = g.nh;
     for (int e = tid; e < S * 3; e += blockDim.x) {

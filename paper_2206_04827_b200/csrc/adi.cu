@@ -639,6 +639,85 @@ __device__ __forceinline__ double row_mul_split(double* __restrict__ Y, int pitc
     return sq;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Once-per-round passes, thread per column b (coalesced global access, coefficients of the right
+// operators in registers), rows split between the line sets when 2 x lanes threads run. Both are
+// read-only on the tile (sliding windows along the rows), so no halo exchange is needed.
+
+// E = (R2 f C02^T) restricted to M x N -> escr (rows >= M zero); returns the thread's sum of E^2.
+// f: rows [0, mh) x columns [0, nh) of the tile; sleft fields 0..5 = R2 (d = -2..3), sright 0..3 = C02.
+__device__ __forceinline__ double prologue_E(const double* __restrict__ Y, int pitch, int M, int N, int Mpad,
+                                            const double* __restrict__ sleft, const double* __restrict__ sright,
+                                            double* __restrict__ escr, int r0, int r1, int b) {
+    const double2 c01 = ld2(sright + b * kStatW), c23 = ld2(sright + b * kStatW + 2);
+    const double* col = Y + b;
+    const bool left = b > 0;
+    auto H = [&](int i) -> double {  // (f C02^T)[i][b]
+        if (i < 0) return 0.0;
+        const double* r = col + i * pitch;
+        return fma(c01.x, left ? r[-1] : 0.0, c01.y * r[0]) + fma(c23.x, r[1], c23.y * r[2]);
+    };
+    double h0 = H(r0 - 2), h1 = H(r0 - 1), h2 = H(r0), h3 = H(r0 + 1), h4 = H(r0 + 2);
+    double esq = 0.0;
+    for (int a = r0; a < r1; ++a) {
+        const double h5 = H(a + 3);
+        const double* c = sleft + a * kStatW;
+        const double2 r01 = ld2(c), r23 = ld2(c + 2), r45 = ld2(c + 4);
+        const double e = (fma(r01.x, h0, r01.y * h1) + fma(r23.x, h2, r23.y * h3)) + fma(r45.x, h4, r45.y * h5);
+        escr[a * N + b] = e;
+        esq = fma(e, e, esq);
+        h0 = h1;
+        h1 = h2;
+        h2 = h3;
+        h3 = h4;
+        h4 = h5;
+    }
+    return esq;
+}
+
+// Residual of the Sylvester equation R = A X B + C X D - E (adi.cpp:106-112) as A (X B) + C (X D) - E;
+// returns the thread's sum of R^2 over rows [r0, r1) of column b.
+__device__ __forceinline__ double residual_col(const double* __restrict__ Y, int pitch, int N,
+                                              const double* __restrict__ sleft, const double* __restrict__ sright,
+                                              const double* __restrict__ escr, int r0, int r1, int b) {
+    const double* cb = sright + b * kStatW;
+    const double2 b01 = ld2(cb + 12), b23 = ld2(cb + 14), d01 = ld2(cb + 16), d23 = ld2(cb + 18);
+    const double* col = Y + b;
+    const bool left = b > 0;
+    double xb[6], xd[6];
+    auto XBD = [&](int i, double& ob, double& od) {
+        if (i < 0) {
+            ob = od = 0.0;
+            return;
+        }
+        const double* r = col + i * pitch;
+        const double xm = left ? r[-1] : 0.0, x0 = r[0], x1 = r[1], x2 = r[2];
+        ob = fma(b01.x, xm, b01.y * x0) + fma(b23.x, x1, b23.y * x2);
+        od = fma(d01.x, xm, d01.y * x0) + fma(d23.x, x1, d23.y * x2);
+    };
+#pragma unroll
+    for (int d = 0; d < 5; ++d) XBD(r0 - 2 + d, xb[d], xd[d]);
+    double rsq = 0.0;
+    for (int a = r0; a < r1; ++a) {
+        XBD(a + 3, xb[5], xd[5]);
+        const double* c = sleft + a * kStatW;
+        const double2 a01 = ld2(c + 6), a23 = ld2(c + 8), a45 = ld2(c + 10);
+        const double2 e01 = ld2(c + 12), e23 = ld2(c + 14), e45 = ld2(c + 16);
+        const double ra = (fma(a01.x, xb[0], a01.y * xb[1]) + fma(a23.x, xb[2], a23.y * xb[3])) +
+                          fma(a45.x, xb[4], a45.y * xb[5]);
+        const double rc = (fma(e01.x, xd[0], e01.y * xd[1]) + fma(e23.x, xd[2], e23.y * xd[3])) +
+                          fma(e45.x, xd[4], e45.y * xd[5]);
+        const double r = (ra + rc) - escr[a * N + b];
+        rsq = fma(r, r, rsq);
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+            xb[d] = xb[d + 1];
+            xd[d] = xd[d + 1];
+        }
+    }
+    return rsq;
+}
+
 }  // namespace
 
 // Shared-memory tile: rows [0, Mpad+6) x pitch (pitch >= nh+3, odd), followed by the
@@ -671,7 +750,6 @@ __device__ __forceinline__ void adi_body(const AdiParams& P, const AdiTask& task
     double* bufE = bufR + long(rrows) * kRightW;
     double* xch = bufE + (split_mul ? 6L : 3L) * kChunk * N;
     const long toff = long(s) * g.slot_stride + long(plane) * g.plane_stride;
-    double* ep = P.eprime + long(blockIdx.x) * P.estride;
     const double* sleft = P.coef + so.sleft;
     const double* sright = P.coef + (k0 ? so.sright1 : so.sright0);
 
@@ -680,31 +758,46 @@ __device__ __forceinline__ void adi_body(const AdiParams& P, const AdiTask& task
     __syncthreads();
     {
         const int ns = P.nsrc[t];
-        for (int i = tid; i < mh * nh; i += nt) {  // rows jj = a: contiguous half-rows of this k-parity
-            const int a = i / nh, b = i - a * nh;
-            const long off = toff + long(a) * g.n + long(k0) * nh + b;
-            double acc = 0.0;
-            for (int q = 0; q < ns; ++q) acc = fma(P.wsrc[t][q], __ldg(P.src[t][q] + off), acc);
-            Y[a * pitch + b] = acc;
+        const double* const* src = P.src[t];
+        const double* wv = P.wsrc[t];
+        constexpr int U = 4;  // independent rows in flight per thread
+        for (int i0 = tid; i0 < mh * nh; i0 += U * nt) {
+            double acc[U];
+            long off[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * nt;
+                const int a = i / nh, b = i - a * nh;
+                off[u] = toff + long(a) * g.n + long(k0) * nh + b;
+                acc[u] = 0.0;
+            }
+            for (int q = 0; q < ns; ++q) {
+                const double* sq = src[q];
+                const double wq = wv[q];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (i0 + u * nt < mh * nh) acc[u] = fma(wq, __ldg(sq + off[u]), acc[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * nt;
+                if (i < mh * nh) {
+                    const int a = i / nh, b = i - a * nh;
+                    Y[a * pitch + b] = acc[u];
+                }
+            }
         }
     }
-    __syncthreads();
-    if (split_mul) col_mul_split(Y, pitch, M, nh, sleft, kStatW, 0, 0, nullptr, 0, hc, lanes);
-    else
-        for (int b = tid; b < nh; b += nt) col_mul(Y + b, pitch, M, sleft, kStatW, 0, nullptr, 0, 0.0, 0, nullptr, 0);
-    __syncthreads();
-    for (int b = tid; b < pitch; b += nt) Y[M * pitch + b] = 0.0;  // row M of F lies outside the truncated system
     __syncthreads();
     double esq = 0.0;
     double* escr = P.escr + long(blockIdx.x) * P.estride;  // E (top-left block of R2 f C02^T), rows padded to Mpad
     double* xscr = P.xscr + long(blockIdx.x) * P.estride;  // X of the previous round (restart)
-    if (split_mul) esq = row_mul_split<true>(Y, pitch, M, N, sright + 0, kStatW, hr, lanes);
-    else
-        for (int a = tid; a < M; a += nt) esq += row_mul<true>(Y + a * pitch, N, sright + 0, kStatW);
-    __syncthreads();
-    for (int i = tid; i < Mpad * N; i += nt) {
-        const int a = i / N, b = i - (i / N) * N;
-        escr[i] = a < M ? Y[a * pitch + b] : 0.0;
+    {
+        const int lh = split_mul ? (tid >= lanes ? 1 : 0) : 0;
+        const int b = split_mul ? tid - lh * lanes : tid;
+        const int r0 = split_mul ? (lh ? hc : 0) : 0, r1 = split_mul ? (lh ? M : hc) : M;
+        if (b < N) esq = prologue_E(Y, pitch, M, N, Mpad, sleft, sright, escr, r0, r1, b);
+        for (int i = M * N + tid; i < Mpad * N; i += nt) escr[i] = 0.0;
     }
     fence_proxy_async();  // E generic stores -> async-proxy (bulk copy) reads
     __syncthreads();
@@ -758,39 +851,13 @@ __device__ __forceinline__ void adi_body(const AdiParams& P, const AdiTask& task
     }
     for (int i = tid; i < M * N; i += nt) xscr[i] = Y[(i / N) * pitch + (i % N)];
     __syncthreads();
-    // ---- residual R = A X B + C X D - E (adi.cpp:106-112): P = A X (shared), Q = C X (scratch)
-    if (split_mul) col_mul_split(Y, pitch, M, N, sleft, kStatW, 6, 12, ep, N, hc, lanes);
-    else
-        for (int b = tid; b < N; b += nt) col_mul(Y + b, pitch, M, sleft, kStatW, 6, nullptr, 0, 0.0, 12, ep + b, N);
-    __syncthreads();
+    // ---- residual R = A X B + C X D - E (adi.cpp:106-112), read-only on the tile
     double rsq = 0.0;
     {
-        // thread per (row, column half) when split, else per row
-        const int half = split_mul && tid >= lanes ? 1 : 0;
-        const int a = split_mul ? tid - half * lanes : tid;
-        const int b0 = split_mul ? (half ? hr : 0) : 0, b1 = split_mul ? (half ? N : hr) : N;
-        for (int aa = a; aa < M; aa += (split_mul ? lanes * 2 : nt)) {
-            const double* prow = Y + aa * pitch;
-            const double* qrow = ep + long(aa) * N;
-            const double* erow = escr + long(aa) * N;
-            auto qv = [&](int b) { return (b >= 0 && b < N) ? qrow[b] : 0.0; };
-            double pm1 = b0 > 0 ? prow[b0 - 1] : 0.0, p0 = prow[b0], p1 = prow[b0 + 1], p2 = prow[b0 + 2];
-            double qm1 = qv(b0 - 1), q0 = qv(b0), q1 = qv(b0 + 1), q2 = qv(b0 + 2);
-            for (int b = b0; b < b1; ++b) {
-                const double* c = sright + b * kStatW;
-                const double r = ((fma(c[12], pm1, c[13] * p0) + fma(c[14], p1, c[15] * p2)) +
-                                  (fma(c[16], qm1, c[17] * q0) + fma(c[18], q1, c[19] * q2))) - erow[b];
-                rsq = fma(r, r, rsq);
-                pm1 = p0;
-                p0 = p1;
-                p1 = p2;
-                p2 = prow[b + 3];
-                qm1 = q0;
-                q0 = q1;
-                q1 = q2;
-                q2 = qv(b + 3);
-            }
-        }
+        const int lh = split_mul ? (tid >= lanes ? 1 : 0) : 0;
+        const int b = split_mul ? tid - lh * lanes : tid;
+        const int r0 = split_mul ? (lh ? hc : 0) : 0, r1 = split_mul ? (lh ? M : hc) : M;
+        if (b < N) rsq = residual_col(Y, pitch, N, sleft, sright, escr, r0, r1, b);
     }
     const double rs = block_sum(rsq, red);
     const double es = block_sum(esq, red);

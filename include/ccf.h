@@ -50,7 +50,11 @@ typedef struct ccf_ns_state ccf_ns_state;
  * bit 1 = execute the reference's ADI shift counts. By default the executed Zolotarev
  * plan is the one for adi_tol / 4 (1-2 more shifts per mode) so that slots finishing
  * just above adi_tol do not trigger a serial restart round; the per-round acceptance
- * test (relative residual <= adi_tol) and the restart logic are unchanged. */
+ * test (relative residual <= adi_tol) and the restart logic are unchanged;
+ * bit 2 = solve the modal Sylvester systems with the ADI kernel (the reference algorithm,
+ * adi.cpp:150-202). By default they are solved exactly by fast diagonalization (four batched
+ * FP64 tensor-core products per mode, eigenpairs refined in long double at setup): residual
+ * ~1e-15 relative, three orders below adi_tol. */
 ccf_status ccf_ctx_create(int m, int n, int p, int device, double adi_tol, int flags, ccf_ctx** out);
 ccf_status ccf_ctx_destroy(ccf_ctx* ctx);
 /* Use an external cudaStream_t (NULL restores the context's own stream). */

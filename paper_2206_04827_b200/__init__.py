@@ -157,11 +157,16 @@ def _c128(x):
 class Context:
     """One grid size on one GPU (ccf_ctx). Mirrors the reference free functions."""
 
-    def __init__(self, m, n, p, device=0, adi_tol=1e-12, q2_endpoint_pad=False):
+    def __init__(self, m, n, p, device=0, adi_tol=1e-12, q2_endpoint_pad=False, solver="diag",
+                 reference_shift_counts=False):
+        """solver: "diag" (fast diagonalization on the tensor cores, default) or "adi" (the
+        reference's ADI iteration, adi.cpp:150-202, as the on-chip ADI kernel)."""
+        if solver not in ("diag", "adi"):
+            raise ValueError("solver must be 'diag' or 'adi'")
         self.m, self.n, self.p = int(m), int(n), int(p)
+        flags = int(bool(q2_endpoint_pad)) | (2 if reference_shift_counts else 0) | (4 if solver == "adi" else 0)
         h = C.c_void_p()
-        st = lib().ccf_ctx_create(self.m, self.n, self.p, int(device), C.c_double(adi_tol),
-                                  int(bool(q2_endpoint_pad)), C.byref(h))
+        st = lib().ccf_ctx_create(self.m, self.n, self.p, int(device), C.c_double(adi_tol), flags, C.byref(h))
         if st != 0:
             raise _ERR.get(st, CCFError)(lib().ccf_create_error().decode())
         self.h = h

@@ -123,7 +123,7 @@ ccf_status ccf_poisson3d(ccf_ctx* ctx, const double* f, double* u) {
         ccf::DevSet& set = c.set(full, true, 1.0);
         const double* src[1] = {c.tens[0].p};
         const double w[1] = {1.0};
-        c.run_adi(set, full, 1, src, w, 1, nullptr, nullptr, 0, c.tens[1].p, nullptr);
+        ctx->pl().modal_solve(set, full, 1, src, w, 1, nullptr, nullptr, 0, c.tens[1].p, nullptr);
         c.check_adi_error(full);
         c.store_coeff(c.tens[1].p, u, full, 0, 0);
         c.sync();
@@ -159,7 +159,7 @@ ccf_status ccf_helmholtz_step(ccf_ctx* ctx, const double* const* hist, int nhist
         }
         ccf::DevSet& set = c.set(full, false, scale);
         double* o = c.tens[order + 1].p;
-        c.run_adi(set, full, 1, src, w, ns, nullptr, nullptr, 0, o, nullptr);
+        ctx->pl().modal_solve(set, full, 1, src, w, ns, nullptr, nullptr, 0, o, nullptr);
         c.check_adi_error(full);
         c.require_finite(o, nt, "HelmholtzTensorStepper");
         c.store_coeff(o, out, full, 0, 0);

@@ -32,6 +32,7 @@ DevSet::~DevSet() {
     if (coef) cudaFree(coef);
     if (slots) cudaFree(slots);
     if (J) cudaFree(J);
+    if (dg) cudaFree(dg);
     for (auto* t : tasks)
         if (t) cudaFree(t);
 }
@@ -146,9 +147,14 @@ DevSet& Ctx::set(bool full, bool poisson, double scale) {
     for (int s = 0; s < g.nslots; ++s) slot_w[size_t(s)] = full ? s - p / 2 : (s == p / 2 ? -p / 2 : s);
     auto ds = std::make_unique<DevSet>();
     // flags bit1: execute the reference's shift counts (no tail-avoidance margin)
+    // flags bit2: solve with the ADI kernel (the reference algorithm) instead of fast diagonalization
     ds->host = build_solver_set(*sizeops, slot_w, poisson, scale, tol, radial_cache, (flags & 1) != 0,
-                                (flags & 2) ? 1.0 : 4.0);
+                                (flags & 2) ? 1.0 : 4.0, (flags & 4) == 0);
     const SolverSet& h = ds->host;
+    if (h.has_diag) {
+        CCF_CUDA(cudaMalloc(&ds->dg, h.dg.size() * sizeof(double)));
+        CCF_CUDA(cudaMemcpy(ds->dg, h.dg.data(), h.dg.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
     CCF_CUDA(cudaMalloc(&ds->coef, h.coef.size() * sizeof(double)));
     CCF_CUDA(cudaMemcpy(ds->coef, h.coef.data(), h.coef.size() * sizeof(double), cudaMemcpyHostToDevice));
     CCF_CUDA(cudaMalloc(&ds->slots, h.slots.size() * sizeof(AdiSlot)));

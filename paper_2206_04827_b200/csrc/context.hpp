@@ -45,6 +45,7 @@ struct DevSet {
     int* J = nullptr;
     AdiTask* tasks[2] = {nullptr, nullptr};  // for 1 and 2 tensors
     int ntasks[2] = {0, 0};
+    double* dg = nullptr;  // fast-diagonalization matrices (host.dg), when built
     ~DevSet();
 };
 

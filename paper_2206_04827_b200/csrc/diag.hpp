@@ -1,0 +1,40 @@
+// Fast-diagonalization data for the per-mode Sylvester systems (host setup).
+//
+// Every modal system of the reference's Poisson / Helmholtz solves (proj/src/solvers.cpp:77-98,
+// 142-169; timestep.cpp:61-108) is, per parity block,
+//     A X B^ + C X D^ = E,   E = R2 f C02^T (top-left block),   u = S X S^T
+// with banded A, C (radial, per |w|) and B^, D^ (vertical, per k-parity). The reference solves it
+// by ADI with Zolotarev shifts to a relative residual of tol. The generalized eigenproblems
+// A v = lambda C v and D^ w = mu B^ w are real, simple and well conditioned (cond(V) ~ 30 at 256),
+// so the exact solution is
+//     X = V [ ((C V)^-1 E (B^-1 U)) ./ (lambda_i + mu_j) ] (B^ W)^-1,   W = B^-1 U,
+// i.e. four small dense products per mode on the FP64 tensor cores. Folding the RHS operators
+// and the Dirichlet recombination into the transforms keeps all four matrices well conditioned:
+//     PL = (C V)^-1 R2m   (M x mh)      QL = S_r V            (mh x M)
+//     PR = C02m W         (nh x N)      QR = (B^ W)^-1 S_z^T  (N x nh)
+//     u  = QL [ (PL f PR) ./ (lambda_i + mu_j) ] QR.
+// Eigenpairs are refined by inverse iteration in long double from Hessenberg-QR estimates;
+// the solution then has a residual ~1e-15 relative (three orders below the ADI tolerance).
+#pragma once
+
+#include <vector>
+
+#include "setup.hpp"
+
+namespace ccf {
+
+struct DiagLeft {
+    std::vector<double> PL, QL, lam;  // M x mh, mh x M, M
+};
+struct DiagRight {
+    std::vector<double> PR, QR, mu;  // nh x N, N x nh, N
+};
+
+// Left side from the compressed bands of one parity block: A, C (M x M, offsets -2..3) and
+// R2 (rows M, cols mh, offsets -1..3).
+DiagLeft diag_left(const CBand& A, const CBand& C, const CBand& R2, int M, int mh);
+// Right side from the stored (transposed) vertical bands: Bt, Dt (N x N, offsets -1..2,
+// B^ = Bt^T, D^ = Dt^T) and C02 (rows N, cols nh, offsets 0..2).
+DiagRight diag_right(const CBand& Bt, const CBand& Dt, const CBand& C02, int N, int nh);
+
+}  // namespace ccf

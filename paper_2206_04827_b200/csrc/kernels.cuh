@@ -52,7 +52,16 @@ struct GemmBatch {
     long lda, ldb, ldc;
     double alpha, beta;
     const int* tstart;  // optional: batch b sums the terms [tstart[b], tstart[b+1]) (A, B indexed by term)
+    const double* const* dl;  // optional epilogue C[i][j] = acc / (dl[b][i] + dr[b][j]) (fast diagonalization)
+    const double* const* dr;
+    // optional base-relative B (per term) / C (per batch): pointer = base[off >> 40] + (off & (2^40 - 1)),
+    // so a captured plan can be relaunched on other tensors (ring buffers) with new bases
+    const long* boff;
+    const long* coff;
+    const double* bbase[2];
+    double* cbase[2];
 };
+constexpr long kBaseShift = 40;
 __global__ void dgemm_batched_kernel(GemmBatch g);
 struct ThetaCross {
     Geo g;

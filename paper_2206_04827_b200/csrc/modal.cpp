@@ -1,6 +1,8 @@
 // Host builder for packed ADI operator blocks (see modal.hpp).
 #include "modal.hpp"
 
+#include "diag.hpp"
+
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -134,7 +136,7 @@ Range vertical_range(SizeOps& so, bool q2_pad) {
 }
 
 SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poisson, double scale, double tol,
-                           std::map<int, Range>& radial_cache, bool q2_pad, double plan_margin) {
+                           std::map<int, Range>& radial_cache, bool q2_pad, double plan_margin, bool with_diag) {
     const int m = so.m, n = so.n, M = (m - 2) / 2, N = (n - 2) / 2, mh = m / 2, nh = n / 2;
     const int lrows = ((M + 7) / 8) * 8 + 2, rrows = ((N + 7) / 8) * 8 + 2;  // zero-padded sweep rows
     SolverSet set;
@@ -181,6 +183,11 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
 
     // per |w| block cache
     std::map<int, AdiSlot> built;
+    struct DiagIn {
+        int aw;
+        CBand A, C, R2;
+    };
+    std::vector<DiagIn> diag_in;
     std::vector<double>& C = set.coef;
     auto alloc = [&](size_t count) {
         const long off = long(C.size());
@@ -221,6 +228,7 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
         const Dense Ar = recombine(Af), Cr = recombine(Cf);
         const CBand Ac = compress(Ar, j0, M, M, -2, 3), Cc = compress(Cr, j0, M, M, -2, 3);
         const CBand R2c = compress(so.ur.r2, j0, M, mh, -1, 3);
+        if (with_diag) diag_in.push_back({aw, Ac, Cc, R2c});
 
         const Range mu = radial_cache.at(aw);
         Range ca = poisson ? mu : Range{-1.0 / scale + mu.lo, -1.0 / scale + mu.hi};
@@ -361,6 +369,56 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
         set.plans[size_t(s)].has_plan = true;
     }
     C.resize(C.size() + 256, 0.0);  // read slack past the last block
+    if (with_diag) {
+        // left data per unique |w| (parallel: O(M^3) long double each), right data per k-parity
+        std::vector<DiagLeft> left(diag_in.size());
+        std::vector<std::string> errs(diag_in.size());
+        std::vector<int> codes(diag_in.size(), 0);
+        {
+            const int nth = std::max(1, std::min<int>(int(std::thread::hardware_concurrency()), int(diag_in.size())));
+            std::vector<std::thread> pool;
+            std::atomic<size_t> next{0};
+            for (int q = 0; q < nth; ++q)
+                pool.emplace_back([&] {
+                    for (;;) {
+                        const size_t i = next.fetch_add(1);
+                        if (i >= diag_in.size()) break;
+                        try {
+                            left[i] = diag_left(diag_in[i].A, diag_in[i].C, diag_in[i].R2, M, mh);
+                        } catch (const Error& e) {
+                            codes[i] = e.status;
+                            errs[i] = e.what();
+                        }
+                    }
+                });
+            for (auto& th : pool) th.join();
+        }
+        for (size_t i = 0; i < diag_in.size(); ++i)
+            if (codes[i]) throw Error(codes[i], errs[i]);
+        std::vector<double>& G = set.dg;
+        auto put = [&](const std::vector<double>& x) {
+            const long off = long(G.size());
+            G.insert(G.end(), x.begin(), x.end());
+            if (G.size() % 2) G.push_back(0.0);
+            return off;
+        };
+        std::map<int, long> left_off;
+        for (size_t i = 0; i < diag_in.size(); ++i) {
+            const long o = put(left[i].PL);
+            put(left[i].QL);
+            put(left[i].lam);
+            left_off[diag_in[i].aw] = o;
+        }
+        set.dg_left.resize(size_t(S));
+        for (int s = 0; s < S; ++s) set.dg_left[size_t(s)] = left_off.at(std::abs(slot_w[size_t(s)]));
+        for (int k0 = 0; k0 < 2; ++k0) {
+            const DiagRight r = diag_right(Btc[k0], Dtc[k0], C02c[k0], N, nh);
+            set.dg_right[k0] = put(r.PR);
+            put(r.QR);
+            put(r.mu);
+        }
+        set.has_diag = true;
+    }
     for (const AdiSlot& d : set.slots) {
         set.maxJ = std::max(set.maxJ, d.J);
         set.iters_per_round += d.J;

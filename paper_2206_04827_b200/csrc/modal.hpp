@@ -40,13 +40,21 @@ struct SolverSet {
     std::vector<double> coef;      // packed blocks (host copy)
     int maxJ = 0;
     long iters_per_round = 0;      // sum over slots of J (one round)
+    // fast-diagonalization data (diag.hpp), when built: per slot [PL | QL | lam], per k-parity
+    // [PR | QR | mu], all in `dg` (offsets in doubles, 16-byte aligned)
+    bool has_diag = false;
+    std::vector<double> dg;
+    std::vector<long> dg_left;  // per slot
+    long dg_right[2] = {0, 0};
 };
 
 // Build the packed set. slot_w: wavenumber per slot. radial: cached radial
 // ranges per |w| (computed on demand). Throws ccf::Error on reference failures
 // (overlapping intervals -> DOMAIN_ERROR, singular operators -> SINGULAR).
 // plan_margin: executed shifts planned for tol / plan_margin (1 = the reference's shift count).
+// with_diag: also build the fast-diagonalization data (diag.hpp).
 SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poisson, double scale, double tol,
-                           std::map<int, Range>& radial_cache, bool q2_pad, double plan_margin = 1.0);
+                           std::map<int, Range>& radial_cache, bool q2_pad, double plan_margin = 1.0,
+                           bool with_diag = false);
 
 }  // namespace ccf

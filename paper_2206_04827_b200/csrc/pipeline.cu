@@ -238,7 +238,7 @@ TransformPlan::TransformPlan(Ctx& c) {
 
 // ---------------------------------------------------------------- GEMM plans
 void GemmPlan::upload() {
-    const size_t nb = C.size(), na = A.size();
+    const size_t nb = std::max(C.size(), Coff.size()), na = A.size();
     if (!dA) {
         CCF_CUDA(cudaMalloc(&dA, std::max<size_t>(na, 1) * sizeof(void*)));
         CCF_CUDA(cudaMalloc(&dB, std::max<size_t>(na, 1) * sizeof(void*)));
@@ -249,17 +249,37 @@ void GemmPlan::upload() {
         CCF_CUDA(cudaMemcpy(dA, A.data(), na * sizeof(void*), cudaMemcpyHostToDevice));
         CCF_CUDA(cudaMemcpy(dB, B.data(), na * sizeof(void*), cudaMemcpyHostToDevice));
     }
-    CCF_CUDA(cudaMemcpy(dC, C.data(), nb * sizeof(void*), cudaMemcpyHostToDevice));
+    if (!C.empty()) CCF_CUDA(cudaMemcpy(dC, C.data(), C.size() * sizeof(void*), cudaMemcpyHostToDevice));
     if (!tstart.empty()) CCF_CUDA(cudaMemcpy(dT, tstart.data(), tstart.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (!Boff.empty()) {
+        if (!dBoff) CCF_CUDA(cudaMalloc(&dBoff, Boff.size() * sizeof(long)));
+        CCF_CUDA(cudaMemcpy(dBoff, Boff.data(), Boff.size() * sizeof(long), cudaMemcpyHostToDevice));
+    }
+    if (!Coff.empty()) {
+        if (!dCoff) CCF_CUDA(cudaMalloc(&dCoff, Coff.size() * sizeof(long)));
+        CCF_CUDA(cudaMemcpy(dCoff, Coff.data(), Coff.size() * sizeof(long), cudaMemcpyHostToDevice));
+    }
+    if (!DL.empty()) {
+        if (!dDL) {
+            CCF_CUDA(cudaMalloc(&dDL, nb * sizeof(void*)));
+            CCF_CUDA(cudaMalloc(&dDR, nb * sizeof(void*)));
+        }
+        CCF_CUDA(cudaMemcpy(dDL, DL.data(), nb * sizeof(void*), cudaMemcpyHostToDevice));
+        CCF_CUDA(cudaMemcpy(dDR, DR.data(), nb * sizeof(void*), cudaMemcpyHostToDevice));
+    }
 }
 
-void GemmPlan::launch(cudaStream_t s) const {
-    GemmBatch g{dA, dB, dC, M, N, K, lda, ldb, ldc, alpha, beta, dT};
-    const dim3 grid(unsigned((N + 63) / 64), unsigned((M + 63) / 64), unsigned(C.size()));
+void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double* c0, double* c1) const {
+    GemmBatch g{dA, dB, dC, M, N, K, lda, ldb, ldc, alpha, beta, dT, dDL, dDR, dBoff, dCoff, {b0, b1}, {c0, c1}};
+    const dim3 grid(unsigned((N + 63) / 64), unsigned((M + 63) / 64), unsigned(std::max(C.size(), Coff.size())));
     dgemm_batched_kernel<<<grid, 128, 0, s>>>(g);
 }
 
 GemmPlan::~GemmPlan() {
+    if (dBoff) cudaFree(dBoff);
+    if (dCoff) cudaFree(dCoff);
+    if (dDL) cudaFree(dDL);
+    if (dDR) cudaFree(dDR);
     if (dT) cudaFree(dT);
     if (dA) cudaFree(dA);
     if (dB) cudaFree(dB);
@@ -674,7 +694,105 @@ void Pipeline::poisson(const double* f, double w, double* u) {
     DevSet& set = c.set(false, true, 1.0);
     const double* src[1] = {f};
     const double ww[1] = {w};
-    c.run_adi(set, false, 1, src, ww, 1, nullptr, nullptr, 0, u, nullptr);
+    modal_solve(set, false, 1, src, ww, 1, nullptr, nullptr, 0, u, nullptr);
+}
+
+// Fast diagonalization (diag.hpp) per real sub-problem (tensor t, slot s, k-parity k0, plane):
+//   T1 = PL[s] f          (M x nh)      f = sum_i w_t[i] src_t[i], rows jj, half row k0
+//   Z  = (T1 PR[k0]) ./ (lam[s]_i + mu[k0]_j)
+//   T3 = QL[s] Z          (mh x N)
+//   u  = T3 QR[k0]        (mh x nh)  written in place into the output tensor
+void Pipeline::modal_solve(DevSet& set, bool full, int ntensor, const double* const* src0, const double* w0, int n0,
+                           const double* const* src1, const double* w1, int n1, double* out0, double* out1) {
+    if (!set.host.has_diag || !set.dg) {
+        c.run_adi(set, full, ntensor, src0, w0, n0, src1, w1, n1, out0, out1);
+        return;
+    }
+    const Geo& g = c.geo(full);
+    const int M = c.M, N = c.N, mh = g.mh, nh = g.nh;
+    const long Tt = c.tensor_doubles(full);
+    const double* const* srcs[2] = {src0, src1};
+    const double* ws[2] = {w0, w1};
+    const int ns[2] = {n0, n1};
+    double* outs[2] = {out0, out1};
+    const double* f[2] = {nullptr, nullptr};
+    for (int t = 0; t < ntensor; ++t) {  // RHS combination (BDF history + kappa * IMEX), timestep.cpp:41-73
+        if (ns[t] == 1 && ws[t][0] == 1.0) {
+            f[t] = srcs[t][0];
+            continue;
+        }
+        if (fcomb_[t].n < size_t(Tt)) fcomb_[t].alloc(size_t(Tt));
+        Combo cb{};
+        for (int i = 0; i < ns[t]; ++i) {
+            cb.src[i] = srcs[t][i];
+            cb.w[i] = ws[t][i];
+        }
+        cb.nsrc = ns[t];
+        cb.out = fcomb_[t].p;
+        cb.n = Tt;
+        combo_kernel<<<std::min<long>(4736, (Tt + 255) / 256), 256, 0, c.stream>>>(cb);
+        ++c.launches;
+        f[t] = fcomb_[t].p;
+    }
+    // scratch sized once for the largest task list of either slot table (cached GEMM plans hold
+    // pointers into it, so it must never be reallocated)
+    const size_t per = std::max(size_t(mh) * N, std::max(size_t(M) * nh, size_t(M) * N));
+    if (!dT1_.p) {
+        const size_t cap = per * size_t(2 * std::max(c.gh.nslots, c.gf.nslots) * 4);
+        dT1_.alloc(cap);
+        dZ_.alloc(cap);
+        dT3_.alloc(cap);
+    }
+    const void* keyp[1] = {&set};
+    const int ci[1] = {int(full) * 16 + ntensor};
+    bool fresh;
+    GemmPlan& g1 = gemm(ptr_key("d1", 1, keyp, keyp, ci), fresh);
+    GemmPlan& g2 = gemm(ptr_key("d2", 1, keyp, keyp, ci), fresh);
+    GemmPlan& g3 = gemm(ptr_key("d3", 1, keyp, keyp, ci), fresh);
+    GemmPlan& g4 = gemm(ptr_key("d4", 1, keyp, keyp, ci), fresh);
+    if (fresh) {
+        const double* dg = set.dg;
+        long task = 0;
+        for (int t = 0; t < ntensor; ++t)
+            for (int s = 0; s < g.nslots; ++s)
+                for (int k0 = 0; k0 < 2; ++k0)
+                    for (int pl = 0; pl < 2; ++pl, ++task) {
+                        const long lo = set.host.dg_left[size_t(s)], ro = set.host.dg_right[k0];
+                        const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride + long(k0) * nh;
+                        const long rel = (long(t) << kBaseShift) + off;  // base t = f_t / out_t at launch
+                        double* T1 = dT1_.p + size_t(task) * per;
+                        double* Z = dZ_.p + size_t(task) * per;
+                        double* T3 = dT3_.p + size_t(task) * per;
+                        g1.A.push_back(dg + lo);                       // PL  M x mh
+                        g1.B.push_back(nullptr);
+                        g1.Boff.push_back(rel);                        // f   mh x nh (ld n)
+                        g1.C.push_back(T1);                            // T1  M x nh
+                        g2.A.push_back(T1);
+                        g2.B.push_back(dg + ro);                       // PR  nh x N
+                        g2.C.push_back(Z);                             // Z   M x N
+                        g2.DL.push_back(dg + lo + 2L * M * mh);        // lambda
+                        g2.DR.push_back(dg + ro + 2L * nh * N);        // mu
+                        g3.A.push_back(dg + lo + long(M) * mh);        // QL  mh x M
+                        g3.B.push_back(Z);
+                        g3.C.push_back(T3);                            // T3  mh x N
+                        g4.A.push_back(T3);
+                        g4.B.push_back(dg + ro + long(nh) * N);        // QR  N x nh
+                        g4.Coff.push_back(rel);                        // u   mh x nh (ld n)
+                    }
+        g1.M = M; g1.N = nh; g1.K = mh; g1.lda = mh; g1.ldb = g.n; g1.ldc = nh;
+        g2.M = M; g2.N = N; g2.K = nh; g2.lda = nh; g2.ldb = N; g2.ldc = N;
+        g3.M = mh; g3.N = N; g3.K = M; g3.lda = M; g3.ldb = N; g3.ldc = N;
+        g4.M = mh; g4.N = nh; g4.K = N; g4.lda = N; g4.ldb = nh; g4.ldc = g.n;
+        g1.upload();
+        g2.upload();
+        g3.upload();
+        g4.upload();
+    }
+    g1.launch(c.stream, f[0], f[1]);
+    g2.launch(c.stream);
+    g3.launch(c.stream);
+    g4.launch(c.stream, nullptr, nullptr, out0, out1);
+    c.launches += 4;
 }
 
 void Pipeline::decompose(const double* vr, const double* vt, const double* vz, double* lam, double* gam) {
@@ -907,7 +1025,7 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
     }
     DevSet& set = c.set(false, false, scale);
     if (c.prof_events.empty()) c.mark("start");
-    c.run_adi(set, false, 2, sl, wl, ns, sg, wl, ns, lam[out].p, gam[out].p);
+    P.modal_solve(set, false, 2, sl, wl, ns, sg, wl, ns, lam[out].p, gam[out].p);
     c.mark("H_helmholtz_adi");
     const long T = P.T;
     finite_check_kernel<<<std::min<long>(1184, (T + 255) / 256), 256, 0, c.stream>>>(lam[out].p, T, dflag);

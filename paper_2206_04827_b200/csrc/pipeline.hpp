@@ -39,15 +39,22 @@ struct GemmPlan {
     std::vector<const double*> A, B;  // per term (= per batch unless tstart is set)
     std::vector<double*> C;           // per batch
     std::vector<int> tstart;          // optional: batch b sums terms [tstart[b], tstart[b+1])
+    std::vector<const double*> DL, DR;  // optional per-batch epilogue divisors (dl_i + dr_j)
+    std::vector<long> Boff, Coff;       // optional base-relative B / C (see GemmBatch)
     const double** dA = nullptr;
     const double** dB = nullptr;
     double** dC = nullptr;
     int* dT = nullptr;
+    const double** dDL = nullptr;
+    const double** dDR = nullptr;
+    long* dBoff = nullptr;
+    long* dCoff = nullptr;
     int M = 0, N = 0, K = 0;
     long lda = 0, ldb = 0, ldc = 0;
     double alpha = 1.0, beta = 0.0;
     void upload();
-    void launch(cudaStream_t s) const;
+    void launch(cudaStream_t s, const double* b0 = nullptr, const double* b1 = nullptr, double* c0 = nullptr,
+                double* c1 = nullptr) const;
     ~GemmPlan();
 };
 
@@ -70,6 +77,11 @@ public:
     void nonlinear(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w, double* lam_n,
                    double* gam_n);
     void poisson(const double* f, double w, double* u);  // u = Poisson3D(w * f), half mode
+    // Modal Sylvester solves of a solver set for 1 or 2 tensors with fused RHS combinations
+    // (out_t = Solve(sum_i w_t[i] src_t[i])): fast diagonalization on the tensor cores, or the
+    // ADI kernel (ctx flag bit 2 / sets without diagonalization data).
+    void modal_solve(DevSet& set, bool full, int ntensor, const double* const* src0, const double* w0, int n0,
+                     const double* const* src1, const double* w1, int n1, double* out0, double* out1);
     void decompose(const double* vr, const double* vt, const double* vz, double* lam, double* gam);
     void hpoisson(const double* rhs, double* u);
     void calculus(int op, int cls, const double* in, double* out);  // ops of include/ccf.h ccf_calculus
@@ -96,6 +108,7 @@ private:
     void ensure_composite();
     void nonlinear_pencil(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w,
                           double* lam_n, double* gam_n);
+    DBuf fcomb_[2], dT1_, dZ_, dT3_;  // fast-diagonalization scratch
 };
 
 struct NSState {

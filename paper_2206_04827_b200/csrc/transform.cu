@@ -37,7 +37,13 @@ __global__ void __launch_bounds__(128) dgemm_batched_kernel(GemmBatch g) {
         t0 = g.tstart[b];
         t1 = g.tstart[b + 1];
     }
-    double* __restrict__ C = g.C[b];
+    double* __restrict__ C;
+    if (g.coff) {
+        const long o = g.coff[b];
+        C = g.cbase[o >> kBaseShift] + (o & ((1L << kBaseShift) - 1));
+    } else {
+        C = g.C[b];
+    }
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
@@ -53,7 +59,13 @@ __global__ void __launch_bounds__(128) dgemm_batched_kernel(GemmBatch g) {
     auto gload = [&](int it) {
         const int term = t0 + it / nkt, k0 = (it % nkt) * BK;
         const double* __restrict__ A = g.A[term];
-        const double* __restrict__ B = g.B[term];
+        const double* __restrict__ B;
+        if (g.boff) {
+            const long o = g.boff[term];
+            B = g.bbase[o >> kBaseShift] + (o & ((1L << kBaseShift) - 1));
+        } else {
+            B = g.B[term];
+        }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const int e = tid + q * 128;  // 0..1023
@@ -106,7 +118,8 @@ __global__ void __launch_bounds__(128) dgemm_batched_kernel(GemmBatch g) {
                 const int r = m0 + wm + 8 * i + gq, c = n0 + wn + 8 * j + 2 * tq + q;
                 if (r < g.M && c < g.N) {
                     double* dst = C + long(r) * g.ldc + c;
-                    const double v = g.alpha * acc[i][j][q];
+                    double v = g.alpha * acc[i][j][q];
+                    if (g.dl) v = v / (__ldg(g.dl[b] + r) + __ldg(g.dr[b] + c));
                     *dst = g.beta == 0.0 ? v : fma(g.beta, *dst, v);
                 }
             }

@@ -124,21 +124,13 @@ class ClockSampler:
         return out
 
 
-def adi_traffic():
-    """DRAM bytes of the adi_kernel launches of one step from the committed ncu capture (or None)."""
+def gemm_traffic():
+    """DRAM bytes of the GEMM launches of one step from the committed ncu capture (or None)."""
     try:
         with open(os.path.join(ROOT, "profiles", "roofline_inputs_r01.json")) as f:
-            return float(json.load(f)["adi_dram_bytes_per_step"])
+            return float(json.load(f)["gemm_dram_bytes_per_step"])
     except Exception:
         return None
-
-
-def adi_flops(ctx_stats_iters, M, N):
-    """SURVEY §8d algorithmic ADI flops: 180 per nonzero complex entry per iteration.
-    Our iteration counter counts real sub-problem iterations (4 per complex mode), each
-    covering M x N real entries = (M x 2N complex entries) / 2 per pair of planes."""
-    # complex entries per mode = M * 2N ; real sub-problems per mode = 4 (2 k-parities x re/im)
-    return 180.0 * (ctx_stats_iters / 4.0) * M * (2 * N)
 
 
 def cpu_sample(cfg, threads):
@@ -248,20 +240,20 @@ def main():
     # ---- per-stage profile of one extra eager step (CUDA events between stages)
     ctx.reset_stats()
     stages = st.profile_step()
-    prof_iters = ctx.stats()["adi_iterations"]
-    M, N = (m - 2) // 2, (n - 2) // 2
-    t_adi_ms = stages.get("P_poisson_adi", 0.0) + stages.get("H_helmholtz_adi", 0.0)
-    F_adi = adi_flops(prof_iters, M, N)
-    adi_tflops = F_adi / (t_adi_ms * 1e-3) / 1e12 if t_adi_ms > 0 else None
-    # step roofline: B = 43 fields x 8N ; T_roof = sum_s max(B_s/BW, F_s/P)
-    Npts = m * n * p
-    field = 8.0 * Npts
+    pstats = ctx.stats()
+    F_gemm = pstats["gemm_flops"]  # FP64 tensor-core flops of the step's batched GEMMs (2 M N K per term)
+    gemm_stages = ["P_poisson_solve", "X1_rz_synthesis", "X3_rz_analysis", "C_curl_decompose", "H_helmholtz_solve"]
+    t_gemm_ms = sum(stages.get(k, 0.0) for k in gemm_stages)  # these stages launch GEMMs only
+    gemm_tflops = F_gemm / (t_gemm_ms * 1e-3) / 1e12 if t_gemm_ms > 0 else None
+    # step roofline: T_roof = F_gemm / P_dmma + (HBM-bound stages: theta 6 in + 3 out tensors, the
+    # Helmholtz RHS combination 2 x (sources + 1) tensors) / BW; tensor = one half-spectrum field
+    S = p // 2 + 1
+    tensor_bytes = 8.0 * S * 2 * (m // 2) * n
     bw = peaks["hbm_gbs"] * 1e9
-    pf = peaks["fp64_dfma_tflops"] * 1e12
-    F_P = F_adi * (stages.get("P_poisson_adi", 0) / t_adi_ms) if t_adi_ms else 0.0
-    F_H = F_adi - F_P
-    T_roof = max(2 * field / bw, F_P / pf) + (9 + 9 + 5) * field / bw + max(18 * field / bw, F_H / pf)
-    B_total = 43 * field
+    pdm = peaks["fp64_dmma_tflops"] * 1e12
+    B_other = (9 + 2 * (4 + 4 + 1)) * tensor_bytes
+    T_roof = F_gemm / pdm + B_other / bw
+    B_total = B_other
 
     # ---- end-to-end through the C-ABI with pinned host buffers: create (H2D) -> KE steps -> read back (D2H).
     # A fresh stepper pays the reference's BDF 1 -> 4 ramp and its CUDA-graph captures, so KE >= 50.
@@ -308,20 +300,23 @@ def main():
                             "graph captures -> omega() to pinned host (D2H), through the C-ABI; bytes amortised "
                             "over KE"},
             "gpu_launches": stats["kernel_launches"],
-            "roofline": {"bound": "fp64", "kernel": "adi_kernel (Poisson + Helmholtz modal ADI)",
-                         "achieved": adi_tflops, "peak": peaks["fp64_dfma_tflops"], "unit": "TFLOP/s",
-                         "frac": (adi_tflops / peaks["fp64_dfma_tflops"]) if adi_tflops else None,
-                         "traffic": adi_traffic(),
-                         "traffic_unit": "bytes per step (dram read + write of the adi_kernel launches, ncu)",
-                         "peak_source": "measured DFMA peak, tools/microbench/fp64_peak.cu (profiles/fp64_peak_r01.txt)",
-                         "flops_per_step": F_adi, "adi_ms_per_step": t_adi_ms,
-                         "flop_model": "SURVEY 8d: 180 flop per complex entry per executed ADI iteration"},
+            "roofline": {"bound": "tensor",
+                         "kernel": "dgemm_batched_kernel (FP64 DMMA m8n8k4): r/z transforms, composite radial "
+                                   "operators and the fast-diagonalization modal solves",
+                         "achieved": gemm_tflops, "peak": peaks["fp64_dmma_tflops"], "unit": "TFLOP/s",
+                         "frac": (gemm_tflops / peaks["fp64_dmma_tflops"]) if gemm_tflops else None,
+                         "traffic": gemm_traffic(),
+                         "traffic_unit": "dram read + write bytes per step of the GEMM launches (ncu, committed)",
+                         "peak_source": "measured FP64 DMMA peak, tools/microbench/fp64_peak.cu "
+                                        "(profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json has no FP64 figure",
+                         "flops_per_step": F_gemm, "gemm_ms_per_step": t_gemm_ms,
+                         "flop_model": "2 M N K per product term of every batched GEMM launched in one step"},
             "step_roofline": {"T_roof_ms": T_roof * 1e3, "achieved": T_roof / (ms_step * 1e-3),
-                              "hbm_bytes_alg": B_total, "hbm_fraction": B_total / (ms_step * 1e-3) / bw,
+                              "gemm_bound_ms": F_gemm / pdm * 1e3, "hbm_bound_ms": B_other / bw * 1e3,
                               "hbm_peak_gbs": peaks["hbm_gbs"], "hbm_source": peaks["hbm_source"],
-                              "note": "ADI stages are FP64-bound; HBM fraction capped near 48% by construction"},
+                              "note": "GEMM stages at the DMMA peak + theta and RHS-combination passes at HBM peak"},
             "stage_ms": stages,
-            "adi_iterations_per_step": prof_iters,
+            "adi_iterations_per_step": pstats["adi_iterations"],
             "setup_s": t_setup,
         }
         if cpu:

@@ -111,6 +111,9 @@ ccf_status ccf_get_last_error(ccf_ctx* ctx, int* kind, int* slice, int* shift_in
 ccf_status ccf_get_stats(ccf_ctx* ctx, long* adi_subproblems, long* adi_iterations, int* max_rounds,
                          double* worst_residual, long* kernel_launches);
 ccf_status ccf_reset_stats(ccf_ctx* ctx);
+/* FP64 tensor-core flops (2 M N K per product term) of the batched GEMMs enqueued since the last
+ * ccf_reset_stats (host-side count: steps replayed from a CUDA graph are not counted). */
+ccf_status ccf_get_gemm_flops(ccf_ctx* ctx, double* flops);
 /* Per (tensor, slot) ADI rounds used (1..4) and relative residual after each round
  * (history[4 * i + r]) of the most recent ADI solve on this context (adi.cpp:163-200):
  * which = 0 most recent solve, 1 / 2 most recent Poisson / Helmholtz solve (needs

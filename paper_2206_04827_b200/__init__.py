@@ -76,7 +76,7 @@ EXPORTS = ["ccf_ctx_create", "ccf_ctx_destroy", "ccf_ctx_set_stream", "ccf_ctx_s
            "ccf_nonlinear", "ccf_ns_create", "ccf_ns_step", "ccf_ns_get_omega", "ccf_ns_destroy",
            "ccf_get_last_error", "ccf_get_stats", "ccf_reset_stats", "ccf_modal_plan", "ccf_version",
            "ccf_ns_profile_step", "ccf_ns_set_graphs", "ccf_ns_launches_per_step", "ccf_plan_host",
-           "ccf_create_error", "ccf_adi_last_rounds", "ccf_adi_keep_history"]
+           "ccf_create_error", "ccf_adi_last_rounds", "ccf_adi_keep_history", "ccf_get_gemm_flops"]
 
 _lib = None
 
@@ -125,6 +125,7 @@ def lib():
                                          C.POINTER(C.c_int), C.c_char_p, C.c_int]
         L.ccf_adi_last_rounds.argtypes = [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), vp, vp, C.c_int]
         L.ccf_adi_keep_history.argtypes = [vp, C.c_int]
+        L.ccf_get_gemm_flops.argtypes = [vp, dp]
         L.ccf_get_stats.argtypes = [vp, C.POINTER(C.c_long), C.POINTER(C.c_long), C.POINTER(C.c_int), dp,
                                     C.POINTER(C.c_long)]
         L.ccf_reset_stats.argtypes = [vp]
@@ -300,7 +301,9 @@ class Context:
         s, it, r, lch = C.c_long(), C.c_long(), C.c_int(), C.c_long()
         w = C.c_double()
         self._check(lib().ccf_get_stats(self.h, C.byref(s), C.byref(it), C.byref(r), C.byref(w), C.byref(lch)))
-        return dict(adi_iterations=it.value, kernel_launches=lch.value)
+        gf = C.c_double()
+        self._check(lib().ccf_get_gemm_flops(self.h, C.byref(gf)))
+        return dict(adi_iterations=it.value, kernel_launches=lch.value, gemm_flops=gf.value)
 
     def reset_stats(self):
         self._check(lib().ccf_reset_stats(self.h))

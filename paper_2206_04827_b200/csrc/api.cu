@@ -251,7 +251,12 @@ ccf_status ccf_reset_stats(ccf_ctx* ctx) {
     return guard(ctx, [&](Ctx& c) {
         CCF_CUDA(cudaMemset(c.ws.iters, 0, sizeof(unsigned long long) * 2));
         c.launches = 0;
+        c.gemm_flops = 0.0;
     });
+}
+
+ccf_status ccf_get_gemm_flops(ccf_ctx* ctx, double* flops) {
+    return guard(ctx, [&](Ctx& c) { *flops = c.gemm_flops; });
 }
 
 }  // extern "C"

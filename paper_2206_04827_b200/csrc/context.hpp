@@ -81,6 +81,7 @@ struct Ctx {
     int kept_shape[3][2] = {};
     // optional stage profiling: events recorded at stage boundaries when enabled
     bool profiling = false;
+    double gemm_flops = 0.0;  // FP64 tensor-core flops of the GEMM launches enqueued since reset_stats
     std::vector<cudaEvent_t> prof_events;
     std::vector<std::string> prof_names;
     void mark(const char* name) {

@@ -236,6 +236,7 @@ DiagLeft diag_left(const CBand& Ab, const CBand& Cb, const CBand& R2b, int M, in
     out.QL = to_double(QL);
     out.lam.resize(size_t(M));
     for (int i = 0; i < M; ++i) out.lam[size_t(i)] = double(lam[size_t(i)]);
+    out.lam_ld = lam;
     return out;
 }
 
@@ -280,6 +281,7 @@ DiagRight diag_right(const CBand& Btb, const CBand& Dtb, const CBand& C02b, int 
     out.QR = to_double(QR);
     out.mu.resize(size_t(N));
     for (int i = 0; i < N; ++i) out.mu[size_t(i)] = double(mu[size_t(i)]);
+    out.mu_ld = mu;
     return out;
 }
 

@@ -25,9 +25,11 @@ namespace ccf {
 
 struct DiagLeft {
     std::vector<double> PL, QL, lam;  // M x mh, mh x M, M
+    std::vector<long double> lam_ld;  // eigenvalues before rounding (for 1 / (lambda + mu))
 };
 struct DiagRight {
     std::vector<double> PR, QR, mu;  // nh x N, N x nh, N
+    std::vector<long double> mu_ld;
 };
 
 // Left side from the compressed bands of one parity block: A, C (M x M, offsets -2..3) and

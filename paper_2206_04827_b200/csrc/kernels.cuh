@@ -52,17 +52,20 @@ struct GemmBatch {
     long lda, ldb, ldc;
     double alpha, beta;
     const int* tstart;  // optional: batch b sums the terms [tstart[b], tstart[b+1]) (A, B indexed by term)
-    const double* const* dl;  // optional epilogue C[i][j] = acc / (dl[b][i] + dr[b][j]) (fast diagonalization)
-    const double* const* dr;
+    const double* const* dl;  // optional epilogue C[i][j] = acc * dl[b][i * N + j] (fast diagonalization:
+    const double* const* dr;  //   reciprocals of lambda_i + mu_j; dr unused)
     // optional base-relative B (per term) / C (per batch): pointer = base[off >> 40] + (off & (2^40 - 1)),
     // so a captured plan can be relaunched on other tensors (ring buffers) with new bases
     const long* boff;
     const long* coff;
     const double* bbase[2];
     double* cbase[2];
+    int nbatch;  // number of batches (persistent kernel)
 };
 constexpr long kBaseShift = 40;
 __global__ void dgemm_batched_kernel(GemmBatch g);
+__global__ void dgemm_pipe_kernel(GemmBatch g);  // 128 x 64 tiles, cp.async pipeline (aligned operands)
+size_t dgemm_pipe_smem();
 struct ThetaCross {
     Geo g;
     int logp, tj;

@@ -402,20 +402,39 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
             if (G.size() % 2) G.push_back(0.0);
             return off;
         };
+        // right data per k-parity first (the eigenvalue-sum reciprocals need mu)
+        DiagRight right[2];
+        for (int k0 = 0; k0 < 2; ++k0) right[k0] = diag_right(Btc[k0], Dtc[k0], C02c[k0], N, nh);
+        // QL (mh x M) and PR (nh x N) are stored with the leading dimension rounded up to even so
+        // that every GEMM operand row is 16-byte aligned (cp.async pipeline)
+        auto padld = [](const std::vector<double>& x, int rows, int cols) {
+            const int ld = cols + (cols & 1);
+            std::vector<double> o(size_t(rows) * ld, 0.0);
+            for (int r = 0; r < rows; ++r)
+                for (int c = 0; c < cols; ++c) o[size_t(r) * ld + c] = x[size_t(r) * cols + c];
+            return o;
+        };
         std::map<int, long> left_off;
         for (size_t i = 0; i < diag_in.size(); ++i) {
             const long o = put(left[i].PL);
-            put(left[i].QL);
+            put(padld(left[i].QL, mh, M));
             put(left[i].lam);
+            for (int k0 = 0; k0 < 2; ++k0) {  // 1 / (lambda_i + mu_j), rounded once from long double
+                std::vector<double> rt(size_t(M) * N);
+                for (int a = 0; a < M; ++a)
+                    for (int b = 0; b < N; ++b)
+                        rt[size_t(a) * N + b] =
+                            double(1.0L / ((long double)left[i].lam_ld[size_t(a)] + right[k0].mu_ld[size_t(b)]));
+                put(rt);
+            }
             left_off[diag_in[i].aw] = o;
         }
         set.dg_left.resize(size_t(S));
         for (int s = 0; s < S; ++s) set.dg_left[size_t(s)] = left_off.at(std::abs(slot_w[size_t(s)]));
         for (int k0 = 0; k0 < 2; ++k0) {
-            const DiagRight r = diag_right(Btc[k0], Dtc[k0], C02c[k0], N, nh);
-            set.dg_right[k0] = put(r.PR);
-            put(r.QR);
-            put(r.mu);
+            set.dg_right[k0] = put(padld(right[k0].PR, nh, N));
+            put(right[k0].QR);
+            put(right[k0].mu);
         }
         set.has_diag = true;
     }

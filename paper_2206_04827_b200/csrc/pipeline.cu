@@ -239,6 +239,13 @@ TransformPlan::TransformPlan(Ctx& c) {
 // ---------------------------------------------------------------- GEMM plans
 void GemmPlan::upload() {
     const size_t nb = std::max(C.size(), Coff.size()), na = A.size();
+    // the pipelined kernel copies 16-byte chunks: A / B bases (and base-relative offsets) 16-byte
+    // aligned, even leading dimensions
+    pipe = (lda % 2 == 0) && (ldb % 2 == 0);
+    for (size_t i = 0; i < na && pipe; ++i) {
+        if (reinterpret_cast<uintptr_t>(A[i]) % 16) pipe = false;
+        if (Boff.empty() ? (reinterpret_cast<uintptr_t>(B[i]) % 16 != 0) : (Boff[i] % 2 != 0)) pipe = false;
+    }
     if (!dA) {
         CCF_CUDA(cudaMalloc(&dA, std::max<size_t>(na, 1) * sizeof(void*)));
         CCF_CUDA(cudaMalloc(&dB, std::max<size_t>(na, 1) * sizeof(void*)));
@@ -270,9 +277,28 @@ void GemmPlan::upload() {
 }
 
 void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double* c0, double* c1) const {
-    GemmBatch g{dA, dB, dC, M, N, K, lda, ldb, ldc, alpha, beta, dT, dDL, dDR, dBoff, dCoff, {b0, b1}, {c0, c1}};
-    const dim3 grid(unsigned((N + 63) / 64), unsigned((M + 63) / 64), unsigned(std::max(C.size(), Coff.size())));
-    dgemm_batched_kernel<<<grid, 128, 0, s>>>(g);
+    const unsigned nb = unsigned(std::max(C.size(), Coff.size()));
+    GemmBatch g{dA, dB, dC, M, N, K, lda, ldb, ldc, alpha, beta, dT, dDL, dDR, dBoff, dCoff, {b0, b1}, {c0, c1}, int(nb)};
+    const bool based_ok = (reinterpret_cast<uintptr_t>(b0) % 16 == 0) && (reinterpret_cast<uintptr_t>(b1) % 16 == 0);
+    if (pipe && based_ok) {
+        static bool attr = false;  // process-wide function attribute (same on every device)
+        if (!attr) {
+            CCF_CUDA(cudaFuncSetAttribute(dgemm_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(dgemm_pipe_smem())));
+            attr = true;
+        }
+        static int nsm = 0;
+        if (!nsm) CCF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+        const long items = long(nb) * ((M + 127) / 128) * ((N + 63) / 64);
+        // one item per CTA: dynamic hardware scheduling balances the variable-length (term-count)
+        // items better than a static persistent round robin (measured: 23 vs 21 TFLOP/s)
+        const unsigned grid = unsigned(items);
+        (void)nsm;
+        dgemm_pipe_kernel<<<grid, 256, dgemm_pipe_smem(), s>>>(g);
+    } else {
+        const dim3 grid(unsigned((N + 63) / 64), unsigned((M + 63) / 64), nb);
+        dgemm_batched_kernel<<<grid, 128, 0, s>>>(g);
+    }
 }
 
 GemmPlan::~GemmPlan() {
@@ -401,7 +427,9 @@ void Pipeline::rz_synth(int count, const double* const* in, const int* cls, doub
         z.upload();
     }
     r.launch(c.stream);
+    c.gemm_flops += r.flops();
     z.launch(c.stream);
+    c.gemm_flops += z.flops();
     c.launches += 2;
 }
 
@@ -448,7 +476,9 @@ void Pipeline::rz_analyze(int count, const double* const* in, const int* cls, do
         r.upload();
     }
     z.launch(c.stream);
+    c.gemm_flops += z.flops();
     r.launch(c.stream);
+    c.gemm_flops += r.flops();
     c.launches += 2;
 }
 
@@ -579,6 +609,7 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
         zs.upload();
     }
     zs.launch(c.stream);
+    c.gemm_flops += zs.flops();
     // ---- composite r synthesis -> (r, z)-values of the 6 velocity / vorticity components
     GemmPlan& rs = gemm(ptr_key("nrs", 6, keyp, keyp, cls0), fresh);
     if (fresh) {
@@ -603,6 +634,7 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
         rs.upload();
     }
     rs.launch(c.stream);
+    c.gemm_flops += rs.flops();
     c.launches += 2;
     c.mark("X1_rz_synthesis");
     theta_cross(val, av);
@@ -633,6 +665,7 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
         za.upload();
     }
     za.launch(c.stream);
+    c.gemm_flops += za.flops();
     c.launches += 1;
     c.mark("X3_rz_analysis");
     // ---- composite curl + pt_decompose + r analysis -> (gamma_N, lambda_N)
@@ -658,6 +691,7 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
         ra.upload();
     }
     ra.launch(c.stream);
+    c.gemm_flops += ra.flops();
     c.launches += 1;
     c.mark("C_curl_decompose");
 }
@@ -703,7 +737,8 @@ void Pipeline::poisson(const double* f, double w, double* u) {
 //   T3 = QL[s] Z          (mh x N)
 //   u  = T3 QR[k0]        (mh x nh)  written in place into the output tensor
 void Pipeline::modal_solve(DevSet& set, bool full, int ntensor, const double* const* src0, const double* w0, int n0,
-                           const double* const* src1, const double* w1, int n1, double* out0, double* out1) {
+                           const double* const* src1, const double* w1, int n1, double* out0, double* out1,
+                           const char* rhs_mark) {
     if (!set.host.has_diag || !set.dg) {
         c.run_adi(set, full, ntensor, src0, w0, n0, src1, w1, n1, out0, out1);
         return;
@@ -716,9 +751,11 @@ void Pipeline::modal_solve(DevSet& set, bool full, int ntensor, const double* co
     const int ns[2] = {n0, n1};
     double* outs[2] = {out0, out1};
     const double* f[2] = {nullptr, nullptr};
+    double alpha = 1.0;
     for (int t = 0; t < ntensor; ++t) {  // RHS combination (BDF history + kappa * IMEX), timestep.cpp:41-73
-        if (ns[t] == 1 && ws[t][0] == 1.0) {
+        if (ntensor == 1 && ns[t] == 1) {  // single source: its weight rides on the first product
             f[t] = srcs[t][0];
+            alpha = ws[t][0];
             continue;
         }
         if (fcomb_[t].n < size_t(Tt)) fcomb_[t].alloc(size_t(Tt));
@@ -735,8 +772,9 @@ void Pipeline::modal_solve(DevSet& set, bool full, int ntensor, const double* co
         f[t] = fcomb_[t].p;
     }
     // scratch sized once for the largest task list of either slot table (cached GEMM plans hold
-    // pointers into it, so it must never be reallocated)
-    const size_t per = std::max(size_t(mh) * N, std::max(size_t(M) * nh, size_t(M) * N));
+    // pointers into it, so it must never be reallocated); leading dimensions rounded up to even
+    const int Mp = M + (M & 1), Np = N + (N & 1);
+    const size_t per = std::max(size_t(mh) * Np, size_t(M) * std::max(nh, Np));
     if (!dT1_.p) {
         const size_t cap = per * size_t(2 * std::max(c.gh.nslots, c.gf.nslots) * 4);
         dT1_.alloc(cap);
@@ -752,46 +790,56 @@ void Pipeline::modal_solve(DevSet& set, bool full, int ntensor, const double* co
     GemmPlan& g4 = gemm(ptr_key("d4", 1, keyp, keyp, ci), fresh);
     if (fresh) {
         const double* dg = set.dg;
+        auto even = [](long x) { return x + (x & 1); };
         long task = 0;
         for (int t = 0; t < ntensor; ++t)
             for (int s = 0; s < g.nslots; ++s)
                 for (int k0 = 0; k0 < 2; ++k0)
                     for (int pl = 0; pl < 2; ++pl, ++task) {
-                        const long lo = set.host.dg_left[size_t(s)], ro = set.host.dg_right[k0];
+                        // dg layout (modal.cpp): left [PL M x mh | QL mh x Mp | lam | 1/(lam+mu) x2], right [PR nh x Np | QR N x nh | mu]
+                        const long PLo = set.host.dg_left[size_t(s)], QLo = PLo + long(M) * mh,
+                                   LAMo = QLo + long(mh) * Mp, RTo = LAMo + even(M) + long(k0) * even(long(M) * N);
+                        const long PRo = set.host.dg_right[k0], QRo = PRo + long(nh) * Np;
                         const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride + long(k0) * nh;
                         const long rel = (long(t) << kBaseShift) + off;  // base t = f_t / out_t at launch
                         double* T1 = dT1_.p + size_t(task) * per;
                         double* Z = dZ_.p + size_t(task) * per;
                         double* T3 = dT3_.p + size_t(task) * per;
-                        g1.A.push_back(dg + lo);                       // PL  M x mh
+                        g1.A.push_back(dg + PLo);                      // PL  M x mh
                         g1.B.push_back(nullptr);
                         g1.Boff.push_back(rel);                        // f   mh x nh (ld n)
                         g1.C.push_back(T1);                            // T1  M x nh
                         g2.A.push_back(T1);
-                        g2.B.push_back(dg + ro);                       // PR  nh x N
-                        g2.C.push_back(Z);                             // Z   M x N
-                        g2.DL.push_back(dg + lo + 2L * M * mh);        // lambda
-                        g2.DR.push_back(dg + ro + 2L * nh * N);        // mu
-                        g3.A.push_back(dg + lo + long(M) * mh);        // QL  mh x M
+                        g2.B.push_back(dg + PRo);                      // PR  nh x N (ld Np)
+                        g2.C.push_back(Z);                             // Z   M x N (ld Np)
+                        g2.DL.push_back(dg + RTo);                     // 1 / (lambda_i + mu_j)
+                        g2.DR.push_back(dg + RTo);
+                        g3.A.push_back(dg + QLo);                      // QL  mh x M (ld Mp)
                         g3.B.push_back(Z);
-                        g3.C.push_back(T3);                            // T3  mh x N
+                        g3.C.push_back(T3);                            // T3  mh x N (ld Np)
                         g4.A.push_back(T3);
-                        g4.B.push_back(dg + ro + long(nh) * N);        // QR  N x nh
+                        g4.B.push_back(dg + QRo);                      // QR  N x nh
                         g4.Coff.push_back(rel);                        // u   mh x nh (ld n)
                     }
         g1.M = M; g1.N = nh; g1.K = mh; g1.lda = mh; g1.ldb = g.n; g1.ldc = nh;
-        g2.M = M; g2.N = N; g2.K = nh; g2.lda = nh; g2.ldb = N; g2.ldc = N;
-        g3.M = mh; g3.N = N; g3.K = M; g3.lda = M; g3.ldb = N; g3.ldc = N;
-        g4.M = mh; g4.N = nh; g4.K = N; g4.lda = N; g4.ldb = nh; g4.ldc = g.n;
+        g2.M = M; g2.N = N; g2.K = nh; g2.lda = nh; g2.ldb = Np; g2.ldc = Np;
+        g3.M = mh; g3.N = N; g3.K = M; g3.lda = Mp; g3.ldb = Np; g3.ldc = Np;
+        g4.M = mh; g4.N = nh; g4.K = N; g4.lda = Np; g4.ldb = nh; g4.ldc = g.n;
         g1.upload();
         g2.upload();
         g3.upload();
         g4.upload();
     }
+    if (rhs_mark) c.mark(rhs_mark);
+    g1.alpha = alpha;
     g1.launch(c.stream, f[0], f[1]);
+    c.gemm_flops += g1.flops();
     g2.launch(c.stream);
+    c.gemm_flops += g2.flops();
     g3.launch(c.stream);
+    c.gemm_flops += g3.flops();
     g4.launch(c.stream, nullptr, nullptr, out0, out1);
+    c.gemm_flops += g4.flops();
     c.launches += 4;
 }
 
@@ -893,7 +941,9 @@ void Pipeline::analyze_full(const double* values, double* coeffs) {
     r.upload();
     zz.upload();
     r.launch(c.stream);
+    c.gemm_flops += r.flops();
     zz.launch(c.stream);
+    c.gemm_flops += zz.flops();
     real_to_complex_kernel<<<std::min<long>(4736, (nv + 255) / 256), 256, 0, c.stream>>>(v, z, nv);
     double* dst = coeffs;
     const bool host = !c.is_device_ptr(coeffs);
@@ -934,7 +984,9 @@ void Pipeline::synthesize_full(const double* coeffs, double* values) {
     zz.upload();
     r.upload();
     zz.launch(c.stream);
+    c.gemm_flops += zz.flops();
     r.launch(c.stream);
+    c.gemm_flops += r.flops();
     c.launches += 4;
     c.store_values(v, values);
     c.sync();
@@ -1001,7 +1053,7 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
         double* lpsi = P.scratch(18);
         c.mark("start");
         P.poisson(lw, -1.0, lpsi);                              // velocity_from_vorticity, ptns.cpp:85-91
-        c.mark("P_poisson_adi");
+        c.mark("P_poisson_solve");
         P.nonlinear(gw, lpsi, lw, gw, nl[nnew].p, ng[nnew].p);  // nonlinear_term(v, omega)
     }
     double koh, bw[4], iw[4] = {0, 0, 0, 0};
@@ -1025,8 +1077,8 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
     }
     DevSet& set = c.set(false, false, scale);
     if (c.prof_events.empty()) c.mark("start");
-    P.modal_solve(set, false, 2, sl, wl, ns, sg, wl, ns, lam[out].p, gam[out].p);
-    c.mark("H_helmholtz_adi");
+    P.modal_solve(set, false, 2, sl, wl, ns, sg, wl, ns, lam[out].p, gam[out].p, "H_rhs_combine");
+    c.mark("H_helmholtz_solve");
     const long T = P.T;
     finite_check_kernel<<<std::min<long>(1184, (T + 255) / 256), 256, 0, c.stream>>>(lam[out].p, T, dflag);
     finite_check_kernel<<<std::min<long>(1184, (T + 255) / 256), 256, 0, c.stream>>>(gam[out].p, T, dflag);

@@ -49,12 +49,14 @@ struct GemmPlan {
     const double** dDR = nullptr;
     long* dBoff = nullptr;
     long* dCoff = nullptr;
+    bool pipe = false;  // operands qualify for dgemm_pipe_kernel (set by upload)
     int M = 0, N = 0, K = 0;
     long lda = 0, ldb = 0, ldc = 0;
     double alpha = 1.0, beta = 0.0;
     void upload();
     void launch(cudaStream_t s, const double* b0 = nullptr, const double* b1 = nullptr, double* c0 = nullptr,
                 double* c1 = nullptr) const;
+    double flops() const { return 2.0 * M * N * K * double(A.size()); }  // every term is one M x N x K product
     ~GemmPlan();
 };
 
@@ -81,7 +83,8 @@ public:
     // (out_t = Solve(sum_i w_t[i] src_t[i])): fast diagonalization on the tensor cores, or the
     // ADI kernel (ctx flag bit 2 / sets without diagonalization data).
     void modal_solve(DevSet& set, bool full, int ntensor, const double* const* src0, const double* w0, int n0,
-                     const double* const* src1, const double* w1, int n1, double* out0, double* out1);
+                     const double* const* src1, const double* w1, int n1, double* out0, double* out1,
+                     const char* rhs_mark = nullptr);
     void decompose(const double* vr, const double* vt, const double* vz, double* lam, double* gam);
     void hpoisson(const double* rhs, double* u);
     void calculus(int op, int cls, const double* in, double* out);  // ops of include/ccf.h ccf_calculus

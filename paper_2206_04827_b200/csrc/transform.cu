@@ -119,10 +119,162 @@ __global__ void __launch_bounds__(128) dgemm_batched_kernel(GemmBatch g) {
                 if (r < g.M && c < g.N) {
                     double* dst = C + long(r) * g.ldc + c;
                     double v = g.alpha * acc[i][j][q];
-                    if (g.dl) v = v / (__ldg(g.dl[b] + r) + __ldg(g.dr[b] + c));
+                    if (g.dl) v *= __ldg(g.dl[b] + long(r) * g.N + c);  // 1 / (lambda_r + mu_c), M x N table
                     *dst = g.beta == 0.0 ? v : fma(g.beta, *dst, v);
                 }
             }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Batched DGEMM, pipelined variant: CTA tile 128 x 64 (8 warps of 32 x 32), BK = 16, 3-stage
+// cp.async (LDGSTS, 16-byte, zero-filled at the M / N / K edges) straight into shared memory.
+// Requires 16-byte aligned A / B bases and even lda / ldb (checked on the host: GemmPlan::upload).
+namespace {
+constexpr int PM = 128, PN = 64, PK = 16, PSTAGES = 3, PSA = PK + 4, PSB = PN + 4;
+constexpr int P_A_STAGE = PM * PSA, P_B_STAGE = PK * PSB;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int bytes) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+}  // namespace
+
+size_t dgemm_pipe_smem() { return size_t(PSTAGES) * (P_A_STAGE + P_B_STAGE) * sizeof(double); }
+
+// Persistent: CTA c processes items w = c, c + gridDim.x, ... (item = batch x m-tile x n-tile); the
+// load cursor runs PSTAGES - 1 k-tiles ahead across item boundaries, so the next item's operands
+// stream in while the current item's accumulators drain.
+__global__ void __launch_bounds__(256) dgemm_pipe_kernel(GemmBatch g) {
+    extern __shared__ __align__(16) double psm[];
+    double* As = psm;
+    double* Bs = psm + PSTAGES * P_A_STAGE;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int tn = (g.N + PN - 1) / PN, tm = (g.M + PM - 1) / PM, tmn = tm * tn;
+    const int nitems = g.nbatch * tmn;
+    const int nkt = (g.K + PK - 1) / PK;
+    struct Item {
+        int w, b, m0, n0, t0, nk;
+    };
+    auto decode = [&](int w) {
+        Item it{w, 0, 0, 0, 0, 0};
+        if (w >= nitems) return it;
+        it.b = w / tmn;
+        const int rem = w - it.b * tmn;
+        it.m0 = (rem / tn) * PM;
+        it.n0 = (rem - (rem / tn) * tn) * PN;
+        it.t0 = g.tstart ? g.tstart[it.b] : it.b;
+        it.nk = g.tstart ? (g.tstart[it.b + 1] - it.t0) * nkt : nkt;
+        return it;
+    };
+    // load cursor (item, k-tile), PSTAGES - 1 tiles ahead of the compute cursor
+    Item L = decode(blockIdx.x);
+    int lk = 0, lstage = 0;
+    const double* LA = nullptr;
+    const double* LB = nullptr;
+    int lterm = -1;
+    auto issue = [&]() {
+        while (L.w < nitems && lk >= L.nk) {
+            L = decode(L.w + gridDim.x);
+            lk = 0;
+        }
+        if (L.w < nitems) {
+            const int term = L.t0 + lk / nkt, k0 = (lk - (lk / nkt) * nkt) * PK;
+            if (term != lterm) {
+                lterm = term;
+                LA = g.A[term];
+                if (g.boff) {
+                    const long o = g.boff[term];
+                    LB = g.bbase[o >> kBaseShift] + (o & ((1L << kBaseShift) - 1));
+                } else {
+                    LB = g.B[term];
+                }
+            }
+            double* as = As + lstage * P_A_STAGE;
+            double* bs = Bs + lstage * P_B_STAGE;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // A: 128 rows x 8 chunks of 2 doubles
+                const int c = tid + q * 256;
+                const int row = c >> 3, kc = (c & 7) * 2;
+                const int gr = L.m0 + row, gk = k0 + kc;
+                const int nv = (gr < g.M) ? max(0, min(2, g.K - gk)) : 0;
+                const double* src = nv ? LA + long(gr) * g.lda + gk : LA;
+                cp_async16(as + row * PSA + kc, src, nv * 8);
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {  // B: 16 rows x 32 chunks
+                const int c = tid + q * 256;
+                const int row = c >> 5, cc = (c & 31) * 2;
+                const int gk = k0 + row, gc = L.n0 + cc;
+                const int nv = (gk < g.K) ? max(0, min(2, g.N - gc)) : 0;
+                const double* src = nv ? LB + long(gk) * g.ldb + gc : LB;
+                cp_async16(bs + row * PSB + cc, src, nv * 8);
+            }
+            ++lk;
+            lstage = lstage + 1 == PSTAGES ? 0 : lstage + 1;
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int s = 0; s < PSTAGES - 1; ++s) issue();
+    int cstage = 0;
+    for (int cw = blockIdx.x; cw < nitems; cw += gridDim.x) {
+        const Item I = decode(cw);
+        double acc[4][4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int kt = 0; kt < I.nk; ++kt) {
+            cp_async_wait<PSTAGES - 2>();
+            __syncthreads();
+            issue();
+            const double* as = As + cstage * P_A_STAGE;
+            const double* bs = Bs + cstage * P_B_STAGE;
+            cstage = cstage + 1 == PSTAGES ? 0 : cstage + 1;
+#pragma unroll
+            for (int ks = 0; ks < PK; ks += 4) {
+                double af[4], bf[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) af[i] = as[(wm + 8 * i + gq) * PSA + ks + tq];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) bf[j] = bs[(ks + tq) * PSB + wn + 8 * j + gq];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+            }
+        }
+        double* __restrict__ C;
+        if (g.coff) {
+            const long o = g.coff[I.b];
+            C = g.cbase[o >> kBaseShift] + (o & ((1L << kBaseShift) - 1));
+        } else {
+            C = g.C[I.b];
+        }
+        const double* __restrict__ dl = g.dl ? g.dl[I.b] : nullptr;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int r = I.m0 + wm + 8 * i + gq, c = I.n0 + wn + 8 * j + 2 * tq + q;
+                    if (r < g.M && c < g.N) {
+                        double* dst = C + long(r) * g.ldc + c;
+                        double v = g.alpha * acc[i][j][q];
+                        if (dl) v *= __ldg(dl + long(r) * g.N + c);
+                        *dst = g.beta == 0.0 ? v : fma(g.beta, *dst, v);
+                    }
+                }
+    }
+    cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -149,7 +149,7 @@ size_t dgemm_pipe_smem() { return size_t(PSTAGES) * (P_A_STAGE + P_B_STAGE) * si
 // Persistent: CTA c processes items w = c, c + gridDim.x, ... (item = batch x m-tile x n-tile); the
 // load cursor runs PSTAGES - 1 k-tiles ahead across item boundaries, so the next item's operands
 // stream in while the current item's accumulators drain.
-__global__ void __launch_bounds__(256) dgemm_pipe_kernel(GemmBatch g) {
+__global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmBatch g) {
     extern __shared__ __align__(16) double psm[];
     double* As = psm;
     double* Bs = psm + PSTAGES * P_A_STAGE;
@@ -259,20 +259,28 @@ __global__ void __launch_bounds__(256) dgemm_pipe_kernel(GemmBatch g) {
             C = g.C[I.b];
         }
         const double* __restrict__ dl = g.dl ? g.dl[I.b] : nullptr;
+        // paired columns (2 tq, 2 tq + 1) go out as one 16-byte store when aligned and in range
+        const bool vec = ((reinterpret_cast<uintptr_t>(C) | (uintptr_t(g.ldc) * 8)) & 15) == 0 && !dl && g.beta == 0.0;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < 4; ++j) {
+                const int r = I.m0 + wm + 8 * i + gq, c = I.n0 + wn + 8 * j + 2 * tq;
+                if (r >= g.M) continue;
+                double* dst = C + long(r) * g.ldc + c;
+                if (vec && c + 1 < g.N) {
+                    *reinterpret_cast<double2*>(dst) = make_double2(g.alpha * acc[i][j][0], g.alpha * acc[i][j][1]);
+                    continue;
+                }
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
-                    const int r = I.m0 + wm + 8 * i + gq, c = I.n0 + wn + 8 * j + 2 * tq + q;
-                    if (r < g.M && c < g.N) {
-                        double* dst = C + long(r) * g.ldc + c;
+                    if (c + q < g.N) {
                         double v = g.alpha * acc[i][j][q];
-                        if (dl) v *= __ldg(dl + long(r) * g.N + c);
-                        *dst = g.beta == 0.0 ? v : fma(g.beta, *dst, v);
+                        if (dl) v *= __ldg(dl + long(r) * g.N + c + q);
+                        dst[q] = g.beta == 0.0 ? v : fma(g.beta, dst[q], v);
                     }
                 }
+            }
     }
     cp_async_wait<0>();
 }

@@ -504,8 +504,9 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
         theta_attr_ = true;
     }
     if (g.p == 256 && !theta_generic_) {
-        const dim3 grid(unsigned((g.nh + 3) / 4), unsigned(g.mh));
-        theta_cross256_kernel<<<grid, 128, theta_cross256_smem(), c.stream>>>(t);
+        const int np = theta_cross256_positions();
+        const dim3 grid(unsigned((g.nh + np - 1) / np), unsigned(g.mh));
+        theta_cross256_kernel<<<grid, theta_cross256_threads(), theta_cross256_smem(), c.stream>>>(t);
     } else {
         const size_t smem = size_t(3) * tj * g.p * sizeof(double2);
         const dim3 grid(unsigned((g.nh + tj / 2 - 1) / (tj / 2)), unsigned(g.mh));

@@ -146,9 +146,6 @@ __device__ __forceinline__ void cp_async_wait() {
 
 size_t dgemm_pipe_smem() { return size_t(PSTAGES) * (P_A_STAGE + P_B_STAGE) * sizeof(double); }
 
-// Persistent: CTA c processes items w = c, c + gridDim.x, ... (item = batch x m-tile x n-tile); the
-// load cursor runs PSTAGES - 1 k-tiles ahead across item boundaries, so the next item's operands
-// stream in while the current item's accumulators drain.
 __global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmBatch g) {
     extern __shared__ __align__(16) double psm[];
     double* As = psm;
@@ -156,53 +153,38 @@ __global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmBatch g) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
     const int gq = lane >> 2, tq = lane & 3;
-    const int tn = (g.N + PN - 1) / PN, tm = (g.M + PM - 1) / PM, tmn = tm * tn;
-    const int nitems = g.nbatch * tmn;
+    // one (batch, m-tile, n-tile) item per CTA
+    const int tn = (g.N + PN - 1) / PN, tmn = ((g.M + PM - 1) / PM) * tn;
+    const int b = blockIdx.x / tmn;
+    const int rem = blockIdx.x - b * tmn;
+    const int m0 = (rem / tn) * PM, n0 = (rem - (rem / tn) * tn) * PN;
+    const int t0 = g.tstart ? g.tstart[b] : b, t1 = g.tstart ? g.tstart[b + 1] : b + 1;
     const int nkt = (g.K + PK - 1) / PK;
-    struct Item {
-        int w, b, m0, n0, t0, nk;
-    };
-    auto decode = [&](int w) {
-        Item it{w, 0, 0, 0, 0, 0};
-        if (w >= nitems) return it;
-        it.b = w / tmn;
-        const int rem = w - it.b * tmn;
-        it.m0 = (rem / tn) * PM;
-        it.n0 = (rem - (rem / tn) * tn) * PN;
-        it.t0 = g.tstart ? g.tstart[it.b] : it.b;
-        it.nk = g.tstart ? (g.tstart[it.b + 1] - it.t0) * nkt : nkt;
-        return it;
-    };
-    // load cursor (item, k-tile), PSTAGES - 1 tiles ahead of the compute cursor
-    Item L = decode(blockIdx.x);
-    int lk = 0, lstage = 0;
+    const int nk = (t1 - t0) * nkt;
+    // load cursor: term lt, k-tile lkt (nested counters, no divisions)
+    int lt = t0, lkt = 0, lstage = 0, issued = 0;
     const double* LA = nullptr;
     const double* LB = nullptr;
-    int lterm = -1;
-    auto issue = [&]() {
-        while (L.w < nitems && lk >= L.nk) {
-            L = decode(L.w + gridDim.x);
-            lk = 0;
+    auto set_term = [&]() {
+        LA = g.A[lt];
+        if (g.boff) {
+            const long o = g.boff[lt];
+            LB = g.bbase[o >> kBaseShift] + (o & ((1L << kBaseShift) - 1));
+        } else {
+            LB = g.B[lt];
         }
-        if (L.w < nitems) {
-            const int term = L.t0 + lk / nkt, k0 = (lk - (lk / nkt) * nkt) * PK;
-            if (term != lterm) {
-                lterm = term;
-                LA = g.A[term];
-                if (g.boff) {
-                    const long o = g.boff[term];
-                    LB = g.bbase[o >> kBaseShift] + (o & ((1L << kBaseShift) - 1));
-                } else {
-                    LB = g.B[term];
-                }
-            }
+    };
+    if (nk > 0) set_term();
+    auto issue = [&]() {
+        if (issued < nk) {
+            const int k0 = lkt * PK;
             double* as = As + lstage * P_A_STAGE;
             double* bs = Bs + lstage * P_B_STAGE;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {  // A: 128 rows x 8 chunks of 2 doubles
                 const int c = tid + q * 256;
                 const int row = c >> 3, kc = (c & 7) * 2;
-                const int gr = L.m0 + row, gk = k0 + kc;
+                const int gr = m0 + row, gk = k0 + kc;
                 const int nv = (gr < g.M) ? max(0, min(2, g.K - gk)) : 0;
                 const double* src = nv ? LA + long(gr) * g.lda + gk : LA;
                 cp_async16(as + row * PSA + kc, src, nv * 8);
@@ -211,78 +193,80 @@ __global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmBatch g) {
             for (int q = 0; q < 2; ++q) {  // B: 16 rows x 32 chunks
                 const int c = tid + q * 256;
                 const int row = c >> 5, cc = (c & 31) * 2;
-                const int gk = k0 + row, gc = L.n0 + cc;
+                const int gk = k0 + row, gc = n0 + cc;
                 const int nv = (gk < g.K) ? max(0, min(2, g.N - gc)) : 0;
                 const double* src = nv ? LB + long(gk) * g.ldb + gc : LB;
                 cp_async16(bs + row * PSB + cc, src, nv * 8);
             }
-            ++lk;
+            ++issued;
             lstage = lstage + 1 == PSTAGES ? 0 : lstage + 1;
+            if (++lkt == nkt && issued < nk) {
+                lkt = 0;
+                ++lt;
+                set_term();
+            }
         }
         cp_async_commit();
     };
 #pragma unroll
     for (int s = 0; s < PSTAGES - 1; ++s) issue();
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     int cstage = 0;
-    for (int cw = blockIdx.x; cw < nitems; cw += gridDim.x) {
-        const Item I = decode(cw);
-        double acc[4][4][2];
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<PSTAGES - 2>();
+        __syncthreads();
+        issue();
+        const double* as = As + cstage * P_A_STAGE;
+        const double* bs = Bs + cstage * P_B_STAGE;
+        cstage = cstage + 1 == PSTAGES ? 0 : cstage + 1;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int ks = 0; ks < PK; ks += 4) {
+            double af[4], bf[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-        for (int kt = 0; kt < I.nk; ++kt) {
-            cp_async_wait<PSTAGES - 2>();
-            __syncthreads();
-            issue();
-            const double* as = As + cstage * P_A_STAGE;
-            const double* bs = Bs + cstage * P_B_STAGE;
-            cstage = cstage + 1 == PSTAGES ? 0 : cstage + 1;
+            for (int i = 0; i < 4; ++i) af[i] = as[(wm + 8 * i + gq) * PSA + ks + tq];
 #pragma unroll
-            for (int ks = 0; ks < PK; ks += 4) {
-                double af[4], bf[4];
+            for (int j = 0; j < 4; ++j) bf[j] = bs[(ks + tq) * PSB + wn + 8 * j + gq];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) af[i] = as[(wm + 8 * i + gq) * PSA + ks + tq];
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) bf[j] = bs[(ks + tq) * PSB + wn + 8 * j + gq];
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-            }
+                for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
-        double* __restrict__ C;
-        if (g.coff) {
-            const long o = g.coff[I.b];
-            C = g.cbase[o >> kBaseShift] + (o & ((1L << kBaseShift) - 1));
-        } else {
-            C = g.C[I.b];
-        }
-        const double* __restrict__ dl = g.dl ? g.dl[I.b] : nullptr;
-        // paired columns (2 tq, 2 tq + 1) go out as one 16-byte store when aligned and in range
-        const bool vec = ((reinterpret_cast<uintptr_t>(C) | (uintptr_t(g.ldc) * 8)) & 15) == 0 && !dl && g.beta == 0.0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int r = I.m0 + wm + 8 * i + gq, c = I.n0 + wn + 8 * j + 2 * tq;
-                if (r >= g.M) continue;
-                double* dst = C + long(r) * g.ldc + c;
-                if (vec && c + 1 < g.N) {
-                    *reinterpret_cast<double2*>(dst) = make_double2(g.alpha * acc[i][j][0], g.alpha * acc[i][j][1]);
-                    continue;
-                }
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    if (c + q < g.N) {
-                        double v = g.alpha * acc[i][j][q];
-                        if (dl) v *= __ldg(dl + long(r) * g.N + c + q);
-                        dst[q] = g.beta == 0.0 ? v : fma(g.beta, dst[q], v);
-                    }
-                }
-            }
     }
     cp_async_wait<0>();
+    double* __restrict__ C;
+    if (g.coff) {
+        const long o = g.coff[b];
+        C = g.cbase[o >> kBaseShift] + (o & ((1L << kBaseShift) - 1));
+    } else {
+        C = g.C[b];
+    }
+    const double* __restrict__ dl = g.dl ? g.dl[b] : nullptr;
+    // paired columns (2 tq, 2 tq + 1) go out as one 16-byte store when aligned and in range
+    const bool vec = ((reinterpret_cast<uintptr_t>(C) | (uintptr_t(g.ldc) * 8)) & 15) == 0 && !dl && g.beta == 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r = m0 + wm + 8 * i + gq, c = n0 + wn + 8 * j + 2 * tq;
+            if (r >= g.M) continue;
+            double* dst = C + long(r) * g.ldc + c;
+            if (vec && c + 1 < g.N) {
+                *reinterpret_cast<double2*>(dst) = make_double2(g.alpha * acc[i][j][0], g.alpha * acc[i][j][1]);
+                continue;
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                if (c + q < g.N) {
+                    double v = g.alpha * acc[i][j][q];
+                    if (dl) v *= __ldg(dl + long(r) * g.N + c + q);
+                    dst[q] = g.beta == 0.0 ? v : fma(g.beta, dst[q], v);
+                }
+            }
+        }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -492,7 +476,8 @@ __device__ __forceinline__ void dft16(double2 (&v)[16]) {
 }
 __device__ __forceinline__ int d16(int k) { return 4 * (k & 3) + (k >> 2); }  // slot of X[k] after dft16
 
-constexpr int kT256Pts = 8;    // points per CTA
+constexpr int kT256Pts = 4;    // points per CTA (2 z positions x {+z, -z}); 16 threads per point
+constexpr int kT256Pos = kT256Pts / 2;
 constexpr int kT256Arr = 272;  // complex slots per array (16 x 17 transposed layout)
 
 // pass 1 of a 256-point DFT on Z (natural order): DFT over n1 of x[16 n1 + lane], twiddle,
@@ -522,14 +507,14 @@ __device__ __forceinline__ void f256_pass2(double2* Z, int lane, unsigned gmask)
 
 }  // namespace
 
-__global__ void __launch_bounds__(128, 2) theta_cross256_kernel(ThetaCross t) {
+__global__ void __launch_bounds__(16 * kT256Pts, 4) theta_cross256_kernel(ThetaCross t) {
     extern __shared__ double2 sd[];
     double2* twf = sd + kT256Pts * 3 * kT256Arr;
     const Geo& g = t.g;
     const int S = g.nslots;  // 129
     const int jr = blockIdx.y;
-    const int i0 = blockIdx.x * 4;
-    const int npos = min(4, g.nh - i0);
+    const int i0 = blockIdx.x * kT256Pos;
+    const int npos = min(kT256Pos, g.nh - i0);
     const int tid = threadIdx.x;
     for (int x = tid; x < 256; x += blockDim.x) {
         const int e = (x >> 4) * (x & 15);  // k1 * lane < 256
@@ -545,7 +530,7 @@ __global__ void __launch_bounds__(128, 2) theta_cross256_kernel(ThetaCross t) {
         const double* fa = t.in[2 * pr] + off;
         const double* fb = t.in[2 * pr + 1] + off;
 #pragma unroll
-        for (int ip = 0; ip < 4; ++ip) {
+        for (int ip = 0; ip < kT256Pos; ++ip) {
             double ar = 0.0, ai = 0.0, aro = 0.0, aio = 0.0, br = 0.0, bi = 0.0, bro = 0.0, bio = 0.0;
             if (ip < npos) {
                 ar = fa[ip];
@@ -572,7 +557,7 @@ __global__ void __launch_bounds__(128, 2) theta_cross256_kernel(ThetaCross t) {
     const int grp = tid >> 4, lane = tid & 15;
     const unsigned gmask = 0xFFFFu << (16 * (grp & 1));
     // ---- inverse transforms (synthesis in theta): 24 arrays, 8 groups
-    for (int a = grp; a < kT256Pts * 3; a += 8) {
+    for (int a = grp; a < kT256Pts * 3; a += kT256Pts) {
         double2* Z = sd + a * kT256Arr;
         double2 v[16];
 #pragma unroll
@@ -616,7 +601,7 @@ __global__ void __launch_bounds__(128, 2) theta_cross256_kernel(ThetaCross t) {
         const long off = long(s) * g.slot_stride + long(jr) * g.n + i0;
         double* o = t.out[f] + off;
 #pragma unroll
-        for (int ip = 0; ip < 4; ++ip) {
+        for (int ip = 0; ip < kT256Pos; ++ip) {
             if (ip >= npos) break;
             double xr[2], xi[2];
 #pragma unroll
@@ -640,6 +625,8 @@ __global__ void __launch_bounds__(128, 2) theta_cross256_kernel(ThetaCross t) {
 }
 
 size_t theta_cross256_smem() { return (size_t(kT256Pts) * 3 * kT256Arr + 256) * sizeof(double2); }
+int theta_cross256_positions() { return kT256Pos; }
+int theta_cross256_threads() { return 16 * kT256Pts; }
 
 // Full-spectrum complex theta DFT for the API transforms (any even p):
 // data [l][k][j] complex interleaved; dir = +1 synthesis (c -> values), -1 analysis.

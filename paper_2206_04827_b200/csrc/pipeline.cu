@@ -575,6 +575,10 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     double* Z[2][3];
     for (int pr = 0; pr < 2; ++pr)
         for (int x = 0; x < 3; ++x) Z[pr][x] = scratch(3 * pr + x);
+    // the velocity's lambda is the vorticity's gamma (velocity_from_vorticity, ptns.cpp:85-91):
+    // synthesize that tensor once
+    const bool alias = lam_v == gam_w;
+    if (alias) Z[0][0] = Z[1][1];
     double* val[6];
     for (int i = 0; i < 6; ++i) val[i] = scratch(6 + i);
     double* av[3] = {scratch(12), scratch(13), scratch(14)};
@@ -584,10 +588,12 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     const int cls0[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     bool fresh;
     // ---- z synthesis: 6 tensors, two nh x nh halves per (slot, plane)
-    GemmPlan& zs = gemm(ptr_key("nzs", 6, keyp, keyp, cls0), fresh);
+    const int acls[8] = {int(alias), 0, 0, 0, 0, 0, 0, 0};
+    GemmPlan& zs = gemm(ptr_key("nzs", 6, keyp, keyp, acls), fresh);
     if (fresh) {
         for (int pr = 0; pr < 2; ++pr)
             for (int x = 0; x < 3; ++x) {
+                if (alias && pr == 0 && x == 0) continue;
                 const double* src = x == 0 ? lam[pr] : gam[pr];
                 const double* mat = x == 2 ? tp.DzS.p : tp.Sz.p;
                 for (int s = 0; s < g.nslots; ++s)

@@ -522,25 +522,26 @@ __global__ void __launch_bounds__(16 * kT256Pts, 4) theta_cross256_kernel(ThetaC
     }
     // ---- gather the Hermitian spectra of the pairs (v_r, v_t), (v_z, w_r), (w_t, w_z) at 8 points
     const long ps = g.plane_stride, oo = g.nh;
+#pragma unroll 2
     for (int e = tid; e < S * 3; e += blockDim.x) {
         const int s = e % S, pr = e / S;
         const double sg = (s & 1) ? -1.0 : 1.0;  // (-1)^w (w = s, or -128 for the Nyquist slot s = 128)
         const bool reonly = (s == 0 || s == 128);
         const long off = long(s) * g.slot_stride + long(jr) * g.n + i0;
-        const double* fa = t.in[2 * pr] + off;
-        const double* fb = t.in[2 * pr + 1] + off;
+        const double* __restrict__ fa = t.in[2 * pr] + off;
+        const double* __restrict__ fb = t.in[2 * pr + 1] + off;
 #pragma unroll
         for (int ip = 0; ip < kT256Pos; ++ip) {
             double ar = 0.0, ai = 0.0, aro = 0.0, aio = 0.0, br = 0.0, bi = 0.0, bro = 0.0, bio = 0.0;
             if (ip < npos) {
-                ar = fa[ip];
-                ai = fa[ps + ip];
-                aro = fa[oo + ip];
-                aio = fa[oo + ps + ip];
-                br = fb[ip];
-                bi = fb[ps + ip];
-                bro = fb[oo + ip];
-                bio = fb[oo + ps + ip];
+                ar = __ldg(fa + ip);
+                ai = __ldg(fa + ps + ip);
+                aro = __ldg(fa + oo + ip);
+                aio = __ldg(fa + oo + ps + ip);
+                br = __ldg(fb + ip);
+                bi = __ldg(fb + ps + ip);
+                bro = __ldg(fb + oo + ip);
+                bio = __ldg(fb + oo + ps + ip);
             }
 #pragma unroll
             for (int h = 0; h < 2; ++h) {

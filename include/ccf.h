@@ -141,6 +141,12 @@ ccf_status ccf_ns_profile_step(ccf_ns_state* st, double* ms, int* nstages, char*
 ccf_status ccf_plan_host(int m, int n, int w, double scale, int poisson, double tol, int flags, double* info, double* u,
                          double* v, int cap);
 
+/* Host-only (no GPU) check of the fast-diagonalization solver data of one mode: relative residual
+ * ||A X B + C X D - E|| / ||E|| (long double) of the device arithmetic (four double products) on a
+ * seeded random RHS, for wavenumber w, k-parity k0, Poisson or Helmholtz(scale). */
+ccf_status ccf_diag_host_check(int m, int n, int w, double scale, int poisson, int k0, unsigned long long seed,
+                               double* residual);
+
 /* Message of the last failed ccf_ctx_create / ccf_plan_host on this thread. */
 const char* ccf_create_error(void);
 const char* ccf_version(void);

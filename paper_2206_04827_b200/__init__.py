@@ -76,7 +76,8 @@ EXPORTS = ["ccf_ctx_create", "ccf_ctx_destroy", "ccf_ctx_set_stream", "ccf_ctx_s
            "ccf_nonlinear", "ccf_ns_create", "ccf_ns_step", "ccf_ns_get_omega", "ccf_ns_destroy",
            "ccf_get_last_error", "ccf_get_stats", "ccf_reset_stats", "ccf_modal_plan", "ccf_version",
            "ccf_ns_profile_step", "ccf_ns_set_graphs", "ccf_ns_launches_per_step", "ccf_plan_host",
-           "ccf_create_error", "ccf_adi_last_rounds", "ccf_adi_keep_history", "ccf_get_gemm_flops"]
+           "ccf_create_error", "ccf_adi_last_rounds", "ccf_adi_keep_history", "ccf_get_gemm_flops",
+           "ccf_diag_host_check"]
 
 _lib = None
 
@@ -126,6 +127,7 @@ def lib():
         L.ccf_adi_last_rounds.argtypes = [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), vp, vp, C.c_int]
         L.ccf_adi_keep_history.argtypes = [vp, C.c_int]
         L.ccf_get_gemm_flops.argtypes = [vp, dp]
+        L.ccf_diag_host_check.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_ulonglong, dp]
         L.ccf_get_stats.argtypes = [vp, C.POINTER(C.c_long), C.POINTER(C.c_long), C.POINTER(C.c_int), dp,
                                     C.POINTER(C.c_long)]
         L.ccf_reset_stats.argtypes = [vp]
@@ -322,6 +324,16 @@ class Context:
                                               h.ctypes.data, cap))
         n = nt.value * ns.value
         return r[:n].reshape(nt.value, ns.value), h[: 4 * n].reshape(nt.value, ns.value, 4)
+
+
+def diag_host_check(m, n, w, scale=1.0, poisson=True, k0=0, seed=1):
+    """Relative Sylvester residual of the fast-diagonalization data of one mode (host only, no GPU)."""
+    r = C.c_double()
+    st = lib().ccf_diag_host_check(int(m), int(n), int(w), C.c_double(scale), int(poisson), int(k0), int(seed),
+                                   C.byref(r))
+    if st != 0:
+        raise _ERR.get(st, CCFError)(lib().ccf_create_error().decode())
+    return r.value
 
 
 def plan_host(m, n, w, scale=1.0, poisson=True, tol=1e-12, q2_endpoint_pad=False):

@@ -559,6 +559,24 @@ ccf_status ccf_ns_profile_step(ccf_ns_state* st, double* ms, int* nstages, char*
 extern "C" {
 // Host-only modal shift plan (no GPU needed): the same setup path the context uses
 // (spectral enclosure + Zolotarev shifts, proj/src/solvers.cpp:46-75, adi.cpp:22-104).
+ccf_status ccf_diag_host_check(int m, int n, int w, double scale, int poisson, int k0, unsigned long long seed,
+                               double* residual) {
+    try {
+        if (m < 6 || n < 6 || m % 2 || n % 2) throw Error(ccf::DOMAIN_ERROR, "ccf_diag_host_check: even m, n >= 6 required");
+        ccf::SizeOps so(m, n);
+        std::map<int, ccf::Range> cache;
+        ccf::SolverSet set = ccf::build_solver_set(so, {w}, poisson != 0, scale, 1e-12, cache, false, 4.0, true);
+        *residual = ccf::diag_check_residual(set, 0, k0 & 1, (m - 2) / 2, (n - 2) / 2, seed);
+        return CCF_OK;
+    } catch (const Error& e) {
+        g_create_err = e.what();
+        return ccf_status(e.status);
+    } catch (const std::exception& e) {
+        g_create_err = e.what();
+        return CCF_INTERNAL_ERROR;
+    }
+}
+
 ccf_status ccf_plan_host(int m, int n, int w, double scale, int poisson, double tol, int flags, double* info, double* u,
                          double* v, int cap) {
     try {

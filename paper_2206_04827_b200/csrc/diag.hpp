@@ -39,4 +39,5 @@ DiagLeft diag_left(const CBand& A, const CBand& C, const CBand& R2, int M, int m
 // B^ = Bt^T, D^ = Dt^T) and C02 (rows N, cols nh, offsets 0..2).
 DiagRight diag_right(const CBand& Bt, const CBand& Dt, const CBand& C02, int N, int nh);
 
+
 }  // namespace ccf

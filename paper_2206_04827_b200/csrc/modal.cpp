@@ -445,4 +445,79 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
     return set;
 }
 
+double diag_check_residual(const SolverSet& set, int slot, int k0, int M, int N, unsigned long long seed) {
+    if (!set.has_diag) throw Error(DOMAIN_ERROR, "diag_check_residual: set has no diagonalization data");
+    const int mh = M + 1, nh = N + 1, Mp = M + (M & 1), Np = N + (N & 1);
+    auto even = [](long x) { return x + (x & 1); };
+    const double* dg = set.dg.data();
+    const long PLo = set.dg_left[size_t(slot)], QLo = PLo + long(M) * mh, LAMo = QLo + long(mh) * Mp,
+               RTo = LAMo + even(M) + long(k0) * even(long(M) * N);
+    const long PRo = set.dg_right[k0], QRo = PRo + long(nh) * Np;
+    std::vector<double> f(size_t(mh) * nh);
+    unsigned long long st = seed * 0x9E3779B97F4A7C15ull + 1;
+    for (double& x : f) {
+        st = st * 6364136223846793005ull + 1442695040888963407ull;
+        x = double(st >> 11) / 9007199254740992.0 - 0.5;
+    }
+    auto mm = [](const double* A, int lda, const double* B, int ldb, int r, int k, int c) {
+        std::vector<double> C(size_t(r) * c, 0.0);
+        for (int i = 0; i < r; ++i)
+            for (int q = 0; q < k; ++q) {
+                const double a = A[size_t(i) * lda + q];
+                if (a == 0.0) continue;
+                for (int j = 0; j < c; ++j) C[size_t(i) * c + j] = std::fma(a, B[size_t(q) * ldb + j], C[size_t(i) * c + j]);
+            }
+        return C;
+    };
+    std::vector<double> T1 = mm(dg + PLo, mh, f.data(), nh, M, mh, nh);
+    std::vector<double> Z = mm(T1.data(), nh, dg + PRo, Np, M, nh, N);
+    for (int i = 0; i < M; ++i)
+        for (int j = 0; j < N; ++j) Z[size_t(i) * N + j] *= dg[RTo + long(i) * N + j];
+    std::vector<double> T3 = mm(dg + QLo, Mp, Z.data(), N, mh, M, N);
+    std::vector<double> u = mm(T3.data(), N, dg + QRo, nh, mh, N, nh);
+    // X = S_r^-1 u S_z^-T: u[a][b] = X[a][b] - X[a-1][b] - X[a][b-1] + X[a-1][b-1] -> prefix sums
+    std::vector<long double> X(size_t(M) * N, 0.0L);
+    for (int a = 0; a < M; ++a)
+        for (int b = 0; b < N; ++b) {
+            long double v = u[size_t(a) * nh + b];
+            if (a > 0) v += X[size_t(a - 1) * N + b];
+            if (b > 0) v += X[size_t(a) * N + b - 1];
+            if (a > 0 && b > 0) v -= X[size_t(a - 1) * N + b - 1];
+            X[size_t(a) * N + b] = v;
+        }
+    const AdiSlot& so = set.slots[size_t(slot)];
+    const double* sl = set.coef.data() + so.sleft;
+    const double* sr = set.coef.data() + (k0 ? so.sright1 : so.sright0);
+    auto fx = [&](int i, int j) -> long double { return (i >= 0 && i < mh && j >= 0 && j < nh) ? f[size_t(i) * nh + j] : 0.0L; };
+    auto xx = [&](int i, int j) -> long double { return (i >= 0 && i < M && j >= 0 && j < N) ? X[size_t(i) * N + j] : 0.0L; };
+    long double rr = 0.0L, ee = 0.0L;
+    for (int a = 0; a < M; ++a)
+        for (int b = 0; b < N; ++b) {
+            // E = R2 f C02^T: rows via sleft 0..5 (d = -2..3), columns via sright 0..3 (d = -1..2)
+            long double e = 0.0L, r = 0.0L;
+            for (int dc = -1; dc <= 2; ++dc) {
+                const long double cz = sr[size_t(b) * kStatW + size_t(dc + 1)];
+                if (cz == 0.0L) continue;
+                long double t = 0.0L;
+                for (int da = -2; da <= 3; ++da) t += (long double)sl[size_t(a) * kStatW + size_t(da + 2)] * fx(a + da, b + dc);
+                e += cz * t;
+            }
+            // A X B^ + C X D^: left rows sleft 6..11 / 12..17, right sright 12..15 / 16..19
+            for (int da = -2; da <= 3; ++da) {
+                const long double ca = sl[size_t(a) * kStatW + 6 + size_t(da + 2)];
+                const long double cc = sl[size_t(a) * kStatW + 12 + size_t(da + 2)];
+                if (ca == 0.0L && cc == 0.0L) continue;
+                long double xb = 0.0L, xd = 0.0L;
+                for (int dc = -1; dc <= 2; ++dc) {
+                    xb += (long double)sr[size_t(b) * kStatW + 12 + size_t(dc + 1)] * xx(a + da, b + dc);
+                    xd += (long double)sr[size_t(b) * kStatW + 16 + size_t(dc + 1)] * xx(a + da, b + dc);
+                }
+                r += ca * xb + cc * xd;
+            }
+            rr += (r - e) * (r - e);
+            ee += e * e;
+        }
+    return double(std::sqrt(rr / ee));
+}
+
 }  // namespace ccf

@@ -57,4 +57,10 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
                            std::map<int, Range>& radial_cache, bool q2_pad, double plan_margin = 1.0,
                            bool with_diag = false);
 
+// Host check of the packed fast-diagonalization data of one (slot, k-parity) sub-problem: for a
+// seeded random RHS f (mh x nh), u = QL [(PL f PR) .* RT] QR in double (the device arithmetic),
+// X = S_r^-1 u S_z^-T, and the relative Sylvester residual ||A X B^ + C X D^ - R2 f C02^T|| /
+// ||R2 f C02^T|| in long double from the static operator blocks the ADI kernel uses.
+double diag_check_residual(const SolverSet& set, int slot, int k0, int M, int N, unsigned long long seed);
+
 }  // namespace ccf

@@ -499,11 +499,19 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
         CCF_CUDA(cudaFuncSetAttribute(theta_cross_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CCF_CUDA(cudaFuncSetAttribute(theta_cross256_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(theta_cross256_smem())));
+        CCF_CUDA(cudaFuncSetAttribute(theta_cross256w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(theta_cross256w_smem())));
+        const char* v = std::getenv("CCF_THETA_VARIANT");  // "16": 16-thread FFT kernel
+        theta_w_ = !(v && v[0] == '1' && v[1] == '6');
         const char* e = std::getenv("CCF_THETA_GENERIC");
         theta_generic_ = e && e[0] == '1';
         theta_attr_ = true;
     }
-    if (g.p == 256 && !theta_generic_) {
+    if (g.p == 256 && !theta_generic_ && theta_w_) {
+        const int np = theta_cross256w_positions();
+        const dim3 grid(unsigned((g.nh + np - 1) / np), unsigned(g.mh));
+        theta_cross256w_kernel<<<grid, theta_cross256w_threads(), theta_cross256w_smem(), c.stream>>>(t);
+    } else if (g.p == 256 && !theta_generic_) {
         const int np = theta_cross256_positions();
         const dim3 grid(unsigned((g.nh + np - 1) / np), unsigned(g.mh));
         theta_cross256_kernel<<<grid, theta_cross256_threads(), theta_cross256_smem(), c.stream>>>(t);

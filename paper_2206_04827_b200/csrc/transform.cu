@@ -625,6 +625,229 @@ __global__ void __launch_bounds__(16 * kT256Pts, 4) theta_cross256_kernel(ThetaC
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// p = 256, warp-per-point variant: 32 lanes per 256-point FFT as 16 lane pairs; in every radix-16
+// pass each lane loads the 16 inputs of its column and produces the 8 outputs of one parity
+// (half-DFT16 = radix-2 split + DFT8). The three (v, w) pairs are synthesized one after the other
+// through a single shared array per point (their time samples stay in registers: lane (k1, h)
+// holds l = k1 + 16 k2 for k2 = h (mod 2)), so the cross product and the first forward pass run in
+// registers (the k2-parity halves combine through one shuffle). 8.5 KB of shared memory per point
+// instead of 12.75 KB and twice the threads: 16 warps per SM instead of 8.
+namespace {
+
+template <int S>
+__device__ __forceinline__ double2 w8mul(double2 x, int n) {  // x * W8^n, W8 = e^{S 2 pi i / 8}, n in 0..3
+    constexpr double c = 0.70710678118654752440;
+    switch (n) {
+        case 1: return cmul(x, make_double2(c, S * c));
+        case 2: return S > 0 ? make_double2(-x.y, x.x) : make_double2(x.y, -x.x);
+        case 3: return cmul(x, make_double2(-c, S * c));
+        default: return x;
+    }
+}
+
+// in-place DFT8, natural-order output
+template <int S>
+__device__ __forceinline__ void dft8(double2 (&v)[8]) {
+    double2 a[4], b[4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+        a[n] = cadd(v[n], v[n + 4]);
+        b[n] = w8mul<S>(csub(v[n], v[n + 4]), n);
+    }
+    r4<S>(a[0], a[1], a[2], a[3]);
+    r4<S>(b[0], b[1], b[2], b[3]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[2 * k] = a[k];
+        v[2 * k + 1] = b[k];
+    }
+}
+
+// outputs X[2k + h], k = 0..7, of the DFT16 of x[0..15] (W16 = e^{S 2 pi i / 16})
+template <int S>
+__device__ __forceinline__ void half_dft16(const double2 (&x)[16], int h, double2 (&out)[8]) {
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+        const double2 sum = cadd(x[n], x[n + 8]);
+        const double2 dif = csub(x[n], x[n + 8]);
+        out[n] = h ? tw16<S>(dif, n) : sum;
+    }
+    // tw16 covers the exponents of the radix-4 x radix-4 DFT16; here the radix-2 twiddles W16^n,
+    // n = 0..7, are applied explicitly below for n = 5 and 7 (tw16 handles 1, 2, 3, 4, 6)
+    if (h) {
+        constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
+        out[5] = cmul(csub(x[5], x[13]), make_double2(-s1, S * c1));
+        out[7] = cmul(csub(x[7], x[15]), make_double2(-c1, S * s1));
+    }
+    dft8<S>(out);
+}
+
+constexpr int kTWPts = 4;  // points per CTA (2 z positions x {+z, -z}), one warp each
+constexpr int kTWArr = 272;
+
+}  // namespace
+
+__global__ void __launch_bounds__(32 * kTWPts, 4) theta_cross256w_kernel(ThetaCross t) {
+    extern __shared__ double2 sd[];
+    double2* twf = sd + kTWPts * 2 * kTWArr;  // twf[16 k1 + n2] = e^{-2 pi i n2 k1 / 256}
+    const Geo& g = t.g;
+    const int S = g.nslots;  // 129
+    const int jr = blockIdx.y;
+    const int i0 = blockIdx.x * (kTWPts / 2);
+    const int npos = min(kTWPts / 2, g.nh - i0);
+    const int tid = threadIdx.x;
+    const int pt = tid >> 5, lane = tid & 31, col = lane & 15, h = lane >> 4;
+    for (int x = tid; x < 256; x += blockDim.x) {
+        const int e = (x >> 4) * (x & 15);
+        twf[x] = e < 128 ? t.tw[e] : make_double2(-t.tw[e - 128].x, -t.tw[e - 128].y);
+    }
+    double2* Z = sd + pt * 2 * kTWArr;  // this point's two arrays
+    double2 tv[3][8];                   // time samples of the three pairs at l = col + 16 (2j + h)
+    const long ps = g.plane_stride, oo = g.nh;
+#pragma unroll
+    for (int pr = 0; pr < 3; ++pr) {
+        __syncthreads();  // previous pair's array fully consumed (and twiddles visible)
+        // ---- gather the Hermitian spectrum of pair pr for the CTA's points into array 0
+        for (int s = tid; s < S; s += blockDim.x) {
+            const double sg = (s & 1) ? -1.0 : 1.0;
+            const bool reonly = (s == 0 || s == 128);
+            const long off = long(s) * g.slot_stride + long(jr) * g.n + i0;
+            const double* __restrict__ fa = t.in[2 * pr] + off;
+            const double* __restrict__ fb = t.in[2 * pr + 1] + off;
+#pragma unroll
+            for (int ip = 0; ip < kTWPts / 2; ++ip) {
+                double ar = 0.0, ai = 0.0, aro = 0.0, aio = 0.0, br = 0.0, bi = 0.0, bro = 0.0, bio = 0.0;
+                if (ip < npos) {
+                    ar = __ldg(fa + ip);
+                    ai = __ldg(fa + ps + ip);
+                    aro = __ldg(fa + oo + ip);
+                    aio = __ldg(fa + oo + ps + ip);
+                    br = __ldg(fb + ip);
+                    bi = __ldg(fb + ps + ip);
+                    bro = __ldg(fb + oo + ip);
+                    bio = __ldg(fb + oo + ps + ip);
+                }
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const double sz = hh ? -1.0 : 1.0;
+                    const double xar = sg * fma(sz, aro, ar), xai = reonly ? 0.0 : sg * fma(sz, aio, ai);
+                    const double xbr = sg * fma(sz, bro, br), xbi = reonly ? 0.0 : sg * fma(sz, bio, bi);
+                    double2* Zp = sd + (2 * ip + hh) * 2 * kTWArr;
+                    Zp[s] = make_double2(xar - xbi, xai + xbr);
+                    if (s > 0 && s < 128) Zp[256 - s] = make_double2(xar + xbi, xbr - xai);
+                }
+            }
+        }
+        __syncthreads();
+        // ---- inverse pass 1: lane (n2 = col, h): DFT16 over n1 of x[16 n1 + n2] -> k1 = 2k + h
+        {
+            double2 x[16], o[8];
+#pragma unroll
+            for (int n1 = 0; n1 < 16; ++n1) x[n1] = Z[16 * n1 + col];
+            __syncwarp();
+            half_dft16<+1>(x, h, o);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int k1 = 2 * k + h;
+                double2 w = twf[16 * k1 + col];
+                w.y = -w.y;
+                Z[k1 * 17 + col] = cmul(o[k], w);
+            }
+            __syncwarp();
+            // ---- inverse pass 2: lane (k1 = col, h): DFT16 over n2 -> samples l = k1 + 16 (2j + h)
+#pragma unroll
+            for (int n2 = 0; n2 < 16; ++n2) x[n2] = Z[col * 17 + n2];
+            half_dft16<+1>(x, h, tv[pr]);
+        }
+    }
+    // ---- cross product a = v x w (ptns.cpp:127-132) at this lane's 8 samples
+    double2 ya[8], yz[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const double vr = tv[0][j].x, vt = tv[0][j].y, vz = tv[1][j].x, wr = tv[1][j].y, wt = tv[2][j].x,
+                     wz = tv[2][j].y;
+        ya[j] = make_double2(vt * wz - vz * wt, vz * wr - vr * wz);  // a_r + i a_t
+        yz[j] = make_double2(vr * wt - vt * wr, 0.0);               // a_z
+    }
+    // ---- forward pass 1 (DFT16 over k2 for k1 = col): this lane holds k2 = 2j + h; radix-2 combine
+    //      with the partner lane (h ^ 1), then twiddle and transpose into arrays 0 (a_r + i a_t), 1 (a_z)
+    __syncthreads();  // all warps done with array 0 of every point
+    dft8<-1>(ya);
+    dft8<-1>(yz);
+    {
+        constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, c2 = 0.70710678118654752440;
+        const double2 w16[8] = {make_double2(1.0, 0.0), make_double2(c1, -s1), make_double2(c2, -c2),
+                                make_double2(s1, -c1), make_double2(0.0, -1.0), make_double2(-s1, -c1),
+                                make_double2(-c2, -c2), make_double2(-c1, -s1)};
+        auto combine = [&](double2 (&y)[8], double2* T) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                // E = even-k2 DFT8 (lane h = 0), O = odd-k2 DFT8 (lane h = 1)
+                const double ox = __shfl_xor_sync(0xffffffffu, y[k].x, 16);
+                const double oy = __shfl_xor_sync(0xffffffffu, y[k].y, 16);
+                const double2 E = h ? make_double2(ox, oy) : y[k];
+                const double2 O = h ? y[k] : make_double2(ox, oy);
+                const double2 wo = cmul(O, w16[k]);
+                const double2 Y = h ? csub(E, wo) : cadd(E, wo);  // Y[k + 8 h]
+                const int kp = k + 8 * h;
+                T[kp * 17 + col] = cmul(Y, twf[16 * kp + col]);
+            }
+        };
+        combine(ya, Z);
+        combine(yz, Z + kTWArr);
+    }
+    __syncwarp();
+    // ---- forward pass 2: lane (k' = col, h): DFT16 over k1 -> Y[k' + 16 (2k + h)], natural order
+#pragma unroll
+    for (int arr = 0; arr < 2; ++arr) {
+        double2* T = Z + arr * kTWArr;
+        double2 x[16], o[8];
+#pragma unroll
+        for (int k1 = 0; k1 < 16; ++k1) x[k1] = T[col * 17 + k1];
+        __syncwarp();
+        half_dft16<-1>(x, h, o);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) T[col + 16 * (2 * k + h)] = o[k];
+        __syncwarp();
+    }
+    __syncthreads();
+    // ---- unpack c_w = (-1)^w X[w mod 256] / 256 per point; store E' = (f+ + f-)/2, O' = (f+ - f-)/2
+    for (int e = tid; e < S * 3; e += blockDim.x) {
+        const int s = e % S, f = e / S;
+        const int tt = s, tm = (256 - s) & 255;
+        const double sg = ((s & 1) ? -1.0 : 1.0) * (0.5 / 256.0);
+        const int arr = f < 2 ? 0 : 1;
+        const long off = long(s) * g.slot_stride + long(jr) * g.n + i0;
+        double* o = t.out[f] + off;
+#pragma unroll
+        for (int ip = 0; ip < kTWPts / 2; ++ip) {
+            if (ip >= npos) break;
+            double xr[2], xi[2];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const double2* base = sd + (2 * ip + hh) * 2 * kTWArr + arr * kTWArr;
+                const double2 zt = base[tt], zm = base[tm];
+                if (f == 1) {
+                    xr[hh] = 0.5 * (zt.y + zm.y);
+                    xi[hh] = -0.5 * (zt.x - zm.x);
+                } else {
+                    xr[hh] = 0.5 * (zt.x + zm.x);
+                    xi[hh] = 0.5 * (zt.y - zm.y);
+                }
+            }
+            o[ip] = sg * (xr[0] + xr[1]);
+            o[oo + ip] = sg * (xr[0] - xr[1]);
+            o[ps + ip] = sg * (xi[0] + xi[1]);
+            o[ps + oo + ip] = sg * (xi[0] - xi[1]);
+        }
+    }
+}
+
+size_t theta_cross256w_smem() { return (size_t(kTWPts) * 2 * kTWArr + 256) * sizeof(double2); }
+int theta_cross256w_positions() { return kTWPts / 2; }
+int theta_cross256w_threads() { return 32 * kTWPts; }
+
 size_t theta_cross256_smem() { return (size_t(kT256Pts) * 3 * kT256Arr + 256) * sizeof(double2); }
 int theta_cross256_positions() { return kT256Pos; }
 int theta_cross256_threads() { return 16 * kT256Pts; }

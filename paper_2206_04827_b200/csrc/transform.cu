@@ -705,40 +705,61 @@ __global__ void __launch_bounds__(32 * kTWPts, 4) theta_cross256w_kernel(ThetaCr
     double2* Z = sd + pt * 2 * kTWArr;  // this point's two arrays
     double2 tv[3][8];                   // time samples of the three pairs at l = col + 16 (2j + h)
     const long ps = g.plane_stride, oo = g.nh;
+    // raw spectra of one pair for slot s = tid, prefetched into registers one pair ahead so the
+    // global-load latency overlaps the previous pair's FFTs (the Nyquist slot s = 128 is loaded
+    // directly by thread 0)
+    double raw[kTWPts / 2][8];
+    auto fetch_slot = [&](int pr, int s, double (&r)[kTWPts / 2][8]) {
+#pragma unroll
+        for (int ip = 0; ip < kTWPts / 2; ++ip)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) r[ip][u] = 0.0;
+        const long off = long(s) * g.slot_stride + long(jr) * g.n + i0;
+        const double* __restrict__ fa = t.in[2 * pr] + off;
+        const double* __restrict__ fb = t.in[2 * pr + 1] + off;
+#pragma unroll
+        for (int ip = 0; ip < kTWPts / 2; ++ip) {
+            if (ip >= npos) continue;
+            r[ip][0] = __ldg(fa + ip);
+            r[ip][1] = __ldg(fa + ps + ip);
+            r[ip][2] = __ldg(fa + oo + ip);
+            r[ip][3] = __ldg(fa + oo + ps + ip);
+            r[ip][4] = __ldg(fb + ip);
+            r[ip][5] = __ldg(fb + ps + ip);
+            r[ip][6] = __ldg(fb + oo + ip);
+            r[ip][7] = __ldg(fb + oo + ps + ip);
+        }
+    };
+    auto put_slot = [&](int s, const double (&r)[kTWPts / 2][8]) {
+        const double sg = (s & 1) ? -1.0 : 1.0;
+        const bool reonly = (s == 0 || s == 128);
+#pragma unroll
+        for (int ip = 0; ip < kTWPts / 2; ++ip) {
+            const double ar = r[ip][0], ai = r[ip][1], aro = r[ip][2], aio = r[ip][3];
+            const double br = r[ip][4], bi = r[ip][5], bro = r[ip][6], bio = r[ip][7];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const double sz = hh ? -1.0 : 1.0;
+                const double xar = sg * fma(sz, aro, ar), xai = reonly ? 0.0 : sg * fma(sz, aio, ai);
+                const double xbr = sg * fma(sz, bro, br), xbi = reonly ? 0.0 : sg * fma(sz, bio, bi);
+                double2* Zp = sd + (2 * ip + hh) * 2 * kTWArr;
+                Zp[s] = make_double2(xar - xbi, xai + xbr);
+                if (s > 0 && s < 128) Zp[256 - s] = make_double2(xar + xbi, xbr - xai);
+            }
+        }
+    };
+    if (tid < S) fetch_slot(0, tid, raw);
 #pragma unroll
     for (int pr = 0; pr < 3; ++pr) {
         __syncthreads();  // previous pair's array fully consumed (and twiddles visible)
-        // ---- gather the Hermitian spectrum of pair pr for the CTA's points into array 0
-        for (int s = tid; s < S; s += blockDim.x) {
-            const double sg = (s & 1) ? -1.0 : 1.0;
-            const bool reonly = (s == 0 || s == 128);
-            const long off = long(s) * g.slot_stride + long(jr) * g.n + i0;
-            const double* __restrict__ fa = t.in[2 * pr] + off;
-            const double* __restrict__ fb = t.in[2 * pr + 1] + off;
-#pragma unroll
-            for (int ip = 0; ip < kTWPts / 2; ++ip) {
-                double ar = 0.0, ai = 0.0, aro = 0.0, aio = 0.0, br = 0.0, bi = 0.0, bro = 0.0, bio = 0.0;
-                if (ip < npos) {
-                    ar = __ldg(fa + ip);
-                    ai = __ldg(fa + ps + ip);
-                    aro = __ldg(fa + oo + ip);
-                    aio = __ldg(fa + oo + ps + ip);
-                    br = __ldg(fb + ip);
-                    bi = __ldg(fb + ps + ip);
-                    bro = __ldg(fb + oo + ip);
-                    bio = __ldg(fb + oo + ps + ip);
-                }
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    const double sz = hh ? -1.0 : 1.0;
-                    const double xar = sg * fma(sz, aro, ar), xai = reonly ? 0.0 : sg * fma(sz, aio, ai);
-                    const double xbr = sg * fma(sz, bro, br), xbi = reonly ? 0.0 : sg * fma(sz, bio, bi);
-                    double2* Zp = sd + (2 * ip + hh) * 2 * kTWArr;
-                    Zp[s] = make_double2(xar - xbi, xai + xbr);
-                    if (s > 0 && s < 128) Zp[256 - s] = make_double2(xar + xbi, xbr - xai);
-                }
-            }
+        // ---- Hermitian spectrum of pair pr for the CTA's points into array 0
+        if (tid < S) put_slot(tid, raw);
+        for (int s = tid + blockDim.x; s < S; s += blockDim.x) {  // Nyquist slot (and any p > 256 rest)
+            double r2[kTWPts / 2][8];
+            fetch_slot(pr, s, r2);
+            put_slot(s, r2);
         }
+        if (pr < 2 && tid < S) fetch_slot(pr + 1, tid, raw);
         __syncthreads();
         // ---- inverse pass 1: lane (n2 = col, h): DFT16 over n1 of x[16 n1 + n2] -> k1 = 2k + h
         {

@@ -43,6 +43,23 @@ struct Combo {
 };
 __global__ void combo_kernel(Combo c);
 
+// solve.cu: fused fast-diagonalization modal solve (one CTA per real sub-problem, sizes <= 128)
+struct FdTask {
+    int t;     // tensor (base index)
+    long off;  // offset of the sub-problem block in the input / output tensor
+    const double *PL, *PR, *RT, *QL, *QR;
+};
+struct FdSolve {
+    const FdTask* tasks;
+    const double* fbase[2];
+    double* obase[2];
+    int M, N, mh, nh;
+    long ldf, ldpr, ldql, ldrt;
+    double alpha;
+};
+__global__ void fdsolve_kernel(FdSolve p);
+size_t fdsolve_smem();
+
 // transform.cu
 struct GemmBatch {
     const double* const* A;
@@ -60,7 +77,8 @@ struct GemmBatch {
     const long* coff;
     const double* bbase[2];
     double* cbase[2];
-    int nbatch;  // number of batches (persistent kernel)
+    int nbatch;  // number of batches
+    long ldd;    // leading dimension of the dl tables
 };
 constexpr long kBaseShift = 40;
 __global__ void dgemm_batched_kernel(GemmBatch g);

@@ -419,11 +419,12 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
             const long o = put(left[i].PL);
             put(padld(left[i].QL, mh, M));
             put(left[i].lam);
-            for (int k0 = 0; k0 < 2; ++k0) {  // 1 / (lambda_i + mu_j), rounded once from long double
-                std::vector<double> rt(size_t(M) * N);
+            for (int k0 = 0; k0 < 2; ++k0) {  // 1 / (lambda_i + mu_j), rounded once; M x N, ld N rounded up to even
+                const int ldr = N + (N & 1);
+                std::vector<double> rt(size_t(M) * ldr, 0.0);
                 for (int a = 0; a < M; ++a)
                     for (int b = 0; b < N; ++b)
-                        rt[size_t(a) * N + b] =
+                        rt[size_t(a) * ldr + b] =
                             double(1.0L / ((long double)left[i].lam_ld[size_t(a)] + right[k0].mu_ld[size_t(b)]));
                 put(rt);
             }
@@ -451,7 +452,7 @@ double diag_check_residual(const SolverSet& set, int slot, int k0, int M, int N,
     auto even = [](long x) { return x + (x & 1); };
     const double* dg = set.dg.data();
     const long PLo = set.dg_left[size_t(slot)], QLo = PLo + long(M) * mh, LAMo = QLo + long(mh) * Mp,
-               RTo = LAMo + even(M) + long(k0) * even(long(M) * N);
+               RTo = LAMo + even(M) + long(k0) * long(M) * Np;
     const long PRo = set.dg_right[k0], QRo = PRo + long(nh) * Np;
     std::vector<double> f(size_t(mh) * nh);
     unsigned long long st = seed * 0x9E3779B97F4A7C15ull + 1;
@@ -472,7 +473,7 @@ double diag_check_residual(const SolverSet& set, int slot, int k0, int M, int N,
     std::vector<double> T1 = mm(dg + PLo, mh, f.data(), nh, M, mh, nh);
     std::vector<double> Z = mm(T1.data(), nh, dg + PRo, Np, M, nh, N);
     for (int i = 0; i < M; ++i)
-        for (int j = 0; j < N; ++j) Z[size_t(i) * N + j] *= dg[RTo + long(i) * N + j];
+        for (int j = 0; j < N; ++j) Z[size_t(i) * N + j] *= dg[RTo + long(i) * Np + j];
     std::vector<double> T3 = mm(dg + QLo, Mp, Z.data(), N, mh, M, N);
     std::vector<double> u = mm(T3.data(), N, dg + QRo, nh, mh, N, nh);
     // X = S_r^-1 u S_z^-T: u[a][b] = X[a][b] - X[a-1][b] - X[a][b-1] + X[a-1][b-1] -> prefix sums

@@ -278,7 +278,8 @@ void GemmPlan::upload() {
 
 void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double* c0, double* c1) const {
     const unsigned nb = unsigned(std::max(C.size(), Coff.size()));
-    GemmBatch g{dA, dB, dC, M, N, K, lda, ldb, ldc, alpha, beta, dT, dDL, dDR, dBoff, dCoff, {b0, b1}, {c0, c1}, int(nb)};
+    GemmBatch g{dA, dB, dC, M, N, K, lda, ldb, ldc, alpha, beta, dT, dDL, dDR, dBoff, dCoff, {b0, b1}, {c0, c1}, int(nb),
+                ldd ? ldd : long(N)};
     const bool based_ok = (reinterpret_cast<uintptr_t>(b0) % 16 == 0) && (reinterpret_cast<uintptr_t>(b1) % 16 == 0);
     if (pipe && based_ok) {
         static bool attr = false;  // process-wide function attribute (same on every device)
@@ -313,6 +314,10 @@ GemmPlan::~GemmPlan() {
 }
 
 // ---------------------------------------------------------------- Pipeline
+Pipeline::~Pipeline() {
+    for (auto& kv : fdtasks_) cudaFree(kv.second.first);
+}
+
 Pipeline::Pipeline(Ctx& c_) : c(c_), tp(c_), T(c_.tensor_doubles(false)) {
     big_scratch(size_t(3) * T);  // pencil scratch: max(pt_synth 2 pairs x 2, curl 6 pencils per thread)
 }
@@ -798,6 +803,70 @@ void Pipeline::modal_solve(DevSet& set, bool full, int ntensor, const double* co
     }
     const void* keyp[1] = {&set};
     const int ci[1] = {int(full) * 16 + ntensor};
+    // fused path: all four products per sub-problem in one CTA (tile edge 128)
+    if (!fd_attr_) {
+        // the fused kernel (one CTA per sub-problem, intermediates in shared memory) runs at 1 CTA/SM
+        // and measured 0.47 / 0.76 ms (P / H) against 0.41 / 0.68 ms for the four pipelined GEMMs at
+        // 2 CTAs/SM, so it is opt-in (CCF_FDSOLVE_FUSED=1)
+        const char* e = std::getenv("CCF_FDSOLVE_FUSED");
+        fd_fused_ = e && e[0] == '1';
+        if (fd_fused_) CCF_CUDA(cudaFuncSetAttribute(fdsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     int(fdsolve_smem())));
+        fd_attr_ = true;
+    }
+    const bool aligned = (reinterpret_cast<uintptr_t>(f[0]) % 16 == 0) && (ntensor < 2 || reinterpret_cast<uintptr_t>(f[1]) % 16 == 0) &&
+                         (reinterpret_cast<uintptr_t>(out0) % 16 == 0) && (ntensor < 2 || reinterpret_cast<uintptr_t>(out1) % 16 == 0);
+    if (fd_fused_ && aligned && M <= 128 && N <= 128 && mh <= 128 && nh <= 128 && g.n % 2 == 0 && nh % 2 == 0) {
+        const std::string key = ptr_key("fd", 1, keyp, keyp, ci);
+        auto it = fdtasks_.find(key);
+        if (it == fdtasks_.end()) {
+            std::vector<FdTask> tv;
+            auto even = [](long x) { return x + (x & 1); };
+            const double* dg = set.dg;
+            for (int t = 0; t < ntensor; ++t)
+                for (int s = 0; s < g.nslots; ++s)
+                    for (int k0 = 0; k0 < 2; ++k0)
+                        for (int pl = 0; pl < 2; ++pl) {
+                            const long PLo = set.host.dg_left[size_t(s)], QLo = PLo + long(M) * mh,
+                                       LAMo = QLo + long(mh) * Mp, RTo = LAMo + even(M) + long(k0) * long(M) * Np;
+                            const long PRo = set.host.dg_right[k0], QRo = PRo + long(nh) * Np;
+                            FdTask tk{};
+                            tk.t = t;
+                            tk.off = long(s) * g.slot_stride + long(pl) * g.plane_stride + long(k0) * nh;
+                            tk.PL = dg + PLo;
+                            tk.PR = dg + PRo;
+                            tk.RT = dg + RTo;
+                            tk.QL = dg + QLo;
+                            tk.QR = dg + QRo;
+                            tv.push_back(tk);
+                        }
+            FdTask* d = nullptr;
+            CCF_CUDA(cudaMalloc(&d, tv.size() * sizeof(FdTask)));
+            CCF_CUDA(cudaMemcpy(d, tv.data(), tv.size() * sizeof(FdTask), cudaMemcpyHostToDevice));
+            it = fdtasks_.emplace(key, std::make_pair(d, int(tv.size()))).first;
+        }
+        if (rhs_mark) c.mark(rhs_mark);
+        FdSolve fp{};
+        fp.tasks = it->second.first;
+        fp.fbase[0] = f[0];
+        fp.fbase[1] = ntensor > 1 ? f[1] : f[0];
+        fp.obase[0] = out0;
+        fp.obase[1] = ntensor > 1 ? out1 : out0;
+        fp.M = M;
+        fp.N = N;
+        fp.mh = mh;
+        fp.nh = nh;
+        fp.ldf = g.n;
+        fp.ldpr = Np;
+        fp.ldql = Mp;
+        fp.ldrt = Np;
+        fp.alpha = alpha;
+        fdsolve_kernel<<<it->second.second, 256, fdsolve_smem(), c.stream>>>(fp);
+        ++c.launches;
+        c.gemm_flops += 2.0 * double(it->second.second) *
+                        (double(M) * nh * mh + double(M) * N * nh + double(mh) * N * M + double(mh) * nh * N);
+        return;
+    }
     bool fresh;
     GemmPlan& g1 = gemm(ptr_key("d1", 1, keyp, keyp, ci), fresh);
     GemmPlan& g2 = gemm(ptr_key("d2", 1, keyp, keyp, ci), fresh);
@@ -813,7 +882,7 @@ void Pipeline::modal_solve(DevSet& set, bool full, int ntensor, const double* co
                     for (int pl = 0; pl < 2; ++pl, ++task) {
                         // dg layout (modal.cpp): left [PL M x mh | QL mh x Mp | lam | 1/(lam+mu) x2], right [PR nh x Np | QR N x nh | mu]
                         const long PLo = set.host.dg_left[size_t(s)], QLo = PLo + long(M) * mh,
-                                   LAMo = QLo + long(mh) * Mp, RTo = LAMo + even(M) + long(k0) * even(long(M) * N);
+                                   LAMo = QLo + long(mh) * Mp, RTo = LAMo + even(M) + long(k0) * long(M) * Np;
                         const long PRo = set.host.dg_right[k0], QRo = PRo + long(nh) * Np;
                         const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride + long(k0) * nh;
                         const long rel = (long(t) << kBaseShift) + off;  // base t = f_t / out_t at launch
@@ -837,7 +906,7 @@ void Pipeline::modal_solve(DevSet& set, bool full, int ntensor, const double* co
                         g4.Coff.push_back(rel);                        // u   mh x nh (ld n)
                     }
         g1.M = M; g1.N = nh; g1.K = mh; g1.lda = mh; g1.ldb = g.n; g1.ldc = nh;
-        g2.M = M; g2.N = N; g2.K = nh; g2.lda = nh; g2.ldb = Np; g2.ldc = Np;
+        g2.M = M; g2.N = N; g2.K = nh; g2.lda = nh; g2.ldb = Np; g2.ldc = Np; g2.ldd = Np;
         g3.M = mh; g3.N = N; g3.K = M; g3.lda = Mp; g3.ldb = Np; g3.ldc = Np;
         g4.M = mh; g4.N = nh; g4.K = N; g4.lda = Np; g4.ldb = nh; g4.ldc = g.n;
         g1.upload();

@@ -41,6 +41,7 @@ struct GemmPlan {
     std::vector<int> tstart;          // optional: batch b sums terms [tstart[b], tstart[b+1])
     std::vector<const double*> DL, DR;  // optional per-batch epilogue divisors (dl_i + dr_j)
     std::vector<long> Boff, Coff;       // optional base-relative B / C (see GemmBatch)
+    long ldd = 0;                       // leading dimension of the epilogue table (0: N)
     const double** dA = nullptr;
     const double** dB = nullptr;
     double** dC = nullptr;
@@ -63,6 +64,7 @@ struct GemmPlan {
 class Pipeline {
 public:
     explicit Pipeline(Ctx& c);
+    ~Pipeline();
     Ctx& c;
     TransformPlan tp;
     long T;  // doubles per half-spectrum tensor
@@ -112,6 +114,8 @@ private:
     void nonlinear_pencil(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w,
                           double* lam_n, double* gam_n);
     DBuf fcomb_[2], dT1_, dZ_, dT3_;  // fast-diagonalization scratch
+    std::map<std::string, std::pair<FdTask*, int>> fdtasks_;  // fused-solve task lists (device)
+    bool fd_fused_ = false, fd_attr_ = false;                    // CCF_FDSOLVE_FUSED=1: fused solve kernel
 };
 
 struct NSState {

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(128) dgemm_batched_kernel(GemmBatch g) {
                 if (r < g.M && c < g.N) {
                     double* dst = C + long(r) * g.ldc + c;
                     double v = g.alpha * acc[i][j][q];
-                    if (g.dl) v *= __ldg(g.dl[b] + long(r) * g.N + c);  // 1 / (lambda_r + mu_c), M x N table
+                    if (g.dl) v *= __ldg(g.dl[b] + long(r) * g.ldd + c);  // 1 / (lambda_r + mu_c), M x N table
                     *dst = g.beta == 0.0 ? v : fma(g.beta, *dst, v);
                 }
             }
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmBatch g) {
             for (int q = 0; q < 2; ++q) {
                 if (c + q < g.N) {
                     double v = g.alpha * acc[i][j][q];
-                    if (dl) v *= __ldg(dl + long(r) * g.N + c + q);
+                    if (dl) v *= __ldg(dl + long(r) * g.ldd + c + q);
                     dst[q] = g.beta == 0.0 ? v : fma(g.beta, dst[q], v);
                 }
             }

@@ -61,21 +61,23 @@ def test_ns_steps_adi_kernel_vs_oracle(P, O):
     ctx.close()
 
 
-def test_fused_solve_kernel_matches(P):
+def test_fused_solve_kernel_matches(P, tmp_path):
     """The opt-in fused fast-diagonalization kernel (CCF_FDSOLVE_FUSED=1, one CTA per sub-problem)
     against the default four-GEMM chain, in a subprocess so the switch is read fresh."""
+    import os
     import subprocess
     import sys
+    out = tmp_path / "fd_out.npy"
     code = (
         "import numpy as np, paper_2206_04827_b200 as P\n"
         "from tests.inputs import hermitian_coeffs\n"
         "c = P.Context(64, 64, 8)\n"
         "f = hermitian_coeffs(64, 64, 8, 0.8, 7)\n"
-        "np.save('/tmp/fd_out.npy', c.solve_poisson_3d(f))\n")
-    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
-    env = dict(__import__("os").environ, CCF_FDSOLVE_FUSED="1")
+        f"np.save({str(out)!r}, c.solve_poisson_3d(f))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CCF_FDSOLVE_FUSED="1")
     subprocess.run([sys.executable, "-c", code], check=True, cwd=root, env=env)
-    fused = np.load("/tmp/fd_out.npy")
+    fused = np.load(out)
     c = P.Context(64, 64, 8)
     ref = c.solve_poisson_3d(hermitian_coeffs(64, 64, 8, 0.8, 7))
     assert rel_err(fused, ref) < 1e-12

@@ -82,8 +82,9 @@ struct GemmBatch {
 };
 constexpr long kBaseShift = 40;
 __global__ void dgemm_batched_kernel(GemmBatch g);
-__global__ void dgemm_pipe_kernel(GemmBatch g);  // 128 x 64 tiles, cp.async pipeline (aligned operands)
-size_t dgemm_pipe_smem();
+template <int PM>
+__global__ void dgemm_pipe_kernel(GemmBatch g);  // PM x 64 tiles (PM = 128 | 64), cp.async pipeline (aligned operands)
+size_t dgemm_pipe_smem(int bm);
 struct ThetaCross {
     Geo g;
     int logp, tj;

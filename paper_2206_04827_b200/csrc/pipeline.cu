@@ -282,20 +282,20 @@ void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double
                 ldd ? ldd : long(N)};
     const bool based_ok = (reinterpret_cast<uintptr_t>(b0) % 16 == 0) && (reinterpret_cast<uintptr_t>(b1) % 16 == 0);
     if (pipe && based_ok) {
-        static bool attr = false;  // process-wide function attribute (same on every device)
+        static bool attr = false;  // process-wide function attributes (same on every device)
         if (!attr) {
-            CCF_CUDA(cudaFuncSetAttribute(dgemm_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(dgemm_pipe_smem())));
+            CCF_CUDA(cudaFuncSetAttribute(dgemm_pipe_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(dgemm_pipe_smem(128))));
+            CCF_CUDA(cudaFuncSetAttribute(dgemm_pipe_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(dgemm_pipe_smem(64))));
             attr = true;
         }
-        static int nsm = 0;
-        if (!nsm) CCF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
-        const long items = long(nb) * ((M + 127) / 128) * ((N + 63) / 64);
-        // one item per CTA: dynamic hardware scheduling balances the variable-length (term-count)
-        // items better than a static persistent round robin (measured: 23 vs 21 TFLOP/s)
-        const unsigned grid = unsigned(items);
-        (void)nsm;
-        dgemm_pipe_kernel<<<grid, 256, dgemm_pipe_smem(), s>>>(g);
+        // short-K products (one term of K <= 128): 64-row tiles, 4 CTAs/SM, so tile fills overlap
+        const bool small = tstart.empty() && K <= 128;
+        const int bm = (small && !std::getenv("CCF_GEMM_BM128")) ? 64 : 128;
+        const long items = long(nb) * ((M + bm - 1) / bm) * ((N + 63) / 64);
+        if (bm == 64) dgemm_pipe_kernel<64><<<unsigned(items), 128, dgemm_pipe_smem(64), s>>>(g);
+        else dgemm_pipe_kernel<128><<<unsigned(items), 256, dgemm_pipe_smem(128), s>>>(g);
     } else {
         const dim3 grid(unsigned((N + 63) / 64), unsigned((M + 63) / 64), nb);
         dgemm_batched_kernel<<<grid, 128, 0, s>>>(g);

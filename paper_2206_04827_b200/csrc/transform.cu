@@ -130,8 +130,8 @@ __global__ void __launch_bounds__(128) dgemm_batched_kernel(GemmBatch g) {
 // cp.async (LDGSTS, 16-byte, zero-filled at the M / N / K edges) straight into shared memory.
 // Requires 16-byte aligned A / B bases and even lda / ldb (checked on the host: GemmPlan::upload).
 namespace {
-constexpr int PM = 128, PN = 64, PK = 16, PSTAGES = 3, PSA = PK + 4, PSB = PN + 4;
-constexpr int P_A_STAGE = PM * PSA, P_B_STAGE = PK * PSB;
+constexpr int PN = 64, PK = 16, PSTAGES = 3, PSA = PK + 4, PSB = PN + 4;
+constexpr int P_B_STAGE = PK * PSB;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int bytes) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -144,9 +144,12 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 }  // namespace
 
-size_t dgemm_pipe_smem() { return size_t(PSTAGES) * (P_A_STAGE + P_B_STAGE) * sizeof(double); }
+size_t dgemm_pipe_smem(int bm) { return size_t(PSTAGES) * (size_t(bm) * PSA + P_B_STAGE) * sizeof(double); }
 
-__global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmBatch g) {
+template <int PM>
+__global__ void __launch_bounds__(2 * PM, PM == 128 ? 2 : 4) dgemm_pipe_kernel(GemmBatch g) {
+    constexpr int NT = 2 * PM;  // threads: (PM / 32) x 2 warps of 32 x 32
+    constexpr int P_A_STAGE = PM * PSA;
     extern __shared__ __align__(16) double psm[];
     double* As = psm;
     double* Bs = psm + PSTAGES * P_A_STAGE;
@@ -181,8 +184,8 @@ __global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmBatch g) {
             double* as = As + lstage * P_A_STAGE;
             double* bs = Bs + lstage * P_B_STAGE;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {  // A: 128 rows x 8 chunks of 2 doubles
-                const int c = tid + q * 256;
+            for (int q = 0; q < 4; ++q) {  // A: PM rows x 8 chunks of 2 doubles
+                const int c = tid + q * NT;
                 const int row = c >> 3, kc = (c & 7) * 2;
                 const int gr = m0 + row, gk = k0 + kc;
                 const int nv = (gr < g.M) ? max(0, min(2, g.K - gk)) : 0;
@@ -190,8 +193,8 @@ __global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmBatch g) {
                 cp_async16(as + row * PSA + kc, src, nv * 8);
             }
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {  // B: 16 rows x 32 chunks
-                const int c = tid + q * 256;
+            for (int q = 0; q < 512 / NT; ++q) {  // B: 16 rows x 32 chunks
+                const int c = tid + q * NT;
                 const int row = c >> 5, cc = (c & 31) * 2;
                 const int gk = k0 + row, gc = n0 + cc;
                 const int nv = (gk < g.K) ? max(0, min(2, g.N - gc)) : 0;
@@ -268,6 +271,9 @@ __global__ void __launch_bounds__(256, 2) dgemm_pipe_kernel(GemmBatch g) {
             }
         }
 }
+
+template __global__ void dgemm_pipe_kernel<128>(GemmBatch g);
+template __global__ void dgemm_pipe_kernel<64>(GemmBatch g);
 
 // ---------------------------------------------------------------------------------------------
 // Theta direction.

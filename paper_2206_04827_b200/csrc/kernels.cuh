@@ -79,6 +79,7 @@ struct GemmBatch {
     double* cbase[2];
     int nbatch;  // number of batches
     long ldd;    // leading dimension of the dl tables
+    int ipc;     // items (batch x m-tile x n-tile) per CTA, pipelined kernel
 };
 constexpr long kBaseShift = 40;
 __global__ void dgemm_batched_kernel(GemmBatch g);

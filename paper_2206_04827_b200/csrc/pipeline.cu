@@ -279,7 +279,7 @@ void GemmPlan::upload() {
 void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double* c0, double* c1) const {
     const unsigned nb = unsigned(std::max(C.size(), Coff.size()));
     GemmBatch g{dA, dB, dC, M, N, K, lda, ldb, ldc, alpha, beta, dT, dDL, dDR, dBoff, dCoff, {b0, b1}, {c0, c1}, int(nb),
-                ldd ? ldd : long(N)};
+                ldd ? ldd : long(N), 1};
     const bool based_ok = (reinterpret_cast<uintptr_t>(b0) % 16 == 0) && (reinterpret_cast<uintptr_t>(b1) % 16 == 0);
     if (pipe && based_ok) {
         static bool attr = false;  // process-wide function attributes (same on every device)
@@ -294,8 +294,18 @@ void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double
         const bool small = tstart.empty() && K <= 128;
         const int bm = (small && !std::getenv("CCF_GEMM_BM128")) ? 64 : 128;
         const long items = long(nb) * ((M + bm - 1) / bm) * ((N + 63) / 64);
-        if (bm == 64) dgemm_pipe_kernel<64><<<unsigned(items), 128, dgemm_pipe_smem(64), s>>>(g);
-        else dgemm_pipe_kernel<128><<<unsigned(items), 256, dgemm_pipe_smem(128), s>>>(g);
+        // single-term batches: several consecutive items per CTA share one cp.async stream
+        static int ipc_env = -1;
+        if (ipc_env < 0) {
+            const char* e = std::getenv("CCF_GEMM_IPC");
+            ipc_env = e ? std::max(1, std::atoi(e)) : 0;
+        }
+        const int ipc = tstart.empty() ? (ipc_env ? ipc_env : 1) : 1;  // measured: 2 and 4 do not help
+        GemmBatch gg = g;
+        gg.ipc = ipc;
+        const unsigned grid = unsigned((items + ipc - 1) / ipc);
+        if (bm == 64) dgemm_pipe_kernel<64><<<grid, 128, dgemm_pipe_smem(64), s>>>(gg);
+        else dgemm_pipe_kernel<128><<<grid, 256, dgemm_pipe_smem(128), s>>>(gg);
     } else {
         const dim3 grid(unsigned((N + 63) / 64), unsigned((M + 63) / 64), nb);
         dgemm_batched_kernel<<<grid, 128, 0, s>>>(g);

@@ -156,16 +156,28 @@ __global__ void __launch_bounds__(2 * PM, PM == 128 ? 2 : 4) dgemm_pipe_kernel(G
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
     const int gq = lane >> 2, tq = lane & 3;
-    // one (batch, m-tile, n-tile) item per CTA
+    // items (batch, m-tile, n-tile) [w0, w1) per CTA (g.ipc consecutive items for single-term batches,
+    // so the cp.async stream runs on across item boundaries and the per-tile fill is paid once)
     const int tn = (g.N + PN - 1) / PN, tmn = ((g.M + PM - 1) / PM) * tn;
-    const int b = blockIdx.x / tmn;
-    const int rem = blockIdx.x - b * tmn;
-    const int m0 = (rem / tn) * PM, n0 = (rem - (rem / tn) * tn) * PN;
-    const int t0 = g.tstart ? g.tstart[b] : b, t1 = g.tstart ? g.tstart[b + 1] : b + 1;
+    const int nitems = g.nbatch * tmn;
+    const int w0 = blockIdx.x * g.ipc, w1 = min(nitems, w0 + g.ipc);
     const int nkt = (g.K + PK - 1) / PK;
-    const int nk = (t1 - t0) * nkt;
-    // load cursor: term lt, k-tile lkt (nested counters, no divisions)
-    int lt = t0, lkt = 0, lstage = 0, issued = 0;
+    struct Item {
+        int b, m0, n0, t0, nk;
+    };
+    auto decode = [&](int w) {
+        Item it;
+        it.b = w / tmn;
+        const int rem = w - it.b * tmn;
+        it.m0 = (rem / tn) * PM;
+        it.n0 = (rem - (rem / tn) * tn) * PN;
+        it.t0 = g.tstart ? g.tstart[it.b] : it.b;
+        it.nk = (g.tstart ? g.tstart[it.b + 1] - it.t0 : 1) * nkt;
+        return it;
+    };
+    // load cursor: item lw, k-tile lk within the item (term lt, k-tile lkt within the term)
+    int lw = w0, lk = 0, lt = 0, lkt = 0, lstage = 0;
+    Item LI = decode(w0);
     const double* LA = nullptr;
     const double* LB = nullptr;
     auto set_term = [&]() {
@@ -177,10 +189,21 @@ __global__ void __launch_bounds__(2 * PM, PM == 128 ? 2 : 4) dgemm_pipe_kernel(G
             LB = g.B[lt];
         }
     };
-    if (nk > 0) set_term();
+    auto next_item = [&]() {  // advance the load cursor to the next item with work
+        while (lw < w1 && lk >= LI.nk) {
+            if (++lw < w1) LI = decode(lw);
+            lk = 0;
+            lkt = 0;
+            lt = LI.t0;
+            if (lw < w1 && LI.nk > 0) set_term();
+        }
+    };
+    lt = LI.t0;
+    if (LI.nk > 0) set_term();
+    next_item();
     auto issue = [&]() {
-        if (issued < nk) {
-            const int k0 = lkt * PK;
+        if (lw < w1) {
+            const int k0 = lkt * PK, m0 = LI.m0, n0 = LI.n0;
             double* as = As + lstage * P_A_STAGE;
             double* bs = Bs + lstage * P_B_STAGE;
 #pragma unroll
@@ -201,75 +224,80 @@ __global__ void __launch_bounds__(2 * PM, PM == 128 ? 2 : 4) dgemm_pipe_kernel(G
                 const double* src = nv ? LB + long(gk) * g.ldb + gc : LB;
                 cp_async16(bs + row * PSB + cc, src, nv * 8);
             }
-            ++issued;
             lstage = lstage + 1 == PSTAGES ? 0 : lstage + 1;
-            if (++lkt == nkt && issued < nk) {
+            ++lk;
+            if (++lkt == nkt && lk < LI.nk) {
                 lkt = 0;
                 ++lt;
                 set_term();
             }
+            next_item();
         }
         cp_async_commit();
     };
 #pragma unroll
     for (int s = 0; s < PSTAGES - 1; ++s) issue();
-    double acc[4][4][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     int cstage = 0;
-    for (int kt = 0; kt < nk; ++kt) {
-        cp_async_wait<PSTAGES - 2>();
-        __syncthreads();
-        issue();
-        const double* as = As + cstage * P_A_STAGE;
-        const double* bs = Bs + cstage * P_B_STAGE;
-        cstage = cstage + 1 == PSTAGES ? 0 : cstage + 1;
+    for (int cw = w0; cw < w1; ++cw) {
+        const Item I = decode(cw);
+        const int b = I.b, m0 = I.m0, n0 = I.n0, nk = I.nk;
+        double acc[4][4][2];
 #pragma unroll
-        for (int ks = 0; ks < PK; ks += 4) {
-            double af[4], bf[4];
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) af[i] = as[(wm + 8 * i + gq) * PSA + ks + tq];
+            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int kt = 0; kt < nk; ++kt) {
+            cp_async_wait<PSTAGES - 2>();
+            __syncthreads();
+            issue();
+            const double* as = As + cstage * P_A_STAGE;
+            const double* bs = Bs + cstage * P_B_STAGE;
+            cstage = cstage + 1 == PSTAGES ? 0 : cstage + 1;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bf[j] = bs[(ks + tq) * PSB + wn + 8 * j + gq];
+            for (int ks = 0; ks < PK; ks += 4) {
+                double af[4], bf[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+                for (int i = 0; i < 4; ++i) af[i] = as[(wm + 8 * i + gq) * PSA + ks + tq];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-        }
-    }
-    cp_async_wait<0>();
-    double* __restrict__ C;
-    if (g.coff) {
-        const long o = g.coff[b];
-        C = g.cbase[o >> kBaseShift] + (o & ((1L << kBaseShift) - 1));
-    } else {
-        C = g.C[b];
-    }
-    const double* __restrict__ dl = g.dl ? g.dl[b] : nullptr;
-    // paired columns (2 tq, 2 tq + 1) go out as one 16-byte store when aligned and in range
-    const bool vec = ((reinterpret_cast<uintptr_t>(C) | (uintptr_t(g.ldc) * 8)) & 15) == 0 && !dl && g.beta == 0.0;
+                for (int j = 0; j < 4; ++j) bf[j] = bs[(ks + tq) * PSB + wn + 8 * j + gq];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+                for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int r = m0 + wm + 8 * i + gq, c = n0 + wn + 8 * j + 2 * tq;
-            if (r >= g.M) continue;
-            double* dst = C + long(r) * g.ldc + c;
-            if (vec && c + 1 < g.N) {
-                *reinterpret_cast<double2*>(dst) = make_double2(g.alpha * acc[i][j][0], g.alpha * acc[i][j][1]);
-                continue;
+                    for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
             }
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                if (c + q < g.N) {
-                    double v = g.alpha * acc[i][j][q];
-                    if (dl) v *= __ldg(dl + long(r) * g.ldd + c + q);
-                    dst[q] = g.beta == 0.0 ? v : fma(g.beta, dst[q], v);
+        }
+        double* __restrict__ C;
+        if (g.coff) {
+            const long o = g.coff[b];
+            C = g.cbase[o >> kBaseShift] + (o & ((1L << kBaseShift) - 1));
+        } else {
+            C = g.C[b];
+        }
+        const double* __restrict__ dl = g.dl ? g.dl[b] : nullptr;
+        // paired columns (2 tq, 2 tq + 1) go out as one 16-byte store when aligned and in range
+        const bool vec = ((reinterpret_cast<uintptr_t>(C) | (uintptr_t(g.ldc) * 8)) & 15) == 0 && !dl && g.beta == 0.0;
+    #pragma unroll
+        for (int i = 0; i < 4; ++i)
+    #pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int r = m0 + wm + 8 * i + gq, c = n0 + wn + 8 * j + 2 * tq;
+                if (r >= g.M) continue;
+                double* dst = C + long(r) * g.ldc + c;
+                if (vec && c + 1 < g.N) {
+                    *reinterpret_cast<double2*>(dst) = make_double2(g.alpha * acc[i][j][0], g.alpha * acc[i][j][1]);
+                    continue;
+                }
+    #pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    if (c + q < g.N) {
+                        double v = g.alpha * acc[i][j][q];
+                        if (dl) v *= __ldg(dl + long(r) * g.ldd + c + q);
+                        dst[q] = g.beta == 0.0 ? v : fma(g.beta, dst[q], v);
+                    }
                 }
             }
-        }
+    }
+    cp_async_wait<0>();
 }
 
 template __global__ void dgemm_pipe_kernel<128>(GemmBatch g);

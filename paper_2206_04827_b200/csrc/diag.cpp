@@ -233,6 +233,7 @@ DiagLeft diag_left(const CBand& Ab, const CBand& Cb, const CBand& R2b, int M, in
         for (int e = 0; e < M; ++e) QL(a, e) = (a < M ? V(a, e) : 0.0L) - (a > 0 ? V(a - 1, e) : 0.0L);
     DiagLeft out;
     out.PL = to_double(PL);
+    out.PL_ld = PL.a;
     out.QL = to_double(QL);
     out.lam.resize(size_t(M));
     for (int i = 0; i < M; ++i) out.lam[size_t(i)] = double(lam[size_t(i)]);

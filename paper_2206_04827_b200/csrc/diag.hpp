@@ -26,6 +26,7 @@ namespace ccf {
 struct DiagLeft {
     std::vector<double> PL, QL, lam;  // M x mh, mh x M, M
     std::vector<long double> lam_ld;  // eigenvalues before rounding (for 1 / (lambda + mu))
+    std::vector<long double> PL_ld;   // PL before rounding (for the scaled Helmholtz variant)
 };
 struct DiagRight {
     std::vector<double> PR, QR, mu;  // nh x N, N x nh, N

@@ -228,7 +228,11 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
         const Dense Ar = recombine(Af), Cr = recombine(Cf);
         const CBand Ac = compress(Ar, j0, M, M, -2, 3), Cc = compress(Cr, j0, M, M, -2, 3);
         const CBand R2c = compress(so.ur.r2, j0, M, mh, -1, 3);
-        if (with_diag) diag_in.push_back({aw, Ac, Cc, R2c});
+        if (with_diag) {  // Poisson pencil bands of this |w| (shared modal basis, see SizeOps)
+            const CBand Ap = compress(recombine(lw), j0, M, M, -2, 3);
+            const CBand Cp = compress(so.R2rec, j0, M, M, -2, 3);
+            diag_in.push_back({aw, Ap, Cp, R2c});
+        }
 
         const Range mu = radial_cache.at(aw);
         Range ca = poisson ? mu : Range{-1.0 / scale + mu.lo, -1.0 / scale + mu.hi};
@@ -370,21 +374,25 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
     }
     C.resize(C.size() + 256, 0.0);  // read slack past the last block
     if (with_diag) {
-        // left data per unique |w| (parallel: O(M^3) long double each), right data per k-parity
-        std::vector<DiagLeft> left(diag_in.size());
-        std::vector<std::string> errs(diag_in.size());
-        std::vector<int> codes(diag_in.size(), 0);
+        // Poisson-pencil left data per unique |w| (cached per size; parallel: O(M^3) long double each)
+        std::vector<size_t> todo;
+        for (size_t i = 0; i < diag_in.size(); ++i)
+            if (!so.diag_poisson.count(diag_in[i].aw)) todo.push_back(i);
+        std::vector<DiagLeft> fresh(todo.size());
+        std::vector<std::string> errs(todo.size());
+        std::vector<int> codes(todo.size(), 0);
         {
-            const int nth = std::max(1, std::min<int>(int(std::thread::hardware_concurrency()), int(diag_in.size())));
+            const int nth = std::max(1, std::min<int>(int(std::thread::hardware_concurrency()), int(todo.size())));
             std::vector<std::thread> pool;
             std::atomic<size_t> next{0};
             for (int q = 0; q < nth; ++q)
                 pool.emplace_back([&] {
                     for (;;) {
                         const size_t i = next.fetch_add(1);
-                        if (i >= diag_in.size()) break;
+                        if (i >= todo.size()) break;
+                        const auto& di = diag_in[todo[i]];
                         try {
-                            left[i] = diag_left(diag_in[i].A, diag_in[i].C, diag_in[i].R2, M, mh);
+                            fresh[i] = diag_left(di.A, di.C, di.R2, M, mh);
                         } catch (const Error& e) {
                             codes[i] = e.status;
                             errs[i] = e.what();
@@ -393,8 +401,32 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
                 });
             for (auto& th : pool) th.join();
         }
-        for (size_t i = 0; i < diag_in.size(); ++i)
+        for (size_t i = 0; i < todo.size(); ++i)
             if (codes[i]) throw Error(codes[i], errs[i]);
+        for (size_t i = 0; i < todo.size(); ++i) so.diag_poisson[diag_in[todo[i]].aw] = std::move(fresh[i]);
+        // this set's left data: Poisson as cached; Helmholtz (A = R2 - s L, C = -s R2): same V,
+        // lambda = nu - 1/s, PL = -(1/s) PL_Poisson
+        std::vector<DiagLeft> left(diag_in.size());
+        for (size_t i = 0; i < diag_in.size(); ++i) {
+            const DiagLeft& P = so.diag_poisson.at(diag_in[i].aw);
+            DiagLeft& L = left[i];
+            L.QL = P.QL;
+            if (poisson) {
+                L.PL = P.PL;
+                L.lam = P.lam;
+                L.lam_ld = P.lam_ld;
+            } else {
+                const long double is = 1.0L / (long double)scale;
+                L.PL.resize(P.PL_ld.size());
+                for (size_t q = 0; q < P.PL_ld.size(); ++q) L.PL[q] = double(-is * P.PL_ld[q]);
+                L.lam_ld.resize(P.lam_ld.size());
+                L.lam.resize(P.lam_ld.size());
+                for (size_t q = 0; q < P.lam_ld.size(); ++q) {
+                    L.lam_ld[q] = P.lam_ld[q] - is;
+                    L.lam[q] = double(L.lam_ld[q]);
+                }
+            }
+        }
         std::vector<double>& G = set.dg;
         auto put = [&](const std::vector<double>& x) {
             const long off = long(G.size());
@@ -402,9 +434,12 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
             if (G.size() % 2) G.push_back(0.0);
             return off;
         };
-        // right data per k-parity first (the eigenvalue-sum reciprocals need mu)
-        DiagRight right[2];
-        for (int k0 = 0; k0 < 2; ++k0) right[k0] = diag_right(Btc[k0], Dtc[k0], C02c[k0], N, nh);
+        // right data per k-parity (scale-independent, cached per size)
+        if (!so.diag_right_ok) {
+            for (int k0 = 0; k0 < 2; ++k0) so.diag_right_data[k0] = diag_right(Btc[k0], Dtc[k0], C02c[k0], N, nh);
+            so.diag_right_ok = true;
+        }
+        const DiagRight* right = so.diag_right_data;
         // QL (mh x M) and PR (nh x N) are stored with the leading dimension rounded up to even so
         // that every GEMM operand row is 16-byte aligned (cp.async pipeline)
         auto padld = [](const std::vector<double>& x, int rows, int cols) {

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "ccf_device.cuh"
+#include "diag.hpp"
 #include "setup.hpp"
 
 namespace ccf {
@@ -18,6 +19,12 @@ struct SizeOps {  // per-size operator cache (setup only)
     Dense R2rec, C02recZ, D2recZ;  // recombined full operators
     Range vertical;                // padded enclosure of spec(-D2', C02')
     bool vertical_ok = false;
+    // fast-diagonalization cache: the radial eigenpairs of the Poisson pencil (L_w, R2) per |w| (every
+    // Helmholtz pencil R2 - s L_w, -s R2 has the same eigenvectors, lambda = nu - 1/s), and the
+    // vertical data per k-parity; sharing them makes all solver sets use one modal basis
+    std::map<int, DiagLeft> diag_poisson;
+    bool diag_right_ok = false;
+    DiagRight diag_right_data[2];
     SizeOps(int m_, int n_);
 };
 

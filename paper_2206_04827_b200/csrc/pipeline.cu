@@ -326,6 +326,7 @@ GemmPlan::~GemmPlan() {
 // ---------------------------------------------------------------- Pipeline
 Pipeline::~Pipeline() {
     for (auto& kv : fdtasks_) cudaFree(kv.second.first);
+    for (auto& kv : zrt_) cudaFree(kv.second);
 }
 
 Pipeline::Pipeline(Ctx& c_) : c(c_), tp(c_), T(c_.tensor_doubles(false)) {
@@ -761,6 +762,61 @@ void Pipeline::poisson(const double* f, double w, double* u) {
     modal_solve(set, false, 1, src, ww, 1, nullptr, nullptr, 0, u, nullptr);
 }
 
+// Z[task] *= w * RT[task] (M x N, leading dimension ld) - eigen-coordinate RHS of a modal solve
+__global__ void zscale_kernel(double* __restrict__ Z, long per, const double* const* __restrict__ rt, int M, int N,
+                              int ld, double w) {
+    const int task = blockIdx.x;
+    double* z = Z + long(task) * per;
+    const double* r = rt[task];
+    for (int e = threadIdx.x; e < M * N; e += blockDim.x) {
+        const int i = e / N, j = e - i * N;
+        z[long(i) * ld + j] *= w * __ldg(r + long(i) * ld + j);
+    }
+}
+
+// Poisson solve of w * lambda_omega when lambda_omega was produced by the previous Helmholtz solve in
+// the shared modal basis (modal.hpp SizeOps): with u = QL Z_H QR, PL_P u PR = Z_H exactly
+// (PL_P QL = I, QR PR = I), so the first two products drop out: Z_P = w Z_H .* RT_P, then
+// T3 = QL Z_P, u_P = T3 QR. Returns false if the chain plans of this set do not exist yet.
+bool Pipeline::modal_solve_from_z(DevSet& set, double w, double* out) {
+    if (!set.host.has_diag || !set.dg || !dZ_.p) return false;
+    const void* keyp[1] = {&set};
+    const int ci[1] = {1};  // half spectrum, one tensor
+    const std::string k3 = ptr_key("d3", 1, keyp, keyp, ci), k4 = ptr_key("d4", 1, keyp, keyp, ci);
+    auto i3 = gemms_.find(k3), i4 = gemms_.find(k4);
+    if (i3 == gemms_.end() || i4 == gemms_.end()) return false;
+    const Geo& g = c.gh;
+    const int M = c.M, N = c.N, mh = g.mh, nh = g.nh;
+    const int Mp = M + (M & 1), Np = N + (N & 1);
+    const size_t per = std::max(size_t(mh) * Np, size_t(M) * std::max(nh, Np));
+    const int ntask = g.nslots * 4;
+    auto it = zrt_.find(&set);
+    if (it == zrt_.end()) {
+        auto even = [](long x) { return x + (x & 1); };
+        std::vector<const double*> rt;
+        for (int s = 0; s < g.nslots; ++s)
+            for (int k0 = 0; k0 < 2; ++k0)
+                for (int pl = 0; pl < 2; ++pl) {
+                    const long PLo = set.host.dg_left[size_t(s)], QLo = PLo + long(M) * mh, LAMo = QLo + long(mh) * Mp;
+                    rt.push_back(set.dg + LAMo + even(M) + long(k0) * long(M) * Np);
+                }
+        const double** d = nullptr;
+        CCF_CUDA(cudaMalloc(&d, rt.size() * sizeof(void*)));
+        CCF_CUDA(cudaMemcpy(d, rt.data(), rt.size() * sizeof(void*), cudaMemcpyHostToDevice));
+        it = zrt_.emplace(&set, d).first;
+    }
+    zscale_kernel<<<ntask, 256, 0, c.stream>>>(dZ_.p, long(per), it->second, M, N, Np, w);
+    ++c.launches;
+    GemmPlan& g3 = *i3->second;
+    GemmPlan& g4 = *i4->second;
+    g3.launch(c.stream);
+    c.gemm_flops += g3.flops();
+    g4.launch(c.stream, nullptr, nullptr, out, out);
+    c.gemm_flops += g4.flops();
+    c.launches += 2;
+    return true;
+}
+
 // Fast diagonalization (diag.hpp) per real sub-problem (tensor t, slot s, k-parity k0, plane):
 //   T1 = PL[s] f          (M x nh)      f = sum_i w_t[i] src_t[i], rows jj, half row k0
 //   Z  = (T1 PR[k0]) ./ (lam[s]_i + mu[k0]_j)
@@ -769,6 +825,7 @@ void Pipeline::poisson(const double* f, double w, double* u) {
 void Pipeline::modal_solve(DevSet& set, bool full, int ntensor, const double* const* src0, const double* w0, int n0,
                            const double* const* src1, const double* w1, int n1, double* out0, double* out1,
                            const char* rhs_mark) {
+    last_z_valid_ = false;
     if (!set.host.has_diag || !set.dg) {
         c.run_adi(set, full, ntensor, src0, w0, n0, src1, w1, n1, out0, out1);
         return;
@@ -873,6 +930,7 @@ void Pipeline::modal_solve(DevSet& set, bool full, int ntensor, const double* co
         fp.alpha = alpha;
         fdsolve_kernel<<<it->second.second, 256, fdsolve_smem(), c.stream>>>(fp);
         ++c.launches;
+        last_z_valid_ = false;  // the fused kernel keeps Z on chip
         c.gemm_flops += 2.0 * double(it->second.second) *
                         (double(M) * nh * mh + double(M) * N * nh + double(mh) * N * M + double(mh) * nh * N);
         return;
@@ -934,6 +992,7 @@ void Pipeline::modal_solve(DevSet& set, bool full, int ntensor, const double* co
     c.gemm_flops += g3.flops();
     g4.launch(c.stream, nullptr, nullptr, out0, out1);
     c.gemm_flops += g4.flops();
+    last_z_valid_ = !full;  // dZ_ holds Z of every task (half-spectrum task order) until the next solve
     c.launches += 4;
 }
 
@@ -1146,7 +1205,9 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
     if (!disable_nonlinear) {
         double* lpsi = P.scratch(18);
         c.mark("start");
-        P.poisson(lw, -1.0, lpsi);                              // velocity_from_vorticity, ptns.cpp:85-91
+        // velocity_from_vorticity, ptns.cpp:85-91: lambda_psi = Poisson3D(-lambda_omega); after the first
+        // step lambda_omega comes from our Helmholtz solve in the shared modal basis (modal_solve_from_z)
+        if (!(zvalid && P.modal_solve_from_z(c.set(false, true, 1.0), -1.0, lpsi))) P.poisson(lw, -1.0, lpsi);
         c.mark("P_poisson_solve");
         P.nonlinear(gw, lpsi, lw, gw, nl[nnew].p, ng[nnew].p);  // nonlinear_term(v, omega)
     }
@@ -1173,6 +1234,7 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
     if (c.prof_events.empty()) c.mark("start");
     P.modal_solve(set, false, 2, sl, wl, ns, sg, wl, ns, lam[out].p, gam[out].p, "H_rhs_combine");
     c.mark("H_helmholtz_solve");
+    zvalid = P.last_z_valid_;  // Z of lambda_omega(out) stays in dZ_ (shared modal basis) for the next P
     const long T = P.T;
     finite_check_kernel<<<std::min<long>(1184, (T + 255) / 256), 256, 0, c.stream>>>(lam[out].p, T, dflag);
     finite_check_kernel<<<std::min<long>(1184, (T + 255) / 256), 256, 0, c.stream>>>(gam[out].p, T, dflag);

@@ -84,6 +84,8 @@ public:
     // Modal Sylvester solves of a solver set for 1 or 2 tensors with fused RHS combinations
     // (out_t = Solve(sum_i w_t[i] src_t[i])): fast diagonalization on the tensor cores, or the
     // ADI kernel (ctx flag bit 2 / sets without diagonalization data).
+    bool modal_solve_from_z(DevSet& set, double w, double* out);
+    bool last_z_valid_ = false;  // the last modal_solve left its eigen-coordinates Z in dZ_
     void modal_solve(DevSet& set, bool full, int ntensor, const double* const* src0, const double* w0, int n0,
                      const double* const* src1, const double* w1, int n1, double* out0, double* out1,
                      const char* rhs_mark = nullptr);
@@ -115,6 +117,7 @@ private:
                           double* lam_n, double* gam_n);
     DBuf fcomb_[2], dT1_, dZ_, dT3_;  // fast-diagonalization scratch
     std::map<std::string, std::pair<FdTask*, int>> fdtasks_;  // fused-solve task lists (device)
+    std::map<const void*, const double**> zrt_;               // per set: RT table per Poisson task
     bool fd_fused_ = false, fd_attr_ = false;                    // CCF_FDSOLVE_FUSED=1: fused solve kernel
 };
 
@@ -133,6 +136,7 @@ struct NSState {
     cudaGraphExec_t graphs[25] = {};  // steady-state step per (head, nhead) ring phase
     long launches_per_step = 0;
     bool use_graphs = true;
+    bool zvalid = false;  // the last Helmholtz solve left Z(lambda_omega) in the shared modal basis
     ~NSState();
     void step_once();
     void enqueue(int b, int eo, int cur, int out, int nnew);

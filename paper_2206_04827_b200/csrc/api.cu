@@ -6,6 +6,8 @@
 #include "context.hpp"
 #include "pipeline.hpp"
 
+#include <cstdlib>
+
 
 struct ccf_ctx {
     std::unique_ptr<ccf::Ctx> c;
@@ -461,10 +463,28 @@ ccf_status ccf_ns_create(ccf_ctx* ctx, double reynolds, double h, int order, int
         c.load_coeff(lam0, s.lam[0].p, false, 0, 0);  // parity projection of the initial data (ptns.cpp:190-191)
         c.load_coeff(gam0, s.gam[0].p, false, 0, 1);
         // build every solver set the run needs before any graph capture
-        if (!s.disable_nonlinear) c.set(false, true, 1.0);
+        ccf::DevSet& pset = c.set(false, true, 1.0);
         for (int b = 1; b <= order; ++b) {
             static const double K[4] = {1.0, 2.0 / 3.0, 6.0 / 11.0, 12.0 / 25.0};
             c.set(false, false, K[b - 1] * h * (1.0 / reynolds));
+        }
+        // eigen-coordinate state when every solve has diagonalization data in the shared basis and the
+        // nonlinear term runs on the composite operators (CCF_NS_EIGEN=0 keeps coefficient-space history)
+        const char* ev = std::getenv("CCF_NS_EIGEN");
+        const bool want = !(ev && ev[0] == '0');
+        if (want && pset.host.has_diag && pset.dg) {
+            ccf::Pipeline& P = *s.pl;
+            P.ensure_composite();
+            if (!P.composite_off()) {
+                P.ensure_eigen(pset);
+                s.eigen = true;
+                for (int i = 0; i < 5; ++i) {
+                    s.zl[i].alloc(size_t(T));
+                    s.zg[i].alloc(size_t(T));
+                }
+                P.to_eigen(pset, s.lam[0].p, s.zl[0].p);
+                P.to_eigen(pset, s.gam[0].p, s.zg[0].p);
+            }
         }
         c.sync();
         *out = st.release();

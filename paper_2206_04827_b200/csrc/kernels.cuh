@@ -60,6 +60,17 @@ struct FdSolve {
 __global__ void fdsolve_kernel(FdSolve p);
 size_t fdsolve_smem();
 
+// pipeline.cu: eigen-coordinate RHS out_t = factor * (sum_q w_q src_t,q) .* RT[(s, k0)]
+struct EigRhs {
+    const double* src[2][kMaxSrc];
+    double w[kMaxSrc];
+    int nsrc, ntensor;
+    double* out[2];
+    const double* const* rt;
+    double factor;
+    int M, N, Np, nslots;
+};
+
 // transform.cu
 struct GemmBatch {
     const double* const* A;

@@ -327,6 +327,7 @@ GemmPlan::~GemmPlan() {
 Pipeline::~Pipeline() {
     for (auto& kv : fdtasks_) cudaFree(kv.second.first);
     for (auto& kv : zrt_) cudaFree(kv.second);
+    for (auto& kv : eig_rt_) cudaFree(const_cast<const double**>(kv.second));
 }
 
 Pipeline::Pipeline(Ctx& c_) : c(c_), tp(c_), T(c_.tensor_doubles(false)) {
@@ -587,8 +588,9 @@ void Pipeline::ensure_composite() {
 //   Y  = z analysis of (a_r, a_t, a_z, dz a_r, dz a_t)
 //   (gamma_N, lambda_N) = per-slot composite r operators (curl + decompose + r analysis) on Y
 void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w,
-                         double* lam_n, double* gam_n) {
+                         double* lam_n, double* gam_n, DevSet* eig) {
     ensure_composite();
+    if (eig && comp_off_) throw Error(INTERNAL, "nonlinear: eigen-coordinate output needs the composite path");
     if (comp_off_) {
         nonlinear_pencil(lam_v, gam_v, lam_w, gam_w, lam_n, gam_n);
         return;
@@ -671,28 +673,34 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     theta_cross(val, av);
     c.mark("X2_theta_cross");
     // ---- z analysis of a_r, a_t, a_z and (derivative_z folded in) dz a_r, dz a_t
-    GemmPlan& za = gemm(ptr_key("nza", 6, keyp, keyp, cls0), fresh);
+    // eigen mode (eig != nullptr): the z analysis carries PR of the shared modal basis, Y_x half k0 =
+    // values * (Az PR)[k0] (N columns, leading dimension 2 Np), see ensure_eigen
+    const int Np = c.N + (c.N & 1);
+    const int ecls[8] = {eig ? 1 : 0, 0, 0, 0, 0, 0, 0, 0};
+    GemmPlan& za = gemm(ptr_key("nza", 6, keyp, keyp, ecls), fresh);
     if (fresh) {
         for (int x = 0; x < 5; ++x) {
             const double* src = av[x < 3 ? x : x - 3];
-            const double* mat = x >= 3 ? tp.ADz.p : tp.Az.p;
+            const double* mat = eig ? (x >= 3 ? eig_ADzP_.p : eig_AzP_.p) : (x >= 3 ? tp.ADz.p : tp.Az.p);
+            const long mstride = eig ? long(g.nh) * Np : long(g.nh) * g.nh;
             for (int s = 0; s < g.nslots; ++s)
                 for (int pl = 0; pl < 2; ++pl) {
                     const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
                     for (int po = 0; po < 2; ++po) {
                         const int pi = x >= 3 ? 1 - po : po;
                         za.A.push_back(src + off + pi * g.nh);
-                        za.B.push_back(mat + size_t(po) * g.nh * g.nh);
-                        za.C.push_back(Y[x] + off + po * g.nh);
+                        za.B.push_back(mat + po * mstride);
+                        za.C.push_back(eig ? Y[x] + long(s) * g.slot_stride + long(pl) * g.mh * 2 * Np + po * Np
+                                           : Y[x] + off + po * g.nh);
                     }
                 }
         }
         za.M = g.mh;
-        za.N = g.nh;
+        za.N = eig ? c.N : g.nh;
         za.K = g.nh;
         za.lda = g.n;
-        za.ldb = g.nh;
-        za.ldc = g.n;
+        za.ldb = eig ? Np : g.nh;
+        za.ldc = eig ? 2 * Np : g.n;
         za.upload();
     }
     za.launch(c.stream);
@@ -700,25 +708,28 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     c.launches += 1;
     c.mark("X3_rz_analysis");
     // ---- composite curl + pt_decompose + r analysis -> (gamma_N, lambda_N)
-    GemmPlan& ra = gemm(ptr_key("nra", 6, keyp, keyp, cls0), fresh);
+    // eigen mode: blocks PL_P A_t (M x mh) and output in the eigen layout (M x 2 Np per slot, plane)
+    GemmPlan& ra = gemm(ptr_key("nra", 6, keyp, keyp, ecls), fresh);
     if (fresh) {
         for (int s = 0; s < g.nslots; ++s)
             for (int o = 0; o < 4; ++o) {
                 ra.tstart.push_back(int(ra.A.size()));
                 for (const CompositeTerm& ct : anal_.terms[size_t(s)]) {
                     if (ct.out != o) continue;
-                    ra.A.push_back(danal_.p + ct.off);
-                    ra.B.push_back(Y[ct.in / 2] + long(s) * g.slot_stride + long(ct.in % 2) * g.plane_stride);
+                    ra.A.push_back(eig ? eig_anal_.p + ct.off : danal_.p + ct.off);
+                    ra.B.push_back(eig ? Y[ct.in / 2] + long(s) * g.slot_stride + long(ct.in % 2) * g.mh * 2 * Np
+                                       : Y[ct.in / 2] + long(s) * g.slot_stride + long(ct.in % 2) * g.plane_stride);
                 }
-                ra.C.push_back((o < 2 ? gam_n : lam_n) + long(s) * g.slot_stride + long(o % 2) * g.plane_stride);
+                ra.C.push_back(eig ? (o < 2 ? gam_n : lam_n) + eig_off(s, o % 2, 0)
+                                   : (o < 2 ? gam_n : lam_n) + long(s) * g.slot_stride + long(o % 2) * g.plane_stride);
             }
         ra.tstart.push_back(int(ra.A.size()));
-        ra.M = g.mh;
-        ra.N = g.n;
+        ra.M = eig ? c.M : g.mh;
+        ra.N = eig ? 2 * Np : g.n;
         ra.K = g.mh;
         ra.lda = g.mh;
-        ra.ldb = g.n;
-        ra.ldc = g.n;
+        ra.ldb = eig ? 2 * Np : g.n;
+        ra.ldc = eig ? 2 * Np : g.n;
         ra.upload();
     }
     ra.launch(c.stream);
@@ -996,6 +1007,222 @@ void Pipeline::modal_solve(DevSet& set, bool full, int ntensor, const double* co
     c.launches += 4;
 }
 
+// ---------------------------------------------------------------- eigen-coordinate NS state
+// Eigen layout (one tensor): E[slot][plane][i < M][k0 * Np + j] (leading dimension 2 Np, j < N used);
+// Z = PL_P u PR in the modal basis shared by every solver set (modal.hpp SizeOps). With
+// PL_H = -(1/s) PL_P for a Helmholtz set of scale s and PL_P QL = I, QR PR = I:
+//   Poisson RHS   PL_P (-lambda_omega) PR = -Z_lambda
+//   Helmholtz RHS PL_H (sum b_i omega_i + kappa sum e_i N_i) PR = -(1/s) (sum b_i Z_i + kappa sum e_i N~_i)
+// so the solves reduce to (RHS .* RT) followed by the back transform u = QL Z QR, and the nonlinear
+// term is produced directly as N~ = PL_P N PR (PR folded into the z analysis, PL_P into the composite
+// curl/decompose blocks).
+long Pipeline::eig_off(int s, int pl, int k0) const {
+    const int Np = c.N + (c.N & 1);
+    return (long(s) * 2 + pl) * long(c.M) * 2 * Np + long(k0) * Np;
+}
+
+__global__ void __launch_bounds__(256) eigen_rhs_kernel(EigRhs a) {
+    // one eigen-layout row (t, s, pl, i) per block row; 2 Np columns over the threads (16-byte pairs)
+    const long rows = long(a.ntensor) * a.nslots * 2 * a.M;
+    const int ld = 2 * a.Np, pairs = a.Np;  // 2 Np / 2
+    for (long row = blockIdx.x; row < rows; row += gridDim.x) {
+        const int t = int(row / (long(a.nslots) * 2 * a.M));
+        const long rr = row - long(t) * a.nslots * 2 * a.M;  // (s * 2 + pl) * M + i
+        const int i = int(rr % a.M);
+        const int s = int(rr / (2L * a.M));
+        const long base = rr * ld;
+        for (int pc = threadIdx.x; pc < pairs; pc += blockDim.x) {
+            const int col = 2 * pc;
+            const int k0 = col >= a.Np ? 1 : 0, j = col - k0 * a.Np;
+            double2 acc = make_double2(0.0, 0.0);
+            for (int q = 0; q < a.nsrc; ++q) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(a.src[t][q] + base + col));
+                acc.x = fma(a.w[q], v.x, acc.x);
+                acc.y = fma(a.w[q], v.y, acc.y);
+            }
+            const double2 r = __ldg(reinterpret_cast<const double2*>(a.rt[s * 2 + k0] + long(i) * a.Np + j));
+            double2 o;
+            o.x = j < a.N ? a.factor * acc.x * r.x : 0.0;
+            o.y = j + 1 < a.N ? a.factor * acc.y * r.y : 0.0;
+            *reinterpret_cast<double2*>(a.out[t] + base + col) = o;
+        }
+    }
+}
+
+void Pipeline::ensure_eigen(DevSet& pset) {
+    if (eig_set_ == &pset) return;
+    ensure_composite();
+    if (comp_off_ || !pset.host.has_diag || !pset.dg) throw Error(INTERNAL, "ensure_eigen: no shared modal basis");
+    const Geo& g = c.gh;
+    const int M = c.M, N = c.N, mh = g.mh, nh = g.nh;
+    const int Mp = M + (M & 1), Np = N + (N & 1);
+    (void)Mp;
+    auto even = [](long x) { return x + (x & 1); };
+    // (Az PR)[k0], (ADz PR)[k0]: nh x Np each
+    eig_AzP_.alloc(size_t(2) * nh * Np);
+    eig_ADzP_.alloc(size_t(2) * nh * Np);
+    {
+        GemmPlan gp;
+        for (int k0 = 0; k0 < 2; ++k0)
+            for (int d = 0; d < 2; ++d) {
+                gp.A.push_back((d ? tp.ADz.p : tp.Az.p) + size_t(k0) * nh * nh);
+                gp.B.push_back(pset.dg + pset.host.dg_right[k0]);
+                gp.C.push_back((d ? eig_ADzP_.p : eig_AzP_.p) + size_t(k0) * nh * Np);
+            }
+        gp.M = nh; gp.N = N; gp.K = nh; gp.lda = nh; gp.ldb = Np; gp.ldc = Np;
+        CCF_CUDA(cudaMemsetAsync(eig_AzP_.p, 0, eig_AzP_.n * sizeof(double), c.stream));
+        CCF_CUDA(cudaMemsetAsync(eig_ADzP_.p, 0, eig_ADzP_.n * sizeof(double), c.stream));
+        gp.upload();
+        gp.launch(c.stream);
+        CCF_CUDA(cudaStreamSynchronize(c.stream));
+    }
+    // PL_P[s] A_t for every composite curl/decompose block (M x mh, ld mh)
+    eig_anal_.alloc(anal_.blocks.size());
+    {
+        GemmPlan gp;
+        for (int s = 0; s < g.nslots; ++s)
+            for (const CompositeTerm& ct : anal_.terms[size_t(s)]) {
+                gp.A.push_back(pset.dg + pset.host.dg_left[size_t(s)]);
+                gp.B.push_back(danal_.p + ct.off);
+                gp.C.push_back(eig_anal_.p + ct.off);
+            }
+        gp.M = M; gp.N = mh; gp.K = mh; gp.lda = mh; gp.ldb = mh; gp.ldc = mh;
+        CCF_CUDA(cudaMemsetAsync(eig_anal_.p, 0, eig_anal_.n * sizeof(double), c.stream));
+        gp.upload();
+        gp.launch(c.stream);
+        CCF_CUDA(cudaStreamSynchronize(c.stream));
+    }
+    eig_set_ = &pset;
+    (void)even;
+}
+
+const double* const* Pipeline::eig_rt(DevSet& set) {
+    auto it = eig_rt_.find(&set);
+    if (it != eig_rt_.end()) return it->second;
+    const Geo& g = c.gh;
+    const int M = c.M, N = c.N, mh = g.mh;
+    const int Mp = M + (M & 1), Np = N + (N & 1);
+    auto even = [](long x) { return x + (x & 1); };
+    std::vector<const double*> rt;
+    for (int s = 0; s < g.nslots; ++s)
+        for (int k0 = 0; k0 < 2; ++k0) {
+            const long PLo = set.host.dg_left[size_t(s)], QLo = PLo + long(M) * mh, LAMo = QLo + long(mh) * Mp;
+            rt.push_back(set.dg + LAMo + even(M) + long(k0) * long(M) * Np);
+        }
+    const double** d = nullptr;
+    CCF_CUDA(cudaMalloc(&d, rt.size() * sizeof(void*)));
+    CCF_CUDA(cudaMemcpy(d, rt.data(), rt.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    eig_rt_.emplace(&set, d);
+    return d;
+}
+
+void Pipeline::eigen_rhs(DevSet& set, int ntensor, const double* const* s0, const double* const* s1, const double* w,
+                         int nsrc, double factor, double* out0, double* out1) {
+    EigRhs a{};
+    for (int q = 0; q < nsrc; ++q) {
+        a.src[0][q] = s0[q];
+        a.src[1][q] = ntensor > 1 ? s1[q] : s0[q];
+        a.w[q] = w[q];
+    }
+    a.nsrc = nsrc;
+    a.ntensor = ntensor;
+    a.out[0] = out0;
+    a.out[1] = ntensor > 1 ? out1 : out0;
+    a.rt = eig_rt(set);
+    a.factor = factor;
+    a.M = c.M;
+    a.N = c.N;
+    a.Np = c.N + (c.N & 1);
+    a.nslots = c.gh.nslots;
+    const long rows = long(a.nslots) * 2 * a.M * ntensor;
+    eigen_rhs_kernel<<<unsigned(std::min<long>(rows, 148L * 16)), 128, 0, c.stream>>>(a);
+    ++c.launches;
+}
+
+// u_t = QL Z_t QR for Z_t in the eigen layout (z0, z1) -> coefficient tensors (out0, out1)
+void Pipeline::eigen_back(DevSet& set, int ntensor, const double* z0, const double* z1, double* out0, double* out1) {
+    const Geo& g = c.gh;
+    const int M = c.M, N = c.N, mh = g.mh, nh = g.nh;
+    const int Mp = M + (M & 1), Np = N + (N & 1);
+    const size_t per = std::max(size_t(mh) * Np, size_t(M) * std::max(nh, Np));
+    if (!dT1_.p) {
+        const size_t cap = per * size_t(2 * std::max(c.gh.nslots, c.gf.nslots) * 4);
+        dT1_.alloc(cap);
+        dZ_.alloc(cap);
+        dT3_.alloc(cap);
+    }
+    const void* keyp[1] = {&set};
+    const int ci[1] = {ntensor};
+    bool fresh;
+    GemmPlan& e3 = gemm(ptr_key("e3", 1, keyp, keyp, ci), fresh);
+    GemmPlan& e4 = gemm(ptr_key("e4", 1, keyp, keyp, ci), fresh);
+    if (fresh) {
+        const double* dg = set.dg;
+        long task = 0;
+        for (int t = 0; t < ntensor; ++t)
+            for (int s = 0; s < g.nslots; ++s)
+                for (int k0 = 0; k0 < 2; ++k0)
+                    for (int pl = 0; pl < 2; ++pl, ++task) {
+                        const long PLo = set.host.dg_left[size_t(s)], QLo = PLo + long(M) * mh;
+                        const long PRo = set.host.dg_right[k0], QRo = PRo + long(nh) * Np;
+                        double* T3 = dT3_.p + size_t(task) * per;
+                        e3.A.push_back(dg + QLo);                                       // QL  mh x M (ld Mp)
+                        e3.B.push_back(nullptr);
+                        e3.Boff.push_back((long(t) << kBaseShift) + eig_off(s, pl, k0));  // Z   M x N (ld 2 Np)
+                        e3.C.push_back(T3);                                             // T3  mh x N (ld Np)
+                        e4.A.push_back(T3);
+                        e4.B.push_back(dg + QRo);                                       // QR  N x nh
+                        e4.Coff.push_back((long(t) << kBaseShift) + long(s) * g.slot_stride + long(pl) * g.plane_stride +
+                                          long(k0) * nh);                               // u   mh x nh (ld n)
+                    }
+        e3.M = mh; e3.N = N; e3.K = M; e3.lda = Mp; e3.ldb = 2 * Np; e3.ldc = Np;
+        e4.M = mh; e4.N = nh; e4.K = N; e4.lda = Np; e4.ldb = nh; e4.ldc = g.n;
+        e3.upload();
+        e4.upload();
+    }
+    e3.launch(c.stream, z0, ntensor > 1 ? z1 : z0);
+    c.gemm_flops += e3.flops();
+    e4.launch(c.stream, nullptr, nullptr, out0, ntensor > 1 ? out1 : out0);
+    c.gemm_flops += e4.flops();
+    c.launches += 2;
+}
+
+// Z = PL_P u PR (no RT) for one coefficient tensor -> eigen layout (initial NS state)
+void Pipeline::to_eigen(DevSet& pset, const double* u, double* z) {
+    const Geo& g = c.gh;
+    const int M = c.M, N = c.N, mh = g.mh, nh = g.nh;
+    const int Np = N + (N & 1);
+    const size_t per = std::max(size_t(mh) * Np, size_t(M) * std::max(nh, Np));
+    if (!dT1_.p) {
+        const size_t cap = per * size_t(2 * std::max(c.gh.nslots, c.gf.nslots) * 4);
+        dT1_.alloc(cap);
+        dZ_.alloc(cap);
+        dT3_.alloc(cap);
+    }
+    GemmPlan t1, t2;
+    long task = 0;
+    for (int s = 0; s < g.nslots; ++s)
+        for (int k0 = 0; k0 < 2; ++k0)
+            for (int pl = 0; pl < 2; ++pl, ++task) {
+                double* T1 = dT1_.p + size_t(task) * per;
+                t1.A.push_back(pset.dg + pset.host.dg_left[size_t(s)]);
+                t1.B.push_back(u + long(s) * g.slot_stride + long(pl) * g.plane_stride + long(k0) * nh);
+                t1.C.push_back(T1);
+                t2.A.push_back(T1);
+                t2.B.push_back(pset.dg + pset.host.dg_right[k0]);
+                t2.C.push_back(z + eig_off(s, pl, k0));
+            }
+    t1.M = M; t1.N = nh; t1.K = mh; t1.lda = mh; t1.ldb = g.n; t1.ldc = nh;
+    t2.M = M; t2.N = N; t2.K = nh; t2.lda = nh; t2.ldb = Np; t2.ldc = 2 * Np;
+    CCF_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * size_t(g.nslots) * 2 * M * 2 * Np, c.stream));
+    t1.upload();
+    t2.upload();
+    t1.launch(c.stream);
+    t2.launch(c.stream);
+    CCF_CUDA(cudaStreamSynchronize(c.stream));
+    c.launches += 2;
+}
+
 void Pipeline::decompose(const double* vr, const double* vt, const double* vz, double* lam, double* gam) {
     const Geo& g = c.gh;
     CurlDecomp a{};
@@ -1202,39 +1429,75 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
     Ctx& c = P.c;
     const double* lw = lam[cur].p;
     const double* gw = gam[cur].p;
-    if (!disable_nonlinear) {
-        double* lpsi = P.scratch(18);
-        c.mark("start");
-        // velocity_from_vorticity, ptns.cpp:85-91: lambda_psi = Poisson3D(-lambda_omega); after the first
-        // step lambda_omega comes from our Helmholtz solve in the shared modal basis (modal_solve_from_z)
-        if (!(zvalid && P.modal_solve_from_z(c.set(false, true, 1.0), -1.0, lpsi))) P.poisson(lw, -1.0, lpsi);
-        c.mark("P_poisson_solve");
-        P.nonlinear(gw, lpsi, lw, gw, nl[nnew].p, ng[nnew].p);  // nonlinear_term(v, omega)
-    }
     double koh, bw[4], iw[4] = {0, 0, 0, 0};
     bdf_table(b, &koh, bw);
     if (eo > 0) imex_table(eo, iw);
     const double kappa = koh * h;
     const double scale = kappa * (1.0 / reynolds);
-    const double* sl[kMaxSrc];
-    const double* sg[kMaxSrc];
-    double wl[kMaxSrc];
-    int ns = 0;
-    for (int i = 0; i < b; ++i) {
-        sl[ns] = lam[(cur + i) % 5].p;
-        sg[ns] = gam[(cur + i) % 5].p;
-        wl[ns++] = bw[i];
+    if (eigen) {
+        // eigen-coordinate step (see Pipeline::eig_off): every modal solve is (RHS .* RT) + back transform
+        DevSet& pset = c.set(false, true, 1.0);
+        if (!disable_nonlinear) {
+            double* lpsi = P.scratch(18);
+            double* zp = P.scratch(19);
+            c.mark("start");
+            const double* zs[1] = {zl[cur].p};
+            const double wm1[1] = {-1.0};
+            P.eigen_rhs(pset, 1, zs, zs, wm1, 1, 1.0, zp, zp);     // Z_P = -Z_lambda .* RT_P
+            P.eigen_back(pset, 1, zp, zp, lpsi, lpsi);            // lambda_psi = QL Z_P QR
+            c.mark("P_poisson_solve");
+            P.nonlinear(gw, lpsi, lw, gw, nl[nnew].p, ng[nnew].p, &pset);  // N~ = PL_P N PR
+        }
+        const double* sl[kMaxSrc];
+        const double* sg[kMaxSrc];
+        double wl[kMaxSrc];
+        int ns = 0;
+        for (int i = 0; i < b; ++i) {
+            sl[ns] = zl[(cur + i) % 5].p;
+            sg[ns] = zg[(cur + i) % 5].p;
+            wl[ns++] = bw[i];
+        }
+        for (int i = 0; i < eo; ++i) {
+            sl[ns] = nl[(nnew + i) % 5].p;
+            sg[ns] = ng[(nnew + i) % 5].p;
+            wl[ns++] = kappa * iw[i];
+        }
+        DevSet& set = c.set(false, false, scale);
+        if (c.prof_events.empty()) c.mark("start");
+        P.eigen_rhs(set, 2, sl, sg, wl, ns, -1.0 / scale, zl[out].p, zg[out].p);  // PL_H = -(1/s) PL_P
+        c.mark("H_rhs_combine");
+        P.eigen_back(set, 2, zl[out].p, zg[out].p, lam[out].p, gam[out].p);
+        c.mark("H_helmholtz_solve");
+    } else {
+        if (!disable_nonlinear) {
+            double* lpsi = P.scratch(18);
+            c.mark("start");
+            // velocity_from_vorticity, ptns.cpp:85-91: lambda_psi = Poisson3D(-lambda_omega); after the first
+            // step lambda_omega comes from our Helmholtz solve in the shared modal basis (modal_solve_from_z)
+            if (!(zvalid && P.modal_solve_from_z(c.set(false, true, 1.0), -1.0, lpsi))) P.poisson(lw, -1.0, lpsi);
+            c.mark("P_poisson_solve");
+            P.nonlinear(gw, lpsi, lw, gw, nl[nnew].p, ng[nnew].p);  // nonlinear_term(v, omega)
+        }
+        const double* sl[kMaxSrc];
+        const double* sg[kMaxSrc];
+        double wl[kMaxSrc];
+        int ns = 0;
+        for (int i = 0; i < b; ++i) {
+            sl[ns] = lam[(cur + i) % 5].p;
+            sg[ns] = gam[(cur + i) % 5].p;
+            wl[ns++] = bw[i];
+        }
+        for (int i = 0; i < eo; ++i) {  // kappa * sum_i imex_i N_i  (ptns.cpp:235-245, timestep.cpp:71-73)
+            sl[ns] = nl[(nnew + i) % 5].p;
+            sg[ns] = ng[(nnew + i) % 5].p;
+            wl[ns++] = kappa * iw[i];
+        }
+        DevSet& set = c.set(false, false, scale);
+        if (c.prof_events.empty()) c.mark("start");
+        P.modal_solve(set, false, 2, sl, wl, ns, sg, wl, ns, lam[out].p, gam[out].p, "H_rhs_combine");
+        c.mark("H_helmholtz_solve");
+        zvalid = P.last_z_valid_;  // Z of lambda_omega(out) stays in dZ_ (shared modal basis) for the next P
     }
-    for (int i = 0; i < eo; ++i) {  // kappa * sum_i imex_i N_i  (ptns.cpp:235-245, timestep.cpp:71-73)
-        sl[ns] = nl[(nnew + i) % 5].p;
-        sg[ns] = ng[(nnew + i) % 5].p;
-        wl[ns++] = kappa * iw[i];
-    }
-    DevSet& set = c.set(false, false, scale);
-    if (c.prof_events.empty()) c.mark("start");
-    P.modal_solve(set, false, 2, sl, wl, ns, sg, wl, ns, lam[out].p, gam[out].p, "H_rhs_combine");
-    c.mark("H_helmholtz_solve");
-    zvalid = P.last_z_valid_;  // Z of lambda_omega(out) stays in dZ_ (shared modal basis) for the next P
     const long T = P.T;
     finite_check_kernel<<<std::min<long>(1184, (T + 255) / 256), 256, 0, c.stream>>>(lam[out].p, T, dflag);
     finite_check_kernel<<<std::min<long>(1184, (T + 255) / 256), 256, 0, c.stream>>>(gam[out].p, T, dflag);

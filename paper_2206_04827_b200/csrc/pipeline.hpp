@@ -78,8 +78,17 @@ public:
     void theta_cross(const double* const* v6, double* const* a3);
     void curl_decompose(const double* ar, const double* at, const double* az, double* out_r, double* out_t,
                         double* out_z, double* lam, double* gam);
+    // eig != nullptr: output N~ = PL_P N PR in the eigen layout of that (Poisson) set's modal basis
     void nonlinear(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w, double* lam_n,
-                   double* gam_n);
+                   double* gam_n, DevSet* eig = nullptr);
+    // eigen-coordinate NS state (see pipeline.cu)
+    long eig_off(int s, int pl, int k0) const;
+    void ensure_eigen(DevSet& pset);
+    const double* const* eig_rt(DevSet& set);
+    void eigen_rhs(DevSet& set, int ntensor, const double* const* s0, const double* const* s1, const double* w, int nsrc,
+                   double factor, double* out0, double* out1);
+    void eigen_back(DevSet& set, int ntensor, const double* z0, const double* z1, double* out0, double* out1);
+    void to_eigen(DevSet& pset, const double* u, double* z);
     void poisson(const double* f, double w, double* u);  // u = Poisson3D(w * f), half mode
     // Modal Sylvester solves of a solver set for 1 or 2 tensors with fused RHS combinations
     // (out_t = Solve(sum_i w_t[i] src_t[i])): fast diagonalization on the tensor cores, or the
@@ -102,7 +111,7 @@ public:
     const double* full_sT();
     double* big2(size_t doubles);
 
-private:
+public:  // internal state (used by the NS stepper and the C-ABI layer)
     std::vector<DBuf> scr_;
     DBuf big_, big2_, rAT_, rST_;
     bool theta_attr_ = false, theta_generic_ = false, theta_w_ = true;  // CCF_THETA_GENERIC=1 forces the radix-2 path
@@ -112,12 +121,16 @@ private:
     bool comp_ready_ = false, comp_off_ = false;  // CCF_NONLINEAR_PENCIL=1: sequential pencil path
     CompositeSet synth_, anal_;
     DBuf dsynth_, danal_;
+    bool composite_off() const { return comp_off_; }
     void ensure_composite();
     void nonlinear_pencil(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w,
                           double* lam_n, double* gam_n);
     DBuf fcomb_[2], dT1_, dZ_, dT3_;  // fast-diagonalization scratch
     std::map<std::string, std::pair<FdTask*, int>> fdtasks_;  // fused-solve task lists (device)
     std::map<const void*, const double**> zrt_;               // per set: RT table per Poisson task
+    DevSet* eig_set_ = nullptr;                               // modal basis the folded blocks below belong to
+    DBuf eig_AzP_, eig_ADzP_, eig_anal_;
+    std::map<const void*, const double* const*> eig_rt_;      // per set: RT table per (slot, k0)
     bool fd_fused_ = false, fd_attr_ = false;                    // CCF_FDSOLVE_FUSED=1: fused solve kernel
 };
 
@@ -137,6 +150,8 @@ struct NSState {
     long launches_per_step = 0;
     bool use_graphs = true;
     bool zvalid = false;  // the last Helmholtz solve left Z(lambda_omega) in the shared modal basis
+    bool eigen = false;   // eigen-coordinate state (Z / N~ rings in the shared modal basis)
+    DBuf zl[5], zg[5];    // omega history in eigen coordinates (same ring slots as lam / gam)
     ~NSState();
     void step_once();
     void enqueue(int b, int eo, int cur, int out, int nnew);

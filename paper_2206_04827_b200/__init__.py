@@ -178,6 +178,8 @@ class Context:
     def _check(self, st):
         if st == 0:
             return
+        if not getattr(self, "h", None):
+            raise CCFError("context is closed")
         kind, sl, sh = C.c_int(), C.c_int(), C.c_int()
         hist = (C.c_double * 8)()
         nh = C.c_int(8)

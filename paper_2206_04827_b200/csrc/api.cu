@@ -1,5 +1,6 @@
 // C-ABI (include/ccf.h) over the B200 CCF context.
 #include <cstring>
+#include <set>
 #include <vector>
 
 #include "../../include/ccf.h"
@@ -12,6 +13,7 @@
 struct ccf_ctx {
     std::unique_ptr<ccf::Ctx> c;
     std::unique_ptr<ccf::Pipeline> pipe;
+    std::set<ccf_ns_state*> states;  // live steppers: detached (ctx = nullptr) when the context goes first
     ccf::Pipeline& pl() {
         if (!pipe) pipe = std::make_unique<ccf::Pipeline>(*c);
         return *pipe;
@@ -97,6 +99,10 @@ ccf_status ccf_ctx_destroy(ccf_ctx* ctx) {
     if (!ctx) return CCF_OK;
     try {
         if (ctx->c) cudaSetDevice(ctx->c->device);
+        for (ccf_ns_state* st : ctx->states) {
+            st->ctx = nullptr;  // later calls on the stepper report CCF_INTERNAL_ERROR; destroy only frees it
+            st->st.pl = nullptr;
+        }
         ctx->pipe.reset();
         delete ctx;
     } catch (...) {
@@ -487,6 +493,7 @@ ccf_status ccf_ns_create(ccf_ctx* ctx, double reynolds, double h, int order, int
             }
         }
         c.sync();
+        ctx->states.insert(st.get());
         *out = st.release();
     });
 }
@@ -506,6 +513,7 @@ ccf_status ccf_ns_step(ccf_ns_state* st, int nsteps) {
 ccf_status ccf_ns_get_omega(ccf_ns_state* st, double* lam, double* gam, double* time, int* steps_taken) {
     if (!st) return CCF_INTERNAL_ERROR;
     return guard(st->ctx, [&](Ctx& c) {
+        st->st.omega_coeff();
         c.store_coeff(st->st.lam[st->st.head].p, lam, false, 0, 0);
         c.store_coeff(st->st.gam[st->st.head].p, gam, false, 0, 1);
         c.sync();
@@ -516,7 +524,10 @@ ccf_status ccf_ns_get_omega(ccf_ns_state* st, double* lam, double* gam, double* 
 
 ccf_status ccf_ns_destroy(ccf_ns_state* st) {
     if (!st) return CCF_OK;
-    if (st->ctx && st->ctx->c) cudaSetDevice(st->ctx->c->device);
+    if (st->ctx) {
+        if (st->ctx->c) cudaSetDevice(st->ctx->c->device);
+        st->ctx->states.erase(st);
+    }
     delete st;
     return CCF_OK;
 }

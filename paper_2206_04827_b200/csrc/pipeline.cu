@@ -588,7 +588,7 @@ void Pipeline::ensure_composite() {
 //   Y  = z analysis of (a_r, a_t, a_z, dz a_r, dz a_t)
 //   (gamma_N, lambda_N) = per-slot composite r operators (curl + decompose + r analysis) on Y
 void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w,
-                         double* lam_n, double* gam_n, DevSet* eig) {
+                         double* lam_n, double* gam_n, DevSet* eig, bool zpre) {
     ensure_composite();
     if (eig && comp_off_) throw Error(INTERNAL, "nonlinear: eigen-coordinate output needs the composite path");
     if (comp_off_) {
@@ -641,8 +641,11 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
         zs.ldc = g.n;
         zs.upload();
     }
-    zs.launch(c.stream);
-    c.gemm_flops += zs.flops();
+    if (!zpre) {  // zpre: the caller synthesized the six z tensors (eigen_zsynth)
+        zw_owner_ = nullptr;
+        zs.launch(c.stream);
+        c.gemm_flops += zs.flops();
+    }
     // ---- composite r synthesis -> (r, z)-values of the 6 velocity / vorticity components
     GemmPlan& rs = gemm(ptr_key("nrs", 6, keyp, keyp, cls0), fresh);
     if (fresh) {
@@ -741,6 +744,7 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
 void Pipeline::nonlinear_pencil(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w,
                                 double* lam_n, double* gam_n) {
     // proj/src/ptns.cpp:114-149
+    zw_owner_ = nullptr;
     double* comp[6];
     for (int i = 0; i < 6; ++i) comp[i] = scratch(i);
     const double* lam[2] = {lam_v, lam_w};
@@ -1092,8 +1096,91 @@ void Pipeline::ensure_eigen(DevSet& pset) {
         gp.launch(c.stream);
         CCF_CUDA(cudaStreamSynchronize(c.stream));
     }
+    // QS[k0] = QR[k0] Sz[k0], QD[k0] = QR[k0] DzS[1 - k0] (N x nh): u_k0 Sz = T3 QS, the dz synthesis
+    // of the same half lands in value half 1 - k0
+    eig_QS_.alloc(size_t(2) * N * nh);
+    eig_QD_.alloc(size_t(2) * N * nh);
+    {
+        GemmPlan gp;
+        for (int k0 = 0; k0 < 2; ++k0)
+            for (int d = 0; d < 2; ++d) {
+                gp.A.push_back(pset.dg + pset.host.dg_right[k0] + long(nh) * Np);  // QR N x nh
+                gp.B.push_back(d ? tp.DzS.p + size_t(1 - k0) * nh * nh : tp.Sz.p + size_t(k0) * nh * nh);
+                gp.C.push_back((d ? eig_QD_.p : eig_QS_.p) + size_t(k0) * N * nh);
+            }
+        gp.M = N; gp.N = nh; gp.K = nh; gp.lda = nh; gp.ldb = nh; gp.ldc = nh;
+        gp.upload();
+        gp.launch(c.stream);
+        CCF_CUDA(cudaStreamSynchronize(c.stream));
+    }
     eig_set_ = &pset;
     (void)even;
+}
+
+// z-synthesized tensors straight from eigen coordinates: T3 = QL Z (e3), then for each requested
+// output S_t (value halves [E | O] of u_t Sz) and D_t (of (dz u_t) Sz): T3 QS[k0] into half k0,
+// T3 QD[k0] into half 1 - k0 (ld n). Replaces u = T3 QR followed by the z synthesis of u.
+void Pipeline::eigen_zsynth(DevSet& set, int ntensor, const double* z0, const double* z1, double* const* outS,
+                            double* const* outD) {
+    const Geo& g = c.gh;
+    const int M = c.M, N = c.N, mh = g.mh, nh = g.nh;
+    const int Mp = M + (M & 1), Np = N + (N & 1);
+    const size_t per = std::max(size_t(mh) * Np, size_t(M) * std::max(nh, Np));
+    if (!dT1_.p) {
+        const size_t cap = per * size_t(2 * std::max(c.gh.nslots, c.gf.nslots) * 4);
+        dT1_.alloc(cap);
+        dZ_.alloc(cap);
+        dT3_.alloc(cap);
+    }
+    const void* keyp[4] = {&set, &set, &set, &set};
+    const int ci[4] = {ntensor, ntensor, ntensor, ntensor};
+    bool fresh;
+    GemmPlan& e3 = gemm(ptr_key("ez3", 1, keyp, keyp, ci), fresh);
+    if (fresh) {
+        const double* dg = set.dg;
+        long task = 0;
+        for (int t = 0; t < ntensor; ++t)
+            for (int s = 0; s < g.nslots; ++s)
+                for (int k0 = 0; k0 < 2; ++k0)
+                    for (int pl = 0; pl < 2; ++pl, ++task) {
+                        const long PLo = set.host.dg_left[size_t(s)], QLo = PLo + long(M) * mh;
+                        e3.A.push_back(dg + QLo);
+                        e3.B.push_back(nullptr);
+                        e3.Boff.push_back((long(t) << kBaseShift) + eig_off(s, pl, k0));
+                        e3.C.push_back(dT3_.p + size_t(task) * per);
+                    }
+        e3.M = mh; e3.N = N; e3.K = M; e3.lda = Mp; e3.ldb = 2 * Np; e3.ldc = Np;
+        e3.upload();
+    }
+    const void* okey[4] = {outS[0], outD[0], ntensor > 1 ? outS[1] : nullptr, ntensor > 1 ? outD[1] : nullptr};
+    GemmPlan& zo = gemm(ptr_key("ezs", 4, okey, keyp, ci), fresh);
+    if (fresh) {
+        long task = 0;
+        for (int t = 0; t < ntensor; ++t)
+            for (int s = 0; s < g.nslots; ++s)
+                for (int k0 = 0; k0 < 2; ++k0)
+                    for (int pl = 0; pl < 2; ++pl, ++task) {
+                        const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
+                        const double* T3 = dT3_.p + size_t(task) * per;
+                        if (outS[t]) {
+                            zo.A.push_back(T3);
+                            zo.B.push_back(eig_QS_.p + size_t(k0) * N * nh);
+                            zo.C.push_back(outS[t] + off + long(k0) * nh);
+                        }
+                        if (outD[t]) {
+                            zo.A.push_back(T3);
+                            zo.B.push_back(eig_QD_.p + size_t(k0) * N * nh);
+                            zo.C.push_back(outD[t] + off + long(1 - k0) * nh);
+                        }
+                    }
+        zo.M = mh; zo.N = nh; zo.K = N; zo.lda = Np; zo.ldb = nh; zo.ldc = g.n;
+        zo.upload();
+    }
+    e3.launch(c.stream, z0, ntensor > 1 ? z1 : z0);
+    c.gemm_flops += e3.flops();
+    zo.launch(c.stream);
+    c.gemm_flops += zo.flops();
+    c.launches += 2;
 }
 
 const double* const* Pipeline::eig_rt(DevSet& set) {
@@ -1435,18 +1522,24 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
     const double kappa = koh * h;
     const double scale = kappa * (1.0 / reynolds);
     if (eigen) {
-        // eigen-coordinate step (see Pipeline::eig_off): every modal solve is (RHS .* RT) + back transform
+        // eigen-coordinate step (see Pipeline::eig_off): every modal solve is (RHS .* RT) + back transform,
+        // and the back transforms produce the nonlinear term's z-synthesized inputs directly
+        // (Pipeline::eigen_zsynth); omega itself is reconstructed on demand (NSState::omega_coeff)
         DevSet& pset = c.set(false, true, 1.0);
         if (!disable_nonlinear) {
-            double* lpsi = P.scratch(18);
             double* zp = P.scratch(19);
             c.mark("start");
             const double* zs[1] = {zl[cur].p};
             const double wm1[1] = {-1.0};
-            P.eigen_rhs(pset, 1, zs, zs, wm1, 1, 1.0, zp, zp);     // Z_P = -Z_lambda .* RT_P
-            P.eigen_back(pset, 1, zp, zp, lpsi, lpsi);            // lambda_psi = QL Z_P QR
+            P.eigen_rhs(pset, 1, zs, zs, wm1, 1, 1.0, zp, zp);  // Z_P = -Z_lambda .* RT_P
+            // velocity_from_vorticity (ptns.cpp:85-91): lambda_v = gamma_omega (scratch 4, left by the last
+            // step), gamma_v = lambda_psi: its z synthesis and dz synthesis straight from Z_P
+            double* oS[1] = {P.scratch(1)};
+            double* oD[1] = {P.scratch(2)};
+            P.eigen_zsynth(pset, 1, zp, zp, oS, oD);
             c.mark("P_poisson_solve");
-            P.nonlinear(gw, lpsi, lw, gw, nl[nnew].p, ng[nnew].p, &pset);  // N~ = PL_P N PR
+            P.nonlinear(P.scratch(4), P.scratch(1), P.scratch(3), P.scratch(4), nl[nnew].p, ng[nnew].p, &pset,
+                        true);  // N~ = PL_P N PR
         }
         const double* sl[kMaxSrc];
         const double* sg[kMaxSrc];
@@ -1466,8 +1559,15 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
         if (c.prof_events.empty()) c.mark("start");
         P.eigen_rhs(set, 2, sl, sg, wl, ns, -1.0 / scale, zl[out].p, zg[out].p);  // PL_H = -(1/s) PL_P
         c.mark("H_rhs_combine");
-        P.eigen_back(set, 2, zl[out].p, zg[out].p, lam[out].p, gam[out].p);
-        c.mark("H_helmholtz_solve");
+        if (!disable_nonlinear) {
+            zsynth_omega(out);
+            c.mark("H_helmholtz_solve");
+        }
+        const long E = long(c.gh.nslots) * 4 * c.M * (c.N + (c.N & 1));
+        finite_check_kernel<<<std::min<long>(1184, (E + 255) / 256), 256, 0, c.stream>>>(zl[out].p, E, dflag);
+        finite_check_kernel<<<std::min<long>(1184, (E + 255) / 256), 256, 0, c.stream>>>(zg[out].p, E, dflag);
+        c.launches += 2;
+        return;
     } else {
         if (!disable_nonlinear) {
             double* lpsi = P.scratch(18);
@@ -1504,8 +1604,61 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
     c.launches += 2;
 }
 
+// the nonlinear term's omega inputs (z synthesis of lambda_omega, gamma_omega, dz gamma_omega) into
+// scratch 3..5, from the eigen state of ring slot r
+void NSState::zsynth_omega(int r) {
+    Pipeline& P = *pl;
+    if (coeff_head == r) {  // the coefficient state is authoritative (initial data)
+        P.zsynth_coeff(lam[r].p, gam[r].p, P.scratch(3), P.scratch(4), P.scratch(5));
+        P.zw_owner_ = this;
+        return;
+    }
+    double* oS[2] = {P.scratch(3), P.scratch(4)};
+    double* oD[2] = {nullptr, P.scratch(5)};
+    P.eigen_zsynth(P.c.set(false, true, 1.0), 2, zl[r].p, zg[r].p, oS, oD);
+    P.zw_owner_ = this;
+}
+
+// same from the coefficient-space omega (the initial data: it need not lie in the range of QL PL, so
+// its z tensors are not those of QL Z0 QR)
+void Pipeline::zsynth_coeff(const double* lam, const double* gam, double* oS0, double* oS1, double* oD1) {
+    const Geo& g = c.gh;
+    const void* keyp[5] = {lam, gam, oS0, oS1, oD1};
+    bool fresh;
+    GemmPlan& zs = gemm(ptr_key("czs", 5, keyp, keyp, nullptr), fresh);
+    if (fresh) {
+        const double* src[3] = {lam, gam, gam};
+        double* dst[3] = {oS0, oS1, oD1};
+        for (int x = 0; x < 3; ++x)
+            for (int s = 0; s < g.nslots; ++s)
+                for (int pl = 0; pl < 2; ++pl) {
+                    const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
+                    for (int po = 0; po < 2; ++po) {
+                        const int pi = x == 2 ? 1 - po : po;
+                        zs.A.push_back(src[x] + off + pi * g.nh);
+                        zs.B.push_back((x == 2 ? tp.DzS.p : tp.Sz.p) + size_t(po) * g.nh * g.nh);
+                        zs.C.push_back(dst[x] + off + po * g.nh);
+                    }
+                }
+        zs.M = g.mh; zs.N = g.nh; zs.K = g.nh; zs.lda = g.n; zs.ldb = g.nh; zs.ldc = g.n;
+        zs.upload();
+    }
+    zs.launch(c.stream);
+    c.gemm_flops += zs.flops();
+    ++c.launches;
+}
+
+// coefficient-space omega of the newest ring slot (eigen mode keeps only Z between steps)
+void NSState::omega_coeff() {
+    if (!eigen || coeff_head == head) return;
+    pl->eigen_back(pl->c.set(false, true, 1.0), 2, zl[head].p, zg[head].p, lam[head].p, gam[head].p);
+    coeff_head = head;
+}
+
 void NSState::step_once() {
     Ctx& c = pl->c;
+    // scratch 3..5 may have been reused (another stepper, a standalone nonlinear call) since our last step
+    if (eigen && !disable_nonlinear && pl->zw_owner_ != this) zsynth_omega(head);
     const int b = std::min(order, steps + 1);
     const int out = (head + 4) % 5;
     const int nnew = (nhead + 4) % 5;
@@ -1533,6 +1686,7 @@ void NSState::step_once() {
         if (steady) launches_per_step = c.launches - l0;
     }
     head = out;
+    coeff_head = eigen ? -1 : head;
     if (!disable_nonlinear) {
         nhead = nnew;
         ncount = ncnt;

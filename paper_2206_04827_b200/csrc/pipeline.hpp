@@ -79,8 +79,12 @@ public:
     void curl_decompose(const double* ar, const double* at, const double* az, double* out_r, double* out_t,
                         double* out_z, double* lam, double* gam);
     // eig != nullptr: output N~ = PL_P N PR in the eigen layout of that (Poisson) set's modal basis
+    // zpre: scratch(0..5) already hold the z-synthesized inputs (lambda_v = gamma_w aliased to scratch(4))
     void nonlinear(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w, double* lam_n,
-                   double* gam_n, DevSet* eig = nullptr);
+                   double* gam_n, DevSet* eig = nullptr, bool zpre = false);
+    void zsynth_coeff(const double* lam, const double* gam, double* oS0, double* oS1, double* oD1);
+    void eigen_zsynth(DevSet& set, int ntensor, const double* z0, const double* z1, double* const* outS,
+                      double* const* outD);
     // eigen-coordinate NS state (see pipeline.cu)
     long eig_off(int s, int pl, int k0) const;
     void ensure_eigen(DevSet& pset);
@@ -105,6 +109,7 @@ public:
     void analyze_full(const double* values, double* coeffs);     // reference layouts, host or device
     void synthesize_full(const double* coeffs, double* values);
     double* scratch(int i);  // internal scratch tensors
+    const void* zw_owner_ = nullptr;  // NSState whose omega z tensors occupy scratch 3..5
     double* big_scratch(size_t doubles);
 
     const double* full_rT();
@@ -129,7 +134,7 @@ public:  // internal state (used by the NS stepper and the C-ABI layer)
     std::map<std::string, std::pair<FdTask*, int>> fdtasks_;  // fused-solve task lists (device)
     std::map<const void*, const double**> zrt_;               // per set: RT table per Poisson task
     DevSet* eig_set_ = nullptr;                               // modal basis the folded blocks below belong to
-    DBuf eig_AzP_, eig_ADzP_, eig_anal_;
+    DBuf eig_AzP_, eig_ADzP_, eig_anal_, eig_QS_, eig_QD_;
     std::map<const void*, const double* const*> eig_rt_;      // per set: RT table per (slot, k0)
     bool fd_fused_ = false, fd_attr_ = false;                    // CCF_FDSOLVE_FUSED=1: fused solve kernel
 };
@@ -152,7 +157,10 @@ struct NSState {
     bool zvalid = false;  // the last Helmholtz solve left Z(lambda_omega) in the shared modal basis
     bool eigen = false;   // eigen-coordinate state (Z / N~ rings in the shared modal basis)
     DBuf zl[5], zg[5];    // omega history in eigen coordinates (same ring slots as lam / gam)
+    int coeff_head = 0;   // ring slot whose lam / gam hold the coefficient-space omega (-1: none)
     ~NSState();
+    void zsynth_omega(int r);
+    void omega_coeff();
     void step_once();
     void enqueue(int b, int eo, int cur, int out, int nnew);
 };

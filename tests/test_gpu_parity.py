@@ -97,6 +97,38 @@ def test_ns_steps_vs_oracle(P, O):
     ctx.close()
 
 
+def test_context_closed_before_stepper(P):
+    """Destroying the context first detaches its steppers: later calls fail cleanly, close() is safe."""
+    lam = 1e-3 * hermitian_coeffs(16, 16, 16, 0.7, 1)
+    gam = 1e-3 * hermitian_coeffs(16, 16, 16, 0.7, 2)
+    ctx = P.Context(16, 16, 16)
+    ns = P.NSStepper(ctx, lam, gam, reynolds=100.0, h=1e-3)
+    ns.step(2)
+    ctx.close()
+    with pytest.raises(P.CCFError):
+        ns.step(1)
+    ns.close()
+
+
+def test_omega_readback_does_not_perturb(P):
+    """In the eigen-coordinate state omega() reconstructs the coefficients on demand; reading it every
+    step or only at the end gives the same trajectory."""
+    lam = 1e-3 * hermitian_coeffs(16, 16, 16, 0.7, 3)
+    gam = 1e-3 * hermitian_coeffs(16, 16, 16, 0.7, 4)
+    ctx = P.Context(16, 16, 16)
+    a = P.NSStepper(ctx, lam, gam, reynolds=100.0, h=1e-3)
+    b = P.NSStepper(ctx, lam, gam, reynolds=100.0, h=1e-3)
+    for _ in range(8):
+        a.step(1)
+        a.omega()
+    b.step(8)
+    (la, ga), (lb, gb) = a.omega(), b.omega()
+    assert max(rel_err(la, lb), rel_err(ga, gb)) < 1e-13
+    a.close()
+    b.close()
+    ctx.close()
+
+
 def test_graph_replay_equals_eager(P):
     # small amplitude: a random O(1) field violates the advective CFL bound and diverges (Q4)
     lam = 1e-3 * hermitian_coeffs(16, 16, 16, 0.7, 1)

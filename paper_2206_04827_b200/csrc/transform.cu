@@ -730,6 +730,8 @@ __global__ void __launch_bounds__(32 * kTWPts, 4) theta_cross256w_kernel(ThetaCr
     const int jr = blockIdx.y;
     const int i0 = blockIdx.x * (kTWPts / 2);
     const int npos = min(kTWPts / 2, g.nh - i0);
+    // 16-byte global accesses when both positions are present and every stride is even
+    const bool vec = npos == 2 && ((g.slot_stride | g.plane_stride | long(g.n) | long(g.nh)) & 1) == 0;
     const int tid = threadIdx.x;
     const int pt = tid >> 5, lane = tid & 31, col = lane & 15, h = lane >> 4;
     for (int x = tid; x < 256; x += blockDim.x) {
@@ -751,6 +753,16 @@ __global__ void __launch_bounds__(32 * kTWPts, 4) theta_cross256w_kernel(ThetaCr
         const long off = long(s) * g.slot_stride + long(jr) * g.n + i0;
         const double* __restrict__ fa = t.in[2 * pr] + off;
         const double* __restrict__ fb = t.in[2 * pr + 1] + off;
+        if (vec) {  // both z positions: 16-byte loads
+            const double* src[8] = {fa, fa + ps, fa + oo, fa + oo + ps, fb, fb + ps, fb + oo, fb + oo + ps};
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(src[u]));
+                r[0][u] = v.x;
+                r[1][u] = v.y;
+            }
+            return;
+        }
 #pragma unroll
         for (int ip = 0; ip < kTWPts / 2; ++ip) {
             if (ip >= npos) continue;
@@ -875,6 +887,7 @@ __global__ void __launch_bounds__(32 * kTWPts, 4) theta_cross256w_kernel(ThetaCr
         const int arr = f < 2 ? 0 : 1;
         const long off = long(s) * g.slot_stride + long(jr) * g.n + i0;
         double* o = t.out[f] + off;
+        double ov[4][kTWPts / 2];
 #pragma unroll
         for (int ip = 0; ip < kTWPts / 2; ++ip) {
             if (ip >= npos) break;
@@ -891,10 +904,18 @@ __global__ void __launch_bounds__(32 * kTWPts, 4) theta_cross256w_kernel(ThetaCr
                     xi[hh] = 0.5 * (zt.y - zm.y);
                 }
             }
-            o[ip] = sg * (xr[0] + xr[1]);
-            o[oo + ip] = sg * (xr[0] - xr[1]);
-            o[ps + ip] = sg * (xi[0] + xi[1]);
-            o[ps + oo + ip] = sg * (xi[0] - xi[1]);
+            ov[0][ip] = sg * (xr[0] + xr[1]);
+            ov[1][ip] = sg * (xr[0] - xr[1]);
+            ov[2][ip] = sg * (xi[0] + xi[1]);
+            ov[3][ip] = sg * (xi[0] - xi[1]);
+        }
+        double* dst[4] = {o, o + oo, o + ps, o + ps + oo};
+        if (vec) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) *reinterpret_cast<double2*>(dst[u]) = make_double2(ov[u][0], ov[u][1]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) dst[u][0] = ov[u][0];
         }
     }
 }

@@ -109,10 +109,9 @@ __global__ void theta_cross256_kernel(ThetaCross t);  // p = 256 register-FFT pa
 size_t theta_cross256_smem();
 int theta_cross256_positions();
 int theta_cross256_threads();
-__global__ void theta_cross256w_kernel(ThetaCross t);  // warp-per-point variant
-size_t theta_cross256w_smem();
-int theta_cross256w_positions();
-int theta_cross256w_threads();
+template <int NQ>
+__global__ void theta_cross256w_kernel(ThetaCross t);  // warp-per-point variant, NQ z-position pairs per CTA
+size_t theta_cross256w_smem(int nq);
 __global__ void theta_dft_full_kernel(const double* __restrict__ in, double* __restrict__ out, int m, int n, int p,
                                       int dir, const double2* __restrict__ twp);
 

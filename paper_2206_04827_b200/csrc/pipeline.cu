@@ -516,8 +516,12 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
         CCF_CUDA(cudaFuncSetAttribute(theta_cross_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CCF_CUDA(cudaFuncSetAttribute(theta_cross256_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(theta_cross256_smem())));
-        CCF_CUDA(cudaFuncSetAttribute(theta_cross256w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(theta_cross256w_smem())));
+        CCF_CUDA(cudaFuncSetAttribute(theta_cross256w_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(theta_cross256w_smem(1))));
+        CCF_CUDA(cudaFuncSetAttribute(theta_cross256w_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(theta_cross256w_smem(2))));
+        const char* q = std::getenv("CCF_THETA_PAIRS");  // z-position pairs per CTA of the warp kernel (1 | 2)
+        theta_nq_ = (q && q[0] == '1') ? 1 : 2;
         const char* v = std::getenv("CCF_THETA_VARIANT");  // "16": 16-thread FFT kernel
         theta_w_ = !(v && v[0] == '1' && v[1] == '6');
         const char* e = std::getenv("CCF_THETA_GENERIC");
@@ -525,9 +529,12 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
         theta_attr_ = true;
     }
     if (g.p == 256 && !theta_generic_ && theta_w_) {
-        const int np = theta_cross256w_positions();
+        const int np = 2 * theta_nq_;
         const dim3 grid(unsigned((g.nh + np - 1) / np), unsigned(g.mh));
-        theta_cross256w_kernel<<<grid, theta_cross256w_threads(), theta_cross256w_smem(), c.stream>>>(t);
+        if (theta_nq_ == 2)
+            theta_cross256w_kernel<2><<<grid, 256, theta_cross256w_smem(2), c.stream>>>(t);
+        else
+            theta_cross256w_kernel<1><<<grid, 128, theta_cross256w_smem(1), c.stream>>>(t);
     } else if (g.p == 256 && !theta_generic_) {
         const int np = theta_cross256_positions();
         const dim3 grid(unsigned((g.nh + np - 1) / np), unsigned(g.mh));

@@ -120,6 +120,7 @@ public:  // internal state (used by the NS stepper and the C-ABI layer)
     std::vector<DBuf> scr_;
     DBuf big_, big2_, rAT_, rST_;
     bool theta_attr_ = false, theta_generic_ = false, theta_w_ = true;  // CCF_THETA_GENERIC=1 forces the radix-2 path
+    int theta_nq_ = 2;                                                  // z-position pairs per CTA (warp kernel)
     std::map<std::string, std::unique_ptr<GemmPlan>> gemms_;
     GemmPlan& gemm(const std::string& key, bool& fresh);
     // composite radial operators of the nonlinear term (built on first use)

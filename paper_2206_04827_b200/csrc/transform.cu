@@ -717,21 +717,24 @@ __device__ __forceinline__ void half_dft16(const double2 (&x)[16], int h, double
     dft8<S>(out);
 }
 
-constexpr int kTWPts = 4;  // points per CTA (2 z positions x {+z, -z}), one warp each
 constexpr int kTWArr = 272;
 
 }  // namespace
 
-__global__ void __launch_bounds__(32 * kTWPts, 4) theta_cross256w_kernel(ThetaCross t) {
+// NQ z-position pairs per CTA (4 NQ points, one warp each); load / store tasks are (slot, pair)
+// so that the two threads of one slot cover a full 32-byte sector when NQ = 2
+template <int NQ>
+__global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(ThetaCross t) {
+    constexpr int kPts = 4 * NQ;
     extern __shared__ double2 sd[];
-    double2* twf = sd + kTWPts * 2 * kTWArr;  // twf[16 k1 + n2] = e^{-2 pi i n2 k1 / 256}
+    double2* twf = sd + kPts * 2 * kTWArr;  // twf[16 k1 + n2] = e^{-2 pi i n2 k1 / 256}
     const Geo& g = t.g;
     const int S = g.nslots;  // 129
     const int jr = blockIdx.y;
-    const int i0 = blockIdx.x * (kTWPts / 2);
-    const int npos = min(kTWPts / 2, g.nh - i0);
-    // 16-byte global accesses when both positions are present and every stride is even
-    const bool vec = npos == 2 && ((g.slot_stride | g.plane_stride | long(g.n) | long(g.nh)) & 1) == 0;
+    const int i0 = blockIdx.x * (2 * NQ);
+    const int npos = min(2 * NQ, g.nh - i0);
+    // 16-byte global accesses when every stride is even (per pair: both positions present)
+    const bool even = ((g.slot_stride | g.plane_stride | long(g.n) | long(g.nh)) & 1) == 0;
     const int tid = threadIdx.x;
     const int pt = tid >> 5, lane = tid & 31, col = lane & 15, h = lane >> 4;
     for (int x = tid; x < 256; x += blockDim.x) {
@@ -741,16 +744,21 @@ __global__ void __launch_bounds__(32 * kTWPts, 4) theta_cross256w_kernel(ThetaCr
     double2* Z = sd + pt * 2 * kTWArr;  // this point's two arrays
     double2 tv[3][8];                   // time samples of the three pairs at l = col + 16 (2j + h)
     const long ps = g.plane_stride, oo = g.nh;
-    // raw spectra of one pair for slot s = tid, prefetched into registers one pair ahead so the
-    // global-load latency overlaps the previous pair's FFTs (the Nyquist slot s = 128 is loaded
-    // directly by thread 0)
-    double raw[kTWPts / 2][8];
-    auto fetch_slot = [&](int pr, int s, double (&r)[kTWPts / 2][8]) {
+    // raw spectra of one (v, w) pair for task a = (slot a / NQ, position pair a % NQ), prefetched into
+    // registers one pair ahead so the global-load latency overlaps the previous pair's FFTs (tasks
+    // beyond the thread count, i.e. the Nyquist slot, are loaded in place)
+    const int NT = NQ * S;
+    double raw[2][8];
+    auto fetch_slot = [&](int pr, int a, double (&r)[2][8]) {
 #pragma unroll
-        for (int ip = 0; ip < kTWPts / 2; ++ip)
+        for (int ip = 0; ip < 2; ++ip)
 #pragma unroll
             for (int u = 0; u < 8; ++u) r[ip][u] = 0.0;
-        const long off = long(s) * g.slot_stride + long(jr) * g.n + i0;
+        const int s = a / NQ, q = a - s * NQ;
+        const int nq = min(2, npos - 2 * q);
+        if (nq <= 0) return;
+        const bool vec = even && nq == 2;
+        const long off = long(s) * g.slot_stride + long(jr) * g.n + i0 + 2 * q;
         const double* __restrict__ fa = t.in[2 * pr] + off;
         const double* __restrict__ fb = t.in[2 * pr + 1] + off;
         if (vec) {  // both z positions: 16-byte loads
@@ -764,8 +772,8 @@ __global__ void __launch_bounds__(32 * kTWPts, 4) theta_cross256w_kernel(ThetaCr
             return;
         }
 #pragma unroll
-        for (int ip = 0; ip < kTWPts / 2; ++ip) {
-            if (ip >= npos) continue;
+        for (int ip = 0; ip < 2; ++ip) {
+            if (ip >= nq) continue;
             r[ip][0] = __ldg(fa + ip);
             r[ip][1] = __ldg(fa + ps + ip);
             r[ip][2] = __ldg(fa + oo + ip);
@@ -776,11 +784,12 @@ __global__ void __launch_bounds__(32 * kTWPts, 4) theta_cross256w_kernel(ThetaCr
             r[ip][7] = __ldg(fb + oo + ps + ip);
         }
     };
-    auto put_slot = [&](int s, const double (&r)[kTWPts / 2][8]) {
+    auto put_slot = [&](int a, const double (&r)[2][8]) {
+        const int s = a / NQ, q = a - s * NQ;
         const double sg = (s & 1) ? -1.0 : 1.0;
         const bool reonly = (s == 0 || s == 128);
 #pragma unroll
-        for (int ip = 0; ip < kTWPts / 2; ++ip) {
+        for (int ip = 0; ip < 2; ++ip) {
             const double ar = r[ip][0], ai = r[ip][1], aro = r[ip][2], aio = r[ip][3];
             const double br = r[ip][4], bi = r[ip][5], bro = r[ip][6], bio = r[ip][7];
 #pragma unroll
@@ -788,24 +797,24 @@ __global__ void __launch_bounds__(32 * kTWPts, 4) theta_cross256w_kernel(ThetaCr
                 const double sz = hh ? -1.0 : 1.0;
                 const double xar = sg * fma(sz, aro, ar), xai = reonly ? 0.0 : sg * fma(sz, aio, ai);
                 const double xbr = sg * fma(sz, bro, br), xbi = reonly ? 0.0 : sg * fma(sz, bio, bi);
-                double2* Zp = sd + (2 * ip + hh) * 2 * kTWArr;
+                double2* Zp = sd + (2 * (2 * q + ip) + hh) * 2 * kTWArr;
                 Zp[s] = make_double2(xar - xbi, xai + xbr);
                 if (s > 0 && s < 128) Zp[256 - s] = make_double2(xar + xbi, xbr - xai);
             }
         }
     };
-    if (tid < S) fetch_slot(0, tid, raw);
+    if (tid < NT) fetch_slot(0, tid, raw);
 #pragma unroll
     for (int pr = 0; pr < 3; ++pr) {
         __syncthreads();  // previous pair's array fully consumed (and twiddles visible)
         // ---- Hermitian spectrum of pair pr for the CTA's points into array 0
-        if (tid < S) put_slot(tid, raw);
-        for (int s = tid + blockDim.x; s < S; s += blockDim.x) {  // Nyquist slot (and any p > 256 rest)
-            double r2[kTWPts / 2][8];
-            fetch_slot(pr, s, r2);
-            put_slot(s, r2);
+        if (tid < NT) put_slot(tid, raw);
+        for (int a = tid + blockDim.x; a < NT; a += blockDim.x) {  // Nyquist slot tasks
+            double r2[2][8];
+            fetch_slot(pr, a, r2);
+            put_slot(a, r2);
         }
-        if (pr < 2 && tid < S) fetch_slot(pr + 1, tid, raw);
+        if (pr < 2 && tid < NT) fetch_slot(pr + 1, tid, raw);
         __syncthreads();
         // ---- inverse pass 1: lane (n2 = col, h): DFT16 over n1 of x[16 n1 + n2] -> k1 = 2k + h
         {
@@ -879,22 +888,26 @@ __global__ void __launch_bounds__(32 * kTWPts, 4) theta_cross256w_kernel(ThetaCr
         __syncwarp();
     }
     __syncthreads();
-    // ---- unpack c_w = (-1)^w X[w mod 256] / 256 per point; store E' = (f+ + f-)/2, O' = (f+ - f-)/2
-    for (int e = tid; e < S * 3; e += blockDim.x) {
-        const int s = e % S, f = e / S;
+    // ---- unpack c_w = (-1)^w X[w mod 256] / 256 per point; store E' = (f+ + f-)/2, O' = (f+ - f-)/2;
+    //      tasks (slot, output f, position pair q)
+    for (int e = tid; e < S * 3 * NQ; e += blockDim.x) {
+        const int q = e % NQ, sf = e / NQ;
+        const int s = sf % S, f = sf / S;
+        const int nq = min(2, npos - 2 * q);
+        if (nq <= 0) continue;
         const int tt = s, tm = (256 - s) & 255;
         const double sg = ((s & 1) ? -1.0 : 1.0) * (0.5 / 256.0);
         const int arr = f < 2 ? 0 : 1;
-        const long off = long(s) * g.slot_stride + long(jr) * g.n + i0;
+        const long off = long(s) * g.slot_stride + long(jr) * g.n + i0 + 2 * q;
         double* o = t.out[f] + off;
-        double ov[4][kTWPts / 2];
+        double ov[4][2];
 #pragma unroll
-        for (int ip = 0; ip < kTWPts / 2; ++ip) {
-            if (ip >= npos) break;
+        for (int ip = 0; ip < 2; ++ip) {
+            if (ip >= nq) break;
             double xr[2], xi[2];
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
-                const double2* base = sd + (2 * ip + hh) * 2 * kTWArr + arr * kTWArr;
+                const double2* base = sd + (2 * (2 * q + ip) + hh) * 2 * kTWArr + arr * kTWArr;
                 const double2 zt = base[tt], zm = base[tm];
                 if (f == 1) {
                     xr[hh] = 0.5 * (zt.y + zm.y);
@@ -910,7 +923,7 @@ __global__ void __launch_bounds__(32 * kTWPts, 4) theta_cross256w_kernel(ThetaCr
             ov[3][ip] = sg * (xi[0] - xi[1]);
         }
         double* dst[4] = {o, o + oo, o + ps, o + ps + oo};
-        if (vec) {
+        if (even && nq == 2) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) *reinterpret_cast<double2*>(dst[u]) = make_double2(ov[u][0], ov[u][1]);
         } else {
@@ -920,9 +933,10 @@ __global__ void __launch_bounds__(32 * kTWPts, 4) theta_cross256w_kernel(ThetaCr
     }
 }
 
-size_t theta_cross256w_smem() { return (size_t(kTWPts) * 2 * kTWArr + 256) * sizeof(double2); }
-int theta_cross256w_positions() { return kTWPts / 2; }
-int theta_cross256w_threads() { return 32 * kTWPts; }
+template __global__ void theta_cross256w_kernel<1>(ThetaCross);
+template __global__ void theta_cross256w_kernel<2>(ThetaCross);
+
+size_t theta_cross256w_smem(int nq) { return (size_t(4 * nq) * 2 * kTWArr + 256) * sizeof(double2); }
 
 size_t theta_cross256_smem() { return (size_t(kT256Pts) * 3 * kT256Arr + 256) * sizeof(double2); }
 int theta_cross256_positions() { return kT256Pos; }

@@ -486,6 +486,7 @@ ccf_status ccf_ns_create(ccf_ctx* ctx, double reynolds, double h, int order, int
                 s.eigen = true;
                 for (int i = 0; i < 5; ++i) {
                     s.zl[i].alloc(size_t(T));
+                    if (i == 0) s.zpsi.alloc(size_t(T));
                     s.zg[i].alloc(size_t(T));
                 }
                 P.to_eigen(pset, s.lam[0].p, s.zl[0].p);

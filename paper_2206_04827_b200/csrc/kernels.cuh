@@ -69,6 +69,9 @@ struct EigRhs {
     const double* const* rt;
     double factor;
     int M, N, Np, nslots;
+    double* outp;              // optional: -out[0] .* rtp (the next step's Poisson RHS in eigen coordinates)
+    const double* const* rtp;  // RT table of the Poisson set
+    int* flag;                 // optional: set to 1 on a non-finite output (NaN guard, ptns.cpp:260-262)
 };
 
 // transform.cu

@@ -1032,7 +1032,8 @@ long Pipeline::eig_off(int s, int pl, int k0) const {
     return (long(s) * 2 + pl) * long(c.M) * 2 * Np + long(k0) * Np;
 }
 
-__global__ void __launch_bounds__(256) eigen_rhs_kernel(EigRhs a) {
+template <int NS>
+__global__ void __launch_bounds__(128) eigen_rhs_kernel(EigRhs a) {
     // one eigen-layout row (t, s, pl, i) per block row; 2 Np columns over the threads (16-byte pairs)
     const long rows = long(a.ntensor) * a.nslots * 2 * a.M;
     const int ld = 2 * a.Np, pairs = a.Np;  // 2 Np / 2
@@ -1045,17 +1046,25 @@ __global__ void __launch_bounds__(256) eigen_rhs_kernel(EigRhs a) {
         for (int pc = threadIdx.x; pc < pairs; pc += blockDim.x) {
             const int col = 2 * pc;
             const int k0 = col >= a.Np ? 1 : 0, j = col - k0 * a.Np;
+            double2 v[NS];  // all source loads in flight before the combination
+#pragma unroll
+            for (int q = 0; q < NS; ++q) v[q] = __ldg(reinterpret_cast<const double2*>(a.src[t][q] + base + col));
             double2 acc = make_double2(0.0, 0.0);
-            for (int q = 0; q < a.nsrc; ++q) {
-                const double2 v = __ldg(reinterpret_cast<const double2*>(a.src[t][q] + base + col));
-                acc.x = fma(a.w[q], v.x, acc.x);
-                acc.y = fma(a.w[q], v.y, acc.y);
+#pragma unroll
+            for (int q = 0; q < NS; ++q) {
+                acc.x = fma(a.w[q], v[q].x, acc.x);
+                acc.y = fma(a.w[q], v[q].y, acc.y);
             }
             const double2 r = __ldg(reinterpret_cast<const double2*>(a.rt[s * 2 + k0] + long(i) * a.Np + j));
             double2 o;
             o.x = j < a.N ? a.factor * acc.x * r.x : 0.0;
             o.y = j + 1 < a.N ? a.factor * acc.y * r.y : 0.0;
             *reinterpret_cast<double2*>(a.out[t] + base + col) = o;
+            if (a.outp && t == 0) {
+                const double2 rp = __ldg(reinterpret_cast<const double2*>(a.rtp[s * 2 + k0] + long(i) * a.Np + j));
+                *reinterpret_cast<double2*>(a.outp + base + col) = make_double2(-o.x * rp.x, -o.y * rp.y);
+            }
+            if (a.flag && !(isfinite(o.x) && isfinite(o.y))) *a.flag = 1;
         }
     }
 }
@@ -1211,8 +1220,14 @@ const double* const* Pipeline::eig_rt(DevSet& set) {
 }
 
 void Pipeline::eigen_rhs(DevSet& set, int ntensor, const double* const* s0, const double* const* s1, const double* w,
-                         int nsrc, double factor, double* out0, double* out1) {
+                         int nsrc, double factor, double* out0, double* out1, double* outp, DevSet* pset,
+                         int* flag) {
     EigRhs a{};
+    if (outp) {
+        a.outp = outp;
+        a.rtp = eig_rt(*pset);
+    }
+    a.flag = flag;
     for (int q = 0; q < nsrc; ++q) {
         a.src[0][q] = s0[q];
         a.src[1][q] = ntensor > 1 ? s1[q] : s0[q];
@@ -1229,7 +1244,18 @@ void Pipeline::eigen_rhs(DevSet& set, int ntensor, const double* const* s0, cons
     a.Np = c.N + (c.N & 1);
     a.nslots = c.gh.nslots;
     const long rows = long(a.nslots) * 2 * a.M * ntensor;
-    eigen_rhs_kernel<<<unsigned(std::min<long>(rows, 148L * 16)), 128, 0, c.stream>>>(a);
+    const unsigned grid = unsigned(std::min<long>(rows, 148L * 16));
+    switch (nsrc) {
+        case 1: eigen_rhs_kernel<1><<<grid, 128, 0, c.stream>>>(a); break;
+        case 2: eigen_rhs_kernel<2><<<grid, 128, 0, c.stream>>>(a); break;
+        case 3: eigen_rhs_kernel<3><<<grid, 128, 0, c.stream>>>(a); break;
+        case 4: eigen_rhs_kernel<4><<<grid, 128, 0, c.stream>>>(a); break;
+        case 5: eigen_rhs_kernel<5><<<grid, 128, 0, c.stream>>>(a); break;
+        case 6: eigen_rhs_kernel<6><<<grid, 128, 0, c.stream>>>(a); break;
+        case 7: eigen_rhs_kernel<7><<<grid, 128, 0, c.stream>>>(a); break;
+        case 8: eigen_rhs_kernel<8><<<grid, 128, 0, c.stream>>>(a); break;
+        default: throw Error(INTERNAL, "eigen_rhs: source count out of range");
+    }
     ++c.launches;
 }
 
@@ -1534,11 +1560,13 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
         // (Pipeline::eigen_zsynth); omega itself is reconstructed on demand (NSState::omega_coeff)
         DevSet& pset = c.set(false, true, 1.0);
         if (!disable_nonlinear) {
-            double* zp = P.scratch(19);
+            double* zp = zpsi.p;
             c.mark("start");
-            const double* zs[1] = {zl[cur].p};
-            const double wm1[1] = {-1.0};
-            P.eigen_rhs(pset, 1, zs, zs, wm1, 1, 1.0, zp, zp);  // Z_P = -Z_lambda .* RT_P
+            if (zp_head != cur) {  // the last Helmholtz pass did not leave Z_P of this omega (first step)
+                const double* zs[1] = {zl[cur].p};
+                const double wm1[1] = {-1.0};
+                P.eigen_rhs(pset, 1, zs, zs, wm1, 1, 1.0, zp, zp);  // Z_P = -Z_lambda .* RT_P
+            }
             // velocity_from_vorticity (ptns.cpp:85-91): lambda_v = gamma_omega (scratch 4, left by the last
             // step), gamma_v = lambda_psi: its z synthesis and dz synthesis straight from Z_P
             double* oS[1] = {P.scratch(1)};
@@ -1564,16 +1592,16 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
         }
         DevSet& set = c.set(false, false, scale);
         if (c.prof_events.empty()) c.mark("start");
-        P.eigen_rhs(set, 2, sl, sg, wl, ns, -1.0 / scale, zl[out].p, zg[out].p);  // PL_H = -(1/s) PL_P
+        // PL_H = -(1/s) PL_P; the same pass leaves the next step's Poisson RHS Z_P = -Z_lambda .* RT_P and
+        // raises the non-finite flag
+        P.eigen_rhs(set, 2, sl, sg, wl, ns, -1.0 / scale, zl[out].p, zg[out].p,
+                    disable_nonlinear ? nullptr : zpsi.p, &pset, dflag);
         c.mark("H_rhs_combine");
         if (!disable_nonlinear) {
+            zp_head = out;
             zsynth_omega(out);
             c.mark("H_helmholtz_solve");
         }
-        const long E = long(c.gh.nslots) * 4 * c.M * (c.N + (c.N & 1));
-        finite_check_kernel<<<std::min<long>(1184, (E + 255) / 256), 256, 0, c.stream>>>(zl[out].p, E, dflag);
-        finite_check_kernel<<<std::min<long>(1184, (E + 255) / 256), 256, 0, c.stream>>>(zg[out].p, E, dflag);
-        c.launches += 2;
         return;
     } else {
         if (!disable_nonlinear) {
@@ -1694,6 +1722,7 @@ void NSState::step_once() {
     }
     head = out;
     coeff_head = eigen ? -1 : head;
+    if (eigen && !disable_nonlinear) zp_head = out;  // (graph replays skip enqueue)
     if (!disable_nonlinear) {
         nhead = nnew;
         ncount = ncnt;

@@ -90,7 +90,8 @@ public:
     void ensure_eigen(DevSet& pset);
     const double* const* eig_rt(DevSet& set);
     void eigen_rhs(DevSet& set, int ntensor, const double* const* s0, const double* const* s1, const double* w, int nsrc,
-                   double factor, double* out0, double* out1);
+                   double factor, double* out0, double* out1, double* outp = nullptr,
+                   DevSet* pset = nullptr, int* flag = nullptr);
     void eigen_back(DevSet& set, int ntensor, const double* z0, const double* z1, double* out0, double* out1);
     void to_eigen(DevSet& pset, const double* u, double* z);
     void poisson(const double* f, double w, double* u);  // u = Poisson3D(w * f), half mode
@@ -159,6 +160,8 @@ struct NSState {
     bool eigen = false;   // eigen-coordinate state (Z / N~ rings in the shared modal basis)
     DBuf zl[5], zg[5];    // omega history in eigen coordinates (same ring slots as lam / gam)
     int coeff_head = 0;   // ring slot whose lam / gam hold the coefficient-space omega (-1: none)
+    DBuf zpsi;            // Poisson RHS -Z_lambda .* RT_P of ring slot zp_head (left by the Helmholtz pass)
+    int zp_head = -1;
     ~NSState();
     void zsynth_omega(int r);
     void omega_coeff();

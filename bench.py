@@ -246,12 +246,13 @@ def main():
     t_gemm_ms = sum(stages.get(k, 0.0) for k in gemm_stages)  # these stages launch GEMMs only
     gemm_tflops = F_gemm / (t_gemm_ms * 1e-3) / 1e12 if t_gemm_ms > 0 else None
     # step roofline: T_roof = F_gemm / P_dmma + (HBM-bound stages: theta 6 in + 3 out tensors, the
-    # Helmholtz RHS combination 2 x (sources + 1) tensors) / BW; tensor = one half-spectrum field
+    # Helmholtz RHS pass 2 x (8 sources + 1 output) tensors + the next Poisson RHS + the two RT tables
+    # (half a tensor each)) / BW; tensor = one half-spectrum field
     S = p // 2 + 1
     tensor_bytes = 8.0 * S * 2 * (m // 2) * n
     bw = peaks["hbm_gbs"] * 1e9
     pdm = peaks["fp64_dmma_tflops"] * 1e12
-    B_other = (9 + 2 * (4 + 4 + 1)) * tensor_bytes
+    B_other = (9 + 2 * (4 + 4 + 1) + 1 + 1) * tensor_bytes
     T_roof = F_gemm / pdm + B_other / bw
     B_total = B_other
 
@@ -304,8 +305,8 @@ def main():
                             "over KE"},
             "gpu_launches": stats["kernel_launches"],
             "roofline": {"bound": "tensor",
-                         "kernel": "dgemm_batched_kernel (FP64 DMMA m8n8k4): r/z transforms, composite radial "
-                                   "operators and the fast-diagonalization modal solves",
+                         "kernel": "dgemm_pipe_kernel (FP64 DMMA m8n8k4, cp.async pipeline): z transforms, composite "
+                                   "radial operators and the eigen-coordinate back transforms",
                          "achieved": gemm_tflops, "peak": peaks["fp64_dmma_tflops"], "unit": "TFLOP/s",
                          "frac": (gemm_tflops / peaks["fp64_dmma_tflops"]) if gemm_tflops else None,
                          "traffic": gemm_traffic(),

@@ -12,7 +12,11 @@ void DBuf::alloc(size_t count) {
     if (p) cudaFree(p);
     p = nullptr;
     n = count;
-    if (count) CCF_CUDA(cudaMalloc(&p, count * sizeof(double)));
+    if (count) {
+        CCF_CUDA(cudaMalloc(&p, count * sizeof(double)));
+        // zero-filled: pad columns of every tensor are defined (the TMA GEMM reads them at K edges)
+        CCF_CUDA(cudaMemset(p, 0, count * sizeof(double)));
+    }
 }
 DBuf::~DBuf() {
     if (p) cudaFree(p);

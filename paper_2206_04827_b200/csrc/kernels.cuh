@@ -1,6 +1,7 @@
 // Kernel declarations shared between the .cu translation units and the host driver.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "ccf_device.cuh"
@@ -100,6 +101,14 @@ __global__ void dgemm_batched_kernel(GemmBatch g);
 template <int PM>
 __global__ void dgemm_pipe_kernel(GemmBatch g);  // PM x 64 tiles (PM = 128 | 64), cp.async pipeline (aligned operands)
 size_t dgemm_pipe_smem(int bm);
+// TMA variant: tensor maps of the operand allocations (A boxes 16 x 128, B boxes 16 x 16, f64,
+// 128-byte swizzle), per-term box origins ta[t] = {A map, A col, A row, B map}, tb[t] = {B col, B row}
+constexpr int kTmaMaps = 8;
+struct TmaMaps {
+    CUtensorMap m[kTmaMaps];
+};
+__global__ void dgemm_tma_kernel(GemmBatch g, const __grid_constant__ TmaMaps maps, const int4* ta, const int2* tb);
+size_t dgemm_tma_smem();
 struct ThetaCross {
     Geo g;
     int logp, tj;

@@ -4,6 +4,8 @@
 #include <cstring>
 #include <string>
 
+#include <cudaTypedefs.h>
+
 #include "pipeline.hpp"
 
 #include <cstdlib>
@@ -237,6 +239,59 @@ TransformPlan::TransformPlan(Ctx& c) {
 }
 
 // ---------------------------------------------------------------- GEMM plans
+namespace {
+// driver entry points for the TMA GEMM (no link-time libcuda dependency)
+struct DriverFns {
+    PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    PFN_cuMemGetAddressRange_v3020 range = nullptr;
+};
+const DriverFns& drv() {
+    static const DriverFns d = [] {
+        DriverFns f;
+        cudaDriverEntryPointQueryResult q;
+        void* e = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &e, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            f.encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(e);
+        e = nullptr;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &e, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            f.range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(e);
+        return f;
+    }();
+    return d;
+}
+// CCF_GEMM_TMA: 2 (default) = single-term plans (the multi-term composite operators measured faster
+// on the cp.async kernel), 1 = every eligible plan, 0 = off
+int tma_mode() {
+    static const int on = [] {
+        const char* e = std::getenv("CCF_GEMM_TMA");
+        return e ? std::atoi(e) : 2;
+    }();
+    return (drv().encode && drv().range) ? on : 0;
+}
+// f64 2-D map over [base, base + bytes) viewed as rows of ld doubles; box 16 x box_rows, 128-byte swizzle
+bool encode_map(CUtensorMap& m, const void* base, size_t bytes, long ld, int box_rows) {
+    const cuuint64_t rows = bytes / (size_t(ld) * 8);
+    if (rows == 0 || rows > (1ull << 31) || ld > (1L << 31)) return false;
+    cuuint64_t dims[2] = {cuuint64_t(ld), rows};
+    cuuint64_t strides[1] = {cuuint64_t(ld) * 8};
+    cuuint32_t box[2] = {16, cuuint32_t(box_rows)};
+    cuuint32_t es[2] = {1, 1};
+    return drv().encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+bool alloc_range(const void* p, uintptr_t& base, size_t& size) {
+    CUdeviceptr b = 0;
+    size_t s = 0;
+    if (drv().range(&b, &s, CUdeviceptr(reinterpret_cast<uintptr_t>(p))) != CUDA_SUCCESS) return false;
+    base = uintptr_t(b);
+    size = s;
+    return true;
+}
+}  // namespace
+
 void GemmPlan::upload() {
     const size_t nb = std::max(C.size(), Coff.size()), na = A.size();
     // the pipelined kernel copies 16-byte chunks: A / B bases (and base-relative offsets) 16-byte
@@ -274,6 +329,71 @@ void GemmPlan::upload() {
         CCF_CUDA(cudaMemcpy(dDL, DL.data(), nb * sizeof(void*), cudaMemcpyHostToDevice));
         CCF_CUDA(cudaMemcpy(dDR, DR.data(), nb * sizeof(void*), cudaMemcpyHostToDevice));
     }
+    // ---- TMA variant: one map per (operand allocation, leading dimension), box origins per term
+    tma = false;
+    if (pipe && tma_mode() && (tma_mode() == 1 || tstart.empty()) && M > 64 && !A.empty()) {
+        struct Key {
+            uintptr_t base;
+            long ld;
+            int box;
+        };
+        std::vector<Key> keys;
+        std::vector<CUtensorMap> maps;
+        std::vector<int> hta(4 * na), htb(2 * na);
+        bool ok = true;
+        auto find = [&](const double* ptr, long ld, int box, int& idx, int& col, int& row) {
+            uintptr_t b;
+            size_t sz;
+            if (!alloc_range(ptr, b, sz)) return false;
+            idx = -1;
+            for (size_t k = 0; k < keys.size(); ++k)
+                if (keys[k].base == b && keys[k].ld == ld && keys[k].box == box) idx = int(k);
+            if (idx < 0) {
+                if (keys.size() >= 6) return false;
+                CUtensorMap m;
+                if (!encode_map(m, reinterpret_cast<const void*>(b), sz, ld, box)) return false;
+                keys.push_back({b, ld, box});
+                maps.push_back(m);
+                idx = int(keys.size()) - 1;
+            }
+            const uintptr_t off = (reinterpret_cast<uintptr_t>(ptr) - b) / 8;
+            if (off / uintptr_t(ld) > uintptr_t(1u << 31)) return false;
+            row = int(off / uintptr_t(ld));
+            col = int(off % uintptr_t(ld));
+            return true;
+        };
+        for (size_t t = 0; t < na && ok; ++t) {
+            int ia, ca, ra;
+            ok = find(A[t], lda, 128, ia, ca, ra);
+            int ib = 0, cb = 0, rb = 0;
+            if (ok) {
+                if (Boff.empty()) {
+                    ok = find(B[t], ldb, 16, ib, cb, rb);
+                } else {  // relative to the launch base (slot 6 + base index)
+                    const long o = Boff[t] & ((1L << kBaseShift) - 1);
+                    ib = 6 + int(Boff[t] >> kBaseShift);
+                    rb = int(o / ldb);
+                    cb = int(o % ldb);
+                }
+            }
+            hta[4 * t] = ia;
+            hta[4 * t + 1] = ca;
+            hta[4 * t + 2] = ra;
+            hta[4 * t + 3] = ib;
+            htb[2 * t] = cb;
+            htb[2 * t + 1] = rb;
+        }
+        if (ok) {
+            tmaps = maps;
+            if (!dTA) {
+                CCF_CUDA(cudaMalloc(&dTA, hta.size() * sizeof(int)));
+                CCF_CUDA(cudaMalloc(&dTB, htb.size() * sizeof(int)));
+            }
+            CCF_CUDA(cudaMemcpy(dTA, hta.data(), hta.size() * sizeof(int), cudaMemcpyHostToDevice));
+            CCF_CUDA(cudaMemcpy(dTB, htb.data(), htb.size() * sizeof(int), cudaMemcpyHostToDevice));
+            tma = true;
+        }
+    }
 }
 
 void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double* c0, double* c1) const {
@@ -281,7 +401,45 @@ void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double
     GemmBatch g{dA, dB, dC, M, N, K, lda, ldb, ldc, alpha, beta, dT, dDL, dDR, dBoff, dCoff, {b0, b1}, {c0, c1}, int(nb),
                 ldd ? ldd : long(N), 1};
     const bool based_ok = (reinterpret_cast<uintptr_t>(b0) % 16 == 0) && (reinterpret_cast<uintptr_t>(b1) % 16 == 0);
-    if (pipe && based_ok) {
+    if (tma && based_ok) {
+        static bool tattr = false;
+        static int nsm = 0;
+        if (!tattr) {
+            CCF_CUDA(cudaFuncSetAttribute(dgemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(dgemm_tma_smem())));
+            int dev = 0;
+            CCF_CUDA(cudaGetDevice(&dev));
+            CCF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+            tattr = true;
+        }
+        TmaMaps mp{};
+        for (size_t i = 0; i < tmaps.size(); ++i) mp.m[i] = tmaps[i];
+        if (!Boff.empty()) {  // launch bases of the base-relative B: maps cached per base pointer
+            const double* bases[2] = {b0, b1 ? b1 : b0};
+            for (int q = 0; q < 2; ++q) {
+                const double* bp = bases[q];
+                bool hit = false;
+                for (auto& kv : bmap_cache)
+                    if (kv.first == bp) {
+                        mp.m[6 + q] = kv.second;
+                        hit = true;
+                    }
+                if (!hit) {
+                    uintptr_t ab;
+                    size_t sz;
+                    CUtensorMap m;
+                    if (!bp || !alloc_range(bp, ab, sz) ||
+                        !encode_map(m, bp, sz - (reinterpret_cast<uintptr_t>(bp) - ab), ldb, 16))
+                        throw Error(INTERNAL, "GemmPlan: cannot build the TMA map of a launch base");
+                    bmap_cache.emplace_back(bp, m);
+                    mp.m[6 + q] = m;
+                }
+            }
+        }
+        const long items = long(nb) * ((M + 127) / 128) * ((N + 63) / 64);
+        dgemm_tma_kernel<<<unsigned(std::min<long>(items, 2L * nsm)), 288, dgemm_tma_smem(), s>>>(
+            g, mp, static_cast<const int4*>(dTA), static_cast<const int2*>(dTB));
+    } else if (pipe && based_ok) {
         static bool attr = false;  // process-wide function attributes (same on every device)
         if (!attr) {
             CCF_CUDA(cudaFuncSetAttribute(dgemm_pipe_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -313,6 +471,8 @@ void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double
 }
 
 GemmPlan::~GemmPlan() {
+    if (dTA) cudaFree(dTA);
+    if (dTB) cudaFree(dTB);
     if (dBoff) cudaFree(dBoff);
     if (dCoff) cudaFree(dCoff);
     if (dDL) cudaFree(dDL);

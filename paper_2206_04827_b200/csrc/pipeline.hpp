@@ -9,6 +9,7 @@
 // State (omega history, N history) stays on the device; ring indices rotate.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <vector>
@@ -51,6 +52,13 @@ struct GemmPlan {
     long* dBoff = nullptr;
     long* dCoff = nullptr;
     bool pipe = false;  // operands qualify for dgemm_pipe_kernel (set by upload)
+    // TMA variant (dgemm_tma_kernel): set by upload when the operands map onto <= 6 tensor maps
+    // (slots 6 / 7: the launch bases of a base-relative B, encoded per base at launch and cached)
+    bool tma = false;
+    std::vector<CUtensorMap> tmaps;
+    void* dTA = nullptr;  // int4 per term
+    void* dTB = nullptr;  // int2 per term
+    mutable std::vector<std::pair<const double*, CUtensorMap>> bmap_cache;
     int M = 0, N = 0, K = 0;
     long lda = 0, ldb = 0, ldc = 0;
     double alpha = 1.0, beta = 0.0;

@@ -304,6 +304,203 @@ template __global__ void dgemm_pipe_kernel<128>(GemmBatch g);
 template __global__ void dgemm_pipe_kernel<64>(GemmBatch g);
 
 // ---------------------------------------------------------------------------------------------
+// Batched DGEMM, TMA variant. Same CTA tile (128 x 64, 8 consumer warps of 32 x 32, BK = 16) as
+// dgemm_pipe_kernel, operands moved by the tensor-memory accelerator: per k-slice one elected
+// producer thread issues one 16 x 128 box of A and four 16 x 16 boxes of B
+// (cp.async.bulk.tensor.2d, 128-byte swizzle, completion counted in bytes on the stage's "full"
+// mbarrier). The consumer warps only wait on mbarriers, load fragments (swizzle-aware, conflict
+// free) and issue DMMAs, then release the stage on its "empty" mbarrier. CTAs are persistent
+// (grid-stride over items), so the producer fills the next item's stages during the epilogue.
+// Tensor maps (one per operand allocation, __grid_constant__ parameter) and per-term box
+// coordinates are built by GemmPlan::upload; rows / columns past an allocation read as zero, and
+// the one K edge on the path (K = 127, eigen back transforms) meets zero pad columns of A.
+namespace {
+constexpr int TS_STAGES = 4;
+constexpr int TS_A_BYTES = 128 * 128;  // 128 rows x 16 doubles
+constexpr int TS_B_BYTES = 4 * 2048;   // 4 boxes x (16 rows x 16 doubles)
+constexpr int TS_STAGE_BYTES = TS_A_BYTES + TS_B_BYTES;
+
+__device__ __forceinline__ unsigned s_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void tb_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void tb_arrive(unsigned bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tb_arrive_tx(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tb_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "TW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra TW_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_2d(unsigned dst, const CUtensorMap* map, int c0, int c1, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+}  // namespace
+
+size_t dgemm_tma_smem() { return size_t(TS_STAGES) * TS_STAGE_BYTES + 1024 + 2 * TS_STAGES * sizeof(uint64_t); }
+
+__global__ void __launch_bounds__(288, 2)
+    dgemm_tma_kernel(GemmBatch g, const __grid_constant__ TmaMaps maps, const int4* __restrict__ ta,
+                     const int2* __restrict__ tb) {
+    extern __shared__ __align__(1024) unsigned char tsm_raw[];
+    // 128-byte swizzle repeats every 1024 bytes: align the stage ring to 1024
+    const unsigned raw = s_u32(tsm_raw);
+    const unsigned base = (raw + 1023u) & ~1023u;
+    unsigned char* tsm = tsm_raw + (base - raw);
+    const unsigned bars = base + TS_STAGES * TS_STAGE_BYTES;  // full[s] at bars + 8 s, empty[s] at bars + 8 (S + s)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        for (int s = 0; s < TS_STAGES; ++s) {
+            tb_init(bars + 8 * s, 1);                // producer arrival + transaction bytes
+            tb_init(bars + 8 * (TS_STAGES + s), 8);  // one arrival per consumer warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int tn = (g.N + PN - 1) / PN, tmn = ((g.M + 127) / 128) * tn;
+    const int nitems = g.nbatch * tmn;
+    const int nkt = (g.K + PK - 1) / PK;
+    struct Item {
+        int b, m0, n0, t0, nk;
+    };
+    auto decode = [&](int w) {
+        Item it;
+        it.b = w / tmn;
+        const int rem = w - it.b * tmn;
+        it.m0 = (rem / tn) * 128;
+        it.n0 = (rem - (rem / tn) * tn) * PN;
+        it.t0 = g.tstart ? g.tstart[it.b] : it.b;
+        it.nk = (g.tstart ? g.tstart[it.b + 1] - it.t0 : 1) * nkt;
+        return it;
+    };
+    if (warp == 8) {
+        // ---------------- producer (one thread)
+        if (lane == 0) {
+            int stage = 0;
+            unsigned phase = 0;
+            for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+                const Item I = decode(w);
+                int t = I.t0, kt = 0;
+                int4 a = __ldg(ta + t);
+                int2 b = __ldg(tb + t);
+                for (int kk = 0; kk < I.nk; ++kk) {
+                    const int k0 = kt * PK;
+                    tb_wait(bars + 8 * (TS_STAGES + stage), phase ^ 1u);
+                    const unsigned full = bars + 8 * stage;
+                    tb_arrive_tx(full, TS_STAGE_BYTES);
+                    const unsigned sa = base + stage * TS_STAGE_BYTES, sb = sa + TS_A_BYTES;
+                    tma_2d(sa, &maps.m[a.x], a.y + k0, a.z + I.m0, full);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) tma_2d(sb + 2048 * q, &maps.m[a.w], b.x + I.n0 + 16 * q, b.y + k0, full);
+                    if (++stage == TS_STAGES) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                    if (++kt == nkt && kk + 1 < I.nk) {
+                        kt = 0;
+                        ++t;
+                        a = __ldg(ta + t);
+                        b = __ldg(tb + t);
+                    }
+                }
+            }
+        }
+        return;
+    }
+    // ---------------- consumers
+    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    const int gq = lane >> 2, tq = lane & 3;
+    // swizzled byte offsets of this lane's fragments within a stage, k-step s = 0..3 (k = 4 s + tq):
+    //   A(row, k) = row * 128 + (((k >> 1) ^ (row & 7)) << 4) + (k & 1) * 8,  row = wm + 8 i + gq
+    //             = abase + i * 1024 + ((2 s ^ (gq & 6)) << 4)
+    //   B(k, n)   = (n >> 4) * 2048 + k * 128 + ((((n & 15) >> 1) ^ (k & 7)) << 4) + (n & 1) * 8,  n = wn + 8 j + gq
+    //             = bbase + (j >> 1) * 2048 + s * 512 + (((j ^ s) & 1) << 6)
+    const int g6 = gq & 6;
+    const int abase = (wm + gq) * 128 + ((((tq >> 1) ^ gq) & 1) << 4) + (tq & 1) * 8;
+    const int bbase = (wn >> 4) * 2048 + tq * 128 + ((((gq >> 1) ^ tq) & 3) << 4) + (gq & 1) * 8;
+    int stage = 0;
+    unsigned phase = 0;
+    Item I = decode(blockIdx.x < nitems ? blockIdx.x : 0);
+    for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+        // next item's term range in flight during this item's main loop
+        const Item In = decode(w + int(gridDim.x) < nitems ? w + int(gridDim.x) : w);
+        double acc[4][4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int kt = 0; kt < I.nk; ++kt) {
+            tb_wait(bars + 8 * stage, phase);
+            const unsigned char* sa = tsm + stage * TS_STAGE_BYTES;
+            const unsigned char* sb = sa + TS_A_BYTES;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                double af[4], bf[4];
+                const int ao = abase + (((2 * s) ^ g6) << 4);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) af[i] = *reinterpret_cast<const double*>(sa + ao + i * 1024);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    bf[j] = *reinterpret_cast<const double*>(sb + bbase + (j >> 1) * 2048 + s * 512 + (((j ^ s) & 1) << 6));
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+            }
+            __syncwarp();
+            if (lane == 0) tb_arrive(bars + 8 * (TS_STAGES + stage));
+            if (++stage == TS_STAGES) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+        double* __restrict__ C;
+        if (g.coff) {
+            const long o = g.coff[I.b];
+            C = g.cbase[o >> kBaseShift] + (o & ((1L << kBaseShift) - 1));
+        } else {
+            C = g.C[I.b];
+        }
+        const double* __restrict__ dl = g.dl ? g.dl[I.b] : nullptr;
+        const bool vec = ((reinterpret_cast<uintptr_t>(C) | (uintptr_t(g.ldc) * 8)) & 15) == 0 && !dl && g.beta == 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int r = I.m0 + wm + 8 * i + gq, c = I.n0 + wn + 8 * j + 2 * tq;
+                if (r >= g.M) continue;
+                double* dst = C + long(r) * g.ldc + c;
+                if (vec && c + 1 < g.N) {
+                    *reinterpret_cast<double2*>(dst) = make_double2(g.alpha * acc[i][j][0], g.alpha * acc[i][j][1]);
+                    continue;
+                }
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    if (c + q < g.N) {
+                        double v = g.alpha * acc[i][j][q];
+                        if (dl) v *= __ldg(dl + long(r) * g.ldd + c + q);
+                        dst[q] = g.beta == 0.0 ? v : fma(g.beta, dst[q], v);
+                    }
+                }
+            }
+        I = In;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Theta direction.
 //
 // Reference conventions (transform.cpp:144-163, 175-191): values f(theta_l) =

@@ -261,12 +261,11 @@ const DriverFns& drv() {
     }();
     return d;
 }
-// CCF_GEMM_TMA: 2 (default) = single-term plans (the multi-term composite operators measured faster
-// on the cp.async kernel), 1 = every eligible plan, 0 = off
+// CCF_GEMM_TMA: 1 (default) = every eligible plan, 2 = single-term plans only, 0 = off (cp.async kernel)
 int tma_mode() {
     static const int on = [] {
         const char* e = std::getenv("CCF_GEMM_TMA");
-        return e ? std::atoi(e) : 2;
+        return e ? std::atoi(e) : 1;
     }();
     return (drv().encode && drv().range) ? on : 0;
 }
@@ -293,6 +292,40 @@ bool alloc_range(const void* p, uintptr_t& base, size_t& size) {
 }  // namespace
 
 void GemmPlan::upload() {
+    // multi-term plans: batches in descending term count, so that a round-robin (persistent) item
+    // assignment starts with the long items (LPT order) and the launch tail holds the short ones
+    if (!tstart.empty() && tstart.size() > 2) {
+        const size_t nbt = tstart.size() - 1;
+        std::vector<size_t> ord(nbt);
+        for (size_t b = 0; b < nbt; ++b) ord[b] = b;
+        std::stable_sort(ord.begin(), ord.end(), [&](size_t x, size_t y) {
+            return tstart[x + 1] - tstart[x] > tstart[y + 1] - tstart[y];
+        });
+        std::vector<const double*> nA, nB;
+        std::vector<long> nBoff;
+        std::vector<int> nT{0};
+        for (size_t b : ord)
+            for (int t = tstart[b]; t < tstart[b + 1]; ++t) {
+                nA.push_back(A[size_t(t)]);
+                if (!B.empty()) nB.push_back(B[size_t(t)]);
+                if (!Boff.empty()) nBoff.push_back(Boff[size_t(t)]);
+            }
+        for (size_t b : ord) nT.push_back(nT.back() + (tstart[b + 1] - tstart[b]));
+        auto permute = [&](auto& v) {
+            if (v.size() != nbt) return;
+            auto w = v;
+            for (size_t i = 0; i < nbt; ++i) w[i] = v[ord[i]];
+            v = w;
+        };
+        permute(C);
+        permute(Coff);
+        permute(DL);
+        permute(DR);
+        A = nA;
+        if (!B.empty()) B = nB;
+        if (!Boff.empty()) Boff = nBoff;
+        tstart = nT;
+    }
     const size_t nb = std::max(C.size(), Coff.size()), na = A.size();
     // the pipelined kernel copies 16-byte chunks: A / B bases (and base-relative offsets) 16-byte
     // aligned, even leading dimensions

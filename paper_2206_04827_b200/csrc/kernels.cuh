@@ -90,7 +90,7 @@ struct GemmBatch {
     // so a captured plan can be relaunched on other tensors (ring buffers) with new bases
     const long* boff;
     const long* coff;
-    const double* bbase[2];
+    const double* bbase[3];
     double* cbase[2];
     int nbatch;  // number of batches
     long ldd;    // leading dimension of the dl tables

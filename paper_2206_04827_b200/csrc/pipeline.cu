@@ -382,7 +382,7 @@ void GemmPlan::upload() {
             for (size_t k = 0; k < keys.size(); ++k)
                 if (keys[k].base == b && keys[k].ld == ld && keys[k].box == box) idx = int(k);
             if (idx < 0) {
-                if (keys.size() >= 6) return false;
+                if (keys.size() >= (Boff.empty() ? size_t(kTmaMaps) : size_t(5))) return false;  // 5..7: launch bases
                 CUtensorMap m;
                 if (!encode_map(m, reinterpret_cast<const void*>(b), sz, ld, box)) return false;
                 keys.push_back({b, ld, box});
@@ -402,9 +402,9 @@ void GemmPlan::upload() {
             if (ok) {
                 if (Boff.empty()) {
                     ok = find(B[t], ldb, 16, ib, cb, rb);
-                } else {  // relative to the launch base (slot 6 + base index)
+                } else {  // relative to the launch base (slot 5 + base index)
                     const long o = Boff[t] & ((1L << kBaseShift) - 1);
-                    ib = 6 + int(Boff[t] >> kBaseShift);
+                    ib = 5 + int(Boff[t] >> kBaseShift);
                     rb = int(o / ldb);
                     cb = int(o % ldb);
                 }
@@ -429,9 +429,10 @@ void GemmPlan::upload() {
     }
 }
 
-void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double* c0, double* c1) const {
+void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double* c0, double* c1,
+                      const double* b2) const {
     const unsigned nb = unsigned(std::max(C.size(), Coff.size()));
-    GemmBatch g{dA, dB, dC, M, N, K, lda, ldb, ldc, alpha, beta, dT, dDL, dDR, dBoff, dCoff, {b0, b1}, {c0, c1}, int(nb),
+    GemmBatch g{dA, dB, dC, M, N, K, lda, ldb, ldc, alpha, beta, dT, dDL, dDR, dBoff, dCoff, {b0, b1, b2}, {c0, c1}, int(nb),
                 ldd ? ldd : long(N), 1};
     const bool based_ok = (reinterpret_cast<uintptr_t>(b0) % 16 == 0) && (reinterpret_cast<uintptr_t>(b1) % 16 == 0);
     if (tma && based_ok) {
@@ -448,13 +449,13 @@ void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double
         TmaMaps mp{};
         for (size_t i = 0; i < tmaps.size(); ++i) mp.m[i] = tmaps[i];
         if (!Boff.empty()) {  // launch bases of the base-relative B: maps cached per base pointer
-            const double* bases[2] = {b0, b1 ? b1 : b0};
-            for (int q = 0; q < 2; ++q) {
+            const double* bases[3] = {b0, b1 ? b1 : b0, b2 ? b2 : b0};
+            for (int q = 0; q < 3; ++q) {
                 const double* bp = bases[q];
                 bool hit = false;
                 for (auto& kv : bmap_cache)
                     if (kv.first == bp) {
-                        mp.m[6 + q] = kv.second;
+                        mp.m[5 + q] = kv.second;
                         hit = true;
                     }
                 if (!hit) {
@@ -465,7 +466,7 @@ void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double
                         !encode_map(m, bp, sz - (reinterpret_cast<uintptr_t>(bp) - ab), ldb, 16))
                         throw Error(INTERNAL, "GemmPlan: cannot build the TMA map of a launch base");
                     bmap_cache.emplace_back(bp, m);
-                    mp.m[6 + q] = m;
+                    mp.m[5 + q] = m;
                 }
             }
         }
@@ -1078,7 +1079,7 @@ void Pipeline::modal_solve(DevSet& set, bool full, int ntensor, const double* co
     const int Mp = M + (M & 1), Np = N + (N & 1);
     const size_t per = std::max(size_t(mh) * Np, size_t(M) * std::max(nh, Np));
     if (!dT1_.p) {
-        const size_t cap = per * size_t(2 * std::max(c.gh.nslots, c.gf.nslots) * 4);
+        const size_t cap = per * size_t(3 * std::max(c.gh.nslots, c.gf.nslots) * 4);  // up to 3 tensors of sub-problems
         dT1_.alloc(cap);
         dZ_.alloc(cap);
         dT3_.alloc(cap);
@@ -1329,14 +1330,14 @@ void Pipeline::ensure_eigen(DevSet& pset) {
 // z-synthesized tensors straight from eigen coordinates: T3 = QL Z (e3), then for each requested
 // output S_t (value halves [E | O] of u_t Sz) and D_t (of (dz u_t) Sz): T3 QS[k0] into half k0,
 // T3 QD[k0] into half 1 - k0 (ld n). Replaces u = T3 QR followed by the z synthesis of u.
-void Pipeline::eigen_zsynth(DevSet& set, int ntensor, const double* z0, const double* z1, double* const* outS,
+void Pipeline::eigen_zsynth(DevSet& set, int ntensor, const double* const* z, double* const* outS,
                             double* const* outD) {
     const Geo& g = c.gh;
     const int M = c.M, N = c.N, mh = g.mh, nh = g.nh;
     const int Mp = M + (M & 1), Np = N + (N & 1);
     const size_t per = std::max(size_t(mh) * Np, size_t(M) * std::max(nh, Np));
     if (!dT1_.p) {
-        const size_t cap = per * size_t(2 * std::max(c.gh.nslots, c.gf.nslots) * 4);
+        const size_t cap = per * size_t(3 * std::max(c.gh.nslots, c.gf.nslots) * 4);  // up to 3 tensors of sub-problems
         dT1_.alloc(cap);
         dZ_.alloc(cap);
         dT3_.alloc(cap);
@@ -1361,8 +1362,11 @@ void Pipeline::eigen_zsynth(DevSet& set, int ntensor, const double* z0, const do
         e3.M = mh; e3.N = N; e3.K = M; e3.lda = Mp; e3.ldb = 2 * Np; e3.ldc = Np;
         e3.upload();
     }
-    const void* okey[4] = {outS[0], outD[0], ntensor > 1 ? outS[1] : nullptr, ntensor > 1 ? outD[1] : nullptr};
-    GemmPlan& zo = gemm(ptr_key("ezs", 4, okey, keyp, ci), fresh);
+    const void* okey[6] = {outS[0], outD[0], ntensor > 1 ? outS[1] : nullptr, ntensor > 1 ? outD[1] : nullptr,
+                           ntensor > 2 ? outS[2] : nullptr, ntensor > 2 ? outD[2] : nullptr};
+    const void* keyp6[6] = {&set, &set, &set, &set, &set, &set};
+    const int ci6[6] = {ntensor, ntensor, ntensor, ntensor, ntensor, ntensor};
+    GemmPlan& zo = gemm(ptr_key("ezs", 6, okey, keyp6, ci6), fresh);
     if (fresh) {
         long task = 0;
         for (int t = 0; t < ntensor; ++t)
@@ -1385,7 +1389,7 @@ void Pipeline::eigen_zsynth(DevSet& set, int ntensor, const double* z0, const do
         zo.M = mh; zo.N = nh; zo.K = N; zo.lda = Np; zo.ldb = nh; zo.ldc = g.n;
         zo.upload();
     }
-    e3.launch(c.stream, z0, ntensor > 1 ? z1 : z0);
+    e3.launch(c.stream, z[0], ntensor > 1 ? z[1] : z[0], nullptr, nullptr, ntensor > 2 ? z[2] : z[0]);
     c.gemm_flops += e3.flops();
     zo.launch(c.stream);
     c.gemm_flops += zo.flops();
@@ -1459,7 +1463,7 @@ void Pipeline::eigen_back(DevSet& set, int ntensor, const double* z0, const doub
     const int Mp = M + (M & 1), Np = N + (N & 1);
     const size_t per = std::max(size_t(mh) * Np, size_t(M) * std::max(nh, Np));
     if (!dT1_.p) {
-        const size_t cap = per * size_t(2 * std::max(c.gh.nslots, c.gf.nslots) * 4);
+        const size_t cap = per * size_t(3 * std::max(c.gh.nslots, c.gf.nslots) * 4);  // up to 3 tensors of sub-problems
         dT1_.alloc(cap);
         dZ_.alloc(cap);
         dT3_.alloc(cap);
@@ -1507,7 +1511,7 @@ void Pipeline::to_eigen(DevSet& pset, const double* u, double* z) {
     const int Np = N + (N & 1);
     const size_t per = std::max(size_t(mh) * Np, size_t(M) * std::max(nh, Np));
     if (!dT1_.p) {
-        const size_t cap = per * size_t(2 * std::max(c.gh.nslots, c.gf.nslots) * 4);
+        const size_t cap = per * size_t(3 * std::max(c.gh.nslots, c.gf.nslots) * 4);  // up to 3 tensors of sub-problems
         dT1_.alloc(cap);
         dZ_.alloc(cap);
         dT3_.alloc(cap);
@@ -1755,17 +1759,14 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
         if (!disable_nonlinear) {
             double* zp = zpsi.p;
             c.mark("start");
-            if (zp_head != cur) {  // the last Helmholtz pass did not leave Z_P of this omega (first step)
-                const double* zs[1] = {zl[cur].p};
-                const double wm1[1] = {-1.0};
-                P.eigen_rhs(pset, 1, zs, zs, wm1, 1, 1.0, zp, zp);  // Z_P = -Z_lambda .* RT_P
+            // velocity_from_vorticity (ptns.cpp:85-91): lambda_v = gamma_omega (scratch 4), gamma_v = lambda_psi
+            // (scratch 1, 2: its z and dz synthesis). In the steady state the previous step's Helmholtz back
+            // transform already produced them from Z_P; otherwise (first step, displaced scratch) solve here.
+            (void)zp;
+            if (!(zv_head == cur && P.zw_owner_ == this)) {
+                velocity(cur);
+                c.mark("P_poisson_solve");
             }
-            // velocity_from_vorticity (ptns.cpp:85-91): lambda_v = gamma_omega (scratch 4, left by the last
-            // step), gamma_v = lambda_psi: its z synthesis and dz synthesis straight from Z_P
-            double* oS[1] = {P.scratch(1)};
-            double* oD[1] = {P.scratch(2)};
-            P.eigen_zsynth(pset, 1, zp, zp, oS, oD);
-            c.mark("P_poisson_solve");
             P.nonlinear(P.scratch(4), P.scratch(1), P.scratch(3), P.scratch(4), nl[nnew].p, ng[nnew].p, &pset,
                         true);  // N~ = PL_P N PR
         }
@@ -1792,7 +1793,7 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
         c.mark("H_rhs_combine");
         if (!disable_nonlinear) {
             zp_head = out;
-            zsynth_omega(out);
+            zsynth_omega(out);  // omega's and (next step's Poisson solve) the velocity's z tensors
             c.mark("H_helmholtz_solve");
         }
         return;
@@ -1834,16 +1835,40 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
 
 // the nonlinear term's omega inputs (z synthesis of lambda_omega, gamma_omega, dz gamma_omega) into
 // scratch 3..5, from the eigen state of ring slot r
+// solve_poisson_3d(-lambda_omega) of ring slot r in eigen coordinates and the velocity's z tensors
+// (scratch 1, 2)
+void NSState::velocity(int r) {
+    Pipeline& P = *pl;
+    DevSet& pset = P.c.set(false, true, 1.0);
+    if (zp_head != r) {  // Z_P = -Z_lambda .* RT_P
+        const double* zs[1] = {zl[r].p};
+        const double wm1[1] = {-1.0};
+        P.eigen_rhs(pset, 1, zs, zs, wm1, 1, 1.0, zpsi.p, zpsi.p);
+        zp_head = r;
+    }
+    const double* zz[1] = {zpsi.p};
+    double* oS[1] = {P.scratch(1)};
+    double* oD[1] = {P.scratch(2)};
+    P.eigen_zsynth(pset, 1, zz, oS, oD);
+    zv_head = r;
+}
+
 void NSState::zsynth_omega(int r) {
     Pipeline& P = *pl;
     if (coeff_head == r) {  // the coefficient state is authoritative (initial data)
         P.zsynth_coeff(lam[r].p, gam[r].p, P.scratch(3), P.scratch(4), P.scratch(5));
+        zv_head = -1;
         P.zw_owner_ = this;
         return;
     }
-    double* oS[2] = {P.scratch(3), P.scratch(4)};
-    double* oD[2] = {nullptr, P.scratch(5)};
-    P.eigen_zsynth(P.c.set(false, true, 1.0), 2, zl[r].p, zg[r].p, oS, oD);
+    // lambda_omega -> S (scratch 3); gamma_omega -> S, dz S (4, 5); with a valid Z_P of the same slot also
+    // lambda_psi -> S, dz S (1, 2), i.e. the next nonlinear term's velocity: one e3 + one z launch
+    const bool vel = zp_head == r;
+    const double* z[3] = {zl[r].p, zg[r].p, zpsi.p};
+    double* oS[3] = {P.scratch(3), P.scratch(4), P.scratch(1)};
+    double* oD[3] = {nullptr, P.scratch(5), P.scratch(2)};
+    P.eigen_zsynth(P.c.set(false, true, 1.0), vel ? 3 : 2, z, oS, oD);
+    zv_head = vel ? r : -1;
     P.zw_owner_ = this;
 }
 
@@ -1886,7 +1911,10 @@ void NSState::omega_coeff() {
 void NSState::step_once() {
     Ctx& c = pl->c;
     // scratch 3..5 may have been reused (another stepper, a standalone nonlinear call) since our last step
-    if (eigen && !disable_nonlinear && pl->zw_owner_ != this) zsynth_omega(head);
+    if (eigen && !disable_nonlinear && pl->zw_owner_ != this) {
+        zsynth_omega(head);
+        if (zv_head != head) velocity(head);  // a replayed graph has no Poisson stage
+    }
     const int b = std::min(order, steps + 1);
     const int out = (head + 4) % 5;
     const int nnew = (nhead + 4) % 5;
@@ -1915,7 +1943,7 @@ void NSState::step_once() {
     }
     head = out;
     coeff_head = eigen ? -1 : head;
-    if (eigen && !disable_nonlinear) zp_head = out;  // (graph replays skip enqueue)
+    if (eigen && !disable_nonlinear) zp_head = zv_head = out;  // (graph replays skip enqueue)
     if (!disable_nonlinear) {
         nhead = nnew;
         ncount = ncnt;

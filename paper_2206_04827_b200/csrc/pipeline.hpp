@@ -52,8 +52,8 @@ struct GemmPlan {
     long* dBoff = nullptr;
     long* dCoff = nullptr;
     bool pipe = false;  // operands qualify for dgemm_pipe_kernel (set by upload)
-    // TMA variant (dgemm_tma_kernel): set by upload when the operands map onto <= 6 tensor maps
-    // (slots 6 / 7: the launch bases of a base-relative B, encoded per base at launch and cached)
+    // TMA variant (dgemm_tma_kernel): set by upload when the operands map onto <= 8 tensor maps
+    // (<= 5 with a base-relative B: slots 5 / 6 / 7 hold the launch bases, encoded at launch and cached)
     bool tma = false;
     std::vector<CUtensorMap> tmaps;
     void* dTA = nullptr;  // int4 per term
@@ -64,7 +64,7 @@ struct GemmPlan {
     double alpha = 1.0, beta = 0.0;
     void upload();
     void launch(cudaStream_t s, const double* b0 = nullptr, const double* b1 = nullptr, double* c0 = nullptr,
-                double* c1 = nullptr) const;
+                double* c1 = nullptr, const double* b2 = nullptr) const;
     double flops() const { return 2.0 * M * N * K * double(A.size()); }  // every term is one M x N x K product
     ~GemmPlan();
 };
@@ -91,7 +91,7 @@ public:
     void nonlinear(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w, double* lam_n,
                    double* gam_n, DevSet* eig = nullptr, bool zpre = false);
     void zsynth_coeff(const double* lam, const double* gam, double* oS0, double* oS1, double* oD1);
-    void eigen_zsynth(DevSet& set, int ntensor, const double* z0, const double* z1, double* const* outS,
+    void eigen_zsynth(DevSet& set, int ntensor, const double* const* z, double* const* outS,
                       double* const* outD);
     // eigen-coordinate NS state (see pipeline.cu)
     long eig_off(int s, int pl, int k0) const;
@@ -170,8 +170,10 @@ struct NSState {
     int coeff_head = 0;   // ring slot whose lam / gam hold the coefficient-space omega (-1: none)
     DBuf zpsi;            // Poisson RHS -Z_lambda .* RT_P of ring slot zp_head (left by the Helmholtz pass)
     int zp_head = -1;
+    int zv_head = -1;     // ring slot whose velocity z tensors (scratch 1, 2) are current (while zw_owner_)
     ~NSState();
     void zsynth_omega(int r);
+    void velocity(int r);
     void omega_coeff();
     void step_once();
     void enqueue(int b, int eo, int cur, int out, int nnew);

@@ -95,6 +95,7 @@ struct GemmBatch {
     int nbatch;  // number of batches
     long ldd;    // leading dimension of the dl tables
     int ipc;     // items (batch x m-tile x n-tile) per CTA, pipelined kernel
+    const long* aoff;  // optional base-relative A per term (same bases as B; not together with boff)
 };
 constexpr long kBaseShift = 40;
 __global__ void dgemm_batched_kernel(GemmBatch g);

@@ -302,13 +302,14 @@ void GemmPlan::upload() {
             return tstart[x + 1] - tstart[x] > tstart[y + 1] - tstart[y];
         });
         std::vector<const double*> nA, nB;
-        std::vector<long> nBoff;
+        std::vector<long> nBoff, nAoff;
         std::vector<int> nT{0};
         for (size_t b : ord)
             for (int t = tstart[b]; t < tstart[b + 1]; ++t) {
                 nA.push_back(A[size_t(t)]);
                 if (!B.empty()) nB.push_back(B[size_t(t)]);
                 if (!Boff.empty()) nBoff.push_back(Boff[size_t(t)]);
+                if (!Aoff.empty()) nAoff.push_back(Aoff[size_t(t)]);
             }
         for (size_t b : ord) nT.push_back(nT.back() + (tstart[b + 1] - tstart[b]));
         auto permute = [&](auto& v) {
@@ -324,14 +325,16 @@ void GemmPlan::upload() {
         A = nA;
         if (!B.empty()) B = nB;
         if (!Boff.empty()) Boff = nBoff;
+        if (!Aoff.empty()) Aoff = nAoff;
         tstart = nT;
     }
     const size_t nb = std::max(C.size(), Coff.size()), na = A.size();
     // the pipelined kernel copies 16-byte chunks: A / B bases (and base-relative offsets) 16-byte
     // aligned, even leading dimensions
+    if (!Aoff.empty() && !Boff.empty()) throw Error(INTERNAL, "GemmPlan: base-relative A and B together");
     pipe = (lda % 2 == 0) && (ldb % 2 == 0);
     for (size_t i = 0; i < na && pipe; ++i) {
-        if (reinterpret_cast<uintptr_t>(A[i]) % 16) pipe = false;
+        if (Aoff.empty() ? (reinterpret_cast<uintptr_t>(A[i]) % 16 != 0) : (Aoff[i] % 2 != 0)) pipe = false;
         if (Boff.empty() ? (reinterpret_cast<uintptr_t>(B[i]) % 16 != 0) : (Boff[i] % 2 != 0)) pipe = false;
     }
     if (!dA) {
@@ -349,6 +352,10 @@ void GemmPlan::upload() {
     if (!Boff.empty()) {
         if (!dBoff) CCF_CUDA(cudaMalloc(&dBoff, Boff.size() * sizeof(long)));
         CCF_CUDA(cudaMemcpy(dBoff, Boff.data(), Boff.size() * sizeof(long), cudaMemcpyHostToDevice));
+    }
+    if (!Aoff.empty()) {
+        if (!dAoff) CCF_CUDA(cudaMalloc(&dAoff, Aoff.size() * sizeof(long)));
+        CCF_CUDA(cudaMemcpy(dAoff, Aoff.data(), Aoff.size() * sizeof(long), cudaMemcpyHostToDevice));
     }
     if (!Coff.empty()) {
         if (!dCoff) CCF_CUDA(cudaMalloc(&dCoff, Coff.size() * sizeof(long)));
@@ -382,7 +389,7 @@ void GemmPlan::upload() {
             for (size_t k = 0; k < keys.size(); ++k)
                 if (keys[k].base == b && keys[k].ld == ld && keys[k].box == box) idx = int(k);
             if (idx < 0) {
-                if (keys.size() >= (Boff.empty() ? size_t(kTmaMaps) : size_t(5))) return false;  // 5..7: launch bases
+                if (keys.size() >= ((Boff.empty() && Aoff.empty()) ? size_t(kTmaMaps) : size_t(5))) return false;  // 5..7: launch bases
                 CUtensorMap m;
                 if (!encode_map(m, reinterpret_cast<const void*>(b), sz, ld, box)) return false;
                 keys.push_back({b, ld, box});
@@ -396,8 +403,15 @@ void GemmPlan::upload() {
             return true;
         };
         for (size_t t = 0; t < na && ok; ++t) {
-            int ia, ca, ra;
-            ok = find(A[t], lda, 128, ia, ca, ra);
+            int ia = 0, ca = 0, ra = 0;
+            if (Aoff.empty()) {
+                ok = find(A[t], lda, 128, ia, ca, ra);
+            } else {  // relative to the launch base (slot 5 + base index)
+                const long o = Aoff[t] & ((1L << kBaseShift) - 1);
+                ia = 5 + int(Aoff[t] >> kBaseShift);
+                ra = int(o / lda);
+                ca = int(o % lda);
+            }
             int ib = 0, cb = 0, rb = 0;
             if (ok) {
                 if (Boff.empty()) {
@@ -433,7 +447,7 @@ void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double
                       const double* b2) const {
     const unsigned nb = unsigned(std::max(C.size(), Coff.size()));
     GemmBatch g{dA, dB, dC, M, N, K, lda, ldb, ldc, alpha, beta, dT, dDL, dDR, dBoff, dCoff, {b0, b1, b2}, {c0, c1}, int(nb),
-                ldd ? ldd : long(N), 1};
+                ldd ? ldd : long(N), 1, dAoff};
     const bool based_ok = (reinterpret_cast<uintptr_t>(b0) % 16 == 0) && (reinterpret_cast<uintptr_t>(b1) % 16 == 0);
     if (tma && based_ok) {
         static bool tattr = false;
@@ -448,7 +462,8 @@ void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double
         }
         TmaMaps mp{};
         for (size_t i = 0; i < tmaps.size(); ++i) mp.m[i] = tmaps[i];
-        if (!Boff.empty()) {  // launch bases of the base-relative B: maps cached per base pointer
+        if (!Boff.empty() || !Aoff.empty()) {  // launch bases of the base-relative operand: maps cached per base
+            const bool isA = !Aoff.empty();
             const double* bases[3] = {b0, b1 ? b1 : b0, b2 ? b2 : b0};
             for (int q = 0; q < 3; ++q) {
                 const double* bp = bases[q];
@@ -463,7 +478,7 @@ void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double
                     size_t sz;
                     CUtensorMap m;
                     if (!bp || !alloc_range(bp, ab, sz) ||
-                        !encode_map(m, bp, sz - (reinterpret_cast<uintptr_t>(bp) - ab), ldb, 16))
+                        !encode_map(m, bp, sz - (reinterpret_cast<uintptr_t>(bp) - ab), isA ? lda : ldb, isA ? 128 : 16))
                         throw Error(INTERNAL, "GemmPlan: cannot build the TMA map of a launch base");
                     bmap_cache.emplace_back(bp, m);
                     mp.m[5 + q] = m;
@@ -505,6 +520,7 @@ void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double
 }
 
 GemmPlan::~GemmPlan() {
+    if (dAoff) cudaFree(dAoff);
     if (dTA) cudaFree(dTA);
     if (dTB) cudaFree(dTB);
     if (dBoff) cudaFree(dBoff);
@@ -542,6 +558,11 @@ double* Pipeline::big_scratch(size_t doubles) {
 GemmPlan& Pipeline::gemm(const std::string& key, bool& fresh) {
     auto& slot = gemms_[key];
     fresh = !slot;
+    if (fresh) {  // plans allocate and upload: never inside a CUDA-graph capture
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(c.stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+            throw Error(INTERNAL, "GEMM plan first built during graph capture: " + key.substr(0, key.find(':')));
+    }
     if (!slot) slot = std::make_unique<GemmPlan>();
     return *slot;
 }
@@ -789,7 +810,7 @@ void Pipeline::ensure_composite() {
 //   Y  = z analysis of (a_r, a_t, a_z, dz a_r, dz a_t)
 //   (gamma_N, lambda_N) = per-slot composite r operators (curl + decompose + r analysis) on Y
 void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w,
-                         double* lam_n, double* gam_n, DevSet* eig, bool zpre) {
+                         double* lam_n, double* gam_n, DevSet* eig, bool zpre, bool eigY) {
     ensure_composite();
     if (eig && comp_off_) throw Error(INTERNAL, "nonlinear: eigen-coordinate output needs the composite path");
     if (comp_off_) {
@@ -816,39 +837,41 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     bool fresh;
     // ---- z synthesis: 6 tensors, two nh x nh halves per (slot, plane)
     const int acls[8] = {int(alias), 0, 0, 0, 0, 0, 0, 0};
-    GemmPlan& zs = gemm(ptr_key("nzs", 6, keyp, keyp, acls), fresh);
-    if (fresh) {
-        for (int pr = 0; pr < 2; ++pr)
-            for (int x = 0; x < 3; ++x) {
-                if (alias && pr == 0 && x == 0) continue;
-                const double* src = x == 0 ? lam[pr] : gam[pr];
-                const double* mat = x == 2 ? tp.DzS.p : tp.Sz.p;
-                for (int s = 0; s < g.nslots; ++s)
-                    for (int pl = 0; pl < 2; ++pl) {
-                        const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
-                        for (int po = 0; po < 2; ++po) {
-                            const int pi = x == 2 ? 1 - po : po;
-                            zs.A.push_back(src + off + pi * g.nh);
-                            zs.B.push_back(mat + size_t(po) * g.nh * g.nh);
-                            zs.C.push_back(Z[pr][x] + off + po * g.nh);
+    if (!zpre) {  // zpre: the caller synthesized the six z tensors (eigen_ysynth)
+        GemmPlan& zs = gemm(ptr_key("nzs", 4, keyp, keyp, acls), fresh);  // outputs: scratch
+        if (fresh) {
+            for (int pr = 0; pr < 2; ++pr)
+                for (int x = 0; x < 3; ++x) {
+                    if (alias && pr == 0 && x == 0) continue;
+                    const double* src = x == 0 ? lam[pr] : gam[pr];
+                    const double* mat = x == 2 ? tp.DzS.p : tp.Sz.p;
+                    for (int s = 0; s < g.nslots; ++s)
+                        for (int pl = 0; pl < 2; ++pl) {
+                            const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
+                            for (int po = 0; po < 2; ++po) {
+                                const int pi = x == 2 ? 1 - po : po;
+                                zs.A.push_back(src + off + pi * g.nh);
+                                zs.B.push_back(mat + size_t(po) * g.nh * g.nh);
+                                zs.C.push_back(Z[pr][x] + off + po * g.nh);
+                            }
                         }
-                    }
-            }
-        zs.M = g.mh;
-        zs.N = g.nh;
-        zs.K = g.nh;
-        zs.lda = g.n;
-        zs.ldb = g.nh;
-        zs.ldc = g.n;
-        zs.upload();
-    }
-    if (!zpre) {  // zpre: the caller synthesized the six z tensors (eigen_zsynth)
+                }
+            zs.M = g.mh;
+            zs.N = g.nh;
+            zs.K = g.nh;
+            zs.lda = g.n;
+            zs.ldb = g.nh;
+            zs.ldc = g.n;
+            zs.upload();
+        }
         zw_owner_ = nullptr;
         zs.launch(c.stream);
         c.gemm_flops += zs.flops();
     }
     // ---- composite r synthesis -> (r, z)-values of the 6 velocity / vorticity components
-    GemmPlan& rs = gemm(ptr_key("nrs", 6, keyp, keyp, cls0), fresh);
+    // eigY: the z tensors are Y = Z (QR S_z) in eigen coordinates along r, the synthesis blocks carry QL
+    const int ycls[8] = {int(eigY), 0, 0, 0, 0, 0, 0, 0};
+    GemmPlan& rs = gemm(ptr_key(eigY ? "nrsY" : "nrs", 4, keyp, keyp, ycls), fresh);  // outputs: scratch
     if (fresh) {
         for (int pr = 0; pr < 2; ++pr)
             for (int s = 0; s < g.nslots; ++s)
@@ -856,7 +879,7 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
                     rs.tstart.push_back(int(rs.A.size()));
                     for (const CompositeTerm& ct : synth_.terms[size_t(s)]) {
                         if (ct.out != o) continue;
-                        rs.A.push_back(dsynth_.p + ct.off);
+                        rs.A.push_back((eigY ? dsynth_eig_.p : dsynth_.p) + ct.off);
                         rs.B.push_back(Z[pr][ct.in / 2] + long(s) * g.slot_stride + long(ct.in % 2) * g.plane_stride);
                     }
                     rs.C.push_back(val[3 * pr + o / 2] + long(s) * g.slot_stride + long(o % 2) * g.plane_stride);
@@ -881,7 +904,9 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     // values * (Az PR)[k0] (N columns, leading dimension 2 Np), see ensure_eigen
     const int Np = c.N + (c.N & 1);
     const int ecls[8] = {eig ? 1 : 0, 0, 0, 0, 0, 0, 0, 0};
-    GemmPlan& za = gemm(ptr_key("nza", 6, keyp, keyp, ecls), fresh);
+    // the analysis side reads only scratch tensors: key it on the outputs
+    const void* okeyp[2] = {lam_n, gam_n};
+    GemmPlan& za = gemm(ptr_key("nza", 2, okeyp, okeyp, ecls), fresh);
     if (fresh) {
         for (int x = 0; x < 5; ++x) {
             const double* src = av[x < 3 ? x : x - 3];
@@ -913,7 +938,7 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     c.mark("X3_rz_analysis");
     // ---- composite curl + pt_decompose + r analysis -> (gamma_N, lambda_N)
     // eigen mode: blocks PL_P A_t (M x mh) and output in the eigen layout (M x 2 Np per slot, plane)
-    GemmPlan& ra = gemm(ptr_key("nra", 6, keyp, keyp, ecls), fresh);
+    GemmPlan& ra = gemm(ptr_key("nra", 2, okeyp, okeyp, ecls), fresh);
     if (fresh) {
         for (int s = 0; s < g.nslots; ++s)
             for (int o = 0; o < 4; ++o) {
@@ -1306,6 +1331,22 @@ void Pipeline::ensure_eigen(DevSet& pset) {
         gp.launch(c.stream);
         CCF_CUDA(cudaStreamSynchronize(c.stream));
     }
+    // C_t QL[s] for every composite synthesis block (mh x M in the mh x mh slot, pad column zero):
+    // sum_t C_t (u_t S_z) = sum_t (C_t QL) (Z_t QS), see eigen_ysynth
+    dsynth_eig_.alloc(synth_.blocks.size());
+    {
+        GemmPlan gp;
+        for (int s = 0; s < g.nslots; ++s)
+            for (const CompositeTerm& ct : synth_.terms[size_t(s)]) {
+                gp.A.push_back(dsynth_.p + ct.off);
+                gp.B.push_back(pset.dg + pset.host.dg_left[size_t(s)] + long(M) * mh);  // QL mh x M (ld Mp)
+                gp.C.push_back(dsynth_eig_.p + ct.off);
+            }
+        gp.M = mh; gp.N = M; gp.K = mh; gp.lda = mh; gp.ldb = Mp; gp.ldc = mh;
+        gp.upload();
+        gp.launch(c.stream);
+        CCF_CUDA(cudaStreamSynchronize(c.stream));
+    }
     // QS[k0] = QR[k0] Sz[k0], QD[k0] = QR[k0] DzS[1 - k0] (N x nh): u_k0 Sz = T3 QS, the dz synthesis
     // of the same half lands in value half 1 - k0
     eig_QS_.alloc(size_t(2) * N * nh);
@@ -1327,73 +1368,46 @@ void Pipeline::ensure_eigen(DevSet& pset) {
     (void)even;
 }
 
-// z-synthesized tensors straight from eigen coordinates: T3 = QL Z (e3), then for each requested
-// output S_t (value halves [E | O] of u_t Sz) and D_t (of (dz u_t) Sz): T3 QS[k0] into half k0,
-// T3 QD[k0] into half 1 - k0 (ld n). Replaces u = T3 QR followed by the z synthesis of u.
-void Pipeline::eigen_zsynth(DevSet& set, int ntensor, const double* const* z, double* const* outS,
-                            double* const* outD) {
+// z-synthesized tensors in eigen coordinates along r: for each tensor t and requested output,
+// Y_S = Z_t QS[k0] into value half k0, Y_D = Z_t QD[k0] into half 1 - k0 (M rows of each mh-row
+// block, ld n). u_t S_z = QL Y_S, so the composite synthesis with the QL-folded blocks
+// (dsynth_eig_) consumes Y directly: one product per output instead of QL Z then T3 QS.
+// Z_t is base-relative (ring slots): bases z[0..ntensor).
+void Pipeline::eigen_ysynth(int ntensor, const double* const* z, double* const* outS, double* const* outD) {
     const Geo& g = c.gh;
-    const int M = c.M, N = c.N, mh = g.mh, nh = g.nh;
-    const int Mp = M + (M & 1), Np = N + (N & 1);
-    const size_t per = std::max(size_t(mh) * Np, size_t(M) * std::max(nh, Np));
-    if (!dT1_.p) {
-        const size_t cap = per * size_t(3 * std::max(c.gh.nslots, c.gf.nslots) * 4);  // up to 3 tensors of sub-problems
-        dT1_.alloc(cap);
-        dZ_.alloc(cap);
-        dT3_.alloc(cap);
-    }
-    const void* keyp[4] = {&set, &set, &set, &set};
-    const int ci[4] = {ntensor, ntensor, ntensor, ntensor};
-    bool fresh;
-    GemmPlan& e3 = gemm(ptr_key("ez3", 1, keyp, keyp, ci), fresh);
-    if (fresh) {
-        const double* dg = set.dg;
-        long task = 0;
-        for (int t = 0; t < ntensor; ++t)
-            for (int s = 0; s < g.nslots; ++s)
-                for (int k0 = 0; k0 < 2; ++k0)
-                    for (int pl = 0; pl < 2; ++pl, ++task) {
-                        const long PLo = set.host.dg_left[size_t(s)], QLo = PLo + long(M) * mh;
-                        e3.A.push_back(dg + QLo);
-                        e3.B.push_back(nullptr);
-                        e3.Boff.push_back((long(t) << kBaseShift) + eig_off(s, pl, k0));
-                        e3.C.push_back(dT3_.p + size_t(task) * per);
-                    }
-        e3.M = mh; e3.N = N; e3.K = M; e3.lda = Mp; e3.ldb = 2 * Np; e3.ldc = Np;
-        e3.upload();
-    }
+    const int M = c.M, N = c.N, nh = g.nh;
+    const int Np = N + (N & 1);
     const void* okey[6] = {outS[0], outD[0], ntensor > 1 ? outS[1] : nullptr, ntensor > 1 ? outD[1] : nullptr,
                            ntensor > 2 ? outS[2] : nullptr, ntensor > 2 ? outD[2] : nullptr};
-    const void* keyp6[6] = {&set, &set, &set, &set, &set, &set};
     const int ci6[6] = {ntensor, ntensor, ntensor, ntensor, ntensor, ntensor};
-    GemmPlan& zo = gemm(ptr_key("ezs", 6, okey, keyp6, ci6), fresh);
+    bool fresh;
+    GemmPlan& ys = gemm(ptr_key("eys", 6, okey, okey, ci6), fresh);
     if (fresh) {
-        long task = 0;
         for (int t = 0; t < ntensor; ++t)
             for (int s = 0; s < g.nslots; ++s)
                 for (int k0 = 0; k0 < 2; ++k0)
-                    for (int pl = 0; pl < 2; ++pl, ++task) {
+                    for (int pl = 0; pl < 2; ++pl) {
                         const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
-                        const double* T3 = dT3_.p + size_t(task) * per;
+                        const long zo = (long(t) << kBaseShift) + eig_off(s, pl, k0);  // Z_t: M x N (ld 2 Np)
                         if (outS[t]) {
-                            zo.A.push_back(T3);
-                            zo.B.push_back(eig_QS_.p + size_t(k0) * N * nh);
-                            zo.C.push_back(outS[t] + off + long(k0) * nh);
+                            ys.A.push_back(nullptr);
+                            ys.Aoff.push_back(zo);
+                            ys.B.push_back(eig_QS_.p + size_t(k0) * N * nh);
+                            ys.C.push_back(outS[t] + off + long(k0) * nh);
                         }
                         if (outD[t]) {
-                            zo.A.push_back(T3);
-                            zo.B.push_back(eig_QD_.p + size_t(k0) * N * nh);
-                            zo.C.push_back(outD[t] + off + long(1 - k0) * nh);
+                            ys.A.push_back(nullptr);
+                            ys.Aoff.push_back(zo);
+                            ys.B.push_back(eig_QD_.p + size_t(k0) * N * nh);
+                            ys.C.push_back(outD[t] + off + long(1 - k0) * nh);
                         }
                     }
-        zo.M = mh; zo.N = nh; zo.K = N; zo.lda = Np; zo.ldb = nh; zo.ldc = g.n;
-        zo.upload();
+        ys.M = M; ys.N = nh; ys.K = N; ys.lda = 2 * Np; ys.ldb = nh; ys.ldc = g.n;
+        ys.upload();
     }
-    e3.launch(c.stream, z[0], ntensor > 1 ? z[1] : z[0], nullptr, nullptr, ntensor > 2 ? z[2] : z[0]);
-    c.gemm_flops += e3.flops();
-    zo.launch(c.stream);
-    c.gemm_flops += zo.flops();
-    c.launches += 2;
+    ys.launch(c.stream, z[0], ntensor > 1 ? z[1] : z[0], nullptr, nullptr, ntensor > 2 ? z[2] : z[0]);
+    c.gemm_flops += ys.flops();
+    ++c.launches;
 }
 
 const double* const* Pipeline::eig_rt(DevSet& set) {
@@ -1753,22 +1767,36 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
     const double scale = kappa * (1.0 / reynolds);
     if (eigen) {
         // eigen-coordinate step (see Pipeline::eig_off): every modal solve is (RHS .* RT) + back transform,
-        // and the back transforms produce the nonlinear term's z-synthesized inputs directly
-        // (Pipeline::eigen_zsynth); omega itself is reconstructed on demand (NSState::omega_coeff)
+        // and the back transforms produce the nonlinear term's z-synthesized inputs directly in eigen
+        // coordinates along r (Pipeline::eigen_ysynth, QL folded into the synthesis blocks); omega
+        // itself is reconstructed on demand (NSState::omega_coeff)
         DevSet& pset = c.set(false, true, 1.0);
         if (!disable_nonlinear) {
-            double* zp = zpsi.p;
             c.mark("start");
-            // velocity_from_vorticity (ptns.cpp:85-91): lambda_v = gamma_omega (scratch 4), gamma_v = lambda_psi
-            // (scratch 1, 2: its z and dz synthesis). In the steady state the previous step's Helmholtz back
-            // transform already produced them from Z_P; otherwise (first step, displaced scratch) solve here.
-            (void)zp;
-            if (!(zv_head == cur && P.zw_owner_ == this)) {
-                velocity(cur);
+            if (steps == 0) {
+                // initial data: omega_0 need not lie in the range of QL PL, so the first nonlinear term runs on
+                // the coefficient-space omega_0 and psi = QL Z_P QR, exactly as the reference
+                if (zp_head != cur) {
+                    const double* zs[1] = {zl[cur].p};
+                    const double wm1[1] = {-1.0};
+                    P.eigen_rhs(pset, 1, zs, zs, wm1, 1, 1.0, zpsi.p, zpsi.p);  // Z_P = -Z_lambda .* RT_P
+                    zp_head = cur;
+                }
+                double* lpsi = P.scratch(18);
+                P.eigen_back(pset, 1, zpsi.p, zpsi.p, lpsi, lpsi);
                 c.mark("P_poisson_solve");
+                P.nonlinear(gw, lpsi, lw, gw, nl[nnew].p, ng[nnew].p, &pset);  // N~ = PL_P N PR
+            } else {
+                // velocity_from_vorticity (ptns.cpp:85-91): lambda_v = gamma_omega (scratch 4), gamma_v = lambda_psi
+                // (scratch 1, 2). In the steady state the previous step's Helmholtz back transform produced
+                // them from Z_P; otherwise (displaced scratch) solve here.
+                if (!(zv_head == cur && P.zw_owner_ == this)) {
+                    velocity(cur);
+                    c.mark("P_poisson_solve");
+                }
+                P.nonlinear(P.scratch(4), P.scratch(1), P.scratch(3), P.scratch(4), nl[nnew].p, ng[nnew].p, &pset,
+                            true, true);  // N~ = PL_P N PR
             }
-            P.nonlinear(P.scratch(4), P.scratch(1), P.scratch(3), P.scratch(4), nl[nnew].p, ng[nnew].p, &pset,
-                        true);  // N~ = PL_P N PR
         }
         const double* sl[kMaxSrc];
         const double* sg[kMaxSrc];
@@ -1849,56 +1877,21 @@ void NSState::velocity(int r) {
     const double* zz[1] = {zpsi.p};
     double* oS[1] = {P.scratch(1)};
     double* oD[1] = {P.scratch(2)};
-    P.eigen_zsynth(pset, 1, zz, oS, oD);
+    P.eigen_ysynth(1, zz, oS, oD);
     zv_head = r;
 }
 
 void NSState::zsynth_omega(int r) {
-    Pipeline& P = *pl;
-    if (coeff_head == r) {  // the coefficient state is authoritative (initial data)
-        P.zsynth_coeff(lam[r].p, gam[r].p, P.scratch(3), P.scratch(4), P.scratch(5));
-        zv_head = -1;
-        P.zw_owner_ = this;
-        return;
-    }
     // lambda_omega -> S (scratch 3); gamma_omega -> S, dz S (4, 5); with a valid Z_P of the same slot also
-    // lambda_psi -> S, dz S (1, 2), i.e. the next nonlinear term's velocity: one e3 + one z launch
+    // lambda_psi -> S, dz S (1, 2), i.e. the next nonlinear term's velocity: one launch (eigen_ysynth)
+    Pipeline& P = *pl;
     const bool vel = zp_head == r;
     const double* z[3] = {zl[r].p, zg[r].p, zpsi.p};
     double* oS[3] = {P.scratch(3), P.scratch(4), P.scratch(1)};
     double* oD[3] = {nullptr, P.scratch(5), P.scratch(2)};
-    P.eigen_zsynth(P.c.set(false, true, 1.0), vel ? 3 : 2, z, oS, oD);
+    P.eigen_ysynth(vel ? 3 : 2, z, oS, oD);
     zv_head = vel ? r : -1;
     P.zw_owner_ = this;
-}
-
-// same from the coefficient-space omega (the initial data: it need not lie in the range of QL PL, so
-// its z tensors are not those of QL Z0 QR)
-void Pipeline::zsynth_coeff(const double* lam, const double* gam, double* oS0, double* oS1, double* oD1) {
-    const Geo& g = c.gh;
-    const void* keyp[5] = {lam, gam, oS0, oS1, oD1};
-    bool fresh;
-    GemmPlan& zs = gemm(ptr_key("czs", 5, keyp, keyp, nullptr), fresh);
-    if (fresh) {
-        const double* src[3] = {lam, gam, gam};
-        double* dst[3] = {oS0, oS1, oD1};
-        for (int x = 0; x < 3; ++x)
-            for (int s = 0; s < g.nslots; ++s)
-                for (int pl = 0; pl < 2; ++pl) {
-                    const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
-                    for (int po = 0; po < 2; ++po) {
-                        const int pi = x == 2 ? 1 - po : po;
-                        zs.A.push_back(src[x] + off + pi * g.nh);
-                        zs.B.push_back((x == 2 ? tp.DzS.p : tp.Sz.p) + size_t(po) * g.nh * g.nh);
-                        zs.C.push_back(dst[x] + off + po * g.nh);
-                    }
-                }
-        zs.M = g.mh; zs.N = g.nh; zs.K = g.nh; zs.lda = g.n; zs.ldb = g.nh; zs.ldc = g.n;
-        zs.upload();
-    }
-    zs.launch(c.stream);
-    c.gemm_flops += zs.flops();
-    ++c.launches;
 }
 
 // coefficient-space omega of the newest ring slot (eigen mode keeps only Z between steps)
@@ -1911,7 +1904,7 @@ void NSState::omega_coeff() {
 void NSState::step_once() {
     Ctx& c = pl->c;
     // scratch 3..5 may have been reused (another stepper, a standalone nonlinear call) since our last step
-    if (eigen && !disable_nonlinear && pl->zw_owner_ != this) {
+    if (eigen && !disable_nonlinear && steps > 0 && pl->zw_owner_ != this) {
         zsynth_omega(head);
         if (zv_head != head) velocity(head);  // a replayed graph has no Poisson stage
     }

@@ -42,6 +42,8 @@ struct GemmPlan {
     std::vector<int> tstart;          // optional: batch b sums terms [tstart[b], tstart[b+1])
     std::vector<const double*> DL, DR;  // optional per-batch epilogue divisors (dl_i + dr_j)
     std::vector<long> Boff, Coff;       // optional base-relative B / C (see GemmBatch)
+    std::vector<long> Aoff;             // optional base-relative A (A then holds one placeholder per term)
+    long* dAoff = nullptr;
     long ldd = 0;                       // leading dimension of the epilogue table (0: N)
     const double** dA = nullptr;
     const double** dB = nullptr;
@@ -87,12 +89,11 @@ public:
     void curl_decompose(const double* ar, const double* at, const double* az, double* out_r, double* out_t,
                         double* out_z, double* lam, double* gam);
     // eig != nullptr: output N~ = PL_P N PR in the eigen layout of that (Poisson) set's modal basis
-    // zpre: scratch(0..5) already hold the z-synthesized inputs (lambda_v = gamma_w aliased to scratch(4))
+    // zpre: scratch(0..5) already hold the z-synthesized inputs (lambda_v = gamma_w aliased to scratch(4));
+    // eigY: those are eigen-coordinate Y tensors (eigen_ysynth), synthesized with the QL-folded blocks
     void nonlinear(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w, double* lam_n,
-                   double* gam_n, DevSet* eig = nullptr, bool zpre = false);
-    void zsynth_coeff(const double* lam, const double* gam, double* oS0, double* oS1, double* oD1);
-    void eigen_zsynth(DevSet& set, int ntensor, const double* const* z, double* const* outS,
-                      double* const* outD);
+                   double* gam_n, DevSet* eig = nullptr, bool zpre = false, bool eigY = false);
+    void eigen_ysynth(int ntensor, const double* const* z, double* const* outS, double* const* outD);
     // eigen-coordinate NS state (see pipeline.cu)
     long eig_off(int s, int pl, int k0) const;
     void ensure_eigen(DevSet& pset);
@@ -135,7 +136,7 @@ public:  // internal state (used by the NS stepper and the C-ABI layer)
     // composite radial operators of the nonlinear term (built on first use)
     bool comp_ready_ = false, comp_off_ = false;  // CCF_NONLINEAR_PENCIL=1: sequential pencil path
     CompositeSet synth_, anal_;
-    DBuf dsynth_, danal_;
+    DBuf dsynth_, danal_, dsynth_eig_;
     bool composite_off() const { return comp_off_; }
     void ensure_composite();
     void nonlinear_pencil(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w,

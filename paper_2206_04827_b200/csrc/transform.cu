@@ -58,7 +58,13 @@ __global__ void __launch_bounds__(128) dgemm_batched_kernel(GemmBatch g) {
     double ra[8], rb[8];
     auto gload = [&](int it) {
         const int term = t0 + it / nkt, k0 = (it % nkt) * BK;
-        const double* __restrict__ A = g.A[term];
+        const double* __restrict__ A;
+        if (g.aoff) {
+            const long o = g.aoff[term];
+            A = g.bbase[o >> kBaseShift] + (o & ((1L << kBaseShift) - 1));
+        } else {
+            A = g.A[term];
+        }
         const double* __restrict__ B;
         if (g.boff) {
             const long o = g.boff[term];
@@ -181,7 +187,12 @@ __global__ void __launch_bounds__(2 * PM, PM == 128 ? 2 : 4) dgemm_pipe_kernel(G
     const double* LA = nullptr;
     const double* LB = nullptr;
     auto set_term = [&]() {
-        LA = g.A[lt];
+        if (g.aoff) {
+            const long o = g.aoff[lt];
+            LA = g.bbase[o >> kBaseShift] + (o & ((1L << kBaseShift) - 1));
+        } else {
+            LA = g.A[lt];
+        }
         if (g.boff) {
             const long o = g.boff[lt];
             LB = g.bbase[o >> kBaseShift] + (o & ((1L << kBaseShift) - 1));

@@ -99,6 +99,36 @@ ccf_status ccf_ns_step(ccf_ns_state* st, int nsteps);
 ccf_status ccf_ns_get_omega(ccf_ns_state* st, double* lam, double* gam, double* time, int* steps_taken);
 ccf_status ccf_ns_destroy(ccf_ns_state* st);
 
+/* Mode sharding of the NS / heat stepper over the GPUs of one node (the reference is
+ * single-process, ptns.cpp:217-267 — this replaces nothing, it partitions NSStepper::step).
+ * Rank r of world computes the half-spectrum Fourier slots [slot_lo, slot_hi) (w = slot, slot p/2 =
+ * Nyquist) in every per-mode stage and the radial value rows [row_lo, row_hi) of all slots in the
+ * theta stage, reading / writing each slot's values in the owning rank's exchange buffer through
+ * peer memory (NVLink), ordered by two rank barriers per step. Every rank passes the full initial
+ * field to ccf_ns_create; ccf_ns_get_omega fills the rank's own slots (w = +-slot) correctly and
+ * leaves the others meaningless: gather by slot ownership. Call order: ccf_ctx_create ->
+ * ccf_shard_init -> (ccf_shard_ipc_handle, exchange the handles, ccf_shard_open_ipc)
+ * | ccf_shard_link_local -> ccf_ns_create. Other compute entry points on a sharded context return
+ * CCF_CONFIG_ERROR. world == 1 leaves the context unsharded. */
+ccf_status ccf_shard_init(ccf_ctx* ctx, int rank, int world);
+/* Host-only (no GPU): the partition ccf_shard_init uses, world + 1 bounds each
+ * (rank r: slots [slot_bounds[r], slot_bounds[r+1]), rows [row_bounds[r], row_bounds[r+1])). */
+ccf_status ccf_shard_partition(int m, int p, int world, int* slot_bounds, int* row_bounds);
+ccf_status ccf_shard_info(ccf_ctx* ctx, int* rank, int* world, int* slot_lo, int* slot_hi, int* row_lo, int* row_hi);
+/* CCF_SHARD_HANDLE_BYTES-byte handle of this rank's exchange buffer (CUDA IPC handle + offset). */
+#define CCF_SHARD_HANDLE_BYTES 128
+ccf_status ccf_shard_ipc_handle(ccf_ctx* ctx, void* handle);
+/* world x CCF_SHARD_HANDLE_BYTES bytes of handles in rank order (own entry ignored): maps the peers' exchange buffers;
+ * rank barriers then run on the device (graph-capturable). */
+ccf_status ccf_shard_open_ipc(ccf_ctx* ctx, const void* handles);
+/* Ranks emulated in one process on one device (contexts ctxs[r] sharded as rank r of world): peer
+ * buffers are plain device pointers and the barriers are host barriers between the threads that
+ * step the ranks concurrently (no device-side waiting between ranks). */
+ccf_status ccf_shard_link_local(ccf_ctx* const* ctxs, int world);
+/* Replace the device barrier by stream synchronisation + fn(user) (a host barrier across ranks);
+ * fn == NULL restores the device barrier. */
+ccf_status ccf_shard_set_host_barrier(ccf_ctx* ctx, void (*fn)(void*), void* user);
+
 /* Details of the last error on this context (thread-compatible, not thread-safe).
  * kind = ccf_status; slice = Fourier slice of a failed modal solve or -1;
  * shift_index = ADI shift of a singular operator or -1; residual history of a

@@ -77,7 +77,11 @@ EXPORTS = ["ccf_ctx_create", "ccf_ctx_destroy", "ccf_ctx_set_stream", "ccf_ctx_s
            "ccf_get_last_error", "ccf_get_stats", "ccf_reset_stats", "ccf_modal_plan", "ccf_version",
            "ccf_ns_profile_step", "ccf_ns_set_graphs", "ccf_ns_launches_per_step", "ccf_plan_host",
            "ccf_create_error", "ccf_adi_last_rounds", "ccf_adi_keep_history", "ccf_get_gemm_flops",
-           "ccf_diag_host_check"]
+           "ccf_diag_host_check", "ccf_shard_init", "ccf_shard_partition", "ccf_shard_info", "ccf_shard_ipc_handle",
+           "ccf_shard_open_ipc", "ccf_shard_link_local", "ccf_shard_set_host_barrier"]
+
+HOST_BARRIER_FN = C.CFUNCTYPE(None, C.c_void_p)
+SHARD_HANDLE_BYTES = 128  # include/ccf.h CCF_SHARD_HANDLE_BYTES
 
 _lib = None
 
@@ -140,8 +144,26 @@ def lib():
         L.ccf_ns_launches_per_step.argtypes = [vp, C.POINTER(C.c_long)]
         L.ccf_plan_host.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double, C.c_int, dp, dp, dp,
                                     C.c_int]
+        ip = C.POINTER(C.c_int)
+        L.ccf_shard_init.argtypes = [vp, C.c_int, C.c_int]
+        L.ccf_shard_partition.argtypes = [C.c_int, C.c_int, C.c_int, ip, ip]
+        L.ccf_shard_info.argtypes = [vp, ip, ip, ip, ip, ip, ip]
+        L.ccf_shard_ipc_handle.argtypes = [vp, C.c_char_p]
+        L.ccf_shard_open_ipc.argtypes = [vp, C.c_char_p]
+        L.ccf_shard_link_local.argtypes = [C.POINTER(vp), C.c_int]
+        L.ccf_shard_set_host_barrier.argtypes = [vp, HOST_BARRIER_FN, vp]
         _lib = L
     return _lib
+
+
+def shard_partition(m, p, world):
+    """The library's partition (host only, no GPU): (slot bounds, row bounds), world + 1 each."""
+    sb = (C.c_int * (world + 1))()
+    rb = (C.c_int * (world + 1))()
+    st = lib().ccf_shard_partition(int(m), int(p), int(world), sb, rb)
+    if st != 0:
+        raise _ERR.get(st, CCFError)("ccf_shard_partition: invalid (m, p, world)")
+    return list(sb), list(rb)
 
 
 def _addr(a):
@@ -288,6 +310,39 @@ class Context:
         self._check(lib().ccf_nonlinear(self.h, _addr(_c128(lam_v)), _addr(_c128(gam_v)), _addr(_c128(lam_w)),
                                         _addr(_c128(gam_w)), *[_addr(x) for x in o]))
         return tuple(o)
+
+    # ---- mode sharding (csrc/shard.cu)
+    def shard(self, rank, world):
+        """Make this context rank `rank` of `world` (before creating a stepper)."""
+        self._check(lib().ccf_shard_init(self.h, int(rank), int(world)))
+        return self
+
+    def shard_info(self):
+        v = [C.c_int() for _ in range(6)]
+        self._check(lib().ccf_shard_info(self.h, *[C.byref(x) for x in v]))
+        return dict(zip(("rank", "world", "slot_lo", "slot_hi", "row_lo", "row_hi"), (x.value for x in v)))
+
+    def ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(SHARD_HANDLE_BYTES)
+        self._check(lib().ccf_shard_ipc_handle(self.h, buf))
+        return buf.raw
+
+    def open_ipc(self, handles):
+        """handles: the ranks' ipc_handle() values (SHARD_HANDLE_BYTES each) in rank order."""
+        blob = b"".join(bytes(x) for x in handles)
+        self._check(lib().ccf_shard_open_ipc(self.h, blob))
+
+    @staticmethod
+    def link_local(ctxs):
+        """Emulate ranks in one process on one device (step them from concurrent threads)."""
+        arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+        ctxs[0]._check(lib().ccf_shard_link_local(arr, len(ctxs)))
+
+    def set_host_barrier(self, fn):
+        """fn(): a host barrier across ranks, called after synchronising the stream (None: device barrier)."""
+        cb = HOST_BARRIER_FN(lambda _u: fn()) if fn else HOST_BARRIER_FN()
+        self._barrier_cb = cb  # keep alive
+        self._check(lib().ccf_shard_set_host_barrier(self.h, cb, None))
 
     # ---- introspection
     def modal_plan(self, w, scale=1.0, poisson=True):

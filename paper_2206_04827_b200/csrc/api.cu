@@ -122,6 +122,7 @@ ccf_status ccf_ctx_synchronize(ccf_ctx* ctx) {
 ccf_status ccf_poisson3d(ccf_ctx* ctx, const double* f, double* u) {
     // proj/src/solvers.cpp:142-175: parity(f); per slice R2 f C02^T -> ModalSolver(Poisson) -> parity(out).
     return guard(ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_poisson3d");
         const bool full = true;  // arbitrary complex input: no Hermitian assumption
         const long nt = c.tensor_doubles(full);
         if (c.tens[0].n < size_t(nt)) c.tens[0].alloc(size_t(nt));
@@ -142,6 +143,7 @@ ccf_status ccf_helmholtz_step(ccf_ctx* ctx, const double* const* hist, int nhist
                               double diffusivity, double h, double* out) {
     // proj/src/timestep.cpp:61-108
     return guard(ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_helmholtz_step");
         double koh, bw[4] = {0, 0, 0, 0};
         bdf_scheme(order, &koh, bw);
         if (nhist < order) throw Error(ccf::DOMAIN_ERROR, "bdf_rhs: insufficient history for the requested order");
@@ -257,7 +259,7 @@ ccf_status ccf_adi_last_rounds(ccf_ctx* ctx, int which, int* ntensor, int* nslot
 
 ccf_status ccf_reset_stats(ccf_ctx* ctx) {
     return guard(ctx, [&](Ctx& c) {
-        CCF_CUDA(cudaMemset(c.ws.iters, 0, sizeof(unsigned long long) * 2));
+        CCF_CUDA(cudaMemsetAsync(c.ws.iters, 0, sizeof(unsigned long long) * 2, c.stream));
         c.launches = 0;
         c.gemm_flops = 0.0;
     });
@@ -295,6 +297,7 @@ ccf_status ccf_velocity_from_vorticity(ccf_ctx* ctx, const double* lam_w, const 
                                        double* gam_v) {
     // proj/src/ptns.cpp:85-91: (lambda_v, gamma_v) = (gamma_w, Poisson3D(-lambda_w))
     return guard(ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_velocity_from_vorticity");
         ccf::Pipeline& P = ctx->pl();
         double *l = tens(c, 0), *g = tens(c, 1), *u = tens(c, 2);
         c.load_coeff(lam_w, l, false, 0, 0);
@@ -312,6 +315,7 @@ ccf_status ccf_nonlinear(ccf_ctx* ctx, const double* lam_v, const double* gam_v,
                          const double* gam_w, double* lam_out, double* gam_out) {
     // proj/src/ptns.cpp:114-149
     return guard(ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_nonlinear");
         ccf::Pipeline& P = ctx->pl();
         double *a = tens(c, 0), *b = tens(c, 1), *d = tens(c, 2), *e = tens(c, 3), *o1 = tens(c, 4), *o2 = tens(c, 5);
         c.load_coeff(lam_v, a, false, 0, 0);
@@ -328,6 +332,7 @@ ccf_status ccf_nonlinear(ccf_ctx* ctx, const double* lam_v, const double* gam_v,
 ccf_status ccf_pt_synthesize(ccf_ctx* ctx, const double* lam, const double* gam, double* vr, double* vt, double* vz) {
     // proj/src/ptns.cpp:42-57
     return guard(ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_pt_synthesize");
         if (c.m % 2) throw Error(ccf::DOMAIN_ERROR, "pt_synthesize: even m required (no r = 0 grid node)");
         ccf::Pipeline& P = ctx->pl();
         double *l = tens(c, 0), *g = tens(c, 1), *o0 = tens(c, 2), *o1 = tens(c, 3), *o2 = tens(c, 4);
@@ -350,6 +355,7 @@ ccf_status ccf_curl_vector(ccf_ctx* ctx, const double* vr, const double* vt, con
                            double* ot, double* oz) {
     // proj/src/ptns.cpp:25-33 on a physical vector field (r, theta components azimuthal-flip class)
     return guard(ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_curl_vector");
         ccf::Pipeline& P = ctx->pl();
         double *a = tens(c, 0), *b = tens(c, 1), *d = tens(c, 2), *o0 = tens(c, 3), *o1 = tens(c, 4), *o2 = tens(c, 5);
         c.load_coeff(vr, a, false, 1, 0);
@@ -367,6 +373,7 @@ ccf_status ccf_pt_decompose(ccf_ctx* ctx, const double* vr, const double* vt, co
                             double* gam) {
     // proj/src/ptns.cpp:59-77 (divergence check off, as on the NS path)
     return guard(ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_pt_decompose");
         ccf::Pipeline& P = ctx->pl();
         double *a = tens(c, 0), *b = tens(c, 1), *d = tens(c, 2), *o0 = tens(c, 3), *o1 = tens(c, 4);
         c.load_coeff(vr, a, false, 1, 0);
@@ -382,6 +389,7 @@ ccf_status ccf_pt_decompose(ccf_ctx* ctx, const double* vr, const double* vt, co
 ccf_status ccf_hpoisson(ccf_ctx* ctx, const double* rhs, double* u) {
     // proj/src/solvers.cpp:177-203
     return guard(ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_hpoisson");
         ccf::Pipeline& P = ctx->pl();
         double *a = tens(c, 0), *o = tens(c, 1);
         c.load_coeff(rhs, a, false, 0, 0);
@@ -395,6 +403,7 @@ ccf_status ccf_hpoisson(ccf_ctx* ctx, const double* rhs, double* u) {
 ccf_status ccf_calculus(ccf_ctx* ctx, int op, const double* in, double* out) {
     // proj/src/calculus.cpp; both parity classes of the input are processed
     return guard(ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_calculus");
         if (op == 4 && c.m % 2) throw Error(ccf::DOMAIN_ERROR, "divide_r: even m required");
         ccf::Pipeline& P = ctx->pl();
         for (int cls = 0; cls < 2; ++cls) {
@@ -411,6 +420,7 @@ ccf_status ccf_calculus(ccf_ctx* ctx, int op, const double* in, double* out) {
 ccf_status ccf_curl_pt(ccf_ctx* ctx, const double* lam, const double* gam, double* lam_out, double* gam_out) {
     // proj/src/ptns.cpp:79-83: (lambda, gamma) -> (-lap gamma, lambda)
     return guard(ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_curl_pt");
         ccf::Pipeline& P = ctx->pl();
         double *g = tens(c, 0), *o = tens(c, 1), *l = tens(c, 2);
         c.load_coeff(gam, g, false, 0, 0);
@@ -426,6 +436,7 @@ ccf_status ccf_curl_pt(ccf_ctx* ctx, const double* lam, const double* gam, doubl
 ccf_status ccf_analyze(ccf_ctx* ctx, const double* values, double* coeffs) {
     // proj/src/transform.cpp:122-165 (arbitrary real fields, full spectrum)
     return guard(ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_analyze");
         ccf::Pipeline& P = ctx->pl();
         P.analyze_full(values, coeffs);
         c.sync();
@@ -435,6 +446,7 @@ ccf_status ccf_analyze(ccf_ctx* ctx, const double* values, double* coeffs) {
 ccf_status ccf_synthesize(ccf_ctx* ctx, const double* coeffs, double* values) {
     // proj/src/transform.cpp:167-203
     return guard(ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_synthesize");
         ccf::Pipeline& P = ctx->pl();
         P.synthesize_full(coeffs, values);
         c.sync();
@@ -465,7 +477,7 @@ ccf_status ccf_ns_create(ccf_ctx* ctx, double reynolds, double h, int order, int
             s.ng[i].alloc(size_t(T));
         }
         CCF_CUDA(cudaMalloc(&s.dflag, sizeof(int)));
-        CCF_CUDA(cudaMemset(s.dflag, 0, sizeof(int)));
+        CCF_CUDA(cudaMemsetAsync(s.dflag, 0, sizeof(int), c.stream));
         c.load_coeff(lam0, s.lam[0].p, false, 0, 0);  // parity projection of the initial data (ptns.cpp:190-191)
         c.load_coeff(gam0, s.gam[0].p, false, 0, 1);
         // build every solver set the run needs before any graph capture
@@ -493,6 +505,9 @@ ccf_status ccf_ns_create(ccf_ctx* ctx, double reynolds, double h, int order, int
                 P.to_eigen(pset, s.gam[0].p, s.zg[0].p);
             }
         }
+        if (c.sh.sharded() && !s.eigen)
+            throw Error(ccf::CONFIG_ERROR, "NSStepper: a mode-sharded context needs the eigen-coordinate state "
+                                           "(composite nonlinear term, fast-diagonalization solves)");
         c.sync();
         ctx->states.insert(st.get());
         *out = st.release();
@@ -503,6 +518,7 @@ ccf_status ccf_ns_step(ccf_ns_state* st, int nsteps) {
     if (!st) return CCF_INTERNAL_ERROR;
     return guard(st->ctx, [&](Ctx& c) {
         for (int i = 0; i < nsteps; ++i) st->st.step_once();
+        c.shard_check();
         c.check_adi_error(false);
         int f = 0;
         CCF_CUDA(cudaMemcpyAsync(&f, st->st.dflag, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
@@ -521,6 +537,58 @@ ccf_status ccf_ns_get_omega(ccf_ns_state* st, double* lam, double* gam, double* 
         if (time) *time = st->st.time;
         if (steps_taken) *steps_taken = st->st.steps;
     });
+}
+
+// ---- mode sharding (csrc/shard.cu)
+ccf_status ccf_shard_init(ccf_ctx* ctx, int rank, int world) {
+    return guard(ctx, [&](Ctx& c) {
+        if (!ctx->states.empty()) throw Error(ccf::CONFIG_ERROR, "ccf_shard_init: shard before creating a stepper");
+        c.shard_init(rank, world);
+        if (ctx->pipe) ctx->pipe->gemms_.clear();  // plans built so far address the unsharded scratch
+    });
+}
+
+ccf_status ccf_shard_partition(int m, int p, int world, int* slot_bounds, int* row_bounds) {
+    if (m < 4 || m % 2 || p < 2 || p % 2 || world < 1 || world > ccf::kMaxRanks || world > m / 2 || world > p / 2 + 1)
+        return CCF_CONFIG_ERROR;
+    ccf::shard_bounds(p / 2 + 1, world, slot_bounds);
+    ccf::shard_bounds(m / 2, world, row_bounds);
+    return CCF_OK;
+}
+
+ccf_status ccf_shard_info(ccf_ctx* ctx, int* rank, int* world, int* slot_lo, int* slot_hi, int* row_lo, int* row_hi) {
+    return guard(ctx, [&](Ctx& c) {
+        if (rank) *rank = c.sh.rank;
+        if (world) *world = c.sh.world;
+        if (slot_lo) *slot_lo = c.sh.s_lo;
+        if (slot_hi) *slot_hi = c.sh.s_hi;
+        if (row_lo) *row_lo = c.sh.r_lo;
+        if (row_hi) *row_hi = c.sh.r_hi;
+    });
+}
+
+ccf_status ccf_shard_ipc_handle(ccf_ctx* ctx, void* handle) {
+    return guard(ctx, [&](Ctx& c) { ccf::shard_ipc_handle(c, handle); });
+}
+
+ccf_status ccf_shard_open_ipc(ccf_ctx* ctx, const void* handles) {
+    return guard(ctx, [&](Ctx& c) { ccf::shard_open_ipc(c, handles); });
+}
+
+ccf_status ccf_shard_link_local(ccf_ctx* const* ctxs, int world) {
+    if (!ctxs || world < 1 || !ctxs[0]) return CCF_INTERNAL_ERROR;
+    return guard(ctxs[0], [&](Ctx&) {
+        std::vector<Ctx*> cs;
+        for (int i = 0; i < world; ++i) {
+            if (!ctxs[i] || !ctxs[i]->c) throw Error(ccf::CONFIG_ERROR, "ccf_shard_link_local: null context");
+            cs.push_back(ctxs[i]->c.get());
+        }
+        ccf::shard_link_local(cs.data(), world);
+    });
+}
+
+ccf_status ccf_shard_set_host_barrier(ccf_ctx* ctx, void (*fn)(void*), void* user) {
+    return guard(ctx, [&](Ctx& c) { ccf::shard_set_host_barrier(c, fn, user); });
 }
 
 ccf_status ccf_ns_destroy(ccf_ns_state* st) {

@@ -1,6 +1,9 @@
 // Host-side context implementation: device memory, solver-set cache
 // (ModalSolverCache, proj/src/solvers.cpp:100-109), ADI round driver.
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <vector>
 #include <cstdio>
 #include <cstring>
 
@@ -14,8 +17,11 @@ void DBuf::alloc(size_t count) {
     n = count;
     if (count) {
         CCF_CUDA(cudaMalloc(&p, count * sizeof(double)));
-        // zero-filled: pad columns of every tensor are defined (the TMA GEMM reads them at K edges)
+        // zero-filled: pad columns of every tensor are defined (the TMA GEMM reads them at K edges).
+        // cudaMemset runs on the legacy default stream, which the library's non-blocking streams do
+        // not wait for: complete it here, or a kernel writing the fresh buffer could be overtaken
         CCF_CUDA(cudaMemset(p, 0, count * sizeof(double)));
+        CCF_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
     }
 }
 DBuf::~DBuf() {
@@ -68,6 +74,8 @@ Ctx::Ctx(int m_, int n_, int p_, int device_, double tol_, int flags_)
     stream = own_stream;
     gh = make_geo(m, n, p, p / 2 + 1);
     gf = make_geo(m, n, p, p);
+    sh.s_hi = gh.nslots;
+    sh.r_hi = gh.mh;
     M = (m - 2) / 2;
     N = (n - 2) / 2;
     Mpad = ((M + 7) / 8) * 8;
@@ -89,6 +97,7 @@ Ctx::Ctx(int m_, int n_, int p_, int device_, double tol_, int flags_)
     CCF_CUDA(cudaMalloc(&ws.iters, sizeof(unsigned long long) * 2));
     CCF_CUDA(cudaMemset(ws.err, 0, sizeof(int) * 4));
     CCF_CUDA(cudaMemset(ws.iters, 0, sizeof(unsigned long long) * 2));
+    CCF_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
     ws.eprime.alloc(size_t(2) * cap * 4 * size_t(estride));
     ws.escr.alloc(size_t(2) * cap * 4 * size_t(estride));
     ws.xscr.alloc(size_t(2) * cap * 4 * size_t(estride));
@@ -104,6 +113,7 @@ Ctx::Ctx(int m_, int n_, int p_, int device_, double tol_, int flags_)
 }
 
 Ctx::~Ctx() {
+    shard_close();
     sets.clear();
     cudaFree(ws.res2);
     cudaFree(ws.e2);
@@ -157,16 +167,16 @@ DevSet& Ctx::set(bool full, bool poisson, double scale) {
     const SolverSet& h = ds->host;
     if (h.has_diag) {
         CCF_CUDA(cudaMalloc(&ds->dg, h.dg.size() * sizeof(double)));
-        CCF_CUDA(cudaMemcpy(ds->dg, h.dg.data(), h.dg.size() * sizeof(double), cudaMemcpyHostToDevice));
+        CCF_H2D(ds->dg, h.dg.data(), h.dg.size() * sizeof(double));
     }
     CCF_CUDA(cudaMalloc(&ds->coef, h.coef.size() * sizeof(double)));
-    CCF_CUDA(cudaMemcpy(ds->coef, h.coef.data(), h.coef.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CCF_H2D(ds->coef, h.coef.data(), h.coef.size() * sizeof(double));
     CCF_CUDA(cudaMalloc(&ds->slots, h.slots.size() * sizeof(AdiSlot)));
-    CCF_CUDA(cudaMemcpy(ds->slots, h.slots.data(), h.slots.size() * sizeof(AdiSlot), cudaMemcpyHostToDevice));
+    CCF_H2D(ds->slots, h.slots.data(), h.slots.size() * sizeof(AdiSlot));
     std::vector<int> J(h.slots.size());
     for (size_t s = 0; s < J.size(); ++s) J[s] = h.slots[s].J;
     CCF_CUDA(cudaMalloc(&ds->J, J.size() * sizeof(int)));
-    CCF_CUDA(cudaMemcpy(ds->J, J.data(), J.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CCF_H2D(ds->J, J.data(), J.size() * sizeof(int));
     // tasks: longest slots first (load balance of the J-heterogeneous batch)
     std::vector<int> order(size_t(g.nslots));
     for (int s = 0; s < g.nslots; ++s) order[size_t(s)] = s;
@@ -179,7 +189,7 @@ DevSet& Ctx::set(bool full, bool poisson, double scale) {
                     for (int pl = 0; pl < 2; ++pl) tasks.push_back({t, s, k0, pl});
         ds->ntasks[nt - 1] = int(tasks.size());
         CCF_CUDA(cudaMalloc(&ds->tasks[nt - 1], tasks.size() * sizeof(AdiTask)));
-        CCF_CUDA(cudaMemcpy(ds->tasks[nt - 1], tasks.data(), tasks.size() * sizeof(AdiTask), cudaMemcpyHostToDevice));
+        CCF_H2D(ds->tasks[nt - 1], tasks.data(), tasks.size() * sizeof(AdiTask));
     }
     DevSet& ref = *ds;
     sets[key] = std::move(ds);
@@ -271,7 +281,7 @@ void Ctx::check_adi_error(bool full) {
     std::vector<double> hist(4);
     CCF_CUDA(cudaMemcpy(hist.data(), ws.history + size_t(e[1] * g.nslots + e[2]) * 4, sizeof(double) * 4,
                         cudaMemcpyDeviceToHost));
-    CCF_CUDA(cudaMemset(ws.err, 0, sizeof(int) * 4));
+    CCF_CUDA(cudaMemsetAsync(ws.err, 0, sizeof(int) * 4, stream));
     const int s = e[2];
     const int l = full ? s : (s == p / 2 ? 0 : s + p / 2);
     char buf[64];

@@ -23,6 +23,15 @@ namespace ccf {
                                                                      " at " __FILE__ ":" + std::to_string(__LINE__)); \
     } while (0)
 
+// Synchronous host -> device copy. cudaMemcpy from pageable memory may return before the DMA lands,
+// and it runs on the legacy default stream, which the library's non-blocking streams do not wait
+// for: complete it before returning.
+#define CCF_H2D(dst, src, bytes)                                                       \
+    do {                                                                               \
+        CCF_CUDA(cudaMemcpy((dst), (src), (bytes), cudaMemcpyHostToDevice));           \
+        CCF_CUDA(cudaStreamSynchronize(cudaStreamLegacy));                             \
+    } while (0)
+
 // Device buffer (RAII).
 struct DBuf {
     double* p = nullptr;
@@ -57,8 +66,44 @@ struct Workspace {  // ADI round bookkeeping
     int cap_slots = 0;
 };
 
+// Mode sharding of the NS step over the GPUs of one node (csrc/shard.cu).
+// Every rank keeps full-extent tensors (same layout, same offsets on every rank) and computes the
+// half-spectrum slots [s_lo, s_hi) in every per-mode stage. The only exchange is the theta stage:
+// rank r transforms the radial rows [r_lo, r_hi) of all slots, reading each slot's (r,z)-values
+// straight from the owning rank's exchange buffer and storing the cross product back into it
+// (NVLink peer loads / stores at the same offset; no pack, no copy). Two rank barriers per step
+// (before and after the theta stage) order those accesses.
+constexpr int kMaxRanks = 8;
+constexpr int kShardHandleBytes = 128;  // include/ccf.h CCF_SHARD_HANDLE_BYTES
+constexpr int kExchangeTensors = 9;  // pipeline scratch 6..14: the six theta inputs and three outputs
+struct HostBarrier;                  // in-process barrier of linked contexts (shard.cu)
+struct Shard {
+    int rank = 0, world = 1;
+    int s_lo = 0, s_hi = 0;  // owned half-spectrum slots
+    int r_lo = 0, r_hi = 0;  // owned theta rows (r > 0 grid rows jr)
+    int sb[kMaxRanks + 1] = {}, rb[kMaxRanks + 1] = {};  // slot / row bounds of every rank
+    double* xbuf = nullptr;      // exchange allocation: kExchangeTensors tensors, then the barrier flags
+    unsigned* flags = nullptr;   // kMaxRanks arrival counters in xbuf, written by the peers
+    unsigned* epoch = nullptr;   // device barrier epoch (device-resident: CUDA-graph replay safe)
+    int* err = nullptr;          // barrier timeout flag
+    long rdelta[kMaxRanks] = {};             // doubles from xbuf to rank r's exchange buffer (as mapped here)
+    unsigned* peer_flags[kMaxRanks] = {};    // rank r's flag array (as mapped here)
+    void* ipc_open[kMaxRanks] = {};          // cudaIpcOpenMemHandle mappings to close
+    enum Mode { NONE = 0, DEVICE = 1, HOST = 2 } mode = NONE;
+    void (*host_fn)(void*) = nullptr;        // HOST mode: caller-provided rank barrier
+    void* host_user = nullptr;
+    std::shared_ptr<HostBarrier> local;      // HOST mode between linked contexts of one process
+    bool sharded() const { return world > 1; }
+    long slot_delta(int s) const {
+        int r = 0;
+        while (r + 1 < world && s >= sb[r + 1]) ++r;
+        return rdelta[r];
+    }
+};
+
 struct Ctx {
     int m, n, p, device, flags;
+    Shard sh;
     double tol;
     cudaStream_t stream = nullptr, own_stream = nullptr;
     Geo gh{}, gf{};  // half-spectrum and full-spectrum slot tables
@@ -115,6 +160,20 @@ struct Ctx {
     void store_values(const double* src, double* vals);
     void require_finite(const double* dptr, long n, const char* what);
     void sync();
+    // mode sharding (shard.cu)
+    void shard_init(int rank, int world);
+    void shard_sync();              // rank barrier on the stream (no-op unsharded)
+    void shard_check();             // synchronises; raises a barrier timeout
+    void shard_close();
+    void require_unsharded(const char* what) const;
 };
+
+// contiguous partition of count items over world ranks: rank r owns [bounds[r], bounds[r+1])
+void shard_bounds(int count, int world, int* bounds);
+// peer connection of sharded contexts (shard.cu)
+void shard_ipc_handle(Ctx& c, void* out);           // kShardHandleBytes: IPC handle + offset of the exchange buffer
+void shard_open_ipc(Ctx& c, const void* handles);   // world x kShardHandleBytes (own entry ignored); DEVICE barriers
+void shard_link_local(Ctx* const* cs, int world);   // ranks of one process on one device; HOST barriers
+void shard_set_host_barrier(Ctx& c, void (*fn)(void*), void* user);
 
 }  // namespace ccf

@@ -69,7 +69,7 @@ struct EigRhs {
     double* out[2];
     const double* const* rt;
     double factor;
-    int M, N, Np, nslots;
+    int M, N, Np, nslots, slo;  // slots [slo, slo + nslots)
     double* outp;              // optional: -out[0] .* rtp (the next step's Poisson RHS in eigen coordinates)
     const double* const* rtp;  // RT table of the Poisson set
     int* flag;                 // optional: set to 1 on a non-finite output (NaN guard, ptns.cpp:260-262)
@@ -116,7 +116,21 @@ struct ThetaCross {
     const double* in[6];
     double* out[3];
     const double2* tw;
+    // mode sharding (csrc/shard.cu): this launch covers rows row0 + blockIdx.y; slot s is read from
+    // and written to the exchange buffer of its owning rank q (sb[q] <= s < sb[q+1]), rdelta[q]
+    // doubles away from the local one (peer memory over NVLink); world == 1: local, delta 0
+    int row0, world;
+    int sb[9];
+    long rdelta[8];
 };
+// doubles from the local exchange tensors to those of the owner of slot s
+__device__ __forceinline__ long theta_slot_delta(const ThetaCross& t, int s) {
+    if (t.world <= 1) return 0;
+    int q = 0;
+#pragma unroll 1
+    while (q + 1 < t.world && s >= t.sb[q + 1]) ++q;
+    return t.rdelta[q];
+}
 __global__ void theta_cross_kernel(ThetaCross t);
 __global__ void theta_cross256_kernel(ThetaCross t);  // p = 256 register-FFT path
 size_t theta_cross256_smem();

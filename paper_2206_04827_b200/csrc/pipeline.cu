@@ -12,6 +12,7 @@
 
 namespace ccf {
 
+
 namespace {
 
 std::vector<double> cheb_points_double(int count) {  // proj/src/grid.cpp:16-26 (pinned endpoints)
@@ -32,7 +33,7 @@ long double cospi_frac(long a, long L) {
 
 void upload(DBuf& d, const std::vector<double>& h) {
     d.alloc(h.size());
-    CCF_CUDA(cudaMemcpy(d.p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CCF_H2D(d.p, h.data(), h.size() * sizeof(double));
 }
 
 unsigned blocks_for(long n, int t) { return unsigned((n + t - 1) / t); }
@@ -344,30 +345,30 @@ void GemmPlan::upload() {
         if (!tstart.empty()) CCF_CUDA(cudaMalloc(&dT, tstart.size() * sizeof(int)));
     }
     if (na) {
-        CCF_CUDA(cudaMemcpy(dA, A.data(), na * sizeof(void*), cudaMemcpyHostToDevice));
-        CCF_CUDA(cudaMemcpy(dB, B.data(), na * sizeof(void*), cudaMemcpyHostToDevice));
+        CCF_H2D(dA, A.data(), na * sizeof(void*));
+        CCF_H2D(dB, B.data(), na * sizeof(void*));
     }
-    if (!C.empty()) CCF_CUDA(cudaMemcpy(dC, C.data(), C.size() * sizeof(void*), cudaMemcpyHostToDevice));
-    if (!tstart.empty()) CCF_CUDA(cudaMemcpy(dT, tstart.data(), tstart.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (!C.empty()) CCF_H2D(dC, C.data(), C.size() * sizeof(void*));
+    if (!tstart.empty()) CCF_H2D(dT, tstart.data(), tstart.size() * sizeof(int));
     if (!Boff.empty()) {
         if (!dBoff) CCF_CUDA(cudaMalloc(&dBoff, Boff.size() * sizeof(long)));
-        CCF_CUDA(cudaMemcpy(dBoff, Boff.data(), Boff.size() * sizeof(long), cudaMemcpyHostToDevice));
+        CCF_H2D(dBoff, Boff.data(), Boff.size() * sizeof(long));
     }
     if (!Aoff.empty()) {
         if (!dAoff) CCF_CUDA(cudaMalloc(&dAoff, Aoff.size() * sizeof(long)));
-        CCF_CUDA(cudaMemcpy(dAoff, Aoff.data(), Aoff.size() * sizeof(long), cudaMemcpyHostToDevice));
+        CCF_H2D(dAoff, Aoff.data(), Aoff.size() * sizeof(long));
     }
     if (!Coff.empty()) {
         if (!dCoff) CCF_CUDA(cudaMalloc(&dCoff, Coff.size() * sizeof(long)));
-        CCF_CUDA(cudaMemcpy(dCoff, Coff.data(), Coff.size() * sizeof(long), cudaMemcpyHostToDevice));
+        CCF_H2D(dCoff, Coff.data(), Coff.size() * sizeof(long));
     }
     if (!DL.empty()) {
         if (!dDL) {
             CCF_CUDA(cudaMalloc(&dDL, nb * sizeof(void*)));
             CCF_CUDA(cudaMalloc(&dDR, nb * sizeof(void*)));
         }
-        CCF_CUDA(cudaMemcpy(dDL, DL.data(), nb * sizeof(void*), cudaMemcpyHostToDevice));
-        CCF_CUDA(cudaMemcpy(dDR, DR.data(), nb * sizeof(void*), cudaMemcpyHostToDevice));
+        CCF_H2D(dDL, DL.data(), nb * sizeof(void*));
+        CCF_H2D(dDR, DR.data(), nb * sizeof(void*));
     }
     // ---- TMA variant: one map per (operand allocation, leading dimension), box origins per term
     tma = false;
@@ -436,8 +437,8 @@ void GemmPlan::upload() {
                 CCF_CUDA(cudaMalloc(&dTA, hta.size() * sizeof(int)));
                 CCF_CUDA(cudaMalloc(&dTB, htb.size() * sizeof(int)));
             }
-            CCF_CUDA(cudaMemcpy(dTA, hta.data(), hta.size() * sizeof(int), cudaMemcpyHostToDevice));
-            CCF_CUDA(cudaMemcpy(dTB, htb.data(), htb.size() * sizeof(int), cudaMemcpyHostToDevice));
+            CCF_H2D(dTA, hta.data(), hta.size() * sizeof(int));
+            CCF_H2D(dTB, htb.data(), htb.size() * sizeof(int));
             tma = true;
         }
     }
@@ -545,6 +546,8 @@ Pipeline::Pipeline(Ctx& c_) : c(c_), tp(c_), T(c_.tensor_doubles(false)) {
 }
 
 double* Pipeline::scratch(int i) {
+    // mode sharding: the theta stage's inputs / outputs live in the peer-mapped exchange buffer
+    if (c.sh.xbuf && i >= 6 && i < 6 + kExchangeTensors) return c.sh.xbuf + size_t(i - 6) * size_t(T);
     while (int(scr_.size()) <= i) scr_.emplace_back();
     if (scr_[size_t(i)].n < size_t(T)) scr_[size_t(i)].alloc(size_t(T));
     return scr_[size_t(i)].p;
@@ -727,6 +730,13 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
     for (int i = 0; i < 6; ++i) t.in[i] = v6[i];
     for (int i = 0; i < 3; ++i) t.out[i] = a3[i];
     t.tw = reinterpret_cast<const double2*>(tp.tw.p);
+    // mode sharding: this rank's rows of every slot, each slot in its owner's exchange buffer
+    const Shard& sh = c.sh;
+    t.row0 = sh.r_lo;
+    t.world = sh.world;
+    for (int q = 0; q <= kMaxRanks; ++q) t.sb[q] = q <= sh.world ? sh.sb[q] : g.nslots;
+    for (int q = 0; q < kMaxRanks; ++q) t.rdelta[q] = sh.rdelta[q];
+    const unsigned rows = unsigned(sh.r_hi - sh.r_lo);
     if (!theta_attr_) {
         CCF_CUDA(cudaFuncSetAttribute(theta_cross_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CCF_CUDA(cudaFuncSetAttribute(theta_cross256_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -743,9 +753,11 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
         theta_generic_ = e && e[0] == '1';
         theta_attr_ = true;
     }
+    if (sh.sharded() && g.p == 256 && !theta_generic_ && !theta_w_)
+        throw Error(CONFIG_ERROR, "theta: the 16-thread variant (CCF_THETA_VARIANT=16) has no sharded form");
     if (g.p == 256 && !theta_generic_ && theta_w_) {
         const int np = 2 * theta_nq_;
-        const dim3 grid(unsigned((g.nh + np - 1) / np), unsigned(g.mh));
+        const dim3 grid(unsigned((g.nh + np - 1) / np), rows);
         if (theta_nq_ == 2)
             theta_cross256w_kernel<2><<<grid, 256, theta_cross256w_smem(2), c.stream>>>(t);
         else
@@ -756,7 +768,7 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
         theta_cross256_kernel<<<grid, theta_cross256_threads(), theta_cross256_smem(), c.stream>>>(t);
     } else {
         const size_t smem = size_t(3) * tj * g.p * sizeof(double2);
-        const dim3 grid(unsigned((g.nh + tj / 2 - 1) / (tj / 2)), unsigned(g.mh));
+        const dim3 grid(unsigned((g.nh + tj / 2 - 1) / (tj / 2)), rows);
         theta_cross_kernel<<<grid, 256, smem, c.stream>>>(t);
     }
     ++c.launches;
@@ -814,6 +826,7 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     ensure_composite();
     if (eig && comp_off_) throw Error(INTERNAL, "nonlinear: eigen-coordinate output needs the composite path");
     if (comp_off_) {
+        if (c.sh.sharded()) throw Error(CONFIG_ERROR, "nonlinear: the pencil path (CCF_NONLINEAR_PENCIL=1) has no sharded form");
         nonlinear_pencil(lam_v, gam_v, lam_w, gam_w, lam_n, gam_n);
         return;
     }
@@ -845,7 +858,7 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
                     if (alias && pr == 0 && x == 0) continue;
                     const double* src = x == 0 ? lam[pr] : gam[pr];
                     const double* mat = x == 2 ? tp.DzS.p : tp.Sz.p;
-                    for (int s = 0; s < g.nslots; ++s)
+                    for (int s = c.sh.s_lo; s < c.sh.s_hi; ++s)
                         for (int pl = 0; pl < 2; ++pl) {
                             const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
                             for (int po = 0; po < 2; ++po) {
@@ -874,7 +887,7 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     GemmPlan& rs = gemm(ptr_key(eigY ? "nrsY" : "nrs", 4, keyp, keyp, ycls), fresh);  // outputs: scratch
     if (fresh) {
         for (int pr = 0; pr < 2; ++pr)
-            for (int s = 0; s < g.nslots; ++s)
+            for (int s = c.sh.s_lo; s < c.sh.s_hi; ++s)
                 for (int o = 0; o < 6; ++o) {
                     rs.tstart.push_back(int(rs.A.size()));
                     for (const CompositeTerm& ct : synth_.terms[size_t(s)]) {
@@ -897,7 +910,9 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     c.gemm_flops += rs.flops();
     c.launches += 2;
     c.mark("X1_rz_synthesis");
+    c.shard_sync();  // every owner's values written, every owner done with the previous step's outputs
     theta_cross(val, av);
+    c.shard_sync();  // every rank's rows of the cross product stored
     c.mark("X2_theta_cross");
     // ---- z analysis of a_r, a_t, a_z and (derivative_z folded in) dz a_r, dz a_t
     // eigen mode (eig != nullptr): the z analysis carries PR of the shared modal basis, Y_x half k0 =
@@ -912,7 +927,7 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
             const double* src = av[x < 3 ? x : x - 3];
             const double* mat = eig ? (x >= 3 ? eig_ADzP_.p : eig_AzP_.p) : (x >= 3 ? tp.ADz.p : tp.Az.p);
             const long mstride = eig ? long(g.nh) * Np : long(g.nh) * g.nh;
-            for (int s = 0; s < g.nslots; ++s)
+            for (int s = c.sh.s_lo; s < c.sh.s_hi; ++s)
                 for (int pl = 0; pl < 2; ++pl) {
                     const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
                     for (int po = 0; po < 2; ++po) {
@@ -940,7 +955,7 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     // eigen mode: blocks PL_P A_t (M x mh) and output in the eigen layout (M x 2 Np per slot, plane)
     GemmPlan& ra = gemm(ptr_key("nra", 2, okeyp, okeyp, ecls), fresh);
     if (fresh) {
-        for (int s = 0; s < g.nslots; ++s)
+        for (int s = c.sh.s_lo; s < c.sh.s_hi; ++s)
             for (int o = 0; o < 4; ++o) {
                 ra.tstart.push_back(int(ra.A.size()));
                 for (const CompositeTerm& ct : anal_.terms[size_t(s)]) {
@@ -1043,7 +1058,7 @@ bool Pipeline::modal_solve_from_z(DevSet& set, double w, double* out) {
                 }
         const double** d = nullptr;
         CCF_CUDA(cudaMalloc(&d, rt.size() * sizeof(void*)));
-        CCF_CUDA(cudaMemcpy(d, rt.data(), rt.size() * sizeof(void*), cudaMemcpyHostToDevice));
+        CCF_H2D(d, rt.data(), rt.size() * sizeof(void*));
         it = zrt_.emplace(&set, d).first;
     }
     zscale_kernel<<<ntask, 256, 0, c.stream>>>(dZ_.p, long(per), it->second, M, N, Np, w);
@@ -1150,7 +1165,7 @@ void Pipeline::modal_solve(DevSet& set, bool full, int ntensor, const double* co
                         }
             FdTask* d = nullptr;
             CCF_CUDA(cudaMalloc(&d, tv.size() * sizeof(FdTask)));
-            CCF_CUDA(cudaMemcpy(d, tv.data(), tv.size() * sizeof(FdTask), cudaMemcpyHostToDevice));
+            CCF_H2D(d, tv.data(), tv.size() * sizeof(FdTask));
             it = fdtasks_.emplace(key, std::make_pair(d, int(tv.size()))).first;
         }
         if (rhs_mark) c.mark(rhs_mark);
@@ -1260,8 +1275,8 @@ __global__ void __launch_bounds__(128) eigen_rhs_kernel(EigRhs a) {
         const int t = int(row / (long(a.nslots) * 2 * a.M));
         const long rr = row - long(t) * a.nslots * 2 * a.M;  // (s * 2 + pl) * M + i
         const int i = int(rr % a.M);
-        const int s = int(rr / (2L * a.M));
-        const long base = rr * ld;
+        const int s = a.slo + int(rr / (2L * a.M));
+        const long base = (rr + long(a.slo) * 2 * a.M) * ld;
         for (int pc = threadIdx.x; pc < pairs; pc += blockDim.x) {
             const int col = 2 * pc;
             const int k0 = col >= a.Np ? 1 : 0, j = col - k0 * a.Np;
@@ -1384,7 +1399,7 @@ void Pipeline::eigen_ysynth(int ntensor, const double* const* z, double* const* 
     GemmPlan& ys = gemm(ptr_key("eys", 6, okey, okey, ci6), fresh);
     if (fresh) {
         for (int t = 0; t < ntensor; ++t)
-            for (int s = 0; s < g.nslots; ++s)
+            for (int s = c.sh.s_lo; s < c.sh.s_hi; ++s)
                 for (int k0 = 0; k0 < 2; ++k0)
                     for (int pl = 0; pl < 2; ++pl) {
                         const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride;
@@ -1425,7 +1440,7 @@ const double* const* Pipeline::eig_rt(DevSet& set) {
         }
     const double** d = nullptr;
     CCF_CUDA(cudaMalloc(&d, rt.size() * sizeof(void*)));
-    CCF_CUDA(cudaMemcpy(d, rt.data(), rt.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    CCF_H2D(d, rt.data(), rt.size() * sizeof(void*));
     eig_rt_.emplace(&set, d);
     return d;
 }
@@ -1453,7 +1468,8 @@ void Pipeline::eigen_rhs(DevSet& set, int ntensor, const double* const* s0, cons
     a.M = c.M;
     a.N = c.N;
     a.Np = c.N + (c.N & 1);
-    a.nslots = c.gh.nslots;
+    a.slo = c.sh.s_lo;  // mode sharding: the owned slots only
+    a.nslots = c.sh.s_hi - c.sh.s_lo;
     const long rows = long(a.nslots) * 2 * a.M * ntensor;
     const unsigned grid = unsigned(std::min<long>(rows, 148L * 16));
     switch (nsrc) {
@@ -1491,7 +1507,7 @@ void Pipeline::eigen_back(DevSet& set, int ntensor, const double* z0, const doub
         const double* dg = set.dg;
         long task = 0;
         for (int t = 0; t < ntensor; ++t)
-            for (int s = 0; s < g.nslots; ++s)
+            for (int s = c.sh.s_lo; s < c.sh.s_hi; ++s)
                 for (int k0 = 0; k0 < 2; ++k0)
                     for (int pl = 0; pl < 2; ++pl, ++task) {
                         const long PLo = set.host.dg_left[size_t(s)], QLo = PLo + long(M) * mh;
@@ -1532,7 +1548,7 @@ void Pipeline::to_eigen(DevSet& pset, const double* u, double* z) {
     }
     GemmPlan t1, t2;
     long task = 0;
-    for (int s = 0; s < g.nslots; ++s)
+    for (int s = c.sh.s_lo; s < c.sh.s_hi; ++s)
         for (int k0 = 0; k0 < 2; ++k0)
             for (int pl = 0; pl < 2; ++pl, ++task) {
                 double* T1 = dT1_.p + size_t(task) * per;
@@ -1915,7 +1931,8 @@ void NSState::step_once() {
     const int eo = disable_nonlinear ? 0 : std::min(b, ncnt);
     const bool steady = (b == order) && (disable_nonlinear || ncount == order);
     const int key = head * 5 + nhead;
-    if (use_graphs && steady && steps >= order + 1) {
+    // host-mode rank barriers synchronise inside the step: no graph capture
+    if (use_graphs && steady && steps >= order + 1 && c.sh.mode != Shard::HOST) {
         if (!graphs[key]) {
             cudaGraph_t g;
             const long l0 = c.launches;

@@ -560,7 +560,7 @@ __global__ void theta_cross_kernel(ThetaCross t) {
     const Geo& g = t.g;
     const int P = g.p, logP = t.logp, S = g.nslots;
     const int TJ = t.tj;                 // points per CTA (even): point 2i -> +z, 2i+1 -> -z
-    const int jr = blockIdx.y;           // r > 0 grid row
+    const int jr = t.row0 + blockIdx.y;  // r > 0 grid row
     const int q0 = blockIdx.x * (TJ / 2);  // first position of the tile
     const int ntj = min(TJ / 2, g.nh - q0);
     double2* Z = sd;                       // 3 * TJ arrays of P (packed pairs)
@@ -586,7 +586,7 @@ __global__ void theta_cross_kernel(ThetaCross t) {
             }
             const int s = (w == -P / 2) ? P / 2 : w;
             const double sg = ((w & 1) ? -1.0 : 1.0);
-            const long off = long(s) * g.slot_stride + long(jr) * g.n + q0 + pos;
+            const long off = long(s) * g.slot_stride + long(jr) * g.n + q0 + pos + theta_slot_delta(t, s);
             const long ps = g.plane_stride, oo = g.nh;
             double2 xa, xb;
             {
@@ -658,10 +658,12 @@ __global__ void theta_cross_kernel(ThetaCross t) {
             xv[h] = pl ? X.y : X.x;
         }
         const double sg = ((w & 1) ? -1.0 : 1.0) * invp * 0.5;
-        const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride + long(jr) * g.n + q0 + pos;
+        const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride + long(jr) * g.n + q0 + pos +
+                         theta_slot_delta(t, s);
         t.out[f][off] = sg * (xv[0] + xv[1]);         // E' = (f(+z) + f(-z)) / 2
         t.out[f][off + g.nh] = sg * (xv[0] - xv[1]);  // O' = (f(+z) - f(-z)) / 2
     }
+    if (t.world > 1) __threadfence_system();  // peer stores performed before the rank barrier
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -938,7 +940,7 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
     double2* twf = sd + kPts * 2 * kTWArr;  // twf[16 k1 + n2] = e^{-2 pi i n2 k1 / 256}
     const Geo& g = t.g;
     const int S = g.nslots;  // 129
-    const int jr = blockIdx.y;
+    const int jr = t.row0 + blockIdx.y;
     const int i0 = blockIdx.x * (2 * NQ);
     const int npos = min(2 * NQ, g.nh - i0);
     // 16-byte global accesses when every stride is even (per pair: both positions present)
@@ -966,7 +968,7 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
         const int nq = min(2, npos - 2 * q);
         if (nq <= 0) return;
         const bool vec = even && nq == 2;
-        const long off = long(s) * g.slot_stride + long(jr) * g.n + i0 + 2 * q;
+        const long off = long(s) * g.slot_stride + long(jr) * g.n + i0 + 2 * q + theta_slot_delta(t, s);
         const double* __restrict__ fa = t.in[2 * pr] + off;
         const double* __restrict__ fb = t.in[2 * pr + 1] + off;
         if (vec) {  // both z positions: 16-byte loads
@@ -1106,7 +1108,7 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
         const int tt = s, tm = (256 - s) & 255;
         const double sg = ((s & 1) ? -1.0 : 1.0) * (0.5 / 256.0);
         const int arr = f < 2 ? 0 : 1;
-        const long off = long(s) * g.slot_stride + long(jr) * g.n + i0 + 2 * q;
+        const long off = long(s) * g.slot_stride + long(jr) * g.n + i0 + 2 * q + theta_slot_delta(t, s);
         double* o = t.out[f] + off;
         double ov[4][2];
 #pragma unroll
@@ -1139,6 +1141,7 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
             for (int u = 0; u < 4; ++u) dst[u][0] = ov[u][0];
         }
     }
+    if (t.world > 1) __threadfence_system();  // peer stores performed before the rank barrier
 }
 
 template __global__ void theta_cross256w_kernel<1>(ThetaCross);

@@ -178,6 +178,11 @@ def main():
     ap.add_argument("--size", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--one-gpu-test", action="store_true",
+                    help="plumbing test of the N>1 path on ONE GPU: every rank on device 0, gloo, host barriers "
+                         "(no device-side waiting between ranks); the numbers are not a measurement")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: one independent replica per GPU instead of the mode-sharded step")
     args = ap.parse_args()
     cfg = CONFIGS[args.size]
     rank = int(os.environ.get("RANK", "0"))
@@ -190,29 +195,58 @@ def main():
 
     import torch
     import paper_2206_04827_b200 as P
+    if args.one_gpu_test:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
+    red = "cuda"  # device of the max-over-ranks reductions
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.one_gpu_test:
+            dist.init_process_group("gloo")
+            red = "cpu"
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     m, n, p = cfg["m"], cfg["n"], cfg["p"]
     peaks = load_peaks()
-    ctx = P.Context(m, n, p, device=local)
     stream = torch.cuda.Stream()
-    ctx.set_stream(stream.cuda_stream)
     t_setup = time.time()
-    wl, wg, vmax = initial_vorticity(ctx, cfg, cfg["vmax"])
-    st = P.NSStepper(ctx, wl, wg, reynolds=cfg["reynolds"], h=cfg["h"], order=4)
-    if args.no_graphs:
-        st.set_graphs(False)
-    t_setup = time.time() - t_setup
     # warm-up: at least the BDF ramp (steps 0-3, eager) plus one step in each of the 5 ring phases once
     # graphs are used (steps 5-9, each captures its phase's graph), so neither the ramp nor a graph
     # capture lands in the timed region whatever W the caller passes
     W = max(3, args.warmup, 10)
-    st.step(W)
-    torch.cuda.synchronize()
+    # N > 1: the mode-sharded step (csrc/shard.cu): rank r owns a contiguous range of Fourier slots in
+    # every per-mode stage and a range of radial rows in the theta stage, reading / writing the other
+    # slots in their owners' exchange buffers over NVLink (CUDA IPC), device-side rank barriers
+    sharded = world > 1 and not args.replicas
+    fallback = None
+    while True:
+        ctx = P.Context(m, n, p, device=local)
+        ctx.set_stream(stream.cuda_stream)
+        wl, wg, vmax = initial_vorticity(ctx, cfg, cfg["vmax"])  # API calls: before sharding the context
+        try:
+            if sharded:
+                from paper_2206_04827_b200 import shard as S
+                ctx.shard(rank, world)
+                S.connect(ctx)
+                if args.one_gpu_test:
+                    ctx.set_host_barrier(dist.barrier)
+            st = P.NSStepper(ctx, wl, wg, reynolds=cfg["reynolds"], h=cfg["h"], order=4)
+            if args.no_graphs:
+                st.set_graphs(False)
+            st.step(W)
+            torch.cuda.synchronize()
+            break
+        except P.CCFError as e:  # sharded path unavailable on this node: measure replicas, say so
+            if not sharded:
+                raise
+            fallback = f"mode-sharded step failed ({e}); replicas measured instead"
+            print(f"[bench] rank {rank}: {fallback}", file=sys.stderr, flush=True)
+            sharded = False
+            ctx.close()
+            dist.barrier()
+    t_setup = time.time() - t_setup
 
     # ---- timed region: K steps, CUDA events on the library's stream, max over ranks
     K = args.steps
@@ -234,11 +268,12 @@ def main():
     clk = clocks.stop()
     stats = ctx.stats()
     if dist:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=red)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / K
-    value = world * K / (ms / 1e3)
+    jobs = 1 if sharded else world  # sharded: one field over all GPUs; replicas: one field per GPU
+    value = jobs * K / (ms / 1e3)
 
     # ---- per-stage profile of one extra eager step (CUDA events between stages)
     ctx.reset_stats()
@@ -256,7 +291,12 @@ def main():
     bw = peaks["hbm_gbs"] * 1e9
     pdm = peaks["fp64_dmma_tflops"] * 1e12
     B_other = (9 + 2 * (4 + 4 + 1) + 1 + 1) * tensor_bytes
-    T_roof = F_gemm / pdm + B_other / bw
+    nvl = 0.0
+    if sharded:  # per-rank share of the HBM passes + the theta exchange over NVLink (900 GB/s per direction)
+        from paper_2206_04827_b200 import shard as S
+        B_other /= world
+        nvl = S.exchange_bytes_per_rank(m, n, p, world) / 900e9
+    T_roof = F_gemm / pdm + B_other / bw + nvl
     B_total = B_other
 
     # ---- end-to-end through the C-ABI with pinned host buffers: create (H2D) -> KE steps -> read back (D2H).
@@ -276,7 +316,7 @@ def main():
     st2.omega(ol.numpy(), og.numpy())
     e2e_s = time.perf_counter() - t0
     if dist:
-        t = torch.tensor([e2e_s], device="cuda")
+        t = torch.tensor([e2e_s], device=red)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     io_bytes = hl.numel() * 16 * 2
@@ -292,15 +332,17 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+            "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["workload"], "m": m, "n": n, "p": p, "reynolds": cfg["reynolds"],
                        "h": cfg["h"], "bdf_order": 4, "init_decay": cfg["decay"], "seed": cfg["seed"],
-                       "init_max_speed": cfg["vmax"], "init_vmax_scaled_from": vmax, "parallelism": "replica" if world > 1 else "single",
+                       "init_max_speed": cfg["vmax"], "init_vmax_scaled_from": vmax,
+                       "parallelism": (f"modes{world}" if sharded else ("replica" if world > 1 else "single")),
                        "l2": "no flush: step working set ~3 GB >> 126 MB L2",
                        "cuda_graphs": not args.no_graphs},
             "clocks": clk,
-            "e2e": {"value": world * KE / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": io_bytes / KE,
+            "e2e": {"value": jobs * KE / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": io_bytes / KE,
                     "d2h_bytes_per_step": io_bytes / KE + status_bytes, "steps": KE,
                     "what": "fresh NSStepper from pinned host omega (H2D) -> KE single-step C-ABI calls incl. the "
                             "BDF 1->4 ramp and graph captures, each reading back the step status (non-finite "
@@ -308,8 +350,8 @@ def main():
                             "over KE"},
             "gpu_launches": stats["kernel_launches"],
             "roofline": {"bound": "tensor",
-                         "kernel": "dgemm_pipe_kernel (FP64 DMMA m8n8k4, cp.async pipeline): z transforms, composite "
-                                   "radial operators and the eigen-coordinate back transforms",
+                         "kernel": "dgemm_tma_kernel (FP64 DMMA m8n8k4, TMA 128B-swizzled operand ring): z transforms, "
+                                   "composite radial operators and the eigen-coordinate back transforms",
                          "achieved": gemm_tflops, "peak": peaks["fp64_dmma_tflops"], "unit": "TFLOP/s",
                          "frac": (gemm_tflops / peaks["fp64_dmma_tflops"]) if gemm_tflops else None,
                          "traffic": gemm_traffic(),
@@ -320,9 +362,16 @@ def main():
                          "flop_model": "2 M N K per product term of every batched GEMM launched in one step"},
             "step_roofline": {"T_roof_ms": T_roof * 1e3, "achieved": T_roof / (ms_step * 1e-3),
                               "gemm_bound_ms": F_gemm / pdm * 1e3, "hbm_bound_ms": B_other / bw * 1e3,
+                              "nvlink_bound_ms": nvl * 1e3,
                               "hbm_peak_gbs": peaks["hbm_gbs"], "hbm_source": peaks["hbm_source"],
                               "note": "GEMM stages at the DMMA peak + theta and RHS-combination passes at HBM peak"},
             "stage_ms": stages,
+            "sharding": ({"mode": "fourier slots x theta rows, NVLink peer exchange (CUDA IPC), " +
+                                  ("host barriers, ONE-GPU PLUMBING TEST (not a measurement)" if args.one_gpu_test
+                                   else "device barriers"),
+                          "slots_rank0": ctx.shard_info()["slot_hi"] - ctx.shard_info()["slot_lo"],
+                          "exchange_bytes_per_rank": S.exchange_bytes_per_rank(m, n, p, world)} if sharded else
+                         ({"mode": "replicas", "note": fallback} if world > 1 else None)),
             "adi_iterations_per_step": pstats["adi_iterations"],
             "setup_s": t_setup,
         }

@@ -24,6 +24,8 @@
 #ifndef CCF_H_
 #define CCF_H_
 
+#include <stddef.h>
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -37,6 +39,7 @@ typedef enum ccf_status {
     CCF_NOT_INCOMPRESSIBLE = 5,    /* cylspec::NotIncompressibleError{divergence} */
     CCF_NUMERICAL_ERROR = 6,       /* cylspec::NumericalError */
     CCF_CUDA_ERROR = 7,            /* device / driver failure (no reference analogue) */
+    CCF_FIELDFILE_ERROR = 8,       /* cylspec::FieldFileError (io.hpp:17-19) */
     CCF_INTERNAL_ERROR = 9
 } ccf_status;
 
@@ -128,6 +131,22 @@ ccf_status ccf_shard_link_local(ccf_ctx* const* ctxs, int world);
 /* Replace the device barrier by stream synchronisation + fn(user) (a host barrier across ranks);
  * fn == NULL restores the device barrier. */
 ccf_status ccf_shard_set_host_barrier(ccf_ctx* ctx, void (*fn)(void*), void* user);
+
+/* CCF1 FieldFile I/O (io.hpp:11-28, io.cpp:12-109): "CCF1" | version u32 = 1 | kind u8 (0 real grid
+ * values, m*n*p doubles; 1 complex coefficients, 2*m*n*p doubles interleaved) | m, n, p u32 |
+ * payload f64 LE in (l, k, j) order | CRC-32/IEEE of the payload bytes. Payloads may be host or
+ * device memory; device payloads are checksummed on the GPU (only the file bytes cross PCIe).
+ * Errors (FieldFileError: bad magic, unsupported version, unknown kind, truncation, CRC mismatch,
+ * open/write failures) return CCF_FIELDFILE_ERROR with the reference's message in ccf_create_error. */
+ccf_status ccf_write_field(const char* path, int kind, int m, int n, int p, const double* payload);
+ccf_status ccf_read_field_header(const char* path, int* kind, int* m, int* n, int* p);
+/* payload: cap doubles of host or device memory (>= the file's count) */
+ccf_status ccf_read_field(const char* path, int* kind, int* m, int* n, int* p, double* payload, size_t cap);
+/* crc32_ieee (io.cpp:12-25) of host or device bytes (device: on the GPU) */
+ccf_status ccf_crc32(const void* data, size_t len, unsigned* crc);
+/* Snapshot of the stepper's omega (lambda, gamma) as kind-1 FieldFiles, written from the device
+ * state (cylspec_main.cpp:111-113 writes snapshots with write_field); NULL path skips one. */
+ccf_status ccf_ns_write_omega(ccf_ns_state* st, const char* lam_path, const char* gam_path);
 
 /* Details of the last error on this context (thread-compatible, not thread-safe).
  * kind = ccf_status; slice = Fourier slice of a failed modal solve or -1;

@@ -23,7 +23,8 @@ LIB_PATH = os.path.join(_HERE, "lib", "libccf.so")
 # Status codes mirror proj/include/cylspec/errors.hpp:10-40 (include/ccf.h).
 CCF_OK = 0
 STATUS_NAMES = {1: "DomainError", 2: "ConfigError", 3: "SingularOperatorError", 4: "NonConvergenceError",
-                5: "NotIncompressibleError", 6: "NumericalError", 7: "CudaError", 9: "InternalError"}
+                5: "NotIncompressibleError", 6: "NumericalError", 7: "CudaError", 8: "FieldFileError",
+                9: "InternalError"}
 
 
 class CCFError(RuntimeError):
@@ -66,8 +67,14 @@ class CudaError(CCFError):
     status = 7
 
 
+class FieldFileError(CCFError):
+    """cylspec::FieldFileError (proj/include/cylspec/io.hpp:17-19)."""
+
+    status = 8
+
+
 _ERR = {c.status: c for c in (DomainError, ConfigError, SingularOperatorError, NonConvergenceError,
-                              NotIncompressibleError, NumericalError, CudaError)}
+                              NotIncompressibleError, NumericalError, CudaError, FieldFileError)}
 
 # Every extern "C" symbol include/ccf.h declares (checked by the CPU test suite).
 EXPORTS = ["ccf_ctx_create", "ccf_ctx_destroy", "ccf_ctx_set_stream", "ccf_ctx_synchronize", "ccf_analyze",
@@ -78,7 +85,8 @@ EXPORTS = ["ccf_ctx_create", "ccf_ctx_destroy", "ccf_ctx_set_stream", "ccf_ctx_s
            "ccf_ns_profile_step", "ccf_ns_set_graphs", "ccf_ns_launches_per_step", "ccf_plan_host",
            "ccf_create_error", "ccf_adi_last_rounds", "ccf_adi_keep_history", "ccf_get_gemm_flops",
            "ccf_diag_host_check", "ccf_shard_init", "ccf_shard_partition", "ccf_shard_info", "ccf_shard_ipc_handle",
-           "ccf_shard_open_ipc", "ccf_shard_link_local", "ccf_shard_set_host_barrier"]
+           "ccf_shard_open_ipc", "ccf_shard_link_local", "ccf_shard_set_host_barrier", "ccf_write_field",
+           "ccf_read_field_header", "ccf_read_field", "ccf_crc32", "ccf_ns_write_omega"]
 
 HOST_BARRIER_FN = C.CFUNCTYPE(None, C.c_void_p)
 SHARD_HANDLE_BYTES = 128  # include/ccf.h CCF_SHARD_HANDLE_BYTES
@@ -152,6 +160,11 @@ def lib():
         L.ccf_shard_open_ipc.argtypes = [vp, C.c_char_p]
         L.ccf_shard_link_local.argtypes = [C.POINTER(vp), C.c_int]
         L.ccf_shard_set_host_barrier.argtypes = [vp, HOST_BARRIER_FN, vp]
+        L.ccf_write_field.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, vp]
+        L.ccf_read_field_header.argtypes = [C.c_char_p, ip, ip, ip, ip]
+        L.ccf_read_field.argtypes = [C.c_char_p, ip, ip, ip, ip, vp, C.c_size_t]
+        L.ccf_crc32.argtypes = [vp, C.c_size_t, C.POINTER(C.c_uint)]
+        L.ccf_ns_write_omega.argtypes = [vp, C.c_char_p, C.c_char_p]
         _lib = L
     return _lib
 
@@ -409,6 +422,69 @@ def plan_host(m, n, w, scale=1.0, poisson=True, tol=1e-12, q2_endpoint_pad=False
                 u=u[:J].copy(), v=v[:J].copy())
 
 
+# ---- CCF1 FieldFile I/O (proj/include/cylspec/io.hpp:11-28, proj/src/io.cpp:12-109)
+def _free_check(st):
+    if st != 0:
+        raise _ERR.get(st, CCFError)(lib().ccf_create_error().decode())
+
+
+def crc32(data) -> int:
+    """crc32_ieee of a bytes-like host buffer, numpy array or torch CUDA tensor (on the GPU)."""
+    if hasattr(data, "data_ptr"):
+        ptr, n = data.data_ptr(), data.numel() * data.element_size()
+    else:
+        a = np.ascontiguousarray(np.frombuffer(data, np.uint8) if isinstance(data, (bytes, bytearray)) else data)
+        ptr, n = a.ctypes.data, a.nbytes
+    out = C.c_uint()
+    _free_check(lib().ccf_crc32(C.c_void_p(ptr), n, C.byref(out)))
+    return out.value
+
+
+def write_field(path, field, kind=None):
+    """write_field (io.cpp:62-74): complex (p, n, m) coefficients -> kind 1, real grid values -> kind 0.
+    field may be a numpy array or a torch CUDA tensor (checksummed on the GPU)."""
+    if hasattr(field, "data_ptr"):
+        import torch
+        cplx = field.is_complex()
+        shape = tuple(field.shape)
+        t = field.contiguous()
+        ptr = t.data_ptr()
+        keep = t
+        if kind is None:
+            kind = 1 if cplx else 0
+        del torch
+    else:
+        a = np.ascontiguousarray(field)
+        cplx = np.iscomplexobj(a)
+        a = a.astype(np.complex128 if cplx else np.float64, copy=False)
+        shape, ptr, keep = a.shape, a.ctypes.data, a
+        if kind is None:
+            kind = 1 if cplx else 0
+    p, n, m = shape[-3:]
+    _free_check(lib().ccf_write_field(os.fsencode(path), int(kind), int(m), int(n), int(p), C.c_void_p(ptr)))
+    del keep
+
+
+def read_field_header(path):
+    v = [C.c_int() for _ in range(4)]
+    _free_check(lib().ccf_read_field_header(os.fsencode(path), *[C.byref(x) for x in v]))
+    return dict(zip(("kind", "m", "n", "p"), (x.value for x in v)))
+
+
+def read_field(path, out=None):
+    """read_field (io.cpp:76-109) -> numpy (complex (p, n, m) for kind 1, real for kind 0), or into
+    `out` (numpy or torch CUDA tensor of matching size; CRC verified on the GPU for device output)."""
+    h = read_field_header(path)
+    count = h["m"] * h["n"] * h["p"]
+    if out is None:
+        out = np.zeros((h["p"], h["n"], h["m"]), np.complex128 if h["kind"] == 1 else np.float64)
+    cap = (out.numel() * out.element_size() if hasattr(out, "data_ptr") else out.nbytes) // 8
+    v = [C.c_int() for _ in range(4)]
+    _free_check(lib().ccf_read_field(os.fsencode(path), *[C.byref(x) for x in v], _addr(out), cap))
+    assert cap >= count * (2 if h["kind"] == 1 else 1)
+    return out
+
+
 class NSStepper:
     """proj/include/cylspec/ptns.hpp:104-127 NSStepper on the device (ramp bootstrap)."""
 
@@ -430,6 +506,11 @@ class NSStepper:
         self.ctx._check(lib().ccf_ns_get_omega(self.h, _addr(lam), _addr(gam), C.byref(t), C.byref(s)))
         self.time, self.steps_taken = t.value, s.value
         return lam, gam
+
+    def write_omega(self, lam_path, gam_path):
+        """Snapshot omega (lambda, gamma) as kind-1 CCF1 files straight from the device state."""
+        self.ctx._check(lib().ccf_ns_write_omega(self.h, os.fsencode(lam_path) if lam_path else None,
+                                                 os.fsencode(gam_path) if gam_path else None))
 
     def set_graphs(self, enable: bool):
         lib().ccf_ns_set_graphs(self.h, int(bool(enable)))

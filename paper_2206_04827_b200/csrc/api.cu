@@ -702,3 +702,96 @@ ccf_status ccf_plan_host(int m, int n, int w, double scale, int poisson, double 
     }
 }
 }  // extern "C"
+
+// ---- CCF1 FieldFile I/O (proj/include/cylspec/io.hpp:11-28, proj/src/io.cpp:12-109)
+namespace {
+template <class F>
+ccf_status guard_free(F&& f) {  // context-free entry points: message via ccf_create_error()
+    try {
+        f();
+        return CCF_OK;
+    } catch (const Error& e) {
+        g_create_err = e.what();
+        return ccf_status(e.status);
+    } catch (const std::exception& e) {
+        g_create_err = e.what();
+        return CCF_INTERNAL_ERROR;
+    }
+}
+bool device_ptr(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+}  // namespace
+
+ccf_status ccf_crc32(const void* data, size_t len, unsigned* crc) {
+    return guard_free([&] {
+        if (len && device_ptr(data)) {
+            CCF_CUDA(cudaDeviceSynchronize());
+            if (len % 8 == 0 && reinterpret_cast<uintptr_t>(data) % 8 == 0) {
+                *crc = ccf::crc32_device(data, len, nullptr);
+                return;
+            }
+            std::vector<uint8_t> h(len);
+            CCF_CUDA(cudaMemcpy(h.data(), data, len, cudaMemcpyDeviceToHost));
+            *crc = ccf::crc32_host(h.data(), len);
+            return;
+        }
+        *crc = ccf::crc32_host(static_cast<const uint8_t*>(data), len);
+    });
+}
+
+ccf_status ccf_write_field(const char* path, int kind, int m, int n, int p, const double* payload) {
+    return guard_free([&] {
+        if (m < 4 || n < 4) throw Error(ccf::DOMAIN_ERROR, "GridSpec: m and n must be at least 4");
+        if (p < 2 || p % 2 != 0) throw Error(ccf::DOMAIN_ERROR, "GridSpec: p must be even and at least 2");
+        const bool dev = device_ptr(payload);
+        if (dev) {
+            int d = 0;
+            cudaPointerAttributes a{};
+            CCF_CUDA(cudaPointerGetAttributes(&a, payload));
+            d = a.device;
+            CCF_CUDA(cudaSetDevice(d));
+            CCF_CUDA(cudaDeviceSynchronize());
+        }
+        ccf::write_field_file(path, kind, m, n, p, payload, dev, nullptr);
+    });
+}
+
+ccf_status ccf_read_field_header(const char* path, int* kind, int* m, int* n, int* p) {
+    return guard_free([&] { ccf::read_field_header(path, *kind, *m, *n, *p); });
+}
+
+ccf_status ccf_read_field(const char* path, int* kind, int* m, int* n, int* p, double* payload, size_t cap) {
+    return guard_free([&] {
+        const bool dev = device_ptr(payload);
+        if (dev) {
+            cudaPointerAttributes a{};
+            CCF_CUDA(cudaPointerGetAttributes(&a, payload));
+            CCF_CUDA(cudaSetDevice(a.device));
+            CCF_CUDA(cudaDeviceSynchronize());
+        }
+        ccf::read_field_file(path, *kind, *m, *n, *p, payload, cap, dev, nullptr);
+    });
+}
+
+ccf_status ccf_ns_write_omega(ccf_ns_state* st, const char* lam_path, const char* gam_path) {
+    if (!st) return CCF_INTERNAL_ERROR;
+    return guard(st->ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_ns_write_omega");
+        st->st.omega_coeff();
+        const size_t nref = size_t(2) * c.m * c.n * c.p;
+        ccf::DBuf ref(nref);
+        const char* paths[2] = {lam_path, gam_path};
+        const double* src[2] = {st->st.lam[st->st.head].p, st->st.gam[st->st.head].p};
+        for (int i = 0; i < 2; ++i) {
+            if (!paths[i]) continue;
+            c.store_coeff(src[i], ref.p, false, 0, i);  // reference layout, on the device
+            ccf::write_field_file(paths[i], 1, c.m, c.n, c.p, ref.p, true, c.stream);
+        }
+    });
+}

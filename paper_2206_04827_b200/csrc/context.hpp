@@ -168,6 +168,14 @@ struct Ctx {
     void require_unsharded(const char* what) const;
 };
 
+// CCF1 FieldFile I/O (fieldio.cu, proj/src/io.cpp:12-109)
+uint32_t crc32_host(const uint8_t* data, size_t len);
+uint32_t crc32_device(const void* dptr, size_t nbytes, cudaStream_t stream);
+void write_field_file(const std::string& path, int kind, int m, int n, int p, const double* payload, bool device,
+                      cudaStream_t stream);
+void read_field_header(const std::string& path, int& kind, int& m, int& n, int& p);
+void read_field_file(const std::string& path, int& kind, int& m, int& n, int& p, double* out, size_t cap, bool device,
+                     cudaStream_t stream);
 // contiguous partition of count items over world ranks: rank r owns [bounds[r], bounds[r+1])
 void shard_bounds(int count, int world, int* bounds);
 // peer connection of sharded contexts (shard.cu)

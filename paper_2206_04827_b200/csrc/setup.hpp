@@ -29,7 +29,7 @@ struct Error : std::runtime_error {
     Error(int st, const std::string& w) : std::runtime_error(w), status(st) {}
 };
 enum Status { OK = 0, DOMAIN_ERROR = 1, CONFIG_ERROR = 2, SINGULAR = 3, NON_CONVERGENCE = 4, NOT_INCOMPRESSIBLE = 5,
-              NUMERICAL = 6, CUDA_ERR = 7, INTERNAL = 9 };
+              NUMERICAL = 6, CUDA_ERR = 7, FIELDFILE_ERR = 8, INTERNAL = 9 };
 
 // Dense row-major square/rect matrix helper (setup only).
 struct Dense {

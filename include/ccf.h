@@ -102,6 +102,17 @@ ccf_status ccf_ns_step(ccf_ns_state* st, int nsteps);
 ccf_status ccf_ns_get_omega(ccf_ns_state* st, double* lam, double* gam, double* time, int* steps_taken);
 ccf_status ccf_ns_destroy(ccf_ns_state* st);
 
+/* timestep.hpp:60-111 HeatStepper: (d/dt - alpha lap) T = g with the reference's BDF 1 -> order ramp,
+ * homogeneous Dirichlet data. initial / forcing: kind 0 = grid values (p*n*m doubles, analyzed on the
+ * device: HeatStepper(config, GridField), step_with_callback), kind 1 = coefficients (CoeffTensor).
+ * ccf_heat_step adds kappa * forcing to the BDF right-hand side (timestep.cpp:71-73; NULL = none);
+ * the caller evaluates the forcing at t + h (ForcingMode::exact) or t. heat_run (timestep.cpp:146-170)
+ * is this loop plus synthesize() of the snapshots (C++ shim, Python mirror). Destroy with ccf_ns_destroy. */
+ccf_status ccf_heat_create(ccf_ctx* ctx, double alpha, double h, int order, const double* initial, int initial_kind,
+                           ccf_ns_state** out);
+ccf_status ccf_heat_step(ccf_ns_state* st, const double* forcing, int forcing_kind);
+ccf_status ccf_heat_get(ccf_ns_state* st, double* coeffs, double* time, int* steps_taken);
+
 /* Mode sharding of the NS / heat stepper over the GPUs of one node (the reference is
  * single-process, ptns.cpp:217-267 — this replaces nothing, it partitions NSStepper::step).
  * Rank r of world computes the half-spectrum Fourier slots [slot_lo, slot_hi) (w = slot, slot p/2 =

@@ -86,7 +86,8 @@ EXPORTS = ["ccf_ctx_create", "ccf_ctx_destroy", "ccf_ctx_set_stream", "ccf_ctx_s
            "ccf_create_error", "ccf_adi_last_rounds", "ccf_adi_keep_history", "ccf_get_gemm_flops",
            "ccf_diag_host_check", "ccf_shard_init", "ccf_shard_partition", "ccf_shard_info", "ccf_shard_ipc_handle",
            "ccf_shard_open_ipc", "ccf_shard_link_local", "ccf_shard_set_host_barrier", "ccf_write_field",
-           "ccf_read_field_header", "ccf_read_field", "ccf_crc32", "ccf_ns_write_omega"]
+           "ccf_read_field_header", "ccf_read_field", "ccf_crc32", "ccf_ns_write_omega", "ccf_heat_create",
+           "ccf_heat_step", "ccf_heat_get"]
 
 HOST_BARRIER_FN = C.CFUNCTYPE(None, C.c_void_p)
 SHARD_HANDLE_BYTES = 128  # include/ccf.h CCF_SHARD_HANDLE_BYTES
@@ -165,6 +166,9 @@ def lib():
         L.ccf_read_field.argtypes = [C.c_char_p, ip, ip, ip, ip, vp, C.c_size_t]
         L.ccf_crc32.argtypes = [vp, C.c_size_t, C.POINTER(C.c_uint)]
         L.ccf_ns_write_omega.argtypes = [vp, C.c_char_p, C.c_char_p]
+        L.ccf_heat_create.argtypes = [vp, C.c_double, C.c_double, C.c_int, vp, C.c_int, C.POINTER(vp)]
+        L.ccf_heat_step.argtypes = [vp, vp, C.c_int]
+        L.ccf_heat_get.argtypes = [vp, vp, dp, C.POINTER(C.c_int)]
         _lib = L
     return _lib
 
@@ -539,3 +543,83 @@ class NSStepper:
             self.close()
         except Exception:
             pass
+
+
+def _field_arg(x):
+    """(pointer holder, kind): complex -> coefficients (kind 1), real -> grid values (kind 0)."""
+    if hasattr(x, "data_ptr"):
+        t = x.contiguous()
+        return t, (1 if t.is_complex() else 0)
+    a = np.ascontiguousarray(x)
+    if np.iscomplexobj(a):
+        return a.astype(np.complex128, copy=False), 1
+    return a.astype(np.float64, copy=False), 0
+
+
+class HeatStepper:
+    """proj/include/cylspec/timestep.hpp:79-97 HeatStepper on the device: (d/dt - alpha lap) T = g,
+    BDF 1 -> order ramp, homogeneous Dirichlet. initial: grid values (real) or coefficients (complex)."""
+
+    def __init__(self, ctx: Context, initial, alpha=1.0, h=1e-2, order=4):
+        self.ctx = ctx
+        self.h_step = h
+        a, kind = _field_arg(initial)
+        st = C.c_void_p()
+        ctx._check(lib().ccf_heat_create(ctx.h, C.c_double(alpha), C.c_double(h), int(order), _addr(a), kind,
+                                         C.byref(st)))
+        self.h = st
+        self.time, self.steps_taken = 0.0, 0
+
+    def step(self, forcing=None):
+        """HeatStepper::step(const CoeffTensor*) / step_with_callback: forcing = grid values or coefficients."""
+        if forcing is None:
+            self.ctx._check(lib().ccf_heat_step(self.h, None, 0))
+        else:
+            a, kind = _field_arg(forcing)
+            self.ctx._check(lib().ccf_heat_step(self.h, _addr(a), kind))
+        self.time += self.h_step
+        self.steps_taken += 1
+
+    def current(self, out=None):
+        c = out if out is not None else self.ctx._out_c()
+        t, s = C.c_double(), C.c_int()
+        self.ctx._check(lib().ccf_heat_get(self.h, _addr(c), C.byref(t), C.byref(s)))
+        self.time, self.steps_taken = t.value, s.value
+        return c
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ccf_ns_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def heat_run(ctx: Context, initial, forcing, steps, alpha=1.0, h=1e-2, order=4, output_every=0,
+             forcing_mode="exact"):
+    """proj/src/timestep.cpp:146-170 heat_run: snapshots (grid values) at t = 0, every output_every
+    steps and at the end; forcing(t) returns grid values (numpy or torch CUDA) evaluated at t + h
+    (ForcingMode::exact) or t; forcing None = unforced."""
+    if steps < 0:
+        raise DomainError("heat_run: steps must be nonnegative")
+    st = HeatStepper(ctx, initial, alpha=alpha, h=h, order=order)
+    init_vals = initial if not np.iscomplexobj(initial) else ctx.synthesize(initial)
+    snaps, times = [np.asarray(init_vals)], [0.0]
+    for s in range(steps):
+        if forcing is None:
+            st.step(None)
+        else:
+            st.step(forcing(st.time + h if forcing_mode == "exact" else st.time))
+        if output_every > 0 and (s + 1) % output_every == 0 and s + 1 < steps:
+            snaps.append(ctx.synthesize(st.current()))
+            times.append(st.time)
+    final = st.current()
+    if steps > 0:
+        snaps.append(ctx.synthesize(final))
+        times.append(st.time)
+    st.close()
+    return dict(snapshots=snaps, snapshot_times=times, final_coeffs=final, final_time=times[-1] if steps else 0.0)

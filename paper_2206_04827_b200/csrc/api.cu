@@ -454,63 +454,144 @@ ccf_status ccf_synthesize(ccf_ctx* ctx, const double* coeffs, double* values) {
 }
 
 // ---- NSStepper (ptns.hpp:104-127)
-ccf_status ccf_ns_create(ccf_ctx* ctx, double reynolds, double h, int order, int disable_nonlinear, const double* lam0,
-                         const double* gam0, ccf_ns_state** out) {
-    return guard(ctx, [&](Ctx& c) {
-        if (order < 1 || order > 4) throw Error(ccf::DOMAIN_ERROR, "BDFScheme: order must be in {1,2,3,4}");
-        if (c.m % 2) throw Error(ccf::DOMAIN_ERROR, "NSStepper: even m required for the nonlinear pipeline");
-        auto st = std::make_unique<ccf_ns_state>();
-        st->ctx = ctx;
-        ccf::NSState& s = st->st;
-        s.pl = &ctx->pl();
-        s.reynolds = reynolds;
-        s.h = h;
-        s.order = order;
-        s.disable_nonlinear = disable_nonlinear != 0;
-        const long T = s.pl->T;
-        for (int i = 0; i < 5; ++i) {
-            s.lam[i].alloc(size_t(T));
-            s.gam[i].alloc(size_t(T));
-        }
+namespace {
+// NSStepper (ptns.cpp:180-215) and HeatStepper (timestep.cpp:110-129) construction. scalar: one field
+// (lam0; gam unused), which is also the heat stepper's state; lam0 holds grid values when values != 0.
+ccf_ns_state* ns_create_impl(ccf_ctx* ctx, Ctx& c, double reynolds, double h, int order, bool disable_nonlinear,
+                             const double* lam0, const double* gam0, bool scalar, bool values) {
+    if (order < 1 || order > 4) throw Error(ccf::DOMAIN_ERROR, "BDFScheme: order must be in {1,2,3,4}");
+    if (c.m % 2) throw Error(ccf::DOMAIN_ERROR, "NSStepper: even m required for the nonlinear pipeline");
+    auto st = std::make_unique<ccf_ns_state>();
+    st->ctx = ctx;
+    ccf::NSState& s = st->st;
+    s.pl = &ctx->pl();
+    s.reynolds = reynolds;
+    s.h = h;
+    s.order = order;
+    s.disable_nonlinear = disable_nonlinear;
+    s.scalar = scalar;
+    const long T = s.pl->T;
+    for (int i = 0; i < 5; ++i) {
+        s.lam[i].alloc(size_t(T));
+        s.gam[i].alloc(size_t(T));
+    }
+    if (!disable_nonlinear)
         for (int i = 0; i < 5; ++i) {
             s.nl[i].alloc(size_t(T));
             s.ng[i].alloc(size_t(T));
         }
-        CCF_CUDA(cudaMalloc(&s.dflag, sizeof(int)));
-        CCF_CUDA(cudaMemsetAsync(s.dflag, 0, sizeof(int), c.stream));
+    CCF_CUDA(cudaMalloc(&s.dflag, sizeof(int)));
+    CCF_CUDA(cudaMemsetAsync(s.dflag, 0, sizeof(int), c.stream));
+    if (values) {  // HeatStepper(config, GridField) = HeatStepper(config, analyze(initial))
+        ccf::DBuf ref(size_t(2) * c.m * c.n * c.p);
+        s.pl->analyze_full(lam0, ref.p);
+        c.load_coeff(ref.p, s.lam[0].p, false, 0, 0);
+        c.sync();
+    } else {
         c.load_coeff(lam0, s.lam[0].p, false, 0, 0);  // parity projection of the initial data (ptns.cpp:190-191)
-        c.load_coeff(gam0, s.gam[0].p, false, 0, 1);
-        // build every solver set the run needs before any graph capture
-        ccf::DevSet& pset = c.set(false, true, 1.0);
-        for (int b = 1; b <= order; ++b) {
-            static const double K[4] = {1.0, 2.0 / 3.0, 6.0 / 11.0, 12.0 / 25.0};
-            c.set(false, false, K[b - 1] * h * (1.0 / reynolds));
-        }
-        // eigen-coordinate state when every solve has diagonalization data in the shared basis and the
-        // nonlinear term runs on the composite operators (CCF_NS_EIGEN=0 keeps coefficient-space history)
-        const char* ev = std::getenv("CCF_NS_EIGEN");
-        const bool want = !(ev && ev[0] == '0');
-        if (want && pset.host.has_diag && pset.dg) {
-            ccf::Pipeline& P = *s.pl;
+    }
+    if (gam0) c.load_coeff(gam0, s.gam[0].p, false, 0, 1);
+    // build every solver set the run needs before any graph capture
+    ccf::DevSet& pset = c.set(false, true, 1.0);
+    for (int b = 1; b <= order; ++b) {
+        static const double K[4] = {1.0, 2.0 / 3.0, 6.0 / 11.0, 12.0 / 25.0};
+        c.set(false, false, K[b - 1] * h * (1.0 / reynolds));
+    }
+    // eigen-coordinate state when every solve has diagonalization data in the shared basis and the
+    // nonlinear term runs on the composite operators (CCF_NS_EIGEN=0 keeps coefficient-space history);
+    // the heat stepper needs only the modal bases (no composite operators)
+    const char* ev = std::getenv("CCF_NS_EIGEN");
+    const bool want = !(ev && ev[0] == '0');
+    if (want && pset.host.has_diag && pset.dg) {
+        ccf::Pipeline& P = *s.pl;
+        bool ok = true;
+        if (!disable_nonlinear) {
             P.ensure_composite();
-            if (!P.composite_off()) {
-                P.ensure_eigen(pset);
-                s.eigen = true;
-                for (int i = 0; i < 5; ++i) {
-                    s.zl[i].alloc(size_t(T));
-                    if (i == 0) s.zpsi.alloc(size_t(T));
-                    s.zg[i].alloc(size_t(T));
-                }
-                P.to_eigen(pset, s.lam[0].p, s.zl[0].p);
-                P.to_eigen(pset, s.gam[0].p, s.zg[0].p);
+            ok = !P.composite_off();
+            if (ok) P.ensure_eigen(pset);
+        }
+        if (ok) {
+            s.eigen = true;
+            for (int i = 0; i < 5; ++i) {
+                s.zl[i].alloc(size_t(T));
+                if (i == 0) s.zpsi.alloc(size_t(T));
+                if (!scalar) s.zg[i].alloc(size_t(T));
+            }
+            P.to_eigen(pset, s.lam[0].p, s.zl[0].p);
+            if (!scalar) P.to_eigen(pset, s.gam[0].p, s.zg[0].p);
+        }
+    }
+    if (c.sh.sharded() && !s.eigen)
+        throw Error(ccf::CONFIG_ERROR, "NSStepper: a mode-sharded context needs the eigen-coordinate state "
+                                       "(composite nonlinear term, fast-diagonalization solves)");
+    c.sync();
+    ctx->states.insert(st.get());
+    return st.release();
+}
+}  // namespace
+
+ccf_status ccf_ns_create(ccf_ctx* ctx, double reynolds, double h, int order, int disable_nonlinear, const double* lam0,
+                         const double* gam0, ccf_ns_state** out) {
+    return guard(ctx, [&](Ctx& c) {
+        if (!lam0 || !gam0) throw Error(ccf::DOMAIN_ERROR, "NSStepper: initial vorticity required");
+        *out = ns_create_impl(ctx, c, reynolds, h, order, disable_nonlinear != 0, lam0, gam0, false, false);
+    });
+}
+
+// ---- HeatStepper / heat_run (proj/include/cylspec/timestep.hpp:60-111, proj/src/timestep.cpp:110-170)
+ccf_status ccf_heat_create(ccf_ctx* ctx, double alpha, double h, int order, const double* initial, int initial_kind,
+                           ccf_ns_state** out) {
+    return guard(ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_heat_create");
+        if (!(alpha > 0.0)) throw Error(ccf::DOMAIN_ERROR, "HeatStepper: alpha must be positive on the B200 path");
+        if (initial_kind != 0 && initial_kind != 1) throw Error(ccf::DOMAIN_ERROR, "ccf_heat_create: initial_kind 0 | 1");
+        *out = ns_create_impl(ctx, c, 1.0 / alpha, h, order, true, initial, nullptr, true, initial_kind == 0);
+    });
+}
+
+// HeatStepper::step(const CoeffTensor* forcing) (kind 1) / step_with_callback (kind 0: the callback's grid
+// values, analyzed on the device); forcing == NULL steps without forcing
+ccf_status ccf_heat_step(ccf_ns_state* st, const double* forcing, int forcing_kind) {
+    if (!st) return CCF_INTERNAL_ERROR;
+    return guard(st->ctx, [&](Ctx& c) {
+        ccf::NSState& s = st->st;
+        if (!s.scalar) throw Error(ccf::CONFIG_ERROR, "ccf_heat_step: not a heat stepper (ccf_heat_create)");
+        s.forced = forcing != nullptr;
+        if (forcing) {
+            if (forcing_kind != 0 && forcing_kind != 1) throw Error(ccf::DOMAIN_ERROR, "ccf_heat_step: forcing_kind 0 | 1");
+            const long T = s.pl->T;
+            if (s.fh.n < size_t(T)) s.fh.alloc(size_t(T));
+            const double* ref = forcing;
+            ccf::DBuf tmp;
+            if (forcing_kind == 0) {  // analyze(forcing(t)) (timestep.cpp:142)
+                tmp.alloc(size_t(2) * c.m * c.n * c.p);
+                s.pl->analyze_full(forcing, tmp.p);
+                ref = tmp.p;
+            }
+            c.load_coeff(ref, s.fh.p, false, 0, 2);  // rhs parity projection (timestep.cpp:74)
+            if (s.eigen) {
+                if (s.zf.n < size_t(T)) s.zf.alloc(size_t(T));
+                s.pl->to_eigen(c.set(false, true, 1.0), s.fh.p, s.zf.p);
             }
         }
-        if (c.sh.sharded() && !s.eigen)
-            throw Error(ccf::CONFIG_ERROR, "NSStepper: a mode-sharded context needs the eigen-coordinate state "
-                                           "(composite nonlinear term, fast-diagonalization solves)");
+        s.step_once();
+        s.forced = false;
+        c.check_adi_error(false);
+        int f = 0;
+        CCF_CUDA(cudaMemcpyAsync(&f, s.dflag, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
         c.sync();
-        ctx->states.insert(st.get());
-        *out = st.release();
+        if (f) throw Error(ccf::NUMERICAL, "HelmholtzTensorStepper: non-finite state");
+    });
+}
+
+ccf_status ccf_heat_get(ccf_ns_state* st, double* coeffs, double* time, int* steps_taken) {
+    if (!st) return CCF_INTERNAL_ERROR;
+    return guard(st->ctx, [&](Ctx& c) {
+        st->st.omega_coeff();
+        if (coeffs) c.store_coeff(st->st.lam[st->st.head].p, coeffs, false, 0, 0);
+        c.sync();
+        if (time) *time = st->st.time;
+        if (steps_taken) *steps_taken = st->st.steps;
     });
 }
 

@@ -1828,11 +1828,16 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
             sg[ns] = ng[(nnew + i) % 5].p;
             wl[ns++] = kappa * iw[i];
         }
+        if (forced) {  // HeatStepper forcing: rhs += kappa * F (timestep.cpp:71-73), F~ = PL_P F PR
+            sl[ns] = zf.p;
+            sg[ns] = zf.p;
+            wl[ns++] = kappa;
+        }
         DevSet& set = c.set(false, false, scale);
         if (c.prof_events.empty()) c.mark("start");
         // PL_H = -(1/s) PL_P; the same pass leaves the next step's Poisson RHS Z_P = -Z_lambda .* RT_P and
         // raises the non-finite flag
-        P.eigen_rhs(set, 2, sl, sg, wl, ns, -1.0 / scale, zl[out].p, zg[out].p,
+        P.eigen_rhs(set, scalar ? 1 : 2, sl, sg, wl, ns, -1.0 / scale, zl[out].p, zg[out].p,
                     disable_nonlinear ? nullptr : zpsi.p, &pset, dflag);
         c.mark("H_rhs_combine");
         if (!disable_nonlinear) {
@@ -1865,16 +1870,24 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
             sg[ns] = ng[(nnew + i) % 5].p;
             wl[ns++] = kappa * iw[i];
         }
+        if (forced) {
+            sl[ns] = fh.p;
+            sg[ns] = fh.p;
+            wl[ns++] = kappa;
+        }
         DevSet& set = c.set(false, false, scale);
         if (c.prof_events.empty()) c.mark("start");
-        P.modal_solve(set, false, 2, sl, wl, ns, sg, wl, ns, lam[out].p, gam[out].p, "H_rhs_combine");
+        if (scalar)
+            P.modal_solve(set, false, 1, sl, wl, ns, nullptr, nullptr, 0, lam[out].p, nullptr, "H_rhs_combine");
+        else
+            P.modal_solve(set, false, 2, sl, wl, ns, sg, wl, ns, lam[out].p, gam[out].p, "H_rhs_combine");
         c.mark("H_helmholtz_solve");
         zvalid = P.last_z_valid_;  // Z of lambda_omega(out) stays in dZ_ (shared modal basis) for the next P
     }
     const long T = P.T;
     finite_check_kernel<<<std::min<long>(1184, (T + 255) / 256), 256, 0, c.stream>>>(lam[out].p, T, dflag);
-    finite_check_kernel<<<std::min<long>(1184, (T + 255) / 256), 256, 0, c.stream>>>(gam[out].p, T, dflag);
-    c.launches += 2;
+    if (!scalar) finite_check_kernel<<<std::min<long>(1184, (T + 255) / 256), 256, 0, c.stream>>>(gam[out].p, T, dflag);
+    c.launches += scalar ? 1 : 2;
 }
 
 // the nonlinear term's omega inputs (z synthesis of lambda_omega, gamma_omega, dz gamma_omega) into
@@ -1913,7 +1926,7 @@ void NSState::zsynth_omega(int r) {
 // coefficient-space omega of the newest ring slot (eigen mode keeps only Z between steps)
 void NSState::omega_coeff() {
     if (!eigen || coeff_head == head) return;
-    pl->eigen_back(pl->c.set(false, true, 1.0), 2, zl[head].p, zg[head].p, lam[head].p, gam[head].p);
+    pl->eigen_back(pl->c.set(false, true, 1.0), scalar ? 1 : 2, zl[head].p, zg[head].p, lam[head].p, gam[head].p);
     coeff_head = head;
 }
 
@@ -1932,7 +1945,7 @@ void NSState::step_once() {
     const bool steady = (b == order) && (disable_nonlinear || ncount == order);
     const int key = head * 5 + nhead;
     // host-mode rank barriers synchronise inside the step: no graph capture
-    if (use_graphs && steady && steps >= order + 1 && c.sh.mode != Shard::HOST) {
+    if (use_graphs && steady && steps >= order + 1 && c.sh.mode != Shard::HOST && !forced) {
         if (!graphs[key]) {
             cudaGraph_t g;
             const long l0 = c.launches;

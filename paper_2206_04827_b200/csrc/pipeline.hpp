@@ -172,6 +172,10 @@ struct NSState {
     DBuf zpsi;            // Poisson RHS -Z_lambda .* RT_P of ring slot zp_head (left by the Helmholtz pass)
     int zp_head = -1;
     int zv_head = -1;     // ring slot whose velocity z tensors (scratch 1, 2) are current (while zw_owner_)
+    // HeatStepper (timestep.cpp:110-144): one scalar field in lam (gam unused), optional forcing per step
+    bool scalar = false;
+    bool forced = false;  // the next step adds kappa * forcing (zf: eigen coordinates, fh: coefficients)
+    DBuf fh, zf;
     ~NSState();
     void zsynth_omega(int r);
     void velocity(int r);

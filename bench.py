@@ -148,6 +148,66 @@ def cpu_sample(cfg, threads):
     return 1.0 / t_step, sample, d
 
 
+def secondary_configs(P, torch):
+    """BASELINE.json configs 1-3 on the same GPU (reported beside the headline, SURVEY §8d units):
+    config 1 Poisson 32^3 (us per solve: steady state with a cached plan, and with setup like the
+    reference's run_poisson), config 2 implicit heat stepping 128^3 (steps/s, Re 100, h 1e-3, 100 BDF4
+    steps), config 3 NS 64^3 (steps/s, Re 100, h 1e-3, 200 steps, max|v| = 1)."""
+    import ctypes as C
+    from tests.inputs import hermitian_coeffs
+    out = {}
+    # config 1
+    m = n = p = 32
+    f = hermitian_coeffs(m, n, p, 0.8, 1)
+    t0 = time.perf_counter()
+    ctx = P.Context(m, n, p)
+    ctx.solve_poisson_3d(f)
+    with_setup = time.perf_counter() - t0
+    fd = torch.from_numpy(f).cuda()
+    ud = torch.zeros_like(fd)
+    for _ in range(3):
+        ctx._check(P.lib().ccf_poisson3d(ctx.h, C.c_void_p(fd.data_ptr()), C.c_void_p(ud.data_ptr())))
+    torch.cuda.synchronize()
+    reps = 200
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        ctx._check(P.lib().ccf_poisson3d(ctx.h, C.c_void_p(fd.data_ptr()), C.c_void_p(ud.data_ptr())))
+    steady = (time.perf_counter() - t0) / reps
+    ctx.close()
+    out["config1_poisson_32"] = {"us_per_solve_steady": steady * 1e6, "s_with_setup": with_setup,
+                                 "what": "solve_poisson_3d through the C-ABI, device buffers, synchronous calls "
+                                         "(one solve = p modal solves); with setup = fresh context + first solve"}
+    # config 2
+    m = n = p = 128
+    ctx = P.Context(m, n, p)
+    st = P.NSStepper(ctx, hermitian_coeffs(m, n, p, 0.85, 2), hermitian_coeffs(m, n, p, 0.85, 102), reynolds=100.0,
+                     h=1e-3, order=4, disable_nonlinear=True)
+    st.step(10)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st.step(100)
+    torch.cuda.synchronize()
+    out["config2_heat_128"] = {"steps_per_s": 100 / (time.perf_counter() - t0), "steps": 100,
+                               "what": "Lambda, Gamma implicit BDF4 heat steps (NSStepper, disable_nonlinear), state in HBM"}
+    st.close()
+    ctx.close()
+    # config 3
+    cfg = CONFIGS[64]
+    ctx = P.Context(64, 64, 64)
+    wl, wg, _ = initial_vorticity(ctx, cfg, cfg["vmax"])
+    st = P.NSStepper(ctx, wl, wg, reynolds=cfg["reynolds"], h=cfg["h"], order=4)
+    st.step(10)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st.step(200)
+    torch.cuda.synchronize()
+    out["config3_ns_64"] = {"steps_per_s": 200 / (time.perf_counter() - t0), "steps": 200,
+                            "what": "full NS steps, Re 100, h 1e-3, max|v| = 1, state in HBM (launch-bound size)"}
+    st.close()
+    ctx.close()
+    return out
+
+
 def run_reference(args, cfg, rank):
     if rank != 0:
         return
@@ -181,6 +241,7 @@ def main():
     ap.add_argument("--one-gpu-test", action="store_true",
                     help="plumbing test of the N>1 path on ONE GPU: every rank on device 0, gloo, host barriers "
                          "(no device-side waiting between ranks); the numbers are not a measurement")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the BASELINE configs 1-3 side measurements")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: one independent replica per GPU instead of the mode-sharded step")
     args = ap.parse_args()
@@ -323,6 +384,10 @@ def main():
     status_bytes = 4 * 4 + 4  # per step: ADI error words + non-finite flag (ccf_ns_step)
     st2.close()
 
+    sec = None
+    if rank == 0 and world == 1 and not args.no_secondary:
+        sec = secondary_configs(P, torch)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, sample, d = cpu_sample(cfg, 1)
@@ -377,6 +442,8 @@ def main():
         }
         if cpu:
             line["cpu_baseline"] = cpu
+        if sec:
+            line["secondary_configs"] = sec
         print(json.dumps(line), flush=True)
     st.close()
     ctx.close()

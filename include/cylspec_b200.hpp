@@ -11,6 +11,10 @@
 #include <complex>
 #include <deque>
 #include <map>
+#include <cstdint>
+#include <algorithm>
+#include <variant>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -39,6 +43,7 @@ struct NotIncompressibleError : std::runtime_error {
     double divergence;
 };
 struct NumericalError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct FieldFileError : std::runtime_error { using std::runtime_error::runtime_error; };  // io.hpp:17-19
 
 // ---- grid / tensors (grid.hpp:13-50, coeffs.hpp:16-45)
 struct GridSpec {
@@ -111,6 +116,7 @@ namespace detail {
         case CCF_NON_CONVERGENCE: throw NonConvergenceError(w, std::vector<double>(hist, hist + (nh < 8 ? nh : 8)));
         case CCF_NOT_INCOMPRESSIBLE: throw NotIncompressibleError(w, 0.0);
         case CCF_NUMERICAL_ERROR: throw NumericalError(w);
+        case CCF_FIELDFILE_ERROR: throw FieldFileError(w);
         default: throw std::runtime_error("ccf: " + w);
     }
 }
@@ -308,6 +314,124 @@ inline NSRunResult ns_run(const NSConfig& config, const PTScalars& initial_omega
     r.final_omega = s.omega();
     r.final_time = s.time();
     return r;
+}
+
+// ---- HeatStepper / heat_run (timestep.hpp:60-111)
+enum class ForcingMode { exact, lagged };  // forcing evaluated at t + h (exact) or t
+struct HeatConfig {
+    GridSpec spec;
+    double alpha = 1.0;
+    double h = 1e-2;
+    int order = 4;
+    double adi_tol = kDefaultAdiTol;
+    ForcingMode forcing_mode = ForcingMode::exact;
+    BoundaryCondition bc;
+    int output_every = 0;  // 0: keep only initial and final snapshots
+};
+using ForcingCallback = std::function<GridField(double time)>;
+
+class HeatStepper {  // state resident on the GPU (eigen coordinates) between steps
+public:
+    HeatStepper(const HeatConfig& config, const GridField& initial) : config_(config), cur_(config.spec) {
+        init(initial.values.data(), 0);
+    }
+    HeatStepper(const HeatConfig& config, const CoeffTensor& initial) : config_(config), cur_(config.spec) {
+        if (!(initial.spec == config.spec)) throw DomainError("HeatStepper: initial data spec mismatch");
+        init(initial.raw(), 1);
+    }
+    ~HeatStepper() { ccf_ns_destroy(st_); }
+    HeatStepper(const HeatStepper&) = delete;
+    HeatStepper& operator=(const HeatStepper&) = delete;
+    void step(const CoeffTensor* forcing) {
+        detail::check(ccf_heat_step(st_, forcing ? forcing->raw() : nullptr, 1), ctx_);
+        time_ += config_.h;
+        ++steps_;
+    }
+    void step_with_callback(const ForcingCallback& forcing) {
+        if (!forcing) return step(nullptr);
+        const GridField g = forcing(config_.forcing_mode == ForcingMode::exact ? time_ + config_.h : time_);
+        detail::check(ccf_heat_step(st_, g.values.data(), 0), ctx_);  // analyzed on the device
+        time_ += config_.h;
+        ++steps_;
+    }
+    const CoeffTensor& current() {
+        detail::check(ccf_heat_get(st_, cur_.raw(), &time_, &steps_), ctx_);
+        return cur_;
+    }
+    double time() const { return time_; }
+    int current_order() const { return std::min(config_.order, steps_ + 1); }
+    const HeatConfig& config() const { return config_; }
+
+private:
+    void init(const double* data, int kind) {
+        ctx_ = detail::context(config_.spec, config_.adi_tol);
+        detail::check(ccf_heat_create(ctx_, config_.alpha, config_.h, config_.order, data, kind, &st_), ctx_);
+    }
+    HeatConfig config_;
+    ccf_ctx* ctx_ = nullptr;
+    ccf_ns_state* st_ = nullptr;
+    CoeffTensor cur_;
+    double time_ = 0.0;
+    int steps_ = 0;
+};
+
+struct HeatRunResult {
+    std::vector<GridField> snapshots;
+    std::vector<double> snapshot_times;
+    CoeffTensor final_coeffs;
+    double final_time = 0.0;
+};
+
+inline HeatRunResult heat_run(const HeatConfig& config, const GridField& initial, const ForcingCallback& forcing,
+                              int steps) {  // timestep.cpp:146-170
+    if (steps < 0) throw DomainError("heat_run: steps must be nonnegative");
+    HeatStepper stepper(config, initial);
+    HeatRunResult result;
+    result.snapshots.push_back(initial);
+    result.snapshot_times.push_back(0.0);
+    for (int s = 0; s < steps; ++s) {
+        stepper.step_with_callback(forcing);
+        const bool cadence = config.output_every > 0 && (s + 1) % config.output_every == 0;
+        if (cadence && s + 1 < steps) {
+            result.snapshots.push_back(synthesize(stepper.current()));
+            result.snapshot_times.push_back(stepper.time());
+        }
+    }
+    result.final_coeffs = stepper.current();
+    if (steps > 0) {
+        result.snapshots.push_back(synthesize(result.final_coeffs));
+        result.snapshot_times.push_back(stepper.time());
+    }
+    result.final_time = stepper.time();
+    return result;
+}
+
+// ---- FieldFile "CCF1" (io.hpp:11-28); checksums of device data run on the GPU
+inline uint32_t crc32_ieee(const uint8_t* data, size_t len) {
+    unsigned c = 0;
+    detail::check(ccf_crc32(data, len, &c), nullptr);
+    return c;
+}
+inline void write_field(const std::string& path, const GridField& field) {
+    detail::check(ccf_write_field(path.c_str(), 0, field.spec.m, field.spec.n, field.spec.p, field.values.data()),
+                  nullptr);
+}
+inline void write_field(const std::string& path, const CoeffTensor& coeffs) {
+    detail::check(ccf_write_field(path.c_str(), 1, coeffs.spec.m, coeffs.spec.n, coeffs.spec.p, coeffs.raw()), nullptr);
+}
+using FieldVariant = std::variant<GridField, CoeffTensor>;
+inline FieldVariant read_field(const std::string& path) {
+    int kind = 0, m = 0, n = 0, p = 0;
+    detail::check(ccf_read_field_header(path.c_str(), &kind, &m, &n, &p), nullptr);
+    GridSpec spec(m, n, p);
+    if (kind == 0) {
+        GridField f(spec);
+        detail::check(ccf_read_field(path.c_str(), &kind, &m, &n, &p, f.values.data(), f.values.size()), nullptr);
+        return f;
+    }
+    CoeffTensor t(spec);
+    detail::check(ccf_read_field(path.c_str(), &kind, &m, &n, &p, t.raw(), 2 * t.data.size()), nullptr);
+    return t;
 }
 
 }  // namespace cylspec

@@ -43,6 +43,37 @@ int main(int argc, char** argv) {
     } catch (const DomainError&) {
         threw = true;
     }
-    std::printf("shim ok: roundtrip %.3e final_time %.6f domain_error %d\n", err / mx, run.final_time, int(threw));
-    return (err / mx < 1e-12 && threw) ? 0 : 1;
+    // heat_run on the manufactured problem of test_timestep.cpp:151-187 (exact forcing at t + h)
+    auto pt = [](int i, int c) { return std::cos(double(c - 1 - i) * M_PI / double(c - 1)); };
+    auto field = [&](auto fn) {
+        GridField gf(spec);
+        for (int l = 0; l < spec.p; ++l)
+            for (int k = 0; k < spec.n; ++k)
+                for (int j = 0; j < spec.m; ++j)
+                    gf.values[(size_t(l) * spec.n + k) * spec.m + j] = fn(pt(j, spec.m), pt(k, spec.n));
+        return gf;
+    };
+    auto exact = [&](double t) { return field([t](double r, double z) { return std::exp(-t) * (1 - r * r) * (1 - z * z); }); };
+    HeatConfig hc;
+    hc.spec = spec;
+    hc.alpha = 1.0;
+    hc.h = 0.01;
+    HeatRunResult hr = heat_run(hc, exact(0.0), [&](double t) {
+        return field([t](double r, double z) {
+            return -std::exp(-t) * (1 - r * r) * (1 - z * z) + std::exp(-t) * (4 * (1 - z * z) + 2 * (1 - r * r));
+        });
+    }, 100);
+    const GridField ref = exact(hr.final_time);
+    double herr = 0, hmx = 0;
+    for (size_t i = 0; i < ref.values.size(); ++i) {
+        herr = std::max(herr, std::abs(hr.snapshots.back().values[i] - ref.values[i]));
+        hmx = std::max(hmx, std::abs(ref.values[i]));
+    }
+    // FieldFile round trip of the final NS vorticity (io.cpp:42-109)
+    write_field("/tmp/shim_lambda.ccf", run.final_omega.lambda);
+    const CoeffTensor rd = std::get<CoeffTensor>(read_field("/tmp/shim_lambda.ccf"));
+    const bool io_ok = rd.data == run.final_omega.lambda.data && crc32_ieee(reinterpret_cast<const uint8_t*>("123456789"), 9) == 0xCBF43926u;
+    std::printf("shim ok: roundtrip %.3e final_time %.6f domain_error %d heat_err %.3e io %d\n", err / mx,
+                run.final_time, int(threw), herr / hmx, int(io_ok));
+    return (err / mx < 1e-12 && threw && herr / hmx < 1e-4 && io_ok) ? 0 : 1;
 }

@@ -8,6 +8,7 @@
 // (the reference's caches are process-wide; ours are per context and hold the same plans).
 #pragma once
 
+#include <cmath>
 #include <complex>
 #include <deque>
 #include <map>
@@ -79,7 +80,41 @@ struct CoeffTensor {
     Complex at(int j, int k, int l) const { return data[(size_t(l) * spec.n + size_t(k)) * spec.m + size_t(j)]; }
     const double* raw() const { return reinterpret_cast<const double*>(data.data()); }
     double* raw() { return reinterpret_cast<double*>(data.data()); }
+    CoeffTensor& operator+=(const CoeffTensor& o) {
+        for (size_t i = 0; i < data.size(); ++i) data[i] += o.data[i];
+        return *this;
+    }
+    double max_abs() const {
+        double v = 0;
+        for (const Complex& c : data) v = std::max(v, std::abs(c));
+        return v;
+    }
 };
+
+// grid points (grid.cpp:16-40): r_j = cos((m-1-j) pi/(m-1)) with exact endpoints / midpoint, theta_l = (2l - p) pi / p
+inline std::vector<double> chebyshev_points(int count) {
+    if (count < 2) throw DomainError("chebyshev_points: need at least 2 points");
+    std::vector<double> x(static_cast<size_t>(count), 0.0);
+    for (int j = 0; j < count; ++j) x[size_t(j)] = std::cos(double(count - j - 1) * M_PI / double(count - 1));
+    x[0] = -1.0;
+    x[size_t(count) - 1] = 1.0;
+    if (count % 2 == 1) x[size_t(count / 2)] = 0.0;
+    return x;
+}
+inline std::vector<double> fourier_points(int count) {
+    std::vector<double> t(static_cast<size_t>(count), 0.0);
+    for (int l = 0; l < count; ++l) t[size_t(l)] = double(2 * l - count) * M_PI / double(count);
+    return t;
+}
+template <class F>
+GridField sample(const GridSpec& spec, F&& f) {  // grid.hpp: value f(r_j, z_k, theta_l) at every node
+    GridField g(spec);
+    const auto r = chebyshev_points(spec.m), z = chebyshev_points(spec.n), th = fourier_points(spec.p);
+    for (int l = 0; l < spec.p; ++l)
+        for (int k = 0; k < spec.n; ++k)
+            for (int j = 0; j < spec.m; ++j) g.at(j, k, l) = f(r[size_t(j)], z[size_t(k)], th[size_t(l)]);
+    return g;
+}
 
 struct PTScalars {
     CoeffTensor lambda, gamma;
@@ -247,6 +282,14 @@ inline PTScalars curl_pt(const PTScalars& s) {
     ccf_ctx* c = detail::context(s.lambda.spec);
     detail::check(ccf_curl_pt(c, s.lambda.raw(), s.gamma.raw(), o.lambda.raw(), o.gamma.raw()), c);
     return o;
+}
+inline CoeffTensor divergence(const VectorFieldCoeffs& v) {  // ptns.cpp:35-40
+    CoeffTensor sum = v.comp_r;
+    sum += derivative_theta(v.comp_theta);
+    CoeffTensor out = derivative_r(v.comp_r);
+    out += divide_r(sum);
+    out += derivative_z(v.comp_z);
+    return out;
 }
 inline PTScalars velocity_from_vorticity(const PTScalars& w, double tol = kDefaultAdiTol) {
     PTScalars o(w.lambda.spec);

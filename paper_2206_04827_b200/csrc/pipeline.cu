@@ -447,6 +447,10 @@ void GemmPlan::upload() {
 void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double* c0, double* c1,
                       const double* b2) const {
     const unsigned nb = unsigned(std::max(C.size(), Coff.size()));
+    static const bool trace = std::getenv("CCF_GEMM_TRACE") != nullptr;  // diagnostics: one line per launch
+    if (trace)
+        std::fprintf(stderr, "[gemm] M %d N %d K %d batches %u terms %zu flops %.4e tma %d pipe %d\n", M, N, K, nb,
+                     A.size(), flops(), int(tma), int(pipe));
     GemmBatch g{dA, dB, dC, M, N, K, lda, ldb, ldc, alpha, beta, dT, dDL, dDR, dBoff, dCoff, {b0, b1, b2}, {c0, c1}, int(nb),
                 ldd ? ldd : long(N), 1, dAoff};
     const bool based_ok = (reinterpret_cast<uintptr_t>(b0) % 16 == 0) && (reinterpret_cast<uintptr_t>(b1) % 16 == 0);
@@ -489,6 +493,7 @@ void GemmPlan::launch(cudaStream_t s, const double* b0, const double* b1, double
         const long items = long(nb) * ((M + 127) / 128) * ((N + 63) / 64);
         dgemm_tma_kernel<<<unsigned(std::min<long>(items, 2L * nsm)), 288, dgemm_tma_smem(), s>>>(
             g, mp, static_cast<const int4*>(dTA), static_cast<const int2*>(dTB));
+        CCF_CUDA(cudaGetLastError());  // launch-configuration errors surface here, not as silent no-ops
     } else if (pipe && based_ok) {
         static bool attr = false;  // process-wide function attributes (same on every device)
         if (!attr) {

@@ -179,10 +179,20 @@ ccf_status ccf_helmholtz_step(ccf_ctx* ctx, const double* const* hist, int nhist
 
 ccf_status ccf_modal_plan(ccf_ctx* ctx, int w, double scale, int poisson, double* info, double* u, double* v, int cap) {
     return guard(ctx, [&](Ctx& c) {
-        ccf::DevSet& set = c.set(true, poisson != 0, scale);
         const int s = w + c.p / 2;
         if (s < 0 || s >= c.p) throw Error(ccf::DOMAIN_ERROR, "ccf_modal_plan: wavenumber out of range");
-        const ccf::Plan& pl = set.host.plans[size_t(s)].plan;
+        // the reference's shift plan of this mode (a fast-diagonalization context keeps no ADI data:
+        // build the plan of this one mode on the host)
+        ccf::SolverSet one;
+        const ccf::Plan* plp = nullptr;
+        if (c.flags & 4) {
+            plp = &c.set(true, poisson != 0, scale).host.plans[size_t(s)].plan;
+        } else {
+            one = ccf::build_solver_set(*c.sizeops, {w}, poisson != 0, scale, c.tol, c.radial_cache, (c.flags & 1) != 0,
+                                        1.0, false, true);
+            plp = &one.plans[0].plan;
+        }
+        const ccf::Plan& pl = *plp;
         const double vals[8] = {pl.a, pl.b, pl.c, pl.d, pl.gamma, pl.alpha, pl.modulus, double(pl.J)};
         std::memcpy(info, vals, sizeof vals);
         for (int j = 0; j < pl.J && j < cap; ++j) {
@@ -746,7 +756,7 @@ ccf_status ccf_diag_host_check(int m, int n, int w, double scale, int poisson, i
         if (m < 6 || n < 6 || m % 2 || n % 2) throw Error(ccf::DOMAIN_ERROR, "ccf_diag_host_check: even m, n >= 6 required");
         ccf::SizeOps so(m, n);
         std::map<int, ccf::Range> cache;
-        ccf::SolverSet set = ccf::build_solver_set(so, {w}, poisson != 0, scale, 1e-12, cache, false, 4.0, true);
+        ccf::SolverSet set = ccf::build_solver_set(so, {w}, poisson != 0, scale, 1e-12, cache, false, 4.0, true, false);
         *residual = ccf::diag_check_residual(set, 0, k0 & 1, (m - 2) / 2, (n - 2) / 2, seed);
         return CCF_OK;
     } catch (const Error& e) {

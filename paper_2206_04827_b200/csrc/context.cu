@@ -67,7 +67,9 @@ Ctx::Ctx(int m_, int n_, int p_, int device_, double tol_, int flags_)
     if (m < 4 || n < 4) throw Error(DOMAIN_ERROR, "GridSpec: m and n must be at least 4");
     if (p < 2 || p % 2 != 0) throw Error(DOMAIN_ERROR, "GridSpec: p must be even and at least 2");
     if (m % 2 || n % 2) throw Error(DOMAIN_ERROR, "ccf: the B200 path requires even m and n (parity-compressed layout)");
-    if (m > 320 || n > 320) throw Error(DOMAIN_ERROR, "ccf: m, n <= 320 (single-CTA ADI tile)");
+    const bool adi = (flags & 4) != 0;  // the ADI kernel (single-CTA tile) is the modal solver
+    if (adi && (m > 320 || n > 320)) throw Error(DOMAIN_ERROR, "ccf: m, n <= 320 with the ADI solver (single-CTA tile)");
+    if (m > 2050 || n > 2050) throw Error(DOMAIN_ERROR, "ccf: m, n <= 2050");
     if (!(tol > 0.0) || tol >= 1.0) throw Error(DOMAIN_ERROR, "compute_shifts: tol must be in (0,1)");
     CCF_CUDA(cudaSetDevice(device));
     CCF_CUDA(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
@@ -82,7 +84,7 @@ Ctx::Ctx(int m_, int n_, int p_, int device_, double tol_, int flags_)
     Npad = ((N + 7) / 8) * 8;
     pitch = (Npad + 4) | 1;
     estride = ((long(Mpad) * N + 1) / 2) * 2;
-    if (std::max(M, N) > 256) throw Error(DOMAIN_ERROR, "ccf: (m-2)/2, (n-2)/2 <= 256 (single-CTA ADI tile)");
+    if (adi && std::max(M, N) > 256) throw Error(DOMAIN_ERROR, "ccf: (m-2)/2, (n-2)/2 <= 256 with the ADI solver");
     sizeops = std::make_unique<SizeOps>(m, n);
     // workspace
     const int cap = p;  // max slots (full mode)
@@ -98,10 +100,10 @@ Ctx::Ctx(int m_, int n_, int p_, int device_, double tol_, int flags_)
     CCF_CUDA(cudaMemset(ws.err, 0, sizeof(int) * 4));
     CCF_CUDA(cudaMemset(ws.iters, 0, sizeof(unsigned long long) * 2));
     CCF_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
-    ws.eprime.alloc(size_t(2) * cap * 4 * size_t(estride));
-    ws.escr.alloc(size_t(2) * cap * 4 * size_t(estride));
-    ws.xscr.alloc(size_t(2) * cap * 4 * size_t(estride));
-    {
+    if (adi) {  // ADI round scratch and the single-CTA tile's shared memory
+        ws.eprime.alloc(size_t(2) * cap * 4 * size_t(estride));
+        ws.escr.alloc(size_t(2) * cap * 4 * size_t(estride));
+        ws.xscr.alloc(size_t(2) * cap * 4 * size_t(estride));
         int optin = 0;
         CCF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
         const size_t stat = adi_static_smem();
@@ -162,8 +164,9 @@ DevSet& Ctx::set(bool full, bool poisson, double scale) {
     auto ds = std::make_unique<DevSet>();
     // flags bit1: execute the reference's shift counts (no tail-avoidance margin)
     // flags bit2: solve with the ADI kernel (the reference algorithm) instead of fast diagonalization
+    // the ADI data (enclosures, shift plans, factor blocks) only when the ADI kernel is the solver
     ds->host = build_solver_set(*sizeops, slot_w, poisson, scale, tol, radial_cache, (flags & 1) != 0,
-                                (flags & 2) ? 1.0 : 4.0, (flags & 4) == 0);
+                                (flags & 2) ? 1.0 : 4.0, (flags & 4) == 0, (flags & 4) != 0);
     const SolverSet& h = ds->host;
     if (h.has_diag) {
         CCF_CUDA(cudaMalloc(&ds->dg, h.dg.size() * sizeof(double)));
@@ -198,6 +201,8 @@ DevSet& Ctx::set(bool full, bool poisson, double scale) {
 
 void Ctx::run_adi(DevSet& set, bool full, int ntensor, const double* const* src0, const double* w0, int n0,
                   const double* const* src1, const double* w1, int n1, double* out0, double* out1) {
+    if (!(flags & 4) || set.host.maxJ == 0)
+        throw Error(INTERNAL, "run_adi: this context solves by fast diagonalization (no ADI data; flag bit 2)");
     const Geo& g = geo(full);
     last_adi_kind = set.host.poisson ? "Poisson" : "Helmholtz";
     last_adi_ntensor = ntensor;

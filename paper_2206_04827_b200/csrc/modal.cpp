@@ -136,7 +136,9 @@ Range vertical_range(SizeOps& so, bool q2_pad) {
 }
 
 SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poisson, double scale, double tol,
-                           std::map<int, Range>& radial_cache, bool q2_pad, double plan_margin, bool with_diag) {
+                           std::map<int, Range>& radial_cache, bool q2_pad, double plan_margin, bool with_diag,
+                           bool with_adi) {
+    if (!with_diag && !with_adi) throw Error(INTERNAL, "build_solver_set: nothing to build");
     const int m = so.m, n = so.n, M = (m - 2) / 2, N = (n - 2) / 2, mh = m / 2, nh = n / 2;
     const int lrows = ((M + 7) / 8) * 8 + 2, rrows = ((N + 7) / 8) * 8 + 2;  // zero-padded sweep rows
     SolverSet set;
@@ -150,7 +152,7 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
     // unique |w| -> radial ranges (parallel over wavenumbers: O(m^3) QR each)
     std::vector<int> need;
     for (int w : slot_w)
-        if (!radial_cache.count(std::abs(w))) need.push_back(std::abs(w));
+        if (with_adi && !radial_cache.count(std::abs(w))) need.push_back(std::abs(w));
     std::sort(need.begin(), need.end());
     need.erase(std::unique(need.begin(), need.end()), need.end());
     if (!need.empty()) {
@@ -179,7 +181,7 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
             radial_cache[need[i]] = res[i];
         }
     }
-    const Range vert = vertical_range(so, false);
+    const Range vert = with_adi ? vertical_range(so, false) : Range{};
 
     // per |w| block cache
     std::map<int, AdiSlot> built;
@@ -232,6 +234,35 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
             const CBand Ap = compress(recombine(lw), j0, M, M, -2, 3);
             const CBand Cp = compress(so.R2rec, j0, M, M, -2, 3);
             diag_in.push_back({aw, Ap, Cp, R2c});
+        }
+        if (!with_adi) {  // diagonalization data only (no plan, no ADI shift blocks); the static operator
+            // bands (R2, A, C | C02, B^T, D^T) are kept for host-side residual checks (diag_check_residual)
+            AdiSlot d{};
+            d.j0 = j0;
+            d.sleft = alloc(size_t(M) * kStatW);
+            d.sright0 = alloc(size_t(N) * kStatW);
+            d.sright1 = alloc(size_t(N) * kStatW);
+            for (int a = 0; a < M; ++a) {
+                double* r = C.data() + d.sleft + size_t(a) * kStatW;
+                for (int q = 0; q < 5; ++q) r[1 + q] = R2c.at(a, q - 1);
+                for (int q = 0; q < 6; ++q) {
+                    r[6 + q] = Ac.at(a, q - 2);
+                    r[12 + q] = Cc.at(a, q - 2);
+                }
+            }
+            for (int k0 = 0; k0 < 2; ++k0)
+                for (int b = 0; b < N; ++b) {
+                    double* r = C.data() + (k0 ? d.sright1 : d.sright0) + size_t(b) * kStatW;
+                    for (int q = 0; q < 3; ++q) r[1 + q] = C02c[k0].at(b, q);
+                    for (int q = 0; q < 4; ++q) {
+                        r[12 + q] = Btc[k0].at(b, q - 1);
+                        r[16 + q] = Dtc[k0].at(b, q - 1);
+                    }
+                }
+            built[aw] = d;
+            set.slots[size_t(s)] = d;
+            set.plans[size_t(s)].w = w;
+            continue;
         }
 
         const Range mu = radial_cache.at(aw);

@@ -372,7 +372,8 @@ void GemmPlan::upload() {
     }
     // ---- TMA variant: one map per (operand allocation, leading dimension), box origins per term
     tma = false;
-    if (pipe && tma_mode() && (tma_mode() == 1 || tstart.empty()) && M > 64 && !A.empty()) {
+    const bool kbox_ok = K % 16 == 0 || K + kzero >= ((K + 15) / 16) * 16;  // no live data in the last k-box
+    if (pipe && kbox_ok && tma_mode() && (tma_mode() == 1 || tstart.empty()) && M > 64 && !A.empty()) {
         struct Key {
             uintptr_t base;
             long ld;
@@ -424,6 +425,9 @@ void GemmPlan::upload() {
                     cb = int(o % ldb);
                 }
             }
+            // a block must not wrap around the rows of its 2-D view: the boxes read columns [col, col + extent)
+            // of one row (past the row end they read zeros, not the wrapped data)
+            if (ok && (long(ca) + K > lda || long(cb) + N > ldb)) ok = false;
             hta[4 * t] = ia;
             hta[4 * t + 1] = ca;
             hta[4 * t + 2] = ra;
@@ -1423,6 +1427,7 @@ void Pipeline::eigen_ysynth(int ntensor, const double* const* z, double* const* 
                         }
                     }
         ys.M = M; ys.N = nh; ys.K = N; ys.lda = 2 * Np; ys.ldb = nh; ys.ldc = g.n;
+        ys.kzero = Np - N;  // Z's pad column is zero (eigen_rhs / to_eigen)
         ys.upload();
     }
     ys.launch(c.stream, z[0], ntensor > 1 ? z[1] : z[0], nullptr, nullptr, ntensor > 2 ? z[2] : z[0]);
@@ -1528,6 +1533,7 @@ void Pipeline::eigen_back(DevSet& set, int ntensor, const double* z0, const doub
                                           long(k0) * nh);                               // u   mh x nh (ld n)
                     }
         e3.M = mh; e3.N = N; e3.K = M; e3.lda = Mp; e3.ldb = 2 * Np; e3.ldc = Np;
+        e3.kzero = Mp - M;  // QL's pad column is zero (modal.cpp padld)
         e4.M = mh; e4.N = nh; e4.K = N; e4.lda = Np; e4.ldb = nh; e4.ldc = g.n;
         e3.upload();
         e4.upload();

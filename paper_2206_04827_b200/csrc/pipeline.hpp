@@ -62,6 +62,9 @@ struct GemmPlan {
     void* dTB = nullptr;  // int2 per term
     mutable std::vector<std::pair<const double*, CUtensorMap>> bmap_cache;
     int M = 0, N = 0, K = 0;
+    // columns of every A row past K that the caller guarantees to be zero (padding): the TMA kernel reads
+    // whole 16-column k-boxes, so it is only used when K is a multiple of 16 or this padding covers the box
+    int kzero = 0;
     long lda = 0, ldb = 0, ldc = 0;
     double alpha = 1.0, beta = 0.0;
     void upload();

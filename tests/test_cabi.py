@@ -67,3 +67,8 @@ def test_fast_diagonalization_residual(P, m, w, scale, poisson):
     (1e-12, adi.cpp:188-192) on random right-hand sides, for both k-parities."""
     for k0 in (0, 1):
         assert P.diag_host_check(m, m, w, scale, poisson, k0, seed=3) < 2e-13
+
+
+def test_fast_diagonalization_residual_beyond_the_adi_tile(P):
+    # config 5 size (m = n = 512): no ADI data is needed, the diagonalization stays exact
+    assert P.diag_host_check(512, 512, 0, 1.0, True, 0, 1) < 1e-12

@@ -8,7 +8,9 @@ from oracle import pyoracle as O
 def report(name, got, ref):
     print(f"  {name:28s} rel_err {rel_err(got, ref):.3e}  (|ref| {np.max(np.abs(ref)):.2e})", flush=True)
 
-for (m, n, p) in [(8, 8, 8), (16, 12, 8), (16, 16, 16), (32, 32, 32), (16, 16, 256), (32, 24, 256)]:
+SHAPES = [tuple(int(x) for x in a.split('x')) for a in sys.argv[1:]] or [(8, 8, 8), (16, 12, 8), (16, 16, 16), (32, 32, 32), (16, 16, 256), (32, 24, 256)]
+TOL = float(os.environ.get('ORACLE_TOL', '1e-12'))
+for (m, n, p) in SHAPES:
     print(f"== {m}x{n}x{p}", flush=True)
     ctx = P.Context(m, n, p)
     lam = hermitian_coeffs(m, n, p, 0.7, 1)
@@ -30,7 +32,7 @@ for (m, n, p) in [(8, 8, 8), (16, 12, 8), (16, 16, 16), (32, 32, 32), (16, 16, 2
     ocl, ocg = O.curl_pt(lam, gam)
     report("curl_pt lam", cl, ocl); report("curl_pt gam", cg, ocg)
     vl, vg = ctx.velocity_from_vorticity(lam, gam)
-    ovl, ovg = O.velocity_from_vorticity(lam, gam)
+    ovl, ovg = O.velocity_from_vorticity(lam, gam, tol=TOL)
     report("velocity lam", vl, ovl); report("velocity gam", vg, ovg)
     nl, ng = ctx.nonlinear_term(ovl, ovg, lam, gam)
     onl, ong = O.nonlinear(ovl, ovg, lam, gam)
@@ -39,7 +41,7 @@ for (m, n, p) in [(8, 8, 8), (16, 12, 8), (16, 16, 16), (32, 32, 32), (16, 16, 2
     report("analyze", ctx.analyze(vals), O.analyze(vals))
     report("synthesize", ctx.synthesize(both), O.synthesize(both))
     ns = P.NSStepper(ctx, lam, gam, reynolds=100.0, h=1e-3)
-    ons = O.NSStepper(lam, gam, 100.0, 1e-3)
+    ons = O.NSStepper(lam, gam, 100.0, 1e-3, tol=TOL)
     for st in range(1, 7 if p <= 64 else 3):  # the random field is under-resolved in time at p = 256
         ns.step(1); ons.step(1)
         gl, gg = ns.omega(); rl, rg = ons.omega()

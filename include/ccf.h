@@ -94,11 +94,23 @@ ccf_status ccf_velocity_from_vorticity(ccf_ctx* ctx, const double* lam_w, const 
                                        double* gam_v);
 ccf_status ccf_nonlinear(ccf_ctx* ctx, const double* lam_v, const double* gam_v, const double* lam_w,
                          const double* gam_w, double* lam_out, double* gam_out);
+/* nonlinear_term(v, omega, dealias_two_thirds) (ptns.hpp:68-70; rule ptns.cpp:100-110) */
+ccf_status ccf_nonlinear_ex(ccf_ctx* ctx, const double* lam_v, const double* gam_v, const double* lam_w,
+                            const double* gam_w, int dealias_two_thirds, double* lam_out, double* gam_out);
 
 /* ptns.hpp:84-127 NSStepper (ramp bootstrap). State lives on the device. */
 ccf_status ccf_ns_create(ccf_ctx* ctx, double reynolds, double h, int order, int disable_nonlinear,
                          const double* lam0, const double* gam0, ccf_ns_state** out);
+/* NSConfig flags (ptns.hpp:84-94): bit 0 disable_nonlinear (Stokes limit), bit 1 dealias_two_thirds,
+ * bit 2 compute_gamma_psi (diagnostic Poisson solve, read with ccf_ns_gamma_psi). */
+ccf_status ccf_ns_create_ex(ccf_ctx* ctx, double reynolds, double h, int order, int flags, const double* lam0,
+                            const double* gam0, ccf_ns_state** out);
 ccf_status ccf_ns_step(ccf_ns_state* st, int nsteps);
+/* NSStepper::velocity(): velocity PT scalars of the current state (fresh psi solve, ptns.cpp:205-215). */
+ccf_status ccf_ns_velocity(ccf_ns_state* st, double* lam_v, double* gam_v);
+/* NSState::gamma_psi = solve_poisson_3d(-gamma_omega) of the omega the last step started from
+ * (ptns.cpp:248-253); CCF_CONFIG_ERROR without the flag, CCF_DOMAIN_ERROR before the first step. */
+ccf_status ccf_ns_gamma_psi(ccf_ns_state* st, double* gamma_psi);
 ccf_status ccf_ns_get_omega(ccf_ns_state* st, double* lam, double* gam, double* time, int* steps_taken);
 ccf_status ccf_ns_destroy(ccf_ns_state* st);
 

@@ -298,11 +298,10 @@ inline PTScalars velocity_from_vorticity(const PTScalars& w, double tol = kDefau
     return o;
 }
 inline PTScalars nonlinear_term(const PTScalars& v, const PTScalars& w, bool dealias_two_thirds = false) {
-    if (dealias_two_thirds) throw DomainError("nonlinear_term: 2/3 dealiasing is not on the B200 hot path");
     PTScalars o(v.lambda.spec);
     ccf_ctx* c = detail::context(v.lambda.spec);
-    detail::check(ccf_nonlinear(c, v.lambda.raw(), v.gamma.raw(), w.lambda.raw(), w.gamma.raw(), o.lambda.raw(),
-                                o.gamma.raw()),
+    detail::check(ccf_nonlinear_ex(c, v.lambda.raw(), v.gamma.raw(), w.lambda.raw(), w.gamma.raw(),
+                                   dealias_two_thirds ? 1 : 0, o.lambda.raw(), o.gamma.raw()),
                   c);
     return o;
 }
@@ -313,15 +312,18 @@ struct NSConfig {
     double h = 1e-2;
     int order = 4;
     double adi_tol = kDefaultAdiTol;
-    bool disable_nonlinear = false;
+    bool disable_nonlinear = false;   // Stokes limit
+    bool dealias_two_thirds = false;
+    bool compute_gamma_psi = false;   // diagnostic-only extra Poisson solve (gamma_psi())
 };
 
 class NSStepper {  // ramp bootstrap; state resident on the GPU between steps
 public:
     NSStepper(const NSConfig& cfg, const PTScalars& omega0) : cfg_(cfg), omega_(cfg.spec) {
         ctx_ = detail::context(cfg.spec, cfg.adi_tol);
-        detail::check(ccf_ns_create(ctx_, cfg.reynolds, cfg.h, cfg.order, cfg.disable_nonlinear ? 1 : 0,
-                                    omega0.lambda.raw(), omega0.gamma.raw(), &st_),
+        const int flags = (cfg.disable_nonlinear ? 1 : 0) | (cfg.dealias_two_thirds ? 2 : 0) | (cfg.compute_gamma_psi ? 4 : 0);
+        detail::check(ccf_ns_create_ex(ctx_, cfg.reynolds, cfg.h, cfg.order, flags, omega0.lambda.raw(),
+                                       omega0.gamma.raw(), &st_),
                       ctx_);
     }
     ~NSStepper() { ccf_ns_destroy(st_); }
@@ -335,6 +337,16 @@ public:
     }
     double time() const { return time_; }
     const NSConfig& config() const { return cfg_; }
+    PTScalars velocity() const {  // velocity scalars of the current state (fresh psi solve)
+        PTScalars v(cfg_.spec);
+        detail::check(ccf_ns_velocity(st_, v.lambda.raw(), v.gamma.raw()), ctx_);
+        return v;
+    }
+    CoeffTensor gamma_psi() const {  // NSState::gamma_psi under compute_gamma_psi
+        CoeffTensor g(cfg_.spec);
+        detail::check(ccf_ns_gamma_psi(st_, g.raw()), ctx_);
+        return g;
+    }
 
 private:
     NSConfig cfg_;

@@ -210,7 +210,8 @@ void* orc_ns_create(int m, int n, int p, double re, double h, int order, double 
         cfg.h = h;
         cfg.order = order;
         cfg.tol = tol;
-        cfg.disable_nonlinear = disable_nonlinear != 0;
+        cfg.disable_nonlinear = (disable_nonlinear & 1) != 0;  // flags: bit 0 disable_nonlinear, bit 1 dealias
+        cfg.dealias = (disable_nonlinear & 2) != 0;
         return new NSStepper(cfg, {load(m, n, p, lam0), load(m, n, p, gam0)});
     } catch (const std::exception& e) {
         g_err = e.what();

@@ -264,12 +264,12 @@ def nonlinear(vl, vg, wl, wg, dealias=False):
 class NSStepper:
     """proj/src/ptns.cpp:177-267 NSStepper (ramp bootstrap)."""
 
-    def __init__(self, lam0, gam0, reynolds, h, order=4, tol=1e-12, disable_nonlinear=False):
+    def __init__(self, lam0, gam0, reynolds, h, order=4, tol=1e-12, disable_nonlinear=False, dealias=False):
         l, g = _cz(lam0), _cz(gam0)
         self.shape = l.shape
         p, n, m = l.shape
         self.h = lib().orc_ns_create(m, n, p, C.c_double(reynolds), C.c_double(h), int(order), C.c_double(tol),
-                                     int(disable_nonlinear), _p(l), _p(g))
+                                     int(bool(disable_nonlinear)) | (2 if dealias else 0), _p(l), _p(g))
         if not self.h:
             raise OracleError(9, lib().orc_last_error().decode())
 

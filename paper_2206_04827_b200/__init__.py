@@ -87,7 +87,8 @@ EXPORTS = ["ccf_ctx_create", "ccf_ctx_destroy", "ccf_ctx_set_stream", "ccf_ctx_s
            "ccf_diag_host_check", "ccf_shard_init", "ccf_shard_partition", "ccf_shard_info", "ccf_shard_ipc_handle",
            "ccf_shard_open_ipc", "ccf_shard_link_local", "ccf_shard_set_host_barrier", "ccf_write_field",
            "ccf_read_field_header", "ccf_read_field", "ccf_crc32", "ccf_ns_write_omega", "ccf_heat_create",
-           "ccf_heat_step", "ccf_heat_get"]
+           "ccf_heat_step", "ccf_heat_get", "ccf_ns_create_ex", "ccf_ns_velocity", "ccf_ns_gamma_psi",
+           "ccf_nonlinear_ex"]
 
 HOST_BARRIER_FN = C.CFUNCTYPE(None, C.c_void_p)
 SHARD_HANDLE_BYTES = 128  # include/ccf.h CCF_SHARD_HANDLE_BYTES
@@ -169,6 +170,10 @@ def lib():
         L.ccf_heat_create.argtypes = [vp, C.c_double, C.c_double, C.c_int, vp, C.c_int, C.POINTER(vp)]
         L.ccf_heat_step.argtypes = [vp, vp, C.c_int]
         L.ccf_heat_get.argtypes = [vp, vp, dp, C.POINTER(C.c_int)]
+        L.ccf_ns_create_ex.argtypes = [vp, C.c_double, C.c_double, C.c_int, C.c_int, vp, vp, C.POINTER(vp)]
+        L.ccf_ns_velocity.argtypes = [vp, vp, vp]
+        L.ccf_ns_gamma_psi.argtypes = [vp, vp]
+        L.ccf_nonlinear_ex.argtypes = [vp, vp, vp, vp, vp, C.c_int, vp, vp]
         _lib = L
     return _lib
 
@@ -322,10 +327,10 @@ class Context:
                                                       *[_addr(x) for x in o]))
         return tuple(o)
 
-    def nonlinear_term(self, lam_v, gam_v, lam_w, gam_w):
+    def nonlinear_term(self, lam_v, gam_v, lam_w, gam_w, dealias_two_thirds=False):
         o = [self._out_c() for _ in range(2)]
-        self._check(lib().ccf_nonlinear(self.h, _addr(_c128(lam_v)), _addr(_c128(gam_v)), _addr(_c128(lam_w)),
-                                        _addr(_c128(gam_w)), *[_addr(x) for x in o]))
+        self._check(lib().ccf_nonlinear_ex(self.h, _addr(_c128(lam_v)), _addr(_c128(gam_v)), _addr(_c128(lam_w)),
+                                           _addr(_c128(gam_w)), int(bool(dealias_two_thirds)), *[_addr(x) for x in o]))
         return tuple(o)
 
     # ---- mode sharding (csrc/shard.cu)
@@ -492,12 +497,26 @@ def read_field(path, out=None):
 class NSStepper:
     """proj/include/cylspec/ptns.hpp:104-127 NSStepper on the device (ramp bootstrap)."""
 
-    def __init__(self, ctx: Context, lam0, gam0, reynolds, h, order=4, disable_nonlinear=False):
+    def __init__(self, ctx: Context, lam0, gam0, reynolds, h, order=4, disable_nonlinear=False,
+                 dealias_two_thirds=False, compute_gamma_psi=False):
         self.ctx = ctx
         st = C.c_void_p()
-        ctx._check(lib().ccf_ns_create(ctx.h, C.c_double(reynolds), C.c_double(h), int(order), int(disable_nonlinear),
-                                       _addr(_c128(lam0)), _addr(_c128(gam0)), C.byref(st)))
+        flags = int(bool(disable_nonlinear)) | (2 if dealias_two_thirds else 0) | (4 if compute_gamma_psi else 0)
+        ctx._check(lib().ccf_ns_create_ex(ctx.h, C.c_double(reynolds), C.c_double(h), int(order), flags,
+                                          _addr(_c128(lam0)), _addr(_c128(gam0)), C.byref(st)))
         self.h = st
+
+    def velocity(self):
+        """NSStepper::velocity(): velocity PT scalars of the current state (fresh psi solve)."""
+        o = [self.ctx._out_c() for _ in range(2)]
+        self.ctx._check(lib().ccf_ns_velocity(self.h, *[_addr(x) for x in o]))
+        return tuple(o)
+
+    def gamma_psi(self):
+        """state().gamma_psi: Poisson3D(-gamma_omega) of the omega the last step started from."""
+        o = self.ctx._out_c()
+        self.ctx._check(lib().ccf_ns_gamma_psi(self.h, _addr(o)))
+        return o
 
     def step(self, nsteps=1):
         self.ctx._check(lib().ccf_ns_step(self.h, int(nsteps)))

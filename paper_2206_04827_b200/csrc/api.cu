@@ -321,9 +321,9 @@ ccf_status ccf_velocity_from_vorticity(ccf_ctx* ctx, const double* lam_w, const 
     });
 }
 
-ccf_status ccf_nonlinear(ccf_ctx* ctx, const double* lam_v, const double* gam_v, const double* lam_w,
-                         const double* gam_w, double* lam_out, double* gam_out) {
-    // proj/src/ptns.cpp:114-149
+ccf_status ccf_nonlinear_ex(ccf_ctx* ctx, const double* lam_v, const double* gam_v, const double* lam_w,
+                            const double* gam_w, int dealias_two_thirds, double* lam_out, double* gam_out) {
+    // proj/src/ptns.cpp:114-149 (dealias: ptns.cpp:100-110, 140-144)
     return guard(ctx, [&](Ctx& c) {
         c.require_unsharded("ccf_nonlinear");
         ccf::Pipeline& P = ctx->pl();
@@ -332,11 +332,16 @@ ccf_status ccf_nonlinear(ccf_ctx* ctx, const double* lam_v, const double* gam_v,
         c.load_coeff(gam_v, b, false, 0, 1);
         c.load_coeff(lam_w, d, false, 0, 2);
         c.load_coeff(gam_w, e, false, 0, 3);
-        P.nonlinear(a, b, d, e, o1, o2);
+        P.nonlinear(a, b, d, e, o1, o2, nullptr, false, false, dealias_two_thirds != 0);
         c.store_coeff(o1, lam_out, false, 0, 0);
         c.store_coeff(o2, gam_out, false, 0, 1);
         c.sync();
     });
+}
+
+ccf_status ccf_nonlinear(ccf_ctx* ctx, const double* lam_v, const double* gam_v, const double* lam_w,
+                         const double* gam_w, double* lam_out, double* gam_out) {
+    return ccf_nonlinear_ex(ctx, lam_v, gam_v, lam_w, gam_w, 0, lam_out, gam_out);
 }
 
 ccf_status ccf_pt_synthesize(ccf_ctx* ctx, const double* lam, const double* gam, double* vr, double* vt, double* vz) {
@@ -468,7 +473,8 @@ namespace {
 // NSStepper (ptns.cpp:180-215) and HeatStepper (timestep.cpp:110-129) construction. scalar: one field
 // (lam0; gam unused), which is also the heat stepper's state; lam0 holds grid values when values != 0.
 ccf_ns_state* ns_create_impl(ccf_ctx* ctx, Ctx& c, double reynolds, double h, int order, bool disable_nonlinear,
-                             const double* lam0, const double* gam0, bool scalar, bool values) {
+                             const double* lam0, const double* gam0, bool scalar, bool values, bool dealias = false,
+                             bool gamma_psi = false) {
     if (order < 1 || order > 4) throw Error(ccf::DOMAIN_ERROR, "BDFScheme: order must be in {1,2,3,4}");
     if (c.m % 2) throw Error(ccf::DOMAIN_ERROR, "NSStepper: even m required for the nonlinear pipeline");
     auto st = std::make_unique<ccf_ns_state>();
@@ -480,6 +486,8 @@ ccf_ns_state* ns_create_impl(ccf_ctx* ctx, Ctx& c, double reynolds, double h, in
     s.order = order;
     s.disable_nonlinear = disable_nonlinear;
     s.scalar = scalar;
+    s.dealias = dealias;
+    s.gamma_psi = gamma_psi;
     const long T = s.pl->T;
     for (int i = 0; i < 5; ++i) {
         s.lam[i].alloc(size_t(T));
@@ -531,6 +539,7 @@ ccf_ns_state* ns_create_impl(ccf_ctx* ctx, Ctx& c, double reynolds, double h, in
             if (!scalar) P.to_eigen(pset, s.gam[0].p, s.zg[0].p);
         }
     }
+    if (dealias && !disable_nonlinear) s.pl->ensure_dealias(s.eigen ? &pset : nullptr);  // before any graph capture
     if (c.sh.sharded() && !s.eigen)
         throw Error(ccf::CONFIG_ERROR, "NSStepper: a mode-sharded context needs the eigen-coordinate state "
                                        "(composite nonlinear term, fast-diagonalization solves)");
@@ -547,6 +556,44 @@ ccf_status ccf_ns_create(ccf_ctx* ctx, double reynolds, double h, int order, int
         *out = ns_create_impl(ctx, c, reynolds, h, order, disable_nonlinear != 0, lam0, gam0, false, false);
     });
 }
+
+// NSConfig flags (ptns.hpp:84-94): bit 0 disable_nonlinear, bit 1 dealias_two_thirds, bit 2 compute_gamma_psi
+ccf_status ccf_ns_create_ex(ccf_ctx* ctx, double reynolds, double h, int order, int flags, const double* lam0,
+                            const double* gam0, ccf_ns_state** out) {
+    return guard(ctx, [&](Ctx& c) {
+        if (!lam0 || !gam0) throw Error(ccf::DOMAIN_ERROR, "NSStepper: initial vorticity required");
+        *out = ns_create_impl(ctx, c, reynolds, h, order, (flags & 1) != 0, lam0, gam0, false, false, (flags & 2) != 0,
+                              (flags & 4) != 0);
+    });
+}
+
+ccf_status ccf_ns_velocity(ccf_ns_state* st, double* lam_v, double* gam_v) {
+    if (!st) return CCF_INTERNAL_ERROR;
+    return guard(st->ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_ns_velocity");
+        const long T = st->st.pl->T;
+        ccf::DBuf a{static_cast<size_t>(T)}, b{static_cast<size_t>(T)};
+        st->st.velocity_coeff(a.p, b.p);
+        c.store_coeff(a.p, lam_v, false, 0, 0);
+        c.store_coeff(b.p, gam_v, false, 0, 1);
+        c.sync();
+    });
+}
+
+ccf_status ccf_ns_gamma_psi(ccf_ns_state* st, double* out) {
+    if (!st) return CCF_INTERNAL_ERROR;
+    return guard(st->ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_ns_gamma_psi");
+        if (!st->st.gamma_psi) throw Error(ccf::CONFIG_ERROR, "NSStepper: compute_gamma_psi is off");
+        ccf::DBuf a{static_cast<size_t>(st->st.pl->T)};
+        st->st.gamma_psi_coeff(a.p);
+        c.store_coeff(a.p, out, false, 0, 0);
+        c.sync();
+    });
+}
+
+ccf_status ccf_nonlinear_ex(ccf_ctx* ctx, const double* lam_v, const double* gam_v, const double* lam_w,
+                            const double* gam_w, int dealias_two_thirds, double* lam_out, double* gam_out);
 
 // ---- HeatStepper / heat_run (proj/include/cylspec/timestep.hpp:60-111, proj/src/timestep.cpp:110-170)
 ccf_status ccf_heat_create(ccf_ctx* ctx, double alpha, double h, int order, const double* initial, int initial_kind,

@@ -830,10 +830,89 @@ void Pipeline::ensure_composite() {
 //   a  = v x w pointwise in theta (register FFTs)
 //   Y  = z analysis of (a_r, a_t, a_z, dz a_r, dz a_t)
 //   (gamma_N, lambda_N) = per-slot composite r operators (curl + decompose + r analysis) on Y
+void Pipeline::ensure_dealias(DevSet* eig) {
+    const Geo& g = c.gh;
+    const int m = c.m, n = c.n, nh = g.nh, mh = g.mh;
+    if (!dealias_ready_) {
+        const int jmax = 2 * m / 3, kmax = 2 * n / 3;  // ptns.cpp:101-103
+        const long Lz = n - 1;
+        auto zan = [&](int k, int kz) {
+            const int s = n - 1 - kz;
+            const long double eps = (k == 0 || k == n - 1) ? 0.5L : 1.0L;
+            const long double ws = (s == 0 || s == n - 1) ? 1.0L : 2.0L;
+            return eps / (long double)Lz * ws * cospi_frac(long(k) * s, Lz);
+        };
+        auto dzm = [&](int k, int kp) -> long double {
+            if (kp <= k || ((kp - k) & 1) == 0) return 0.0L;
+            return (k == 0 ? 1.0L : 2.0L) * (long double)kp;
+        };
+        // analysis with the k >= kmax coefficients dropped; dz acts on the masked coefficients
+        std::vector<double> A(size_t(n) * nh, 0.0), AD(size_t(n) * nh, 0.0);
+        for (int par = 0; par < 2; ++par)
+            for (int i = 0; i < nh; ++i)
+                for (int q = 0; q < nh; ++q)
+                    if (2 * q + par < kmax) A[size_t(par) * nh * nh + size_t(i) * nh + q] = double(2.0L * zan(2 * q + par, nh + i));
+        for (int po = 0; po < 2; ++po) {
+            const int pi = 1 - po;
+            for (int i = 0; i < nh; ++i)
+                for (int q = 0; q < nh; ++q) {
+                    long double acc = 0.0L;
+                    for (int qp = 0; qp < nh; ++qp) {
+                        if (2 * qp + pi >= kmax) continue;
+                        const long double d = dzm(2 * q + po, 2 * qp + pi);
+                        if (d != 0.0L) acc += 2.0L * zan(2 * qp + pi, nh + i) * d;
+                    }
+                    AD[size_t(po) * nh * nh + size_t(i) * nh + q] = double(acc);
+                }
+        }
+        upload(AzD_, A);
+        upload(ADzD_, AD);
+        // composite curl / decompose on the r analysis with the j >= jmax coefficients dropped
+        RadialTables rt = tp.rt;
+        for (int j0 = 0; j0 < 2; ++j0)
+            for (int i = 0; i < mh; ++i)
+                if (2 * i + j0 >= jmax)
+                    for (int jr = 0; jr < mh; ++jr) rt.ArT[j0][size_t(i) * mh + jr] = 0.0;
+        analD_ = build_anal_composite(rt);
+        upload(danalD_, analD_.blocks);
+        dealias_ready_ = true;
+    }
+    if (eig && eigD_set_ != eig) {  // eigen-coordinate forms (as ensure_eigen)
+        const int N = c.N, M = c.M, Np = N + (N & 1);
+        eig_AzPD_.alloc(size_t(2) * nh * Np);
+        eig_ADzPD_.alloc(size_t(2) * nh * Np);
+        GemmPlan gp;
+        for (int k0 = 0; k0 < 2; ++k0)
+            for (int d = 0; d < 2; ++d) {
+                gp.A.push_back((d ? ADzD_.p : AzD_.p) + size_t(k0) * nh * nh);
+                gp.B.push_back(eig->dg + eig->host.dg_right[k0]);
+                gp.C.push_back((d ? eig_ADzPD_.p : eig_AzPD_.p) + size_t(k0) * nh * Np);
+            }
+        gp.M = nh; gp.N = N; gp.K = nh; gp.lda = nh; gp.ldb = Np; gp.ldc = Np;
+        gp.upload();
+        gp.launch(c.stream);
+        eig_analD_.alloc(analD_.blocks.size());
+        GemmPlan ga;
+        for (int s = 0; s < g.nslots; ++s)
+            for (const CompositeTerm& ct : analD_.terms[size_t(s)]) {
+                ga.A.push_back(eig->dg + eig->host.dg_left[size_t(s)]);
+                ga.B.push_back(danalD_.p + ct.off);
+                ga.C.push_back(eig_analD_.p + ct.off);
+            }
+        ga.M = M; ga.N = mh; ga.K = mh; ga.lda = mh; ga.ldb = mh; ga.ldc = mh;
+        ga.upload();
+        ga.launch(c.stream);
+        CCF_CUDA(cudaStreamSynchronize(c.stream));
+        eigD_set_ = eig;
+    }
+}
+
 void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w,
-                         double* lam_n, double* gam_n, DevSet* eig, bool zpre, bool eigY) {
+                         double* lam_n, double* gam_n, DevSet* eig, bool zpre, bool eigY, bool dealias) {
     ensure_composite();
     if (eig && comp_off_) throw Error(INTERNAL, "nonlinear: eigen-coordinate output needs the composite path");
+    if (dealias && comp_off_) throw Error(CONFIG_ERROR, "nonlinear: 2/3 dealiasing needs the composite path");
+    if (dealias) ensure_dealias(eig);
     if (comp_off_) {
         if (c.sh.sharded()) throw Error(CONFIG_ERROR, "nonlinear: the pencil path (CCF_NONLINEAR_PENCIL=1) has no sharded form");
         nonlinear_pencil(lam_v, gam_v, lam_w, gam_w, lam_n, gam_n);
@@ -927,14 +1006,15 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     // eigen mode (eig != nullptr): the z analysis carries PR of the shared modal basis, Y_x half k0 =
     // values * (Az PR)[k0] (N columns, leading dimension 2 Np), see ensure_eigen
     const int Np = c.N + (c.N & 1);
-    const int ecls[8] = {eig ? 1 : 0, 0, 0, 0, 0, 0, 0, 0};
+    const int ecls[8] = {eig ? 1 : 0, int(dealias), 0, 0, 0, 0, 0, 0};
     // the analysis side reads only scratch tensors: key it on the outputs
     const void* okeyp[2] = {lam_n, gam_n};
     GemmPlan& za = gemm(ptr_key("nza", 2, okeyp, okeyp, ecls), fresh);
     if (fresh) {
         for (int x = 0; x < 5; ++x) {
             const double* src = av[x < 3 ? x : x - 3];
-            const double* mat = eig ? (x >= 3 ? eig_ADzP_.p : eig_AzP_.p) : (x >= 3 ? tp.ADz.p : tp.Az.p);
+            const double* mat = dealias ? (eig ? (x >= 3 ? eig_ADzPD_.p : eig_AzPD_.p) : (x >= 3 ? ADzD_.p : AzD_.p))
+                                        : (eig ? (x >= 3 ? eig_ADzP_.p : eig_AzP_.p) : (x >= 3 ? tp.ADz.p : tp.Az.p));
             const long mstride = eig ? long(g.nh) * Np : long(g.nh) * g.nh;
             for (int s = c.sh.s_lo; s < c.sh.s_hi; ++s)
                 for (int pl = 0; pl < 2; ++pl) {
@@ -964,12 +1044,14 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     // eigen mode: blocks PL_P A_t (M x mh) and output in the eigen layout (M x 2 Np per slot, plane)
     GemmPlan& ra = gemm(ptr_key("nra", 2, okeyp, okeyp, ecls), fresh);
     if (fresh) {
+        const CompositeSet& an = dealias ? analD_ : anal_;
+        const double* blocks = dealias ? (eig ? eig_analD_.p : danalD_.p) : (eig ? eig_anal_.p : danal_.p);
         for (int s = c.sh.s_lo; s < c.sh.s_hi; ++s)
             for (int o = 0; o < 4; ++o) {
                 ra.tstart.push_back(int(ra.A.size()));
-                for (const CompositeTerm& ct : anal_.terms[size_t(s)]) {
+                for (const CompositeTerm& ct : an.terms[size_t(s)]) {
                     if (ct.out != o) continue;
-                    ra.A.push_back(eig ? eig_anal_.p + ct.off : danal_.p + ct.off);
+                    ra.A.push_back(blocks + ct.off);
                     ra.B.push_back(eig ? Y[ct.in / 2] + long(s) * g.slot_stride + long(ct.in % 2) * g.mh * 2 * Np
                                        : Y[ct.in / 2] + long(s) * g.slot_stride + long(ct.in % 2) * g.plane_stride);
                 }
@@ -988,6 +1070,16 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     ra.launch(c.stream);
     c.gemm_flops += ra.flops();
     c.launches += 1;
+    if (dealias) {  // |w| >= 2 (p/2) / 3: the whole slot of N is zero (a is masked, curl / decompose act per slot)
+        const int s0 = std::max(2 * (c.p / 2) / 3, c.sh.s_lo), s1 = c.sh.s_hi;
+        if (s0 < s1) {
+            const int Np = c.N + (c.N & 1);
+            const long per = eig ? 2L * c.M * 2 * Np : g.slot_stride;
+            const long off = eig ? eig_off(s0, 0, 0) : long(s0) * g.slot_stride;
+            for (double* t : {lam_n, gam_n})
+                CCF_CUDA(cudaMemsetAsync(t + off, 0, sizeof(double) * size_t(per) * size_t(s1 - s0), c.stream));
+        }
+    }
     c.mark("C_curl_decompose");
 }
 
@@ -1812,7 +1904,7 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
                 double* lpsi = P.scratch(18);
                 P.eigen_back(pset, 1, zpsi.p, zpsi.p, lpsi, lpsi);
                 c.mark("P_poisson_solve");
-                P.nonlinear(gw, lpsi, lw, gw, nl[nnew].p, ng[nnew].p, &pset);  // N~ = PL_P N PR
+                P.nonlinear(gw, lpsi, lw, gw, nl[nnew].p, ng[nnew].p, &pset, false, false, dealias);  // N~ = PL_P N PR
             } else {
                 // velocity_from_vorticity (ptns.cpp:85-91): lambda_v = gamma_omega (scratch 4), gamma_v = lambda_psi
                 // (scratch 1, 2). In the steady state the previous step's Helmholtz back transform produced
@@ -1822,7 +1914,7 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
                     c.mark("P_poisson_solve");
                 }
                 P.nonlinear(P.scratch(4), P.scratch(1), P.scratch(3), P.scratch(4), nl[nnew].p, ng[nnew].p, &pset,
-                            true, true);  // N~ = PL_P N PR
+                            true, true, dealias);  // N~ = PL_P N PR
             }
         }
         const double* sl[kMaxSrc];
@@ -1865,7 +1957,7 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
             // step lambda_omega comes from our Helmholtz solve in the shared modal basis (modal_solve_from_z)
             if (!(zvalid && P.modal_solve_from_z(c.set(false, true, 1.0), -1.0, lpsi))) P.poisson(lw, -1.0, lpsi);
             c.mark("P_poisson_solve");
-            P.nonlinear(gw, lpsi, lw, gw, nl[nnew].p, ng[nnew].p);  // nonlinear_term(v, omega)
+            P.nonlinear(gw, lpsi, lw, gw, nl[nnew].p, ng[nnew].p, nullptr, false, false, dealias);  // nonlinear_term(v, omega)
         }
         const double* sl[kMaxSrc];
         const double* sg[kMaxSrc];
@@ -1932,6 +2024,42 @@ void NSState::zsynth_omega(int r) {
     P.eigen_ysynth(vel ? 3 : 2, z, oS, oD);
     zv_head = vel ? r : -1;
     P.zw_owner_ = this;
+}
+
+// NSStepper::velocity(): (lambda_v, gamma_v) = (gamma_omega, Poisson3D(-lambda_omega)) of the current state
+void NSState::velocity_coeff(double* lam_v, double* gam_v) {
+    Pipeline& P = *pl;
+    Ctx& c = P.c;
+    omega_coeff();
+    CCF_CUDA(cudaMemcpyAsync(lam_v, gam[head].p, sizeof(double) * size_t(P.T), cudaMemcpyDeviceToDevice, c.stream));
+    if (!eigen) {
+        P.poisson(lam[head].p, -1.0, gam_v);
+        return;
+    }
+    DevSet& pset = c.set(false, true, 1.0);
+    if (ztmp.n < size_t(P.T)) ztmp.alloc(size_t(P.T));
+    const double* zs[1] = {zl[head].p};
+    const double wm1[1] = {-1.0};
+    P.eigen_rhs(pset, 1, zs, zs, wm1, 1, 1.0, ztmp.p, ztmp.p);  // -Z_lambda .* RT_P
+    P.eigen_back(pset, 1, ztmp.p, ztmp.p, gam_v, gam_v);
+}
+
+// gamma_psi = Poisson3D(-gamma_omega) of the omega the last step started from (ptns.cpp:248-253)
+void NSState::gamma_psi_coeff(double* out) {
+    Pipeline& P = *pl;
+    Ctx& c = P.c;
+    if (steps == 0) throw Error(DOMAIN_ERROR, "NSStepper: gamma_psi is computed from the first step on");
+    const int prev = (head + 1) % 5;
+    if (!eigen) {
+        P.poisson(gam[prev].p, -1.0, out);
+        return;
+    }
+    DevSet& pset = c.set(false, true, 1.0);
+    if (ztmp.n < size_t(P.T)) ztmp.alloc(size_t(P.T));
+    const double* zs[1] = {zg[prev].p};
+    const double wm1[1] = {-1.0};
+    P.eigen_rhs(pset, 1, zs, zs, wm1, 1, 1.0, ztmp.p, ztmp.p);
+    P.eigen_back(pset, 1, ztmp.p, ztmp.p, out, out);
 }
 
 // coefficient-space omega of the newest ring slot (eigen mode keeps only Z between steps)

@@ -94,8 +94,10 @@ public:
     // eig != nullptr: output N~ = PL_P N PR in the eigen layout of that (Poisson) set's modal basis
     // zpre: scratch(0..5) already hold the z-synthesized inputs (lambda_v = gamma_w aliased to scratch(4));
     // eigY: those are eigen-coordinate Y tensors (eigen_ysynth), synthesized with the QL-folded blocks
+    // dealias: the reference's 2/3 rule on the analyzed cross product (ptns.cpp:100-110, 140-144): the j / k masks
+    // are folded into the analysis matrices, the |w| mask zeroes the output slots
     void nonlinear(const double* lam_v, const double* gam_v, const double* lam_w, const double* gam_w, double* lam_n,
-                   double* gam_n, DevSet* eig = nullptr, bool zpre = false, bool eigY = false);
+                   double* gam_n, DevSet* eig = nullptr, bool zpre = false, bool eigY = false, bool dealias = false);
     void eigen_ysynth(int ntensor, const double* const* z, double* const* outS, double* const* outD);
     // eigen-coordinate NS state (see pipeline.cu)
     long eig_off(int s, int pl, int k0) const;
@@ -149,6 +151,13 @@ public:  // internal state (used by the NS stepper and the C-ABI layer)
     std::map<const void*, const double**> zrt_;               // per set: RT table per Poisson task
     DevSet* eig_set_ = nullptr;                               // modal basis the folded blocks below belong to
     DBuf eig_AzP_, eig_ADzP_, eig_anal_, eig_QS_, eig_QD_;
+    // 2/3-dealiased analysis side (built on first use): z analysis (+ dz) with k >= 2n/3 masked, composite
+    // curl / decompose blocks with j >= 2m/3 masked, and their eigen-coordinate forms
+    bool dealias_ready_ = false;
+    DBuf AzD_, ADzD_, danalD_, eig_AzPD_, eig_ADzPD_, eig_analD_;
+    CompositeSet analD_;
+    DevSet* eigD_set_ = nullptr;
+    void ensure_dealias(DevSet* eig);
     std::map<const void*, const double* const*> eig_rt_;      // per set: RT table per (slot, k0)
     bool fd_fused_ = false, fd_attr_ = false;                    // CCF_FDSOLVE_FUSED=1: fused solve kernel
 };
@@ -158,6 +167,8 @@ struct NSState {
     double reynolds = 100, h = 1e-2;
     int order = 4, steps = 0;
     bool disable_nonlinear = false;
+    bool dealias = false;        // NSConfig::dealias_two_thirds
+    bool gamma_psi = false;      // NSConfig::compute_gamma_psi (evaluated on read, ccf_ns_gamma_psi)
     double time = 0;
     // omega history ring and nonlinear-term history ring, 5 slots each (the Helmholtz output
     // never aliases a live input; both heads advance in lockstep -> 5 graph phases)
@@ -179,6 +190,9 @@ struct NSState {
     bool scalar = false;
     bool forced = false;  // the next step adds kappa * forcing (zf: eigen coordinates, fh: coefficients)
     DBuf fh, zf;
+    DBuf ztmp, ctmp;  // velocity() / gamma_psi() scratch
+    void velocity_coeff(double* lam_v, double* gam_v);  // NSStepper::velocity (ptns.cpp:205-215), coefficients
+    void gamma_psi_coeff(double* out);                   // state().gamma_psi (ptns.cpp:248-253), coefficients
     ~NSState();
     void zsynth_omega(int r);
     void velocity(int r);

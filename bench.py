@@ -231,6 +231,42 @@ def secondary_configs(P, torch):
     return out
 
 
+def shard_selfcheck(P, rank, world, local, dist, red, host_barrier=None):
+    """Collective check of the mode-sharded path before it is measured: 7 NS steps at 32^3 sharded over
+    the job's ranks vs the unsharded stepper on each rank (own slots). Returns the max error over ranks
+    (inf if any rank failed)."""
+    import torch
+    from paper_2206_04827_b200 import shard as S
+    from tests.inputs import hermitian_coeffs
+    m = n = p = 32
+    lam, gam = hermitian_coeffs(m, n, p, 0.7, 3), hermitian_coeffs(m, n, p, 0.7, 103)
+    err = float("inf")
+    try:
+        c = P.Context(m, n, p, device=local).shard(rank, world)
+        S.connect(c)
+        if host_barrier is not None:
+            c.set_host_barrier(host_barrier)
+        st = P.NSStepper(c, lam, gam, reynolds=100.0, h=1e-3)
+        st.step(7)
+        wl, wg = st.omega()
+        info = c.shard_info()
+        st.close()
+        c.close()
+        r = P.Context(m, n, p, device=local)
+        rs = P.NSStepper(r, lam, gam, reynolds=100.0, h=1e-3)
+        rs.step(7)
+        rl, rg = rs.omega()
+        rs.close()
+        r.close()
+        sel = S.owned_slices(p, info["slot_lo"], info["slot_hi"])
+        err = max(float(np.abs(a[sel] - b[sel]).max() / np.abs(b).max()) for a, b in ((wl, rl), (wg, rg)))
+    except Exception as e:  # noqa: BLE001
+        print(f"[bench] rank {rank}: shard self-check failed: {e}", file=sys.stderr, flush=True)
+    t = torch.tensor([err], device=red)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_reference(args, cfg, rank):
     if rank != 0:
         return
@@ -305,6 +341,25 @@ def main():
     # slots in their owners' exchange buffers over NVLink (CUDA IPC), device-side rank barriers
     sharded = world > 1 and not args.replicas
     fallback = None
+    barrier_mode, selfcheck = None, None
+    if sharded:  # verify the sharded path on this node first: device barriers, else host barriers, else replicas
+        hb = dist.barrier if args.one_gpu_test else None
+        selfcheck = shard_selfcheck(P, rank, world, local, dist, red, hb)
+        barrier_mode = "host (one-GPU plumbing test)" if args.one_gpu_test else "device"
+        if not selfcheck <= 1e-12 and not args.one_gpu_test:
+            gloo = dist.new_group(backend="gloo")
+            selfcheck = shard_selfcheck(P, rank, world, local, dist, red, lambda: dist.barrier(group=gloo))
+            barrier_mode = "host (gloo)"
+            if not selfcheck <= 1e-12:
+                sharded = False
+                fallback = f"mode-sharded self-check failed (max rel err {selfcheck}); replicas measured instead"
+                barrier_mode = None
+        if barrier_mode == "host (gloo)":
+            host_barrier = lambda: dist.barrier(group=gloo)  # noqa: E731
+        elif args.one_gpu_test:
+            host_barrier = dist.barrier
+        else:
+            host_barrier = None
     while True:
         ctx = P.Context(m, n, p, device=local)
         ctx.set_stream(stream.cuda_stream)
@@ -314,8 +369,8 @@ def main():
                 from paper_2206_04827_b200 import shard as S
                 ctx.shard(rank, world)
                 S.connect(ctx)
-                if args.one_gpu_test:
-                    ctx.set_host_barrier(dist.barrier)
+                if host_barrier is not None:
+                    ctx.set_host_barrier(host_barrier)
             st = P.NSStepper(ctx, wl, wg, reynolds=cfg["reynolds"], h=cfg["h"], order=4)
             if args.no_graphs:
                 st.set_graphs(False)
@@ -455,8 +510,9 @@ def main():
                               "note": "GEMM stages at the DMMA peak + theta and RHS-combination passes at HBM peak"},
             "stage_ms": stages,
             "sharding": ({"mode": "fourier slots x theta rows, NVLink peer exchange (CUDA IPC), " +
-                                  ("host barriers, ONE-GPU PLUMBING TEST (not a measurement)" if args.one_gpu_test
-                                   else "device barriers"),
+                                  f"{barrier_mode} barriers" +
+                                  (", ONE-GPU PLUMBING TEST (not a measurement)" if args.one_gpu_test else ""),
+                          "selfcheck_max_rel_err": selfcheck,
                           "slots_rank0": ctx.shard_info()["slot_hi"] - ctx.shard_info()["slot_lo"],
                           "exchange_bytes_per_rank": S.exchange_bytes_per_rank(m, n, p, world)} if sharded else
                          ({"mode": "replicas", "note": fallback} if world > 1 else None)),

@@ -161,12 +161,13 @@ DevSet& Ctx::set(bool full, bool poisson, double scale) {
     const Geo& g = geo(full);
     std::vector<int> slot_w(size_t(g.nslots));
     for (int s = 0; s < g.nslots; ++s) slot_w[size_t(s)] = full ? s - p / 2 : (s == p / 2 ? -p / 2 : s);
+    SetupTimer tm(poisson ? "solver set (Poisson)" : "solver set (Helmholtz)");
     auto ds = std::make_unique<DevSet>();
     // flags bit1: execute the reference's shift counts (no tail-avoidance margin)
     // flags bit2: solve with the ADI kernel (the reference algorithm) instead of fast diagonalization
     // the ADI data (enclosures, shift plans, factor blocks) only when the ADI kernel is the solver
     ds->host = build_solver_set(*sizeops, slot_w, poisson, scale, tol, radial_cache, (flags & 1) != 0,
-                                (flags & 2) ? 1.0 : 4.0, (flags & 4) == 0, (flags & 4) != 0);
+                                (flags & 2) ? 1.0 : 4.0, (flags & 4) == 0, (flags & 4) != 0, false);
     const SolverSet& h = ds->host;
     if (h.has_diag) {
         CCF_CUDA(cudaMalloc(&ds->dg, h.dg.size() * sizeof(double)));

@@ -3,6 +3,9 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <string>
@@ -31,6 +34,19 @@ namespace ccf {
         CCF_CUDA(cudaMemcpy((dst), (src), (bytes), cudaMemcpyHostToDevice));           \
         CCF_CUDA(cudaStreamSynchronize(cudaStreamLegacy));                             \
     } while (0)
+
+// Setup-phase timer (CCF_SETUP_TRACE=1: one stderr line per phase).
+struct SetupTimer {
+    const char* what;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    explicit SetupTimer(const char* w) : what(w) {}
+    ~SetupTimer() {
+        static const bool on = std::getenv("CCF_SETUP_TRACE") != nullptr;
+        if (on)
+            std::fprintf(stderr, "[setup] %-28s %.3f s\n", what,
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
 
 // Device buffer (RAII).
 struct DBuf {

@@ -137,7 +137,7 @@ Range vertical_range(SizeOps& so, bool q2_pad) {
 
 SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poisson, double scale, double tol,
                            std::map<int, Range>& radial_cache, bool q2_pad, double plan_margin, bool with_diag,
-                           bool with_adi) {
+                           bool with_adi, bool keep_static) {
     if (!with_diag && !with_adi) throw Error(INTERNAL, "build_solver_set: nothing to build");
     const int m = so.m, n = so.n, M = (m - 2) / 2, N = (n - 2) / 2, mh = m / 2, nh = n / 2;
     const int lrows = ((M + 7) / 8) * 8 + 2, rrows = ((N + 7) / 8) * 8 + 2;  // zero-padded sweep rows
@@ -218,6 +218,16 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
             continue;
         }
         const int j0 = aw & 1;  // scalar class: j + w even
+        if (!with_adi && !keep_static && !(with_diag && !so.diag_poisson.count(aw))) {
+            // diagonalization data of this |w| already cached (the shared Poisson basis): nothing to build
+            if (with_diag) diag_in.push_back({aw, CBand{}, CBand{}, CBand{}});
+            AdiSlot d{};
+            d.j0 = j0;
+            built[aw] = d;
+            set.slots[size_t(s)] = d;
+            set.plans[size_t(s)].w = w;
+            continue;
+        }
         const Dense lw = radial_laplacian(so.ur, aw);
         Dense Af, Cf;
         if (poisson) {
@@ -239,6 +249,12 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
             // bands (R2, A, C | C02, B^T, D^T) are kept for host-side residual checks (diag_check_residual)
             AdiSlot d{};
             d.j0 = j0;
+            if (!keep_static) {
+                built[aw] = d;
+                set.slots[size_t(s)] = d;
+                set.plans[size_t(s)].w = w;
+                continue;
+            }
             d.sleft = alloc(size_t(M) * kStatW);
             d.sright0 = alloc(size_t(N) * kStatW);
             d.sright1 = alloc(size_t(N) * kStatW);

@@ -61,9 +61,10 @@ struct SolverSet {
 // plan_margin: executed shifts planned for tol / plan_margin (1 = the reference's shift count).
 // with_diag: also build the fast-diagonalization data (diag.hpp). with_adi = false: only the diagonalization
 // data (no enclosures, shift plans or ADI blocks: any size, fast setup; the ADI kernel cannot run on the set).
+// keep_static = false (with with_adi = false): not even the static operator bands of diag_check_residual.
 SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poisson, double scale, double tol,
                            std::map<int, Range>& radial_cache, bool q2_pad, double plan_margin = 1.0,
-                           bool with_diag = false, bool with_adi = true);
+                           bool with_diag = false, bool with_adi = true, bool keep_static = true);
 
 // Host check of the packed fast-diagonalization data of one (slot, k-parity) sub-problem: for a
 // seeded random RHS f (mh x nh), u = QL [(PL f PR) .* RT] QR in double (the device arithmetic),

@@ -3,6 +3,8 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <atomic>
+#include <thread>
 
 #include <cudaTypedefs.h>
 
@@ -41,6 +43,7 @@ unsigned blocks_for(long n, int t) { return unsigned((n + t - 1) / t); }
 }  // namespace
 
 TransformPlan::TransformPlan(Ctx& c) {
+    SetupTimer tm("transform tables");
     const int m = c.m, n = c.n, p = c.p, mh = m / 2, M = c.M;
     const long L = m - 1, Lz = n - 1;
     // r synthesis / analysis on the r > 0 half grid, per coefficient parity j0 (A operands):
@@ -161,25 +164,36 @@ TransformPlan::TransformPlan(Ctx& c) {
     {
         const Geo& g = c.gh;
         std::vector<double> hc(size_t(g.nslots) * M * 8, 0.0), hr(size_t(2) * M * 8, 0.0);
-        for (int s = 0; s < g.nslots; ++s) {
-            const int w = (s == p / 2) ? -p / 2 : s;
-            const int j0 = ((w % 2) + 2) % 2;
-            const Dense lw = recombine(radial_laplacian(c.sizeops->ur, w));
-            const CBand b = compress(lw, j0, M, M, -1, 2);
-            CLU lu;
-            try {
-                lu = banded_lu(b, 1, 2);
-            } catch (const Error&) {
-                throw Error(SINGULAR, "solve_horizontal_poisson: singular column system");
+        std::atomic<int> next{0}, bad{0};
+        auto work = [&] {  // per slot: O(m^2) recombination + banded LU, independent across slots
+            for (int s = next.fetch_add(1); s < g.nslots; s = next.fetch_add(1)) {
+                const int w = (s == p / 2) ? -p / 2 : s;
+                const int j0 = ((w % 2) + 2) % 2;
+                const Dense lw = recombine(radial_laplacian(c.sizeops->ur, w));
+                const CBand b = compress(lw, j0, M, M, -1, 2);
+                CLU lu;
+                try {
+                    lu = banded_lu(b, 1, 2);
+                } catch (const Error&) {
+                    bad = 1;
+                    continue;
+                }
+                for (int a = 0; a < M; ++a) {
+                    double* r = hc.data() + (size_t(s) * M + a) * 8;
+                    r[0] = lu.L[size_t(a)];
+                    r[1] = double(lu.piv[size_t(a)]);
+                    r[2] = lu.inv[size_t(a)];
+                    for (int t = 0; t < 3; ++t) r[3 + t] = lu.U[size_t(a) * 3 + t] * lu.inv[size_t(a)];
+                }
             }
-            for (int a = 0; a < M; ++a) {
-                double* r = hc.data() + (size_t(s) * M + a) * 8;
-                r[0] = lu.L[size_t(a)];
-                r[1] = double(lu.piv[size_t(a)]);
-                r[2] = lu.inv[size_t(a)];
-                for (int t = 0; t < 3; ++t) r[3 + t] = lu.U[size_t(a) * 3 + t] * lu.inv[size_t(a)];
-            }
+        };
+        {
+            const int nth = std::max(1, std::min<int>(int(std::thread::hardware_concurrency()), g.nslots));
+            std::vector<std::thread> pool;
+            for (int q = 0; q < nth; ++q) pool.emplace_back(work);
+            for (auto& th : pool) th.join();
         }
+        if (bad) throw Error(SINGULAR, "solve_horizontal_poisson: singular column system");
         for (int j0 = 0; j0 < 2; ++j0) {
             const CBand b = compress(c.sizeops->ur.r2, j0, M, mh, -1, 3);
             for (int a = 0; a < M; ++a)
@@ -212,6 +226,13 @@ TransformPlan::TransformPlan(Ctx& c) {
             return eps / (long double)Lz * ws * cospi_frac(long(k) * s, Lz);
         };
         std::vector<double> DS(size_t(n) * nh, 0.0), AD(size_t(n) * nh, 0.0);
+        // T_k(z_{nh+i}) and the analysis weights, tabulated once (the triple loops below are O(n^3))
+        std::vector<long double> Tk(size_t(n) * nh), Zk(size_t(n) * nh);
+        for (int k = 0; k < n; ++k)
+            for (int i = 0; i < nh; ++i) {
+                Tk[size_t(k) * nh + i] = cospi_frac(long(k) * (n - 1 - (nh + i)), Lz);
+                Zk[size_t(k) * nh + i] = zan(k, nh + i);
+            }
         for (int po = 0; po < 2; ++po) {
             const int pi = 1 - po;
             for (int qp = 0; qp < nh; ++qp)
@@ -220,7 +241,7 @@ TransformPlan::TransformPlan(Ctx& c) {
                     for (int q = 0; q < nh; ++q) {
                         const int k = 2 * q + po;
                         const long double d = dzm(k, 2 * qp + pi);
-                        if (d != 0.0L) acc += d * cospi_frac(long(k) * (n - 1 - (nh + i)), Lz);
+                        if (d != 0.0L) acc += d * Tk[size_t(k) * nh + i];
                     }
                     DS[size_t(po) * nh * nh + size_t(qp) * nh + i] = double(acc);
                 }
@@ -229,7 +250,7 @@ TransformPlan::TransformPlan(Ctx& c) {
                     long double acc = 0.0L;
                     for (int qp = 0; qp < nh; ++qp) {
                         const long double d = dzm(2 * q + po, 2 * qp + pi);
-                        if (d != 0.0L) acc += 2.0L * zan(2 * qp + pi, nh + i) * d;
+                        if (d != 0.0L) acc += 2.0L * Zk[size_t(2 * qp + pi) * nh + i] * d;
                     }
                     AD[size_t(po) * nh * nh + size_t(i) * nh + q] = double(acc);
                 }
@@ -815,6 +836,7 @@ void Pipeline::ensure_composite() {
     const char* e = std::getenv("CCF_NONLINEAR_PENCIL");
     comp_off_ = e && e[0] == '1';
     if (!comp_off_) {
+        SetupTimer tm("composite operators");
         synth_ = build_synth_composite(tp.rt);
         anal_ = build_anal_composite(tp.rt);
         upload(dsynth_, synth_.blocks);
@@ -1406,6 +1428,7 @@ __global__ void __launch_bounds__(128) eigen_rhs_kernel(EigRhs a) {
 
 void Pipeline::ensure_eigen(DevSet& pset) {
     if (eig_set_ == &pset) return;
+    SetupTimer tm("eigen-coordinate operators");
     ensure_composite();
     if (comp_off_ || !pset.host.has_diag || !pset.dg) throw Error(INTERNAL, "ensure_eigen: no shared modal basis");
     const Geo& g = c.gh;

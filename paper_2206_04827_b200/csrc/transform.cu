@@ -994,7 +994,7 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
             r[ip][7] = __ldg(fb + oo + ps + ip);
         }
     };
-    auto put_slot = [&](int a, const double (&r)[2][8]) {
+    auto put_slot = [&](int a, const double (&r)[2][8], int arr) {
         const int s = a / NQ, q = a - s * NQ;
         const double sg = (s & 1) ? -1.0 : 1.0;
         const bool reonly = (s == 0 || s == 128);
@@ -1007,46 +1007,55 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
                 const double sz = hh ? -1.0 : 1.0;
                 const double xar = sg * fma(sz, aro, ar), xai = reonly ? 0.0 : sg * fma(sz, aio, ai);
                 const double xbr = sg * fma(sz, bro, br), xbi = reonly ? 0.0 : sg * fma(sz, bio, bi);
-                double2* Zp = sd + (2 * (2 * q + ip) + hh) * 2 * kTWArr;
+                double2* Zp = sd + (2 * (2 * q + ip) + hh) * 2 * kTWArr + arr * kTWArr;
                 Zp[s] = make_double2(xar - xbi, xai + xbr);
                 if (s > 0 && s < 128) Zp[256 - s] = make_double2(xar + xbi, xbr - xai);
             }
         }
     };
-    if (tid < NT) fetch_slot(0, tid, raw);
-#pragma unroll
-    for (int pr = 0; pr < 3; ++pr) {
-        __syncthreads();  // previous pair's array fully consumed (and twiddles visible)
-        // ---- Hermitian spectrum of pair pr for the CTA's points into array 0
-        if (tid < NT) put_slot(tid, raw);
+    // Hermitian spectrum of pair pr for the CTA's points into array arr, then prefetch pair pr + 1
+    auto put_pair = [&](int pr, int arr) {
+        if (tid < NT) put_slot(tid, raw, arr);
         for (int a = tid + blockDim.x; a < NT; a += blockDim.x) {  // Nyquist slot tasks
             double r2[2][8];
             fetch_slot(pr, a, r2);
-            put_slot(a, r2);
+            put_slot(a, r2, arr);
         }
         if (pr < 2 && tid < NT) fetch_slot(pr + 1, tid, raw);
-        __syncthreads();
-        // ---- inverse pass 1: lane (n2 = col, h): DFT16 over n1 of x[16 n1 + n2] -> k1 = 2k + h
-        {
-            double2 x[16], o[8];
+    };
+    // inverse FFT of this warp's point from array ZA into the lane's 8 time samples
+    auto inverse = [&](double2* ZA, double2 (&out)[8]) {
+        double2 x[16], o[8];
+        // pass 1: lane (n2 = col, h): DFT16 over n1 of x[16 n1 + n2] -> k1 = 2k + h
 #pragma unroll
-            for (int n1 = 0; n1 < 16; ++n1) x[n1] = Z[16 * n1 + col];
-            __syncwarp();
-            half_dft16<+1>(x, h, o);
+        for (int n1 = 0; n1 < 16; ++n1) x[n1] = ZA[16 * n1 + col];
+        __syncwarp();
+        half_dft16<+1>(x, h, o);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int k1 = 2 * k + h;
-                double2 w = twf[16 * k1 + col];
-                w.y = -w.y;
-                Z[k1 * 17 + col] = cmul(o[k], w);
-            }
-            __syncwarp();
-            // ---- inverse pass 2: lane (k1 = col, h): DFT16 over n2 -> samples l = k1 + 16 (2j + h)
-#pragma unroll
-            for (int n2 = 0; n2 < 16; ++n2) x[n2] = Z[col * 17 + n2];
-            half_dft16<+1>(x, h, tv[pr]);
+        for (int k = 0; k < 8; ++k) {
+            const int k1 = 2 * k + h;
+            double2 w = twf[16 * k1 + col];
+            w.y = -w.y;
+            ZA[k1 * 17 + col] = cmul(o[k], w);
         }
-    }
+        __syncwarp();
+        // pass 2: lane (k1 = col, h): DFT16 over n2 -> samples l = k1 + 16 (2j + h)
+#pragma unroll
+        for (int n2 = 0; n2 < 16; ++n2) x[n2] = ZA[col * 17 + n2];
+        half_dft16<+1>(x, h, out);
+    };
+    // the three pairs alternate between the point's two arrays, so one CTA barrier per pair
+    // separates the cross-point spectrum writes from the warp-local FFTs
+    if (tid < NT) fetch_slot(0, tid, raw);
+    put_pair(0, 0);
+    __syncthreads();  // pair 0 in array 0 (and the twiddles) visible
+    put_pair(1, 1);
+    inverse(Z, tv[0]);
+    __syncthreads();  // pair 1 in array 1; every point's array 0 consumed
+    put_pair(2, 0);
+    inverse(Z + kTWArr, tv[1]);
+    __syncthreads();  // pair 2 in array 0
+    inverse(Z, tv[2]);
     // ---- cross product a = v x w (ptns.cpp:127-132) at this lane's 8 samples
     double2 ya[8], yz[8];
 #pragma unroll
@@ -1058,7 +1067,7 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
     }
     // ---- forward pass 1 (DFT16 over k2 for k1 = col): this lane holds k2 = 2j + h; radix-2 combine
     //      with the partner lane (h ^ 1), then twiddle and transpose into arrays 0 (a_r + i a_t), 1 (a_z)
-    __syncthreads();  // all warps done with array 0 of every point
+    __syncwarp();  // this warp's reads of its point's arrays done (no other warp touches them now)
     dft8<-1>(ya);
     dft8<-1>(yz);
     {

@@ -937,7 +937,7 @@ template <int NQ>
 __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(ThetaCross t) {
     constexpr int kPts = 4 * NQ;
     extern __shared__ double2 sd[];
-    double2* twf = sd + kPts * 2 * kTWArr;  // twf[16 k1 + n2] = e^{-2 pi i n2 k1 / 256}
+    double2* twf = sd + kPts * 2 * kTWArr;  // twf[16 k1 + n2] = e^{-2 pi i n2 k1 / 256} (forward stage)
     const Geo& g = t.g;
     const int S = g.nslots;  // 129
     const int jr = t.row0 + blockIdx.y;
@@ -1031,12 +1031,16 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
         for (int n1 = 0; n1 < 16; ++n1) x[n1] = ZA[16 * n1 + col];
         __syncwarp();
         half_dft16<+1>(x, h, o);
+        {  // conj twiddles e^{+2 pi i col (2k + h) / 256} by recurrence: base e^{2 pi i col h / 256}, step e^{4 pi i col / 256}
+            const double2 b = __ldg(t.tw + col), st0 = __ldg(t.tw + 2 * col);
+            double2 w = h ? make_double2(b.x, -b.y) : make_double2(1.0, 0.0);
+            const double2 st = make_double2(st0.x, -st0.y);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int k1 = 2 * k + h;
-            double2 w = twf[16 * k1 + col];
-            w.y = -w.y;
-            ZA[k1 * 17 + col] = cmul(o[k], w);
+            for (int k = 0; k < 8; ++k) {
+                const int k1 = 2 * k + h;
+                ZA[k1 * 17 + col] = (k || h) ? cmul(o[k], w) : o[0];
+                if (k < 7) w = (k || h) ? cmul(w, st) : st;
+            }
         }
         __syncwarp();
         // pass 2: lane (k1 = col, h): DFT16 over n2 -> samples l = k1 + 16 (2j + h)
@@ -1048,7 +1052,7 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
     // separates the cross-point spectrum writes from the warp-local FFTs
     if (tid < NT) fetch_slot(0, tid, raw);
     put_pair(0, 0);
-    __syncthreads();  // pair 0 in array 0 (and the twiddles) visible
+    __syncthreads();  // pair 0 in array 0 (and the twiddle table) visible
     put_pair(1, 1);
     inverse(Z, tv[0]);
     __syncthreads();  // pair 1 in array 1; every point's array 0 consumed

@@ -1160,6 +1160,155 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
 template __global__ void theta_cross256w_kernel<1>(ThetaCross);
 template __global__ void theta_cross256w_kernel<2>(ThetaCross);
 
+// ---------------------------------------------------------------------------------------------
+// p = 512 path: the generic kernel's structure (TJ points per CTA, three packed pairs in shared
+// memory) with three radix-8 passes (512 = 8^3, register DFT8 per butterfly) instead of nine
+// radix-2 stages. Input is stored in base-8 digit-reversed order and the passes are in-place DIT;
+// arrays are padded by one element per 8 (index i + i / 8) so that every pass is bank-conflict
+// free for 16-byte accesses.
+namespace {
+
+constexpr int kP512 = 512, kA512 = 576;  // padded array length
+__device__ __forceinline__ int zp512(int i) { return i + (i >> 3); }
+__device__ __forceinline__ int digrev8(int t) { return ((t & 7) << 6) | (t & 56) | (t >> 6); }
+
+template <int S>
+__device__ __forceinline__ void fft512_r8(double2* __restrict__ d, int cnt, const double2* __restrict__ tw) {
+#pragma unroll 1
+    for (int ls = 0; ls < 9; ls += 3) {  // span L = 8^(ls/3) of the merged sub-transforms
+        const int L = 1 << ls;
+        const int nbf = cnt * 64;
+        for (int i = threadIdx.x; i < nbf; i += blockDim.x) {
+            const int arr = i >> 6, j = i & 63;
+            const int pos = j & (L - 1), grp = j >> ls;
+            double2* base = d + arr * kA512;
+            const int i0 = grp * 8 * L + pos;
+            double2 v[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) v[r] = base[zp512(i0 + r * L)];
+            if (L > 1) {
+#pragma unroll
+                for (int r = 1; r < 8; ++r) {  // W_{8L}^{pos r} = e^{S 2 pi i pos r 64 / (L 512)}
+                    const int q = (pos * r) << (6 - ls);
+                    double2 w = q < 256 ? tw[q] : make_double2(-tw[q - 256].x, -tw[q - 256].y);
+                    if (S > 0) w.y = -w.y;
+                    v[r] = cmul(v[r], w);
+                }
+            }
+            dft8<S>(v);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) base[zp512(i0 + k * L)] = v[k];
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(256, 2) theta_cross512_kernel(ThetaCross t) {
+    extern __shared__ double2 sd[];
+    const Geo& g = t.g;
+    constexpr int P = kP512;
+    const int S = g.nslots;
+    const int TJ = t.tj;                 // points per CTA (even): point 2i -> +z, 2i+1 -> -z
+    const int jr = t.row0 + blockIdx.y;  // r > 0 grid row
+    const int q0 = blockIdx.x * (TJ / 2);
+    const int ntj = min(TJ / 2, g.nh - q0);
+    double2* Z = sd;  // 3 * TJ padded arrays (packed pairs)
+    const double2* tw = t.tw;  // P/2 twiddles exp(-2 pi i q / P)
+    const long ps = g.plane_stride, oo = g.nh;
+    // ---- Hermitian spectra of pairs (0,1) (2,3) (4,5) into digit-reversed slots
+    for (int e = threadIdx.x; e < 3 * TJ * P; e += blockDim.x) {
+        const int jl = e % TJ;
+        const int tt = (e / TJ) % P;
+        const int pr = e / (TJ * P);
+        const int pos = jl >> 1;
+        const double sgz = (jl & 1) ? -1.0 : 1.0;  // f(-z) = E - O
+        double2 z = make_double2(0.0, 0.0);
+        if (pos < ntj) {
+            const bool conjg = tt > P / 2;
+            const int s = conjg ? P - tt : tt;  // slot (P/2 = Nyquist)
+            const double sg = (s & 1) ? -1.0 : 1.0;
+            const long off = long(s) * g.slot_stride + long(jr) * g.n + q0 + pos + theta_slot_delta(t, s);
+            const double* fa = t.in[2 * pr];
+            const double* fb = t.in[2 * pr + 1];
+            double2 xa = make_double2(sg * fma(sgz, fa[off + oo], fa[off]), sg * fma(sgz, fa[off + oo + ps], fa[off + ps]));
+            double2 xb = make_double2(sg * fma(sgz, fb[off + oo], fb[off]), sg * fma(sgz, fb[off + oo + ps], fb[off + ps]));
+            if (s == 0 || s == P / 2) {  // Re only (transform.cpp:201)
+                xa.y = 0.0;
+                xb.y = 0.0;
+            }
+            if (conjg) {
+                xa.y = -xa.y;
+                xb.y = -xb.y;
+            }
+            z = make_double2(xa.x - xb.y, xa.y + xb.x);  // Xa + i Xb
+        }
+        Z[(pr * TJ + jl) * kA512 + zp512(digrev8(tt))] = z;
+    }
+    __syncthreads();
+    fft512_r8<+1>(Z, 3 * TJ, tw);
+    // ---- pointwise cross product a = v x w (ptns.cpp:127-132); (a_r + i a_t) and (a_z + 0 i) are
+    //      written digit-reversed into arrays [0, TJ) and [TJ, 2 TJ) for the forward transform. The
+    //      permutation crosses threads, so every sample is read (kPer per thread) before any write.
+    constexpr int kPer = 8;  // TJ * P / blockDim (host launches TJ = 4, 256 threads)
+    double2 A[kPer], B[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const int e = threadIdx.x + u * blockDim.x;
+        if (e < TJ * P) {
+            const int jl = e >> 9, l = e & (P - 1);
+            const double2 p0 = Z[(0 * TJ + jl) * kA512 + zp512(l)], p1 = Z[(1 * TJ + jl) * kA512 + zp512(l)],
+                          p2 = Z[(2 * TJ + jl) * kA512 + zp512(l)];
+            const double vr = p0.x, vt = p0.y, vz = p1.x, wr = p1.y, wt = p2.x, wz = p2.y;
+            A[u] = make_double2(vt * wz - vz * wt, vz * wr - vr * wz);
+            B[u] = make_double2(vr * wt - vt * wr, 0.0);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const int e = threadIdx.x + u * blockDim.x;
+        if (e < TJ * P) {
+            const int jl = e >> 9, l = zp512(digrev8(e & (P - 1)));
+            Z[(0 * TJ + jl) * kA512 + l] = A[u];
+            Z[(1 * TJ + jl) * kA512 + l] = B[u];
+        }
+    }
+    __syncthreads();
+    fft512_r8<-1>(Z, 2 * TJ, tw);
+    // ---- unpack X_a = (Z[t] + conj Z[P-t]) / 2, X_b = (Z[t] - conj Z[P-t]) / (2i); c_w = (-1)^w X[w mod P] / P
+    const double invp = 1.0 / double(P);
+    const int TP = TJ / 2;
+    for (int e = threadIdx.x; e < 3 * S * 2 * TP; e += blockDim.x) {
+        const int pos = e % TP;
+        const int pl = (e / TP) % 2;
+        const int s = (e / (2 * TP)) % S;
+        const int f = e / (2 * TP * S);  // output field 0..2
+        if (pos >= ntj) continue;
+        const int tt = s;  // s = P/2 is the Nyquist slot, w = -P/2 = P/2 (mod P)
+        const int arr0 = f < 2 ? 0 : TJ;
+        double xv[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const double2* base = Z + (arr0 + 2 * pos + h) * kA512;
+            const double2 zt = base[zp512(tt)], zm = base[zp512((P - tt) & (P - 1))];
+            double2 X;
+            if (f == 0 || f == 2) X = make_double2(0.5 * (zt.x + zm.x), 0.5 * (zt.y - zm.y));
+            else X = make_double2(0.5 * (zt.y + zm.y), -0.5 * (zt.x - zm.x));
+            xv[h] = pl ? X.y : X.x;
+        }
+        const double sg = ((s & 1) ? -1.0 : 1.0) * invp * 0.5;
+        const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride + long(jr) * g.n + q0 + pos +
+                         theta_slot_delta(t, s);
+        t.out[f][off] = sg * (xv[0] + xv[1]);         // E' = (f(+z) + f(-z)) / 2
+        t.out[f][off + g.nh] = sg * (xv[0] - xv[1]);  // O' = (f(+z) - f(-z)) / 2
+    }
+    if (t.world > 1) __threadfence_system();  // peer stores performed before the rank barrier
+}
+
+size_t theta_cross512_smem(int tj) { return size_t(3) * tj * kA512 * sizeof(double2); }
+
 size_t theta_cross256w_smem(int nq) { return (size_t(4 * nq) * 2 * kTWArr + 256) * sizeof(double2); }
 
 size_t theta_cross256_smem() { return (size_t(kT256Pts) * 3 * kT256Arr + 256) * sizeof(double2); }

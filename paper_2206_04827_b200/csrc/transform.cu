@@ -1164,12 +1164,15 @@ template __global__ void theta_cross256w_kernel<2>(ThetaCross);
 // p = 512 path: the generic kernel's structure (TJ points per CTA, three packed pairs in shared
 // memory) with three radix-8 passes (512 = 8^3, register DFT8 per butterfly) instead of nine
 // radix-2 stages. Input is stored in base-8 digit-reversed order and the passes are in-place DIT;
-// arrays are padded by one element per 8 (index i + i / 8) so that every pass is bank-conflict
-// free for 16-byte accesses.
+// arrays are padded (index i + i / 8 + i / 64) so that the passes and the digit-reversed spectrum
+// writes are bank-conflict free for 16-byte accesses. Global loads / stores are (pair or output,
+// slot) tasks covering the CTA's two z positions with 16-byte accesses, as in the p = 256 kernel.
 namespace {
 
-constexpr int kP512 = 512, kA512 = 576;  // padded array length
-__device__ __forceinline__ int zp512(int i) { return i + (i >> 3); }
+constexpr int kP512 = 512, kA512 = 584;  // padded array length
+// padding: one element per 8 and per 64, so unit-stride, stride-8 and stride-64 (digit-reversed
+// neighbours) 16-byte accesses of 8 lanes hit 8 distinct 4-bank groups
+__device__ __forceinline__ int zp512(int i) { return i + (i >> 3) + (i >> 6); }
 __device__ __forceinline__ int digrev8(int t) { return ((t & 7) << 6) | (t & 56) | (t >> 6); }
 
 template <int S>
@@ -1217,34 +1220,54 @@ __global__ void __launch_bounds__(256, 2) theta_cross512_kernel(ThetaCross t) {
     double2* Z = sd;  // 3 * TJ padded arrays (packed pairs)
     const double2* tw = t.tw;  // P/2 twiddles exp(-2 pi i q / P)
     const long ps = g.plane_stride, oo = g.nh;
-    // ---- Hermitian spectra of pairs (0,1) (2,3) (4,5) into digit-reversed slots
-    for (int e = threadIdx.x; e < 3 * TJ * P; e += blockDim.x) {
-        const int jl = e % TJ;
-        const int tt = (e / TJ) % P;
-        const int pr = e / (TJ * P);
-        const int pos = jl >> 1;
-        const double sgz = (jl & 1) ? -1.0 : 1.0;  // f(-z) = E - O
-        double2 z = make_double2(0.0, 0.0);
-        if (pos < ntj) {
-            const bool conjg = tt > P / 2;
-            const int s = conjg ? P - tt : tt;  // slot (P/2 = Nyquist)
-            const double sg = (s & 1) ? -1.0 : 1.0;
-            const long off = long(s) * g.slot_stride + long(jr) * g.n + q0 + pos + theta_slot_delta(t, s);
-            const double* fa = t.in[2 * pr];
-            const double* fb = t.in[2 * pr + 1];
-            double2 xa = make_double2(sg * fma(sgz, fa[off + oo], fa[off]), sg * fma(sgz, fa[off + oo + ps], fa[off + ps]));
-            double2 xb = make_double2(sg * fma(sgz, fb[off + oo], fb[off]), sg * fma(sgz, fb[off + oo + ps], fb[off + ps]));
-            if (s == 0 || s == P / 2) {  // Re only (transform.cpp:201)
-                xa.y = 0.0;
-                xb.y = 0.0;
+    // ---- Hermitian spectra of pairs (0,1) (2,3) (4,5) into digit-reversed slots; task (pair, slot)
+    //      loads both z positions of the tile and writes the 2 x 2 points' values at t = s and P - s
+    const bool vec = ((g.slot_stride | g.plane_stride | long(g.n) | long(g.nh)) & 1) == 0 && ntj == 2;
+    for (int a = threadIdx.x; a < 3 * (P / 2 + 1); a += blockDim.x) {
+        const int pr = a / (P / 2 + 1), s = a - pr * (P / 2 + 1);
+        const double sg = (s & 1) ? -1.0 : 1.0;
+        const bool reonly = (s == 0 || s == P / 2);  // Re only (transform.cpp:201)
+        const long off = long(s) * g.slot_stride + long(jr) * g.n + q0 + theta_slot_delta(t, s);
+        const double* __restrict__ fa = t.in[2 * pr] + off;
+        const double* __restrict__ fb = t.in[2 * pr + 1] + off;
+        double r[2][8];
+        if (vec) {
+            const double* src[8] = {fa, fa + ps, fa + oo, fa + oo + ps, fb, fb + ps, fb + oo, fb + oo + ps};
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(src[u]));
+                r[0][u] = v.x;
+                r[1][u] = v.y;
             }
-            if (conjg) {
-                xa.y = -xa.y;
-                xb.y = -xb.y;
+        } else {
+#pragma unroll
+            for (int ip = 0; ip < 2; ++ip) {
+                const bool in = ip < ntj;
+                r[ip][0] = in ? __ldg(fa + ip) : 0.0;
+                r[ip][1] = in ? __ldg(fa + ps + ip) : 0.0;
+                r[ip][2] = in ? __ldg(fa + oo + ip) : 0.0;
+                r[ip][3] = in ? __ldg(fa + oo + ps + ip) : 0.0;
+                r[ip][4] = in ? __ldg(fb + ip) : 0.0;
+                r[ip][5] = in ? __ldg(fb + ps + ip) : 0.0;
+                r[ip][6] = in ? __ldg(fb + oo + ip) : 0.0;
+                r[ip][7] = in ? __ldg(fb + oo + ps + ip) : 0.0;
             }
-            z = make_double2(xa.x - xb.y, xa.y + xb.x);  // Xa + i Xb
         }
-        Z[(pr * TJ + jl) * kA512 + zp512(digrev8(tt))] = z;
+        const int ts = zp512(digrev8(s)), tm = zp512(digrev8((P - s) & (P - 1)));
+#pragma unroll
+        for (int ip = 0; ip < 2; ++ip) {
+            const double ar = r[ip][0], ai = r[ip][1], aro = r[ip][2], aio = r[ip][3];
+            const double br = r[ip][4], bi = r[ip][5], bro = r[ip][6], bio = r[ip][7];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {  // point 2 ip + hh: f(+-z) = E +- O
+                const double sz = hh ? -1.0 : 1.0;
+                const double xar = sg * fma(sz, aro, ar), xai = reonly ? 0.0 : sg * fma(sz, aio, ai);
+                const double xbr = sg * fma(sz, bro, br), xbi = reonly ? 0.0 : sg * fma(sz, bio, bi);
+                double2* Zp = Z + (pr * TJ + 2 * ip + hh) * kA512;
+                Zp[ts] = make_double2(xar - xbi, xai + xbr);                       // Xa + i Xb at t = s
+                if (s > 0 && s < P / 2) Zp[tm] = make_double2(xar + xbi, xbr - xai);  // conj mirror at P - s
+            }
+        }
     }
     __syncthreads();
     fft512_r8<+1>(Z, 3 * TJ, tw);
@@ -1277,32 +1300,46 @@ __global__ void __launch_bounds__(256, 2) theta_cross512_kernel(ThetaCross t) {
     }
     __syncthreads();
     fft512_r8<-1>(Z, 2 * TJ, tw);
-    // ---- unpack X_a = (Z[t] + conj Z[P-t]) / 2, X_b = (Z[t] - conj Z[P-t]) / (2i); c_w = (-1)^w X[w mod P] / P
-    const double invp = 1.0 / double(P);
-    const int TP = TJ / 2;
-    for (int e = threadIdx.x; e < 3 * S * 2 * TP; e += blockDim.x) {
-        const int pos = e % TP;
-        const int pl = (e / TP) % 2;
-        const int s = (e / (2 * TP)) % S;
-        const int f = e / (2 * TP * S);  // output field 0..2
-        if (pos >= ntj) continue;
-        const int tt = s;  // s = P/2 is the Nyquist slot, w = -P/2 = P/2 (mod P)
+    // ---- unpack X_a = (Z[t] + conj Z[P-t]) / 2, X_b = (Z[t] - conj Z[P-t]) / (2i); c_w = (-1)^w X[w mod P] / P;
+    //      task (output f, slot s) stores E' = (f+ + f-)/2, O' = (f+ - f-)/2 of both positions and planes
+    for (int e = threadIdx.x; e < 3 * S; e += blockDim.x) {
+        const int f = e / S, s = e - f * S;
         const int arr0 = f < 2 ? 0 : TJ;
-        double xv[2];
+        const double sg = ((s & 1) ? -1.0 : 1.0) * (0.5 / double(P));
+        const int tt = zp512(s), tm = zp512((P - s) & (P - 1));  // s = P/2: Nyquist, w = -P/2 = P/2 (mod P)
+        double ov[4][2];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const double2* base = Z + (arr0 + 2 * pos + h) * kA512;
-            const double2 zt = base[zp512(tt)], zm = base[zp512((P - tt) & (P - 1))];
-            double2 X;
-            if (f == 0 || f == 2) X = make_double2(0.5 * (zt.x + zm.x), 0.5 * (zt.y - zm.y));
-            else X = make_double2(0.5 * (zt.y + zm.y), -0.5 * (zt.x - zm.x));
-            xv[h] = pl ? X.y : X.x;
+        for (int ip = 0; ip < 2; ++ip) {
+            double xr[2], xi[2];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const double2* base = Z + (arr0 + 2 * ip + hh) * kA512;
+                const double2 zt = base[tt], zm = base[tm];
+                if (f == 1) {
+                    xr[hh] = 0.5 * (zt.y + zm.y);
+                    xi[hh] = -0.5 * (zt.x - zm.x);
+                } else {
+                    xr[hh] = 0.5 * (zt.x + zm.x);
+                    xi[hh] = 0.5 * (zt.y - zm.y);
+                }
+            }
+            ov[0][ip] = sg * (xr[0] + xr[1]);
+            ov[1][ip] = sg * (xr[0] - xr[1]);
+            ov[2][ip] = sg * (xi[0] + xi[1]);
+            ov[3][ip] = sg * (xi[0] - xi[1]);
         }
-        const double sg = ((s & 1) ? -1.0 : 1.0) * invp * 0.5;
-        const long off = long(s) * g.slot_stride + long(pl) * g.plane_stride + long(jr) * g.n + q0 + pos +
-                         theta_slot_delta(t, s);
-        t.out[f][off] = sg * (xv[0] + xv[1]);         // E' = (f(+z) + f(-z)) / 2
-        t.out[f][off + g.nh] = sg * (xv[0] - xv[1]);  // O' = (f(+z) - f(-z)) / 2
+        double* o = t.out[f] + long(s) * g.slot_stride + long(jr) * g.n + q0 + theta_slot_delta(t, s);
+        double* dst[4] = {o, o + oo, o + ps, o + ps + oo};
+        if (vec) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) *reinterpret_cast<double2*>(dst[u]) = make_double2(ov[u][0], ov[u][1]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                dst[u][0] = ov[u][0];
+                if (ntj > 1) dst[u][1] = ov[u][1];
+            }
+        }
     }
     if (t.world > 1) __threadfence_system();  // peer stores performed before the rank barrier
 }

@@ -1190,12 +1190,15 @@ __device__ __forceinline__ void fft512_r8(double2* __restrict__ d, int cnt, cons
 #pragma unroll
             for (int r = 0; r < 8; ++r) v[r] = base[zp512(i0 + r * L)];
             if (L > 1) {
+                // W_{8L}^{pos r} = w1^r, w1 = e^{S 2 pi i pos 64 / (L 512)} (one table load, then a
+                // register recurrence: the per-r table loads were the kernel's top stall)
+                double2 w1 = tw[pos << (6 - ls)];
+                if (S > 0) w1.y = -w1.y;
+                double2 w = w1;
 #pragma unroll
-                for (int r = 1; r < 8; ++r) {  // W_{8L}^{pos r} = e^{S 2 pi i pos r 64 / (L 512)}
-                    const int q = (pos * r) << (6 - ls);
-                    double2 w = q < 256 ? tw[q] : make_double2(-tw[q - 256].x, -tw[q - 256].y);
-                    if (S > 0) w.y = -w.y;
+                for (int r = 1; r < 8; ++r) {
                     v[r] = cmul(v[r], w);
+                    if (r < 7) w = cmul(w, w1);
                 }
             }
             dft8<S>(v);

@@ -445,22 +445,28 @@ def main():
     hg = torch.from_numpy(np.ascontiguousarray(wg)).pin_memory()
     ol = torch.empty_like(hl).pin_memory()
     og = torch.empty_like(hg).pin_memory()
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    t0 = time.perf_counter()
-    st2 = P.NSStepper(ctx, hl.numpy(), hg.numpy(), reynolds=cfg["reynolds"], h=cfg["h"], order=4)
-    for _ in range(KE):  # one C-ABI step call per step: its status (NaN guard + solver error words) is read back
-        st2.step(1)
-    st2.omega(ol.numpy(), og.numpy())
-    e2e_s = time.perf_counter() - t0
-    if dist:
-        t = torch.tensor([e2e_s], device=red)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    # three full runs (host wall clock is noisier than device events: one run on a box has read 3x
+    # slower); the median is reported and every run is listed
+    e2e_runs = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        st2 = P.NSStepper(ctx, hl.numpy(), hg.numpy(), reynolds=cfg["reynolds"], h=cfg["h"], order=4)
+        for _ in range(KE):  # one C-ABI step call per step: its status (NaN guard + solver error words) is read back
+            st2.step(1)
+        st2.omega(ol.numpy(), og.numpy())
+        e2e_s = time.perf_counter() - t0
+        st2.close()
+        if dist:
+            t = torch.tensor([e2e_s], device=red)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e_runs.append(e2e_s)
+    e2e_s = sorted(e2e_runs)[1]
     io_bytes = hl.numel() * 16 * 2
     status_bytes = 4 * 4 + 4  # per step: ADI error words + non-finite flag (ccf_ns_step)
-    st2.close()
 
     sec = None
     if rank == 0 and world == 1 and not args.no_secondary:
@@ -487,6 +493,7 @@ def main():
             "clocks": clk,
             "e2e": {"value": jobs * KE / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": io_bytes / KE,
                     "d2h_bytes_per_step": io_bytes / KE + status_bytes, "steps": KE,
+                    "runs_steps_per_s": [jobs * KE / x for x in e2e_runs], "of_runs": "median",
                     "what": "fresh NSStepper from pinned host omega (H2D) -> KE single-step C-ABI calls incl. the "
                             "BDF 1->4 ramp and graph captures, each reading back the step status (non-finite "
                             "guard, solver error words) -> omega() to pinned host (D2H); state bytes amortised "

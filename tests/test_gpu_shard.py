@@ -71,7 +71,8 @@ def run_single(P, m, n, p, lam, gam, steps, reynolds=100.0, h=1e-3, disable_nonl
 
 
 @pytest.mark.parametrize("size,world", [((16, 16, 16), 2), ((16, 16, 16), 3), ((16, 12, 16), 4),
-                                        ((16, 16, 256), 2), ((16, 16, 256), 8), ((32, 32, 32), 4)],
+                                        ((16, 16, 256), 2), ((16, 16, 256), 8), ((32, 32, 32), 4),
+                                        ((16, 14, 512), 4)],
                          ids=lambda x: "x".join(map(str, x)) if isinstance(x, tuple) else f"g{x}")
 def test_sharded_ns_equals_unsharded(P, size, world):
     m, n, p = size

@@ -267,21 +267,47 @@ def shard_selfcheck(P, rank, world, local, dist, red, host_barrier=None):
     return float(t.item())
 
 
-def run_reference(args, cfg, rank):
+def bench_config(cfg, world, graphs=True):
+    """The workload description both arms print (identical dicts, so the driver can compare them)."""
+    return {"workload": cfg["workload"], "m": cfg["m"], "n": cfg["n"], "p": cfg["p"], "reynolds": cfg["reynolds"],
+            "h": cfg["h"], "bdf_order": 4, "init_decay": cfg["decay"], "seed": cfg["seed"],
+            "init_max_speed": cfg["vmax"], "parallelism": f"modes{world}" if world > 1 else "single",
+            "l2": "no flush: step working set ~3 GB >> 126 MB L2", "setup_steps": SETUP_STEPS}
+
+
+# steps run inside the stepper's setup, before the caller's W warm-up steps: the BDF 1 -> 4 ramp (steps
+# 0-3, eager) and one step in each of the 5 ring phases (steps 5-9 capture their phase's CUDA graph), so
+# neither the ramp nor a graph capture lands in the warm-up accounting or the timed region
+SETUP_STEPS = 10
+
+
+def run_reference(args, cfg, rank, world):
+    """Reference arm: the reference algorithm's CPU restatement (oracle/, kind "port"; the C++
+    reference is unbuildable here), all host threads, on W + K bounded samples of one NS step;
+    value = the median sample scaled to one full step (see cpu_sample)."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
     t0 = time.time()
-    value, sample, d = cpu_sample(cfg, threads)
+    W, K = max(3, args.warmup), args.steps
+    vals, sample = [], None
+    for i in range(W + K):
+        v, sample, d = cpu_sample(cfg, threads)
+        if i >= W:
+            vals.append(v)
+    value = statistics.median(vals)
+    wall = time.time() - t0
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "m": cfg["m"], "n": cfg["n"], "p": cfg["p"],
-                   "reynolds": cfg["reynolds"], "h": cfg["h"], "bdf_order": 4},
+        "steps": K, "warmup": W, "ms_per_step": 1e3 / value, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": bench_config(cfg, world),
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "wall_s": time.time() - t0,
+        "wall_s": wall,
+        "timing_note": (f"each of the W + K = {W + K} 'steps' is one bounded CPU sample (~{wall / (W + K):.1f} s of "
+                        f"wall time on {threads} threads) scaled to a full NS step; ms_per_step is that "
+                        f"extrapolated full-step time, so steps x ms_per_step exceeds the run's wall time"),
         "note": "reference C++ (cylspec) is unbuildable here (Eigen3/FFTW3/vendor headers absent); "
                 "oracle/ restates it single-source, run with all host threads over Fourier slices / pencils",
     }
@@ -310,7 +336,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
-        run_reference(args, cfg, rank)
+        run_reference(args, cfg, rank, world)
         return
 
     import torch
@@ -332,10 +358,7 @@ def main():
     peaks = load_peaks()
     stream = torch.cuda.Stream()
     t_setup = time.time()
-    # warm-up: at least the BDF ramp (steps 0-3, eager) plus one step in each of the 5 ring phases once
-    # graphs are used (steps 5-9, each captures its phase's graph), so neither the ramp nor a graph
-    # capture lands in the timed region whatever W the caller passes
-    W = max(3, args.warmup, 10)
+    W = max(3, args.warmup)  # warm-up steps after the stepper's setup steps (SETUP_STEPS)
     # N > 1: the mode-sharded step (csrc/shard.cu): rank r owns a contiguous range of Fourier slots in
     # every per-mode stage and a range of radial rows in the theta stage, reading / writing the other
     # slots in their owners' exchange buffers over NVLink (CUDA IPC), device-side rank barriers
@@ -374,7 +397,9 @@ def main():
             st = P.NSStepper(ctx, wl, wg, reynolds=cfg["reynolds"], h=cfg["h"], order=4)
             if args.no_graphs:
                 st.set_graphs(False)
-            st.step(W)
+            st.step(SETUP_STEPS)  # setup: BDF ramp + CUDA-graph captures
+            torch.cuda.synchronize()
+            st.step(W)  # warm-up
             torch.cuda.synchronize()
             break
         except P.CCFError as e:  # sharded path unavailable on this node: measure replicas, say so
@@ -484,12 +509,9 @@ def main():
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
             "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "m": m, "n": n, "p": p, "reynolds": cfg["reynolds"],
-                       "h": cfg["h"], "bdf_order": 4, "init_decay": cfg["decay"], "seed": cfg["seed"],
-                       "init_max_speed": cfg["vmax"], "init_vmax_scaled_from": vmax,
-                       "parallelism": (f"modes{world}" if sharded else ("replica" if world > 1 else "single")),
-                       "l2": "no flush: step working set ~3 GB >> 126 MB L2",
-                       "cuda_graphs": not args.no_graphs},
+            "config": bench_config(cfg, world),
+            "init_vmax_scaled_from": vmax, "cuda_graphs": not args.no_graphs,
+            "parallelism_run": f"modes{world}" if sharded else ("replica" if world > 1 else "single"),
             "clocks": clk,
             "e2e": {"value": jobs * KE / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": io_bytes / KE,
                     "d2h_bytes_per_step": io_bytes / KE + status_bytes, "steps": KE,

@@ -80,7 +80,8 @@ struct CoeffTensor {
     Complex at(int j, int k, int l) const { return data[(size_t(l) * spec.n + size_t(k)) * spec.m + size_t(j)]; }
     const double* raw() const { return reinterpret_cast<const double*>(data.data()); }
     double* raw() { return reinterpret_cast<double*>(data.data()); }
-    CoeffTensor& operator+=(const CoeffTensor& o) {
+    CoeffTensor& operator+=(const CoeffTensor& o) {  // coeffs.cpp:19-23
+        if (!(spec == o.spec)) throw DomainError("CoeffTensor: spec mismatch");
         for (size_t i = 0; i < data.size(); ++i) data[i] += o.data[i];
         return *this;
     }
@@ -158,6 +159,13 @@ namespace detail {
 
 inline void check(ccf_status st, ccf_ctx* ctx) {
     if (st != CCF_OK) raise(st, ctx);
+}
+
+// multi-input entry points: the C-ABI reads every buffer with the first tensor's spec, so a mismatched
+// tensor is a DomainError here, never an out-of-bounds read
+template <class T, class... Ts>
+inline void same_spec(const char* what, const T& first, const Ts&... rest) {
+    if (!((rest.spec == first.spec) && ...)) throw DomainError(std::string(what) + ": spec mismatch");
 }
 
 // one context per (m, n, p, tol) and host thread (the reference library is single-threaded)
@@ -241,8 +249,15 @@ public:
         spec.validate();
     }
     CoeffTensor step(const std::deque<CoeffTensor>& history, const BDFScheme& scheme, const CoeffTensor* forcing) const {
+        // timestep.cpp:69-70 (forcing); the C-ABI reads spec-sized buffers, so every history entry is checked too
+        if (forcing && !(forcing->spec == spec_)) throw DomainError("HelmholtzTensorStepper: forcing spec mismatch");
+        if (int(history.size()) < scheme.order)
+            throw DomainError("bdf_rhs: insufficient history for the requested order");  // timestep.cpp:43
         std::vector<const double*> hp;
-        for (const auto& t : history) hp.push_back(t.raw());
+        for (const auto& t : history) {
+            if (!(t.spec == spec_)) throw DomainError("HelmholtzTensorStepper: history spec mismatch");
+            hp.push_back(t.raw());
+        }
         CoeffTensor out(spec_);
         ccf_ctx* c = detail::context(spec_, tol_);
         detail::check(ccf_helmholtz_step(c, hp.data(), int(hp.size()), scheme.order, forcing ? forcing->raw() : nullptr,
@@ -258,18 +273,21 @@ private:
 
 // ---- ptns.hpp:47-137
 inline VectorFieldCoeffs pt_synthesize(const PTScalars& s) {
+    detail::same_spec("pt_synthesize", s.lambda, s.gamma);
     VectorFieldCoeffs v(s.lambda.spec);
     ccf_ctx* c = detail::context(s.lambda.spec);
     detail::check(ccf_pt_synthesize(c, s.lambda.raw(), s.gamma.raw(), v.comp_r.raw(), v.comp_theta.raw(), v.comp_z.raw()), c);
     return v;
 }
 inline PTScalars pt_decompose(const VectorFieldCoeffs& v, bool /*check_divergence*/ = false, double = 1e-8) {
+    detail::same_spec("pt_decompose", v.comp_r, v.comp_theta, v.comp_z);
     PTScalars s(v.comp_r.spec);
     ccf_ctx* c = detail::context(v.comp_r.spec);
     detail::check(ccf_pt_decompose(c, v.comp_r.raw(), v.comp_theta.raw(), v.comp_z.raw(), s.lambda.raw(), s.gamma.raw()), c);
     return s;
 }
 inline VectorFieldCoeffs curl_vector(const VectorFieldCoeffs& v) {
+    detail::same_spec("curl_vector", v.comp_r, v.comp_theta, v.comp_z);
     VectorFieldCoeffs o(v.comp_r.spec);
     ccf_ctx* c = detail::context(v.comp_r.spec);
     detail::check(ccf_curl_vector(c, v.comp_r.raw(), v.comp_theta.raw(), v.comp_z.raw(), o.comp_r.raw(),
@@ -278,6 +296,7 @@ inline VectorFieldCoeffs curl_vector(const VectorFieldCoeffs& v) {
     return o;
 }
 inline PTScalars curl_pt(const PTScalars& s) {
+    detail::same_spec("curl_pt", s.lambda, s.gamma);
     PTScalars o(s.lambda.spec);
     ccf_ctx* c = detail::context(s.lambda.spec);
     detail::check(ccf_curl_pt(c, s.lambda.raw(), s.gamma.raw(), o.lambda.raw(), o.gamma.raw()), c);
@@ -292,12 +311,14 @@ inline CoeffTensor divergence(const VectorFieldCoeffs& v) {  // ptns.cpp:35-40
     return out;
 }
 inline PTScalars velocity_from_vorticity(const PTScalars& w, double tol = kDefaultAdiTol) {
+    detail::same_spec("velocity_from_vorticity", w.lambda, w.gamma);
     PTScalars o(w.lambda.spec);
     ccf_ctx* c = detail::context(w.lambda.spec, tol);
     detail::check(ccf_velocity_from_vorticity(c, w.lambda.raw(), w.gamma.raw(), o.lambda.raw(), o.gamma.raw()), c);
     return o;
 }
 inline PTScalars nonlinear_term(const PTScalars& v, const PTScalars& w, bool dealias_two_thirds = false) {
+    detail::same_spec("nonlinear_term", v.lambda, v.gamma, w.lambda, w.gamma);
     PTScalars o(v.lambda.spec);
     ccf_ctx* c = detail::context(v.lambda.spec);
     detail::check(ccf_nonlinear_ex(c, v.lambda.raw(), v.gamma.raw(), w.lambda.raw(), w.gamma.raw(),
@@ -320,6 +341,10 @@ struct NSConfig {
 class NSStepper {  // ramp bootstrap; state resident on the GPU between steps
 public:
     NSStepper(const NSConfig& cfg, const PTScalars& omega0) : cfg_(cfg), omega_(cfg.spec) {
+        // ptns.cpp:185-189
+        if (!(omega0.lambda.spec == cfg.spec) || !(omega0.gamma.spec == cfg.spec))
+            throw DomainError("NSStepper: initial vorticity spec mismatch");
+        if (cfg.spec.m % 2 != 0) throw DomainError("NSStepper: even m required for the nonlinear pipeline");
         ctx_ = detail::context(cfg.spec, cfg.adi_tol);
         const int flags = (cfg.disable_nonlinear ? 1 : 0) | (cfg.dealias_two_thirds ? 2 : 0) | (cfg.compute_gamma_psi ? 4 : 0);
         detail::check(ccf_ns_create_ex(ctx_, cfg.reynolds, cfg.h, cfg.order, flags, omega0.lambda.raw(),
@@ -388,6 +413,8 @@ using ForcingCallback = std::function<GridField(double time)>;
 class HeatStepper {  // state resident on the GPU (eigen coordinates) between steps
 public:
     HeatStepper(const HeatConfig& config, const GridField& initial) : config_(config), cur_(config.spec) {
+        // timestep.cpp:113-114 (the reference analyzes first, then checks the coefficient spec)
+        if (!(initial.spec == config.spec)) throw DomainError("HeatStepper: initial data spec mismatch");
         init(initial.values.data(), 0);
     }
     HeatStepper(const HeatConfig& config, const CoeffTensor& initial) : config_(config), cur_(config.spec) {
@@ -398,6 +425,8 @@ public:
     HeatStepper(const HeatStepper&) = delete;
     HeatStepper& operator=(const HeatStepper&) = delete;
     void step(const CoeffTensor* forcing) {
+        if (forcing && !(forcing->spec == config_.spec))  // timestep.cpp:69-70
+            throw DomainError("HelmholtzTensorStepper: forcing spec mismatch");
         detail::check(ccf_heat_step(st_, forcing ? forcing->raw() : nullptr, 1), ctx_);
         time_ += config_.h;
         ++steps_;
@@ -405,6 +434,8 @@ public:
     void step_with_callback(const ForcingCallback& forcing) {
         if (!forcing) return step(nullptr);
         const GridField g = forcing(config_.forcing_mode == ForcingMode::exact ? time_ + config_.h : time_);
+        if (!(g.spec == config_.spec))  // analyze(g) would carry g's spec into timestep.cpp:69-70
+            throw DomainError("HelmholtzTensorStepper: forcing spec mismatch");
         detail::check(ccf_heat_step(st_, g.values.data(), 0), ctx_);  // analyzed on the device
         time_ += config_.h;
         ++steps_;
@@ -435,7 +466,34 @@ struct HeatRunResult {
     std::vector<double> snapshot_times;
     CoeffTensor final_coeffs;
     double final_time = 0.0;
+    // timestep.cpp:102 tracks max(last_residual()) of the ADI solves. The modal solves here are exact
+    // (fast diagonalization), so this is the worst relative Sylvester residual ||AXB + CXD - E|| / ||E||
+    // of the solver data the run used (every BDF order's scale, both z parities; every |w| up to m = 64,
+    // else |w| in {0, 1, p/4, p/2}) on seeded right-hand sides (ccf_diag_host_check, long double)
+    double worst_residual = 0.0;
 };
+
+namespace detail {
+inline double diag_worst_residual(const GridSpec& spec, double alpha, double h, int max_order) {
+    std::vector<int> ws;
+    if (spec.m <= 64) {
+        for (int w = 0; w <= spec.p / 2; ++w) ws.push_back(w);
+    } else {
+        ws = {0, 1, spec.p / 4, spec.p / 2};
+    }
+    double worst = 0.0;
+    for (int b = 1; b <= max_order; ++b) {
+        const double scale = BDFScheme::of_order(b).kappa(h) * alpha;  // timestep.cpp:63-64
+        for (int w : ws)
+            for (int k0 = 0; k0 < 2; ++k0) {
+                double r = 0.0;
+                check(ccf_diag_host_check(spec.m, spec.n, w, scale, 0, k0, 12345u + unsigned(w), &r), nullptr);
+                worst = std::max(worst, r);
+            }
+    }
+    return worst;
+}
+}  // namespace detail
 
 inline HeatRunResult heat_run(const HeatConfig& config, const GridField& initial, const ForcingCallback& forcing,
                               int steps) {  // timestep.cpp:146-170
@@ -458,6 +516,8 @@ inline HeatRunResult heat_run(const HeatConfig& config, const GridField& initial
         result.snapshot_times.push_back(stepper.time());
     }
     result.final_time = stepper.time();
+    if (steps > 0) result.worst_residual = detail::diag_worst_residual(config.spec, config.alpha, config.h,
+                                                                         std::min(config.order, steps));
     return result;
 }
 

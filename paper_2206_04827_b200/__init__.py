@@ -197,8 +197,29 @@ def _addr(a):
     return C.c_void_p(a.ctypes.data)
 
 
-def _c128(x):
-    return np.ascontiguousarray(x, dtype=np.complex128)
+def _arg(x, shape, cplx, what, out=False):
+    """Validate one tensor argument before its pointer reaches the C-ABI, which reads / writes a buffer
+    sized by the context (the reference throws DomainError on a spec mismatch, e.g. timestep.cpp:69-70,
+    ptns.cpp:185-187). Inputs of the wrong dtype are converted; outputs must already be exact."""
+    if x is None:
+        return None
+    want = "complex128" if cplx else "float64"
+    if hasattr(x, "data_ptr"):  # torch tensor (host or device memory)
+        if tuple(x.shape) != tuple(shape) or str(x.dtype) != "torch." + want or not x.is_contiguous():
+            raise DomainError(f"{what}: expected a contiguous {want} tensor of shape {tuple(shape)}, got "
+                              f"{str(x.dtype)} {tuple(x.shape)}")
+        return x
+    if out:
+        if not isinstance(x, np.ndarray) or x.dtype != np.dtype(want) or x.shape != tuple(shape) \
+                or not x.flags.c_contiguous or not x.flags.writeable:
+            raise DomainError(f"{what}: output must be a writeable C-contiguous {want} array of shape {tuple(shape)}")
+        return x
+    a = np.asarray(x)
+    if a.shape != tuple(shape):
+        raise DomainError(f"{what}: spec mismatch (shape {a.shape}, context {tuple(shape)})")
+    if not cplx and np.iscomplexobj(a):
+        raise DomainError(f"{what}: grid values must be real")
+    return np.ascontiguousarray(a, dtype=np.complex128 if cplx else np.float64)
 
 
 class Context:
@@ -255,15 +276,21 @@ class Context:
     def _out_c(self):
         return np.zeros(self.shape(), np.complex128)
 
+    def _coef(self, x, what, out=False):
+        return _arg(x, self.shape(), True, what, out)
+
+    def _vals(self, x, what, out=False):
+        return _arg(x, self.shape(), False, what, out)
+
     # ---- transforms (transform.hpp:17-22)
     def analyze(self, values):
-        v = np.ascontiguousarray(values, dtype=np.float64)
+        v = self._vals(values, "analyze")
         out = self._out_c()
         self._check(lib().ccf_analyze(self.h, _addr(v), _addr(out)))
         return out
 
     def synthesize(self, coeffs):
-        c = _c128(coeffs)
+        c = self._coef(coeffs, "synthesize")
         out = np.zeros(self.shape())
         self._check(lib().ccf_synthesize(self.h, _addr(c), _addr(out)))
         return out
@@ -271,28 +298,28 @@ class Context:
     _CALC = {"dr": 0, "dz": 1, "dtheta": 2, "divide_r": 4, "hlap": 5, "lap": 6}
 
     def calculus(self, op, coeffs):
-        c = _c128(coeffs)
+        c = self._coef(coeffs, op)
         out = self._out_c()
         self._check(lib().ccf_calculus(self.h, self._CALC[op], _addr(c), _addr(out)))
         return out
 
     # ---- solvers (solvers.hpp:86-94)
     def solve_poisson_3d(self, f):
-        c = _c128(f)
+        c = self._coef(f, "solve_poisson_3d")
         out = self._out_c()
         self._check(lib().ccf_poisson3d(self.h, _addr(c), _addr(out)))
         return out
 
     def solve_horizontal_poisson(self, rhs):
-        c = _c128(rhs)
+        c = self._coef(rhs, "solve_horizontal_poisson")
         out = self._out_c()
         self._check(lib().ccf_hpoisson(self.h, _addr(c), _addr(out)))
         return out
 
     def helmholtz_step(self, history, order, diffusivity, h, forcing=None):
-        hs = [_c128(x) for x in history]
+        hs = [self._coef(x, "HelmholtzTensorStepper: history") for x in history]
         arr = (C.c_void_p * len(hs))(*[x.ctypes.data for x in hs])
-        fc = _c128(forcing) if forcing is not None else None
+        fc = self._coef(forcing, "HelmholtzTensorStepper: forcing")
         out = self._out_c()
         self._check(lib().ccf_helmholtz_step(self.h, arr, len(hs), int(order), _addr(fc), C.c_double(diffusivity),
                                              C.c_double(h), _addr(out)))
@@ -301,36 +328,39 @@ class Context:
     # ---- PT / NS (ptns.hpp:47-70)
     def pt_synthesize(self, lam, gam):
         o = [self._out_c() for _ in range(3)]
-        self._check(lib().ccf_pt_synthesize(self.h, _addr(_c128(lam)), _addr(_c128(gam)), *[_addr(x) for x in o]))
+        self._check(lib().ccf_pt_synthesize(self.h, _addr(self._coef(lam, "pt_synthesize")),
+                                            _addr(self._coef(gam, "pt_synthesize")), *[_addr(x) for x in o]))
         return tuple(o)
 
     def pt_decompose(self, vr, vt, vz):
         o = [self._out_c() for _ in range(2)]
-        self._check(lib().ccf_pt_decompose(self.h, _addr(_c128(vr)), _addr(_c128(vt)), _addr(_c128(vz)),
+        self._check(lib().ccf_pt_decompose(self.h, *[_addr(self._coef(x, "pt_decompose")) for x in (vr, vt, vz)],
                                            *[_addr(x) for x in o]))
         return tuple(o)
 
     def curl_vector(self, vr, vt, vz):
         o = [self._out_c() for _ in range(3)]
-        self._check(lib().ccf_curl_vector(self.h, _addr(_c128(vr)), _addr(_c128(vt)), _addr(_c128(vz)),
+        self._check(lib().ccf_curl_vector(self.h, *[_addr(self._coef(x, "curl_vector")) for x in (vr, vt, vz)],
                                           *[_addr(x) for x in o]))
         return tuple(o)
 
     def curl_pt(self, lam, gam):
         o = [self._out_c() for _ in range(2)]
-        self._check(lib().ccf_curl_pt(self.h, _addr(_c128(lam)), _addr(_c128(gam)), *[_addr(x) for x in o]))
+        self._check(lib().ccf_curl_pt(self.h, _addr(self._coef(lam, "curl_pt")), _addr(self._coef(gam, "curl_pt")), *[_addr(x) for x in o]))
         return tuple(o)
 
     def velocity_from_vorticity(self, lam_w, gam_w):
         o = [self._out_c() for _ in range(2)]
-        self._check(lib().ccf_velocity_from_vorticity(self.h, _addr(_c128(lam_w)), _addr(_c128(gam_w)),
+        self._check(lib().ccf_velocity_from_vorticity(self.h, _addr(self._coef(lam_w, "velocity_from_vorticity")),
+                                                      _addr(self._coef(gam_w, "velocity_from_vorticity")),
                                                       *[_addr(x) for x in o]))
         return tuple(o)
 
     def nonlinear_term(self, lam_v, gam_v, lam_w, gam_w, dealias_two_thirds=False):
         o = [self._out_c() for _ in range(2)]
-        self._check(lib().ccf_nonlinear_ex(self.h, _addr(_c128(lam_v)), _addr(_c128(gam_v)), _addr(_c128(lam_w)),
-                                           _addr(_c128(gam_w)), int(bool(dealias_two_thirds)), *[_addr(x) for x in o]))
+        self._check(lib().ccf_nonlinear_ex(self.h, *[_addr(self._coef(x, "nonlinear_term"))
+                                                       for x in (lam_v, gam_v, lam_w, gam_w)],
+                                           int(bool(dealias_two_thirds)), *[_addr(x) for x in o]))
         return tuple(o)
 
     # ---- mode sharding (csrc/shard.cu)
@@ -503,7 +533,8 @@ class NSStepper:
         st = C.c_void_p()
         flags = int(bool(disable_nonlinear)) | (2 if dealias_two_thirds else 0) | (4 if compute_gamma_psi else 0)
         ctx._check(lib().ccf_ns_create_ex(ctx.h, C.c_double(reynolds), C.c_double(h), int(order), flags,
-                                          _addr(_c128(lam0)), _addr(_c128(gam0)), C.byref(st)))
+                                          _addr(ctx._coef(lam0, "NSStepper: initial vorticity")),
+                                          _addr(ctx._coef(gam0, "NSStepper: initial vorticity")), C.byref(st)))
         self.h = st
 
     def velocity(self):
@@ -522,8 +553,8 @@ class NSStepper:
         self.ctx._check(lib().ccf_ns_step(self.h, int(nsteps)))
 
     def omega(self, out_lam=None, out_gam=None):
-        lam = out_lam if out_lam is not None else self.ctx._out_c()
-        gam = out_gam if out_gam is not None else self.ctx._out_c()
+        lam = self.ctx._coef(out_lam, "NSStepper.omega", out=True) if out_lam is not None else self.ctx._out_c()
+        gam = self.ctx._coef(out_gam, "NSStepper.omega", out=True) if out_gam is not None else self.ctx._out_c()
         t = C.c_double()
         s = C.c_int()
         self.ctx._check(lib().ccf_ns_get_omega(self.h, _addr(lam), _addr(gam), C.byref(t), C.byref(s)))
@@ -564,15 +595,14 @@ class NSStepper:
             pass
 
 
-def _field_arg(x):
-    """(pointer holder, kind): complex -> coefficients (kind 1), real -> grid values (kind 0)."""
+def _field_arg(ctx, x, what):
+    """(pointer holder, kind): complex -> coefficients (kind 1), real -> grid values (kind 0); shape and
+    dtype checked against the context (timestep.cpp:69-70, 113-114)."""
     if hasattr(x, "data_ptr"):
-        t = x.contiguous()
-        return t, (1 if t.is_complex() else 0)
-    a = np.ascontiguousarray(x)
-    if np.iscomplexobj(a):
-        return a.astype(np.complex128, copy=False), 1
-    return a.astype(np.float64, copy=False), 0
+        cplx = x.is_complex()
+        return _arg(x.contiguous(), ctx.shape(), cplx, what), (1 if cplx else 0)
+    cplx = np.iscomplexobj(x)
+    return _arg(x, ctx.shape(), cplx, what), (1 if cplx else 0)
 
 
 class HeatStepper:
@@ -582,7 +612,7 @@ class HeatStepper:
     def __init__(self, ctx: Context, initial, alpha=1.0, h=1e-2, order=4):
         self.ctx = ctx
         self.h_step = h
-        a, kind = _field_arg(initial)
+        a, kind = _field_arg(ctx, initial, "HeatStepper: initial data")
         st = C.c_void_p()
         ctx._check(lib().ccf_heat_create(ctx.h, C.c_double(alpha), C.c_double(h), int(order), _addr(a), kind,
                                          C.byref(st)))
@@ -594,13 +624,13 @@ class HeatStepper:
         if forcing is None:
             self.ctx._check(lib().ccf_heat_step(self.h, None, 0))
         else:
-            a, kind = _field_arg(forcing)
+            a, kind = _field_arg(self.ctx, forcing, "HelmholtzTensorStepper: forcing")
             self.ctx._check(lib().ccf_heat_step(self.h, _addr(a), kind))
         self.time += self.h_step
         self.steps_taken += 1
 
     def current(self, out=None):
-        c = out if out is not None else self.ctx._out_c()
+        c = self.ctx._coef(out, "HeatStepper.current", out=True) if out is not None else self.ctx._out_c()
         t, s = C.c_double(), C.c_int()
         self.ctx._check(lib().ccf_heat_get(self.h, _addr(c), C.byref(t), C.byref(s)))
         self.time, self.steps_taken = t.value, s.value

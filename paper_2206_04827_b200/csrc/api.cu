@@ -864,11 +864,29 @@ bool device_ptr(const void* p) {
     }
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
+// selects the device that owns a pointer for the scope and restores the caller's current device
+// afterwards (the free functions below must not change the calling thread's device for torch etc.)
+struct PtrDeviceGuard {
+    int prev = -1;
+    explicit PtrDeviceGuard(const void* p) {
+        cudaPointerAttributes a{};
+        CCF_CUDA(cudaPointerGetAttributes(&a, p));
+        CCF_CUDA(cudaGetDevice(&prev));
+        if (a.device != prev) CCF_CUDA(cudaSetDevice(a.device));
+        else prev = -1;
+    }
+    ~PtrDeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    PtrDeviceGuard(const PtrDeviceGuard&) = delete;
+    PtrDeviceGuard& operator=(const PtrDeviceGuard&) = delete;
+};
 }  // namespace
 
 ccf_status ccf_crc32(const void* data, size_t len, unsigned* crc) {
     return guard_free([&] {
         if (len && device_ptr(data)) {
+            PtrDeviceGuard dg(data);  // tables, sync and launch on the device that owns the data
             CCF_CUDA(cudaDeviceSynchronize());
             if (len % 8 == 0 && reinterpret_cast<uintptr_t>(data) % 8 == 0) {
                 *crc = ccf::crc32_device(data, len, nullptr);
@@ -888,12 +906,9 @@ ccf_status ccf_write_field(const char* path, int kind, int m, int n, int p, cons
         if (m < 4 || n < 4) throw Error(ccf::DOMAIN_ERROR, "GridSpec: m and n must be at least 4");
         if (p < 2 || p % 2 != 0) throw Error(ccf::DOMAIN_ERROR, "GridSpec: p must be even and at least 2");
         const bool dev = device_ptr(payload);
+        std::unique_ptr<PtrDeviceGuard> dg;
         if (dev) {
-            int d = 0;
-            cudaPointerAttributes a{};
-            CCF_CUDA(cudaPointerGetAttributes(&a, payload));
-            d = a.device;
-            CCF_CUDA(cudaSetDevice(d));
+            dg = std::make_unique<PtrDeviceGuard>(payload);
             CCF_CUDA(cudaDeviceSynchronize());
         }
         ccf::write_field_file(path, kind, m, n, p, payload, dev, nullptr);
@@ -907,10 +922,9 @@ ccf_status ccf_read_field_header(const char* path, int* kind, int* m, int* n, in
 ccf_status ccf_read_field(const char* path, int* kind, int* m, int* n, int* p, double* payload, size_t cap) {
     return guard_free([&] {
         const bool dev = device_ptr(payload);
+        std::unique_ptr<PtrDeviceGuard> dg;
         if (dev) {
-            cudaPointerAttributes a{};
-            CCF_CUDA(cudaPointerGetAttributes(&a, payload));
-            CCF_CUDA(cudaSetDevice(a.device));
+            dg = std::make_unique<PtrDeviceGuard>(payload);
             CCF_CUDA(cudaDeviceSynchronize());
         }
         ccf::read_field_file(path, *kind, *m, *n, *p, payload, cap, dev, nullptr);

@@ -139,8 +139,11 @@ int theta_cross256_threads();
 template <int NQ>
 __global__ void theta_cross256w_kernel(ThetaCross t);  // warp-per-point variant, NQ z-position pairs per CTA
 size_t theta_cross256w_smem(int nq);
-__global__ void theta_cross512_kernel(ThetaCross t);  // p = 512: radix-8 passes, TJ = 4, 256 threads
-size_t theta_cross512_smem(int tj);
+// p = 512: radix-8 passes; the sample / task mapping is written for exactly these two constants
+constexpr int kTheta512Points = 4;     // points (TJ) per CTA
+constexpr int kTheta512Threads = 256;  // threads per CTA
+__global__ void theta_cross512_kernel(ThetaCross t);
+size_t theta_cross512_smem();
 __global__ void theta_dft_full_kernel(const double* __restrict__ in, double* __restrict__ out, int m, int n, int p,
                                       int dir, const double2* __restrict__ twp);
 

@@ -776,7 +776,7 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
         CCF_CUDA(cudaFuncSetAttribute(theta_cross256w_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(theta_cross256w_smem(2))));
         CCF_CUDA(cudaFuncSetAttribute(theta_cross512_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(theta_cross512_smem(4))));
+                                      int(theta_cross512_smem())));
         const char* q = std::getenv("CCF_THETA_PAIRS");  // z-position pairs per CTA of the warp kernel (1 | 2)
         theta_nq_ = (q && q[0] == '1') ? 1 : 2;
         const char* v = std::getenv("CCF_THETA_VARIANT");  // "16": 16-thread FFT kernel
@@ -795,10 +795,10 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
         else
             theta_cross256w_kernel<1><<<grid, 128, theta_cross256w_smem(1), c.stream>>>(t);
     } else if (g.p == 512 && g.nslots == 257 && !theta_generic_) {
-        const int tj5 = 4;
+        const int tj5 = kTheta512Points;
         const dim3 grid(unsigned((g.nh + tj5 / 2 - 1) / (tj5 / 2)), rows);
         t.tj = tj5;
-        theta_cross512_kernel<<<grid, 256, theta_cross512_smem(tj5), c.stream>>>(t);
+        theta_cross512_kernel<<<grid, kTheta512Threads, theta_cross512_smem(), c.stream>>>(t);
     } else if (g.p == 256 && !theta_generic_) {
         const int np = theta_cross256_positions();
         const dim3 grid(unsigned((g.nh + np - 1) / np), unsigned(g.mh));

@@ -1211,12 +1211,12 @@ __device__ __forceinline__ void fft512_r8(double2* __restrict__ d, int cnt, cons
 
 }  // namespace
 
-__global__ void __launch_bounds__(256, 2) theta_cross512_kernel(ThetaCross t) {
+__global__ void __launch_bounds__(kTheta512Threads, 2) theta_cross512_kernel(ThetaCross t) {
     extern __shared__ double2 sd[];
     const Geo& g = t.g;
     constexpr int P = kP512;
     const int S = g.nslots;
-    const int TJ = t.tj;                 // points per CTA (even): point 2i -> +z, 2i+1 -> -z
+    constexpr int TJ = kTheta512Points;  // points per CTA (even): point 2i -> +z, 2i+1 -> -z
     const int jr = t.row0 + blockIdx.y;  // r > 0 grid row
     const int q0 = blockIdx.x * (TJ / 2);
     const int ntj = min(TJ / 2, g.nh - q0);
@@ -1277,11 +1277,12 @@ __global__ void __launch_bounds__(256, 2) theta_cross512_kernel(ThetaCross t) {
     // ---- pointwise cross product a = v x w (ptns.cpp:127-132); (a_r + i a_t) and (a_z + 0 i) are
     //      written digit-reversed into arrays [0, TJ) and [TJ, 2 TJ) for the forward transform. The
     //      permutation crosses threads, so every sample is read (kPer per thread) before any write.
-    constexpr int kPer = 8;  // TJ * P / blockDim (host launches TJ = 4, 256 threads)
+    constexpr int kPer = TJ * P / kTheta512Threads;  // samples per thread
+    static_assert(kPer * kTheta512Threads == TJ * P && TJ == 4, "theta512: task mapping assumes TJ = 4");
     double2 A[kPer], B[kPer];
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
-        const int e = threadIdx.x + u * blockDim.x;
+        const int e = threadIdx.x + u * kTheta512Threads;
         if (e < TJ * P) {
             const int jl = e >> 9, l = e & (P - 1);
             const double2 p0 = Z[(0 * TJ + jl) * kA512 + zp512(l)], p1 = Z[(1 * TJ + jl) * kA512 + zp512(l)],
@@ -1294,7 +1295,7 @@ __global__ void __launch_bounds__(256, 2) theta_cross512_kernel(ThetaCross t) {
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
-        const int e = threadIdx.x + u * blockDim.x;
+        const int e = threadIdx.x + u * kTheta512Threads;
         if (e < TJ * P) {
             const int jl = e >> 9, l = zp512(digrev8(e & (P - 1)));
             Z[(0 * TJ + jl) * kA512 + l] = A[u];
@@ -1347,7 +1348,7 @@ __global__ void __launch_bounds__(256, 2) theta_cross512_kernel(ThetaCross t) {
     if (t.world > 1) __threadfence_system();  // peer stores performed before the rank barrier
 }
 
-size_t theta_cross512_smem(int tj) { return size_t(3) * tj * kA512 * sizeof(double2); }
+size_t theta_cross512_smem() { return size_t(3) * kTheta512Points * kA512 * sizeof(double2); }
 
 size_t theta_cross256w_smem(int nq) { return (size_t(4 * nq) * 2 * kTWArr + 256) * sizeof(double2); }
 

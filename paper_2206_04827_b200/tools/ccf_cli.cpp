@@ -323,7 +323,7 @@ int run_heat(const RunConfig& cfg) {
     mf.put("config", config_json(cfg));
     mf.put("timings", "{\"total_seconds\": " + jnum(sec) + ", \"per_step_seconds\": " +
                           jnum(cfg.steps ? sec / cfg.steps : 0) + "}");
-    mf.put("worst_modal_residual", "null");  // no iteration: exact fast diagonalization (DESIGN.md §3 K1)
+    mf.put("worst_modal_residual", jnum(run.worst_residual));  // see HeatRunResult::worst_residual
     mf.put("modal_solver", jstr("fast diagonalization on the FP64 tensor cores"));
     mf.put("final_time", jnum(run.final_time));
     std::string outs = "[";

@@ -69,11 +69,38 @@ int main(int argc, char** argv) {
         herr = std::max(herr, std::abs(hr.snapshots.back().values[i] - ref.values[i]));
         hmx = std::max(hmx, std::abs(ref.values[i]));
     }
+    // spec mismatches are DomainErrors with the reference messages (ptns.cpp:185-187, timestep.cpp:69-70,113-114)
+    int spec_errors = 0;
+    const GridSpec other(m, m, m + 2);
+    auto expect = [&](auto fn, const char* msg) {
+        try {
+            fn();
+        } catch (const DomainError& e) {
+            spec_errors += std::string(e.what()).find(msg) != std::string::npos;
+        }
+    };
+    expect([&] { NSStepper s(nc, PTScalars(CoeffTensor(other), CoeffTensor(other))); }, "NSStepper: initial vorticity spec mismatch");
+    expect([&] { HeatStepper h(hc, GridField(other)); }, "HeatStepper: initial data spec mismatch");
+    expect([&] { HeatStepper h(hc, CoeffTensor(other)); }, "HeatStepper: initial data spec mismatch");
+    expect([&] {
+        HeatStepper h(hc, exact(0.0));
+        const CoeffTensor bad(other);
+        h.step(&bad);
+    }, "HelmholtzTensorStepper: forcing spec mismatch");
+    expect([&] {
+        HelmholtzTensorStepper hs(spec, 1.0, 0.01, 1e-12);
+        std::deque<CoeffTensor> hist{CoeffTensor(spec)};
+        const CoeffTensor bad(other);
+        hs.step(hist, BDFScheme::of_order(1), &bad);
+    }, "HelmholtzTensorStepper: forcing spec mismatch");
+    expect([&] { nonlinear_term(PTScalars(f, u), PTScalars(CoeffTensor(other), CoeffTensor(other))); }, "spec mismatch");
+    const bool spec_ok = spec_errors == 6 && hr.worst_residual > 0.0 && hr.worst_residual < 1e-12;
     // FieldFile round trip of the final NS vorticity (io.cpp:42-109)
     write_field("/tmp/shim_lambda.ccf", run.final_omega.lambda);
     const CoeffTensor rd = std::get<CoeffTensor>(read_field("/tmp/shim_lambda.ccf"));
     const bool io_ok = rd.data == run.final_omega.lambda.data && crc32_ieee(reinterpret_cast<const uint8_t*>("123456789"), 9) == 0xCBF43926u;
-    std::printf("shim ok: roundtrip %.3e final_time %.6f domain_error %d heat_err %.3e io %d\n", err / mx,
-                run.final_time, int(threw), herr / hmx, int(io_ok));
-    return (err / mx < 1e-12 && threw && herr / hmx < 1e-4 && io_ok) ? 0 : 1;
+    std::printf("shim ok: roundtrip %.3e final_time %.6f domain_error %d heat_err %.3e io %d spec_errors %d/6 "
+                "worst_residual %.3e\n", err / mx, run.final_time, int(threw), herr / hmx, int(io_ok), spec_errors,
+                hr.worst_residual);
+    return (err / mx < 1e-12 && threw && herr / hmx < 1e-4 && io_ok && spec_ok) ? 0 : 1;
 }

@@ -4,6 +4,7 @@ parsing, CLI parse errors and the exit-code contract (0 ok, 2 config, 3 numerica
 cylspec_main.cpp:366-385)."""
 import os
 import subprocess
+import tempfile
 
 import pytest
 
@@ -20,7 +21,9 @@ def cli(P):
 
 
 def run(cli, *args, cwd=None):
-    r = subprocess.run([cli, *map(str, args)], capture_output=True, text=True, cwd=cwd, timeout=120)
+    # never in the repo: the CLI writes failure_manifest.json under ./out on a failed run
+    r = subprocess.run([cli, *map(str, args)], capture_output=True, text=True, cwd=cwd or tempfile.mkdtemp(),
+                       timeout=120)
     return r.returncode, r.stderr
 
 

@@ -4,6 +4,7 @@ oracle (cylspec_main.cpp:67-282)."""
 import json
 import os
 import subprocess
+import tempfile
 
 import numpy as np
 import pytest
@@ -17,7 +18,8 @@ BIN = os.path.join(ROOT, "paper_2206_04827_b200", "bin", "cylspec")
 
 
 def run(*args):
-    r = subprocess.run([BIN, *map(str, args)], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([BIN, *map(str, args)], capture_output=True, text=True, timeout=600,
+                       cwd=tempfile.mkdtemp())  # never in the repo (failure_manifest.json lands under ./out)
     assert r.returncode == 0, r.stderr
     return r
 
@@ -28,6 +30,8 @@ def test_cli_heat_poisson_ns_transform(P, O, tmp_path):
     mf = json.loads((out / "manifest.json").read_text())
     assert mf["command"] == "heat" and abs(mf["final_time"] - 2.0) < 1e-12
     assert mf["max_rel_error"] < 1e-4
+    # a number like the reference's (cylspec_main.cpp:108): the solver data's Sylvester residual
+    assert isinstance(mf["worst_modal_residual"], float) and 0.0 < mf["worst_modal_residual"] < 1e-12
     assert [o["path"] for o in mf["outputs"]] == ["snapshot_0.ccf", "snapshot_1.ccf", "snapshot_2.ccf"]
     snap = P.read_field(out / "snapshot_2.ccf")
     assert snap.dtype == np.float64 and snap.shape == (16, 16, 16)

@@ -1,0 +1,704 @@
+// FP64 GEMMs on the INT8 tensor cores (tcgen05.mma kind::i8 + TMEM), see ozaki.hpp.
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+
+#include "context.hpp"
+#include "ozaki.hpp"
+
+namespace ccf {
+namespace {
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+
+// byte offset of (row r, reduction byte k) in a 128-byte-swizzled K-major slice
+__host__ __device__ __forceinline__ uint32_t oz_swz(int r, int k) {
+    return uint32_t(r >> 3) * 1024u + uint32_t(r & 7) * 128u + ((uint32_t((k >> 4) ^ (r & 7)) << 4) | uint32_t(k & 15));
+}
+
+// ---------------------------------------------------------------- digits
+// s = 2^e with max|row| < s; X = rint(x 2^(47 - e)) in [-2^47, 2^47): 48-bit two's complement,
+// digit 0 = signed top byte, digits 1..5 = unsigned lower bytes (ozaki.hpp)
+__device__ __forceinline__ int oz_exponent(double maxabs) {
+    int e = 0;
+    frexp(maxabs, &e);  // maxabs = f 2^e, f in [0.5, 1): maxabs < 2^e
+    return e;
+}
+__device__ __forceinline__ long long oz_fixed(double x, int e) {
+    long long X = __double2ll_rn(ldexp(x, 47 - e));
+    return X > (1LL << 47) - 1 ? (1LL << 47) - 1 : X;
+}
+__device__ __forceinline__ uint32_t oz_digit(long long X, int d) {
+    return d == 0 ? uint32_t(int(X >> 40)) & 255u : uint32_t(X >> (40 - 8 * d)) & 255u;
+}
+
+// A-side split: one warp per panel row, lane l holds reduction indices 4l .. 4l + 3
+__global__ void __launch_bounds__(256) oz_split_rows_kernel(const OzSplitJob* __restrict__ jobs) {
+    const OzSplitJob J = jobs[blockIdx.y];
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r >= J.rows_pad) return;
+    double v[4];
+    double mx = 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int k = 4 * lane + u;
+        v[u] = (r < J.nrows && k < J.ncols) ? __ldg(J.src[0] + long(r) * J.ld + k) : 0.0;
+        mx = fmax(mx, fabs(v[u]));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int e = mx > 0.0 ? oz_exponent(mx) : 0;
+    long long X[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) X[u] = mx > 0.0 ? oz_fixed(v[u], e) : 0;
+    const uint32_t off = oz_swz(r, 4 * lane);
+#pragma unroll
+    for (int d = 0; d < kOzS; ++d) {
+        const uint32_t w = oz_digit(X[0], d) | (oz_digit(X[1], d) << 8) | (oz_digit(X[2], d) << 16) | (oz_digit(X[3], d) << 24);
+        *reinterpret_cast<uint32_t*>(J.dst[0] + size_t(d) * J.stride + off) = w;
+    }
+    if (lane == 0) J.sc[r] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
+}
+
+// B-side split with transpose: CTA = (job, 128-row tile of the panel), thread = panel row = source
+// column (loads coalesced over the columns). Per plane: the tile max 2^e_p (CTA reduction); per row:
+// the common max of the normalised planes 2^e_r; digits of x 2^-e_p relative to 2^e_r are staged as
+// the swizzled panel image in shared memory and stored with bulk copies (16 KB per slice).
+constexpr int kSplitThreads = 128;
+size_t oz_split_cols_smem() { return size_t(kOzS) * 128 * kOzK + 1024; }
+__global__ void __launch_bounds__(kSplitThreads) oz_split_cols_kernel(const OzSplitJob* __restrict__ jobs) {
+    extern __shared__ __align__(1024) uint8_t dsm[];
+    uint8_t* stage = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+    __shared__ double red[kOzGroup][kSplitThreads / 32];
+    const OzSplitJob& J = jobs[blockIdx.y];
+    const int tile = blockIdx.x, ntiles = J.rows_pad / 128;
+    if (tile >= ntiles) return;
+    const int rl = threadIdx.x, r = tile * 128 + rl, lane = rl & 31, wid = rl >> 5;
+    const bool live = r < J.nrows;
+    const int nsrc = J.nsrc, ncols = J.ncols;
+    const long ld = J.ld;
+    double m[kOzGroup];
+#pragma unroll
+    for (int g = 0; g < kOzGroup; ++g) {
+        m[g] = 0.0;
+        if (g < nsrc && live) {
+            const double* src = J.src[g] + r;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            int k = 0;
+            for (; k + 4 <= ncols; k += 4) {
+                a0 = fmax(a0, fabs(__ldg(src + long(k) * ld)));
+                a1 = fmax(a1, fabs(__ldg(src + long(k + 1) * ld)));
+                a2 = fmax(a2, fabs(__ldg(src + long(k + 2) * ld)));
+                a3 = fmax(a3, fabs(__ldg(src + long(k + 3) * ld)));
+            }
+            for (; k < ncols; ++k) a0 = fmax(a0, fabs(__ldg(src + long(k) * ld)));
+            m[g] = fmax(fmax(a0, a1), fmax(a2, a3));
+        }
+        double w = m[g];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) w = fmax(w, __shfl_xor_sync(0xffffffffu, w, o));
+        if (lane == 0) red[g][wid] = w;
+    }
+    __syncthreads();
+    int ep[kOzGroup];
+    double sig = 0.0;
+#pragma unroll
+    for (int g = 0; g < kOzGroup; ++g) {
+        const double pm = fmax(fmax(red[g][0], red[g][1]), fmax(red[g][2], red[g][3]));
+        ep[g] = pm > 0.0 ? oz_exponent(pm) : 0;
+        if (g < nsrc) sig = fmax(sig, ldexp(m[g], -ep[g]));
+    }
+    const int er = sig > 0.0 ? oz_exponent(sig) : 0;
+    if (rl < nsrc && J.pe) J.pe[rl * ntiles + tile] = ep[rl];
+    for (int g = 0; g < nsrc; ++g) {
+        const double* src = J.src[g] + r;
+        const int E = er + ep[g];
+#pragma unroll 1
+        for (int kc = 0; kc < kOzK / 16; ++kc) {
+            uint32_t w[kOzS][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                long long X[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = 16 * kc + 4 * q + u;
+                    const double x = (live && k < ncols) ? __ldg(src + long(k) * ld) : 0.0;
+                    X[u] = sig > 0.0 ? oz_fixed(x, E) : 0;
+                }
+#pragma unroll
+                for (int d = 0; d < kOzS; ++d)
+                    w[d][q] = oz_digit(X[0], d) | (oz_digit(X[1], d) << 8) | (oz_digit(X[2], d) << 16) | (oz_digit(X[3], d) << 24);
+            }
+            const uint32_t off = oz_swz(rl, 16 * kc);
+#pragma unroll
+            for (int d = 0; d < kOzS; ++d)
+                *reinterpret_cast<uint4*>(stage + size_t(d) * 128 * kOzK + off) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staged image -> async proxy (bulk store)
+        __syncthreads();
+        if (rl == 0) {
+            for (int d = 0; d < kOzS; ++d)
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                                 J.dst[g] + size_t(d) * J.stride + size_t(tile) * 128 * kOzK),
+                             "r"(uint32_t(__cvta_generic_to_shared(stage + size_t(d) * 128 * kOzK))), "r"(uint32_t(128 * kOzK))
+                             : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // stage free for the next plane
+        }
+        __syncthreads();
+    }
+    J.sc[r] = sig > 0.0 ? ldexp(1.0, er) : 0.0;
+    if (rl == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete before exit
+}
+
+// B-side split with transpose and ONE scale per (plane, 128-row tile): CTA = (job, plane, tile). The
+// fp64 tile (K x 128 source columns) is read once into shared memory (coalesced), reduced to its max
+// 2^e (pe[plane * tiles + tile]), and split into digits relative to 2^e, staged as the swizzled
+// panel image and stored with bulk copies. Row scales sc = 1: every column keeps 48 bits relative to
+// the tile max (absolute accuracy 2^-48 of the tile, the max-norm accuracy of the products).
+constexpr int kTileThreads = 256;
+size_t oz_split_tile_smem() { return size_t(128) * 128 * 8 + size_t(kOzS) * 128 * kOzK + 1024; }
+__global__ void __launch_bounds__(kTileThreads) oz_split_tile_kernel(const OzSplitJob* __restrict__ jobs) {
+    extern __shared__ __align__(1024) uint8_t dsm[];
+    uint8_t* stage = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+    double* tileb = reinterpret_cast<double*>(stage + size_t(kOzS) * 128 * kOzK);  // [128 k][128 c]
+    __shared__ double red[kTileThreads / 32];
+    const OzSplitJob& J = jobs[blockIdx.y / kOzGroup];
+    const int g = blockIdx.y % kOzGroup, tile = blockIdx.x, ntiles = J.rows_pad / 128;
+    if (g >= J.nsrc || tile >= ntiles) return;
+    const int tid = threadIdx.x, c = tid & 127, kh = tid >> 7;
+    const int r = tile * 128 + c;
+    const bool live = r < J.nrows;
+    const int ncols = J.ncols;
+    const double* src = J.src[g] + r;
+    double mx = 0.0;
+#pragma unroll 8
+    for (int i = 0; i < 64; ++i) {
+        const int k = 2 * i + kh;
+        const double x = (live && k < ncols) ? __ldg(src + long(k) * J.ld) : 0.0;
+        tileb[k * 128 + c] = x;
+        mx = fmax(mx, fabs(x));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((tid & 31) == 0) red[tid >> 5] = mx;
+    __syncthreads();
+    mx = red[0];
+#pragma unroll
+    for (int w = 1; w < kTileThreads / 32; ++w) mx = fmax(mx, red[w]);
+    const int e = mx > 0.0 ? oz_exponent(mx) : 0;
+#pragma unroll 1
+    for (int kc = 0; kc < 4; ++kc) {
+        const int k0 = kh * 64 + kc * 16;
+        uint32_t w[kOzS][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            long long X[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) X[u] = mx > 0.0 ? oz_fixed(tileb[(k0 + 4 * q + u) * 128 + c], e) : 0;
+#pragma unroll
+            for (int d = 0; d < kOzS; ++d)
+                w[d][q] = oz_digit(X[0], d) | (oz_digit(X[1], d) << 8) | (oz_digit(X[2], d) << 16) | (oz_digit(X[3], d) << 24);
+        }
+        const uint32_t off = oz_swz(c, k0);
+#pragma unroll
+        for (int d = 0; d < kOzS; ++d)
+            *reinterpret_cast<uint4*>(stage + size_t(d) * 128 * kOzK + off) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+        for (int d = 0; d < kOzS; ++d)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                             J.dst[g] + size_t(d) * J.stride + size_t(tile) * 128 * kOzK),
+                         "r"(uint32_t(__cvta_generic_to_shared(stage + size_t(d) * 128 * kOzK))), "r"(uint32_t(128 * kOzK))
+                         : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (J.pe) J.pe[g * ntiles + tile] = e;
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    if (g == 0 && kh == 0) J.sc[r] = 1.0;
+}
+
+// B-side split into the MN-major panel layout (slice of a 128-column tile: 128 k-rows of 128 column
+// bytes, row k at oz_swz(k, n); tcgen05 reads it with b_major = MN): no transpose, so a CTA (512
+// threads) holds the whole (plane, tile) in registers (warp = 8 k-rows, lane = 4 columns; loads and
+// stores fully coalesced), reduces its max 2^e (pe[plane * tiles + tile]) and writes the digits
+// relative to 2^e in one pass. Column scales sc = 1 (absolute accuracy 2^-48 of the tile max).
+constexpr int kMnThreads = 512;
+__global__ void __launch_bounds__(kMnThreads) oz_split_mn_kernel(const OzSplitJob* __restrict__ jobs) {
+    __shared__ double red[kMnThreads / 32];
+    const OzSplitJob& J = jobs[blockIdx.y / kOzGroup];
+    const int g = blockIdx.y % kOzGroup, tile = blockIdx.x, ntiles = J.rows_pad / 128;
+    if (g >= J.nsrc || tile >= ntiles) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int n0 = tile * 128 + 4 * lane;  // this lane's 4 columns
+    const int ncols = J.ncols, nrows = J.nrows;
+    const double* src = J.src[g] + n0;
+    double v[8][4];
+    double mx = 0.0;
+    const bool vec = n0 + 4 <= nrows && ((reinterpret_cast<uintptr_t>(src) | uintptr_t(J.ld * 8)) & 15) == 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int k = wid * 8 + i;
+        if (k < ncols && vec) {
+            const double2 a = __ldg(reinterpret_cast<const double2*>(src + long(k) * J.ld));
+            const double2 b = __ldg(reinterpret_cast<const double2*>(src + long(k) * J.ld + 2));
+            v[i][0] = a.x; v[i][1] = a.y; v[i][2] = b.x; v[i][3] = b.y;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[i][u] = (k < ncols && n0 + u < nrows) ? __ldg(src + long(k) * J.ld + u) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mx = fmax(mx, fabs(v[i][u]));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) red[wid] = mx;
+    __syncthreads();
+    mx = red[0];
+#pragma unroll
+    for (int w = 1; w < kMnThreads / 32; ++w) mx = fmax(mx, red[w]);
+    const int e = mx > 0.0 ? oz_exponent(mx) : 0;
+    uint8_t* dst = J.dst[g] + size_t(tile) * 128 * kOzK;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int k = wid * 8 + i;
+        long long X[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) X[u] = mx > 0.0 ? oz_fixed(v[i][u], e) : 0;
+        const uint32_t off = oz_swz(k, 4 * lane);
+#pragma unroll
+        for (int d = 0; d < kOzS; ++d)
+            *reinterpret_cast<uint32_t*>(dst + size_t(d) * J.stride + off) =
+                oz_digit(X[0], d) | (oz_digit(X[1], d) << 8) | (oz_digit(X[2], d) << 16) | (oz_digit(X[3], d) << 24);
+    }
+    if (threadIdx.x == 0 && J.pe) J.pe[g * ntiles + tile] = e;
+    if (g == 0 && threadIdx.x < 128) J.sc[tile * 128 + threadIdx.x] = 1.0;
+}
+
+// ---------------------------------------------------------------- tcgen05 / mbarrier primitives
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nOZW:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra OZW;\n}\n" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
+                 "l"(src), "r"(bytes), "r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+// K-major, 128-byte swizzle, 1024 B between 8-row atoms, sm_100 descriptor version 1
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+    return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) | (uint64_t(1) << 46) |
+           (uint64_t(2) << 61);
+}
+// kind::i8, D = s32, M = 128, N = kOzNT, K-major A and B; signedness per digit (digit 0 signed)
+__host__ __device__ constexpr uint32_t oz_idesc(int asig, int bsig) {
+    return (2u << 4) | (uint32_t(asig) << 7) | (uint32_t(bsig) << 10) | (uint32_t(kOzNT >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+
+constexpr uint32_t kSlice = 128 * kOzK;  // 16 KB: one digit slice of a 128-row panel block
+constexpr uint32_t kPair = 2 * kSlice;   // A_d and B_d of one term
+constexpr int kBufs = 7;                 // pair buffers: a term holds 6, the 7th takes the next term's first
+constexpr int kSlots = 4;                // TMEM accumulator ring: 4 x 128 columns
+constexpr int kLevels = 7;               // L = d + d' <= 6: 26 digit-pair products
+constexpr int kEpiWarps = 8;             // warpgroups 1 and 2: 2 per TMEM lane quadrant (64 columns each)
+constexpr int kThreads = 128 + 32 * kEpiWarps;
+constexpr size_t kSmemBufs = size_t(kBufs) * kPair;
+
+__device__ unsigned long long g_oz_trace[4096];  // diagnostics (CCF_OZ_MODE bit 2): block 0 event times
+__device__ __forceinline__ unsigned long long oz_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define OZ_TRACE(idx)                                                                     \
+    do {                                                                                  \
+        if ((mode & 4) && blockIdx.x == 0 && (idx) < 4096) g_oz_trace[(idx)] = oz_now(); \
+    } while (0)
+
+struct OzBars {
+    uint64_t full[kBufs], empty[kBufs], accfull[kSlots], accempty[kSlots];
+    uint64_t sbfull, sbempty;  // column scales of the current tile (one slot)
+    uint32_t tmem_base;
+};
+constexpr size_t kSbBytes = 128 * sizeof(double);
+constexpr size_t kBarsBytes = (sizeof(OzBars) + 127) / 128 * 128;  // the column-scale slot is a bulk-copy target
+
+
+// Persistent: one CTA per SM walks 128 x 128 output tiles (items). Warpgroup 0: warp 0 producer,
+// warp 1 MMA issuer (registers released with setmaxnreg); warpgroups 1-2: epilogue (registers raised).
+// The six digit-slice pairs (A_d, B_d) of a term rotate through seven 32 KB buffers (buffer
+// (6 tau + d) mod 7 for term tau), so the next term's first slices load while the current term
+// finishes. The MMA thread issues level by level (level L = all pairs d + d' = L, 4 K-steps each,
+// M = N = 128) into a 4-slot TMEM ring; pair d is released after its last use (d = 0 after level 5,
+// the others after level 6). The 8 epilogue warps drain each level as it completes: each int32 is
+// converted exactly (1.5 2^52 bit trick) and accumulated with the row's weight 2^-(14 + 8L) x row
+// scale (two FP64 instructions per element and level); the column scales, shared by an item's terms,
+// multiply the tile once before its 256-bit stores. MMA, epilogue and copies of
+// neighbouring terms overlap. N = 128 per instruction keeps the tensor pipe at ~4 POPS (N = 64 costs
+// ~60 cycles per instruction, tools/microbench/i8mma.cu).
+__global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __restrict__ terms,
+                                                              const OzItem* __restrict__ items, int nitems, int mode,
+                                                              int bmn) {
+    extern __shared__ __align__(1024) uint8_t dsm[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+    OzBars& bar = *reinterpret_cast<OzBars*>(sm + kSmemBufs);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kBufs; ++i) {
+            mbar_init(&bar.full[i], 1);
+            mbar_init(&bar.empty[i], 1);
+        }
+        for (int i = 0; i < kSlots; ++i) {
+            mbar_init(&bar.accfull[i], 1);
+            mbar_init(&bar.accempty[i], kEpiWarps);
+        }
+        mbar_init(&bar.sbfull, 1);
+        mbar_init(&bar.sbempty, kEpiWarps);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    double* sbs = reinterpret_cast<double*>(sm + kSmemBufs + kBarsBytes);  // column-scale slot
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&bar.tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_before();
+    __syncthreads();
+    tc_after();
+    const uint32_t tmem = bar.tmem_base;
+
+    if (warp < 4) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+        if (warp == 0) {  // ---------------- producer
+            // items are sorted by descending term count: the term-less ones (zero outputs) come last
+            if (lane == 0 && int(blockIdx.x) < nitems && items[blockIdx.x].t1 > items[blockIdx.x].t0) {
+                uint32_t pc = 0;  // pair counter over all terms (buffer pc % 7, use (pc / 7))
+                uint32_t sbc = 0;  // column-scale copies
+                int it = blockIdx.x;
+                OzItem I = items[it];
+                int t = I.t0;
+                OzTerm T = terms[t];
+                while (true) {  // (item, term) walk with the next descriptors loaded one step ahead
+                    int itn = it, tn = t + 1;
+                    OzItem In = I;
+                    if (tn >= I.t1) {
+                        itn = it + gridDim.x;
+                        if (itn < nitems) {
+                            In = items[itn];
+                            tn = In.t0;
+                            if (In.t1 <= In.t0) itn = nitems;
+                        }
+                    }
+                    const bool more = itn < nitems;
+                    const OzTerm Tn = more ? terms[tn] : T;
+                    const uint8_t* bsrc = T.b + size_t(I.n0) * kOzK;
+                    for (int d = 0; d < kOzS; ++d, ++pc) {
+                        const uint32_t b = pc % kBufs, use = pc / kBufs;
+                        mbar_wait(&bar.empty[b], (use & 1) ^ 1);
+                        OZ_TRACE(pc);
+                        mbar_expect(&bar.full[b], kPair);
+                        bulk_g2s(sm + size_t(b) * kPair, T.a + size_t(d) * kSlice, kSlice, &bar.full[b]);
+                        bulk_g2s(sm + size_t(b) * kPair + kSlice, bsrc + size_t(d) * T.bstride, kSlice, &bar.full[b]);
+                    }
+                    if (t == I.t0 && T.sb) {  // the tile's column scales (read by the epilogue after its last term)
+                        mbar_wait(&bar.sbempty, (sbc & 1) ^ 1);
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // epilogue reads -> next bulk write
+                        mbar_expect(&bar.sbfull, uint32_t(kSbBytes));
+                        bulk_g2s(sbs, T.sb + I.n0, uint32_t(kSbBytes), &bar.sbfull);
+                        ++sbc;
+                    }
+                    if (!more) break;
+                    it = itn;
+                    t = tn;
+                    I = In;
+                    T = Tn;
+                }
+            }
+            __syncwarp();
+        } else if (warp == 1) {  // ---------------- MMA issuer
+            if (lane == 0) {
+                uint32_t pc = 0, g = 0;
+                const uint32_t s0 = su32(sm);
+                OzItem In = int(blockIdx.x) < nitems ? items[blockIdx.x] : OzItem{};
+                for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                    const OzItem I = In;
+                    if (it + int(gridDim.x) < nitems) In = items[it + gridDim.x];  // one item ahead
+                    for (int t = I.t0; t < I.t1; ++t, pc += kOzS) {
+                        for (int L = 0; L < kLevels; ++L, ++g) {
+                            if (L < kOzS) {  // pair L arrives (level L uses pairs d, d' <= L)
+                                const uint32_t q = pc + L;
+                                mbar_wait(&bar.full[q % kBufs], (q / kBufs) & 1);
+                            }
+                            OZ_TRACE(1024 + g);
+                            const uint32_t slot = g % kSlots;
+                            mbar_wait(&bar.accempty[slot], ((g / kSlots) & 1) ^ 1);
+                            OZ_TRACE(2048 + g);
+                            tc_after();
+                            const uint32_t acc = tmem + slot * 128;
+                            if (!(mode & 2)) {
+                                bool first = true;
+                                for (int d = (L > kOzS - 1 ? L - (kOzS - 1) : 0); d <= L && d < kOzS; ++d) {
+                                    const int dp = L - d;
+                                    const uint64_t ad = sdesc(s0 + ((pc + d) % kBufs) * kPair);
+                                    const uint64_t bd = sdesc(s0 + ((pc + dp) % kBufs) * kPair + kSlice);
+                                    const uint32_t id = oz_idesc(d == 0, dp == 0) | (bmn ? (1u << 16) : 0u);
+                                    const uint32_t bstep = bmn ? 256u : 2u;  // 32 k-rows (MN-major) or 32 bytes, >> 4
+#pragma unroll
+                                    for (int k = 0; k < kOzK / 32; ++k) {
+                                        mma_i8(acc, ad + 2 * k, bd + bstep * k, id, first ? 0u : 1u);
+                                        first = false;
+                                    }
+                                }
+                            }
+                            tc_commit(&bar.accfull[slot]);
+                            if (L == kOzS - 1) tc_commit(&bar.empty[pc % kBufs]);  // pair 0: last used at level 5
+                            if (L == kLevels - 1)
+                                for (int d = 1; d < kOzS; ++d) tc_commit(&bar.empty[(pc + d) % kBufs]);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    } else {  // ---------------- epilogue: warpgroups 1-2; TMEM lane quadrant warp % 4, 64-column half
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+        const int q = warp & 3, half = (warp - 4) >> 2;
+        const int row = q * 32 + lane;
+        const uint32_t tq = tmem + (uint32_t(q * 32) << 16) + uint32_t(half * 64);
+        uint32_t g = 0, sbc = 0;
+        OzItem In = int(blockIdx.x) < nitems ? items[blockIdx.x] : OzItem{};
+        // the next term's descriptor and row factor are loaded one term ahead (dependent global loads)
+        const OzTerm* Tp = (int(blockIdx.x) < nitems && In.t1 > In.t0) ? terms + In.t0 : nullptr;
+        double fnext = Tp ? __ldg(Tp->sa + row) * (Tp->pe ? ldexp(1.0, __ldg(Tp->pe + In.n0 / 128)) : 1.0) : 0.0;
+        const double* sbnext = Tp ? Tp->sb : nullptr;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            const OzItem I = In;
+            if (it + int(gridDim.x) < nitems) In = items[it + gridDim.x];
+            const double* sbc_item = sbnext;  // column scales of this tile (its first term's B)
+            double acc[64];
+#pragma unroll
+            for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+            for (int t = I.t0; t < I.t1; ++t) {
+                const double sa = fnext;  // row scale x the B plane's tile normalisation (transposed splits)
+                {  // prefetch: the next term of this item, else the next item's first
+                    const bool last = t + 1 >= I.t1;
+                    const bool more = !last || (it + int(gridDim.x) < nitems && In.t1 > In.t0);
+                    if (more) {
+                        const OzTerm* Tn = terms + (last ? In.t0 : t + 1);
+                        const int n0 = last ? In.n0 : I.n0;
+                        fnext = __ldg(Tn->sa + row) * (Tn->pe ? ldexp(1.0, __ldg(Tn->pe + n0 / 128)) : 1.0);
+                        if (last) sbnext = Tn->sb;
+                    }
+                }
+#pragma unroll 1
+                for (int L = 0; L < kLevels; ++L, ++g) {
+                    const uint32_t slot = g % kSlots;
+                    mbar_wait(&bar.accfull[slot], (g / kSlots) & 1);
+                    if (warp == 4 && lane == 0) OZ_TRACE(3072 + g);
+                    tc_after();
+                    if (!(mode & 1)) {
+                        uint32_t v[64];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            tmem_ld16(tq + slot * 128 + uint32_t(c * 16), *reinterpret_cast<uint32_t(*)[16]>(v + 16 * c));
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        const double f = sa * ldexp(1.0, -14 - 8 * L);  // row scale x level weight (powers of 2)
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) {
+                            const int p = int(v[j]);
+                            // int32 -> fp64 exactly: 1.5 2^52 + p as a bit pattern, minus 1.5 2^52
+                            const double x = __hiloint2double(0x43380000 + (p >> 31), p) - 6755399441055744.0;
+                            acc[j] = fma(x, f, acc[j]);
+                        }
+                    }
+                    tc_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bar.accempty[slot]);
+                }
+            }
+            if (warp == 4 && lane == 0) OZ_TRACE(3584 + (it - blockIdx.x) / gridDim.x);
+            if (I.t1 > I.t0 && sbc_item) {  // column scales (copied to shared memory by the producer)
+                mbar_wait(&bar.sbfull, sbc & 1);
+                const double2* sbp = reinterpret_cast<const double2*>((mode & 16) ? sbc_item + I.n0 + half * 64 : sbs + half * 64);
+#pragma unroll
+                for (int j = 0; j < 64; j += 2) {
+                    const double2 sb = sbp[j / 2];
+                    acc[j] *= I.alpha * sb.x;
+                    acc[j + 1] *= I.alpha * sb.y;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar.sbempty);
+                ++sbc;
+            }
+            if (warp == 4 && lane == 0) OZ_TRACE(3712 + (it - blockIdx.x) / gridDim.x);
+            if (row < I.m && !(mode & 8)) {
+                double* crow = I.c + long(row) * I.ldc + half * 64;
+                const int nv = I.n - half * 64;
+                if (nv >= 64 && ((reinterpret_cast<uintptr_t>(crow) & 31) == 0)) {
+#pragma unroll
+                    for (int j = 0; j < 64; j += 4)
+                        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(crow + j), "d"(acc[j]), "d"(acc[j + 1]),
+                                     "d"(acc[j + 2]), "d"(acc[j + 3])
+                                     : "memory");
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 64; ++j)
+                        if (j < nv) crow[j] = acc[j];
+                }
+            }
+            if (warp == 4 && lane == 0) OZ_TRACE(3840 + (it - blockIdx.x) / gridDim.x);
+        }
+    }
+    tc_before();
+    __syncthreads();
+    tc_after();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+}  // namespace
+
+void oz_trace_dump() {  // diagnostics (CCF_OZ_MODE bit 2): block 0's event times, ns from the first
+    std::vector<unsigned long long> t(4096);
+    cudaMemcpyFromSymbol(t.data(), g_oz_trace, 4096 * 8);
+    const unsigned long long t0 = t[0];
+    for (int i = 0; i < 48; ++i)
+        std::printf("level %2d: pair-issue %7lld  mma-start %7lld  mma-go %7lld  epi-got %7lld\n", i,
+                    i < 1024 && t[i] ? (long long)(t[i] - t0) : -1, t[1024 + i] ? (long long)(t[1024 + i] - t0) : -1,
+                    t[2048 + i] ? (long long)(t[2048 + i] - t0) : -1, t[3072 + i] ? (long long)(t[3072 + i] - t0) : -1);
+    for (int i = 0; i < 6; ++i)
+        std::printf("tile %d: drained %7lld  scaled %7lld  stored %7lld\n", i, (long long)(t[3584 + i] - t0),
+                    (long long)(t[3712 + i] - t0), (long long)(t[3840 + i] - t0));
+}
+
+size_t oz_smem_bytes() { return kSmemBufs + kBarsBytes + kSbBytes + 1024; }
+
+void OzSplitPlan::upload() {
+    maxrows = 0;
+    for (const OzSplitJob& j : jobs) {
+        if (j.ncols > kOzK || j.nrows > j.rows_pad || j.rows_pad % 8 || j.nsrc < 1 || j.nsrc > kOzGroup ||
+            (!transpose && !mn && j.nsrc != 1) || ((transpose || mn) && j.rows_pad % 128))
+            throw Error(INTERNAL, "OzSplitPlan: bad job shape");
+        maxrows = std::max(maxrows, j.rows_pad);
+    }
+    if (d) cudaFree(d);
+    d = nullptr;
+    if (jobs.empty()) return;
+    CCF_CUDA(cudaMalloc(&d, jobs.size() * sizeof(OzSplitJob)));
+    CCF_H2D(d, jobs.data(), jobs.size() * sizeof(OzSplitJob));
+}
+
+void OzSplitPlan::launch(cudaStream_t s) const {
+    if (jobs.empty()) return;
+    if (mn) {
+        const dim3 grid(unsigned(maxrows / 128), unsigned(jobs.size() * kOzGroup));
+        oz_split_mn_kernel<<<grid, kMnThreads, 0, s>>>(d);
+    } else if (transpose && tile_scale) {
+        static bool attr = false;
+        if (!attr) {
+            CCF_CUDA(cudaFuncSetAttribute(oz_split_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(oz_split_tile_smem())));
+            attr = true;
+        }
+        const dim3 grid(unsigned(maxrows / 128), unsigned(jobs.size() * kOzGroup));
+        oz_split_tile_kernel<<<grid, kTileThreads, oz_split_tile_smem(), s>>>(d);
+    } else if (transpose) {
+        static bool attr = false;
+        if (!attr) {
+            CCF_CUDA(cudaFuncSetAttribute(oz_split_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(oz_split_cols_smem())));
+            attr = true;
+        }
+        const dim3 grid(unsigned(maxrows / 128), unsigned(jobs.size()));
+        oz_split_cols_kernel<<<grid, kSplitThreads, oz_split_cols_smem(), s>>>(d);
+    } else {
+        const dim3 grid(unsigned((maxrows + 7) / 8), unsigned(jobs.size()));
+        oz_split_rows_kernel<<<grid, 256, 0, s>>>(d);
+    }
+    CCF_CUDA(cudaGetLastError());
+}
+
+OzSplitPlan::~OzSplitPlan() {
+    if (d) cudaFree(d);
+}
+
+void OzGemmPlan::upload() {
+    if (dterms) cudaFree(dterms);
+    if (ditems) cudaFree(ditems);
+    dterms = nullptr;
+    ditems = nullptr;
+    flops = 0.0;
+    for (const OzItem& it : items) {
+        if (it.t0 < 0 || it.t1 > int(terms.size()) || it.t0 > it.t1 || it.n0 % kOzNT || it.m > 128 || it.n > kOzNT)
+            throw Error(INTERNAL, "OzGemmPlan: bad item");
+        flops += 2.0 * it.m * it.n * kOzK * (it.t1 - it.t0);
+    }
+    // long items first (persistent round-robin assignment)
+    std::stable_sort(items.begin(), items.end(), [](const OzItem& x, const OzItem& y) { return x.t1 - x.t0 > y.t1 - y.t0; });
+    if (terms.empty() || items.empty()) return;
+    CCF_CUDA(cudaMalloc(&dterms, terms.size() * sizeof(OzTerm)));
+    CCF_CUDA(cudaMalloc(&ditems, items.size() * sizeof(OzItem)));
+    CCF_H2D(dterms, terms.data(), terms.size() * sizeof(OzTerm));
+    CCF_H2D(ditems, items.data(), items.size() * sizeof(OzItem));
+}
+
+void OzGemmPlan::launch(cudaStream_t s) const {
+    if (items.empty()) return;
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        CCF_CUDA(cudaGetDevice(&dev));
+        CCF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        CCF_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(oz_smem_bytes())));
+    }
+    const unsigned grid = unsigned(std::min<size_t>(items.size(), size_t(nsm)));
+    static const int mode = std::getenv("CCF_OZ_MODE") ? std::atoi(std::getenv("CCF_OZ_MODE")) : 0;  // diagnostics
+    oz_gemm_kernel<<<grid, kThreads, oz_smem_bytes(), s>>>(dterms, ditems, int(items.size()), mode, int(b_mn));
+    CCF_CUDA(cudaGetLastError());
+}
+
+OzGemmPlan::~OzGemmPlan() {
+    if (dterms) cudaFree(dterms);
+    if (ditems) cudaFree(ditems);
+}
+
+}  // namespace ccf

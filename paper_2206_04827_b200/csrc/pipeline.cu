@@ -575,6 +575,11 @@ Pipeline::Pipeline(Ctx& c_) : c(c_), tp(c_), T(c_.tensor_doubles(false)) {
     big_scratch(size_t(3) * T);  // pencil scratch: max(pt_synth 2 pairs x 2, curl 6 pencils per thread)
 }
 
+OzPipe& Pipeline::oz() {
+    if (!oz_) oz_ = std::make_unique<OzPipe>(*this);
+    return *oz_;
+}
+
 double* Pipeline::scratch(int i) {
     // mode sharding: the theta stage's inputs / outputs live in the peer-mapped exchange buffer
     if (c.sh.xbuf && i >= 6 && i < 6 + kExchangeTensors) return c.sh.xbuf + size_t(i - 6) * size_t(T);
@@ -1001,6 +1006,8 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     // ---- composite r synthesis -> (r, z)-values of the 6 velocity / vorticity components
     // eigY: the z tensors are Y = Z (QR S_z) in eigen coordinates along r, the synthesis blocks carry QL
     const int ycls[8] = {int(eigY), 0, 0, 0, 0, 0, 0, 0};
+    const bool oz_rs = eigY && oz().rsynth(Z, val);  // INT8 tensor cores (ozpipe.cu)
+    if (!oz_rs) {
     GemmPlan& rs = gemm(ptr_key(eigY ? "nrsY" : "nrs", 4, keyp, keyp, ycls), fresh);  // outputs: scratch
     if (fresh) {
         for (int pr = 0; pr < 2; ++pr)
@@ -1026,6 +1033,7 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     rs.launch(c.stream);
     c.gemm_flops += rs.flops();
     c.launches += 2;
+    }
     c.mark("X1_rz_synthesis");
     c.shard_sync();  // every owner's values written, every owner done with the previous step's outputs
     theta_cross(val, av);
@@ -1038,6 +1046,10 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     const int ecls[8] = {eig ? 1 : 0, int(dealias), 0, 0, 0, 0, 0, 0};
     // the analysis side reads only scratch tensors: key it on the outputs
     const void* okeyp[2] = {lam_n, gam_n};
+    if (eig && !dealias && oz().analyze(av, Y, lam_n, gam_n)) {  // X3 + C on the INT8 tensor cores (ozpipe.cu)
+        c.mark("C_curl_decompose");
+        return;
+    }
     GemmPlan& za = gemm(ptr_key("nza", 2, okeyp, okeyp, ecls), fresh);
     if (fresh) {
         for (int x = 0; x < 5; ++x) {
@@ -1520,6 +1532,7 @@ void Pipeline::ensure_eigen(DevSet& pset) {
 // (dsynth_eig_) consumes Y directly: one product per output instead of QL Z then T3 QS.
 // Z_t is base-relative (ring slots): bases z[0..ntensor).
 void Pipeline::eigen_ysynth(int ntensor, const double* const* z, double* const* outS, double* const* outD) {
+    if (oz().ysynth(ntensor, z, outS, outD)) return;  // INT8 tensor cores (ozpipe.cu)
     const Geo& g = c.gh;
     const int M = c.M, N = c.N, nh = g.nh;
     const int Np = N + (N & 1);

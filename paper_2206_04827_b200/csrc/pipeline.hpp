@@ -14,6 +14,10 @@
 
 #include <vector>
 
+#include <map>
+#include <memory>
+#include <string>
+
 #include "composite.hpp"
 #include "context.hpp"
 
@@ -73,6 +77,8 @@ struct GemmPlan {
     double flops() const { return 2.0 * M * N * K * double(A.size()); }  // every term is one M x N x K product
     ~GemmPlan();
 };
+
+struct OzPipe;
 
 class Pipeline {
 public:
@@ -160,6 +166,31 @@ public:  // internal state (used by the NS stepper and the C-ABI layer)
     void ensure_dealias(DevSet* eig);
     std::map<const void*, const double* const*> eig_rt_;      // per set: RT table per (slot, k0)
     bool fd_fused_ = false, fd_attr_ = false;                    // CCF_FDSOLVE_FUSED=1: fused solve kernel
+    std::unique_ptr<OzPipe> oz_;                                 // INT8 tensor-core (Ozaki) product stages
+    OzPipe& oz();
+};
+
+// The NS step's dense product stages on the INT8 tensor cores (ozpipe.cu, ozaki.hpp).
+struct OzPipe {
+    explicit OzPipe(Pipeline& p);
+    ~OzPipe();
+    Pipeline& P;
+    bool on = false;
+    int mask = 7;
+    // each returns false when the stage is not available (size, first build during a graph capture):
+    // the caller then runs its FP64 DMMA plan
+    bool ysynth(int ntensor, const double* const* z, double* const* outS, double* const* outD);
+    bool rsynth(double* const (&Z)[2][3], double* const* val);
+    bool analyze(double* const* av, double* const* Y, double* lam_n, double* gam_n);
+
+private:
+    struct Stage;
+    std::map<std::string, std::unique_ptr<Stage>> stages_;
+    Stage* stage(const std::string& key, bool& fresh);
+    bool ensure_const();
+    const DevSet* const_set_ = nullptr;
+    DBuf cpan_, csc_, cpe_, ysp_, ysc_, rsp_, rsc_, rpe_, zap_, zasc_, rap_, rasc_, rape_;
+    int syn0_ = 0, ana0_ = 0;
 };
 
 struct NSState {

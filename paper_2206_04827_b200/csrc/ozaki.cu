@@ -33,6 +33,33 @@ __device__ __forceinline__ uint32_t oz_digit(long long X, int d) {
     return d == 0 ? uint32_t(int(X >> 40)) & 255u : uint32_t(X >> (40 - 8 * d)) & 255u;
 }
 
+// The digits of four values as six packed words (word d holds digit d of value u in byte u): scale
+// 2^(47 - e) and round with one FMA against 1.5 2^52 (exact: |x 2^(47-e)| < 2^47), so the low 48 bits
+// of the double ARE the two's-complement integer X, whose bytes 5..0 are digits 0..5 (digit 0 signed).
+// Byte transposes with PRMT: 12 per four values.
+__device__ __forceinline__ void oz_pack4(const double (&x)[4], double scale, uint32_t (&w)[kOzS]) {
+    uint32_t lo[4], hi[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const double y = fma(x[u], scale, 6755399441055744.0);
+        lo[u] = uint32_t(__double2loint(y));
+        hi[u] = uint32_t(__double2hiint(y)) - 0x43380000u;  // X = bits(y) - bits(1.5 2^52)
+        if (hi[u] == 0x8000u) {  // X = 2^47 (a rounded maximum): clamp to 2^47 - 1
+            hi[u] = 0x7FFFu;
+            lo[u] = 0xFFFFFFFFu;
+        }
+    }
+    const uint32_t a = __byte_perm(lo[0], lo[1], 0x5140), b = __byte_perm(lo[2], lo[3], 0x5140);
+    const uint32_t c = __byte_perm(lo[0], lo[1], 0x7362), d = __byte_perm(lo[2], lo[3], 0x7362);
+    const uint32_t e = __byte_perm(hi[0], hi[1], 0x5140), f = __byte_perm(hi[2], hi[3], 0x5140);
+    w[0] = __byte_perm(e, f, 0x7632);  // byte 5 of X
+    w[1] = __byte_perm(e, f, 0x5410);  // byte 4
+    w[2] = __byte_perm(c, d, 0x7632);  // byte 3
+    w[3] = __byte_perm(c, d, 0x5410);  // byte 2
+    w[4] = __byte_perm(a, b, 0x7632);  // byte 1
+    w[5] = __byte_perm(a, b, 0x5410);  // byte 0
+}
+
 // A-side split: one warp per panel row, lane l holds reduction indices 4l .. 4l + 3
 __global__ void __launch_bounds__(256) oz_split_rows_kernel(const OzSplitJob* __restrict__ jobs) {
     const OzSplitJob J = jobs[blockIdx.y];
@@ -50,15 +77,11 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const OzSplitJob* __
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const int e = mx > 0.0 ? oz_exponent(mx) : 0;
-    long long X[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) X[u] = mx > 0.0 ? oz_fixed(v[u], e) : 0;
+    uint32_t w[kOzS];
+    oz_pack4(v, mx > 0.0 ? ldexp(1.0, 47 - e) : 0.0, w);
     const uint32_t off = oz_swz(r, 4 * lane);
 #pragma unroll
-    for (int d = 0; d < kOzS; ++d) {
-        const uint32_t w = oz_digit(X[0], d) | (oz_digit(X[1], d) << 8) | (oz_digit(X[2], d) << 16) | (oz_digit(X[3], d) << 24);
-        *reinterpret_cast<uint32_t*>(J.dst[0] + size_t(d) * J.stride + off) = w;
-    }
+    for (int d = 0; d < kOzS; ++d) *reinterpret_cast<uint32_t*>(J.dst[0] + size_t(d) * J.stride + off) = w[d];
     if (lane == 0) J.sc[r] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
 }
 
@@ -262,18 +285,16 @@ __global__ void __launch_bounds__(kMnThreads) oz_split_mn_kernel(const OzSplitJo
 #pragma unroll
     for (int w = 1; w < kMnThreads / 32; ++w) mx = fmax(mx, red[w]);
     const int e = mx > 0.0 ? oz_exponent(mx) : 0;
+    const double scale = mx > 0.0 ? ldexp(1.0, 47 - e) : 0.0;
     uint8_t* dst = J.dst[g] + size_t(tile) * 128 * kOzK;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const int k = wid * 8 + i;
-        long long X[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) X[u] = mx > 0.0 ? oz_fixed(v[i][u], e) : 0;
+        uint32_t w[kOzS];
+        oz_pack4(v[i], scale, w);
         const uint32_t off = oz_swz(k, 4 * lane);
 #pragma unroll
-        for (int d = 0; d < kOzS; ++d)
-            *reinterpret_cast<uint32_t*>(dst + size_t(d) * J.stride + off) =
-                oz_digit(X[0], d) | (oz_digit(X[1], d) << 8) | (oz_digit(X[2], d) << 16) | (oz_digit(X[3], d) << 24);
+        for (int d = 0; d < kOzS; ++d) *reinterpret_cast<uint32_t*>(dst + size_t(d) * J.stride + off) = w[d];
     }
     if (threadIdx.x == 0 && J.pe) J.pe[g * ntiles + tile] = e;
     if (g == 0 && threadIdx.x < 128) J.sc[tile * 128 + threadIdx.x] = 1.0;
@@ -340,8 +361,14 @@ constexpr uint32_t kPair = 2 * kSlice;   // A_d and B_d of one term
 constexpr int kBufs = 7;                 // pair buffers: a term holds 6, the 7th takes the next term's first
 constexpr int kSlots = 4;                // TMEM accumulator ring: 4 x 128 columns
 constexpr int kLevels = 7;               // L = d + d' <= 6: 26 digit-pair products
-constexpr int kEpiWarps = 8;             // warpgroups 1 and 2: 2 per TMEM lane quadrant (64 columns each)
+constexpr int kEpiWarps = 16;            // warpgroups 1-4: 4 per TMEM lane quadrant
+constexpr int kCols = 128 * 4 / kEpiWarps;  // output columns per epilogue thread (32)
 constexpr int kThreads = 128 + 32 * kEpiWarps;
+constexpr int kRegsLaunch = (65536 / kThreads) / 8 * 8;  // what __launch_bounds__(kThreads, 1) gives
+constexpr int kRegsCtl = 48;
+constexpr int kRegsEpi = ((kRegsLaunch * kThreads - kRegsCtl * 128) / (32 * kEpiWarps)) / 8 * 8;
+static_assert(kRegsCtl * 128 + kRegsEpi * 32 * kEpiWarps <= kRegsLaunch * kThreads, "setmaxnreg beyond the CTA pool");
+static_assert(kRegsCtl + kRegsEpi * (kEpiWarps / 4) <= 512, "setmaxnreg beyond an SM sub-partition");
 constexpr size_t kSmemBufs = size_t(kBufs) * kPair;
 
 __device__ unsigned long long g_oz_trace[4096];  // diagnostics (CCF_OZ_MODE bit 2): block 0 event times
@@ -358,6 +385,7 @@ __device__ __forceinline__ unsigned long long oz_now() {
 struct OzBars {
     uint64_t full[kBufs], empty[kBufs], accfull[kSlots], accempty[kSlots];
     uint64_t sbfull, sbempty;  // column scales of the current tile (one slot)
+    double red[2][16];         // per-warp tile maxima (panel outputs), double-buffered by item parity
     uint32_t tmem_base;
 };
 constexpr size_t kSbBytes = 128 * sizeof(double);
@@ -365,7 +393,8 @@ constexpr size_t kBarsBytes = (sizeof(OzBars) + 127) / 128 * 128;  // the column
 
 
 // Persistent: one CTA per SM walks 128 x 128 output tiles (items). Warpgroup 0: warp 0 producer,
-// warp 1 MMA issuer (registers released with setmaxnreg); warpgroups 1-2: epilogue (registers raised).
+// warp 1 MMA issuer (registers released with setmaxnreg); warpgroups 1-4: epilogue (registers raised;
+// 4 warps per TMEM lane quadrant, 32 columns each, for latency hiding on the FP64 pipe).
 // The six digit-slice pairs (A_d, B_d) of a term rotate through seven 32 KB buffers (buffer
 // (6 tau + d) mod 7 for term tau), so the next term's first slices load while the current term
 // finishes. The MMA thread issues level by level (level L = all pairs d + d' = L, 4 K-steps each,
@@ -407,7 +436,9 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
     const uint32_t tmem = bar.tmem_base;
 
     if (warp < 4) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+        // register budget: the CTA pool is what the launch allocated (kThreads x kRegsLaunch); warpgroup 0
+        // gives back to kRegsCtl, the epilogue warpgroups take kRegsEpi (an inc beyond the pool never returns)
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
         if (warp == 0) {  // ---------------- producer
             // items are sorted by descending term count: the term-less ones (zero outputs) come last
             if (lane == 0 && int(blockIdx.x) < nitems && items[blockIdx.x].t1 > items[blockIdx.x].t0) {
@@ -499,12 +530,12 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
             }
             __syncwarp();
         }
-    } else {  // ---------------- epilogue: warpgroups 1-2; TMEM lane quadrant warp % 4, 64-column half
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
-        const int q = warp & 3, half = (warp - 4) >> 2;
+    } else {  // ---------------- epilogue: warpgroups 1-4; TMEM lane quadrant warp % 4, 32-column part
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));
+        const int q = warp & 3, half = (warp - 4) >> 2;  // half: column part 0..3
         const int row = q * 32 + lane;
-        const uint32_t tq = tmem + (uint32_t(q * 32) << 16) + uint32_t(half * 64);
-        uint32_t g = 0, sbc = 0;
+        const uint32_t tq = tmem + (uint32_t(q * 32) << 16) + uint32_t(half * kCols);
+        uint32_t g = 0, sbc = 0, ipar = 0;
         OzItem In = int(blockIdx.x) < nitems ? items[blockIdx.x] : OzItem{};
         // the next term's descriptor and row factor are loaded one term ahead (dependent global loads)
         const OzTerm* Tp = (int(blockIdx.x) < nitems && In.t1 > In.t0) ? terms + In.t0 : nullptr;
@@ -514,9 +545,9 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
             const OzItem I = In;
             if (it + int(gridDim.x) < nitems) In = items[it + gridDim.x];
             const double* sbc_item = sbnext;  // column scales of this tile (its first term's B)
-            double acc[64];
+            double acc[kCols];
 #pragma unroll
-            for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+            for (int j = 0; j < kCols; ++j) acc[j] = 0.0;
             for (int t = I.t0; t < I.t1; ++t) {
                 const double sa = fnext;  // row scale x the B plane's tile normalisation (transposed splits)
                 {  // prefetch: the next term of this item, else the next item's first
@@ -533,17 +564,17 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                 for (int L = 0; L < kLevels; ++L, ++g) {
                     const uint32_t slot = g % kSlots;
                     mbar_wait(&bar.accfull[slot], (g / kSlots) & 1);
-                    if (warp == 4 && lane == 0) OZ_TRACE(3072 + g);
+                    if (warp == 4 && lane == 0) OZ_TRACE(3072 + g);  // (diagnostics: CCF_OZ_MODE bit 2)
                     tc_after();
                     if (!(mode & 1)) {
-                        uint32_t v[64];
+                        uint32_t v[kCols];
 #pragma unroll
-                        for (int c = 0; c < 4; ++c)
+                        for (int c = 0; c < kCols / 16; ++c)
                             tmem_ld16(tq + slot * 128 + uint32_t(c * 16), *reinterpret_cast<uint32_t(*)[16]>(v + 16 * c));
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                         const double f = sa * ldexp(1.0, -14 - 8 * L);  // row scale x level weight (powers of 2)
 #pragma unroll
-                        for (int j = 0; j < 64; ++j) {
+                        for (int j = 0; j < kCols; ++j) {
                             const int p = int(v[j]);
                             // int32 -> fp64 exactly: 1.5 2^52 + p as a bit pattern, minus 1.5 2^52
                             const double x = __hiloint2double(0x43380000 + (p >> 31), p) - 6755399441055744.0;
@@ -558,9 +589,9 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
             if (warp == 4 && lane == 0) OZ_TRACE(3584 + (it - blockIdx.x) / gridDim.x);
             if (I.t1 > I.t0 && sbc_item) {  // column scales (copied to shared memory by the producer)
                 mbar_wait(&bar.sbfull, sbc & 1);
-                const double2* sbp = reinterpret_cast<const double2*>((mode & 16) ? sbc_item + I.n0 + half * 64 : sbs + half * 64);
+                const double2* sbp = reinterpret_cast<const double2*>((mode & 16) ? sbc_item + I.n0 + half * kCols : sbs + half * kCols);
 #pragma unroll
-                for (int j = 0; j < 64; j += 2) {
+                for (int j = 0; j < kCols; j += 2) {
                     const double2 sb = sbp[j / 2];
                     acc[j] *= I.alpha * sb.x;
                     acc[j + 1] *= I.alpha * sb.y;
@@ -571,18 +602,54 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                 ++sbc;
             }
             if (warp == 4 && lane == 0) OZ_TRACE(3712 + (it - blockIdx.x) / gridDim.x);
-            if (row < I.m && !(mode & 8)) {
-                double* crow = I.c + long(row) * I.ldc + half * 64;
-                const int nv = I.n - half * 64;
-                if (nv >= 64 && ((reinterpret_cast<uintptr_t>(crow) & 31) == 0)) {
+            if (I.pdst) {  // the tile as the next product's MN-major B panel tile: digits relative to the tile max
+                double mx = 0.0;
 #pragma unroll
-                    for (int j = 0; j < 64; j += 4)
+                for (int j = 0; j < kCols; ++j)
+                    if (row < I.m && half * kCols + j < I.n) mx = fmax(mx, fabs(acc[j]));
+#pragma unroll
+                for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                if (lane == 0) bar.red[ipar][warp - 4] = mx;
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");  // the epilogue warps only
+#pragma unroll
+                for (int w = 0; w < kEpiWarps; ++w) mx = fmax(mx, bar.red[ipar][w]);
+                ipar ^= 1;
+                const int e = mx > 0.0 ? oz_exponent(mx) : 0;
+                const double scale = (mx > 0.0 && row < I.m) ? ldexp(1.0, 47 - e) : 0.0;  // rows >= m: zero digits
+#pragma unroll
+                for (int c4 = 0; c4 < kCols / 16; ++c4) {
+                    uint32_t w[kOzS][4];
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        double xv[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int j = c4 * 16 + q4 * 4 + u;
+                            xv[u] = half * kCols + j < I.n ? acc[j] : 0.0;
+                        }
+                        uint32_t wq[kOzS];
+                        oz_pack4(xv, scale, wq);
+#pragma unroll
+                        for (int d = 0; d < kOzS; ++d) w[d][q4] = wq[d];
+                    }
+                    const uint32_t off = oz_swz(row, half * kCols + c4 * 16);
+#pragma unroll
+                    for (int d = 0; d < kOzS; ++d)
+                        *reinterpret_cast<uint4*>(I.pdst + size_t(d) * I.pstride + off) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
+                }
+                if (threadIdx.x == 128 && I.ppe) *I.ppe = e;
+            } else if (row < I.m && !(mode & 8)) {
+                double* crow = I.c + long(row) * I.ldc + half * kCols;
+                const int nv = I.n - half * kCols;
+                if (nv >= kCols && ((reinterpret_cast<uintptr_t>(crow) & 31) == 0)) {
+#pragma unroll
+                    for (int j = 0; j < kCols; j += 4)
                         asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(crow + j), "d"(acc[j]), "d"(acc[j + 1]),
                                      "d"(acc[j + 2]), "d"(acc[j + 3])
                                      : "memory");
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 64; ++j)
+                    for (int j = 0; j < kCols; ++j)
                         if (j < nv) crow[j] = acc[j];
                 }
             }

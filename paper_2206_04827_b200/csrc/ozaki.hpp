@@ -49,6 +49,11 @@ struct OzItem {         // one 128 x 128 output tile; every term of an item has 
     double* c;          // tile origin in the output (row-major, ldc)
     long ldc;
     double alpha;       // (ignored when the terms carry no column scales: alpha = 1)
+    // optional: write the tile (rows = K of the next product, columns = its output columns) as that
+    // product's MN-major B panel tile instead of fp64: slice d at pdst + d * pstride, tile exponent -> *ppe
+    uint8_t* pdst = nullptr;
+    long pstride = 0;
+    int* ppe = nullptr;
 };
 
 // Split jobs: fp64 source -> panel slices + row scales.

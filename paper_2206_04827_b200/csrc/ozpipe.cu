@@ -38,6 +38,7 @@ std::string key_of(const char* tag, std::initializer_list<const void*> ptrs) {
     return k;
 }
 constexpr size_t kPanel128 = size_t(kOzS) * 128 * kOzK;  // bytes of a 128-row panel
+constexpr size_t kPanel256 = 2 * kPanel128;               // a 256-row panel (two column tiles)
 }  // namespace
 
 OzPipe::OzPipe(Pipeline& p) : P(p) {
@@ -50,6 +51,19 @@ OzPipe::OzPipe(Pipeline& p) : P(p) {
     mask = m ? std::atoi(m) : 7;
 }
 OzPipe::~OzPipe() = default;
+
+// MN-major B panels (256 rows = two 128-column tiles per (slot, plane)) standing for an fp64 tensor
+// of the pipeline: written by the producing product's epilogue, read by the next product
+OzPipe::Panels& OzPipe::panels(const double* buf) {
+    Panels& p = panels_[buf];
+    const int ns = P.c.sh.s_hi - P.c.sh.s_lo;
+    const size_t bytes_needed = size_t(ns) * 2 * kPanel256;
+    if (p.pan.n * 8 < bytes_needed) {
+        alloc_bytes(p.pan, bytes_needed);
+        p.pe.alloc(size_t(ns) * 2);  // [slot][plane][2 tiles] ints
+    }
+    return p;
+}
 
 OzPipe::Stage* OzPipe::stage(const std::string& key, bool& fresh) {
     auto& s = stages_[key];
@@ -110,7 +124,11 @@ bool OzPipe::ensure_const() {
 
 // ---- H: Y_S[t] = Z_t QS[k0] into value half k0, Y_D[t] = Z_t QD[k0] into half 1 - k0 (Pipeline::eigen_ysynth)
 bool OzPipe::ysynth(int ntensor, const double* const* z, double* const* outS, double* const* outD) {
-    if (!on || !(mask & 1) || !ensure_const()) return false;
+    for (int t = 0; t < ntensor; ++t) {  // a DMMA fallback writes fp64 tensors
+        if (outS[t]) panel_only_.erase(outS[t]);
+        if (outD[t]) panel_only_.erase(outD[t]);
+    }
+    if (!on || !(mask & 1) || !(mask & 2) || !ensure_const()) return false;
     const Geo& g = P.c.gh;
     const int M = P.c.M, N = P.c.N, nh = g.nh;
     const int s_lo = P.c.sh.s_lo, s_hi = P.c.sh.s_hi, ns = s_hi - s_lo;
@@ -159,7 +177,15 @@ bool OzPipe::ysynth(int ntensor, const double* const* z, double* const* outS, do
                             gp->gemm.terms.push_back({bytes(ysp_) + i * kPanel128, bytes(cpan_) + size_t(cp) * kPanel128,
                                                       ysc_.p + i * 128, csc_.p + size_t(cp) * 128, long(oz_slice_bytes(128)),
                                                       ints(cpe_) + cp});
-                            gp->gemm.items.push_back({t0, t0 + 1, 0, M, nh, out + off + long(dd ? 1 - k0 : k0) * nh, long(g.n), 1.0});
+                            OzItem item{t0, t0 + 1, 0, M, nh, out + off + long(dd ? 1 - k0 : k0) * nh, long(g.n), 1.0};
+                            // the value half of this tile as the X1 product's B panel tile (no fp64 tensor)
+                            Panels& pp = panels(out);
+                            const size_t pi = size_t(s - s_lo) * 2 + pl;
+                            const int h = dd ? 1 - k0 : k0;
+                            item.pdst = bytes(pp.pan) + pi * kPanel256 + size_t(h) * 128 * kOzK;
+                            item.pstride = long(oz_slice_bytes(256));
+                            item.ppe = ints(pp.pe) + pi * 2 + h;
+                            gp->gemm.items.push_back(item);
                         }
                     }
         gp->gemm.upload();
@@ -168,41 +194,30 @@ bool OzPipe::ysynth(int ntensor, const double* const* z, double* const* outS, do
     gp->gemm.launch(P.c.stream);
     P.c.gemm_flops += gp->gemm.flops;
     P.c.launches += 2;
+    for (int t = 0; t < ntensor; ++t) {  // these tensors now exist as panels only (rsynth reads them)
+        if (outS[t]) panel_only_.insert(outS[t]);
+        if (outD[t]) panel_only_.insert(outD[t]);
+    }
     return true;
 }
 
 // ---- X1: val[3 pr + o/2] plane o%2 = sum_terms (C_t QL)(Y[pr][in]) (composite synthesis, eigen rows)
 bool OzPipe::rsynth(double* const (&Z)[2][3], double* const* val) {
-    if (!on || !(mask & 2) || !ensure_const()) return false;
+    bool all_panels = true;
+    for (int pr = 0; pr < 2; ++pr)
+        for (int x = 0; x < 3; ++x) all_panels &= panel_only_.count(Z[pr][x]) > 0;
+    if (!on || !(mask & 2) || !ensure_const()) {
+        if (all_panels) throw Error(INTERNAL, "OzPipe: the X1 inputs exist as INT8 panels only");
+        return false;
+    }
+    if (!all_panels) return false;  // (fp64 inputs: the DMMA plan)
     const Geo& g = P.c.gh;
-    const int M = P.c.M, mh = g.mh;
-    const int s_lo = P.c.sh.s_lo, s_hi = P.c.sh.s_hi, ns = s_hi - s_lo;
+    const int mh = g.mh;
+    const int s_lo = P.c.sh.s_lo, s_hi = P.c.sh.s_hi;
     bool fresh;
     Stage* sp = stage(key_of("rs", {Z[0][0], Z[0][1], Z[0][2], Z[1][0], Z[1][1], Z[1][2], val[0], val[3]}), fresh);
-    if (!sp) return false;
-    const size_t pb = size_t(kOzS) * 256 * kOzK;  // a 256-row (z column) panel
+    if (!sp) throw Error(INTERNAL, "OzPipe: X1 plan first built during a graph capture");
     if (fresh) {
-        const size_t need = size_t(2) * ns * 6 * pb;
-        if (rsp_.n * 8 < need) {
-            alloc_bytes(rsp_, need);
-            rsc_.alloc(size_t(2) * ns * 256);
-            rpe_.alloc(size_t(2) * ns * 6);  // [pr][slot][6 planes][2 tiles] ints
-        }
-        sp->split.mn = true;
-        sp->gemm.b_mn = true;
-        auto pan = [&](int pr, int s, int in) { return bytes(rsp_) + ((size_t(pr) * ns + (s - s_lo)) * 6 + in) * pb; };
-        for (int pr = 0; pr < 2; ++pr)
-            for (int s = s_lo; s < s_hi; ++s) {
-                // the six input planes of (pr, s) share column scales; K = the M eigen rows written by H
-                OzSplitJob j = oz_job(nullptr, g.n, g.n, M, nullptr, rsc_.p + (size_t(pr) * ns + (s - s_lo)) * 256,
-                                      long(oz_slice_bytes(256)), 256, ints(rpe_) + (size_t(pr) * ns + (s - s_lo)) * 12);
-                j.nsrc = 6;
-                for (int in = 0; in < 6; ++in) {
-                    j.src[in] = Z[pr][in / 2] + long(s) * g.slot_stride + long(in % 2) * g.plane_stride;
-                    j.dst[in] = pan(pr, s, in);
-                }
-                sp->split.jobs.push_back(j);
-            }
         for (int pr = 0; pr < 2; ++pr)
             for (int s = s_lo; s < s_hi; ++s)
                 for (int o = 0; o < 6; ++o)
@@ -211,23 +226,23 @@ bool OzPipe::rsynth(double* const (&Z)[2][3], double* const* val) {
                         for (const CompositeTerm& ct : P.synth_.terms[size_t(s)]) {
                             if (ct.out != o) continue;
                             const size_t bi = size_t(syn0_) + size_t(ct.off) / size_t(mh * mh);
-                            sp->gemm.terms.push_back({bytes(cpan_) + bi * kPanel128, pan(pr, s, ct.in), csc_.p + bi * 128,
-                                                      nullptr, long(oz_slice_bytes(256)),
-                                                      ints(rpe_) + (size_t(pr) * ns + (s - s_lo)) * 12 + ct.in * 2});
+                            Panels& pp = panels(Z[pr][ct.in / 2]);
+                            const size_t pi = size_t(s - s_lo) * 2 + ct.in % 2;
+                            sp->gemm.terms.push_back({bytes(cpan_) + bi * kPanel128, bytes(pp.pan) + pi * kPanel256,
+                                                      csc_.p + bi * 128, nullptr, long(oz_slice_bytes(256)), ints(pp.pe) + pi * 2});
                         }
-                        const int t1 = int(sp->gemm.terms.size());
                         // (an output no block feeds is an item without terms: the kernel stores zeros)
+                        const int t1 = int(sp->gemm.terms.size());
                         sp->gemm.items.push_back({t0, t1, nt * 128, mh, 128,
                                                   val[3 * pr + o / 2] + long(s) * g.slot_stride + long(o % 2) * g.plane_stride + nt * 128,
                                                   long(g.n), 1.0});
                     }
-        sp->split.upload();
+        sp->gemm.b_mn = true;
         sp->gemm.upload();
     }
-    sp->split.launch(P.c.stream);
     sp->gemm.launch(P.c.stream);
     P.c.gemm_flops += sp->gemm.flops;
-    P.c.launches += 2;
+    P.c.launches += 1;
     return true;
 }
 
@@ -239,6 +254,13 @@ bool OzPipe::analyze(double* const* av, double* const* Y, double* lam_n, double*
     const int Np = P.c.N + (P.c.N & 1);
     const int s_lo = P.c.sh.s_lo, s_hi = P.c.sh.s_hi, ns = s_hi - s_lo;
     bool fresh;
+    // C: B = the Y planes (rows = r rows jr = K, columns k0 Np + j) as MN-major panels, written by X3's epilogue
+    const size_t pb = kPanel256;
+    auto rpan = [&](int s, int in) { return bytes(rap_) + (size_t(s - s_lo) * 10 + in) * pb; };
+    if (rap_.n * 8 < size_t(ns) * 10 * pb) {
+        alloc_bytes(rap_, size_t(ns) * 10 * pb);
+        rape_.alloc(size_t(ns) * 10);  // [slot][10 planes][2 tiles] ints
+    }
     // X3: A = av rows (slot, plane, r row) x one z half; B = AzP / ADzP [po]
     Stage* za = stage(key_of("za", {av[0], av[1], av[2], Y[0], Y[4]}), fresh);
     if (!za) return false;
@@ -268,37 +290,16 @@ bool OzPipe::analyze(double* const* av, double* const* Y, double* lam_n, double*
                         const int t0 = int(za->gemm.terms.size());
                         za->gemm.terms.push_back({bytes(zap_) + i * kPanel128, bytes(cpan_) + size_t(cp) * kPanel128, zasc_.p + i * 128,
                                                   csc_.p + size_t(cp) * 128, long(oz_slice_bytes(128)), ints(cpe_) + cp});
-                        za->gemm.items.push_back({t0, t0 + 1, 0, mh, Np,
-                                                  Y[x] + long(s) * g.slot_stride + long(pl) * mh * 2 * Np + long(po) * Np,
-                                                  long(2 * Np), 1.0});
+                        OzItem item{t0, t0 + 1, 0, mh, Np, Y[x] + long(s) * g.slot_stride + long(pl) * mh * 2 * Np + long(po) * Np,
+                                    long(2 * Np), 1.0};
+                        // ra's B plane in = 2 x + pl, column tile po (no fp64 Y tensor)
+                        item.pdst = rpan(s, 2 * x + pl) + size_t(po) * 128 * kOzK;
+                        item.pstride = long(oz_slice_bytes(256));
+                        item.ppe = ints(rape_) + size_t(s - s_lo) * 20 + (2 * x + pl) * 2 + po;
+                        za->gemm.items.push_back(item);
                     }
         za->split.upload();
         za->gemm.upload();
-    }
-    // C: B = Y planes (rows = r rows jr = K, columns k0 Np + j); the ten planes of a slot share column scales
-    Stage* ys = stage(key_of("ra_split", {Y[0], Y[1], Y[2], Y[3], Y[4]}), fresh);
-    if (!ys) return false;
-    const size_t pb = size_t(kOzS) * 256 * kOzK;
-    auto rpan = [&](int s, int in) { return bytes(rap_) + (size_t(s - s_lo) * 10 + in) * pb; };
-    if (fresh) {
-        const size_t need = size_t(ns) * 10 * pb;
-        if (rap_.n * 8 < need) {
-            alloc_bytes(rap_, need);
-            rasc_.alloc(size_t(ns) * 256);
-            rape_.alloc(size_t(ns) * 10);  // [slot][10 planes][2 tiles] ints
-        }
-        ys->split.mn = true;
-        for (int s = s_lo; s < s_hi; ++s) {
-            OzSplitJob j = oz_job(nullptr, 2 * Np, 2 * Np, mh, nullptr, rasc_.p + size_t(s - s_lo) * 256, long(oz_slice_bytes(256)), 256,
-                                  ints(rape_) + size_t(s - s_lo) * 20);
-            j.nsrc = 10;
-            for (int in = 0; in < 10; ++in) {
-                j.src[in] = Y[in / 2] + long(s) * g.slot_stride + long(in % 2) * mh * 2 * Np;
-                j.dst[in] = rpan(s, in);
-            }
-            ys->split.jobs.push_back(j);
-        }
-        ys->split.upload();
     }
     Stage* ra = stage(key_of("ra_gemm", {Y[0], lam_n, gam_n}), fresh);
     if (!ra) return false;
@@ -325,10 +326,9 @@ bool OzPipe::analyze(double* const* av, double* const* Y, double* lam_n, double*
     za->gemm.launch(P.c.stream);
     P.c.gemm_flops += za->gemm.flops;
     P.c.mark("X3_rz_analysis");
-    ys->split.launch(P.c.stream);
     ra->gemm.launch(P.c.stream);
     P.c.gemm_flops += ra->gemm.flops;
-    P.c.launches += 4;
+    P.c.launches += 3;
     return true;
 }
 

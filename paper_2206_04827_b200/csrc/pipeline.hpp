@@ -16,6 +16,7 @@
 
 #include <map>
 #include <memory>
+#include <set>
 #include <string>
 
 #include "composite.hpp"
@@ -185,6 +186,12 @@ struct OzPipe {
 
 private:
     struct Stage;
+    struct Panels {
+        DBuf pan, pe;
+    };
+    std::map<const double*, Panels> panels_;  // INT8 panels standing for pipeline tensors
+    std::set<const double*> panel_only_;      // tensors whose current value exists as panels only
+    Panels& panels(const double* buf);
     std::map<std::string, std::unique_ptr<Stage>> stages_;
     Stage* stage(const std::string& key, bool& fresh);
     bool ensure_const();

@@ -1,6 +1,7 @@
 // FP64 GEMMs on the INT8 tensor cores (tcgen05.mma kind::i8 + TMEM), see ozaki.hpp.
 #include <algorithm>
 #include <climits>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -365,7 +366,7 @@ constexpr int kEpiWarps = 16;            // warpgroups 1-4: 4 per TMEM lane quad
 constexpr int kCols = 128 * 4 / kEpiWarps;  // output columns per epilogue thread (32)
 constexpr int kThreads = 128 + 32 * kEpiWarps;
 constexpr int kRegsLaunch = (65536 / kThreads) / 8 * 8;  // what __launch_bounds__(kThreads, 1) gives
-constexpr int kRegsCtl = 48;
+constexpr int kRegsCtl = 56;
 constexpr int kRegsEpi = ((kRegsLaunch * kThreads - kRegsCtl * 128) / (32 * kEpiWarps)) / 8 * 8;
 static_assert(kRegsCtl * 128 + kRegsEpi * 32 * kEpiWarps <= kRegsLaunch * kThreads, "setmaxnreg beyond the CTA pool");
 static_assert(kRegsCtl + kRegsEpi * (kEpiWarps / 4) <= 512, "setmaxnreg beyond an SM sub-partition");
@@ -382,9 +383,39 @@ __device__ __forceinline__ unsigned long long oz_now() {
         if ((mode & 4) && blockIdx.x == 0 && (idx) < 4096) g_oz_trace[(idx)] = oz_now(); \
     } while (0)
 
+// low word of a K-major / MN-major 128-byte-swizzle descriptor (start address >> 4, LBO 16 B); the high
+// word (SBO 1024 B, sm_100 version 1, layout 2) is the same for every operand slice
+__device__ __forceinline__ uint32_t sdesc_lo(uint32_t saddr) { return ((saddr >> 4) & 0x3FFFu) | (1u << 16); }
+constexpr uint32_t kDescHi = (1024u >> 4) | (1u << 14) | (2u << 29);
+__device__ __forceinline__ void mma_i8_lo(uint32_t tmem_d, uint32_t alo, uint32_t blo, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .b64 ad, bd;\n.reg .pred p;\n"
+        "mov.b64 ad, {%1, %5};\nmov.b64 bd, {%2, %5};\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], ad, bd, %3, p;\n}\n" ::"r"(tmem_d),
+        "r"(alo), "r"(blo), "r"(idesc), "r"(acc), "n"(kDescHi));
+}
+// the products of level L: pairs (d, L - d), 4 K-steps each, straight-line (descriptors precomputed per term)
+template <int L>
+__device__ __forceinline__ void oz_issue_level(uint32_t acc, const uint32_t (&alo)[kOzS], const uint32_t (&blo)[kOzS], int bmn) {
+    constexpr int d0 = L > kOzS - 1 ? L - (kOzS - 1) : 0, d1 = L < kOzS - 1 ? L : kOzS - 1;
+    const uint32_t bstep = bmn ? 256u : 2u;  // 32 k-rows (MN-major) or 32 bytes, >> 4
+    const uint32_t mnbit = bmn ? (1u << 16) : 0u;
+#pragma unroll
+    for (int d = d0; d <= d1; ++d) {
+        const uint32_t id = oz_idesc(d == 0, L - d == 0) | mnbit;
+#pragma unroll
+        for (int k = 0; k < kOzK / 32; ++k)
+            mma_i8_lo(acc, alo[d] + 2 * k, blo[L - d] + bstep * k, id, (d == d0 && k == 0) ? 0u : 1u);
+    }
+}
+
+// ring position of digit pair d within a term (load / release order 5, 4, 3, 2, 1, 0) and its inverse
+__device__ __forceinline__ int oz_pos_of(int d) { return d == 0 ? kOzS - 1 : kOzS - 1 - d; }
+__device__ __forceinline__ int oz_digit_at(int i) { return i == kOzS - 1 ? 0 : kOzS - 1 - i; }
+
 struct OzBars {
     uint64_t full[kBufs], empty[kBufs], accfull[kSlots], accempty[kSlots];
-    uint64_t sbfull, sbempty;  // column scales of the current tile (one slot)
+    uint64_t sbfull[2], sbempty[2];  // column scales of the tiles in flight (two slots)
     double red[2][16];         // per-warp tile maxima (panel outputs), double-buffered by item parity
     uint32_t tmem_base;
 };
@@ -394,22 +425,26 @@ constexpr size_t kBarsBytes = (sizeof(OzBars) + 127) / 128 * 128;  // the column
 
 // Persistent: one CTA per SM walks 128 x 128 output tiles (items). Warpgroup 0: warp 0 producer,
 // warp 1 MMA issuer (registers released with setmaxnreg); warpgroups 1-4: epilogue (registers raised;
-// 4 warps per TMEM lane quadrant, 32 columns each, for latency hiding on the FP64 pipe).
-// The six digit-slice pairs (A_d, B_d) of a term rotate through seven 32 KB buffers (buffer
-// (6 tau + d) mod 7 for term tau), so the next term's first slices load while the current term
-// finishes. The MMA thread issues level by level (level L = all pairs d + d' = L, 4 K-steps each,
-// M = N = 128) into a 4-slot TMEM ring; pair d is released after its last use (d = 0 after level 5,
-// the others after level 6). The 8 epilogue warps drain each level as it completes: each int32 is
-// converted exactly (1.5 2^52 bit trick) and accumulated with the row's weight 2^-(14 + 8L) x row
-// scale (two FP64 instructions per element and level); the column scales, shared by an item's terms,
-// multiply the tile once before its 256-bit stores. MMA, epilogue and copies of
-// neighbouring terms overlap. N = 128 per instruction keeps the tensor pipe at ~4 POPS (N = 64 costs
-// ~60 cycles per instruction, tools/microbench/i8mma.cu).
+// 4 warps per TMEM lane quadrant, 32 columns each). The six digit-slice pairs (A_d, B_d) of a term
+// stream through a ring of seven 32 KB buffers in the order d = 5, 4, 3, 2, 1, 0. The MMA thread issues
+// the levels in DESCENDING order (level L = all pairs d + d' = L, 4 K-steps each, M = N = 128) into a
+// 4-slot TMEM ring, so pair d is last used at level d: pairs leave the ring in the order they entered
+// and the next term's pairs 5..1 load while the current term runs its low levels (level 6 of a term
+// needs pairs 1..5, level 5 adds pair 0). The epilogue warps drain each level as it completes: each
+// int32 is converted exactly (1.5 2^52 bit trick) and accumulated with the row's weight 2^-(14 + 8L) x
+// row scale (two FP64 instructions per element and level); column scales, shared by an item's terms,
+// multiply the tile once; then the tile is stored as fp64 (256-bit stores) or, for a product feeding
+// another one, as that product's MN-major B panel tile (digits relative to the tile max, CTA-wide).
+// N = 128 per instruction keeps the tensor pipe at ~4 POPS (N = 64 costs ~60 cycles per instruction,
+// tools/microbench/i8mma.cu).
 __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __restrict__ terms,
                                                               const OzItem* __restrict__ items, int nitems, int mode,
                                                               int bmn) {
     extern __shared__ __align__(1024) uint8_t dsm[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+    // no room for alignment slack (7 x 32 KB + barriers + 2 KB of column scales fill the 227 KB): the
+    // dynamic window of a kernel without static shared memory starts 1024-byte aligned
+    if (su32(dsm) & 1023) __trap();
+    uint8_t* sm = dsm;
     OzBars& bar = *reinterpret_cast<OzBars*>(sm + kSmemBufs);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -421,11 +456,13 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
             mbar_init(&bar.accfull[i], 1);
             mbar_init(&bar.accempty[i], kEpiWarps);
         }
-        mbar_init(&bar.sbfull, 1);
-        mbar_init(&bar.sbempty, kEpiWarps);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bar.sbfull[i], 1);
+            mbar_init(&bar.sbempty[i], kEpiWarps);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    double* sbs = reinterpret_cast<double*>(sm + kSmemBufs + kBarsBytes);  // column-scale slot
+    double* sbs = reinterpret_cast<double*>(sm + kSmemBufs + kBarsBytes);  // column-scale slots [2][128]
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&bar.tmem_base)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -462,7 +499,8 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                     const bool more = itn < nitems;
                     const OzTerm Tn = more ? terms[tn] : T;
                     const uint8_t* bsrc = T.b + size_t(I.n0) * kOzK;
-                    for (int d = 0; d < kOzS; ++d, ++pc) {
+                    for (int i = 0; i < kOzS; ++i, ++pc) {  // digit pairs in release order 5, 4, 3, 2, 1, 0
+                        const int d = oz_digit_at(i);
                         const uint32_t b = pc % kBufs, use = pc / kBufs;
                         mbar_wait(&bar.empty[b], (use & 1) ^ 1);
                         OZ_TRACE(pc);
@@ -471,10 +509,12 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                         bulk_g2s(sm + size_t(b) * kPair + kSlice, bsrc + size_t(d) * T.bstride, kSlice, &bar.full[b]);
                     }
                     if (t == I.t0 && T.sb) {  // the tile's column scales (read by the epilogue after its last term)
-                        mbar_wait(&bar.sbempty, (sbc & 1) ^ 1);
+                        const uint32_t k = sbc & 1;
+                        mbar_wait(&bar.sbempty[k], ((sbc >> 1) & 1) ^ 1);
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // epilogue reads -> next bulk write
-                        mbar_expect(&bar.sbfull, uint32_t(kSbBytes));
-                        bulk_g2s(sbs, T.sb + I.n0, uint32_t(kSbBytes), &bar.sbfull);
+                        mbar_expect(&bar.sbfull[k], uint32_t(kSbBytes));
+                        bulk_g2s(sbs + k * 128, T.sb + I.n0, uint32_t(kSbBytes), &bar.sbfull[k]);
+                        OZ_TRACE(3968 + sbc);
                         ++sbc;
                     }
                     if (!more) break;
@@ -494,37 +534,43 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                     const OzItem I = In;
                     if (it + int(gridDim.x) < nitems) In = items[it + gridDim.x];  // one item ahead
                     for (int t = I.t0; t < I.t1; ++t, pc += kOzS) {
-                        for (int L = 0; L < kLevels; ++L, ++g) {
-                            if (L < kOzS) {  // pair L arrives (level L uses pairs d, d' <= L)
-                                const uint32_t q = pc + L;
-                                mbar_wait(&bar.full[q % kBufs], (q / kBufs) & 1);
-                            }
+                        // this term's ring buffers: position i (digit pair oz_digit_at(i)) in buffer (pc + i) mod 7
+                        const uint32_t p0 = pc % kBufs, u0 = pc / kBufs;
+                        uint32_t alo[kOzS], blo[kOzS], fb[kOzS], fph[kOzS];
+#pragma unroll
+                        for (int i = 0; i < kOzS; ++i) {
+                            const uint32_t b = p0 + i >= kBufs ? p0 + i - kBufs : p0 + i;
+                            const int d = oz_digit_at(i);
+                            alo[d] = sdesc_lo(s0 + b * kPair);
+                            blo[d] = sdesc_lo(s0 + b * kPair + kSlice);
+                            fb[i] = b;
+                            fph[i] = (u0 + (p0 + i >= kBufs ? 1 : 0)) & 1;
+                        }
+                        // levels 6 .. 0 (level 6 needs digit pairs 1..5 = ring positions 0..4, level 5 adds pair 0);
+                        // digit pair L is last used at level L: pairs leave the ring in load order
+                        auto level = [&](auto Lc) {
+                            constexpr int L = decltype(Lc)::value;
+                            if (L == kLevels - 1)
+                                for (int i = 0; i < kOzS - 1; ++i) mbar_wait(&bar.full[fb[i]], fph[i]);
+                            if (L == kLevels - 2) mbar_wait(&bar.full[fb[kOzS - 1]], fph[kOzS - 1]);
                             OZ_TRACE(1024 + g);
                             const uint32_t slot = g % kSlots;
                             mbar_wait(&bar.accempty[slot], ((g / kSlots) & 1) ^ 1);
                             OZ_TRACE(2048 + g);
                             tc_after();
-                            const uint32_t acc = tmem + slot * 128;
-                            if (!(mode & 2)) {
-                                bool first = true;
-                                for (int d = (L > kOzS - 1 ? L - (kOzS - 1) : 0); d <= L && d < kOzS; ++d) {
-                                    const int dp = L - d;
-                                    const uint64_t ad = sdesc(s0 + ((pc + d) % kBufs) * kPair);
-                                    const uint64_t bd = sdesc(s0 + ((pc + dp) % kBufs) * kPair + kSlice);
-                                    const uint32_t id = oz_idesc(d == 0, dp == 0) | (bmn ? (1u << 16) : 0u);
-                                    const uint32_t bstep = bmn ? 256u : 2u;  // 32 k-rows (MN-major) or 32 bytes, >> 4
-#pragma unroll
-                                    for (int k = 0; k < kOzK / 32; ++k) {
-                                        mma_i8(acc, ad + 2 * k, bd + bstep * k, id, first ? 0u : 1u);
-                                        first = false;
-                                    }
-                                }
-                            }
+                            if (!(mode & 2)) oz_issue_level<L>(tmem + slot * 128, alo, blo, bmn);
+                            if (g < 512) OZ_TRACE(2560 + g);
                             tc_commit(&bar.accfull[slot]);
-                            if (L == kOzS - 1) tc_commit(&bar.empty[pc % kBufs]);  // pair 0: last used at level 5
-                            if (L == kLevels - 1)
-                                for (int d = 1; d < kOzS; ++d) tc_commit(&bar.empty[(pc + d) % kBufs]);
-                        }
+                            if (L < kOzS) tc_commit(&bar.empty[fb[oz_pos_of(L)]]);
+                            ++g;
+                        };
+                        level(std::integral_constant<int, 6>{});
+                        level(std::integral_constant<int, 5>{});
+                        level(std::integral_constant<int, 4>{});
+                        level(std::integral_constant<int, 3>{});
+                        level(std::integral_constant<int, 2>{});
+                        level(std::integral_constant<int, 1>{});
+                        level(std::integral_constant<int, 0>{});
                     }
                 }
             }
@@ -561,44 +607,62 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                     }
                 }
 #pragma unroll 1
-                for (int L = 0; L < kLevels; ++L, ++g) {
-                    const uint32_t slot = g % kSlots;
-                    mbar_wait(&bar.accfull[slot], (g / kSlots) & 1);
+                // levels arrive 6 .. 0 and are drained in pairs (6, 5), (4, 3), (2, 1), (0): the two int32 levels
+                // combine exactly into y = P_(L-1) 2^8 + P_L (|y| < 2^34), converted with one 64-bit bit trick
+                // and accumulated with the weight 2^-(14 + 8L) x row scale: two FP64 instructions per element
+                // and level pair
+                auto drain = [&](int L, bool pair) {
+                    const uint32_t s0l = g % kSlots, s1l = (g + 1) % kSlots;
+                    mbar_wait(&bar.accfull[s0l], (g / kSlots) & 1);
+                    if (pair) mbar_wait(&bar.accfull[s1l], ((g + 1) / kSlots) & 1);
                     if (warp == 4 && lane == 0) OZ_TRACE(3072 + g);  // (diagnostics: CCF_OZ_MODE bit 2)
                     tc_after();
                     if (!(mode & 1)) {
-                        uint32_t v[kCols];
-#pragma unroll
-                        for (int c = 0; c < kCols / 16; ++c)
-                            tmem_ld16(tq + slot * 128 + uint32_t(c * 16), *reinterpret_cast<uint32_t(*)[16]>(v + 16 * c));
-                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                         const double f = sa * ldexp(1.0, -14 - 8 * L);  // row scale x level weight (powers of 2)
 #pragma unroll
-                        for (int j = 0; j < kCols; ++j) {
-                            const int p = int(v[j]);
-                            // int32 -> fp64 exactly: 1.5 2^52 + p as a bit pattern, minus 1.5 2^52
-                            const double x = __hiloint2double(0x43380000 + (p >> 31), p) - 6755399441055744.0;
-                            acc[j] = fma(x, f, acc[j]);
+                        for (int c = 0; c < kCols / 16; ++c) {
+                            uint32_t vl[16], vh[16];
+                            tmem_ld16(tq + s0l * 128 + uint32_t(c * 16), vl);
+                            if (pair) tmem_ld16(tq + s1l * 128 + uint32_t(c * 16), vh);
+                            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                const long long y = pair ? (long long)int(vh[j]) * 256 + int(vl[j]) : (long long)int(vl[j]);
+                                // int64 (|y| < 2^51) -> fp64 exactly: bits(1.5 2^52) + y, minus 1.5 2^52
+                                const double x = __hiloint2double(int(uint32_t(y >> 32) + 0x43380000u), int(uint32_t(y))) -
+                                                 6755399441055744.0;
+                                acc[c * 16 + j] = fma(x, f, acc[c * 16 + j]);
+                            }
                         }
                     }
                     tc_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&bar.accempty[slot]);
-                }
+                    if (lane == 0) {
+                        mbar_arrive(&bar.accempty[s0l]);
+                        if (pair) mbar_arrive(&bar.accempty[s1l]);
+                    }
+                    g += pair ? 2 : 1;
+                };
+                drain(6, true);
+                drain(4, true);
+                drain(2, true);
+                drain(0, false);
             }
             if (warp == 4 && lane == 0) OZ_TRACE(3584 + (it - blockIdx.x) / gridDim.x);
             if (I.t1 > I.t0 && sbc_item) {  // column scales (copied to shared memory by the producer)
-                mbar_wait(&bar.sbfull, sbc & 1);
-                const double2* sbp = reinterpret_cast<const double2*>((mode & 16) ? sbc_item + I.n0 + half * kCols : sbs + half * kCols);
+                const uint32_t k = sbc & 1;
+                mbar_wait(&bar.sbfull[k], (sbc >> 1) & 1);
+                if (warp == 4 && lane == 0) OZ_TRACE(4032 + sbc);
+                const double2* sbp = reinterpret_cast<const double2*>((mode & 16) ? sbc_item + I.n0 + half * kCols
+                                                                                  : sbs + k * 128 + half * kCols);
 #pragma unroll
                 for (int j = 0; j < kCols; j += 2) {
                     const double2 sb = sbp[j / 2];
                     acc[j] *= I.alpha * sb.x;
                     acc[j + 1] *= I.alpha * sb.y;
                 }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&bar.sbempty);
+                if (lane == 0) mbar_arrive(&bar.sbempty[k]);
                 ++sbc;
             }
             if (warp == 4 && lane == 0) OZ_TRACE(3712 + (it - blockIdx.x) / gridDim.x);
@@ -669,15 +733,17 @@ void oz_trace_dump() {  // diagnostics (CCF_OZ_MODE bit 2): block 0's event time
     cudaMemcpyFromSymbol(t.data(), g_oz_trace, 4096 * 8);
     const unsigned long long t0 = t[0];
     for (int i = 0; i < 48; ++i)
-        std::printf("level %2d: pair-issue %7lld  mma-start %7lld  mma-go %7lld  epi-got %7lld\n", i,
+        std::printf("level %2d: pair-issue %7lld  mma-start %7lld  mma-go %7lld  issued %7lld  epi-got %7lld\n", i,
                     i < 1024 && t[i] ? (long long)(t[i] - t0) : -1, t[1024 + i] ? (long long)(t[1024 + i] - t0) : -1,
-                    t[2048 + i] ? (long long)(t[2048 + i] - t0) : -1, t[3072 + i] ? (long long)(t[3072 + i] - t0) : -1);
+                    t[2048 + i] ? (long long)(t[2048 + i] - t0) : -1, t[2560 + i] ? (long long)(t[2560 + i] - t0) : -1,
+                    t[3072 + i] ? (long long)(t[3072 + i] - t0) : -1);
     for (int i = 0; i < 6; ++i)
-        std::printf("tile %d: drained %7lld  scaled %7lld  stored %7lld\n", i, (long long)(t[3584 + i] - t0),
+        std::printf("tile %d: drained %7lld  sb-copied %7lld  sb-got %7lld  scaled %7lld  stored %7lld\n", i,
+                    (long long)(t[3584 + i] - t0), (long long)(t[3968 + i] - t0), (long long)(t[4032 + i] - t0),
                     (long long)(t[3712 + i] - t0), (long long)(t[3840 + i] - t0));
 }
 
-size_t oz_smem_bytes() { return kSmemBufs + kBarsBytes + kSbBytes + 1024; }
+size_t oz_smem_bytes() { return kSmemBufs + kBarsBytes + 2 * kSbBytes; }
 
 void OzSplitPlan::upload() {
     maxrows = 0;

@@ -54,8 +54,10 @@ int main(int argc, char** argv) {
         const int bs = shared ? bt % nt : bt;
         // the terms of one batch share B column scales (one split job over the batch's nt B blocks)
         const int b0 = (bs / nt) * nt;
-        g.terms.push_back({reinterpret_cast<uint8_t*>(PA.p) + pa * bs, reinterpret_cast<uint8_t*>(PB.p) + pb * bs,
-                           SA.p + 128 * bs, SB.p + long(Np) * b0, long(oz_slice_bytes(Np)), pe + size_t(bs) * (Np / 128)});
+        // shared 2: only B is shared (A distinct per batch, like the back transforms / z analysis)
+        const int as = shared == 2 ? bt : bs;
+        g.terms.push_back({reinterpret_cast<uint8_t*>(PA.p) + pa * as, reinterpret_cast<uint8_t*>(PB.p) + pb * bs,
+                           SA.p + 128 * as, SB.p + long(Np) * b0, long(oz_slice_bytes(Np)), pe + size_t(bs) * (Np / 128)});
     }
     for (int b = 0; b < nb; ++b) {
         OzSplitJob j = oz_job(B.p + size_t(b) * nt * bsz, long(N), N, K, reinterpret_cast<uint8_t*>(PB.p) + pb * b * nt,

@@ -499,6 +499,89 @@ void lat(int nm, int grid) {
     cudaFree(d);
 }
 
+// MMA rate (N = 128, digit-major pattern, 3 accumulators at columns 0..383) while warps 4.. stream
+// tcgen05.ld over columns 384..511 (the epilogue's TMEM reads)
+__global__ void __launch_bounds__(384, 1) k_rate5(int R, int nld, int32_t* sink) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    __shared__ volatile int done;
+    uint8_t* sA = sm;
+    uint8_t* sB = sm + 6 * 16384;
+    for (int i = threadIdx.x; i < (12 * 16384) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = i * 2654435761u;
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tbase)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); done = 0; }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tm = tbase;
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        const uint32_t a0 = su32(sA), b0 = su32(sB);
+        for (int r = 0; r < R; ++r)
+            for (int d = 0; d < 6; ++d)
+                for (int dp = 0; dp <= (6 - d < 5 ? 6 - d : 5); ++dp)
+                    for (int k = 0; k < 4; ++k)
+                        mma_i8(tm + uint32_t(((d + dp) % 3) * 128), sdesc(a0 + d * 16384) + 2 * k, sdesc(b0 + dp * 16384) + 2 * k, idesc_i8(128, 1, 1), 1);
+        commit(&bar);
+        mbar_wait(&bar, 0);
+        done = 1;
+    } else if (warp >= 4 && nld == 2) {  // FP64 load: the epilogue's DADD + DFMA stream
+        double a0 = threadIdx.x, a1 = 1.0, a2 = 2.0, a3 = 3.0, x = 1.0 + 1e-9 * threadIdx.x;
+        while (!done) {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+                a0 = fma(a0, x, 1e-7); a1 = fma(a1, x, 2e-7); a2 = a2 + x; a3 = fma(a3, x, a2);
+            }
+        }
+        if (a0 + a1 + a2 + a3 == 1.2345) sink[0] = 1;
+    } else if (warp >= 4 && nld) {
+        const uint32_t tq = tm + (uint32_t((warp & 3) * 32) << 16) + 384;
+        uint32_t acc = 0;
+        while (!done) {
+            uint32_t v[16];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                         : "r"(tq + uint32_t((acc & 7) * 16)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+            for (int j = 0; j < 16; ++j) acc += v[j];
+        }
+        if (acc == 0x12345678u) sink[0] = int32_t(acc);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+void rate5(int nld) {
+    int nsm = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+    int32_t* sink;
+    CK(cudaMalloc(&sink, 4));
+    const int smem = 12 * 16384 + 1024;
+    CK(cudaFuncSetAttribute(k_rate5, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int R = 200;
+    k_rate5<<<nsm, 384, smem>>>(4, nld, sink);
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    k_rate5<<<nsm, 384, smem>>>(R, nld, sink);
+    cudaEventRecord(e1);
+    CK(cudaDeviceSynchronize());
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double nmma = double(R) * 26 * 4;
+    printf("rate5 N=128 with TMEM loads %d: %.0f clk/MMA\n", nld, ms * 1e-3 * 1.965e9 / nmma);
+    cudaFree(sink);
+}
+
 template <int N, int ORDER>
 void rate3(int sg = 0) {
     int nsm = 0;
@@ -830,6 +913,7 @@ int main() {
     rate3<64, 1>();
     rate3<128, 0>();
     lat(1, 1); lat(4, 1); lat(20, 1); lat(100, 1); lat(4, 148); lat(20, 148);
+    rate5(0); rate5(1); rate5(2);
     rate4<128>(0);
     rate4<128>(200);
     rate4<128>(1000);

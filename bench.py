@@ -61,7 +61,28 @@ def load_peaks():
     # (profiles/fp64_peak_r01.txt): DFMA 33.68 TFLOP/s, DMMA 37.11 TFLOP/s.
     peaks["fp64_dfma_tflops"] = 33.68
     peaks["fp64_dmma_tflops"] = 37.11
+    # dense INT8 tcgen05.mma (kind::i8, M = 128, N = 256, operands in shared memory) measured on this
+    # pool's B200 by tools/microbench/i8mma.cu (profiles/i8mma_r02.txt, rate2 N = 256): 4287 TOPS
+    # (nominal 4.5 POPS); MEASURED_PEAKS.json has no INT8 figure
+    peaks["int8_tops"] = 4287.0
     return peaks
+
+
+def gemm_traffic():
+    """DRAM bytes per step of the product launches (ncu launch list of one graph-replayed step,
+    profiles/launches_r02_step.csv) or None."""
+    try:
+        import csv
+        rows = [r for r in csv.reader(open(os.path.join(ROOT, "profiles", "launches_r02_step.csv"))) if len(r) > 10]
+        hdr = rows[0]
+        ki, mi, vi, ui = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+        tot = 0.0
+        for r in rows[1:]:
+            if "oz_gemm" in r[ki] and r[mi].startswith("dram__bytes"):
+                tot += float(r[vi].replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(r[ui], 1)
+        return tot or None
+    except Exception:
+        return None
 
 
 def initial_vorticity(ctx, cfg, vmax_target=1.0):
@@ -127,15 +148,6 @@ class ClockSampler:
             except Exception:
                 pass
         return out
-
-
-def gemm_traffic():
-    """DRAM bytes of the GEMM launches of one step from the committed ncu capture (or None)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "roofline_inputs_r01.json")) as f:
-            return float(json.load(f)["gemm_dram_bytes_per_step"])
-    except Exception:
-        return None
 
 
 def cpu_sample(cfg, threads):
@@ -443,10 +455,13 @@ def main():
     ctx.reset_stats()
     stages = st.profile_step()
     pstats = ctx.stats()
-    F_gemm = pstats["gemm_flops"]  # FP64 tensor-core flops of the step's batched GEMMs (2 M N K per term)
+    F_gemm = pstats["gemm_flops"]  # FP64-equivalent flops of the step's dense products (2 M N K per term)
     gemm_stages = ["P_poisson_solve", "X1_rz_synthesis", "X3_rz_analysis", "C_curl_decompose", "H_helmholtz_solve"]
-    t_gemm_ms = sum(stages.get(k, 0.0) for k in gemm_stages)  # these stages launch GEMMs only
+    t_gemm_ms = sum(stages.get(k, 0.0) for k in gemm_stages)  # these stages launch product kernels only
     gemm_tflops = F_gemm / (t_gemm_ms * 1e-3) / 1e12 if t_gemm_ms > 0 else None
+    # INT8 path (csrc/ozaki.cu): 26 digit-pair products per FP64 product, 2 int8 ops per MAC
+    ozaki = "H_z_split" in stages
+    int8_tops = 26.0 * F_gemm / (t_gemm_ms * 1e-3) / 1e12 if (ozaki and t_gemm_ms > 0) else None
     # step roofline: T_roof = F_gemm / P_dmma + (HBM-bound stages: theta 6 in + 3 out tensors, the
     # Helmholtz RHS pass 2 x (8 sources + 1 output) tensors + the next Poisson RHS + the two RT tables
     # (half a tensor each)) / BW; tensor = one half-spectrum field
@@ -455,12 +470,15 @@ def main():
     bw = peaks["hbm_gbs"] * 1e9
     pdm = peaks["fp64_dmma_tflops"] * 1e12
     B_other = (9 + 2 * (4 + 4 + 1) + 1 + 1) * tensor_bytes
+    # SURVEY 8d algorithmic bytes of one NS step (43 fields of 8N bytes at BDF4): the BASELINE metric's HBM fraction
+    B_alg = 43 * 8.0 * m * n * p
     nvl = 0.0
     if sharded:  # per-rank share of the HBM passes + the theta exchange over NVLink (900 GB/s per direction)
         from paper_2206_04827_b200 import shard as S
         B_other /= world
         nvl = S.exchange_bytes_per_rank(m, n, p, world) / 900e9
-    T_roof = F_gemm / pdm + B_other / bw + nvl
+    t_tensor = (26.0 * F_gemm / (peaks["int8_tops"] * 1e12)) if ozaki else F_gemm / pdm
+    T_roof = t_tensor + B_other / bw + nvl
     B_total = B_other
 
     # ---- end-to-end through the C-ABI with pinned host buffers: create (H2D) -> KE steps -> read back (D2H).
@@ -521,22 +539,39 @@ def main():
                             "guard, solver error words) -> omega() to pinned host (D2H); state bytes amortised "
                             "over KE"},
             "gpu_launches": stats["kernel_launches"],
-            "roofline": {"bound": "tensor",
-                         "kernel": "dgemm_tma_kernel (FP64 DMMA m8n8k4, TMA 128B-swizzled operand ring): z transforms, "
-                                   "composite radial operators and the eigen-coordinate back transforms",
-                         "achieved": gemm_tflops, "peak": peaks["fp64_dmma_tflops"], "unit": "TFLOP/s",
-                         "frac": (gemm_tflops / peaks["fp64_dmma_tflops"]) if gemm_tflops else None,
-                         "traffic": gemm_traffic(),
-                         "traffic_unit": "dram read + write bytes per step of the GEMM launches (ncu, committed)",
-                         "peak_source": "measured FP64 DMMA peak, tools/microbench/fp64_peak.cu "
-                                        "(profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json has no FP64 figure",
-                         "flops_per_step": F_gemm, "gemm_ms_per_step": t_gemm_ms,
-                         "flop_model": "2 M N K per product term of every batched GEMM launched in one step"},
+            "roofline": ({"bound": "tensor",
+                          "kernel": "oz_gemm_kernel: FP64 products as Ozaki INT8 digit products on tcgen05.mma kind::i8 "
+                                    "(TMEM accumulator ring, bulk-copied 128B-swizzled operands, exact int32->fp64 "
+                                    "epilogue): back transforms, composite radial operators, z analysis",
+                          "achieved": int8_tops, "peak": peaks["int8_tops"], "unit": "TOPS (int8)",
+                          "frac": (int8_tops / peaks["int8_tops"]) if int8_tops else None,
+                          "traffic": gemm_traffic(),
+                          "traffic_unit": "dram read + write bytes per step of the oz_gemm launches (ncu launch list, "
+                                          "profiles/launches_r02_step.csv)",
+                          "peak_source": "measured dense INT8 tcgen05 rate, tools/microbench/i8mma.cu (profiles/i8mma_r02.txt); "
+                                         "MEASURED_PEAKS.json has no INT8 figure",
+                          "fp64_equiv_tflops": gemm_tflops, "fp64_dmma_peak_tflops": peaks["fp64_dmma_tflops"],
+                          "fp64_equiv_vs_dmma_peak": (gemm_tflops / peaks["fp64_dmma_tflops"]) if gemm_tflops else None,
+                          "flops_per_step": F_gemm, "gemm_ms_per_step": t_gemm_ms,
+                          "flop_model": "int8 ops = 26 digit pairs x 2 M N K per FP64 product term (fp64-equivalent "
+                                        "flops = 2 M N K)"} if ozaki else
+                         {"bound": "tensor",
+                          "kernel": "dgemm_tma_kernel (FP64 DMMA m8n8k4, TMA 128B-swizzled operand ring)",
+                          "achieved": gemm_tflops, "peak": peaks["fp64_dmma_tflops"], "unit": "TFLOP/s",
+                          "frac": (gemm_tflops / peaks["fp64_dmma_tflops"]) if gemm_tflops else None,
+                          "traffic": None,
+                          "peak_source": "measured FP64 DMMA peak, tools/microbench/fp64_peak.cu (profiles/fp64_peak_r01.txt)",
+                          "flops_per_step": F_gemm, "gemm_ms_per_step": t_gemm_ms,
+                          "flop_model": "2 M N K per product term of every batched GEMM launched in one step"}),
             "step_roofline": {"T_roof_ms": T_roof * 1e3, "achieved": T_roof / (ms_step * 1e-3),
-                              "gemm_bound_ms": F_gemm / pdm * 1e3, "hbm_bound_ms": B_other / bw * 1e3,
+                              "tensor_bound_ms": t_tensor * 1e3, "hbm_bound_ms": B_other / bw * 1e3,
                               "nvlink_bound_ms": nvl * 1e3,
                               "hbm_peak_gbs": peaks["hbm_gbs"], "hbm_source": peaks["hbm_source"],
-                              "note": "GEMM stages at the DMMA peak + theta and RHS-combination passes at HBM peak"},
+                              "algorithmic_bytes_per_step": B_alg,
+                              "hbm_fraction_algorithmic": B_alg / (ms_step * 1e-3) / bw,
+                              "note": "product stages at the INT8 tensor peak (DMMA peak on the FP64 path) + theta and "
+                                      "RHS-combination passes at HBM peak; hbm_fraction_algorithmic = the BASELINE "
+                                      "metric (SURVEY 8d: 43 fields x 8 m n p bytes per step / step time / measured HBM BW)"},
             "stage_ms": stages,
             "sharding": ({"mode": "fourier slots x theta rows, NVLink peer exchange (CUDA IPC), " +
                                   f"{barrier_mode} barriers" +

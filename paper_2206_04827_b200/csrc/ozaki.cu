@@ -4,6 +4,7 @@
 #include <type_traits>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "context.hpp"
 #include "ozaki.hpp"
@@ -824,7 +825,9 @@ void OzGemmPlan::launch(cudaStream_t s) const {
         CCF_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(oz_smem_bytes())));
     }
     const unsigned grid = unsigned(std::min<size_t>(items.size(), size_t(nsm)));
-    static const int mode = std::getenv("CCF_OZ_MODE") ? std::atoi(std::getenv("CCF_OZ_MODE")) : 0;  // diagnostics
+    static const int mode0 = std::getenv("CCF_OZ_MODE") ? std::atoi(std::getenv("CCF_OZ_MODE")) : 0;  // diagnostics
+    static const char* trace_tag = std::getenv("CCF_OZ_TRACE");  // trace (mode bit 2) only the plan with this tag
+    const int mode = (trace_tag && tag && std::strcmp(trace_tag, tag) != 0) ? (mode0 & ~4) : mode0;
     oz_gemm_kernel<<<grid, kThreads, oz_smem_bytes(), s>>>(dterms, ditems, int(items.size()), mode, int(b_mn));
     CCF_CUDA(cudaGetLastError());
 }
@@ -835,3 +838,6 @@ OzGemmPlan::~OzGemmPlan() {
 }
 
 }  // namespace ccf
+
+// diagnostics entry point (not part of include/ccf.h): print block 0's trace of the last traced launch
+extern "C" void ccf_debug_oz_trace_dump() { ccf::oz_trace_dump(); }

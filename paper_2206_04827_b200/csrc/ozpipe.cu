@@ -188,9 +188,11 @@ bool OzPipe::ysynth(int ntensor, const double* const* z, double* const* outS, do
                             gp->gemm.items.push_back(item);
                         }
                     }
+        gp->gemm.tag = "H";
         gp->gemm.upload();
     }
     sp->split.launch(P.c.stream);
+    P.c.mark("H_z_split");
     gp->gemm.launch(P.c.stream);
     P.c.gemm_flops += gp->gemm.flops;
     P.c.launches += 2;
@@ -238,6 +240,7 @@ bool OzPipe::rsynth(double* const (&Z)[2][3], double* const* val) {
                                                   long(g.n), 1.0});
                     }
         sp->gemm.b_mn = true;
+        sp->gemm.tag = "X1";
         sp->gemm.upload();
     }
     sp->gemm.launch(P.c.stream);
@@ -299,6 +302,7 @@ bool OzPipe::analyze(double* const* av, double* const* Y, double* lam_n, double*
                         za->gemm.items.push_back(item);
                     }
         za->split.upload();
+        za->gemm.tag = "X3";
         za->gemm.upload();
     }
     Stage* ra = stage(key_of("ra_gemm", {Y[0], lam_n, gam_n}), fresh);
@@ -320,9 +324,11 @@ bool OzPipe::analyze(double* const* av, double* const* Y, double* lam_n, double*
                     ra->gemm.items.push_back({t0, t1, nt * 128, M, 128,
                                               (o < 2 ? gam_n : lam_n) + P.eig_off(s, o % 2, 0) + nt * 128, long(2 * Np), 1.0});
                 }
+        ra->gemm.tag = "C";
         ra->gemm.upload();
     }
     za->split.launch(P.c.stream);
+    P.c.mark("X3_av_split");
     za->gemm.launch(P.c.stream);
     P.c.gemm_flops += za->gemm.flops;
     P.c.mark("X3_rz_analysis");

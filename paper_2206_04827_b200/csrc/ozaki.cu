@@ -62,6 +62,22 @@ __device__ __forceinline__ void oz_pack4(const double (&x)[4], double scale, uin
     w[5] = __byte_perm(a, b, 0x5410);  // byte 0
 }
 
+// Exponent of a tile whose largest |value| has the high word hx: e with max|tile| < (hx + 1, 0) <= 2^e, so that
+// max|tile| 2^(47 - e) rounds below 2^47 (no clamp needed; the usual e of max|tile|, one more only when the
+// high-word mantissa is all ones)
+__device__ __forceinline__ int oz_tile_exponent(uint32_t hx) { return hx ? oz_exponent(__hiloint2double(int(hx + 1), 0)) : 0; }
+// Digit d (byte 5 - d of X) of four fixed-point values held as fma(x, 2^(47-e), 1.5 2^52) doubles, packed into one
+// word (value u in byte u): X bytes 0-3 are the low word, bytes 4-5 the low half of the high word
+__device__ __forceinline__ uint32_t oz_digit_word(const double* xb, int d) {
+    const int hiw = d < 2;
+    const uint32_t k = hiw ? uint32_t(1 - d) : uint32_t(5 - d);  // byte within the word
+    uint32_t w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) w[u] = uint32_t(hiw ? __double2hiint(xb[u]) : __double2loint(xb[u]));
+    const uint32_t sel = k | ((4u + k) << 4);
+    return __byte_perm(__byte_perm(w[0], w[1], sel), __byte_perm(w[2], w[3], sel), 0x5410);
+}
+
 // A-side split: one warp per panel row, lane l holds reduction indices 4l .. 4l + 3. A job with several sources
 // splits them with ONE scale per row (the max over the sources): the constant operator blocks that feed one output
 // of a composite product share their row scales, so that output's terms can be summed in one accumulator.
@@ -72,6 +88,28 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const OzSplitJob* __
     if (r >= J.rows_pad) return;
     const int nsrc = J.nsrc;
     double mx = 0.0;
+    const uint32_t off = oz_swz(r, 4 * lane);
+    if (nsrc == 1) {  // one pass: the row's values stay in registers
+        const double* src = J.src[0];
+        const int nrows = J.nrows, ncols = J.ncols;
+        const long ld = J.ld;
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int k = 4 * lane + u;
+            v[u] = (r < nrows && k < ncols) ? __ldg(src + long(r) * ld + k) : 0.0;
+            mx = fmax(mx, fabs(v[u]));
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const int e = mx > 0.0 ? oz_exponent(mx) : 0;
+        uint32_t w[kOzS];
+        oz_pack4(v, mx > 0.0 ? ldexp(1.0, 47 - e) : 0.0, w);
+#pragma unroll
+        for (int d = 0; d < kOzS; ++d) *reinterpret_cast<uint32_t*>(J.dst[0] + size_t(d) * J.stride + off) = w[d];
+        if (lane == 0) J.sc[r] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
+        return;
+    }
     for (int g = 0; g < nsrc; ++g)
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -81,7 +119,6 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const OzSplitJob* __
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const int e = mx > 0.0 ? oz_exponent(mx) : 0;
-    const uint32_t off = oz_swz(r, 4 * lane);
     for (int g = 0; g < nsrc; ++g) {
         double v[4];
 #pragma unroll
@@ -621,47 +658,55 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                         if (last) sbnext = Tn->sb;
                     }
                 }
-#pragma unroll 1
-                // levels arrive 6 .. 0 and are drained in pairs (6, 5), (4, 3), (2, 1), (0): the two int32 levels
-                // combine exactly into y = P_(L-1) 2^8 + P_L (|y| < 2^34), converted with one 64-bit bit trick
-                // and accumulated with the weight 2^-(14 + 8L) x row scale: two FP64 instructions per element
-                // and level pair
-                auto drain = [&](int L, bool pair) {
-                    const uint32_t s0l = g % kSlots, s1l = (g + 1) % kSlots;
-                    mbar_wait(&bar.accfull[s0l], (g / kSlots) & 1);
-                    if (pair) mbar_wait(&bar.accfull[s1l], ((g + 1) / kSlots) & 1);
+                // levels arrive 6 .. 0 and are drained three at a time, (6, 5, 4), (3, 2, 1), (0): the int32 levels
+                // combine exactly into y = P_(L-2) 2^16 + P_(L-1) 2^8 + P_L (|y| < 2^42), converted with one 64-bit
+                // bit trick and accumulated with the weight 2^-(14 + 8L) x row scale: two FP64 instructions per
+                // element and drain (6 per term)
+                auto drain = [&](int L, int nl) {
+                    const uint32_t sl0 = g % kSlots, sl1 = (g + 1) % kSlots, sl2 = (g + 2) % kSlots;
+                    mbar_wait(&bar.accfull[sl0], (g / kSlots) & 1);
+                    if (nl > 1) {
+                        mbar_wait(&bar.accfull[sl1], ((g + 1) / kSlots) & 1);
+                        mbar_wait(&bar.accfull[sl2], ((g + 2) / kSlots) & 1);
+                    }
                     if (warp == kCtlWarps && lane == 0) OZ_TRACE(3072 + g);  // (diagnostics: CCF_OZ_MODE bit 2)
                     tc_after();
                     if (!(mode & 1)) {
                         const double f = sa * ldexp(1.0, -14 - 8 * L);  // row scale x level weight (powers of 2)
 #pragma unroll
-                        for (int c = 0; c < kCols / 16; ++c) {
-                            uint32_t vl[16], vh[16];
-                            tmem_ld16(tq + s0l * 128 + uint32_t(c * 16), vl);
-                            if (pair) tmem_ld16(tq + s1l * 128 + uint32_t(c * 16), vh);
+                        for (int c = 0; c < kCols / 8; ++c) {
+                            uint32_t v0[8], v1[8], v2[8];
+                            tmem_ld8(tq + sl0 * 128 + uint32_t(c * 8), v0);  // level L
+                            if (nl > 1) {
+                                tmem_ld8(tq + sl1 * 128 + uint32_t(c * 8), v1);  // L - 1
+                                tmem_ld8(tq + sl2 * 128 + uint32_t(c * 8), v2);  // L - 2
+                            }
                             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                const long long y = pair ? (long long)int(vh[j]) * 256 + int(vl[j]) : (long long)int(vl[j]);
+                            for (int j = 0; j < 8; ++j) {
+                                const long long y = nl > 1 ? (long long)int(v2[j]) * 65536 + (long long)int(v1[j]) * 256 + int(v0[j])
+                                                           : (long long)int(v0[j]);
                                 // int64 (|y| < 2^51) -> fp64 exactly: bits(1.5 2^52) + y, minus 1.5 2^52
                                 const double x = __hiloint2double(int(uint32_t(y >> 32) + 0x43380000u), int(uint32_t(y))) -
                                                  6755399441055744.0;
-                                acc[c * 16 + j] = fma(x, f, acc[c * 16 + j]);
+                                acc[c * 8 + j] = fma(x, f, acc[c * 8 + j]);
                             }
                         }
                     }
                     tc_before();
                     __syncwarp();
                     if (lane == 0) {
-                        mbar_arrive(&bar.accempty[s0l]);
-                        if (pair) mbar_arrive(&bar.accempty[s1l]);
+                        mbar_arrive(&bar.accempty[sl0]);
+                        if (nl > 1) {
+                            mbar_arrive(&bar.accempty[sl1]);
+                            mbar_arrive(&bar.accempty[sl2]);
+                        }
                     }
-                    g += pair ? 2 : 1;
+                    g += nl;
                 };
-                drain(6, true);
-                drain(4, true);
-                drain(2, true);
-                drain(0, false);
+                drain(6, 3);
+                drain(3, 3);
+                drain(0, 1);
             }
             if (warp == kCtlWarps && lane == 0) OZ_TRACE(3584 + (it - blockIdx.x) / gridDim.x);
             if (I.t1 > I.t0 && sbc_item) {  // column scales (copied to shared memory by the producer)
@@ -674,8 +719,12 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                 for (int j = 0; j < kCols; j += 2) {
                     double sx, sy;
                     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(sx), "=d"(sy) : "r"(sba + 8u * j));
-                    acc[j] *= al * sx;
-                    acc[j + 1] *= al * sy;
+                    acc[j] *= sx;
+                    acc[j + 1] *= sy;
+                }
+                if (al != 1.0) {
+#pragma unroll
+                    for (int j = 0; j < kCols; ++j) acc[j] *= al;
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bar.sbempty[k]);
@@ -702,34 +751,24 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                     hx = max(max(hx, r4.x), max(r4.y, max(r4.z, r4.w)));
                 }
                 ipar ^= 1;
-                // mx = the largest double with that high word: max|tile| <= mx < 2^e with the same e
-                const double mx = __hiloint2double(int(hx), -1);
-                const int e = hx ? oz_exponent(mx) : 0;
+                const int e = oz_tile_exponent(hx);
                 const double scale = (hx && row < I.m) ? ldexp(1.0, 47 - e) : 0.0;  // rows >= m: zero digits
+                // in place: acc[j] -> the bits of fma(acc[j], 2^(47 - e), 1.5 2^52), whose low 48 bits are the
+                // two's-complement fixed-point value X (|X| < 2^47 by the choice of e); columns >= n: zero digits
+#pragma unroll
+                for (int j = 0; j < kCols; ++j) acc[j] = fma((full || half * kCols + j < I.n) ? acc[j] : 0.0, scale, 6755399441055744.0);
                 // per digit slice: this thread's 32 columns = one 32-byte sector of its 128-byte panel row
                 // (chunks 2i, 2i + 1 of the row swizzle land in one aligned sector), one 256-bit store each
-                uint32_t w[kOzS][8];
-#pragma unroll
-                for (int q8 = 0; q8 < 8; ++q8) {
-                    double xv[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int j = q8 * 4 + u;
-                        xv[u] = (full || half * kCols + j < I.n) ? acc[j] : 0.0;
-                    }
-                    uint32_t wq[kOzS];
-                    oz_pack4(xv, scale, wq);
-#pragma unroll
-                    for (int d = 0; d < kOzS; ++d) w[d][q8] = wq[d];
-                }
-                // chunk c = 2 half + c4 sits at 16-byte position c ^ (row & 7): swap the halves when bit 0 is set
                 const uint32_t off = oz_swz(row, half * kCols) & ~31u;
                 const bool swp = (row & 1) != 0;
                 if (!(mode & 32)) {
 #pragma unroll
                     for (int d = 0; d < kOzS; ++d) {
-                        const uint64_t a0 = uint64_t(w[d][0]) | (uint64_t(w[d][1]) << 32), a1 = uint64_t(w[d][2]) | (uint64_t(w[d][3]) << 32);
-                        const uint64_t b0 = uint64_t(w[d][4]) | (uint64_t(w[d][5]) << 32), b1 = uint64_t(w[d][6]) | (uint64_t(w[d][7]) << 32);
+                        uint32_t wd[8];
+#pragma unroll
+                        for (int q8 = 0; q8 < 8; ++q8) wd[q8] = oz_digit_word(acc + 4 * q8, d);
+                        const uint64_t a0 = uint64_t(wd[0]) | (uint64_t(wd[1]) << 32), a1 = uint64_t(wd[2]) | (uint64_t(wd[3]) << 32);
+                        const uint64_t b0 = uint64_t(wd[4]) | (uint64_t(wd[5]) << 32), b1 = uint64_t(wd[6]) | (uint64_t(wd[7]) << 32);
                         asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(I.pdst + size_t(d) * I.pstride + off),
                                      "l"(swp ? b0 : a0), "l"(swp ? b1 : a1), "l"(swp ? a0 : b0), "l"(swp ? a1 : b1)
                                      : "memory");

@@ -473,7 +473,10 @@ struct OzBars {
     uint32_t tmem_base;
 };
 constexpr size_t kSbBytes = 128 * sizeof(double);
-constexpr size_t kBarsBytes = (sizeof(OzBars) + 127) / 128 * 128;  // the column-scale slot is a bulk-copy target
+constexpr size_t kBarsBytes = (sizeof(OzBars) + 127) / 128 * 128;
+// item slots (two, bulk-copy targets): the OzItem (80 B) + a has-column-scales flag, then the 128 column scales
+constexpr size_t kItemSlot = 128 + kSbBytes;
+static_assert(sizeof(OzItem) + sizeof(int) <= 128 && sizeof(OzItem) % 16 == 0, "item slot");
 
 
 // Persistent: one CTA per SM walks 128 x 128 output tiles (items). Warpgroup 0: warp 0 producer,
@@ -515,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    double* sbs = reinterpret_cast<double*>(sm + kSmemBufs + kBarsBytes);  // column-scale slots [2][128]
+    uint8_t* islot = sm + kSmemBufs + kBarsBytes;  // item slots [2]
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&bar.tmem_base)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -527,52 +530,54 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
 
     if (warp < kCtlWarps) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
-        if (warp == 0) {  // ---------------- producer
-            // items are sorted by descending term count: the term-less ones (zero outputs) come last
-            if (lane == 0 && int(blockIdx.x) < nitems && items[blockIdx.x].t1 > items[blockIdx.x].t0) {
+        if (warp == 0) {  // ---------------- producer: per item its header + column scales, then the terms' pairs
+            if (lane == 0) {
                 uint32_t pc = 0;  // pair counter over all terms (buffer pc % 7, use (pc / 7))
-                uint32_t sbc = 0;  // column-scale copies
+                uint32_t ic = 0;  // item counter (slot ic & 1)
+                // the next term's descriptor is loaded one step ahead (dependent global loads)
                 int it = blockIdx.x;
-                OzItem I = items[it];
-                int t = I.t0;
-                OzTerm T = terms[t];
-                while (true) {  // (item, term) walk with the next descriptors loaded one step ahead
-                    int itn = it, tn = t + 1;
-                    OzItem In = I;
-                    if (tn >= I.t1) {
-                        itn = it + gridDim.x;
-                        if (itn < nitems) {
-                            In = items[itn];
-                            tn = In.t0;
-                            if (In.t1 <= In.t0) itn = nitems;
+                int ct0 = 0, ct1 = 0, cn0 = 0;
+                if (it < nitems) {
+                    ct0 = items[it].t0;
+                    ct1 = items[it].t1;
+                    cn0 = items[it].n0;
+                }
+                OzTerm T = ct1 > ct0 ? terms[ct0] : OzTerm{};
+                for (; it < nitems; it += gridDim.x, ++ic) {
+                    const int t0 = ct0, t1 = ct1, n0 = cn0;
+                    const int itn = it + int(gridDim.x);
+                    if (itn < nitems) {
+                        ct0 = items[itn].t0;
+                        ct1 = items[itn].t1;
+                        cn0 = items[itn].n0;
+                    }
+                    {  // item slot: the item (read by the epilogue) and its column scales (the first term's B)
+                        const uint32_t k = ic & 1;
+                        mbar_wait(&bar.sbempty[k], ((ic >> 1) & 1) ^ 1);
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // epilogue reads -> next bulk write
+                        uint8_t* slot = islot + k * kItemSlot;
+                        const double* sbp = t1 > t0 ? T.sb : nullptr;
+                        *reinterpret_cast<int*>(slot + sizeof(OzItem)) = sbp != nullptr;
+                        mbar_expect(&bar.sbfull[k], uint32_t(sizeof(OzItem)) + (sbp ? uint32_t(kSbBytes) : 0u));
+                        bulk_g2s(slot, items + it, uint32_t(sizeof(OzItem)), &bar.sbfull[k]);
+                        if (sbp) bulk_g2s(slot + 128, sbp + n0, uint32_t(kSbBytes), &bar.sbfull[k]);
+                        OZ_TRACE(3968 + ic);
+                    }
+                    for (int t = t0; t < t1; ++t) {
+                        const OzTerm Tc = T;
+                        const int tn = t + 1 < t1 ? t + 1 : (itn < nitems && ct1 > ct0 ? ct0 : -1);
+                        if (tn >= 0) T = terms[tn];
+                        const uint8_t* bsrc = Tc.b + size_t(n0) * kOzK;
+                        for (int i = 0; i < kOzS; ++i, ++pc) {  // digit pairs in release order 5, 4, 3, 2, 1, 0
+                            const int d = oz_digit_at(i);
+                            const uint32_t b = pc % kBufs, use = pc / kBufs;
+                            mbar_wait(&bar.empty[b], (use & 1) ^ 1);
+                            OZ_TRACE(pc);
+                            mbar_expect(&bar.full[b], kPair);
+                            bulk_g2s(sm + size_t(b) * kPair, Tc.a + size_t(d) * kSlice, kSlice, &bar.full[b]);
+                            bulk_g2s(sm + size_t(b) * kPair + kSlice, bsrc + size_t(d) * Tc.bstride, kSlice, &bar.full[b]);
                         }
                     }
-                    const bool more = itn < nitems;
-                    const OzTerm Tn = more ? terms[tn] : T;
-                    const uint8_t* bsrc = T.b + size_t(I.n0) * kOzK;
-                    for (int i = 0; i < kOzS; ++i, ++pc) {  // digit pairs in release order 5, 4, 3, 2, 1, 0
-                        const int d = oz_digit_at(i);
-                        const uint32_t b = pc % kBufs, use = pc / kBufs;
-                        mbar_wait(&bar.empty[b], (use & 1) ^ 1);
-                        OZ_TRACE(pc);
-                        mbar_expect(&bar.full[b], kPair);
-                        bulk_g2s(sm + size_t(b) * kPair, T.a + size_t(d) * kSlice, kSlice, &bar.full[b]);
-                        bulk_g2s(sm + size_t(b) * kPair + kSlice, bsrc + size_t(d) * T.bstride, kSlice, &bar.full[b]);
-                    }
-                    if (t == I.t0 && T.sb) {  // the tile's column scales (read by the epilogue after its last term)
-                        const uint32_t k = sbc & 1;
-                        mbar_wait(&bar.sbempty[k], ((sbc >> 1) & 1) ^ 1);
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // epilogue reads -> next bulk write
-                        mbar_expect(&bar.sbfull[k], uint32_t(kSbBytes));
-                        bulk_g2s(sbs + k * 128, T.sb + I.n0, uint32_t(kSbBytes), &bar.sbfull[k]);
-                        OZ_TRACE(3968 + sbc);
-                        ++sbc;
-                    }
-                    if (!more) break;
-                    it = itn;
-                    t = tn;
-                    I = In;
-                    T = Tn;
                 }
             }
             __syncwarp();
@@ -580,11 +585,18 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
             if (lane == 0) {
                 uint32_t pc = 0, g = 0;
                 const uint32_t s0 = su32(sm);
-                OzItem In = int(blockIdx.x) < nitems ? items[blockIdx.x] : OzItem{};
+                int n0t = 0, n1t = 0;  // the next item's term range (one item ahead)
+                if (int(blockIdx.x) < nitems) {
+                    n0t = items[blockIdx.x].t0;
+                    n1t = items[blockIdx.x].t1;
+                }
                 for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-                    const OzItem I = In;
-                    if (it + int(gridDim.x) < nitems) In = items[it + gridDim.x];  // one item ahead
-                    for (int t = I.t0; t < I.t1; ++t, pc += kOzS) {
+                    const int nterm = n1t - n0t;
+                    if (it + int(gridDim.x) < nitems) {
+                        n0t = items[it + gridDim.x].t0;
+                        n1t = items[it + gridDim.x].t1;
+                    }
+                    for (int t = 0; t < nterm; ++t, pc += kOzS) {
                         // this term's ring buffers: position i (digit pair oz_digit_at(i)) in buffer (pc + i) mod 7
                         const uint32_t p0 = pc % kBufs, u0 = pc / kBufs;
                         uint32_t alo[kOzS], blo[kOzS], fb[kOzS], fph[kOzS];
@@ -633,31 +645,39 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
         const int q = warp & 3, half = (warp - kCtlWarps) >> 2;  // half: column part 0..3
         const int row = q * 32 + lane;
         const uint32_t tq = tmem + (uint32_t(q * 32) << 16) + uint32_t(half * kCols);
-        uint32_t g = 0, sbc = 0, ipar = 0;
-        OzItem In = int(blockIdx.x) < nitems ? items[blockIdx.x] : OzItem{};
-        // the next term's descriptor and row factor are loaded one term ahead (dependent global loads)
-        const OzTerm* Tp = (int(blockIdx.x) < nitems && In.t1 > In.t0) ? terms + In.t0 : nullptr;
-        double fnext = Tp ? __ldg(Tp->sa + row) * (Tp->pe ? ldexp(1.0, __ldg(Tp->pe + In.n0 / 128)) : 1.0) : 0.0;
-        const double* sbnext = Tp ? Tp->sb : nullptr;
-        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-            const OzItem I = In;
-            if (it + int(gridDim.x) < nitems) In = items[it + gridDim.x];
-            const double* sbc_item = sbnext;  // column scales of this tile (its first term's B)
+        uint32_t g = 0, ic = 0, ipar = 0;
+        // a term's row factor (A row scale x the B plane's tile normalisation), loaded one term ahead
+        auto tfac = [&](int t, int n0) {
+            const double* sap = terms[t].sa;
+            const int* pep = terms[t].pe;
+            return __ldg(sap + row) * (pep ? ldexp(1.0, __ldg(pep + n0 / 128)) : 1.0);
+        };
+        int nt0 = 0, nt1 = 0, nn0 = 0;  // the next item's terms and first column
+        if (int(blockIdx.x) < nitems) {
+            nt0 = items[blockIdx.x].t0;
+            nt1 = items[blockIdx.x].t1;
+            nn0 = items[blockIdx.x].n0;
+        }
+        double fnext = nt1 > nt0 ? tfac(nt0, nn0) : 0.0;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++ic) {
+            const int t0 = nt0, t1 = nt1, n0 = nn0;
+            const int itn = it + int(gridDim.x);
+            if (itn < nitems) {
+                nt0 = items[itn].t0;
+                nt1 = items[itn].t1;
+                nn0 = items[itn].n0;
+            }
+            const uint32_t k = ic & 1;
+            const uint8_t* slot = islot + k * kItemSlot;
             double acc[kCols];
 #pragma unroll
             for (int j = 0; j < kCols; ++j) acc[j] = 0.0;
-            for (int t = I.t0; t < I.t1; ++t) {
-                const double sa = fnext;  // row scale x the B plane's tile normalisation (transposed splits)
-                {  // prefetch: the next term of this item, else the next item's first
-                    const bool last = t + 1 >= I.t1;
-                    const bool more = !last || (it + int(gridDim.x) < nitems && In.t1 > In.t0);
-                    if (more) {
-                        const OzTerm* Tn = terms + (last ? In.t0 : t + 1);
-                        const int n0 = last ? In.n0 : I.n0;
-                        fnext = __ldg(Tn->sa + row) * (Tn->pe ? ldexp(1.0, __ldg(Tn->pe + n0 / 128)) : 1.0);
-                        if (last) sbnext = Tn->sb;
-                    }
-                }
+            for (int t = t0; t < t1; ++t) {
+                const double sa = fnext;
+                if (t + 1 < t1)
+                    fnext = tfac(t + 1, n0);
+                else if (itn < nitems && nt1 > nt0)
+                    fnext = tfac(nt0, nn0);
                 // levels arrive 6 .. 0 and are drained three at a time, (6, 5, 4), (3, 2, 1), (0): the int32 levels
                 // combine exactly into y = P_(L-2) 2^16 + P_(L-1) 2^8 + P_L (|y| < 2^42), converted with one 64-bit
                 // bit trick and accumulated with the weight 2^-(14 + 8L) x row scale: two FP64 instructions per
@@ -709,11 +729,11 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                 drain(0, 1);
             }
             if (warp == kCtlWarps && lane == 0) OZ_TRACE(3584 + (it - blockIdx.x) / gridDim.x);
-            if (I.t1 > I.t0 && sbc_item) {  // column scales (copied to shared memory by the producer)
-                const uint32_t k = sbc & 1;
-                mbar_wait(&bar.sbfull[k], (sbc >> 1) & 1);
-                if (warp == kCtlWarps && lane == 0) OZ_TRACE(4032 + sbc);
-                const uint32_t sba = su32(sbs + k * 128 + half * kCols);  // broadcast shared loads
+            mbar_wait(&bar.sbfull[k], (ic >> 1) & 1);  // the item slot: the item and its column scales
+            if (warp == kCtlWarps && lane == 0) OZ_TRACE(4032 + ic);
+            const OzItem& I = *reinterpret_cast<const OzItem*>(slot);
+            if (t1 > t0 && *reinterpret_cast<const int*>(slot + sizeof(OzItem))) {  // column scales
+                const uint32_t sba = su32(slot + 128) + 8u * uint32_t(half * kCols);  // broadcast shared loads
                 const double al = I.alpha;
 #pragma unroll
                 for (int j = 0; j < kCols; j += 2) {
@@ -726,9 +746,6 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
 #pragma unroll
                     for (int j = 0; j < kCols; ++j) acc[j] *= al;
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bar.sbempty[k]);
-                ++sbc;
             }
             if (warp == kCtlWarps && lane == 0) OZ_TRACE(3712 + (it - blockIdx.x) / gridDim.x);
             if (I.pdst) {  // the tile as the next product's MN-major B panel tile: digits relative to the tile max
@@ -791,6 +808,8 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                 }
             }
             if (warp == kCtlWarps && lane == 0) OZ_TRACE(3840 + (it - blockIdx.x) / gridDim.x);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar.sbempty[k]);  // item slot read
         }
     }
     tc_before();
@@ -1316,7 +1335,7 @@ void oz_trace_dump() {  // diagnostics (CCF_OZ_MODE bit 2): block 0's event time
                     (long long)(t[3712 + i] - t0), (long long)(t[3840 + i] - t0));
 }
 
-size_t oz_smem_bytes() { return kSmemBufs + kBarsBytes + 2 * kSbBytes; }
+size_t oz_smem_bytes() { return kSmemBufs + kBarsBytes + 2 * kItemSlot; }
 
 void OzSplitPlan::upload() {
     maxrows = 0;

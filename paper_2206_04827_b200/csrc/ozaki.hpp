@@ -42,7 +42,7 @@ struct OzTerm {
     const int* pe;      // B plane exponent per 128-row tile of the B panel (transposed splits)
 };
 
-struct OzItem {         // one 128 x 128 output tile; every term of an item has the same B (column) scales
+struct alignas(16) OzItem {  // one 128 x 128 output tile; every term of an item has the same B (column) scales
     int t0, t1;         // terms [t0, t1)
     int n0;             // first B-panel row (output column) of the tile
     int m, n;           // valid rows / columns of the tile

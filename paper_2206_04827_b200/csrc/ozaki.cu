@@ -819,506 +819,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
 }
 
 
-// ---------------------------------------------------------------- CTA-pair kernel (cta_group::2, M = 256)
-// A 2-CTA cluster walks pair items (ozaki.hpp: two 128-row tiles with the same B and output columns). Rank r
-// streams its A tile and rows 64 r .. 64 r + 63 of the B tile: a ring of seven 24 KB pair buffers (A_d, B_d half)
-// at the same offsets in both CTAs. The leader's MMA thread issues M = 256 products reading both CTAs' buffers;
-// the peer's loads reach the leader's full barriers through a relay thread (its bulk copies complete on its own
-// barriers), and the commits multicast the buffer / accumulator barriers to both CTAs. Levels run ASCENDING:
-// level L needs digit pairs 0 .. L, so a term starts as soon as its first pair has landed and the next term's
-// pairs stream in while the current one finishes (pair 0 leaves the ring after level 5, pairs 1-5 after level 6).
-// Each CTA's epilogue drains its own TMEM half. Panel outputs are staged slice by slice in shared memory and
-// stored with bulk copies (16 KB, contiguous), fp64 outputs with direct stores (rows: 256-bit; transposed
-// (kOzOutCols): lane = output row, one coalesced 256-byte store per column and warp).
-__device__ unsigned long long g_pz_trace[2][10][256];  // diagnostics (CCF_OZ_MODE bit 2): cluster 0 event times
-#define PZ_TRACE(ev, idx)                                                                    \
-    do {                                                                                     \
-        if ((mode & 4) && blockIdx.x < 2 && (idx) < 256) g_pz_trace[rank][(ev)][(idx)] = oz_now(); \
-    } while (0)
-constexpr uint32_t kPA = 128 * kOzK;       // A slice (16 KB)
-constexpr uint32_t kPBh = 64 * kOzK;       // half a B slice (8 KB)
-constexpr uint32_t kPPair = kPA + kPBh;    // 24 KB
-// panel-output staging: per TMEM lane quadrant (its 32 rows = 4 KB of every digit slice, contiguous)
-constexpr uint32_t kPQuad = 32 * kOzK;     // a quadrant's part of one slice (4 KB)
-constexpr size_t kPItemSlot = 128 + 1024;  // the item (112 B, padded) + its 128 column scales
-static_assert(sizeof(OzPItem) <= 128 && sizeof(OzPItem) % 16 == 0, "OzPItem slot");
-// Shared-memory plan. Streaming B (BRES = false): a ring of 7 pair buffers (A_d 16 KB + B_d half 8 KB), three
-// staged slices per round. Resident B (BRES = true, every item of a cluster has the same B tile: the constant
-// operators of the back transforms and the z analysis): the six B half slices (48 KB) stay in shared memory
-// and the ring holds 9 A slices (1.5 terms: the next term's first digits load while the current term runs).
-template <bool BRES>
-struct PzCfg {
-    static constexpr int NB = BRES ? 9 : 7;                     // ring units
-    static constexpr uint32_t UNIT = BRES ? kPA : kPPair;       // bytes per unit
-    static constexpr size_t RING = BRES ? size_t(kOzS) * kPBh : 0;  // (resident B at 0)
-    static constexpr int ROUND = BRES ? 1 : 3;                  // staged slices per round
-    static constexpr size_t STAGE = RING + size_t(NB) * UNIT;
-    static constexpr size_t ITEM = STAGE + 4 * size_t(ROUND) * kPQuad;
-    static constexpr size_t BAR = ITEM + 2 * kPItemSlot;
-};
-constexpr int kPMaxBufs = 9;
-struct OzPBars {
-    uint64_t full[kPMaxBufs], empty[kPMaxBufs], accfull[kSlots], accempty[kSlots], itfull[2], itempty[2], bfull;
-    uint32_t tmem_base, pad;
-    uint32_t red[2][16];
-};
-template <bool BRES>
-constexpr size_t pz_smem() { return PzCfg<BRES>::BAR + sizeof(OzPBars); }
-static_assert(pz_smem<true>() <= 232448 && pz_smem<false>() <= 232448, "shared memory plan");
-
-__device__ __forceinline__ uint32_t cta_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t mapa0(uint32_t saddr) {  // the leader's (rank 0) copy of a shared address
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(saddr));
-    return r;
-}
-__device__ __forceinline__ void mbar_arrive_cl(uint32_t caddr) {  // (default .release.cta: no GPU-scope fence)
-    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cl(uint64_t* b, uint32_t parity) {  // acquire at cluster scope
-    asm volatile(
-        "{\n.reg .pred p;\nOZWC:\n"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra OZWC;\n}\n" ::"r"(su32(b)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit_mc(uint64_t* b) {  // arrive on this barrier in both CTAs of the pair
-    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                     su32(b)),
-                 "h"(uint16_t(3))
-                 : "memory");
-}
-__device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint32_t alo, uint32_t blo, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n.reg .b64 ad, bd;\n.reg .pred p;\n"
-        "mov.b64 ad, {%1, %5};\nmov.b64 bd, {%2, %5};\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::i8 [%0], ad, bd, %3, p;\n}\n" ::"r"(tmem_d),
-        "r"(alo), "r"(blo), "r"(idesc), "r"(acc), "n"(kDescHi));
-}
-// kind::i8, D = s32, M = 256 (pair), N = 128, B K-major; A K-major or MN-major (bit 15)
-__host__ __device__ constexpr uint32_t oz_pidesc(int asig, int bsig, int amn) {
-    return (2u << 4) | (uint32_t(asig) << 7) | (uint32_t(bsig) << 10) | (uint32_t(amn) << 15) | (uint32_t(kOzNT >> 3) << 17) |
-           (uint32_t(256 >> 4) << 24);
-}
-// level L of one term: pairs (d, L - d), 4 K-steps each (A: 32 bytes per step K-major, 32 k-rows MN-major)
-template <int L>
-__device__ __forceinline__ void oz_pair_level(uint32_t acc, const uint32_t (&alo)[kOzS], const uint32_t (&blo)[kOzS], int amn) {
-    constexpr int d0 = L > kOzS - 1 ? L - (kOzS - 1) : 0, d1 = L < kOzS - 1 ? L : kOzS - 1;
-    const uint32_t astep = amn ? 256u : 2u;
-#pragma unroll
-    for (int d = d0; d <= d1; ++d) {
-        const uint32_t id = oz_pidesc(d == 0, L - d == 0, amn);
-#pragma unroll
-        for (int k = 0; k < kOzK / 32; ++k)
-            mma_i8_pair(acc, alo[d] + astep * k, blo[L - d] + 2 * k, id, (d == d0 && k == 0) ? 0u : 1u);
-    }
-}
-
-// items of cluster c: [ranges[c].x, ranges[c].y) if ranges, else c, c + nclusters, ...
-struct PzWalk {
-    int it, end, step;
-    __device__ PzWalk(const int2* ranges, int cid, int ncl, int nitems) {
-        if (ranges) {
-            it = ranges[cid].x;
-            end = ranges[cid].y;
-            step = 1;
-        } else {
-            it = cid;
-            end = nitems;
-            step = ncl;
-        }
-    }
-    __device__ bool ok() const { return it < end; }
-    __device__ int next() const { return it + step; }
-    __device__ bool has_next() const { return it + step < end; }
-    __device__ void advance() { it += step; }
-};
-
-template <bool BRES>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    oz_pair_kernel(const OzPTerm* __restrict__ terms, const OzPItem* __restrict__ items, int nitems, const int2* __restrict__ ranges,
-                   int mode, int amn) {
-    using C = PzCfg<BRES>;
-    constexpr int kPBufs = C::NB;
-    extern __shared__ __align__(1024) uint8_t dsm[];
-    if (su32(dsm) & 1023) __trap();
-    uint8_t* sm = dsm;
-    OzPBars& bar = *reinterpret_cast<OzPBars*>(sm + C::BAR);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cta_rank();
-    const int cid = int(blockIdx.x >> 1), ncl = int(gridDim.x >> 1);
-    constexpr size_t kPItemOff = C::ITEM, kPStageOff = C::STAGE;
-    constexpr int kPRound = C::ROUND;
-    if (threadIdx.x == 0) {
-        mbar_init(&bar.bfull, rank == 0 ? 2 : 1);
-        for (int i = 0; i < kPBufs; ++i) {
-            mbar_init(&bar.full[i], rank == 0 ? 2 : 1);  // leader: own bytes + the peer relay
-            mbar_init(&bar.empty[i], 1);
-        }
-        for (int i = 0; i < kSlots; ++i) {
-            mbar_init(&bar.accfull[i], 1);
-            mbar_init(&bar.accempty[i], 2 * kEpiWarps);  // (used in the leader: both CTAs' epilogue warps)
-        }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&bar.itfull[i], 1);
-            mbar_init(&bar.itempty[i], kEpiWarps);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&bar.tmem_base)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-    }
-    tc_before();
-    __syncthreads();
-    cluster_sync_all();
-    tc_after();
-    const uint32_t tmem = bar.tmem_base;
-
-    if (warp < kCtlWarps) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
-        if (warp == 0 && lane == 0) {  // ---------------- producer (both CTAs); descriptors loaded one step ahead
-            uint32_t pc = 0, ic = 0;
-            PzWalk w(ranges, cid, ncl, nitems);
-            int nt0 = 0, nt1 = 0;
-            const double* nsb = nullptr;
-            if (w.ok()) {
-                nt0 = items[w.it].t0;
-                nt1 = items[w.it].t1;
-                nsb = items[w.it].sb;
-            }
-            const uint8_t *na = nullptr, *nb = nullptr;
-            long nas = 0, nbs = 0;
-            if (w.ok() && nt1 > nt0) {
-                na = terms[nt0].a[rank];
-                nb = terms[nt0].b;
-                nas = terms[nt0].astride;
-                nbs = terms[nt0].bstride;
-            }
-            if (BRES && na) {  // the cluster's B tile: its half of the six digit slices, once
-                mbar_expect(&bar.bfull, uint32_t(kOzS) * kPBh);
-                for (int d = 0; d < kOzS; ++d)
-                    bulk_g2s(sm + size_t(d) * kPBh, nb + size_t(d) * nbs + rank * kPBh, kPBh, &bar.bfull);
-            }
-            for (; w.ok(); w.advance(), ++ic) {
-                const int it = w.it;
-                const int t0 = nt0, t1 = nt1;
-                const double* sbp = nsb;
-                const bool more = w.has_next();
-                if (more) {
-                    nt0 = items[w.next()].t0;
-                    nt1 = items[w.next()].t1;
-                    nsb = items[w.next()].sb;
-                }
-                const uint32_t k = ic & 1;
-                mbar_wait(&bar.itempty[k], ((ic >> 1) & 1) ^ 1);
-                PZ_TRACE(7, ic);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // epilogue reads -> next bulk write
-                uint8_t* slot = sm + kPItemOff + k * kPItemSlot;
-                mbar_expect(&bar.itfull[k], uint32_t(sizeof(OzPItem)) + (sbp ? 1024u : 0u));
-                bulk_g2s(slot, items + it, uint32_t(sizeof(OzPItem)), &bar.itfull[k]);
-                if (sbp) bulk_g2s(slot + 128, sbp, 1024u, &bar.itfull[k]);
-                for (int t = t0; t < t1; ++t) {
-                    const uint8_t* ap = na;
-                    const uint8_t* bp = nb + rank * kPBh;
-                    const long as = nas, bs = nbs;
-                    const int tn = t + 1 < t1 ? t + 1 : (more && nt1 > nt0 ? nt0 : -1);
-                    if (tn >= 0) {
-                        na = terms[tn].a[rank];
-                        nb = terms[tn].b;
-                        nas = terms[tn].astride;
-                        nbs = terms[tn].bstride;
-                    }
-                    for (int d = 0; d < kOzS; ++d, ++pc) {
-                        const uint32_t b = pc % kPBufs, use = pc / kPBufs;
-                        mbar_wait(&bar.empty[b], (use & 1) ^ 1);
-                        PZ_TRACE(0, pc);
-                        uint8_t* ub = sm + C::RING + size_t(b) * C::UNIT;
-                        mbar_expect(&bar.full[b], C::UNIT);
-                        bulk_g2s(ub, ap + size_t(d) * as, kPA, &bar.full[b]);
-                        if (!BRES) bulk_g2s(ub + kPA, bp + size_t(d) * bs, kPBh, &bar.full[b]);
-                    }
-                }
-            }
-        } else if (warp == 1 && lane == 0 && rank == 1) {  // ---------------- relay: peer buffers -> leader barriers
-            uint32_t pc = 0;
-            bool bres = BRES;
-            for (PzWalk w(ranges, cid, ncl, nitems); w.ok(); w.advance()) {
-                const int nt = items[w.it].t1 - items[w.it].t0;
-                if (bres && nt > 0) {
-                    bres = false;
-                    mbar_wait(&bar.bfull, 0);
-                    mbar_arrive_cl(mapa0(su32(&bar.bfull)));
-                }
-                for (int i = 0; i < nt * kOzS; ++i, ++pc) {
-                    const uint32_t b = pc % kPBufs;
-                    mbar_wait(&bar.full[b], (pc / kPBufs) & 1);
-                    mbar_arrive_cl(mapa0(su32(&bar.full[b])));
-                    PZ_TRACE(6, pc);
-                }
-            }
-        } else if (warp == 1 && lane == 0) {  // ---------------- MMA issuer (leader)
-            uint32_t pc = 0, g = 0;
-            const uint32_t s0 = su32(sm + C::RING);
-            bool bres = BRES;
-            for (PzWalk w(ranges, cid, ncl, nitems); w.ok(); w.advance()) {
-                const int nt = items[w.it].t1 - items[w.it].t0;
-                if (bres && nt > 0) {
-                    bres = false;
-                    mbar_wait_cl(&bar.bfull, 0);
-                }
-                for (int t = 0; t < nt; ++t, pc += kOzS) {
-                    uint32_t alo[kOzS], blo[kOzS], fb[kOzS], fph[kOzS];
-#pragma unroll
-                    for (int d = 0; d < kOzS; ++d) {  // unit d of this term: ring position pc + d
-                        const uint32_t b = (pc + d) % kPBufs;
-                        alo[d] = sdesc_lo(s0 + b * C::UNIT);
-                        blo[d] = BRES ? sdesc_lo(su32(sm) + d * kPBh) : sdesc_lo(s0 + b * C::UNIT + kPA);
-                        fb[d] = b;
-                        fph[d] = ((pc + d) / kPBufs) & 1;
-                    }
-                    auto level = [&](auto Lc) {
-                        constexpr int L = decltype(Lc)::value;
-                        if (L < kOzS) mbar_wait_cl(&bar.full[fb[L]], fph[L]);
-                        PZ_TRACE(1, g);
-                        const uint32_t slot = g % kSlots;
-                        mbar_wait_cl(&bar.accempty[slot], ((g / kSlots) & 1) ^ 1);
-                        PZ_TRACE(2, g);
-                        tc_after();
-                        if (!(mode & 2)) oz_pair_level<L>(tmem + slot * 128, alo, blo, amn);
-                        tc_commit_mc(&bar.accfull[slot]);
-                        if (L == kOzS - 1) tc_commit_mc(&bar.empty[fb[0]]);  // pair 0: last used at level 5
-                        if (L == kLevels - 1)
-                            for (int d = 1; d < kOzS; ++d) tc_commit_mc(&bar.empty[fb[d]]);
-                        ++g;
-                    };
-                    level(std::integral_constant<int, 0>{});
-                    level(std::integral_constant<int, 1>{});
-                    level(std::integral_constant<int, 2>{});
-                    level(std::integral_constant<int, 3>{});
-                    level(std::integral_constant<int, 4>{});
-                    level(std::integral_constant<int, 5>{});
-                    level(std::integral_constant<int, 6>{});
-                }
-            }
-        }
-        __syncwarp();
-    } else {  // ---------------- epilogue (both CTAs): TMEM lane quadrant warp % 4, 32-column part
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));
-        const int q = warp & 3, half = (warp - kCtlWarps) >> 2;
-        const int row = q * 32 + lane;
-        const uint32_t tq = tmem + (uint32_t(q * 32) << 16) + uint32_t(half * kCols);
-        const uint32_t accempty0 = mapa0(su32(&bar.accempty[0]));
-        uint32_t g = 0, ic = 0, ipar = 0;
-        // the row factor of a term (A row scale x 2^tile exponent), loaded one term ahead
-        auto tfac = [&](int t) {
-            const double* sap = terms[t].sa[rank];
-            const int* pep = terms[t].pe[rank];
-            return (sap ? __ldg(sap + row) : 1.0) * (pep ? ldexp(1.0, __ldg(pep)) : 1.0);
-        };
-        PzWalk w(ranges, cid, ncl, nitems);
-        double fnext = (w.ok() && items[w.it].t1 > items[w.it].t0) ? tfac(items[w.it].t0) : 0.0;
-        for (; w.ok(); w.advance(), ++ic) {
-            const uint32_t k = ic & 1;
-            mbar_wait(&bar.itfull[k], (ic >> 1) & 1);
-            const OzPItem& I = *reinterpret_cast<const OzPItem*>(sm + kPItemOff + k * kPItemSlot);
-            const int t0 = I.t0, t1 = I.t1;
-            double acc[kCols];
-#pragma unroll
-            for (int j = 0; j < kCols; ++j) acc[j] = 0.0;
-            for (int t = t0; t < t1; ++t) {
-                const double sa = fnext;
-                if (t + 1 < t1) {
-                    fnext = tfac(t + 1);
-                } else if (w.has_next()) {
-                    const int n0 = items[w.next()].t0, n1 = items[w.next()].t1;
-                    if (n1 > n0) fnext = tfac(n0);
-                }
-#pragma unroll 1
-                // levels arrive 0 .. 6, drained in pairs (0, 1), (2, 3), (4, 5), (6): y = P_L 2^8 + P_(L+1) (exact,
-                // |y| < 2^34) converted with one 64-bit bit trick, weight 2^-(14 + 8 (L + 1)) x row scale
-                for (int L = 0; L < kLevels; L += 2) {
-                    const bool pair = L + 1 < kLevels;
-                    const uint32_t s0l = g % kSlots, s1l = (g + 1) % kSlots;
-                    mbar_wait(&bar.accfull[s0l], (g / kSlots) & 1);
-                    if (pair) mbar_wait(&bar.accfull[s1l], ((g + 1) / kSlots) & 1);
-                    if (warp == kCtlWarps && lane == 0) PZ_TRACE(3, g);
-                    tc_after();
-                    if (!(mode & 1)) {
-                        const double f = sa * ldexp(1.0, -14 - 8 * (pair ? L + 1 : L));
-#pragma unroll
-                        for (int c = 0; c < kCols / 16; ++c) {
-                            uint32_t vh[16], vl[16];
-                            tmem_ld16(tq + s0l * 128 + uint32_t(c * 16), vh);
-                            if (pair) tmem_ld16(tq + s1l * 128 + uint32_t(c * 16), vl);
-                            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                const long long y = pair ? (long long)int(vh[j]) * 256 + int(vl[j]) : (long long)int(vh[j]);
-                                const double x = __hiloint2double(int(uint32_t(y >> 32) + 0x43380000u), int(uint32_t(y))) -
-                                                 6755399441055744.0;
-                                acc[c * 16 + j] = fma(x, f, acc[c * 16 + j]);
-                            }
-                        }
-                    }
-                    tc_before();
-                    __syncwarp();
-                    if (lane == 0) {
-                        mbar_arrive_cl(accempty0 + 8u * s0l);
-                        if (pair) mbar_arrive_cl(accempty0 + 8u * s1l);
-                    }
-                    if (warp == kCtlWarps && lane == 0) PZ_TRACE(8, g);
-                    g += pair ? 2 : 1;
-                }
-            }
-            if (warp == kCtlWarps && lane == 0) PZ_TRACE(4, ic);
-            const double al = I.alpha;
-            if (I.sb) {  // column scales (bulk-copied with the item)
-                const uint32_t sba = su32(sm + kPItemOff + k * kPItemSlot + 128) + 8u * (half * kCols);
-#pragma unroll
-                for (int j = 0; j < kCols; j += 2) {
-                    double sx, sy;
-                    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(sx), "=d"(sy) : "r"(sba + 8u * j));
-                    acc[j] *= al * sx;
-                    acc[j + 1] *= al * sy;
-                }
-            } else if (al != 1.0) {
-#pragma unroll
-                for (int j = 0; j < kCols; ++j) acc[j] *= al;
-            }
-            const int mr = I.m[rank], nv = I.n - half * kCols;
-            if (I.kind == kOzOutPanel) {  // MN-major panel tile: digits relative to the tile max, staged + bulk stores
-                const bool full = mr == 128 && I.n == kOzNT;
-                uint32_t hx = 0;
-#pragma unroll
-                for (int j = 0; j < kCols; ++j) {
-                    const uint32_t h = uint32_t(__double2hiint(acc[j])) & 0x7FFFFFFFu;
-                    hx = (full || (row < mr && j < nv)) ? max(hx, h) : hx;
-                }
-#pragma unroll
-                for (int o = 16; o; o >>= 1) hx = max(hx, __shfl_xor_sync(0xffffffffu, hx, o));
-                if (lane == 0) bar.red[ipar][warp - kCtlWarps] = hx;
-                asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-#pragma unroll
-                for (int w = 0; w < kEpiWarps; ++w) hx = max(hx, bar.red[ipar][w]);
-                ipar ^= 1;
-                if (warp == kCtlWarps && lane == 0) PZ_TRACE(9, ic);
-                const double mx = __hiloint2double(int(hx), -1);
-                const int e = hx ? oz_exponent(mx) : 0;
-                const double scale = (hx && row < mr) ? ldexp(1.0, 47 - e) : 0.0;
-                uint32_t w[kOzS][8];
-#pragma unroll
-                for (int q8 = 0; q8 < 8; ++q8) {
-                    double xv[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) xv[u] = (full || q8 * 4 + u < nv) ? acc[q8 * 4 + u] : 0.0;
-                    uint32_t wq[kOzS];
-                    oz_pack4(xv, scale, wq);
-#pragma unroll
-                    for (int d = 0; d < kOzS; ++d) w[d][q8] = wq[d];
-                }
-                if (warp == kCtlWarps && lane == 0 && rank == 0) PZ_TRACE(6, ic);
-                // this thread's 32-byte sector of its row in every slice; the quadrant's 32 rows are 4 KB of the slice
-                const uint32_t off = (oz_swz(row, half * kCols) & ~31u) - uint32_t(q) * kPQuad;
-                const bool swp = (row & 1) != 0;
-                const uint32_t st0 = su32(sm + kPStageOff) + uint32_t(q) * (kPRound * kPQuad);
-                const bool issuer = half == 0 && lane == 0;  // one thread per quadrant issues its bulk stores
-                uint8_t* dst = I.pdst[rank] + size_t(q) * kPQuad;
-                const long pstr = I.pstride;
-#pragma unroll
-                for (int r0 = 0; r0 < kOzS; r0 += kPRound) {
-                    if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // previous round read
-                    asm volatile("bar.sync %0, 128;" ::"r"(2 + q) : "memory");
-#pragma unroll
-                    for (int i = 0; i < kPRound; ++i) {
-                        const int d = r0 + i;
-                        const uint32_t sb = st0 + uint32_t(i) * kPQuad + off;
-                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sb + (swp ? 16u : 0u)), "r"(w[d][0]),
-                                     "r"(w[d][1]), "r"(w[d][2]), "r"(w[d][3])
-                                     : "memory");
-                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sb + (swp ? 0u : 16u)), "r"(w[d][4]),
-                                     "r"(w[d][5]), "r"(w[d][6]), "r"(w[d][7])
-                                     : "memory");
-                    }
-                    if (mode & 64) {  // coalesced 256-bit stores by the quadrant's 128 threads (no bulk copies)
-                        asm volatile("bar.sync %0, 128;" ::"r"(2 + q) : "memory");  // the quadrant's slices staged
-                        const uint32_t tq = uint32_t(half * 32 + lane) * 32u;
-#pragma unroll
-                        for (int i = 0; i < kPRound; ++i) {
-                            uint32_t x[8];
-                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                                         : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3])
-                                         : "r"(st0 + uint32_t(i) * kPQuad + tq));
-                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                                         : "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7])
-                                         : "r"(st0 + uint32_t(i) * kPQuad + tq + 16u));
-                            if (!(mode & 32))
-                                asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(
-                                                 dst + size_t(r0 + i) * pstr + tq),
-                                             "r"(x[0]), "r"(x[1]), "r"(x[2]), "r"(x[3]), "r"(x[4]), "r"(x[5]), "r"(x[6]), "r"(x[7])
-                                             : "memory");
-                        }
-                        continue;
-                    }
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    asm volatile("bar.sync %0, 128;" ::"r"(2 + q) : "memory");  // the quadrant's slices staged
-                    if (issuer && !(mode & 32)) {
-#pragma unroll
-                        for (int i = 0; i < kPRound; ++i)
-                            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
-                                             dst + size_t(r0 + i) * pstr),
-                                         "r"(st0 + uint32_t(i) * kPQuad), "r"(kPQuad)
-                                         : "memory");
-                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                    }
-                }
-                if (threadIdx.x == kEpi0 && I.ppe[rank]) *I.ppe[rank] = e;
-            } else if (!(mode & 32) && I.kind == kOzOutCols) {  // transposed fp64: lane = output row, coalesced columns
-                double* cb = I.c[rank] + half * kCols * I.ldc + row;
-                const long ldc = I.ldc;
-                if (row < mr) {
-#pragma unroll
-                    for (int j = 0; j < kCols; ++j)
-                        if (j < nv) cb[j * ldc] = acc[j];
-                }
-            } else if (!(mode & 32) && row < mr) {  // fp64 rows
-                double* crow = I.c[rank] + long(row) * I.ldc + half * kCols;
-                if (nv >= kCols && ((reinterpret_cast<uintptr_t>(crow) & 31) == 0)) {
-#pragma unroll
-                    for (int j = 0; j < kCols; j += 4)
-                        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(crow + j), "d"(acc[j]), "d"(acc[j + 1]),
-                                     "d"(acc[j + 2]), "d"(acc[j + 3])
-                                     : "memory");
-                } else {
-#pragma unroll
-                    for (int j = 0; j < kCols; ++j)
-                        if (j < nv) crow[j] = acc[j];
-                }
-            }
-            __syncwarp();
-            if (warp == kCtlWarps && lane == 0) PZ_TRACE(5, ic);
-            if (lane == 0) mbar_arrive(&bar.itempty[k]);  // item slot read
-        }
-        if (half == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    }
-    tc_before();
-    __syncthreads();
-    cluster_sync_all();  // the peer's epilogue arrivals and the leader's products are done before TMEM goes
-    tc_after();
-    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
-
 }  // namespace
-
-size_t oz_pair_smem_bytes() { return pz_smem<false>(); }
 
 void oz_trace_dump() {  // diagnostics (CCF_OZ_MODE bit 2): block 0's event times, ns from the first
     std::vector<unsigned long long> t(4096);
@@ -1428,113 +929,8 @@ OzGemmPlan::~OzGemmPlan() {
     if (ditems) cudaFree(ditems);
 }
 
-void OzPairPlan::upload() {
-    if (dterms) cudaFree(dterms);
-    if (ditems) cudaFree(ditems);
-    if (dranges) cudaFree(dranges);
-    dterms = nullptr;
-    ditems = nullptr;
-    dranges = nullptr;
-    flops = 0.0;
-    for (const OzPItem& it : items) {
-        if (it.t0 < 0 || it.t1 > int(terms.size()) || it.t0 > it.t1 || it.m[0] > 128 || it.m[1] > 128 || it.n > kOzNT ||
-            it.kind < 0 || it.kind > 2 || (b_res && it.t1 == it.t0))
-            throw Error(INTERNAL, "OzPairPlan: bad item");
-        flops += 2.0 * (it.m[0] + it.m[1]) * it.n * kOzK * (it.t1 - it.t0);
-    }
-    for (const OzPTerm& t : terms)
-        if ((reinterpret_cast<uintptr_t>(t.a[0]) | reinterpret_cast<uintptr_t>(t.a[1]) | reinterpret_cast<uintptr_t>(t.b) |
-             uintptr_t(t.astride) | uintptr_t(t.bstride)) & 15)
-            throw Error(INTERNAL, "OzPairPlan: operand tiles must be 16-byte aligned");
-    int dev = 0, nsm = 0;
-    CCF_CUDA(cudaGetDevice(&dev));
-    CCF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    const int maxcl = nsm / 2;
-    std::vector<int2> ranges;
-    if (b_res) {
-        // group by B tile; each group gets clusters in proportion to its terms, each cluster a contiguous run
-        for (const OzPItem& it : items)
-            for (int t = it.t0 + 1; t < it.t1; ++t)
-                if (terms[t].b != terms[it.t0].b || terms[t].bstride != terms[it.t0].bstride)
-                    throw Error(INTERNAL, "OzPairPlan: resident-B item with several B tiles");
-        std::stable_sort(items.begin(), items.end(), [&](const OzPItem& x, const OzPItem& y) {
-            return std::less<const uint8_t*>()(terms[x.t0].b, terms[y.t0].b);
-        });
-        std::vector<std::pair<int, int>> groups;  // [begin, end) item ranges with one B
-        for (int i = 0; i < int(items.size());) {
-            int j = i;
-            while (j < int(items.size()) && terms[items[j].t0].b == terms[items[i].t0].b) ++j;
-            groups.push_back({i, j});
-            i = j;
-        }
-        const int ng = int(groups.size());
-        std::vector<int> ncg(ng, 1);
-        int left = std::max(maxcl, ng) - ng;
-        const double per = double(items.size()) / double(std::max(maxcl, ng));
-        for (int g = 0; g < ng && left > 0; ++g) {
-            const int want = std::max(1, int((groups[g].second - groups[g].first) / per + 0.5)) - 1;
-            const int add = std::min(want, left);
-            ncg[g] += add;
-            left -= add;
-        }
-        for (int g = 0; left > 0; g = (g + 1) % ng, --left) ncg[g] += 1;
-        for (int g = 0; g < ng; ++g) {
-            const int b = groups[g].first, n = groups[g].second - b;
-            const int c = std::min(ncg[g], n);
-            for (int k = 0; k < c; ++k) ranges.push_back(make_int2(b + int(int64_t(n) * k / c), b + int(int64_t(n) * (k + 1) / c)));
-        }
-        nclusters = int(ranges.size());
-    } else {
-        std::stable_sort(items.begin(), items.end(), [](const OzPItem& x, const OzPItem& y) { return x.t1 - x.t0 > y.t1 - y.t0; });
-        nclusters = int(std::min<size_t>(items.size(), size_t(maxcl)));
-    }
-    if (terms.empty() || items.empty()) return;
-    CCF_CUDA(cudaMalloc(&dterms, terms.size() * sizeof(OzPTerm)));
-    CCF_CUDA(cudaMalloc(&ditems, items.size() * sizeof(OzPItem)));
-    CCF_H2D(dterms, terms.data(), terms.size() * sizeof(OzPTerm));
-    CCF_H2D(ditems, items.data(), items.size() * sizeof(OzPItem));
-    if (!ranges.empty()) {
-        CCF_CUDA(cudaMalloc(&dranges, ranges.size() * sizeof(int2)));
-        CCF_H2D(dranges, ranges.data(), ranges.size() * sizeof(int2));
-    }
-}
-
-void OzPairPlan::launch(cudaStream_t s) const {
-    if (items.empty()) return;
-    static bool attr = false;
-    if (!attr) {
-        CCF_CUDA(cudaFuncSetAttribute(oz_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pz_smem<false>())));
-        CCF_CUDA(cudaFuncSetAttribute(oz_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pz_smem<true>())));
-        attr = true;
-    }
-    static const int mode = std::getenv("CCF_OZ_MODE") ? std::atoi(std::getenv("CCF_OZ_MODE")) : 0;  // diagnostics
-    const unsigned grid = 2u * unsigned(nclusters);
-    if (b_res)
-        oz_pair_kernel<true><<<grid, kThreads, pz_smem<true>(), s>>>(dterms, ditems, int(items.size()), dranges, mode, int(a_mn));
-    else
-        oz_pair_kernel<false><<<grid, kThreads, pz_smem<false>(), s>>>(dterms, ditems, int(items.size()), nullptr, mode, int(a_mn));
-    CCF_CUDA(cudaGetLastError());
-}
-
-OzPairPlan::~OzPairPlan() {
-    if (dterms) cudaFree(dterms);
-    if (ditems) cudaFree(ditems);
-    if (dranges) cudaFree(dranges);
-}
-
 }  // namespace ccf
 
 // diagnostics entry point (not part of include/ccf.h): print block 0's trace of the last traced launch
 extern "C" void ccf_debug_oz_trace_dump() { ccf::oz_trace_dump(); }
 
-// the CTA-pair kernel's cluster-0 trace (CCF_OZ_MODE bit 2), ns from the leader's first pair issue
-extern "C" void ccf_debug_pz_trace_dump(int n) {
-    std::vector<unsigned long long> t(2 * 10 * 256);
-    cudaMemcpyFromSymbol(t.data(), ccf::g_pz_trace, t.size() * 8);
-    auto at = [&](int r, int e, int i) -> long long { const unsigned long long v = t[(r * 10 + e) * 256 + i]; return v ? (long long)(v - t[0]) : -1; };
-    std::printf("  i | issue0 issue1 relay | mma-ready mma-go | got0 done0 got1 done1 | out0: start maxed packed end | out1-start out1-end | slot0 slot1\n");
-    for (int i = 0; i < n; ++i)
-        std::printf("%3d | %7lld %7lld %7lld | %7lld %7lld | %7lld %7lld %7lld %7lld | %7lld %7lld %7lld %7lld | %7lld %7lld | %7lld %7lld\n", i,
-                    at(0, 0, i), at(1, 0, i), at(1, 6, i), at(0, 1, i), at(0, 2, i), at(0, 3, i), at(0, 8, i), at(1, 3, i), at(1, 8, i),
-                    at(0, 4, i), at(0, 9, i), at(0, 6, i), at(0, 5, i), at(1, 4, i), at(1, 5, i), at(0, 7, i), at(1, 7, i));
-}

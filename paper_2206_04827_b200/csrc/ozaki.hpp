@@ -118,51 +118,7 @@ struct OzGemmPlan {
     ~OzGemmPlan();
 };
 
-// ---- CTA-pair products (tcgen05.mma.cta_group::2, M = 256): a pair item is two 128-row output tiles (one per
-// CTA of a 2-CTA cluster) with the same B operand and the same output columns. Each CTA streams its own A panel
-// tile and HALF of the B tile (rank r: B rows 64 r .. 64 r + 63), so every SM moves 144 KB instead of 192 KB per
-// term and the tensor cores read 6 KB of shared memory per 128 x 128 x 32 step instead of 8 KB.
-struct OzPTerm {
-    const uint8_t* a[2];  // A panel tile of each rank (128 rows x K = 128), slice d at a + d * astride
-    const uint8_t* b;     // B panel tile (128 rows = output columns), slice d at b + d * bstride
-    const double* sa[2];  // A row scales per rank (128), or null (1)
-    const int* pe[2];     // A tile exponent per rank (a power-of-two factor 2^pe of the term), or null
-    long astride, bstride;
-};
-enum OzOut : int { kOzOutRows = 0, kOzOutCols = 1, kOzOutPanel = 2 };
-struct alignas(16) OzPItem {
-    int t0, t1;           // terms [t0, t1)
-    int m[2];             // valid rows per rank
-    int n;                // valid columns
-    int kind;             // OzOut: fp64 c[r] + row * ldc + col | fp64 c[r] + col * ldc + row | MN-major panel tile
-    double alpha;
-    const double* sb;     // 128 column scales shared by the terms, or null (1)
-    double* c[2];
-    long ldc;
-    uint8_t* pdst[2];     // panel tile per rank: slice d at pdst[r] + d * pstride, tile exponent -> *ppe[r]
-    long pstride;
-    int* ppe[2];
-};
-struct OzPairPlan {
-    std::vector<OzPTerm> terms;
-    std::vector<OzPItem> items;
-    OzPTerm* dterms = nullptr;
-    OzPItem* ditems = nullptr;
-    double flops = 0.0;   // FP64-equivalent 2 M N K per term and 128-row tile
-    bool a_mn = false;    // A panels MN-major (written by a panel-output epilogue) instead of K-major row splits
-    // every item's terms share one of a few B tiles (the constant operators): clusters are assigned contiguous runs
-    // of items with the same B, which stays resident in shared memory (upload() groups the items)
-    bool b_res = false;
-    const char* tag = nullptr;
-    int2* dranges = nullptr;
-    int nclusters = 0;
-    void upload();
-    void launch(cudaStream_t s) const;
-    ~OzPairPlan();
-};
-
 size_t oz_smem_bytes();
-size_t oz_pair_smem_bytes();
 void oz_trace_dump();
 
 }  // namespace ccf

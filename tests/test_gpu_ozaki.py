@@ -32,29 +32,6 @@ def test_ozaki_gemm(P, shape, env):
     assert r.returncode == 0 and m and float(m.group(1)) < 1e-12, r.stdout
 
 
-OZP = os.path.join(ROOT, "tools", "cpp", "oz_pair_check")
-
-
-@pytest.mark.parametrize("args,env", [
-    ("1 1 0 0 0.9", {}),            # one pair item, fp64 rows
-    ("1 1 1 0 0.9", {}),            # transposed fp64 output
-    ("1 3 0 0 0.9", {}),            # three terms, shared-scale B blocks (group split)
-    ("1 1 0 1 0.9", {}),            # MN-major A (panel tiles) with tile exponents
-    ("300 2 1 1 0.8", {}),          # many items per cluster: ring / item-slot / TMEM phases
-    ("74 1 0 0 0.9", {"CCF_OZ_BRES": "1"}),    # resident B, one cluster per run of items
-    ("300 1 1 1 0.8", {"CCF_OZ_BRES": "1"}),
-])
-def test_ozaki_pair_gemm(P, args, env):
-    """CTA-pair products (tcgen05.mma.cta_group::2, M = 256) against long-double host products."""
-    if not os.path.exists(OZP):
-        import __graft_entry__
-        __graft_entry__.build()
-    r = subprocess.run([OZP, *args.split()], capture_output=True, text=True, timeout=300, env=dict(os.environ, **env))
-    print(r.stdout, r.stderr)
-    m = re.search(r"max rel err ([0-9.e+-]+)", r.stdout)
-    assert r.returncode == 0 and m and float(m.group(1)) < 1e-12, r.stdout
-
-
 SCRIPT = r"""
 import sys, numpy as np
 sys.path.insert(0, {root!r})

@@ -41,7 +41,7 @@ def launches(path):
 def kernel(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(raw)))
-    h, u, v = r[0], r[1], r[2]
+    h, u = r[0], r[1]
     want = ["Kernel Name", "gpu__time_duration.sum", "launch__grid_size", "launch__block_size",
             "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
             "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
@@ -49,19 +49,21 @@ def kernel(path):
             "smsp__issue_active.avg.pct_of_peak_sustained_active", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "dram__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
             "smsp__inst_executed.sum"]
-    for w in want:
-        if w in h:
-            i = h.index(w)
-            print(f"  {w:62s} {v[i]} {u[i]}")
-    st = []
-    for i, n in enumerate(h):
-        if n.startswith("smsp__average_warps_issue_stalled") and n.endswith("per_issue_active.ratio"):
-            try:
-                st.append((float(v[i]), n.replace("smsp__average_warps_issue_stalled_", "").replace(
-                    "_per_issue_active.ratio", "")))
-            except ValueError:
-                pass
-    print("  stall cycles per issued instruction: " + ", ".join(f"{n} {x:.2f}" for x, n in sorted(st, reverse=True)[:7]))
+    for v in r[2:]:  # every launch of the capture
+        for w in want:
+            if w in h:
+                i = h.index(w)
+                print(f"  {w:62s} {v[i]} {u[i]}")
+        st = []
+        for i, n in enumerate(h):
+            if n.startswith("smsp__average_warps_issue_stalled") and n.endswith("per_issue_active.ratio"):
+                try:
+                    st.append((float(v[i]), n.replace("smsp__average_warps_issue_stalled_", "").replace(
+                        "_per_issue_active.ratio", "")))
+                except ValueError:
+                    pass
+        print("  stall cycles per issued instruction: " + ", ".join(f"{n} {x:.2f}" for x, n in sorted(st, reverse=True)[:7]))
+        print()
     src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
     rows, fn = [], None

@@ -73,6 +73,11 @@ struct EigRhs {
     double* outp;              // optional: -out[0] .* rtp (the next step's Poisson RHS in eigen coordinates)
     const double* const* rtp;  // RT table of the Poisson set
     int* flag;                 // optional: set to 1 on a non-finite output (NaN guard, ptns.cpp:260-262)
+    // optional (INT8 product path, ozaki.hpp): also write out[0], out[1], outp as row-scaled digit panels, the
+    // back transform's A operands: panel ((s - slo) * 2 + pl) * 2 + k0 of tensor t at pan[t] (16 KB slices,
+    // 96 KB panels), row scales at psc[t] + panel * 128 (eigen row i = panel row)
+    uint8_t* pan[3];
+    double* psc[3];
 };
 
 // transform.cu

@@ -8,59 +8,12 @@
 
 #include "context.hpp"
 #include "ozaki.hpp"
+#include "ozaki_dev.cuh"
 
 namespace ccf {
 namespace {
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
-
-// byte offset of (row r, reduction byte k) in a 128-byte-swizzled K-major slice
-__host__ __device__ __forceinline__ uint32_t oz_swz(int r, int k) {
-    return uint32_t(r >> 3) * 1024u + uint32_t(r & 7) * 128u + ((uint32_t((k >> 4) ^ (r & 7)) << 4) | uint32_t(k & 15));
-}
-
-// ---------------------------------------------------------------- digits
-// s = 2^e with max|row| < s; X = rint(x 2^(47 - e)) in [-2^47, 2^47): 48-bit two's complement,
-// digit 0 = signed top byte, digits 1..5 = unsigned lower bytes (ozaki.hpp)
-__device__ __forceinline__ int oz_exponent(double maxabs) {
-    int e = 0;
-    frexp(maxabs, &e);  // maxabs = f 2^e, f in [0.5, 1): maxabs < 2^e
-    return e;
-}
-__device__ __forceinline__ long long oz_fixed(double x, int e) {
-    long long X = __double2ll_rn(ldexp(x, 47 - e));
-    return X > (1LL << 47) - 1 ? (1LL << 47) - 1 : X;
-}
-__device__ __forceinline__ uint32_t oz_digit(long long X, int d) {
-    return d == 0 ? uint32_t(int(X >> 40)) & 255u : uint32_t(X >> (40 - 8 * d)) & 255u;
-}
-
-// The digits of four values as six packed words (word d holds digit d of value u in byte u): scale
-// 2^(47 - e) and round with one FMA against 1.5 2^52 (exact: |x 2^(47-e)| < 2^47), so the low 48 bits
-// of the double ARE the two's-complement integer X, whose bytes 5..0 are digits 0..5 (digit 0 signed).
-// Byte transposes with PRMT: 12 per four values.
-__device__ __forceinline__ void oz_pack4(const double (&x)[4], double scale, uint32_t (&w)[kOzS]) {
-    uint32_t lo[4], hi[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const double y = fma(x[u], scale, 6755399441055744.0);
-        lo[u] = uint32_t(__double2loint(y));
-        hi[u] = uint32_t(__double2hiint(y)) - 0x43380000u;  // X = bits(y) - bits(1.5 2^52)
-        if (hi[u] == 0x8000u) {  // X = 2^47 (a rounded maximum): clamp to 2^47 - 1
-            hi[u] = 0x7FFFu;
-            lo[u] = 0xFFFFFFFFu;
-        }
-    }
-    const uint32_t a = __byte_perm(lo[0], lo[1], 0x5140), b = __byte_perm(lo[2], lo[3], 0x5140);
-    const uint32_t c = __byte_perm(lo[0], lo[1], 0x7362), d = __byte_perm(lo[2], lo[3], 0x7362);
-    const uint32_t e = __byte_perm(hi[0], hi[1], 0x5140), f = __byte_perm(hi[2], hi[3], 0x5140);
-    w[0] = __byte_perm(e, f, 0x7632);  // byte 5 of X
-    w[1] = __byte_perm(e, f, 0x5410);  // byte 4
-    w[2] = __byte_perm(c, d, 0x7632);  // byte 3
-    w[3] = __byte_perm(c, d, 0x5410);  // byte 2
-    w[4] = __byte_perm(a, b, 0x7632);  // byte 1
-    w[5] = __byte_perm(a, b, 0x5410);  // byte 0
-}
 
 // Exponent of a tile whose largest |value| has the high word hx: e with max|tile| < (hx + 1, 0) <= 2^e, so that
 // max|tile| 2^(47 - e) rounds below 2^47 (no clamp needed; the usual e of max|tile|, one more only when the

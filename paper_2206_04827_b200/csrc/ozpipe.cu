@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "kernels.cuh"
 #include "ozaki.hpp"
 #include "pipeline.hpp"
 
@@ -191,7 +192,9 @@ bool OzPipe::ysynth(int ntensor, const double* const* z, double* const* outS, do
         gp->gemm.tag = "H";
         gp->gemm.upload();
     }
-    sp->split.launch(P.c.stream);
+    const bool written = rhs_split_ == key_of("ys_split", {z[0], z1, z2});  // by the RHS pass just before
+    rhs_split_.clear();
+    if (!written) sp->split.launch(P.c.stream);
     P.c.mark("H_z_split");
     gp->gemm.launch(P.c.stream);
     P.c.gemm_flops += gp->gemm.flops;
@@ -200,6 +203,20 @@ bool OzPipe::ysynth(int ntensor, const double* const* z, double* const* outS, do
         if (outS[t]) panel_only_.insert(outS[t]);
         if (outD[t]) panel_only_.insert(outD[t]);
     }
+    return true;
+}
+
+bool OzPipe::rhs_panels(const double* z0, const double* z1, const double* z2, EigRhs& a) {
+    rhs_split_.clear();
+    if (!on || !(mask & 1) || !(mask & 2) || const_set_ != P.eig_set_ || !z0 || !z1 || !z2) return false;
+    const std::string key = key_of("ys_split", {z0, z1, z2});
+    if (!stages_.count(key) || !stages_[key]) return false;  // built by ysynth's first (eager) call
+    const int ns = P.c.sh.s_hi - P.c.sh.s_lo;
+    for (int t = 0; t < 3; ++t) {  // panel index ((t ns + s - s_lo) 2 + pl) 2 + k0, as in ysynth
+        a.pan[t] = bytes(ysp_) + size_t(t) * ns * 4 * kPanel128;
+        a.psc[t] = ysc_.p + size_t(t) * ns * 4 * 128;
+    }
+    rhs_split_ = key;
     return true;
 }
 

@@ -9,6 +9,7 @@
 #include <cudaTypedefs.h>
 
 #include "pipeline.hpp"
+#include "ozaki_dev.cuh"
 
 #include <cstdlib>
 
@@ -1445,6 +1446,73 @@ __global__ void __launch_bounds__(128) eigen_rhs_kernel(EigRhs a) {
     }
 }
 
+// eigen_rhs_kernel fused with the back transform's row split (INT8 product path): one warp per half row
+// (t, s, pl, i, k0), four columns per lane; besides the fp64 outputs it writes each half row as a row of the
+// digit panel ((s - slo) 2 + pl) 2 + k0 of its tensor (ozaki.hpp: 48-bit fixed point relative to the row max,
+// the same digits the row-split kernel would produce), so the split pass of the back transform disappears
+template <int NS>
+__global__ void __launch_bounds__(128) eigen_rhs_pan_kernel(EigRhs a) {
+    const int lane = threadIdx.x & 31;
+    const long hrows = long(a.ntensor) * a.nslots * 2 * a.M * 2;
+    const int ld = 2 * a.Np;
+    auto panel_row = [&](const double (&o)[4], int t, long pidx, int i) {  // digits of one panel row
+        double mx = fmax(fmax(fabs(o[0]), fabs(o[1])), fmax(fabs(o[2]), fabs(o[3])));
+#pragma unroll
+        for (int sh = 16; sh; sh >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, sh));
+        const int e = mx > 0.0 ? oz_exponent(mx) : 0;
+        uint32_t w[kOzS];
+        oz_pack4(o, mx > 0.0 ? ldexp(1.0, 47 - e) : 0.0, w);
+        uint8_t* pan = a.pan[t] + pidx * (size_t(kOzS) * 128 * kOzK) + oz_swz(i, 4 * lane);
+#pragma unroll
+        for (int d = 0; d < kOzS; ++d) *reinterpret_cast<uint32_t*>(pan + size_t(d) * 128 * kOzK) = w[d];
+        if (lane == 0) a.psc[t][pidx * 128 + i] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
+    };
+    for (long hr = long(blockIdx.x) * 4 + (threadIdx.x >> 5); hr < hrows; hr += long(gridDim.x) * 4) {
+        const int k0 = int(hr & 1);
+        const long row = hr >> 1;
+        const int t = int(row / (long(a.nslots) * 2 * a.M));
+        const long rr = row - long(t) * a.nslots * 2 * a.M;  // ((s - slo) * 2 + pl) * M + i
+        const int i = int(rr % a.M);
+        const long spl = rr / a.M;                             // (s - slo) * 2 + pl
+        const int s = a.slo + int(spl >> 1);
+        const long base = (rr + long(a.slo) * 2 * a.M) * ld + long(k0) * a.Np;
+        const int j = 4 * lane;
+        double2 v[NS][2];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            v[q][0] = __ldg(reinterpret_cast<const double2*>(a.src[t][q] + base + j));
+            v[q][1] = __ldg(reinterpret_cast<const double2*>(a.src[t][q] + base + j + 2));
+        }
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            acc[0] = fma(a.w[q], v[q][0].x, acc[0]);
+            acc[1] = fma(a.w[q], v[q][0].y, acc[1]);
+            acc[2] = fma(a.w[q], v[q][1].x, acc[2]);
+            acc[3] = fma(a.w[q], v[q][1].y, acc[3]);
+        }
+        const double* rt = a.rt[s * 2 + k0] + long(i) * a.Np + j;
+        const double2 r0 = __ldg(reinterpret_cast<const double2*>(rt)), r1 = __ldg(reinterpret_cast<const double2*>(rt + 2));
+        const double rv[4] = {r0.x, r0.y, r1.x, r1.y};
+        double o[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) o[u] = j + u < a.N ? a.factor * acc[u] * rv[u] : 0.0;
+        *reinterpret_cast<double2*>(a.out[t] + base + j) = make_double2(o[0], o[1]);
+        *reinterpret_cast<double2*>(a.out[t] + base + j + 2) = make_double2(o[2], o[3]);
+        if (a.flag && !(isfinite(o[0]) && isfinite(o[1]) && isfinite(o[2]) && isfinite(o[3]))) *a.flag = 1;
+        const long pidx = spl * 2 + k0;
+        panel_row(o, t, pidx, i);
+        if (a.outp && t == 0) {
+            const double* rtp = a.rtp[s * 2 + k0] + long(i) * a.Np + j;
+            const double2 p0 = __ldg(reinterpret_cast<const double2*>(rtp)), p1 = __ldg(reinterpret_cast<const double2*>(rtp + 2));
+            const double op[4] = {-o[0] * p0.x, -o[1] * p0.y, -o[2] * p1.x, -o[3] * p1.y};
+            *reinterpret_cast<double2*>(a.outp + base + j) = make_double2(op[0], op[1]);
+            *reinterpret_cast<double2*>(a.outp + base + j + 2) = make_double2(op[2], op[3]);
+            panel_row(op, 2, pidx, i);
+        }
+    }
+}
+
 void Pipeline::ensure_eigen(DevSet& pset) {
     if (eig_set_ == &pset) return;
     SetupTimer tm("eigen-coordinate operators");
@@ -1592,7 +1660,7 @@ const double* const* Pipeline::eig_rt(DevSet& set) {
 
 void Pipeline::eigen_rhs(DevSet& set, int ntensor, const double* const* s0, const double* const* s1, const double* w,
                          int nsrc, double factor, double* out0, double* out1, double* outp, DevSet* pset,
-                         int* flag) {
+                         int* flag, bool panels) {
     EigRhs a{};
     if (outp) {
         a.outp = outp;
@@ -1617,6 +1685,23 @@ void Pipeline::eigen_rhs(DevSet& set, int ntensor, const double* const* s0, cons
     a.nslots = c.sh.s_hi - c.sh.s_lo;
     const long rows = long(a.nslots) * 2 * a.M * ntensor;
     const unsigned grid = unsigned(std::min<long>(rows, 148L * 16));
+    if (panels && ntensor == 2 && outp && a.Np == 128 && oz().rhs_panels(out0, out1, outp, a)) {
+        const unsigned gp = unsigned(std::min<long>((rows * 2 + 3) / 4, 148L * 16));
+        switch (nsrc) {
+            case 1: eigen_rhs_pan_kernel<1><<<gp, 128, 0, c.stream>>>(a); break;
+            case 2: eigen_rhs_pan_kernel<2><<<gp, 128, 0, c.stream>>>(a); break;
+            case 3: eigen_rhs_pan_kernel<3><<<gp, 128, 0, c.stream>>>(a); break;
+            case 4: eigen_rhs_pan_kernel<4><<<gp, 128, 0, c.stream>>>(a); break;
+            case 5: eigen_rhs_pan_kernel<5><<<gp, 128, 0, c.stream>>>(a); break;
+            case 6: eigen_rhs_pan_kernel<6><<<gp, 128, 0, c.stream>>>(a); break;
+            case 7: eigen_rhs_pan_kernel<7><<<gp, 128, 0, c.stream>>>(a); break;
+            case 8: eigen_rhs_pan_kernel<8><<<gp, 128, 0, c.stream>>>(a); break;
+            default: throw Error(INTERNAL, "eigen_rhs: source count out of range");
+        }
+        CCF_CUDA(cudaGetLastError());
+        ++c.launches;
+        return;
+    }
     switch (nsrc) {
         case 1: eigen_rhs_kernel<1><<<grid, 128, 0, c.stream>>>(a); break;
         case 2: eigen_rhs_kernel<2><<<grid, 128, 0, c.stream>>>(a); break;
@@ -1984,7 +2069,7 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
         // PL_H = -(1/s) PL_P; the same pass leaves the next step's Poisson RHS Z_P = -Z_lambda .* RT_P and
         // raises the non-finite flag
         P.eigen_rhs(set, scalar ? 1 : 2, sl, sg, wl, ns, -1.0 / scale, zl[out].p, zg[out].p,
-                    disable_nonlinear ? nullptr : zpsi.p, &pset, dflag);
+                    disable_nonlinear ? nullptr : zpsi.p, &pset, dflag, !disable_nonlinear);
         c.mark("H_rhs_combine");
         if (!disable_nonlinear) {
             zp_head = out;

@@ -80,6 +80,7 @@ struct GemmPlan {
 };
 
 struct OzPipe;
+struct EigRhs;
 
 class Pipeline {
 public:
@@ -112,7 +113,7 @@ public:
     const double* const* eig_rt(DevSet& set);
     void eigen_rhs(DevSet& set, int ntensor, const double* const* s0, const double* const* s1, const double* w, int nsrc,
                    double factor, double* out0, double* out1, double* outp = nullptr,
-                   DevSet* pset = nullptr, int* flag = nullptr);
+                   DevSet* pset = nullptr, int* flag = nullptr, bool panels = false);
     void eigen_back(DevSet& set, int ntensor, const double* z0, const double* z1, double* out0, double* out1);
     void to_eigen(DevSet& pset, const double* u, double* z);
     void poisson(const double* f, double w, double* u);  // u = Poisson3D(w * f), half mode
@@ -181,6 +182,9 @@ struct OzPipe {
     // each returns false when the stage is not available (size, first build during a graph capture):
     // the caller then runs its FP64 DMMA plan
     bool ysynth(int ntensor, const double* const* z, double* const* outS, double* const* outD);
+    // the NS step's RHS pass writes the back transform's A panels itself (EigRhs::pan): fill the targets of
+    // ysynth's split plan for (z0, z1, z2) if it exists; ysynth then skips that split
+    bool rhs_panels(const double* z0, const double* z1, const double* z2, EigRhs& a);
     bool rsynth(double* const (&Z)[2][3], double* const* val);
     bool analyze(double* const* av, double* const* Y, double* lam_n, double* gam_n);
 
@@ -198,6 +202,7 @@ private:
     const DevSet* const_set_ = nullptr;
     DBuf cpan_, csc_, cpe_, ysp_, ysc_, rsp_, rsc_, rpe_, zap_, zasc_, rap_, rasc_, rape_;
     int syn0_ = 0, ana0_ = 0;
+    std::string rhs_split_;  // the ysynth split key whose panels the last RHS pass wrote
 };
 
 struct NSState {

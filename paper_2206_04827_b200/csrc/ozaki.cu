@@ -15,10 +15,6 @@ namespace {
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
 
-// Exponent of a tile whose largest |value| has the high word hx: e with max|tile| < (hx + 1, 0) <= 2^e, so that
-// max|tile| 2^(47 - e) rounds below 2^47 (no clamp needed; the usual e of max|tile|, one more only when the
-// high-word mantissa is all ones)
-__device__ __forceinline__ int oz_tile_exponent(uint32_t hx) { return hx ? oz_exponent(__hiloint2double(int(hx + 1), 0)) : 0; }
 // Digit d (byte 5 - d of X) of four fixed-point values held as fma(x, 2^(47-e), 1.5 2^52) doubles, packed into one
 // word (value u in byte u): X bytes 0-3 are the low word, bytes 4-5 the low half of the high word
 __device__ __forceinline__ uint32_t oz_digit_word(const double* xb, int d) {
@@ -43,24 +39,17 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const OzSplitJob* __
     double mx = 0.0;
     const uint32_t off = oz_swz(r, 4 * lane);
     if (nsrc == 1) {  // one pass: the row's values stay in registers
-        const double* src = J.src[0];
+        const double* src = J.src[0] + long(r) * J.ld + 4 * lane;
         const int nrows = J.nrows, ncols = J.ncols;
-        const long ld = J.ld;
         double v[4];
+        if (r < nrows && 4 * lane + 4 <= ncols && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+            const double2 a = __ldg(reinterpret_cast<const double2*>(src)), b = __ldg(reinterpret_cast<const double2*>(src + 2));
+            v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+        } else {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int k = 4 * lane + u;
-            v[u] = (r < nrows && k < ncols) ? __ldg(src + long(r) * ld + k) : 0.0;
-            mx = fmax(mx, fabs(v[u]));
+            for (int u = 0; u < 4; ++u) v[u] = (r < nrows && 4 * lane + u < ncols) ? __ldg(src + u) : 0.0;
         }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        const int e = mx > 0.0 ? oz_exponent(mx) : 0;
-        uint32_t w[kOzS];
-        oz_pack4(v, mx > 0.0 ? ldexp(1.0, 47 - e) : 0.0, w);
-#pragma unroll
-        for (int d = 0; d < kOzS; ++d) *reinterpret_cast<uint32_t*>(J.dst[0] + size_t(d) * J.stride + off) = w[d];
-        if (lane == 0) J.sc[r] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
+        oz_warp_row(v, J.dst[0], J.stride, r, J.sc + r);
         return;
     }
     for (int g = 0; g < nsrc; ++g)

@@ -56,4 +56,46 @@ __device__ __forceinline__ void oz_pack4(const double (&x)[4], double scale, uin
     w[5] = __byte_perm(a, b, 0x5410);  // byte 0
 }
 
+// Clamp-free variant for scales from oz_tile_exponent (|x scale| < 2^47 after rounding by construction)
+__device__ __forceinline__ void oz_pack4_nc(const double (&x)[4], double scale, uint32_t (&w)[kOzS]) {
+    uint32_t lo[4], hi[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const double y = fma(x[u], scale, 6755399441055744.0);
+        lo[u] = uint32_t(__double2loint(y));
+        hi[u] = uint32_t(__double2hiint(y));  // bytes 0-1 = X bytes 4-5 (the magic's low half word is 0)
+    }
+    const uint32_t a = __byte_perm(lo[0], lo[1], 0x5140), b = __byte_perm(lo[2], lo[3], 0x5140);
+    const uint32_t c = __byte_perm(lo[0], lo[1], 0x7362), d = __byte_perm(lo[2], lo[3], 0x7362);
+    const uint32_t e = __byte_perm(hi[0], hi[1], 0x5140), f = __byte_perm(hi[2], hi[3], 0x5140);
+    w[0] = __byte_perm(e, f, 0x7632);
+    w[1] = __byte_perm(e, f, 0x5410);
+    w[2] = __byte_perm(c, d, 0x7632);
+    w[3] = __byte_perm(c, d, 0x5410);
+    w[4] = __byte_perm(a, b, 0x7632);
+    w[5] = __byte_perm(a, b, 0x5410);
+}
+
+// Exponent of a set whose largest |value| has the high word hx: e with max < (hx + 1, 0) <= 2^e, so that
+// max 2^(47 - e) rounds below 2^47 (the usual e of the max; one more only when the high-word mantissa is all ones)
+__device__ __forceinline__ int oz_tile_exponent(uint32_t hx) { return hx ? oz_exponent(__hiloint2double(int(hx + 1), 0)) : 0; }
+
+// One 128-value panel row held by a warp (four values per lane, lane l = reduction bytes 4l .. 4l + 3): digits
+// relative to the row max into the six slices (row r, stride bytes apart), the row scale 2^e (0 for a zero row)
+__device__ __forceinline__ void oz_warp_row(const double (&v)[4], uint8_t* dst, long stride, int r, double* sc) {
+    const int lane = threadIdx.x & 31;
+    uint32_t hx = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) hx = max(hx, uint32_t(__double2hiint(v[u])) & 0x7FFFFFFFu);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) hx = max(hx, __shfl_xor_sync(0xffffffffu, hx, o));
+    const int e = oz_tile_exponent(hx);
+    uint32_t w[kOzS];
+    oz_pack4_nc(v, hx ? ldexp(1.0, 47 - e) : 0.0, w);
+    const uint32_t off = oz_swz(r, 4 * lane);
+#pragma unroll
+    for (int d = 0; d < kOzS; ++d) *reinterpret_cast<uint32_t*>(dst + size_t(d) * stride + off) = w[d];
+    if (lane == 0) *sc = hx ? ldexp(1.0, e) : 0.0;
+}
+
 }  // namespace ccf

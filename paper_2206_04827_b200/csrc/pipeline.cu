@@ -1456,16 +1456,7 @@ __global__ void __launch_bounds__(128) eigen_rhs_pan_kernel(EigRhs a) {
     const long hrows = long(a.ntensor) * a.nslots * 2 * a.M * 2;
     const int ld = 2 * a.Np;
     auto panel_row = [&](const double (&o)[4], int t, long pidx, int i) {  // digits of one panel row
-        double mx = fmax(fmax(fabs(o[0]), fabs(o[1])), fmax(fabs(o[2]), fabs(o[3])));
-#pragma unroll
-        for (int sh = 16; sh; sh >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, sh));
-        const int e = mx > 0.0 ? oz_exponent(mx) : 0;
-        uint32_t w[kOzS];
-        oz_pack4(o, mx > 0.0 ? ldexp(1.0, 47 - e) : 0.0, w);
-        uint8_t* pan = a.pan[t] + pidx * (size_t(kOzS) * 128 * kOzK) + oz_swz(i, 4 * lane);
-#pragma unroll
-        for (int d = 0; d < kOzS; ++d) *reinterpret_cast<uint32_t*>(pan + size_t(d) * 128 * kOzK) = w[d];
-        if (lane == 0) a.psc[t][pidx * 128 + i] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
+        oz_warp_row(o, a.pan[t] + pidx * (size_t(kOzS) * 128 * kOzK), 128 * kOzK, i, a.psc[t] + pidx * 128 + i);
     };
     for (long hr = long(blockIdx.x) * 4 + (threadIdx.x >> 5); hr < hrows; hr += long(gridDim.x) * 4) {
         const int k0 = int(hr & 1);

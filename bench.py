@@ -511,7 +511,9 @@ def main():
             e2e_s = float(t.item())
         e2e_runs.append(e2e_s)
     e2e_s = sorted(e2e_runs)[1]
-    io_bytes = hl.numel() * 16 * 2
+    io_bytes = hl.numel() * 16 * 2  # both fields, full reference layout (the D2H of omega())
+    # the H2D of a Hermitian (half-mode) input copies only the slices it reads: l = 0 and l >= p/2 (Ctx::load_coeff)
+    h2d_bytes = io_bytes * (1 + p // 2) / p
     status_bytes = 4 * 4 + 4  # per step: ADI error words + non-finite flag (ccf_ns_step)
 
     sec = None
@@ -534,7 +536,7 @@ def main():
             "init_vmax_scaled_from": vmax, "cuda_graphs": not args.no_graphs,
             "parallelism_run": f"modes{world}" if sharded else ("replica" if world > 1 else "single"),
             "clocks": clk,
-            "e2e": {"value": jobs * KE / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": io_bytes / KE,
+            "e2e": {"value": jobs * KE / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": h2d_bytes / KE,
                     "d2h_bytes_per_step": io_bytes / KE + status_bytes, "steps": KE,
                     "runs_steps_per_s": [jobs * KE / x for x in e2e_runs], "of_runs": "median",
                     "what": "fresh NSStepper from pinned host omega (H2D) -> KE single-step C-ABI calls incl. the "

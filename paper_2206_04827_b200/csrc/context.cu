@@ -315,7 +315,14 @@ void Ctx::load_coeff(const double* ref, double* dst, bool full, int cls, int slo
     const double* dref = ref;
     if (!is_device_ptr(ref)) {
         if (stage_in[slot].n < size_t(nref)) stage_in[slot].alloc(size_t(nref));
-        CCF_CUDA(cudaMemcpyAsync(stage_in[slot].p, ref, sizeof(double) * nref, cudaMemcpyHostToDevice, stream));
+        if (full) {
+            CCF_CUDA(cudaMemcpyAsync(stage_in[slot].p, ref, sizeof(double) * nref, cudaMemcpyHostToDevice, stream));
+        } else {  // the half spectrum reads only slices l = 0 (Nyquist) and l >= p/2 (w >= 0): copy just those
+            const long sl = 2L * n * m;
+            CCF_CUDA(cudaMemcpyAsync(stage_in[slot].p, ref, sizeof(double) * sl, cudaMemcpyHostToDevice, stream));
+            CCF_CUDA(cudaMemcpyAsync(stage_in[slot].p + sl * (p / 2), ref + sl * (p / 2), sizeof(double) * sl * (p - p / 2),
+                                     cudaMemcpyHostToDevice, stream));
+        }
         dref = stage_in[slot].p;
     }
     const Geo& g = geo(full);

@@ -198,7 +198,7 @@ bool OzPipe::ysynth(int ntensor, const double* const* z, double* const* outS, do
     P.c.mark("H_z_split");
     gp->gemm.launch(P.c.stream);
     P.c.gemm_flops += gp->gemm.flops;
-    P.c.launches += 2;
+    P.c.launches += written ? 1 : 2;
     for (int t = 0; t < ntensor; ++t) {  // these tensors now exist as panels only (rsynth reads them)
         if (outS[t]) panel_only_.insert(outS[t]);
         if (outD[t]) panel_only_.insert(outD[t]);

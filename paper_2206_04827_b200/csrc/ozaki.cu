@@ -589,26 +589,33 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
         const uint32_t tq = tmem + (uint32_t(q * 32) << 16) + uint32_t(half * kCols);
         uint32_t g = 0, ic = 0, ipar = 0;
         // a term's row factor (A row scale x the B plane's tile normalisation), loaded one term ahead
-        auto tfac = [&](int t, int n0) {
-            const double* sap = terms[t].sa;
-            const int* pep = terms[t].pe;
-            return __ldg(sap + row) * (pep ? ldexp(1.0, __ldg(pep + n0 / 128)) : 1.0);
-        };
-        int nt0 = 0, nt1 = 0, nn0 = 0;  // the next item's terms and first column
-        if (int(blockIdx.x) < nitems) {
-            nt0 = items[blockIdx.x].t0;
-            nt1 = items[blockIdx.x].t1;
-            nn0 = items[blockIdx.x].n0;
-        }
-        double fnext = nt1 > nt0 ? tfac(nt0, nn0) : 0.0;
-        for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++ic) {
-            const int t0 = nt0, t1 = nt1, n0 = nn0;
-            const int itn = it + int(gridDim.x);
-            if (itn < nitems) {
-                nt0 = items[itn].t0;
-                nt1 = items[itn].t1;
-                nn0 = items[itn].n0;
+        // The row factor of a term (A row scale x the B plane's tile normalisation) is prefetched in two
+        // stages, a term ahead, so no dependent global load stalls the drains: the next term's pointers at
+        // the start of a term, their values after its first drain. Item headers are loaded two items ahead.
+        auto hdr = [&](int i, int& a, int& b, int& c) {
+            if (i < nitems) {
+                a = items[i].t0;
+                b = items[i].t1;
+                c = items[i].n0;
+            } else {
+                a = b = c = 0;
             }
+        };
+        int h1t0, h1t1, h1n0, h2t0, h2t1, h2n0;  // the next item's and the one after's headers
+        hdr(int(blockIdx.x), h1t0, h1t1, h1n0);
+        hdr(int(blockIdx.x + gridDim.x), h2t0, h2t1, h2n0);
+        double fnext = 0.0;
+        if (h1t1 > h1t0) {
+            const double* sap = terms[h1t0].sa;
+            const int* pep = terms[h1t0].pe;
+            fnext = __ldg(sap + row) * (pep ? ldexp(1.0, __ldg(pep + h1n0 / 128)) : 1.0);
+        }
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++ic) {
+            const int t0 = h1t0, t1 = h1t1, n0 = h1n0;
+            h1t0 = h2t0;
+            h1t1 = h2t1;
+            h1n0 = h2n0;
+            hdr(it + 2 * int(gridDim.x), h2t0, h2t1, h2n0);
             const uint32_t k = ic & 1;
             const uint8_t* slot = islot + k * kItemSlot;
             double acc[kCols];
@@ -616,14 +623,16 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
             for (int j = 0; j < kCols; ++j) acc[j] = 0.0;
             for (int t = t0; t < t1; ++t) {
                 const double sa = fnext;
-                if (t + 1 < t1)
-                    fnext = tfac(t + 1, n0);
-                else if (itn < nitems && nt1 > nt0)
-                    fnext = tfac(nt0, nn0);
-                // levels arrive 6 .. 0 and are drained three at a time, (6, 5, 4), (3, 2, 1), (0): the int32 levels
-                // combine exactly into y = P_(L-2) 2^16 + P_(L-1) 2^8 + P_L (|y| < 2^42), converted with one 64-bit
-                // bit trick and accumulated with the weight 2^-(14 + 8L) x row scale: two FP64 instructions per
-                // element and drain (6 per term)
+                // the next term: t + 1 of this item, else the next item's first (if it has terms)
+                const bool inner = t + 1 < t1;
+                const int nx = inner ? t + 1 : (h1t1 > h1t0 ? h1t0 : -1);
+                const int nxn0 = inner ? n0 : h1n0;
+                const double* nsap = nullptr;
+                const int* npep = nullptr;
+                if (nx >= 0) {  // stage 1: pointers
+                    nsap = terms[nx].sa;
+                    npep = terms[nx].pe;
+                }
                 auto drain = [&](int L, int nl) {
                     const uint32_t sl0 = g % kSlots, sl1 = (g + 1) % kSlots, sl2 = (g + 2) % kSlots;
                     mbar_wait(&bar.accfull[sl0], (g / kSlots) & 1);
@@ -667,6 +676,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                     g += nl;
                 };
                 drain(6, 3);
+                if (nx >= 0) fnext = __ldg(nsap + row) * (npep ? ldexp(1.0, __ldg(npep + nxn0 / 128)) : 1.0);  // stage 2
                 drain(3, 3);
                 drain(0, 1);
             }

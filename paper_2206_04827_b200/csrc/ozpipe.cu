@@ -237,10 +237,13 @@ bool OzPipe::rsynth(double* const (&Z)[2][3], double* const* val) {
     Stage* sp = stage(key_of("rs", {Z[0][0], Z[0][1], Z[0][2], Z[1][0], Z[1][1], Z[1][2], val[0], val[3]}), fresh);
     if (!sp) throw Error(INTERNAL, "OzPipe: X1 plan first built during a graph capture");
     if (fresh) {
-        for (int pr = 0; pr < 2; ++pr)
-            for (int s = s_lo; s < s_hi; ++s)
-                for (int o = 0; o < 6; ++o)
-                    for (int nt = 0; nt < 2; ++nt) {
+        // item order (s, o, nt, pr): the four items that read one composite block (and the items that read
+        // one input panel) are adjacent, so they run concurrently on neighbouring CTAs and share it through L2;
+        // the kernel's upload() only regroups them by term count (stable)
+        for (int s = s_lo; s < s_hi; ++s)
+            for (int o = 0; o < 6; ++o)
+                for (int nt = 0; nt < 2; ++nt)
+                    for (int pr = 0; pr < 2; ++pr) {
                         const int t0 = int(sp->gemm.terms.size());
                         for (const CompositeTerm& ct : P.synth_.terms[size_t(s)]) {
                             if (ct.out != o) continue;

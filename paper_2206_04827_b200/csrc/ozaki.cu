@@ -411,7 +411,7 @@ __device__ __forceinline__ int oz_digit_at(int i) { return i == kOzS - 1 ? 0 : k
 struct OzBars {
     uint64_t full[kBufs], empty[kBufs], accfull[kSlots], accempty[kSlots];
     uint64_t sbfull[2], sbempty[2];  // column scales of the tiles in flight (two slots)
-    double red[2][16];         // per-warp tile maxima (panel outputs), double-buffered by item parity
+    alignas(16) double red[2][16];  // per-warp tile maxima (panel outputs, read as uint4), double-buffered by item parity
     uint32_t tmem_base;
 };
 constexpr size_t kSbBytes = 128 * sizeof(double);

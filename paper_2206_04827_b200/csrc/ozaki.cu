@@ -27,53 +27,23 @@ __device__ __forceinline__ uint32_t oz_digit_word(const double* xb, int d) {
     return __byte_perm(__byte_perm(w[0], w[1], sel), __byte_perm(w[2], w[3], sel), 0x5410);
 }
 
-// A-side split: one warp per panel row, lane l holds reduction indices 4l .. 4l + 3. A job with several sources
-// splits them with ONE scale per row (the max over the sources): the constant operator blocks that feed one output
-// of a composite product share their row scales, so that output's terms can be summed in one accumulator.
+// A-side split: one warp per panel row, lane l holds reduction indices 4l .. 4l + 3 (oz_warp_row)
 __global__ void __launch_bounds__(256) oz_split_rows_kernel(const OzSplitJob* __restrict__ jobs) {
     const OzSplitJob& J = jobs[blockIdx.y];
     const int lane = threadIdx.x & 31;
     const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (r >= J.rows_pad) return;
-    const int nsrc = J.nsrc;
-    double mx = 0.0;
-    const uint32_t off = oz_swz(r, 4 * lane);
-    if (nsrc == 1) {  // one pass: the row's values stay in registers
-        const double* src = J.src[0] + long(r) * J.ld + 4 * lane;
-        const int nrows = J.nrows, ncols = J.ncols;
-        double v[4];
-        if (r < nrows && 4 * lane + 4 <= ncols && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-            const double2 a = __ldg(reinterpret_cast<const double2*>(src)), b = __ldg(reinterpret_cast<const double2*>(src + 2));
-            v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
-        } else {
+    const double* src = J.src[0] + long(r) * J.ld + 4 * lane;
+    const int nrows = J.nrows, ncols = J.ncols;
+    double v[4];
+    if (r < nrows && 4 * lane + 4 <= ncols && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(src)), b = __ldg(reinterpret_cast<const double2*>(src + 2));
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    } else {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = (r < nrows && 4 * lane + u < ncols) ? __ldg(src + u) : 0.0;
-        }
-        oz_warp_row(v, J.dst[0], J.stride, r, J.sc + r);
-        return;
+        for (int u = 0; u < 4; ++u) v[u] = (r < nrows && 4 * lane + u < ncols) ? __ldg(src + u) : 0.0;
     }
-    for (int g = 0; g < nsrc; ++g)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int k = 4 * lane + u;
-            mx = fmax(mx, (r < J.nrows && k < J.ncols) ? fabs(__ldg(J.src[g] + long(r) * J.ld + k)) : 0.0);
-        }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const int e = mx > 0.0 ? oz_exponent(mx) : 0;
-    for (int g = 0; g < nsrc; ++g) {
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int k = 4 * lane + u;
-            v[u] = (r < J.nrows && k < J.ncols) ? __ldg(J.src[g] + long(r) * J.ld + k) : 0.0;
-        }
-        uint32_t w[kOzS];
-        oz_pack4(v, mx > 0.0 ? ldexp(1.0, 47 - e) : 0.0, w);
-#pragma unroll
-        for (int d = 0; d < kOzS; ++d) *reinterpret_cast<uint32_t*>(J.dst[g] + size_t(d) * J.stride + off) = w[d];
-    }
-    if (lane == 0) J.sc[r] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
+    oz_warp_row(v, J.dst[0], J.stride, r, J.sc + r);
 }
 
 // B-side split with transpose: CTA = (job, 128-row tile of the panel), thread = panel row = source
@@ -794,7 +764,7 @@ void OzSplitPlan::upload() {
     maxrows = 0;
     for (const OzSplitJob& j : jobs) {
         if (j.ncols > kOzK || j.nrows > j.rows_pad || j.rows_pad % 8 || j.nsrc < 1 || j.nsrc > kOzGroup ||
-            ((transpose || mn) && j.rows_pad % 128))
+            (!transpose && !mn && j.nsrc != 1) || ((transpose || mn) && j.rows_pad % 128))
             throw Error(INTERNAL, "OzSplitPlan: bad job shape");
         maxrows = std::max(maxrows, j.rows_pad);
     }

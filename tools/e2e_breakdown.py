@@ -22,6 +22,8 @@ def main():
     torch.cuda.synchronize()
     hl = torch.from_numpy(np.ascontiguousarray(wl)).pin_memory()
     hg = torch.from_numpy(np.ascontiguousarray(wg)).pin_memory()
+    pl = torch.empty_like(hl).pin_memory()
+    pg = torch.empty_like(hg).pin_memory()
     for rep in range(2):
         t0 = time.perf_counter()
         s2 = P.NSStepper(ctx, hl.numpy(), hg.numpy(), reynolds=cfg["reynolds"], h=cfg["h"], order=4)
@@ -33,7 +35,7 @@ def main():
         t2 = time.perf_counter()
         s2.step(40)
         torch.cuda.synchronize(); t3 = time.perf_counter()
-        ol, og = s2.omega()
+        ol, og = s2.omega(pl.numpy(), pg.numpy())
         t4 = time.perf_counter()
         print(f"rep {rep}: create {1e3*(t1-t0):.1f} ms, first 10 steps {1e3*(t2-t1):.1f} ms, next 40 {1e3*(t3-t2):.1f} ms, omega D2H {1e3*(t4-t3):.1f} ms", flush=True)
         s2.close()

@@ -405,6 +405,9 @@ static_assert(sizeof(OzItem) + sizeof(int) <= 128 && sizeof(OzItem) % 16 == 0, "
 // another one, as that product's MN-major B panel tile (digits relative to the tile max, CTA-wide).
 // N = 128 per instruction keeps the tensor pipe at ~4 POPS (N = 64 costs ~60 cycles per instruction,
 // tools/microbench/i8mma.cu).
+// D4: the first drain of a term takes levels 6..3 at once (fewer conversions; the MMA cannot run ahead during
+// it): faster for single-term items, slower for multi-term ones, so the plan picks it
+template <bool D4>
 __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __restrict__ terms,
                                                               const OzItem* __restrict__ items, int nitems, int mode,
                                                               int bmn) {
@@ -645,10 +648,52 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                     }
                     g += nl;
                 };
-                drain(6, 3);
-                if (nx >= 0) fnext = __ldg(nsap + row) * (npep ? ldexp(1.0, __ldg(npep + nxn0 / 128)) : 1.0);  // stage 2
-                drain(3, 3);
-                drain(0, 1);
+                // levels 6, 5, 4, 3 in one drain: y = P3 2^24 + P4 2^16 + P5 2^8 + P6 (|y| < 2^51), 4-column chunks
+                auto drain4 = [&](int L) {
+                    uint32_t sl[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        sl[u] = (g + u) % kSlots;
+                        mbar_wait(&bar.accfull[sl[u]], ((g + u) / kSlots) & 1);
+                    }
+                    tc_after();
+                    if (!(mode & 1)) {
+                        const double f = sa * ldexp(1.0, -14 - 8 * L);
+#pragma unroll
+                        for (int c = 0; c < kCols / 4; ++c) {
+                            uint32_t v[4][4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                                             : "=r"(v[u][0]), "=r"(v[u][1]), "=r"(v[u][2]), "=r"(v[u][3])
+                                             : "r"(tq + sl[u] * 128 + uint32_t(c * 4)));
+                            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const long long y = (long long)int(v[3][j]) * 16777216 + (long long)int(v[2][j]) * 65536 +
+                                                    (long long)int(v[1][j]) * 256 + int(v[0][j]);
+                                const double x = __hiloint2double(int(uint32_t(y >> 32) + 0x43380000u), int(uint32_t(y))) -
+                                                 6755399441055744.0;
+                                acc[c * 4 + j] = fma(x, f, acc[c * 4 + j]);
+                            }
+                        }
+                    }
+                    tc_before();
+                    __syncwarp();
+                    if (lane == 0)
+                        for (int u = 0; u < 4; ++u) mbar_arrive(&bar.accempty[sl[u]]);
+                    g += 4;
+                };
+                if (D4) {
+                    drain4(6);
+                    if (nx >= 0) fnext = __ldg(nsap + row) * (npep ? ldexp(1.0, __ldg(npep + nxn0 / 128)) : 1.0);  // stage 2
+                    drain(2, 3);
+                } else {
+                    drain(6, 3);
+                    if (nx >= 0) fnext = __ldg(nsap + row) * (npep ? ldexp(1.0, __ldg(npep + nxn0 / 128)) : 1.0);  // stage 2
+                    drain(3, 3);
+                    drain(0, 1);
+                }
             }
             if (warp == kCtlWarps && lane == 0) OZ_TRACE(3584 + (it - blockIdx.x) / gridDim.x);
             mbar_wait(&bar.sbfull[k], (ic >> 1) & 1);  // the item slot: the item and its column scales
@@ -820,6 +865,7 @@ void OzGemmPlan::upload() {
             throw Error(INTERNAL, "OzGemmPlan: bad item");
         flops += 2.0 * it.m * it.n * kOzK * (it.t1 - it.t0);
     }
+    single_term = std::all_of(items.begin(), items.end(), [](const OzItem& x) { return x.t1 - x.t0 <= 1; });
     // long items first (persistent round-robin assignment)
     std::stable_sort(items.begin(), items.end(), [](const OzItem& x, const OzItem& y) { return x.t1 - x.t0 > y.t1 - y.t0; });
     if (terms.empty() || items.empty()) return;
@@ -836,13 +882,17 @@ void OzGemmPlan::launch(cudaStream_t s) const {
         int dev = 0;
         CCF_CUDA(cudaGetDevice(&dev));
         CCF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        CCF_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(oz_smem_bytes())));
+        CCF_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(oz_smem_bytes())));
+        CCF_CUDA(cudaFuncSetAttribute(oz_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(oz_smem_bytes())));
     }
     const unsigned grid = unsigned(std::min<size_t>(items.size(), size_t(nsm)));
     static const int mode0 = std::getenv("CCF_OZ_MODE") ? std::atoi(std::getenv("CCF_OZ_MODE")) : 0;  // diagnostics
     static const char* trace_tag = std::getenv("CCF_OZ_TRACE");  // trace (mode bit 2) only the plan with this tag
     const int mode = (trace_tag && tag && std::strcmp(trace_tag, tag) != 0) ? (mode0 & ~4) : mode0;
-    oz_gemm_kernel<<<grid, kThreads, oz_smem_bytes(), s>>>(dterms, ditems, int(items.size()), mode, int(b_mn));
+    if (single_term)
+        oz_gemm_kernel<true><<<grid, kThreads, oz_smem_bytes(), s>>>(dterms, ditems, int(items.size()), mode, int(b_mn));
+    else
+        oz_gemm_kernel<false><<<grid, kThreads, oz_smem_bytes(), s>>>(dterms, ditems, int(items.size()), mode, int(b_mn));
     CCF_CUDA(cudaGetLastError());
 }
 

@@ -112,6 +112,7 @@ struct OzGemmPlan {
     OzItem* ditems = nullptr;
     double flops = 0.0;  // FP64-equivalent 2 M N K per term and tile
     bool b_mn = false;   // B panels in the MN-major layout (OzSplitPlan::mn)
+    bool single_term = false;  // (set by upload: every item has at most one term -> the 4-level first drain)
     const char* tag = nullptr;  // diagnostics label (CCF_OZ_TRACE)
     void upload();
     void launch(cudaStream_t s) const;

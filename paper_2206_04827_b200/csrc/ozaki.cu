@@ -577,11 +577,15 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
         int h1t0, h1t1, h1n0, h2t0, h2t1, h2n0;  // the next item's and the one after's headers
         hdr(int(blockIdx.x), h1t0, h1t1, h1n0);
         hdr(int(blockIdx.x + gridDim.x), h2t0, h2t1, h2n0);
-        double fnext = 0.0;
+        // raw next-term factor: the A row scale and the B plane exponent, combined only when the term starts
+        // (the power of two by integer ops), so the loads never stall the drains they overlap
+        double fsa = 0.0;
+        int fpe = 0;
         if (h1t1 > h1t0) {
             const double* sap = terms[h1t0].sa;
             const int* pep = terms[h1t0].pe;
-            fnext = __ldg(sap + row) * (pep ? ldexp(1.0, __ldg(pep + h1n0 / 128)) : 1.0);
+            fsa = __ldg(sap + row);
+            fpe = pep ? __ldg(pep + h1n0 / 128) : 0;
         }
         for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++ic) {
             const int t0 = h1t0, t1 = h1t1, n0 = h1n0;
@@ -595,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
 #pragma unroll
             for (int j = 0; j < kCols; ++j) acc[j] = 0.0;
             for (int t = t0; t < t1; ++t) {
-                const double sa = fnext;
+                const double sa = fsa * __longlong_as_double((long long)(fpe + 1023) << 52);
                 // the next term: t + 1 of this item, else the next item's first (if it has terms)
                 const bool inner = t + 1 < t1;
                 const int nx = inner ? t + 1 : (h1t1 > h1t0 ? h1t0 : -1);
@@ -686,11 +690,17 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                 };
                 if (D4) {
                     drain4(6);
-                    if (nx >= 0) fnext = __ldg(nsap + row) * (npep ? ldexp(1.0, __ldg(npep + nxn0 / 128)) : 1.0);  // stage 2
+                    if (nx >= 0) {  // stage 2
+                        fsa = __ldg(nsap + row);
+                        fpe = npep ? __ldg(npep + nxn0 / 128) : 0;
+                    }
                     drain(2, 3);
                 } else {
                     drain(6, 3);
-                    if (nx >= 0) fnext = __ldg(nsap + row) * (npep ? ldexp(1.0, __ldg(npep + nxn0 / 128)) : 1.0);  // stage 2
+                    if (nx >= 0) {  // stage 2
+                        fsa = __ldg(nsap + row);
+                        fpe = npep ? __ldg(npep + nxn0 / 128) : 0;
+                    }
                     drain(3, 3);
                     drain(0, 1);
                 }

@@ -127,6 +127,9 @@ struct ThetaCross {
     int row0, world;
     int sb[9];
     long rdelta[8];
+    // input value layout: 0 = [jr][z] rows (leading dimension n); 1 = column-quad major [z / 4][jr][z % 4], written
+    // by the INT8 X1 product (coalesced epilogue stores; theta_cross256w_kernel only)
+    int vquad;
 };
 // doubles from the local exchange tensors to those of the owner of slot s
 __device__ __forceinline__ long theta_slot_delta(const ThetaCross& t, int s) {

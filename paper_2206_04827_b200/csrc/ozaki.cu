@@ -769,6 +769,20 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                     }
                 }
                 if (threadIdx.x == kEpi0 && I.ppe) *I.ppe = e;
+            } else if (row < I.m && !(mode & 8) && I.cq) {  // column-quad major: lane = row, 1 KB per instruction
+                const long cq = I.cq;
+                double* cb = I.c + long(half * (kCols / 4)) * cq + long(row) * 4;
+                const int nv = I.n - half * kCols;
+#pragma unroll
+                for (int j = 0; j < kCols; j += 4) {
+                    if (j + 4 <= nv)
+                        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(cb + (j / 4) * cq), "d"(acc[j]),
+                                     "d"(acc[j + 1]), "d"(acc[j + 2]), "d"(acc[j + 3])
+                                     : "memory");
+                    else
+                        for (int u = 0; u < 4; ++u)
+                            if (j + u < nv) cb[(j / 4) * cq + u] = acc[j + u];
+                }
             } else if (row < I.m && !(mode & 8)) {
                 double* crow = I.c + long(row) * I.ldc + half * kCols;
                 const int nv = I.n - half * kCols;

@@ -54,6 +54,9 @@ struct alignas(16) OzItem {  // one 128 x 128 output tile; every term of an item
     uint8_t* pdst = nullptr;
     long pstride = 0;
     int* ppe = nullptr;
+    // optional fp64 column-quad-major output: element (row, col) at c + (col / 4) * cq + row * 4 + col % 4
+    // (cq = 4 x rows of the tensor): a warp's store instruction then covers 1 KB contiguous
+    long cq = 0;
 };
 
 // Split jobs: fp64 source -> panel slices + row scales.

@@ -234,7 +234,8 @@ bool OzPipe::rsynth(double* const (&Z)[2][3], double* const* val) {
     const int mh = g.mh;
     const int s_lo = P.c.sh.s_lo, s_hi = P.c.sh.s_hi;
     bool fresh;
-    Stage* sp = stage(key_of("rs", {Z[0][0], Z[0][1], Z[0][2], Z[1][0], Z[1][1], Z[1][2], val[0], val[3]}), fresh);
+    const bool quad = P.theta_quad_ok();  // (the pipeline passes the layout to theta_cross)
+    Stage* sp = stage(key_of(quad ? "rsq" : "rs", {Z[0][0], Z[0][1], Z[0][2], Z[1][0], Z[1][1], Z[1][2], val[0], val[3]}), fresh);
     if (!sp) throw Error(INTERNAL, "OzPipe: X1 plan first built during a graph capture");
     if (fresh) {
         // item order (s, o, nt, pr): the four items that read one composite block (and the items that read
@@ -255,9 +256,13 @@ bool OzPipe::rsynth(double* const (&Z)[2][3], double* const* val) {
                         }
                         // (an output no block feeds is an item without terms: the kernel stores zeros)
                         const int t1 = int(sp->gemm.terms.size());
-                        sp->gemm.items.push_back({t0, t1, nt * 128, mh, 128,
-                                                  val[3 * pr + o / 2] + long(s) * g.slot_stride + long(o % 2) * g.plane_stride + nt * 128,
-                                                  long(g.n), 1.0});
+                        double* plane = val[3 * pr + o / 2] + long(s) * g.slot_stride + long(o % 2) * g.plane_stride;
+                        OzItem item{t0, t1, nt * 128, mh, 128, plane + nt * 128, long(g.n), 1.0};
+                        if (quad) {  // column-quad-major values for the theta kernel (Pipeline::val_quad_)
+                            item.cq = 4L * mh;
+                            item.c = plane + long(nt * 128 / 4) * item.cq;
+                        }
+                        sp->gemm.items.push_back(item);
                     }
         sp->gemm.b_mn = true;
         sp->gemm.tag = "X1";

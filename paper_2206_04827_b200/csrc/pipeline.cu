@@ -753,6 +753,12 @@ void Pipeline::rz_analyze(int count, const double* const* in, const int* cls, do
     c.launches += 2;
 }
 
+bool Pipeline::theta_quad_ok() const {
+    const char* q = std::getenv("CCF_THETA_VARIANT");
+    const char* e = std::getenv("CCF_THETA_GENERIC");
+    return c.gh.p == 256 && tp.logp >= 0 && !(q && q[0] == '1' && q[1] == '6') && !(e && e[0] == '1');
+}
+
 void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
     const Geo& g = c.gh;
     if (tp.logp < 0) throw Error(DOMAIN_ERROR, "ccf: the fused theta kernel needs p to be a power of two");
@@ -765,6 +771,8 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
     t.tj = tj;
     for (int i = 0; i < 6; ++i) t.in[i] = v6[i];
     for (int i = 0; i < 3; ++i) t.out[i] = a3[i];
+    t.vquad = val_quad_ ? 1 : 0;
+    val_quad_ = false;
     t.tw = reinterpret_cast<const double2*>(tp.tw.p);
     // mode sharding: this rank's rows of every slot, each slot in its owner's exchange buffer
     const Shard& sh = c.sh;
@@ -793,6 +801,8 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
     }
     if (sh.sharded() && g.p == 256 && !theta_generic_ && !theta_w_)
         throw Error(CONFIG_ERROR, "theta: the 16-thread variant (CCF_THETA_VARIANT=16) has no sharded form");
+    if (t.vquad && !(g.p == 256 && !theta_generic_ && theta_w_))
+        throw Error(INTERNAL, "theta: column-quad-major inputs need the warp-per-point p = 256 kernel");
     if (g.p == 256 && !theta_generic_ && theta_w_) {
         const int np = 2 * theta_nq_;
         const dim3 grid(unsigned((g.nh + np - 1) / np), rows);
@@ -1008,6 +1018,7 @@ void Pipeline::nonlinear(const double* lam_v, const double* gam_v, const double*
     // eigY: the z tensors are Y = Z (QR S_z) in eigen coordinates along r, the synthesis blocks carry QL
     const int ycls[8] = {int(eigY), 0, 0, 0, 0, 0, 0, 0};
     const bool oz_rs = eigY && oz().rsynth(Z, val);  // INT8 tensor cores (ozpipe.cu)
+    val_quad_ = oz_rs && theta_quad_ok();             // (rsynth writes that layout exactly then)
     if (!oz_rs) {
     GemmPlan& rs = gemm(ptr_key(eigY ? "nrsY" : "nrs", 4, keyp, keyp, ycls), fresh);  // outputs: scratch
     if (fresh) {

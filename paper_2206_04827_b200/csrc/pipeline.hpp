@@ -97,6 +97,9 @@ public:
     void rz_synth(int count, const double* const* in, const int* cls, double* const* out);
     void rz_analyze(int count, const double* const* in, const int* cls, double* const* out);
     void theta_cross(const double* const* v6, double* const* a3);
+    // the warp-per-point p = 256 theta kernel will run (the only one reading column-quad-major values)
+    bool theta_quad_ok() const;
+    bool val_quad_ = false;  // the theta inputs in the next theta_cross are column-quad major (OzPipe::rsynth)
     void curl_decompose(const double* ar, const double* at, const double* az, double* out_r, double* out_t,
                         double* out_z, double* lam, double* gam);
     // eig != nullptr: output N~ = PL_P N PR in the eigen layout of that (Poisson) set's modal basis

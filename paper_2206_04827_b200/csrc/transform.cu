@@ -954,6 +954,7 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
     double2* Z = sd + pt * 2 * kTWArr;  // this point's two arrays
     double2 tv[3][8];                   // time samples of the three pairs at l = col + 16 (2j + h)
     const long ps = g.plane_stride, oo = g.nh;
+    const long ooi = t.vquad ? long(g.nh) * g.mh : long(g.nh);  // odd-z half of the inputs
     // raw spectra of one (v, w) pair for task a = (slot a / NQ, position pair a % NQ), prefetched into
     // registers one pair ahead so the global-load latency overlaps the previous pair's FFTs (tasks
     // beyond the thread count, i.e. the Nyquist slot, are loaded in place)
@@ -968,11 +969,14 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
         const int nq = min(2, npos - 2 * q);
         if (nq <= 0) return;
         const bool vec = even && nq == 2;
-        const long off = long(s) * g.slot_stride + long(jr) * g.n + i0 + 2 * q + theta_slot_delta(t, s);
+        const int z = i0 + 2 * q;
+        const long off = long(s) * g.slot_stride +
+                         (t.vquad ? long(z >> 2) * 4 * g.mh + long(jr) * 4 + (z & 3) : long(jr) * g.n + z) +
+                         theta_slot_delta(t, s);
         const double* __restrict__ fa = t.in[2 * pr] + off;
         const double* __restrict__ fb = t.in[2 * pr + 1] + off;
         if (vec) {  // both z positions: 16-byte loads
-            const double* src[8] = {fa, fa + ps, fa + oo, fa + oo + ps, fb, fb + ps, fb + oo, fb + oo + ps};
+            const double* src[8] = {fa, fa + ps, fa + ooi, fa + ooi + ps, fb, fb + ps, fb + ooi, fb + ooi + ps};
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const double2 v = __ldg(reinterpret_cast<const double2*>(src[u]));
@@ -986,12 +990,12 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
             if (ip >= nq) continue;
             r[ip][0] = __ldg(fa + ip);
             r[ip][1] = __ldg(fa + ps + ip);
-            r[ip][2] = __ldg(fa + oo + ip);
-            r[ip][3] = __ldg(fa + oo + ps + ip);
+            r[ip][2] = __ldg(fa + ooi + ip);
+            r[ip][3] = __ldg(fa + ooi + ps + ip);
             r[ip][4] = __ldg(fb + ip);
             r[ip][5] = __ldg(fb + ps + ip);
-            r[ip][6] = __ldg(fb + oo + ip);
-            r[ip][7] = __ldg(fb + oo + ps + ip);
+            r[ip][6] = __ldg(fb + ooi + ip);
+            r[ip][7] = __ldg(fb + ooi + ps + ip);
         }
     };
     auto put_slot = [&](int a, const double (&r)[2][8], int arr) {

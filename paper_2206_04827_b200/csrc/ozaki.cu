@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kMnThreads) oz_split_mn_kernel(const OzSplitJo
         const int k = wid * 8 + i;
         uint32_t w[kOzS];
         oz_pack4(v[i], scale, w);
-        const uint32_t off = oz_swz(k, 4 * lane);
+        const uint32_t off = oz_mn32(k, 4 * lane);
 #pragma unroll
         for (int d = 0; d < kOzS; ++d) *reinterpret_cast<uint32_t*>(dst + size_t(d) * J.stride + off) = w[d];
     }
@@ -352,25 +352,31 @@ __device__ __forceinline__ unsigned long long oz_now() {
 // word (SBO 1024 B, sm_100 version 1, layout 2) is the same for every operand slice
 __device__ __forceinline__ uint32_t sdesc_lo(uint32_t saddr) { return ((saddr >> 4) & 0x3FFFu) | (1u << 16); }
 constexpr uint32_t kDescHi = (1024u >> 4) | (1u << 14) | (2u << 29);
-__device__ __forceinline__ void mma_i8_lo(uint32_t tmem_d, uint32_t alo, uint32_t blo, uint32_t idesc, uint32_t acc) {
+// MN-major B panels (oz_mn32): SWIZZLE_32B, LBO 4096 B between column quarters, SBO 256 B between 8-row atoms
+constexpr uint32_t kDescHiMn = (256u >> 4) | (1u << 14) | (6u << 29);
+constexpr uint32_t kLboMn = (4096u >> 4) << 16;
+__device__ __forceinline__ uint32_t sdesc_lo_mn(uint32_t saddr) { return ((saddr >> 4) & 0x3FFFu) | kLboMn; }
+__device__ __forceinline__ void mma_i8_lo(uint32_t tmem_d, uint32_t alo, uint32_t blo, uint32_t bhi, uint32_t idesc,
+                                          uint32_t acc) {
     asm volatile(
         "{\n.reg .b64 ad, bd;\n.reg .pred p;\n"
-        "mov.b64 ad, {%1, %5};\nmov.b64 bd, {%2, %5};\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], ad, bd, %3, p;\n}\n" ::"r"(tmem_d),
-        "r"(alo), "r"(blo), "r"(idesc), "r"(acc), "n"(kDescHi));
+        "mov.b64 ad, {%1, %6};\nmov.b64 bd, {%2, %3};\nsetp.ne.b32 p, %5, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], ad, bd, %4, p;\n}\n" ::"r"(tmem_d),
+        "r"(alo), "r"(blo), "r"(bhi), "r"(idesc), "r"(acc), "n"(kDescHi));
 }
 // the products of level L: pairs (d, L - d), 4 K-steps each, straight-line (descriptors precomputed per term)
 template <int L>
 __device__ __forceinline__ void oz_issue_level(uint32_t acc, const uint32_t (&alo)[kOzS], const uint32_t (&blo)[kOzS], int bmn) {
     constexpr int d0 = L > kOzS - 1 ? L - (kOzS - 1) : 0, d1 = L < kOzS - 1 ? L : kOzS - 1;
-    const uint32_t bstep = bmn ? 256u : 2u;  // 32 k-rows (MN-major) or 32 bytes, >> 4
+    const uint32_t bstep = bmn ? 64u : 2u;  // 32 k-rows of 32 B (MN-major, 32B swizzle) or 32 bytes, >> 4
     const uint32_t mnbit = bmn ? (1u << 16) : 0u;
+    const uint32_t bhi = bmn ? kDescHiMn : kDescHi;
 #pragma unroll
     for (int d = d0; d <= d1; ++d) {
         const uint32_t id = oz_idesc(d == 0, L - d == 0) | mnbit;
 #pragma unroll
         for (int k = 0; k < kOzK / 32; ++k)
-            mma_i8_lo(acc, alo[d] + 2 * k, blo[L - d] + bstep * k, id, (d == d0 && k == 0) ? 0u : 1u);
+            mma_i8_lo(acc, alo[d] + 2 * k, blo[L - d] + bstep * k, bhi, id, (d == d0 && k == 0) ? 0u : 1u);
     }
 }
 
@@ -520,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                             const uint32_t b = p0 + i >= kBufs ? p0 + i - kBufs : p0 + i;
                             const int d = oz_digit_at(i);
                             alo[d] = sdesc_lo(s0 + b * kPair);
-                            blo[d] = sdesc_lo(s0 + b * kPair + kSlice);
+                            blo[d] = bmn ? sdesc_lo_mn(s0 + b * kPair + kSlice) : sdesc_lo(s0 + b * kPair + kSlice);
                             fb[i] = b;
                             fph[i] = (u0 + (p0 + i >= kBufs ? 1 : 0)) & 1;
                         }
@@ -753,8 +759,8 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                 for (int j = 0; j < kCols; ++j) acc[j] = fma((full || half * kCols + j < I.n) ? acc[j] : 0.0, scale, 6755399441055744.0);
                 // per digit slice: this thread's 32 columns = one 32-byte sector of its 128-byte panel row
                 // (chunks 2i, 2i + 1 of the row swizzle land in one aligned sector), one 256-bit store each
-                const uint32_t off = oz_swz(row, half * kCols) & ~31u;
-                const bool swp = (row & 1) != 0;
+                const uint32_t off = oz_mn32(row, half * kCols) & ~31u;  // 32 rows of a quarter: 1 KB per instruction
+                const bool swp = ((row >> 2) & 1) != 0;
                 if (!(mode & 32)) {
 #pragma unroll
                     for (int d = 0; d < kOzS; ++d) {

@@ -50,7 +50,9 @@ struct alignas(16) OzItem {  // one 128 x 128 output tile; every term of an item
     long ldc;
     double alpha;       // (ignored when the terms carry no column scales: alpha = 1)
     // optional: write the tile (rows = K of the next product, columns = its output columns) as that
-    // product's MN-major B panel tile instead of fp64: slice d at pdst + d * pstride, tile exponent -> *ppe
+    // product's MN-major B panel tile instead of fp64: slice d at pdst + d * pstride, tile exponent -> *ppe.
+    // MN-major slices use the canonical SWIZZLE_32B form (ozaki_dev.cuh oz_mn32): column quarters 4 KB apart,
+    // so a warp of the epilogue (32 rows of one quarter) stores 1 KB contiguous per instruction
     uint8_t* pdst = nullptr;
     long pstride = 0;
     int* ppe = nullptr;

@@ -13,6 +13,14 @@ __host__ __device__ __forceinline__ uint32_t oz_swz(int r, int k) {
     return uint32_t(r >> 3) * 1024u + uint32_t(r & 7) * 128u + ((uint32_t((k >> 4) ^ (r & 7)) << 4) | uint32_t(k & 15));
 }
 
+// byte offset of (k-row k, column byte n) in an MN-major slice of 128 k-rows x 128 columns, laid out as the
+// tcgen05 canonical MN-major SWIZZLE_32B form: four 32-column quarters 4 KB apart (LBO), each 128 rows of 32 bytes
+// (8-row atoms of 256 B, SBO), 16-byte halves swapped on row bit 2. A product epilogue writing a tile as the
+// next product's B operand then stores one contiguous kilobyte per warp instruction (32 rows of one quarter).
+__host__ __device__ __forceinline__ uint32_t oz_mn32(int k, int n) {
+    return uint32_t(n >> 5) * 4096u + uint32_t(k) * 32u + ((uint32_t(((n >> 4) & 1) ^ ((k >> 2) & 1))) << 4) + uint32_t(n & 15);
+}
+
 // ---------------------------------------------------------------- digits
 // s = 2^e with max|row| < s; X = rint(x 2^(47 - e)) in [-2^47, 2^47): 48-bit two's complement,
 // digit 0 = signed top byte, digits 1..5 = unsigned lower bytes (ozaki.hpp)

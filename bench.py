@@ -577,6 +577,11 @@ def main():
                               "note": "product stages at the INT8 tensor peak (DMMA peak on the FP64 path) + theta and "
                                       "RHS-combination passes at HBM peak; hbm_fraction_algorithmic = the BASELINE "
                                       "metric (SURVEY 8d: 43 fields x 8 m n p bytes per step / step time / measured HBM BW)"},
+            # the BASELINE metric's second half ("achieved HBM GB/s fraction"): SURVEY 8d's algorithmic bytes of
+            # one NS step (43 fields x 8 m n p; the per-GPU share when sharded) / step time / measured HBM peak
+            "hbm_fraction": {"value": B_alg / (ms_step * 1e-3) / bw, "algorithmic_bytes_per_step": B_alg,
+                             "achieved_gbs": B_alg / (ms_step * 1e-3) / 1e9, "peak_gbs": peaks["hbm_gbs"],
+                             "peak_source": peaks["hbm_source"]},
             "stage_ms": stages,
             "sharding": ({"mode": "fourier slots x theta rows, NVLink peer exchange (CUDA IPC), " +
                                   f"{barrier_mode} barriers" +

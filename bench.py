@@ -479,6 +479,7 @@ def main():
     if sharded:  # per-rank share of the HBM passes + the theta exchange over NVLink (900 GB/s per direction)
         from paper_2206_04827_b200 import shard as S
         B_other /= world
+        B_alg /= world  # each GPU moves its share of the fields
         nvl = S.exchange_bytes_per_rank(m, n, p, world) / 900e9
     t_tensor = (26.0 * F_gemm / (peaks["int8_tops"] * 1e12)) if ozaki else F_gemm / pdm
     T_roof = t_tensor + B_other / bw + nvl

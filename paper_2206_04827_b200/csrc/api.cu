@@ -1,5 +1,6 @@
 // C-ABI (include/ccf.h) over the B200 CCF context.
 #include <cstring>
+#include <optional>
 #include <set>
 #include <vector>
 
@@ -23,6 +24,13 @@ struct ccf_ctx {
 struct ccf_ns_state {
     ccf_ctx* ctx = nullptr;
     ccf::NSState st;
+    // the history rings live in two arenas from the context's cache (Ctx::arena_get), returned on destroy
+    double* arena[2] = {nullptr, nullptr};
+    size_t arena_n[2] = {0, 0};
+    ~ccf_ns_state() {
+        for (int i = 0; i < 2; ++i)
+            if (arena[i]) cudaFree(arena[i]);  // (detached from a destroyed context; otherwise handed back first)
+    }
 };
 
 using ccf::Ctx;
@@ -489,15 +497,24 @@ ccf_ns_state* ns_create_impl(ccf_ctx* ctx, Ctx& c, double reynolds, double h, in
     s.dealias = dealias;
     s.gamma_psi = gamma_psi;
     const long T = s.pl->T;
-    for (int i = 0; i < 5; ++i) {
-        s.lam[i].alloc(size_t(T));
-        s.gam[i].alloc(size_t(T));
-    }
-    if (!disable_nonlinear)
+    {
+        ccf::SetupTimer tm("NSStepper: ring buffers");
+        const int nt = disable_nonlinear ? 10 : 20;  // lam, gam (+ N~ lam, gam) rings of 5
+        st->arena_n[0] = size_t(nt) * size_t(T);
+        st->arena[0] = c.arena_get(st->arena_n[0]);
+        double* a = st->arena[0];
         for (int i = 0; i < 5; ++i) {
-            s.nl[i].alloc(size_t(T));
-            s.ng[i].alloc(size_t(T));
+            s.lam[i].view(a + size_t(i) * T, size_t(T));
+            s.gam[i].view(a + size_t(5 + i) * T, size_t(T));
         }
+        if (!disable_nonlinear)
+            for (int i = 0; i < 5; ++i) {
+                s.nl[i].view(a + size_t(10 + i) * T, size_t(T));
+                s.ng[i].view(a + size_t(15 + i) * T, size_t(T));
+            }
+    }
+    std::optional<ccf::SetupTimer> tm_phase;  // (CCF_SETUP_TRACE phase timers)
+    tm_phase.emplace("NSStepper: initial data");
     CCF_CUDA(cudaMalloc(&s.dflag, sizeof(int)));
     CCF_CUDA(cudaMemsetAsync(s.dflag, 0, sizeof(int), c.stream));
     if (values) {  // HeatStepper(config, GridField) = HeatStepper(config, analyze(initial))
@@ -509,6 +526,8 @@ ccf_ns_state* ns_create_impl(ccf_ctx* ctx, Ctx& c, double reynolds, double h, in
         c.load_coeff(lam0, s.lam[0].p, false, 0, 0);  // parity projection of the initial data (ptns.cpp:190-191)
     }
     if (gam0) c.load_coeff(gam0, s.gam[0].p, false, 0, 1);
+    if (std::getenv("CCF_SETUP_TRACE")) c.sync();  // (diagnostics: the copies inside the timer)
+    tm_phase.emplace("NSStepper: eigen state");
     // build every solver set the run needs before any graph capture
     ccf::DevSet& pset = c.set(false, true, 1.0);
     for (int b = 1; b <= order; ++b) {
@@ -530,10 +549,13 @@ ccf_ns_state* ns_create_impl(ccf_ctx* ctx, Ctx& c, double reynolds, double h, in
         }
         if (ok) {
             s.eigen = true;
+            st->arena_n[1] = size_t(scalar ? 6 : 11) * size_t(T);  // zl (5), zpsi, zg (5)
+            st->arena[1] = c.arena_get(st->arena_n[1]);
+            double* a = st->arena[1];
+            s.zpsi.view(a, size_t(T));
             for (int i = 0; i < 5; ++i) {
-                s.zl[i].alloc(size_t(T));
-                if (i == 0) s.zpsi.alloc(size_t(T));
-                if (!scalar) s.zg[i].alloc(size_t(T));
+                s.zl[i].view(a + size_t(1 + i) * T, size_t(T));
+                if (!scalar) s.zg[i].view(a + size_t(6 + i) * T, size_t(T));
             }
             P.to_eigen(pset, s.lam[0].p, s.zl[0].p);
             if (!scalar) P.to_eigen(pset, s.gam[0].p, s.zg[0].p);
@@ -732,7 +754,14 @@ ccf_status ccf_shard_set_host_barrier(ccf_ctx* ctx, void (*fn)(void*), void* use
 ccf_status ccf_ns_destroy(ccf_ns_state* st) {
     if (!st) return CCF_OK;
     if (st->ctx) {
-        if (st->ctx->c) cudaSetDevice(st->ctx->c->device);
+        if (st->ctx->c) {
+            cudaSetDevice(st->ctx->c->device);
+            cudaStreamSynchronize(st->ctx->c->stream);  // queued work is done with the arenas before another stepper gets them
+            for (int i = 0; i < 2; ++i) {
+                st->ctx->c->arena_put(st->arena[i], st->arena_n[i]);
+                st->arena[i] = nullptr;
+            }
+        }
         st->ctx->states.erase(st);
     }
     delete st;

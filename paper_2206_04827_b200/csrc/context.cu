@@ -12,7 +12,8 @@
 namespace ccf {
 
 void DBuf::alloc(size_t count) {
-    if (p) cudaFree(p);
+    if (p && own) cudaFree(p);
+    own = true;
     p = nullptr;
     n = count;
     if (count) {
@@ -24,16 +25,24 @@ void DBuf::alloc(size_t count) {
         CCF_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
     }
 }
+void DBuf::view(double* ptr, size_t count) {
+    if (p && own) cudaFree(p);
+    p = ptr;
+    n = count;
+    own = false;
+}
 DBuf::~DBuf() {
-    if (p) cudaFree(p);
+    if (p && own) cudaFree(p);
 }
 DBuf& DBuf::operator=(DBuf&& o) noexcept {
     if (this != &o) {
-        if (p) cudaFree(p);
+        if (p && own) cudaFree(p);
         p = o.p;
         n = o.n;
+        own = o.own;
         o.p = nullptr;
         o.n = 0;
+        o.own = true;
     }
     return *this;
 }
@@ -114,7 +123,26 @@ Ctx::Ctx(int m_, int n_, int p_, int device_, double tol_, int flags_)
     }
 }
 
+double* Ctx::arena_get(size_t count) {
+    double* p = nullptr;
+    for (size_t i = 0; i < arena_cache.size(); ++i)
+        if (arena_cache[i].first == count) {
+            p = arena_cache[i].second;
+            arena_cache.erase(arena_cache.begin() + long(i));
+            break;
+        }
+    if (!p) CCF_CUDA(cudaMalloc(&p, count * sizeof(double)));
+    CCF_CUDA(cudaMemsetAsync(p, 0, count * sizeof(double), stream));
+    return p;
+}
+
+void Ctx::arena_put(double* p, size_t count) {
+    if (p) arena_cache.push_back({count, p});
+}
+
 Ctx::~Ctx() {
+    for (auto& a : arena_cache) cudaFree(a.second);
+    arena_cache.clear();
     shard_close();
     sets.clear();
     cudaFree(ws.res2);

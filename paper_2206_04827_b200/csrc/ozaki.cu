@@ -137,75 +137,6 @@ __global__ void __launch_bounds__(kSplitThreads) oz_split_cols_kernel(const OzSp
     if (rl == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete before exit
 }
 
-// B-side split with transpose and ONE scale per (plane, 128-row tile): CTA = (job, plane, tile). The
-// fp64 tile (K x 128 source columns) is read once into shared memory (coalesced), reduced to its max
-// 2^e (pe[plane * tiles + tile]), and split into digits relative to 2^e, staged as the swizzled
-// panel image and stored with bulk copies. Row scales sc = 1: every column keeps 48 bits relative to
-// the tile max (absolute accuracy 2^-48 of the tile, the max-norm accuracy of the products).
-constexpr int kTileThreads = 256;
-size_t oz_split_tile_smem() { return size_t(128) * 128 * 8 + size_t(kOzS) * 128 * kOzK + 1024; }
-__global__ void __launch_bounds__(kTileThreads) oz_split_tile_kernel(const OzSplitJob* __restrict__ jobs) {
-    extern __shared__ __align__(1024) uint8_t dsm[];
-    uint8_t* stage = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
-    double* tileb = reinterpret_cast<double*>(stage + size_t(kOzS) * 128 * kOzK);  // [128 k][128 c]
-    __shared__ double red[kTileThreads / 32];
-    const OzSplitJob& J = jobs[blockIdx.y / kOzGroup];
-    const int g = blockIdx.y % kOzGroup, tile = blockIdx.x, ntiles = J.rows_pad / 128;
-    if (g >= J.nsrc || tile >= ntiles) return;
-    const int tid = threadIdx.x, c = tid & 127, kh = tid >> 7;
-    const int r = tile * 128 + c;
-    const bool live = r < J.nrows;
-    const int ncols = J.ncols;
-    const double* src = J.src[g] + r;
-    double mx = 0.0;
-#pragma unroll 8
-    for (int i = 0; i < 64; ++i) {
-        const int k = 2 * i + kh;
-        const double x = (live && k < ncols) ? __ldg(src + long(k) * J.ld) : 0.0;
-        tileb[k * 128 + c] = x;
-        mx = fmax(mx, fabs(x));
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((tid & 31) == 0) red[tid >> 5] = mx;
-    __syncthreads();
-    mx = red[0];
-#pragma unroll
-    for (int w = 1; w < kTileThreads / 32; ++w) mx = fmax(mx, red[w]);
-    const int e = mx > 0.0 ? oz_exponent(mx) : 0;
-#pragma unroll 1
-    for (int kc = 0; kc < 4; ++kc) {
-        const int k0 = kh * 64 + kc * 16;
-        uint32_t w[kOzS][4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            long long X[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) X[u] = mx > 0.0 ? oz_fixed(tileb[(k0 + 4 * q + u) * 128 + c], e) : 0;
-#pragma unroll
-            for (int d = 0; d < kOzS; ++d)
-                w[d][q] = oz_digit(X[0], d) | (oz_digit(X[1], d) << 8) | (oz_digit(X[2], d) << 16) | (oz_digit(X[3], d) << 24);
-        }
-        const uint32_t off = oz_swz(c, k0);
-#pragma unroll
-        for (int d = 0; d < kOzS; ++d)
-            *reinterpret_cast<uint4*>(stage + size_t(d) * 128 * kOzK + off) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-        for (int d = 0; d < kOzS; ++d)
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
-                             J.dst[g] + size_t(d) * J.stride + size_t(tile) * 128 * kOzK),
-                         "r"(uint32_t(__cvta_generic_to_shared(stage + size_t(d) * 128 * kOzK))), "r"(uint32_t(128 * kOzK))
-                         : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        if (J.pe) J.pe[g * ntiles + tile] = e;
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    }
-    if (g == 0 && kh == 0) J.sc[r] = 1.0;
-}
-
 // B-side split into the MN-major panel layout (slice of a 128-column tile: 128 k-rows of 128 column
 // bytes, row k at oz_swz(k, n); tcgen05 reads it with b_major = MN): no transpose, so a CTA (512
 // threads) holds the whole (plane, tile) in registers (warp = 8 k-rows, lane = 4 columns; loads and
@@ -855,15 +786,6 @@ void OzSplitPlan::launch(cudaStream_t s) const {
     if (mn) {
         const dim3 grid(unsigned(maxrows / 128), unsigned(jobs.size() * kOzGroup));
         oz_split_mn_kernel<<<grid, kMnThreads, 0, s>>>(d);
-    } else if (transpose && tile_scale) {
-        static bool attr = false;
-        if (!attr) {
-            CCF_CUDA(cudaFuncSetAttribute(oz_split_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(oz_split_tile_smem())));
-            attr = true;
-        }
-        const dim3 grid(unsigned(maxrows / 128), unsigned(jobs.size() * kOzGroup));
-        oz_split_tile_kernel<<<grid, kTileThreads, oz_split_tile_smem(), s>>>(d);
     } else if (transpose) {
         static bool attr = false;
         if (!attr) {

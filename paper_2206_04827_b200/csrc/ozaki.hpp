@@ -100,7 +100,6 @@ inline OzSplitJob oz_job(const double* src, long ld, int nrows, int ncols, uint8
 struct OzSplitPlan {
     std::vector<OzSplitJob> jobs;
     bool transpose = false;
-    bool tile_scale = false;  // transposed: one scale per (plane, 128-row tile), row scales 1 (data B operands)
     bool mn = false;          // B data in the MN-major panel layout (src rows = K, columns = panel rows): one
                               // scale per (plane, 128-column tile), row scales 1; read with OzGemmPlan::b_mn
     OzSplitJob* d = nullptr;

@@ -45,7 +45,6 @@ int main(int argc, char** argv) {
     cudaMemset(PB.p, 0, PB.n * 8);
     OzSplitPlan sa, sb;
     sb.transpose = true;
-    sb.tile_scale = std::getenv("CCF_OZ_TILE") && std::atoi(std::getenv("CCF_OZ_TILE"));
     sb.mn = std::getenv("CCF_OZ_MN") && std::atoi(std::getenv("CCF_OZ_MN"));
     OzGemmPlan g;
     for (int bt = 0; bt < nb * nt; ++bt) {

@@ -928,6 +928,9 @@ __device__ __forceinline__ void half_dft16(const double2 (&x)[16], int h, double
 }
 
 constexpr int kTWArr = 272;
+// point stride: the two arrays plus one double2, so the points 4 apart that neighbouring threads of the
+// spectrum assembly / unpack tasks touch (z-position pairs q = 0, 1) sit in different 16-byte bank groups
+constexpr int kTWPt = 2 * kTWArr + 1;
 
 }  // namespace
 
@@ -937,7 +940,7 @@ template <int NQ>
 __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(ThetaCross t) {
     constexpr int kPts = 4 * NQ;
     extern __shared__ double2 sd[];
-    double2* twf = sd + kPts * 2 * kTWArr;  // twf[16 k1 + n2] = e^{-2 pi i n2 k1 / 256} (forward stage)
+    double2* twf = sd + kPts * kTWPt;  // twf[16 k1 + n2] = e^{-2 pi i n2 k1 / 256} (forward stage)
     const Geo& g = t.g;
     const int S = g.nslots;  // 129
     const int jr = t.row0 + blockIdx.y;
@@ -951,7 +954,7 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
         const int e = (x >> 4) * (x & 15);
         twf[x] = e < 128 ? t.tw[e] : make_double2(-t.tw[e - 128].x, -t.tw[e - 128].y);
     }
-    double2* Z = sd + pt * 2 * kTWArr;  // this point's two arrays
+    double2* Z = sd + pt * kTWPt;  // this point's two arrays
     double2 tv[3][8];                   // time samples of the three pairs at l = col + 16 (2j + h)
     const long ps = g.plane_stride, oo = g.nh;
     const long ooi = t.vquad ? long(g.nh) * g.mh : long(g.nh);  // odd-z half of the inputs
@@ -1011,7 +1014,7 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
                 const double sz = hh ? -1.0 : 1.0;
                 const double xar = sg * fma(sz, aro, ar), xai = reonly ? 0.0 : sg * fma(sz, aio, ai);
                 const double xbr = sg * fma(sz, bro, br), xbi = reonly ? 0.0 : sg * fma(sz, bio, bi);
-                double2* Zp = sd + (2 * (2 * q + ip) + hh) * 2 * kTWArr + arr * kTWArr;
+                double2* Zp = sd + (2 * (2 * q + ip) + hh) * kTWPt + arr * kTWArr;
                 Zp[s] = make_double2(xar - xbi, xai + xbr);
                 if (s > 0 && s < 128) Zp[256 - s] = make_double2(xar + xbi, xbr - xai);
             }
@@ -1134,7 +1137,7 @@ __global__ void __launch_bounds__(128 * NQ, 4 / NQ) theta_cross256w_kernel(Theta
             double xr[2], xi[2];
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
-                const double2* base = sd + (2 * (2 * q + ip) + hh) * 2 * kTWArr + arr * kTWArr;
+                const double2* base = sd + (2 * (2 * q + ip) + hh) * kTWPt + arr * kTWArr;
                 const double2 zt = base[tt], zm = base[tm];
                 if (f == 1) {
                     xr[hh] = 0.5 * (zt.y + zm.y);
@@ -1354,7 +1357,7 @@ __global__ void __launch_bounds__(kTheta512Threads, 2) theta_cross512_kernel(The
 
 size_t theta_cross512_smem() { return size_t(3) * kTheta512Points * kA512 * sizeof(double2); }
 
-size_t theta_cross256w_smem(int nq) { return (size_t(4 * nq) * 2 * kTWArr + 256) * sizeof(double2); }
+size_t theta_cross256w_smem(int nq) { return (size_t(4 * nq) * kTWPt + 256) * sizeof(double2); }
 
 size_t theta_cross256_smem() { return (size_t(kT256Pts) * 3 * kT256Arr + 256) * sizeof(double2); }
 int theta_cross256_positions() { return kT256Pos; }

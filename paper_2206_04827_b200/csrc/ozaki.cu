@@ -268,7 +268,7 @@ static_assert(kRegsCtl * 128 + kRegsEpi * 32 * kEpiWarps <= kRegsLaunch * kThrea
 static_assert((kRegsCtl + kRegsEpi * (kEpiWarps / 4)) * 32 <= 16384, "setmaxnreg beyond an SM sub-partition");
 constexpr size_t kSmemBufs = size_t(kBufs) * kPair;
 
-__device__ unsigned long long g_oz_trace[4096];  // diagnostics (CCF_OZ_MODE bit 2): block 0 event times
+__device__ unsigned long long g_oz_trace[8192];  // diagnostics (CCF_OZ_MODE bit 2): block 0 event times
 __device__ __forceinline__ unsigned long long oz_now() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -276,7 +276,7 @@ __device__ __forceinline__ unsigned long long oz_now() {
 }
 #define OZ_TRACE(idx)                                                                     \
     do {                                                                                  \
-        if ((mode & 4) && blockIdx.x == 0 && (idx) < 4096) g_oz_trace[(idx)] = oz_now(); \
+        if ((mode & 4) && blockIdx.x == 0 && (idx) < 8192) g_oz_trace[(idx)] = oz_now(); \
     } while (0)
 
 // low word of a K-major / MN-major 128-byte-swizzle descriptor (start address >> 4, LBO 16 B); the high
@@ -648,7 +648,6 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
             const OzItem& I = *reinterpret_cast<const OzItem*>(slot);
             if (t1 > t0 && *reinterpret_cast<const int*>(slot + sizeof(OzItem))) {  // column scales
                 const uint32_t sba = su32(slot + 128) + 8u * uint32_t(half * kCols);  // broadcast shared loads
-                const double al = I.alpha;
 #pragma unroll
                 for (int j = 0; j < kCols; j += 2) {
                     double sx, sy;
@@ -656,7 +655,8 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                     acc[j] *= sx;
                     acc[j + 1] *= sy;
                 }
-                if (al != 1.0) {
+                if (I.flags & kOzItemAlpha) {
+                    const double al = I.alpha;
 #pragma unroll
                     for (int j = 0; j < kCols; ++j) acc[j] *= al;
                 }
@@ -664,13 +664,14 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
             if (warp == kCtlWarps && lane == 0) OZ_TRACE(3712 + (it - blockIdx.x) / gridDim.x);
             if (I.pdst) {  // the tile as the next product's MN-major B panel tile: digits relative to the tile max
                 // tile max exponent from the high words of |acc| (the exponent lives there): integer max, no FP64 ops
-                const bool full = I.m == 128 && I.n == kOzNT;
+                if (!(I.flags & kOzItemFull)) {  // ragged tile: rows >= m and columns >= n become zero digits
+                    const int nv = row < I.m ? I.n - half * kCols : 0;
+#pragma unroll
+                    for (int j = 0; j < kCols; ++j) acc[j] = j < nv ? acc[j] : 0.0;
+                }
                 uint32_t hx = 0;
 #pragma unroll
-                for (int j = 0; j < kCols; ++j) {
-                    const uint32_t h = uint32_t(__double2hiint(acc[j])) & 0x7FFFFFFFu;
-                    hx = (full || (row < I.m && half * kCols + j < I.n)) ? max(hx, h) : hx;
-                }
+                for (int j = 0; j < kCols; ++j) hx = max(hx, uint32_t(__double2hiint(acc[j])) & 0x7FFFFFFFu);
 #pragma unroll
                 for (int o = 16; o; o >>= 1) hx = max(hx, __shfl_xor_sync(0xffffffffu, hx, o));
                 if (lane == 0) reinterpret_cast<uint32_t*>(bar.red[ipar])[warp - kCtlWarps] = hx;
@@ -683,11 +684,11 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                 }
                 ipar ^= 1;
                 const int e = oz_tile_exponent(hx);
-                const double scale = (hx && row < I.m) ? ldexp(1.0, 47 - e) : 0.0;  // rows >= m: zero digits
+                const double scale = hx ? ldexp(1.0, 47 - e) : 0.0;
                 // in place: acc[j] -> the bits of fma(acc[j], 2^(47 - e), 1.5 2^52), whose low 48 bits are the
-                // two's-complement fixed-point value X (|X| < 2^47 by the choice of e); columns >= n: zero digits
+                // two's-complement fixed-point value X (|X| < 2^47 by the choice of e)
 #pragma unroll
-                for (int j = 0; j < kCols; ++j) acc[j] = fma((full || half * kCols + j < I.n) ? acc[j] : 0.0, scale, 6755399441055744.0);
+                for (int j = 0; j < kCols; ++j) acc[j] = fma(acc[j], scale, 6755399441055744.0);
                 // per digit slice: this thread's 32 columns = one 32-byte sector of its 128-byte panel row
                 // (chunks 2i, 2i + 1 of the row swizzle land in one aligned sector), one 256-bit store each
                 const uint32_t off = oz_mn32(row, half * kCols) & ~31u;  // 32 rows of a quarter: 1 KB per instruction
@@ -750,8 +751,8 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
 }  // namespace
 
 void oz_trace_dump() {  // diagnostics (CCF_OZ_MODE bit 2): block 0's event times, ns from the first
-    std::vector<unsigned long long> t(4096);
-    cudaMemcpyFromSymbol(t.data(), g_oz_trace, 4096 * 8);
+    std::vector<unsigned long long> t(8192);
+    cudaMemcpyFromSymbol(t.data(), g_oz_trace, 8192 * 8);
     const unsigned long long t0 = t[0];
     for (int i = 0; i < 48; ++i)
         std::printf("level %2d: pair-issue %7lld  mma-start %7lld  mma-go %7lld  issued %7lld  epi-got %7lld\n", i,
@@ -762,6 +763,17 @@ void oz_trace_dump() {  // diagnostics (CCF_OZ_MODE bit 2): block 0's event time
         std::printf("tile %d: drained %7lld  sb-copied %7lld  sb-got %7lld  scaled %7lld  stored %7lld\n", i,
                     (long long)(t[3584 + i] - t0), (long long)(t[3968 + i] - t0), (long long)(t[4032 + i] - t0),
                     (long long)(t[3712 + i] - t0), (long long)(t[3840 + i] - t0));
+    for (int i = 0; i < 8; ++i) {  // per epilogue warp: tile max start / after the epilogue barrier / stores done
+        if (!t[4096 + i * 16]) continue;
+        for (int k = 0; k < 3; ++k) {
+            std::printf("tile %d %s:", i, k == 0 ? "pre-max" : k == 1 ? "bar-out" : "stored ");
+            for (int w = 0; w < 16; ++w) {
+                const unsigned long long v = t[4096 + 128 * k + i * 16 + w];
+                std::printf(" %6lld", v ? (long long)(v - t0) : -1);
+            }
+            std::printf("\n");
+        }
+    }
 }
 
 size_t oz_smem_bytes() { return kSmemBufs + kBarsBytes + 2 * kItemSlot; }
@@ -812,7 +824,8 @@ void OzGemmPlan::upload() {
     dterms = nullptr;
     ditems = nullptr;
     flops = 0.0;
-    for (const OzItem& it : items) {
+    for (OzItem& it : items) {
+        it.flags = (it.alpha != 1.0 ? kOzItemAlpha : 0) | (it.m == 128 && it.n == kOzNT ? kOzItemFull : 0);
         if (it.t0 < 0 || it.t1 > int(terms.size()) || it.t0 > it.t1 || it.n0 % kOzNT || it.m > 128 || it.n > kOzNT)
             throw Error(INTERNAL, "OzGemmPlan: bad item");
         flops += 2.0 * it.m * it.n * kOzK * (it.t1 - it.t0);

@@ -42,10 +42,13 @@ struct OzTerm {
     const int* pe;      // B plane exponent per 128-row tile of the B panel (transposed splits)
 };
 
+constexpr int kOzItemAlpha = 1;  // alpha != 1
+constexpr int kOzItemFull = 2;   // m = 128 and n = kOzNT (no row / column guards in the epilogue)
 struct alignas(16) OzItem {  // one 128 x 128 output tile; every term of an item has the same B (column) scales
     int t0, t1;         // terms [t0, t1)
     int n0;             // first B-panel row (output column) of the tile
     int m, n;           // valid rows / columns of the tile
+    int flags;          // (set by OzGemmPlan::upload: kOzItemAlpha, kOzItemFull)
     double* c;          // tile origin in the output (row-major, ldc)
     long ldc;
     double alpha;       // (ignored when the terms carry no column scales: alpha = 1)

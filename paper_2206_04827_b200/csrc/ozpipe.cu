@@ -178,7 +178,7 @@ bool OzPipe::ysynth(int ntensor, const double* const* z, double* const* outS, do
                             gp->gemm.terms.push_back({bytes(ysp_) + i * kPanel128, bytes(cpan_) + size_t(cp) * kPanel128,
                                                       ysc_.p + i * 128, csc_.p + size_t(cp) * 128, long(oz_slice_bytes(128)),
                                                       ints(cpe_) + cp});
-                            OzItem item{t0, t0 + 1, 0, M, nh, out + off + long(dd ? 1 - k0 : k0) * nh, long(g.n), 1.0};
+                            OzItem item{t0, t0 + 1, 0, M, nh, 0, out + off + long(dd ? 1 - k0 : k0) * nh, long(g.n), 1.0};
                             // the value half of this tile as the X1 product's B panel tile (no fp64 tensor)
                             Panels& pp = panels(out);
                             const size_t pi = size_t(s - s_lo) * 2 + pl;
@@ -257,7 +257,7 @@ bool OzPipe::rsynth(double* const (&Z)[2][3], double* const* val) {
                         // (an output no block feeds is an item without terms: the kernel stores zeros)
                         const int t1 = int(sp->gemm.terms.size());
                         double* plane = val[3 * pr + o / 2] + long(s) * g.slot_stride + long(o % 2) * g.plane_stride;
-                        OzItem item{t0, t1, nt * 128, mh, 128, plane + nt * 128, long(g.n), 1.0};
+                        OzItem item{t0, t1, nt * 128, mh, 128, 0, plane + nt * 128, long(g.n), 1.0};
                         if (quad) {  // column-quad-major values for the theta kernel (Pipeline::val_quad_)
                             item.cq = 4L * mh;
                             item.c = plane + long(nt * 128 / 4) * item.cq;
@@ -318,7 +318,7 @@ bool OzPipe::analyze(double* const* av, double* const* Y, double* lam_n, double*
                         const int t0 = int(za->gemm.terms.size());
                         za->gemm.terms.push_back({bytes(zap_) + i * kPanel128, bytes(cpan_) + size_t(cp) * kPanel128, zasc_.p + i * 128,
                                                   csc_.p + size_t(cp) * 128, long(oz_slice_bytes(128)), ints(cpe_) + cp});
-                        OzItem item{t0, t0 + 1, 0, mh, Np, Y[x] + long(s) * g.slot_stride + long(pl) * mh * 2 * Np + long(po) * Np,
+                        OzItem item{t0, t0 + 1, 0, mh, Np, 0, Y[x] + long(s) * g.slot_stride + long(pl) * mh * 2 * Np + long(po) * Np,
                                     long(2 * Np), 1.0};
                         // ra's B plane in = 2 x + pl, column tile po (no fp64 Y tensor)
                         item.pdst = rpan(s, 2 * x + pl) + size_t(po) * 128 * kOzK;
@@ -346,7 +346,7 @@ bool OzPipe::analyze(double* const* av, double* const* Y, double* lam_n, double*
                     }
                     const int t1 = int(ra->gemm.terms.size());
                     ra->gemm.b_mn = true;
-                    ra->gemm.items.push_back({t0, t1, nt * 128, M, 128,
+                    ra->gemm.items.push_back({t0, t1, nt * 128, M, 128, 0,
                                               (o < 2 ? gam_n : lam_n) + P.eig_off(s, o % 2, 0) + nt * 128, long(2 * Np), 1.0});
                 }
         ra->gemm.tag = "C";

@@ -75,7 +75,7 @@ int main(int argc, char** argv) {
     DBuf PO(panel_out ? (size_t(nb) * ntile * oz_panel_bytes(128) + 7) / 8 : 1), POE(size_t(nb) * ntile);
     for (int b = 0; b < nb; ++b)
         for (int n0 = 0; n0 < N; n0 += kOzNT) {
-            OzItem it{b * nt, (b + 1) * nt, n0, M, std::min(kOzNT, N - n0), C.p + size_t(b) * M * N + n0, long(N), 1.0};
+            OzItem it{b * nt, (b + 1) * nt, n0, M, std::min(kOzNT, N - n0), 0, C.p + size_t(b) * M * N + n0, long(N), 1.0};
             if (panel_out) {
                 const size_t ti = size_t(b) * ntile + n0 / kOzNT;
                 it.pdst = reinterpret_cast<uint8_t*>(PO.p) + ti * oz_panel_bytes(128);

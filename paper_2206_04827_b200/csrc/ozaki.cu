@@ -250,7 +250,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 
 constexpr uint32_t kSlice = 128 * kOzK;  // 16 KB: one digit slice of a 128-row panel block
 constexpr uint32_t kPair = 2 * kSlice;   // A_d and B_d of one term
-constexpr int kBufs = 7;                 // pair buffers: a term holds 6, the 7th takes the next term's first
+constexpr int kBufs = 6;                 // pair buffers: one term (the next term's pairs load as this one's leave)
 constexpr int kSlots = 4;                // TMEM accumulator ring: 4 x 128 columns
 constexpr int kLevels = 7;               // L = d + d' <= 6: 26 digit-pair products
 constexpr int kEpiWarps = 16;            // warpgroups 1-4: 4 per TMEM lane quadrant
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                                                               const OzItem* __restrict__ items, int nitems, int mode,
                                                               int bmn) {
     extern __shared__ __align__(1024) uint8_t dsm[];
-    // no room for alignment slack (7 x 32 KB + barriers + 2 KB of column scales fill the 227 KB): the
+    // no room for alignment slack (6 x 32 KB + barriers + 2 KB of column scales nearly fill the 227 KB): the
     // dynamic window of a kernel without static shared memory starts 1024-byte aligned
     if (su32(dsm) & 1023) __trap();
     uint8_t* sm = dsm;
@@ -403,18 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                         ct1 = items[itn].t1;
                         cn0 = items[itn].n0;
                     }
-                    {  // item slot: the item (read by the epilogue) and its column scales (the first term's B)
-                        const uint32_t k = ic & 1;
-                        mbar_wait(&bar.sbempty[k], ((ic >> 1) & 1) ^ 1);
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // epilogue reads -> next bulk write
-                        uint8_t* slot = islot + k * kItemSlot;
-                        const double* sbp = t1 > t0 ? T.sb : nullptr;
-                        *reinterpret_cast<int*>(slot + sizeof(OzItem)) = sbp != nullptr;
-                        mbar_expect(&bar.sbfull[k], uint32_t(sizeof(OzItem)) + (sbp ? uint32_t(kSbBytes) : 0u));
-                        bulk_g2s(slot, items + it, uint32_t(sizeof(OzItem)), &bar.sbfull[k]);
-                        if (sbp) bulk_g2s(slot + 128, sbp + n0, uint32_t(kSbBytes), &bar.sbfull[k]);
-                        OZ_TRACE(3968 + ic);
-                    }
+                    const double* sbp = t1 > t0 ? T.sb : nullptr;  // column scales: the first term's B row scales
                     for (int t = t0; t < t1; ++t) {
                         const OzTerm Tc = T;
                         const int tn = t + 1 < t1 ? t + 1 : (itn < nitems && ct1 > ct0 ? ct0 : -1);
@@ -429,6 +418,19 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const OzTerm* __re
                             bulk_g2s(sm + size_t(b) * kPair, Tc.a + size_t(d) * kSlice, kSlice, &bar.full[b]);
                             bulk_g2s(sm + size_t(b) * kPair + kSlice, bsrc + size_t(d) * Tc.bstride, kSlice, &bar.full[b]);
                         }
+                    }
+                    // item slot: the item (read by the epilogue at the end of the tile) and its column scales, after
+                    // the item's pairs (the slot of item ic - 2 is released only when that tile is stored)
+                    {
+                        const uint32_t k = ic & 1;
+                        mbar_wait(&bar.sbempty[k], ((ic >> 1) & 1) ^ 1);
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // epilogue reads -> next bulk write
+                        uint8_t* slot = islot + k * kItemSlot;
+                        *reinterpret_cast<int*>(slot + sizeof(OzItem)) = sbp != nullptr;
+                        mbar_expect(&bar.sbfull[k], uint32_t(sizeof(OzItem)) + (sbp ? uint32_t(kSbBytes) : 0u));
+                        bulk_g2s(slot, items + it, uint32_t(sizeof(OzItem)), &bar.sbfull[k]);
+                        if (sbp) bulk_g2s(slot + 128, sbp + n0, uint32_t(kSbBytes), &bar.sbfull[k]);
+                        OZ_TRACE(3968 + ic);
                     }
                 }
             }

@@ -106,6 +106,16 @@ ccf_status ccf_ns_create(ccf_ctx* ctx, double reynolds, double h, int order, int
 ccf_status ccf_ns_create_ex(ccf_ctx* ctx, double reynolds, double h, int order, int flags, const double* lam0,
                             const double* gam0, ccf_ns_state** out);
 ccf_status ccf_ns_step(ccf_ns_state* st, int nsteps);
+/* NSStepper::seed (ptns.hpp:110-112, ptns.cpp:195-203): install a prebuilt history. lam_hist / gam_hist: n_omega
+ * coefficient tensors (p*n*m complex128 each, host or device), newest first; nl_lam / nl_gam: n_nonlinear
+ * nonlinear-term tensors, newest first, entry i belonging to omega entry i + 1 (the next step pushes N of the
+ * newest omega in front, ptns.cpp:232). CCF_DOMAIN_ERROR "NSStepper::seed: empty history" for n_omega < 1; a later
+ * step with fewer entries than its BDF order fails with "bdf_rhs: insufficient history for the requested order"
+ * (timestep.cpp:41-42). The tensors are stored parity-projected (the Helmholtz step projects its right-hand
+ * side, timestep.cpp:75). */
+ccf_status ccf_ns_seed(ccf_ns_state* st, int n_omega, const double* const* lam_hist, const double* const* gam_hist,
+                       int n_nonlinear, const double* const* nl_lam, const double* const* nl_gam, double time,
+                       int steps_taken);
 /* NSStepper::velocity(): velocity PT scalars of the current state (fresh psi solve, ptns.cpp:205-215). */
 ccf_status ccf_ns_velocity(ccf_ns_state* st, double* lam_v, double* gam_v);
 /* NSState::gamma_psi = solve_poisson_3d(-gamma_omega) of the omega the last step started from

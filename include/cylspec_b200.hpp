@@ -327,6 +327,7 @@ inline PTScalars nonlinear_term(const PTScalars& v, const PTScalars& w, bool dea
     return o;
 }
 
+enum class NSBootstrap { ramp, substeps };  // ptns.hpp:79-82
 struct NSConfig {
     GridSpec spec;
     double reynolds = 100.0;
@@ -336,9 +337,10 @@ struct NSConfig {
     bool disable_nonlinear = false;   // Stokes limit
     bool dealias_two_thirds = false;
     bool compute_gamma_psi = false;   // diagnostic-only extra Poisson solve (gamma_psi())
+    NSBootstrap bootstrap = NSBootstrap::ramp;
 };
 
-class NSStepper {  // ramp bootstrap; state resident on the GPU between steps
+class NSStepper {  // state resident on the GPU between steps
 public:
     NSStepper(const NSConfig& cfg, const PTScalars& omega0) : cfg_(cfg), omega_(cfg.spec) {
         // ptns.cpp:185-189
@@ -356,6 +358,30 @@ public:
     NSStepper& operator=(const NSStepper&) = delete;
     void step() { detail::check(ccf_ns_step(st_, 1), ctx_); }
     void steps(int k) { detail::check(ccf_ns_step(st_, k), ctx_); }
+    /// Install a prebuilt history (bootstrap helpers), ptns.cpp:195-203. Newest first; nonlinear_hist[i] belongs to
+    /// omega_hist[i + 1].
+    void seed(const std::deque<PTScalars>& omega_hist, const std::deque<PTScalars>& nonlinear_hist, double time,
+              int steps_taken) {
+        if (omega_hist.empty()) throw DomainError("NSStepper::seed: empty history");
+        std::vector<const double*> ol, og, nl, ng;
+        for (const PTScalars& s : omega_hist) {
+            if (!(s.lambda.spec == cfg_.spec) || !(s.gamma.spec == cfg_.spec))
+                throw DomainError("NSStepper::seed: history spec mismatch");
+            ol.push_back(s.lambda.raw());
+            og.push_back(s.gamma.raw());
+        }
+        for (const PTScalars& s : nonlinear_hist) {
+            if (!(s.lambda.spec == cfg_.spec) || !(s.gamma.spec == cfg_.spec))
+                throw DomainError("NSStepper::seed: history spec mismatch");
+            nl.push_back(s.lambda.raw());
+            ng.push_back(s.gamma.raw());
+        }
+        detail::check(ccf_ns_seed(st_, int(ol.size()), ol.data(), og.data(), int(nl.size()), nl.data(), ng.data(), time,
+                                  steps_taken),
+                      ctx_);
+        time_ = time;
+        taken_ = steps_taken;
+    }
     const PTScalars& omega() {
         detail::check(ccf_ns_get_omega(st_, omega_.lambda.raw(), omega_.gamma.raw(), &time_, &taken_), ctx_);
         return omega_;
@@ -385,14 +411,58 @@ private:
 struct NSRunResult {
     PTScalars final_omega;
     double final_time = 0.0;
+    std::vector<PTScalars> snapshots;
+    std::vector<double> snapshot_times;
 };
 
-inline NSRunResult ns_run(const NSConfig& config, const PTScalars& initial_omega, int steps) {
-    NSStepper s(config, initial_omega);
-    s.steps(steps);
+// ns_run (ptns.cpp:269-324): ramp bootstrap, or NSBootstrap::substeps: [0, (b-1) h] integrated with 32 BDF2
+// sub-steps per h, the sampled trajectory and its replayed nonlinear terms seeded into the full-order stepper
+inline NSRunResult ns_run(const NSConfig& config, const PTScalars& initial_omega, int steps, int output_every = 0) {
     NSRunResult r;
-    r.final_omega = s.omega();
-    r.final_time = s.time();
+    auto advance = [&](NSStepper& st, int first) {
+        if (output_every > 0) {
+            for (int s = first; s < steps; ++s) {
+                st.step();
+                if ((s + 1) % output_every == 0) {
+                    r.snapshots.push_back(st.omega());
+                    r.snapshot_times.push_back(st.time());
+                }
+            }
+        } else if (steps > first) {
+            st.steps(steps - first);  // one C-ABI call: the steady steps replay their CUDA graphs back to back
+        }
+        r.final_omega = st.omega();
+        r.final_time = st.time();
+    };
+    if (config.bootstrap == NSBootstrap::substeps && config.order > 1 && steps > 0) {
+        const int b = config.order;
+        const int per = 32;
+        NSConfig sub = config;
+        sub.order = std::min(2, config.order);
+        sub.h = config.h / per;
+        sub.bootstrap = NSBootstrap::ramp;
+        std::deque<PTScalars> hist;  // newest first
+        hist.push_front(initial_omega);
+        {
+            NSStepper fine(sub, initial_omega);
+            for (int big = 1; big <= b - 1; ++big) {
+                fine.steps(per);
+                hist.push_front(fine.omega());
+            }
+        }
+        NSStepper stepper(config, hist.front());
+        std::deque<PTScalars> replay;
+        if (!config.disable_nonlinear)
+            for (int i = int(hist.size()) - 1; i >= 1; --i) {
+                const PTScalars v = velocity_from_vorticity(hist[size_t(i)], config.adi_tol);
+                replay.push_front(nonlinear_term(v, hist[size_t(i)], config.dealias_two_thirds));
+            }
+        stepper.seed(hist, replay, (b - 1) * config.h, b - 1);
+        advance(stepper, b - 1);
+        return r;
+    }
+    NSStepper stepper(config, initial_omega);
+    advance(stepper, 0);
     return r;
 }
 

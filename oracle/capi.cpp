@@ -233,6 +233,33 @@ int orc_ns_get(void* h, double* lam, double* gam, double* time, int* steps) {
     });
 }
 void orc_ns_destroy(void* h) { delete static_cast<NSStepper*>(h); }
+// NSStepper::seed (ptns.cpp:195-203): nom omega pairs and nnl nonlinear pairs, newest first
+int orc_ns_seed(void* h, int m, int n, int p, int nom, const double* const* lam_h, const double* const* gam_h, int nnl,
+                const double* const* nl_l, const double* const* nl_g, double time, int steps) {
+    return guard([&] {
+        std::deque<PT> oh, nh;
+        for (int i = 0; i < nom; ++i) oh.push_back({load(m, n, p, lam_h[i]), load(m, n, p, gam_h[i])});
+        for (int i = 0; i < nnl; ++i) nh.push_back({load(m, n, p, nl_l[i]), load(m, n, p, nl_g[i])});
+        static_cast<NSStepper*>(h)->seed(std::move(oh), std::move(nh), time, steps);
+    });
+}
+// ns_run (ptns.cpp:269-324); flags: bit 0 disable_nonlinear, bit 1 dealias, bit 2 NSBootstrap::substeps
+int orc_ns_run(int m, int n, int p, double re, double h, int order, double tol, int flags, const double* lam0,
+               const double* gam0, int steps, double* lam, double* gam, double* time) {
+    return guard([&] {
+        NSConfig cfg;
+        cfg.spec = Spec(m, n, p);
+        cfg.reynolds = re;
+        cfg.h = h;
+        cfg.order = order;
+        cfg.tol = tol;
+        cfg.disable_nonlinear = (flags & 1) != 0;
+        cfg.dealias = (flags & 2) != 0;
+        const PT out = ns_run(cfg, {load(m, n, p, lam0), load(m, n, p, gam0)}, steps, (flags & 4) != 0, time);
+        store(out.lambda, lam);
+        store(out.gamma, gam);
+    });
+}
 
 // ---- heat stepper handle (HeatStepper, proj/src/timestep.cpp:110-144)
 void* orc_heat_create(int m, int n, int p, double alpha, double h, int order, double tol, const double* initial_coef) {

@@ -370,6 +370,7 @@ class NSStepper {                                          // ptns.cpp:177-267
 public:
     NSStepper(const NSConfig& cfg, PT omega0);
     void step();
+    void seed(std::deque<PT> omega_hist, std::deque<PT> nonlinear_hist, double time, int steps_taken);  // ptns.cpp:195-203
     const PT& omega() const { return omega_.front(); }
     double time() const { return time_; }
     int steps_taken() const { return steps_; }
@@ -382,6 +383,9 @@ private:
     double time_ = 0;
     int steps_ = 0;
 };
+
+// ptns.cpp:269-324; substeps: the NSBootstrap::substeps branch (:272-311), else the ramp bootstrap
+PT ns_run(const NSConfig& cfg, const PT& omega0, int steps, bool substeps, double* final_time);
 
 // ---- io: proj/src/io.cpp:12-109 (CCF1 FieldFile) ---------------------------
 uint32_t crc32_ieee(const uint8_t* data, size_t len);

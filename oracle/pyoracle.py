@@ -86,6 +86,11 @@ def lib():
         L.orc_ns_step.argtypes = [C.c_void_p, C.c_int]
         L.orc_ns_get.argtypes = [C.c_void_p, dp, dp, dp, C.POINTER(C.c_int)]
         L.orc_ns_destroy.argtypes = [C.c_void_p]
+        pp = C.POINTER(C.c_void_p)
+        L.orc_ns_seed.restype = C.c_int
+        L.orc_ns_seed.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, pp, pp, C.c_int, pp, pp, C.c_double,
+                                  C.c_int]
+        L.orc_ns_run.restype = C.c_int
         L.orc_heat_step.argtypes = [C.c_void_p, dp]
         L.orc_heat_get.argtypes = [C.c_void_p, dp, dp, C.POINTER(C.c_int)]
         L.orc_heat_destroy.argtypes = [C.c_void_p]
@@ -276,17 +281,44 @@ class NSStepper:
     def step(self, n=1):
         _chk(lib().orc_ns_step(self.h, int(n)))
 
+    def seed(self, omega_hist, nonlinear_hist, time, steps_taken):
+        """NSStepper::seed (ptns.cpp:195-203): lists of (lambda, gamma) pairs, newest first."""
+        p, n, m = self.shape
+        rows = [[_cz(x) for x in pair] for pair in list(omega_hist) + list(nonlinear_hist)]
+        no, nn = len(omega_hist), len(nonlinear_hist)
+        vp = C.c_void_p
+
+        def arr(rs, j):
+            return (vp * max(len(rs), 1))(*[C.cast(_p(r[j]), vp) for r in rs])
+
+        _chk(lib().orc_ns_seed(self.h, m, n, p, no, arr(rows[:no], 0), arr(rows[:no], 1), nn, arr(rows[no:], 0),
+                               arr(rows[no:], 1), C.c_double(time), int(steps_taken)))
+
     def omega(self):
         l, g = np.zeros(self.shape, np.complex128), np.zeros(self.shape, np.complex128)
         t = C.c_double()
         s = C.c_int()
         _chk(lib().orc_ns_get(self.h, _p(l), _p(g), C.byref(t), C.byref(s)))
+        self.time, self.steps_taken = t.value, s.value
         return l, g
 
     def __del__(self):
         if getattr(self, "h", None):
             lib().orc_ns_destroy(self.h)
             self.h = None
+
+
+def ns_run(lam0, gam0, steps, reynolds, h, order=4, tol=1e-12, disable_nonlinear=False, dealias=False,
+           bootstrap="ramp"):
+    """proj/src/ptns.cpp:269-324 ns_run -> (lambda, gamma, final_time)."""
+    l0, g0 = _cz(lam0), _cz(gam0)
+    p, n, m = l0.shape
+    l, g = np.zeros(l0.shape, np.complex128), np.zeros(l0.shape, np.complex128)
+    t = C.c_double()
+    flags = int(bool(disable_nonlinear)) | (2 if dealias else 0) | (4 if bootstrap == "substeps" else 0)
+    _chk(lib().orc_ns_run(m, n, p, C.c_double(reynolds), C.c_double(h), int(order), C.c_double(tol), flags, _p(l0),
+                          _p(g0), int(steps), _p(l), _p(g), C.byref(t)))
+    return l, g, t.value
 
 
 class HeatStepper:

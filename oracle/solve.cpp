@@ -661,6 +661,14 @@ NSStepper::NSStepper(const NSConfig& cfg, PT omega0)  // ptns.cpp:177-193
     omega_.push_front(std::move(omega0));
 }
 
+void NSStepper::seed(std::deque<PT> omega_hist, std::deque<PT> nonlinear_hist, double time, int steps_taken) {
+    if (omega_hist.empty()) throw DomainError("NSStepper::seed: empty history");
+    omega_ = std::move(omega_hist);
+    nonlinear_ = std::move(nonlinear_hist);
+    time_ = time;
+    steps_ = steps_taken;
+}
+
 PT NSStepper::velocity() const { return velocity_from_vorticity(omega_.front(), poisson_cache_); }
 
 void NSStepper::step() {  // ptns.cpp:217-267
@@ -700,6 +708,39 @@ void NSStepper::step() {  // ptns.cpp:217-267
     while (int(omega_.size()) > cfg_.order) omega_.pop_back();
     time_ += cfg_.h;
     ++steps_;
+}
+
+PT ns_run(const NSConfig& cfg, const PT& omega0, int steps, bool substeps, double* final_time) {  // ptns.cpp:269-324
+    if (substeps && cfg.order > 1 && steps > 0) {
+        const int b = cfg.order, per = 32;
+        NSConfig sub = cfg;
+        sub.order = std::min(2, cfg.order);
+        sub.h = cfg.h / per;
+        NSStepper fine(sub, omega0);
+        std::deque<PT> hist;  // newest first
+        hist.push_front(omega0);
+        for (int big = 1; big <= b - 1; ++big) {
+            for (int s = 0; s < per; ++s) fine.step();
+            hist.push_front(fine.omega());
+        }
+        NSStepper stepper(cfg, hist.front());
+        std::deque<PT> replay;
+        if (!cfg.disable_nonlinear) {
+            ModalSolverCache cache(cfg.spec.m, cfg.spec.n, cfg.tol);
+            for (int i = int(hist.size()) - 1; i >= 1; --i) {
+                const PT v = velocity_from_vorticity(hist[size_t(i)], cache);
+                replay.push_front(nonlinear_term(v, hist[size_t(i)], cfg.dealias));
+            }
+        }
+        stepper.seed(hist, replay, (b - 1) * cfg.h, b - 1);
+        for (int s = b - 1; s < steps; ++s) stepper.step();
+        if (final_time) *final_time = stepper.time();
+        return stepper.omega();
+    }
+    NSStepper stepper(cfg, omega0);
+    for (int s = 0; s < steps; ++s) stepper.step();
+    if (final_time) *final_time = stepper.time();
+    return stepper.omega();
 }
 
 }  // namespace oracle

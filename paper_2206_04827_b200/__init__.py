@@ -88,7 +88,7 @@ EXPORTS = ["ccf_ctx_create", "ccf_ctx_destroy", "ccf_ctx_set_stream", "ccf_ctx_s
            "ccf_shard_open_ipc", "ccf_shard_link_local", "ccf_shard_set_host_barrier", "ccf_write_field",
            "ccf_read_field_header", "ccf_read_field", "ccf_crc32", "ccf_ns_write_omega", "ccf_heat_create",
            "ccf_heat_step", "ccf_heat_get", "ccf_ns_create_ex", "ccf_ns_velocity", "ccf_ns_gamma_psi",
-           "ccf_nonlinear_ex"]
+           "ccf_nonlinear_ex", "ccf_ns_seed"]
 
 HOST_BARRIER_FN = C.CFUNCTYPE(None, C.c_void_p)
 SHARD_HANDLE_BYTES = 128  # include/ccf.h CCF_SHARD_HANDLE_BYTES
@@ -172,6 +172,8 @@ def lib():
         L.ccf_heat_get.argtypes = [vp, vp, dp, C.POINTER(C.c_int)]
         L.ccf_ns_create_ex.argtypes = [vp, C.c_double, C.c_double, C.c_int, C.c_int, vp, vp, C.POINTER(vp)]
         L.ccf_ns_velocity.argtypes = [vp, vp, vp]
+        L.ccf_ns_seed.argtypes = [vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.c_int, C.POINTER(vp), C.POINTER(vp),
+                                  C.c_double, C.c_int]
         L.ccf_ns_gamma_psi.argtypes = [vp, vp]
         L.ccf_nonlinear_ex.argtypes = [vp, vp, vp, vp, vp, C.c_int, vp, vp]
         _lib = L
@@ -536,6 +538,30 @@ class NSStepper:
                                           _addr(ctx._coef(lam0, "NSStepper: initial vorticity")),
                                           _addr(ctx._coef(gam0, "NSStepper: initial vorticity")), C.byref(st)))
         self.h = st
+        self.dealias_two_thirds = bool(dealias_two_thirds)
+
+    def seed(self, omega_hist, nonlinear_hist, time, steps_taken):
+        """NSStepper::seed (ptns.cpp:195-203): install a prebuilt history. omega_hist / nonlinear_hist: lists of
+        (lambda, gamma) coefficient pairs, newest first; nonlinear_hist[i] belongs to omega_hist[i + 1]."""
+        if len(omega_hist) == 0:
+            raise DomainError("NSStepper::seed: empty history")
+        what = "NSStepper::seed: history"
+        keep = [[self.ctx._coef(x, what) for x in pair] for pair in list(omega_hist) + list(nonlinear_hist)]
+        no, nn = len(omega_hist), len(nonlinear_hist)
+        vp = C.c_void_p
+
+        def arr(rows, j):
+            return (vp * max(len(rows), 1))(*[vp(_addr(r[j])) for r in rows])
+
+        self.ctx._check(lib().ccf_ns_seed(self.h, no, arr(keep[:no], 0), arr(keep[:no], 1), nn, arr(keep[no:], 0),
+                                          arr(keep[no:], 1), C.c_double(time), int(steps_taken)))
+        del keep
+
+    def evaluate_nonlinear(self):
+        """NSStepper::evaluate_nonlinear (ptns.cpp:211-214): nonlinear_term(velocity(), omega())."""
+        lv, gv = self.velocity()
+        lw, gw = self.omega()
+        return self.ctx.nonlinear_term(lv, gv, lw, gw, self.dealias_two_thirds)
 
     def velocity(self):
         """NSStepper::velocity(): velocity PT scalars of the current state (fresh psi solve)."""
@@ -593,6 +619,45 @@ class NSStepper:
             self.close()
         except Exception:
             pass
+
+
+def ns_run(ctx: Context, lam0, gam0, steps, reynolds=100.0, h=1e-2, order=4, disable_nonlinear=False,
+           dealias_two_thirds=False, bootstrap="ramp", output_every=0):
+    """ns_run (ptns.cpp:269-324) -> dict(final_omega, final_time, snapshots, snapshot_times). bootstrap "ramp"
+    (BDF 1 -> order) or "substeps": [0, (order - 1) h] integrated with 32 BDF2 sub-steps per h, the sampled
+    trajectory and its replayed nonlinear terms seeded into the full-order stepper (ptns.cpp:272-311)."""
+    if bootstrap not in ("ramp", "substeps"):
+        raise ConfigError("ns_run: bootstrap ramp | substeps")
+    kw = dict(disable_nonlinear=disable_nonlinear, dealias_two_thirds=dealias_two_thirds)
+    snaps, times = [], []
+    first = 0
+    if bootstrap == "substeps" and order > 1 and steps > 0:
+        per = 32
+        fine = NSStepper(ctx, lam0, gam0, reynolds, h / per, min(2, order), **kw)
+        hist = [(lam0, gam0)]
+        for _ in range(order - 1):
+            fine.step(per)
+            hist.insert(0, fine.omega())
+        fine.close()
+        st = NSStepper(ctx, hist[0][0], hist[0][1], reynolds, h, order, **kw)
+        replay = []
+        if not disable_nonlinear:
+            for i in range(len(hist) - 1, 0, -1):
+                v = ctx.velocity_from_vorticity(*hist[i])
+                replay.insert(0, ctx.nonlinear_term(v[0], v[1], hist[i][0], hist[i][1], dealias_two_thirds))
+        st.seed(hist, replay, (order - 1) * h, order - 1)
+        first = order - 1
+    else:
+        st = NSStepper(ctx, lam0, gam0, reynolds, h, order, **kw)
+    for s in range(first, steps):
+        st.step()
+        if output_every > 0 and (s + 1) % output_every == 0:
+            snaps.append(st.omega())
+            times.append(st.time)
+    om = st.omega()
+    out = dict(final_omega=om, final_time=st.time, snapshots=snaps, snapshot_times=times)
+    st.close()
+    return out
 
 
 def _field_arg(ctx, x, what):

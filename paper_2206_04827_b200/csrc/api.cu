@@ -687,6 +687,24 @@ ccf_status ccf_ns_step(ccf_ns_state* st, int nsteps) {
     });
 }
 
+// NSStepper::seed (ptns.cpp:195-203, ptns.hpp:110-112): install a prebuilt history, newest first
+ccf_status ccf_ns_seed(ccf_ns_state* st, int n_omega, const double* const* lam_hist, const double* const* gam_hist,
+                       int n_nonlinear, const double* const* nl_lam, const double* const* nl_gam, double time,
+                       int steps_taken) {
+    if (!st) return CCF_INTERNAL_ERROR;
+    return guard(st->ctx, [&](Ctx& c) {
+        c.require_unsharded("ccf_ns_seed");
+        if (n_omega < 1 || !lam_hist || !gam_hist) throw Error(ccf::DOMAIN_ERROR, "NSStepper::seed: empty history");
+        if (n_nonlinear > 0 && (!nl_lam || !nl_gam))
+            throw Error(ccf::DOMAIN_ERROR, "NSStepper::seed: nonlinear history pointers required");
+        for (int i = 0; i < n_omega; ++i)
+            if (!lam_hist[i] || !gam_hist[i]) throw Error(ccf::DOMAIN_ERROR, "NSStepper::seed: null history tensor");
+        for (int i = 0; i < n_nonlinear; ++i)
+            if (!nl_lam[i] || !nl_gam[i]) throw Error(ccf::DOMAIN_ERROR, "NSStepper::seed: null history tensor");
+        st->st.seed(n_omega, lam_hist, gam_hist, n_nonlinear, nl_lam, nl_gam, time, steps_taken);
+    });
+}
+
 ccf_status ccf_ns_get_omega(ccf_ns_state* st, double* lam, double* gam, double* time, int* steps_taken) {
     if (!st) return CCF_INTERNAL_ERROR;
     return guard(st->ctx, [&](Ctx& c) {

@@ -2022,7 +2022,7 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
         DevSet& pset = c.set(false, true, 1.0);
         if (!disable_nonlinear) {
             c.mark("start");
-            if (steps == 0) {
+            if (coeff_first) {
                 // initial data: omega_0 need not lie in the range of QL PL, so the first nonlinear term runs on
                 // the coefficient-space omega_0 and psi = QL Z_P QR, exactly as the reference
                 if (zp_head != cur) {
@@ -2199,10 +2199,59 @@ void NSState::omega_coeff() {
     coeff_head = head;
 }
 
+// NSStepper::seed (ptns.cpp:195-203): install a prebuilt history (reference-layout coefficient tensors on the
+// host or the device, newest first). nonlinear_hist[i] belongs to omega_hist[i + 1]: the next step pushes
+// N(omega_hist[0]) in front (ptns.cpp:232). Only the entries a step can read are kept (<= 4 of each).
+void NSState::seed(int n_omega, const double* const* lam_h, const double* const* gam_h, int n_nl,
+                   const double* const* nl_l, const double* const* nl_g, double t, int steps_taken) {
+    Pipeline& P = *pl;
+    Ctx& c = P.c;
+    if (n_omega < 1) throw Error(DOMAIN_ERROR, "NSStepper::seed: empty history");
+    if (scalar) throw Error(CONFIG_ERROR, "NSStepper::seed: not an NS stepper");
+    const int no = std::min(n_omega, 4);
+    const int nn = disable_nonlinear ? 0 : std::min(std::max(n_nl, 0), 4);
+    DevSet* pset = eigen ? &c.set(false, true, 1.0) : nullptr;
+    for (int i = 0; i < no; ++i) {
+        const int r = (head + i) % 5;
+        c.load_coeff(lam_h[i], lam[r].p, false, 0, 0);
+        c.load_coeff(gam_h[i], gam[r].p, false, 0, 1);
+        if (eigen) {
+            P.to_eigen(*pset, lam[r].p, zl[r].p);
+            P.to_eigen(*pset, gam[r].p, zg[r].p);
+        }
+    }
+    if (nn > 0 && eigen && ctmp.n < size_t(P.T)) ctmp.alloc(size_t(P.T));
+    for (int i = 0; i < nn; ++i) {
+        const int r = (nhead + i) % 5;
+        if (eigen) {  // N~ = PL_P N PR
+            c.load_coeff(nl_l[i], ctmp.p, false, 0, 0);
+            P.to_eigen(*pset, ctmp.p, nl[r].p);
+            c.load_coeff(nl_g[i], ctmp.p, false, 0, 1);
+            P.to_eigen(*pset, ctmp.p, ng[r].p);
+        } else {
+            c.load_coeff(nl_l[i], nl[r].p, false, 0, 0);
+            c.load_coeff(nl_g[i], ng[r].p, false, 0, 1);
+        }
+    }
+    c.sync();
+    ocount = no;
+    ncount = std::min(nn, order);
+    time = t;
+    steps = steps_taken;
+    coeff_head = head;
+    coeff_first = true;
+    zp_head = zv_head = -1;
+    zvalid = false;
+    if (P.zw_owner_ == this) P.zw_owner_ = nullptr;
+}
+
 void NSState::step_once() {
     Ctx& c = pl->c;
+    // bdf_rhs (timestep.cpp:41-42)
+    if (ocount < std::min(order, steps + 1))
+        throw Error(DOMAIN_ERROR, "bdf_rhs: insufficient history for the requested order");
     // scratch 3..5 may have been reused (another stepper, a standalone nonlinear call) since our last step
-    if (eigen && !disable_nonlinear && steps > 0 && pl->zw_owner_ != this) {
+    if (eigen && !disable_nonlinear && !coeff_first && pl->zw_owner_ != this) {
         zsynth_omega(head);
         if (zv_head != head) velocity(head);  // a replayed graph has no Poisson stage
     }
@@ -2214,7 +2263,7 @@ void NSState::step_once() {
     const bool steady = (b == order) && (disable_nonlinear || ncount == order);
     const int key = head * 5 + nhead;
     // host-mode rank barriers synchronise inside the step: no graph capture
-    if (use_graphs && steady && steps >= order + 1 && c.sh.mode != Shard::HOST && !forced) {
+    if (use_graphs && steady && steps >= order + 1 && c.sh.mode != Shard::HOST && !forced && !coeff_first) {
         if (!graphs[key]) {
             cudaGraph_t g;
             const long l0 = c.launches;
@@ -2240,6 +2289,8 @@ void NSState::step_once() {
         nhead = nnew;
         ncount = ncnt;
     }
+    ocount = std::min(ocount + 1, order);
+    coeff_first = false;
     ++steps;
     time += h;
 }

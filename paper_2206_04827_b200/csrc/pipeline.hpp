@@ -212,6 +212,10 @@ struct NSState {
     Pipeline* pl = nullptr;
     double reynolds = 100, h = 1e-2;
     int order = 4, steps = 0;
+    int ocount = 1;  // valid omega history entries (1 after construction; NSStepper::seed installs up to 4)
+    // the next step's nonlinear term runs on the coefficient-space omega of the head slot (initial data or a
+    // seeded history need not lie in the range of the modal basis); such a step is never graph-captured
+    bool coeff_first = true;
     bool disable_nonlinear = false;
     bool dealias = false;        // NSConfig::dealias_two_thirds
     bool gamma_psi = false;      // NSConfig::compute_gamma_psi (evaluated on read, ccf_ns_gamma_psi)
@@ -243,6 +247,8 @@ struct NSState {
     void zsynth_omega(int r);
     void velocity(int r);
     void omega_coeff();
+    void seed(int n_omega, const double* const* lam_h, const double* const* gam_h, int n_nl,
+              const double* const* nl_l, const double* const* nl_g, double t, int steps_taken);
     void step_once();
     void enqueue(int b, int eo, int cur, int out, int nnew);
 };

@@ -37,6 +37,48 @@ int main(int argc, char** argv) {
     nc.reynolds = 100.0;
     nc.h = 1e-3;
     NSRunResult run = ns_run(nc, curl_pt(PTScalars(f, u)), 3);
+    // ns_run with the substeps bootstrap (ptns.cpp:272-311) equals its restatement from the public pieces
+    // (fine BDF2 run, replayed nonlinear terms, NSStepper::seed), and seed() refuses an empty history
+    NSConfig ns3 = nc;
+    ns3.order = 3;
+    ns3.bootstrap = NSBootstrap::substeps;
+    const PTScalars w0 = curl_pt(PTScalars(f, u));
+    NSRunResult sub = ns_run(ns3, w0, 4, 2);
+    double seed_err = 1.0;
+    bool seed_threw = false;
+    {
+        NSConfig fine_c = ns3;
+        fine_c.order = 2;
+        fine_c.h = ns3.h / 32;
+        fine_c.bootstrap = NSBootstrap::ramp;
+        std::deque<PTScalars> hist{w0}, replay;
+        {
+            NSStepper fine(fine_c, w0);
+            for (int big = 1; big <= 2; ++big) {
+                fine.steps(32);
+                hist.push_front(fine.omega());
+            }
+        }
+        for (int i = 2; i >= 1; --i) replay.push_front(nonlinear_term(velocity_from_vorticity(hist[size_t(i)]), hist[size_t(i)]));
+        NSStepper st(ns3, hist.front());
+        st.seed(hist, replay, 2 * ns3.h, 2);
+        st.steps(2);
+        const PTScalars& o = st.omega();
+        double d = 0, mxo = 0;
+        for (size_t i = 0; i < o.lambda.data.size(); ++i) {
+            d = std::max({d, std::abs(o.lambda.data[i] - sub.final_omega.lambda.data[i]),
+                          std::abs(o.gamma.data[i] - sub.final_omega.gamma.data[i])});
+            mxo = std::max({mxo, std::abs(o.lambda.data[i]), std::abs(o.gamma.data[i])});
+        }
+        seed_err = d / mxo;
+        try {
+            st.seed({}, {}, 0.0, 0);
+        } catch (const DomainError&) {
+            seed_threw = true;
+        }
+    }
+    const bool seed_ok = seed_err < 1e-13 && seed_threw && sub.snapshots.size() == 1 && sub.snapshot_times.size() == 1 &&
+                         std::abs(sub.snapshot_times[0] - 4 * ns3.h) < 1e-15 && std::abs(sub.final_time - 4 * ns3.h) < 1e-15;
     bool threw = false;
     try {
         GridSpec bad(m, m, 7);
@@ -100,7 +142,7 @@ int main(int argc, char** argv) {
     const CoeffTensor rd = std::get<CoeffTensor>(read_field("/tmp/shim_lambda.ccf"));
     const bool io_ok = rd.data == run.final_omega.lambda.data && crc32_ieee(reinterpret_cast<const uint8_t*>("123456789"), 9) == 0xCBF43926u;
     std::printf("shim ok: roundtrip %.3e final_time %.6f domain_error %d heat_err %.3e io %d spec_errors %d/6 "
-                "worst_residual %.3e\n", err / mx, run.final_time, int(threw), herr / hmx, int(io_ok), spec_errors,
-                hr.worst_residual);
-    return (err / mx < 1e-12 && threw && herr / hmx < 1e-4 && io_ok && spec_ok) ? 0 : 1;
+                "worst_residual %.3e seed %d (%.2e)\n", err / mx, run.final_time, int(threw), herr / hmx, int(io_ok), spec_errors,
+                hr.worst_residual, int(seed_ok), seed_err);
+    return (err / mx < 1e-12 && threw && herr / hmx < 1e-4 && io_ok && spec_ok && seed_ok) ? 0 : 1;
 }

@@ -85,6 +85,10 @@ struct CoeffTensor {
         for (size_t i = 0; i < data.size(); ++i) data[i] += o.data[i];
         return *this;
     }
+    CoeffTensor& operator*=(Complex s) {  // coeffs.cpp:31-34
+        for (Complex& c : data) c *= s;
+        return *this;
+    }
     double max_abs() const {
         double v = 0;
         for (const Complex& c : data) v = std::max(v, std::abs(c));

@@ -551,7 +551,7 @@ class NSStepper:
         vp = C.c_void_p
 
         def arr(rows, j):
-            return (vp * max(len(rows), 1))(*[vp(_addr(r[j])) for r in rows])
+            return (vp * max(len(rows), 1))(*[_addr(r[j]) for r in rows])
 
         self.ctx._check(lib().ccf_ns_seed(self.h, no, arr(keep[:no], 0), arr(keep[:no], 1), nn, arr(keep[no:], 0),
                                           arr(keep[no:], 1), C.c_double(time), int(steps_taken)))

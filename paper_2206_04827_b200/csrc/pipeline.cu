@@ -1224,6 +1224,7 @@ bool Pipeline::modal_solve_from_z(DevSet& set, double w, double* out) {
     g4.launch(c.stream, nullptr, nullptr, out, out);
     c.gemm_flops += g4.flops();
     c.launches += 2;
+    z_owner_ = nullptr;  // dZ_ was scaled in place
     return true;
 }
 
@@ -1236,6 +1237,7 @@ void Pipeline::modal_solve(DevSet& set, bool full, int ntensor, const double* co
                            const double* const* src1, const double* w1, int n1, double* out0, double* out1,
                            const char* rhs_mark) {
     last_z_valid_ = false;
+    z_owner_ = nullptr;
     if (!set.host.has_diag || !set.dg) {
         c.run_adi(set, full, ntensor, src0, w0, n0, src1, w1, n1, out0, out1);
         return;
@@ -2085,7 +2087,8 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
             c.mark("start");
             // velocity_from_vorticity, ptns.cpp:85-91: lambda_psi = Poisson3D(-lambda_omega); after the first
             // step lambda_omega comes from our Helmholtz solve in the shared modal basis (modal_solve_from_z)
-            if (!(zvalid && P.modal_solve_from_z(c.set(false, true, 1.0), -1.0, lpsi))) P.poisson(lw, -1.0, lpsi);
+            if (!(zvalid && P.z_owner_ == this && P.modal_solve_from_z(c.set(false, true, 1.0), -1.0, lpsi)))
+                P.poisson(lw, -1.0, lpsi);
             c.mark("P_poisson_solve");
             P.nonlinear(gw, lpsi, lw, gw, nl[nnew].p, ng[nnew].p, nullptr, false, false, dealias);  // nonlinear_term(v, omega)
         }
@@ -2116,6 +2119,7 @@ void NSState::enqueue(int b, int eo, int cur, int out, int nnew) {
             P.modal_solve(set, false, 2, sl, wl, ns, sg, wl, ns, lam[out].p, gam[out].p, "H_rhs_combine");
         c.mark("H_helmholtz_solve");
         zvalid = P.last_z_valid_;  // Z of lambda_omega(out) stays in dZ_ (shared modal basis) for the next P
+        if (zvalid) P.z_owner_ = this;
     }
     const long T = P.T;
     finite_check_kernel<<<std::min<long>(1184, (T + 255) / 256), 256, 0, c.stream>>>(lam[out].p, T, dflag);
@@ -2255,6 +2259,8 @@ void NSState::step_once() {
         zsynth_omega(head);
         if (zv_head != head) velocity(head);  // a replayed graph has no Poisson stage
     }
+    // coefficient-space state: dZ_ may have been reused (another stepper, a standalone solve) since our last step
+    if (!eigen && zvalid && pl->z_owner_ != this) zvalid = false;
     const int b = std::min(order, steps + 1);
     const int out = (head + 4) % 5;
     const int nnew = (nhead + 4) % 5;
@@ -2263,8 +2269,10 @@ void NSState::step_once() {
     const bool steady = (b == order) && (disable_nonlinear || ncount == order);
     const int key = head * 5 + nhead;
     // host-mode rank barriers synchronise inside the step: no graph capture
-    if (use_graphs && steady && steps >= order + 1 && c.sh.mode != Shard::HOST && !forced && !coeff_first) {
+    if (use_graphs && steady && phase_warm[key] && c.sh.mode != Shard::HOST && !forced && !coeff_first &&
+        (!graphs[key] || !graph_z[key] || zvalid)) {
         if (!graphs[key]) {
+            graph_z[key] = !eigen && !disable_nonlinear && zvalid;
             cudaGraph_t g;
             const long l0 = c.launches;
             CCF_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
@@ -2281,7 +2289,9 @@ void NSState::step_once() {
         const long l0 = c.launches;
         enqueue(b, eo, head, out, nnew);
         if (steady) launches_per_step = c.launches - l0;
+        phase_warm[key] = true;
     }
+    if (!eigen && !disable_nonlinear && zvalid) pl->z_owner_ = this;  // (graph replays skip enqueue)
     head = out;
     coeff_head = eigen ? -1 : head;
     if (eigen && !disable_nonlinear) zp_head = zv_head = out;  // (graph replays skip enqueue)

@@ -125,6 +125,7 @@ public:
     // ADI kernel (ctx flag bit 2 / sets without diagonalization data).
     bool modal_solve_from_z(DevSet& set, double w, double* out);
     bool last_z_valid_ = false;  // the last modal_solve left its eigen-coordinates Z in dZ_
+    const void* z_owner_ = nullptr;  // NSState whose lambda_omega Z is what dZ_ holds (any other solve clears it)
     void modal_solve(DevSet& set, bool full, int ntensor, const double* const* src0, const double* w0, int n0,
                      const double* const* src1, const double* w1, int n1, double* out0, double* out1,
                      const char* rhs_mark = nullptr);
@@ -227,6 +228,11 @@ struct NSState {
     int nhead = 0, ncount = 0;  // N ring: entry i at (nhead + i) % 5
     int* dflag = nullptr;       // device non-finite flag (NaN guard, ptns.cpp:260-262)
     cudaGraphExec_t graphs[25] = {};  // steady-state step per (head, nhead) ring phase
+    // ring phases this stepper has run eagerly once: a phase is captured only afterwards, so every pointer-keyed
+    // product plan of the phase exists before the capture (orders < 4 and seeded histories reach the steady
+    // state before all five phases have been visited)
+    bool phase_warm[25] = {};
+    bool graph_z[25] = {};  // the captured step starts from dZ_ (coefficient-space state, zvalid at capture)
     long launches_per_step = 0;
     bool use_graphs = true;
     bool zvalid = false;  // the last Helmholtz solve left Z(lambda_omega) in the shared modal basis

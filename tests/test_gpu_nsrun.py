@@ -9,7 +9,9 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-10
 
 
-def _init(m, n, p, scale=0.05):
+def _init(m, n, p, scale=1e-3):
+    # small amplitude: with O(0.1) data the reference's scheme (explicit nonlinear term, quirk Q1) blows up within
+    # the ~100 fine steps of the substeps bootstrap, on the CPU oracle and the GPU alike
     return hermitian_coeffs(m, n, p, 0.7, 21) * scale, hermitian_coeffs(m, n, p, 0.7, 22) * scale
 
 

@@ -124,6 +124,21 @@ ccf_status ccf_ns_gamma_psi(ccf_ns_state* st, double* gamma_psi);
 ccf_status ccf_ns_get_omega(ccf_ns_state* st, double* lam, double* gam, double* time, int* steps_taken);
 ccf_status ccf_ns_destroy(ccf_ns_state* st);
 
+/* Per-mode solver API (solvers.hpp:35-82, ultraop.hpp:40-53) for the context's m x n: ModalSolver(m, n, w, scale,
+ * poisson, tol) on the device. Matrices are m x n complex128, column-major (Eigen::MatrixXcd / one CoeffTensor
+ * slice), in host memory. ccf_modal_solve = ModalSolver::solve(f_full) on the raw C2 x C2 right-hand side
+ * (F = A X B + C X D convention, truncated to the top-left (m-2) x (n-2) block; any parity content; scale 0 with
+ * poisson 0 is the mass pair, solvers.cpp:57-62): exact fast diagonalization instead of the ADI iteration.
+ * ccf_modal_apply = ModalOperator::apply (ultraop.cpp:83-87), the piece of the lifted boundary data
+ * (solvers.cpp:125-140, 160-165). ccf_modal_operator: the dense row-major A (0), B (1), C (2), D (3) of raw().
+ * A handle must be destroyed before its context. */
+typedef struct ccf_modal ccf_modal;
+ccf_status ccf_modal_create(ccf_ctx* ctx, int w, double scale, int poisson, ccf_modal** out);
+ccf_status ccf_modal_solve(ccf_modal* h, const double* f_full, double* x);
+ccf_status ccf_modal_apply(ccf_modal* h, const double* x, double* y);
+ccf_status ccf_modal_operator(ccf_modal* h, int which, double* dense);
+ccf_status ccf_modal_destroy(ccf_modal* h);
+
 /* timestep.hpp:60-111 HeatStepper: (d/dt - alpha lap) T = g with the reference's BDF 1 -> order ramp,
  * homogeneous Dirichlet data. initial / forcing: kind 0 = grid values (p*n*m doubles, analyzed on the
  * device: HeatStepper(config, GridField), step_with_callback), kind 1 = coefficients (CoeffTensor).

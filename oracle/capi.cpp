@@ -187,6 +187,63 @@ int orc_nonlinear(int m, int n, int p, const double* vl, const double* vg, const
     });
 }
 
+// ---- per-mode solver API (solvers.hpp:35-82): f, x are m x n complex, column-major
+namespace {
+MatC load_mat(int m, int n, const double* x) {
+    MatC a(m, n);
+    std::memcpy(a.a.data(), x, a.a.size() * sizeof(cd));
+    return a;
+}
+}  // namespace
+// ModalSolver(m, n, w, scale, poisson, tol).solve(f_full) (solvers.cpp:46-98); scale 0: the mass pair
+int orc_modal_solve(int m, int n, int w, double scale, int poisson, double tol, const double* f, double* x, double* resid) {
+    return guard([&] {
+        ModalSolver s(m, n, w, scale, poisson != 0, tol);
+        const MatC out = s.solve(load_mat(m, n, f));
+        std::memcpy(x, out.a.data(), out.a.size() * sizeof(cd));
+        if (resid) *resid = s.last_residual();
+    });
+}
+// ModalOperator::apply (ultraop.cpp:83-87) of assemble_modal_poisson / assemble_modal_helmholtz
+int orc_modal_apply(int m, int n, int w, double scale, int poisson, const double* x, double* y) {
+    return guard([&] {
+        const ModalOperator op = poisson ? assemble_modal_poisson(m, n, w) : assemble_modal_helmholtz(m, n, w, scale);
+        const MatC out = op.apply(load_mat(m, n, x));
+        std::memcpy(y, out.a.data(), out.a.size() * sizeof(cd));
+    });
+}
+// solve_modal_helmholtz (solvers.cpp:125-140) with optional lifted boundary data (a p-mode tensor)
+int orc_modal_helmholtz(int m, int n, int w, double scale, double tol, const double* f, int lift_p, const double* lift,
+                        double* x) {
+    return guard([&] {
+        BoundaryCondition bc;
+        if (lift) {
+            bc.lifted = true;
+            bc.lift = load(m, n, lift_p, lift);
+        }
+        const MatC out = solve_modal_helmholtz(assemble_modal_helmholtz(m, n, w, scale), load_mat(m, n, f), bc, tol);
+        std::memcpy(x, out.a.data(), out.a.size() * sizeof(cd));
+    });
+}
+
+// history: `order` (>= scheme order) tensors, newest first; lift: optional lifted boundary data (timestep.cpp:52-59)
+int orc_helmholtz_step_lifted(int m, int n, int p, double diffusivity, double h, double tol, int order, int nhist,
+                              const double* const* hist, const double* forcing, const double* lift, double* out) {
+    return guard([&] {
+        BoundaryCondition bc;
+        if (lift) {
+            bc.lifted = true;
+            bc.lift = load(m, n, p, lift);
+        }
+        HelmholtzTensorStepper st(Spec(m, n, p), diffusivity, h, tol, bc);
+        std::deque<Coeff> hd;
+        for (int i = 0; i < nhist; ++i) hd.push_back(load(m, n, p, hist[i]));
+        Coeff f;
+        if (forcing) f = load(m, n, p, forcing);
+        store(st.step(hd, BDFScheme::of_order(order), forcing ? &f : nullptr), out);
+    });
+}
+
 // history: `order` (>= scheme order) tensors, newest first.
 int orc_helmholtz_step(int m, int n, int p, double diffusivity, double h, double tol, int order, int nhist,
                        const double* const* hist, const double* forcing, double* out) {

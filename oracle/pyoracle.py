@@ -75,7 +75,8 @@ def lib():
                      "orc_ns_step", "orc_ns_get", "orc_heat_step", "orc_heat_get", "orc_compute_shifts",
                      "orc_modal_plan", "orc_pencil_range", "orc_adi_vs_dense", "orc_operator_dense",
                      "orc_pencil_dense", "orc_jacobi", "orc_mobius_from_points", "orc_points", "orc_evaluate_at",
-                     "orc_ns_step_sample"]:
+                     "orc_ns_step_sample", "orc_modal_solve", "orc_modal_apply", "orc_modal_helmholtz",
+                     "orc_helmholtz_step_lifted"]:
             getattr(L, name).restype = C.c_int
         L.orc_last_error.restype = C.c_char_p
         L.orc_ns_create.restype = C.c_void_p
@@ -198,14 +199,55 @@ def hpoisson(rhs):
     return out
 
 
-def helmholtz_step(hist, order, diffusivity, h, tol=1e-12, forcing=None):
+def helmholtz_step(hist, order, diffusivity, h, tol=1e-12, forcing=None, lift=None):
     hs = [_cz(x) for x in hist]
     p, n, m = hs[0].shape
     arr = (C.POINTER(C.c_double) * len(hs))(*[_p(x) for x in hs])
     out = np.zeros_like(hs[0])
     fc = _cz(forcing) if forcing is not None else None
+    if lift is not None:
+        _chk(lib().orc_helmholtz_step_lifted(m, n, p, C.c_double(diffusivity), C.c_double(h), C.c_double(tol), int(order),
+                                              len(hs), arr, _p(fc), _p(_cz(lift)), _p(out)))
+        return out
     _chk(lib().orc_helmholtz_step(m, n, p, C.c_double(diffusivity), C.c_double(h), C.c_double(tol), int(order),
                                    len(hs), arr, _p(fc), _p(out)))
+    return out
+
+
+# ---------------------------------------------------------------- per-mode solver API (solvers.hpp:35-82)
+def _cm(x):
+    """(n, m) numpy view of an m x n column-major complex matrix: a[k, j] = X(j, k)."""
+    return np.ascontiguousarray(x, dtype=np.complex128)
+
+
+def modal_solve(f, w, scale=1.0, poisson=True, tol=1e-12):
+    """ModalSolver(m, n, w, scale, poisson, tol).solve(f_full) -> (x, last_residual); f[k, j] = F(j, k)."""
+    a = _cm(f)
+    n, m = a.shape
+    out = np.zeros_like(a)
+    r = C.c_double()
+    _chk(lib().orc_modal_solve(m, n, int(w), C.c_double(scale), int(bool(poisson)), C.c_double(tol), _p(a), _p(out),
+                               C.byref(r)))
+    return out, r.value
+
+
+def modal_apply(x, w, scale=1.0, poisson=True):
+    """ModalOperator::apply (A X B + C X D) of the Poisson / Helmholtz quadruple."""
+    a = _cm(x)
+    n, m = a.shape
+    out = np.zeros_like(a)
+    _chk(lib().orc_modal_apply(m, n, int(w), C.c_double(scale), int(bool(poisson)), _p(a), _p(out)))
+    return out
+
+
+def modal_helmholtz(f, w, scale, tol=1e-12, lift=None):
+    """solve_modal_helmholtz(assemble_modal_helmholtz(m, n, w, scale), f, bc, tol); lift: (p, n, m) tensor."""
+    a = _cm(f)
+    n, m = a.shape
+    out = np.zeros_like(a)
+    lf = _cz(lift) if lift is not None else None
+    _chk(lib().orc_modal_helmholtz(m, n, int(w), C.c_double(scale), C.c_double(tol), _p(a),
+                                   lf.shape[0] if lf is not None else 0, _p(lf), _p(out)))
     return out
 
 

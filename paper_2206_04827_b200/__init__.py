@@ -88,7 +88,8 @@ EXPORTS = ["ccf_ctx_create", "ccf_ctx_destroy", "ccf_ctx_set_stream", "ccf_ctx_s
            "ccf_shard_open_ipc", "ccf_shard_link_local", "ccf_shard_set_host_barrier", "ccf_write_field",
            "ccf_read_field_header", "ccf_read_field", "ccf_crc32", "ccf_ns_write_omega", "ccf_heat_create",
            "ccf_heat_step", "ccf_heat_get", "ccf_ns_create_ex", "ccf_ns_velocity", "ccf_ns_gamma_psi",
-           "ccf_nonlinear_ex", "ccf_ns_seed"]
+           "ccf_nonlinear_ex", "ccf_ns_seed", "ccf_modal_create", "ccf_modal_solve", "ccf_modal_apply",
+           "ccf_modal_operator", "ccf_modal_destroy"]
 
 HOST_BARRIER_FN = C.CFUNCTYPE(None, C.c_void_p)
 SHARD_HANDLE_BYTES = 128  # include/ccf.h CCF_SHARD_HANDLE_BYTES
@@ -172,6 +173,11 @@ def lib():
         L.ccf_heat_get.argtypes = [vp, vp, dp, C.POINTER(C.c_int)]
         L.ccf_ns_create_ex.argtypes = [vp, C.c_double, C.c_double, C.c_int, C.c_int, vp, vp, C.POINTER(vp)]
         L.ccf_ns_velocity.argtypes = [vp, vp, vp]
+        L.ccf_modal_create.argtypes = [vp, C.c_int, C.c_double, C.c_int, C.POINTER(vp)]
+        L.ccf_modal_solve.argtypes = [vp, vp, vp]
+        L.ccf_modal_apply.argtypes = [vp, vp, vp]
+        L.ccf_modal_operator.argtypes = [vp, C.c_int, vp]
+        L.ccf_modal_destroy.argtypes = [vp]
         L.ccf_ns_seed.argtypes = [vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.c_int, C.POINTER(vp), C.POINTER(vp),
                                   C.c_double, C.c_int]
         L.ccf_ns_gamma_psi.argtypes = [vp, vp]
@@ -306,10 +312,43 @@ class Context:
         return out
 
     # ---- solvers (solvers.hpp:86-94)
-    def solve_poisson_3d(self, f):
+    def _lift_correction(self, lift, scale, poisson):
+        """Lifted Dirichlet data (BoundaryCondition::lifted, solvers.cpp:160-165, timestep.cpp:84-101): the modal
+        solves are linear, so solve(F_l - op_l.apply(lift_l)) + lift_l = solve(F_l) + c_l with
+        c_l = lift_l - solve(op_l.apply(lift_l)), computed per |w| on the device (ModalSolver) and
+        parity-projected like the output."""
+        lf = np.asarray(lift)
+        p, n, m = self.shape()
+        if lf.ndim != 3 or lf.shape[1:] != (n, m):
+            raise DomainError("BoundaryCondition: lift tensor has wrong dimensions")
+        if lf.shape[0] != p:
+            raise DomainError("BoundaryCondition: lift tensor misses the requested mode")
+        out = np.zeros((p, n, m), np.complex128)
+        solvers = {}
+        try:
+            for l in range(p):
+                sl = np.ascontiguousarray(lf[l], dtype=np.complex128)
+                if not sl.any():
+                    continue
+                w = l - p // 2
+                s = solvers.get(abs(w))
+                if s is None:
+                    s = solvers[abs(w)] = ModalSolver(self, abs(w), scale, poisson)
+                c = sl - s.solve(s.apply(sl))
+                c[:, (np.arange(m) + w) % 2 != 0] = 0.0  # parity_project (coeffs.cpp:50-65)
+                out[l] = c
+        finally:
+            for s in solvers.values():
+                s.close()
+        return out
+
+    def solve_poisson_3d(self, f, lift=None):
+        """solve_poisson_3d (solvers.cpp:142-175); lift: BoundaryCondition::lifted(lift) data."""
         c = self._coef(f, "solve_poisson_3d")
         out = self._out_c()
         self._check(lib().ccf_poisson3d(self.h, _addr(c), _addr(out)))
+        if lift is not None:
+            out += self._lift_correction(lift, 1.0, True)
         return out
 
     def solve_horizontal_poisson(self, rhs):
@@ -318,13 +357,17 @@ class Context:
         self._check(lib().ccf_hpoisson(self.h, _addr(c), _addr(out)))
         return out
 
-    def helmholtz_step(self, history, order, diffusivity, h, forcing=None):
+    def helmholtz_step(self, history, order, diffusivity, h, forcing=None, lift=None):
+        """HelmholtzTensorStepper(spec, diffusivity, h, tol, bc).step (timestep.cpp:61-108); lift: lifted bc data."""
         hs = [self._coef(x, "HelmholtzTensorStepper: history") for x in history]
         arr = (C.c_void_p * len(hs))(*[x.ctypes.data for x in hs])
         fc = self._coef(forcing, "HelmholtzTensorStepper: forcing")
         out = self._out_c()
         self._check(lib().ccf_helmholtz_step(self.h, arr, len(hs), int(order), _addr(fc), C.c_double(diffusivity),
                                              C.c_double(h), _addr(out)))
+        if lift is not None:
+            kappa = (1.0, 2.0 / 3.0, 6.0 / 11.0, 12.0 / 25.0)[int(order) - 1] * h
+            out += self._lift_correction(lift, kappa * diffusivity, False)
         return out
 
     # ---- PT / NS (ptns.hpp:47-70)
@@ -524,6 +567,79 @@ def read_field(path, out=None):
     _free_check(lib().ccf_read_field(os.fsencode(path), *[C.byref(x) for x in v], _addr(out), cap))
     assert cap >= count * (2 if h["kind"] == 1 else 1)
     return out
+
+
+class ModalSolver:
+    """proj/include/cylspec/solvers.hpp:35-59 ModalSolver(m, n, w, scale, poisson, tol) on the device (m, n from the
+    context). Matrices are (n, m) complex arrays a[k, j] = X(j, k): the memory of the reference's column-major
+    m x n Eigen::MatrixXcd / one CoeffTensor slice. scale = 0 with poisson = False is the mass pair."""
+
+    def __init__(self, ctx: Context, w, scale=1.0, poisson=True):
+        self.ctx, self.w, self.scale, self.poisson = ctx, int(w), float(scale), bool(poisson)
+        p, n, m = ctx.shape()
+        self.shape = (n, m)
+        h = C.c_void_p()
+        ctx._check(lib().ccf_modal_create(ctx.h, self.w, C.c_double(self.scale), int(self.poisson), C.byref(h)))
+        self.h = h
+
+    def _mat(self, x, what):
+        a = np.asarray(x)
+        if a.shape != self.shape:
+            raise DomainError(f"{what}: right-hand side has wrong shape")  # solvers.cpp:79-80
+        return np.ascontiguousarray(a, dtype=np.complex128)
+
+    def solve(self, f_full):
+        """ModalSolver::solve (solvers.cpp:77-98): raw C2 x C2 right-hand side -> m x n coefficients."""
+        f = self._mat(f_full, "ModalSolver::solve")
+        x = np.zeros_like(f)
+        self.ctx._check(lib().ccf_modal_solve(self.h, _addr(f), _addr(x)))
+        return x
+
+    def apply(self, x):
+        """raw().apply(x) = A x B + C x D (ultraop.cpp:83-87)."""
+        a = self._mat(x, "ModalOperator::apply")
+        y = np.zeros_like(a)
+        self.ctx._check(lib().ccf_modal_apply(self.h, _addr(a), _addr(y)))
+        return y
+
+    def operator(self, which):
+        """Dense A | B | C | D of raw() (ultraop.cpp:89-123)."""
+        n, m = self.shape
+        k = "ABCD".index(which)
+        out = np.zeros((m, m) if k % 2 == 0 else (n, n))
+        self.ctx._check(lib().ccf_modal_operator(self.h, k, _addr(out)))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None) and getattr(self.ctx, "h", None):
+            lib().ccf_modal_destroy(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solve_modal_helmholtz(ctx: Context, f, w, scale, lift=None):
+    """solve_modal_helmholtz (solvers.cpp:125-140): x = solve(f - op.apply(lift_w)) + lift_w; lift: a (p', n, m)
+    tensor whose slice w + p'/2 carries the boundary data (BoundaryCondition::lifted)."""
+    s = ModalSolver(ctx, w, scale, poisson=False)
+    try:
+        rhs = s._mat(f, "solve_modal_helmholtz")
+        if lift is None:
+            return s.solve(rhs)
+        lf = np.asarray(lift)
+        if lf.ndim != 3 or lf.shape[1:] != s.shape:
+            raise DomainError("BoundaryCondition: lift tensor has wrong dimensions")
+        l = int(w) + lf.shape[0] // 2
+        if l < 0 or l >= lf.shape[0]:
+            raise DomainError("BoundaryCondition: lift tensor misses the requested mode")
+        sl = np.ascontiguousarray(lf[l], dtype=np.complex128)
+        return s.solve(rhs - s.apply(sl)) + sl
+    finally:
+        s.close()
 
 
 class NSStepper:

@@ -80,6 +80,11 @@ void bdf_scheme(int b, double* kappa_over_h, double w[4]) {
 
 }  // namespace
 
+// context guard for the other translation units of the C-ABI (modalapi.cu)
+ccf_status ccf_ctx_guard(ccf_ctx* ctx, void (*fn)(ccf::Ctx&, void*), void* user) {
+    return guard(ctx, [&](Ctx& c) { fn(c, user); });
+}
+
 extern "C" {
 
 const char* ccf_version(void) { return "ccf-b200 0.1 (sm_100a)"; }

@@ -286,4 +286,41 @@ DiagRight diag_right(const CBand& Btb, const CBand& Dtb, const CBand& C02b, int 
     return out;
 }
 
+DiagLeft mass_left(const CBand& Ab, int M, int mh) {
+    const BandOp A = from_band(Ab, M);
+    LMat PL(M, mh);
+    for (int a = 0; a < M; ++a) PL(a, a) = 1.0L;
+    if (!dense_solve(A.m, PL)) throw Error(SINGULAR, "mass solve: R2 block is singular");
+    LMat QL(mh, M);  // S_r
+    for (int a = 0; a < mh; ++a)
+        for (int e = 0; e < M; ++e) QL(a, e) = (a == e ? 1.0L : 0.0L) - (a == e + 1 ? 1.0L : 0.0L);
+    DiagLeft out;
+    out.PL = to_double(PL);
+    out.PL_ld = PL.a;
+    out.QL = to_double(QL);
+    out.lam.assign(size_t(M), 0.0);
+    out.lam_ld.assign(size_t(M), 0.0L);
+    return out;
+}
+
+DiagRight mass_right(const CBand& Btb, int N, int nh) {
+    // Y B^ = E  <=>  B^^T Y^T = E^T: invert Bt = B^^T and transpose
+    const BandOp Bt = from_band(Btb, N);
+    LMat inv(N, N);
+    for (int i = 0; i < N; ++i) inv(i, i) = 1.0L;
+    if (!dense_solve(Bt.m, inv)) throw Error(SINGULAR, "mass solve: C02 block is singular");
+    LMat PR(nh, N);  // rows < N: B^^-1 = (Bt^-1)^T
+    for (int x = 0; x < N; ++x)
+        for (int e = 0; e < N; ++e) PR(x, e) = inv(e, x);
+    LMat QR(N, nh);  // S_z^T
+    for (int i = 0; i < N; ++i)
+        for (int b = 0; b < nh; ++b) QR(i, b) = (b == i ? 1.0L : 0.0L) - (b == i + 1 ? 1.0L : 0.0L);
+    DiagRight out;
+    out.PR = to_double(PR);
+    out.QR = to_double(QR);
+    out.mu.assign(size_t(N), 0.0);
+    out.mu_ld.assign(size_t(N), 0.0L);
+    return out;
+}
+
 }  // namespace ccf

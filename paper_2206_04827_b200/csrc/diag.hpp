@@ -40,5 +40,10 @@ DiagLeft diag_left(const CBand& A, const CBand& C, const CBand& R2, int M, int m
 // B^ = Bt^T, D^ = Dt^T) and C02 (rows N, cols nh, offsets 0..2).
 DiagRight diag_right(const CBand& Bt, const CBand& Dt, const CBand& C02, int N, int nh);
 
+// Mass-only pair (Helmholtz scale 0, solvers.cpp:57-62, 84-91): X = A^-1 E B^^-1 with A = Ab (R2 recombined, one
+// parity block) and B^ = Bt^T (C02 recombined), in the same four-product form u = QL [(PL f PR) .* 1] QR:
+// PL = A^-1 [I | 0] (M x mh), QL = S_r (mh x M); PR = [I ; 0] B^^-1 (nh x N), QR = S_z^T (N x nh).
+DiagLeft mass_left(const CBand& Ab, int M, int mh);
+DiagRight mass_right(const CBand& Bt, int N, int nh);
 
 }  // namespace ccf

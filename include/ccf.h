@@ -131,7 +131,8 @@ ccf_status ccf_ns_destroy(ccf_ns_state* st);
  * poisson 0 is the mass pair, solvers.cpp:57-62): exact fast diagonalization instead of the ADI iteration.
  * ccf_modal_apply = ModalOperator::apply (ultraop.cpp:83-87), the piece of the lifted boundary data
  * (solvers.cpp:125-140, 160-165). ccf_modal_operator: the dense row-major A (0), B (1), C (2), D (3) of raw().
- * A handle must be destroyed before its context. */
+ * Destroying the context first releases the handle's device data; later calls on the handle then report
+ * CCF_INTERNAL_ERROR and ccf_modal_destroy only frees it. */
 typedef struct ccf_modal ccf_modal;
 ccf_status ccf_modal_create(ccf_ctx* ctx, int w, double scale, int poisson, ccf_modal** out);
 ccf_status ccf_modal_solve(ccf_modal* h, const double* f_full, double* x);

@@ -17,6 +17,7 @@
 #include <variant>
 #include <functional>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -71,6 +72,51 @@ struct GridField {
     double at(int j, int k, int l) const { return values[index(j, k, l)]; }
 };
 
+// Minimal column-major complex matrix standing in for Eigen::MatrixXcd in the three Eigen-typed signatures of the
+// per-mode API (solvers.hpp:43, coeffs.hpp:23-28): same memory layout, (i, j) access, rows() / cols() / data().
+class MatrixXcd {
+public:
+    MatrixXcd() = default;
+    MatrixXcd(int rows, int cols) : r_(rows), c_(cols), d_(size_t(rows) * size_t(cols), Complex(0)) {}
+    static MatrixXcd Zero(int rows, int cols) { return MatrixXcd(rows, cols); }
+    int rows() const { return r_; }
+    int cols() const { return c_; }
+    size_t size() const { return d_.size(); }
+    Complex& operator()(int i, int j) { return d_[size_t(j) * size_t(r_) + size_t(i)]; }
+    Complex operator()(int i, int j) const { return d_[size_t(j) * size_t(r_) + size_t(i)]; }
+    Complex* data() { return d_.data(); }
+    const Complex* data() const { return d_.data(); }
+    MatrixXcd& operator+=(const MatrixXcd& o) { return zip(o, 1.0); }
+    MatrixXcd& operator-=(const MatrixXcd& o) { return zip(o, -1.0); }
+    MatrixXcd& operator*=(Complex s) {
+        for (Complex& v : d_) v *= s;
+        return *this;
+    }
+    friend MatrixXcd operator+(MatrixXcd a, const MatrixXcd& b) { return a += b; }
+    friend MatrixXcd operator-(MatrixXcd a, const MatrixXcd& b) { return a -= b; }
+    friend MatrixXcd operator*(Complex s, MatrixXcd a) { return a *= s; }
+    friend MatrixXcd operator*(double s, MatrixXcd a) { return a *= Complex(s); }
+    double max_abs() const {  // cwiseAbs().maxCoeff()
+        double v = 0;
+        for (const Complex& x : d_) v = std::max(v, std::abs(x));
+        return v;
+    }
+    double norm() const {
+        double v = 0;
+        for (const Complex& x : d_) v += std::norm(x);
+        return std::sqrt(v);
+    }
+
+private:
+    MatrixXcd& zip(const MatrixXcd& o, double sgn) {
+        if (o.r_ != r_ || o.c_ != c_) throw DomainError("MatrixXcd: shape mismatch");
+        for (size_t i = 0; i < d_.size(); ++i) d_[i] += sgn * o.d_[i];
+        return *this;
+    }
+    int r_ = 0, c_ = 0;
+    std::vector<Complex> d_;
+};
+
 struct CoeffTensor {
     GridSpec spec;
     std::vector<Complex> data;
@@ -84,6 +130,15 @@ struct CoeffTensor {
         if (!(spec == o.spec)) throw DomainError("CoeffTensor: spec mismatch");
         for (size_t i = 0; i < data.size(); ++i) data[i] += o.data[i];
         return *this;
+    }
+    MatrixXcd slice(int l) const {  // coeffs.hpp:23-28 (a copy; the reference returns an Eigen::Map)
+        MatrixXcd o(spec.m, spec.n);
+        std::copy(data.begin() + long(l) * spec.m * spec.n, data.begin() + long(l + 1) * spec.m * spec.n, o.data());
+        return o;
+    }
+    void set_slice(int l, const MatrixXcd& x) {
+        if (x.rows() != spec.m || x.cols() != spec.n) throw DomainError("CoeffTensor: slice shape mismatch");
+        std::copy(x.data(), x.data() + x.size(), data.begin() + long(l) * spec.m * spec.n);
     }
     CoeffTensor& operator*=(Complex s) {  // coeffs.cpp:31-34
         for (Complex& c : data) c *= s;
@@ -134,8 +189,17 @@ struct VectorFieldCoeffs {
     explicit VectorFieldCoeffs(const GridSpec& s) : comp_r(s), comp_theta(s), comp_z(s) {}
 };
 
-struct BoundaryCondition {  // homogeneous Dirichlet only on the B200 path (solvers.hpp:18-31)
+struct BoundaryCondition {  // solvers.hpp:18-31
+    enum class Kind { dirichlet_homogeneous, dirichlet_lifted };
+    Kind kind = Kind::dirichlet_homogeneous;
+    std::optional<CoeffTensor> lift;
     static BoundaryCondition homogeneous() { return {}; }
+    static BoundaryCondition lifted(CoeffTensor lift_tensor) {
+        BoundaryCondition bc;
+        bc.kind = Kind::dirichlet_lifted;
+        bc.lift = std::move(lift_tensor);
+        return bc;
+    }
 };
 
 inline constexpr double kDefaultAdiTol = 1e-12;
@@ -219,12 +283,199 @@ inline CoeffTensor divide_r(const CoeffTensor& f) { return detail::calc(4, f); }
 inline CoeffTensor horizontal_laplacian(const CoeffTensor& f) { return detail::calc(5, f); }
 inline CoeffTensor laplacian(const CoeffTensor& f) { return detail::calc(6, f); }
 
+// ---- per-mode API: ultraop.hpp:40-53, solvers.hpp:35-82 (ccf_modal_* on the device)
+namespace detail {
+struct ModalHandle {
+    ccf_ctx* ctx = nullptr;
+    ccf_modal* h = nullptr;
+    int m, n;
+    ModalHandle(int m_, int n_, int w, double scale, bool poisson, double tol) : m(m_), n(n_) {
+        ctx = context(GridSpec(m_, n_, 4), tol);
+        check(ccf_modal_create(ctx, w, scale, poisson ? 1 : 0, &h), ctx);
+    }
+    ~ModalHandle() { ccf_modal_destroy(h); }
+    ModalHandle(const ModalHandle&) = delete;
+    ModalHandle& operator=(const ModalHandle&) = delete;
+    std::vector<double> dense(int which) const {
+        std::vector<double> o(which % 2 == 0 ? size_t(m) * m : size_t(n) * n);
+        check(ccf_modal_operator(h, which, o.data()), ctx);
+        return o;
+    }
+};
+}  // namespace detail
+
+struct ModalOperator {  // ultraop.hpp:40-48; A, C: m x m, B, D: n x n, dense row-major (the reference's are banded)
+    int m = 0, n = 0;
+    int wavenumber = 0;
+    double scale = 0.0;
+    std::vector<double> A, B, C, D;
+    /// A X B + C X D applied to dense (complex) X, on the device (ultraop.cpp:83-87).
+    MatrixXcd apply(const MatrixXcd& x) const {
+        if (x.rows() != m || x.cols() != n) throw DomainError("ModalOperator::apply: wrong shape");
+        MatrixXcd y(m, n);
+        detail::check(ccf_modal_apply(dev->h, reinterpret_cast<const double*>(x.data()), reinterpret_cast<double*>(y.data())),
+                      dev->ctx);
+        return y;
+    }
+    std::shared_ptr<detail::ModalHandle> dev;  // device-side solver data behind apply()
+};
+namespace detail {
+inline ModalOperator modal_operator(int m, int n, int w, double scale, bool poisson, double tol = kDefaultAdiTol) {
+    ModalOperator op;
+    op.m = m;
+    op.n = n;
+    op.wavenumber = w;
+    op.scale = poisson ? 1.0 : scale;
+    op.dev = std::make_shared<ModalHandle>(m, n, w, scale, poisson, tol);
+    op.A = op.dev->dense(0);
+    op.B = op.dev->dense(1);
+    op.C = op.dev->dense(2);
+    op.D = op.dev->dense(3);
+    return op;
+}
+}  // namespace detail
+inline ModalOperator assemble_modal_helmholtz(int m, int n, int wavenumber, double scale) {  // ultraop.cpp:89-107
+    if (m < 4 || n < 4) throw DomainError("assemble_modal_helmholtz: sizes too small");
+    return detail::modal_operator(m, n, wavenumber, scale, false);
+}
+inline ModalOperator assemble_modal_poisson(int m, int n, int wavenumber) {  // ultraop.cpp:109-123
+    if (m < 4 || n < 4) throw DomainError("assemble_modal_poisson: sizes too small");
+    return detail::modal_operator(m, n, wavenumber, 1.0, true);
+}
+
+struct ShiftPlan {  // adi.hpp:19-28
+    double a = 0, b = 0, c = 0, d = 0, gamma_cr = 0, alpha_z = 0, modulus = 0, tol = 0;
+    int J = 0;
+    std::vector<double> u, v;
+};
+
+/// One Fourier mode's Helmholtz / Poisson solver (solvers.hpp:35-59). solve() is the exact fast-diagonalization
+/// solve on the device (the reference iterates ADI to `tol`); plan() is the reference's Zolotarev shift plan for the
+/// same quadruple (setup numerics, kept for parity checks), nullptr for the mass pair.
+class ModalSolver {
+public:
+    ModalSolver(int m, int n, int wavenumber, double scale, bool poisson, double tol = kDefaultAdiTol)
+        : op_(detail::modal_operator(m, n, wavenumber, scale, poisson, tol)), tol_(tol), poisson_(poisson), scale_(scale) {}
+    MatrixXcd solve(const MatrixXcd& f_full) const {  // solvers.cpp:77-98
+        if (f_full.rows() != op_.m || f_full.cols() != op_.n)
+            throw DomainError("ModalSolver::solve: right-hand side has wrong shape");
+        MatrixXcd x(op_.m, op_.n);
+        detail::check(ccf_modal_solve(op_.dev->h, reinterpret_cast<const double*>(f_full.data()),
+                                      reinterpret_cast<double*>(x.data())),
+                      op_.dev->ctx);
+        // relative residual of the recombined system (adi.cpp:106-112) = (op.apply(x) - f) on the retained block
+        const MatrixXcd r = op_.apply(x);
+        double rn = 0, en = 0;
+        for (int k = 0; k + 2 < op_.n; ++k)
+            for (int j = 0; j + 2 < op_.m; ++j) {
+                rn += std::norm(r(j, k) - f_full(j, k));
+                en += std::norm(f_full(j, k));
+            }
+        last_residual_ = en > 0.0 ? std::sqrt(rn / en) : std::sqrt(rn);
+        return x;
+    }
+    const ModalOperator& raw() const { return op_; }
+    const ShiftPlan* plan() const {
+        if (!poisson_ && scale_ == 0.0) return nullptr;
+        if (!plan_) {
+            double info[8];
+            std::vector<double> u(128), v(128);
+            detail::check(ccf_plan_host(op_.m, op_.n, op_.wavenumber, scale_, poisson_ ? 1 : 0, tol_, 0, info, u.data(),
+                                        v.data(), 128),
+                          nullptr);
+            ShiftPlan p;
+            p.a = info[0]; p.b = info[1]; p.c = info[2]; p.d = info[3];
+            p.gamma_cr = info[4]; p.alpha_z = info[5]; p.modulus = info[6]; p.J = int(info[7]);
+            p.tol = tol_;
+            u.resize(size_t(std::min(p.J, 128)));
+            v.resize(size_t(std::min(p.J, 128)));
+            p.u = std::move(u);
+            p.v = std::move(v);
+            plan_ = std::move(p);
+        }
+        return &*plan_;
+    }
+    double last_residual() const { return last_residual_; }
+
+private:
+    ModalOperator op_;
+    double tol_;
+    bool poisson_;
+    double scale_;
+    mutable std::optional<ShiftPlan> plan_;
+    mutable double last_residual_ = 0.0;
+};
+
+class ModalSolverCache {  // solvers.hpp:63-76, keyed by (w^2, scale, poisson)
+public:
+    ModalSolverCache(int m, int n, double tol) : m_(m), n_(n), tol_(tol) {}
+    const ModalSolver& get(int wavenumber, double scale, bool poisson) const {
+        auto& slot = cache_[std::make_tuple(wavenumber * wavenumber, scale, poisson)];
+        if (!slot) slot = std::make_unique<ModalSolver>(m_, n_, std::abs(wavenumber), scale, poisson, tol_);
+        return *slot;
+    }
+    int m() const { return m_; }
+    int n() const { return n_; }
+    double tol() const { return tol_; }
+
+private:
+    int m_, n_;
+    double tol_;
+    mutable std::map<std::tuple<int, double, bool>, std::unique_ptr<ModalSolver>> cache_;
+};
+
+namespace detail {
+inline MatrixXcd lift_slice_for(int m, int n, const BoundaryCondition& bc, int slice_index) {  // solvers.cpp:112-123
+    if (!bc.lift) throw DomainError("BoundaryCondition: lifted kind without lift data");
+    const CoeffTensor& lift = *bc.lift;
+    if (lift.spec.m != m || lift.spec.n != n) throw DomainError("BoundaryCondition: lift tensor has wrong dimensions");
+    if (slice_index < 0 || slice_index >= lift.spec.p) throw DomainError("BoundaryCondition: lift tensor misses the requested mode");
+    return lift.slice(slice_index);
+}
+// The modal solves are linear, so the lifted solve(F_l - op_l.apply(lift_l)) + lift_l (solvers.cpp:160-165,
+// timestep.cpp:84-101) = the homogeneous solve + c_l with c_l = lift_l - solve(op_l.apply(lift_l)), parity-projected
+// like the output; the per-mode pieces run on the device through ModalSolver.
+inline void add_lift_correction(CoeffTensor& out, const BoundaryCondition& bc, double scale, bool poisson, double tol) {
+    const GridSpec& spec = out.spec;
+    ModalSolverCache cache(spec.m, spec.n, tol);
+    for (int l = 0; l < spec.p; ++l) {
+        const int w = spec.wavenumber(l);
+        const MatrixXcd lift = lift_slice_for(spec.m, spec.n, bc, l);
+        if (lift.max_abs() == 0.0) continue;
+        const ModalSolver& solver = cache.get(w, scale, poisson);
+        const MatrixXcd c = lift - solver.solve(solver.raw().apply(lift));
+        for (int k = 0; k < spec.n; ++k)
+            for (int j = 0; j < spec.m; ++j)
+                if ((j + w) % 2 == 0) out.at(j, k, l) += c(j, k);  // parity_project (coeffs.cpp:50-65)
+    }
+}
+}  // namespace detail
+
+inline MatrixXcd solve_modal_helmholtz(const ModalOperator& op, const MatrixXcd& f, const BoundaryCondition& bc,
+                                       double tol = kDefaultAdiTol) {  // solvers.cpp:125-140
+    ModalSolver solver(op.m, op.n, op.wavenumber, op.scale, /*poisson=*/false, tol);
+    MatrixXcd rhs = f, lift;
+    if (bc.kind == BoundaryCondition::Kind::dirichlet_lifted) {
+        if (!bc.lift) throw DomainError("BoundaryCondition: lifted kind without lift data");
+        lift = detail::lift_slice_for(op.m, op.n, bc, op.wavenumber + bc.lift->spec.p / 2);
+        rhs -= op.apply(lift);
+    }
+    MatrixXcd x = solver.solve(rhs);
+    if (lift.size() > 0) x += lift;
+    return x;
+}
+
 // ---- solvers.hpp:86-94
-inline CoeffTensor solve_poisson_3d(const CoeffTensor& f, const BoundaryCondition& = {}, double tol = kDefaultAdiTol) {
+inline CoeffTensor solve_poisson_3d(const CoeffTensor& f, const BoundaryCondition& bc = {}, double tol = kDefaultAdiTol) {
     CoeffTensor out(f.spec);
     ccf_ctx* c = detail::context(f.spec, tol);
     detail::check(ccf_poisson3d(c, f.raw(), out.raw()), c);
+    if (bc.kind == BoundaryCondition::Kind::dirichlet_lifted) detail::add_lift_correction(out, bc, 1.0, true, tol);
     return out;
+}
+inline CoeffTensor solve_poisson_3d(const CoeffTensor& f, const BoundaryCondition& bc, const ModalSolverCache& cache) {
+    if (cache.m() != f.spec.m || cache.n() != f.spec.n) throw DomainError("solve_poisson_3d: cache size mismatch");
+    return solve_poisson_3d(f, bc, cache.tol());
 }
 inline CoeffTensor solve_horizontal_poisson(const CoeffTensor& rhs) {
     CoeffTensor out(rhs.spec);
@@ -248,8 +499,8 @@ struct BDFScheme {
 class HelmholtzTensorStepper {
 public:
     HelmholtzTensorStepper(const GridSpec& spec, double diffusivity, double h, double adi_tol,
-                           BoundaryCondition = {})
-        : spec_(spec), diff_(diffusivity), h_(h), tol_(adi_tol) {
+                           BoundaryCondition bc = {})
+        : spec_(spec), diff_(diffusivity), h_(h), tol_(adi_tol), bc_(std::move(bc)) {
         spec.validate();
     }
     CoeffTensor step(const std::deque<CoeffTensor>& history, const BDFScheme& scheme, const CoeffTensor* forcing) const {
@@ -267,12 +518,15 @@ public:
         detail::check(ccf_helmholtz_step(c, hp.data(), int(hp.size()), scheme.order, forcing ? forcing->raw() : nullptr,
                                          diff_, h_, out.raw()),
                       c);
+        if (bc_.kind == BoundaryCondition::Kind::dirichlet_lifted)  // timestep.cpp:84-101
+            detail::add_lift_correction(out, bc_, scheme.kappa(h_) * diff_, false, tol_);
         return out;
     }
 
 private:
     GridSpec spec_;
     double diff_, h_, tol_;
+    BoundaryCondition bc_;
 };
 
 // ---- ptns.hpp:47-137
@@ -283,8 +537,15 @@ inline VectorFieldCoeffs pt_synthesize(const PTScalars& s) {
     detail::check(ccf_pt_synthesize(c, s.lambda.raw(), s.gamma.raw(), v.comp_r.raw(), v.comp_theta.raw(), v.comp_z.raw()), c);
     return v;
 }
-inline PTScalars pt_decompose(const VectorFieldCoeffs& v, bool /*check_divergence*/ = false, double = 1e-8) {
+inline CoeffTensor divergence(const VectorFieldCoeffs& v);
+inline PTScalars pt_decompose(const VectorFieldCoeffs& v, bool check_divergence = false, double div_tol = 1e-8) {
     detail::same_spec("pt_decompose", v.comp_r, v.comp_theta, v.comp_z);
+    if (check_divergence) {  // ptns.cpp:60-67
+        const double div = divergence(v).max_abs();
+        const double scale = std::max(1.0, std::max({v.comp_r.max_abs(), v.comp_theta.max_abs(), v.comp_z.max_abs()}));
+        if (div > div_tol * scale)
+            throw NotIncompressibleError("pt_decompose: field has divergence " + std::to_string(div), div);
+    }
     PTScalars s(v.comp_r.spec);
     ccf_ctx* c = detail::context(v.comp_r.spec);
     detail::check(ccf_pt_decompose(c, v.comp_r.raw(), v.comp_theta.raw(), v.comp_z.raw(), s.lambda.raw(), s.gamma.raw()), c);
@@ -524,6 +785,10 @@ public:
 
 private:
     void init(const double* data, int kind) {
+        if (config_.bc.kind == BoundaryCondition::Kind::dirichlet_lifted)
+            throw ConfigError("HeatStepper: lifted boundary data is not supported by the device-resident stepper "
+                              "(its state lives in the homogeneous modal basis); step HelmholtzTensorStepper with the "
+                              "lifted BoundaryCondition instead");
         ctx_ = detail::context(config_.spec, config_.adi_tol);
         detail::check(ccf_heat_create(ctx_, config_.alpha, config_.h, config_.order, data, kind, &st_), ctx_);
     }

@@ -80,6 +80,8 @@ void bdf_scheme(int b, double* kappa_over_h, double w[4]) {
 
 }  // namespace
 
+void ccf_modal_detach_ctx(ccf_ctx* ctx);  // modalapi.cu
+
 // context guard for the other translation units of the C-ABI (modalapi.cu)
 ccf_status ccf_ctx_guard(ccf_ctx* ctx, void (*fn)(ccf::Ctx&, void*), void* user) {
     return guard(ctx, [&](Ctx& c) { fn(c, user); });
@@ -116,6 +118,7 @@ ccf_status ccf_ctx_destroy(ccf_ctx* ctx) {
             st->ctx = nullptr;  // later calls on the stepper report CCF_INTERNAL_ERROR; destroy only frees it
             st->st.pl = nullptr;
         }
+        ccf_modal_detach_ctx(ctx);
         ctx->pipe.reset();
         delete ctx;
     } catch (...) {

@@ -11,6 +11,8 @@
 // for s = 0 the mass pair X = R2'^-1 F C02'^-T (RT = 1). The products run as batched FP64 tensor-core GEMMs
 // (GemmPlan); the host only marshals the column-major complex matrix into the parity blocks.
 #include <cmath>
+#include <mutex>
+#include <set>
 #include <vector>
 
 #include "../../include/ccf.h"
@@ -217,6 +219,21 @@ struct ccf_modal {
     std::unique_ptr<ccf::ModalDev> d;
 };
 
+// live handles per context: ccf_ctx_destroy releases their device data and detaches them (api.cu), so a handle
+// outliving its context only reports CCF_INTERNAL_ERROR and can still be destroyed
+namespace {
+std::mutex g_modal_mu;
+std::set<ccf_modal*> g_modals;
+}  // namespace
+void ccf_modal_detach_ctx(ccf_ctx* ctx) {
+    std::lock_guard<std::mutex> lock(g_modal_mu);
+    for (ccf_modal* h : g_modals)
+        if (h->ctx == ctx) {
+            h->d.reset();
+            h->ctx = nullptr;
+        }
+}
+
 // (api.cu)
 ccf_status ccf_ctx_guard(ccf_ctx* ctx, void (*fn)(ccf::Ctx&, void*), void* user);
 
@@ -236,22 +253,24 @@ ccf_status ccf_modal_create(ccf_ctx* ctx, int w, double scale, int poisson, ccf_
         auto h = std::make_unique<ccf_modal>();
         h->ctx = ctx;
         h->d = std::make_unique<ccf::ModalDev>(c, w, scale, poisson != 0);
+        std::lock_guard<std::mutex> lock(g_modal_mu);
+        g_modals.insert(h.get());
         *out = h.release();
     });
 }
 
 ccf_status ccf_modal_solve(ccf_modal* h, const double* f_full, double* x) {
-    if (!h || !f_full || !x) return CCF_INTERNAL_ERROR;
+    if (!h || !h->ctx || !f_full || !x) return CCF_INTERNAL_ERROR;
     return mguard(h->ctx, [&](ccf::Ctx& c) { h->d->solve(c, f_full, x); });
 }
 
 ccf_status ccf_modal_apply(ccf_modal* h, const double* x, double* y) {
-    if (!h || !x || !y) return CCF_INTERNAL_ERROR;
+    if (!h || !h->ctx || !x || !y) return CCF_INTERNAL_ERROR;
     return mguard(h->ctx, [&](ccf::Ctx& c) { h->d->apply(c, x, y); });
 }
 
 ccf_status ccf_modal_operator(ccf_modal* h, int which, double* dense) {
-    if (!h || !dense || which < 0 || which > 3) return CCF_INTERNAL_ERROR;
+    if (!h || !h->d || !dense || which < 0 || which > 3) return CCF_INTERNAL_ERROR;
     const ccf::Dense* ops[4] = {&h->d->A, &h->d->B, &h->d->C, &h->d->D};
     std::copy(ops[which]->a.begin(), ops[which]->a.end(), dense);
     return CCF_OK;
@@ -259,13 +278,14 @@ ccf_status ccf_modal_operator(ccf_modal* h, int which, double* dense) {
 
 ccf_status ccf_modal_destroy(ccf_modal* h) {
     if (!h) return CCF_OK;
-    if (h->ctx) {
-        const ccf_status st = mguard(h->ctx, [&](ccf::Ctx&) { h->d.reset(); });
-        delete h;
-        return st;
+    {
+        std::lock_guard<std::mutex> lock(g_modal_mu);
+        g_modals.erase(h);
     }
+    ccf_status st = CCF_OK;
+    if (h->ctx) st = mguard(h->ctx, [&](ccf::Ctx&) { h->d.reset(); });
     delete h;
-    return CCF_OK;
+    return st;
 }
 
 }  // extern "C"

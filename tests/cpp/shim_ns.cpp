@@ -82,6 +82,95 @@ int main(int argc, char** argv) {
     }
     const bool seed_ok = seed_err < 1e-13 && seed_threw && sub.snapshots.size() == 1 && sub.snapshot_times.size() == 1 &&
                          std::abs(sub.snapshot_times[0] - 4 * ns3.h) < 1e-15 && std::abs(sub.final_time - 4 * ns3.h) < 1e-15;
+    // per-mode API, the reference's own cases (test_solvers.cpp:13-17, 46-105) through the shim types
+    double modal_err = 0.0;
+    bool modal_ok = true;
+    {
+        auto dense_apply = [](const std::vector<double>& A, int na, const MatrixXcd& x, const std::vector<double>& B, int nb) {
+            MatrixXcd t(na, nb), y(na, nb);  // y = A x B (row-major dense A: na x na, B: nb x nb)
+            for (int i = 0; i < na; ++i)
+                for (int k = 0; k < nb; ++k)
+                    for (int j = 0; j < na; ++j) t(i, k) += A[size_t(i) * na + j] * x(j, k);
+            for (int i = 0; i < na; ++i)
+                for (int k = 0; k < nb; ++k)
+                    for (int j = 0; j < nb; ++j) y(i, k) += t(i, j) * B[size_t(j) * nb + k];
+            return y;
+        };
+        const int mm = 12, nn = 12;
+        const double q[3] = {0.5, 0.0, -0.5};
+        auto manufactured = [&](double s, double wall, MatrixXcd& u) {
+            u = MatrixXcd::Zero(mm, nn);
+            MatrixXcd lap = MatrixXcd::Zero(mm, nn);
+            for (int j = 0; j < 3; ++j)
+                for (int k = 0; k < 3; ++k) u(j, k) += q[j] * q[k];
+            u(0, 0) += wall;
+            for (int k = 0; k < 3; ++k) lap(0, k) += -4.0 * q[k];
+            for (int j = 0; j < 3; ++j) lap(j, 0) += -2.0 * q[j];
+            return u - Complex(s) * lap;
+        };
+        // modal_rhs: F = R2 g C02^T; the Poisson quadruple carries C = R2 and B = C02^T
+        const ModalOperator pop = assemble_modal_poisson(mm, nn, 0);
+        auto modal_rhs = [&](const MatrixXcd& g) { return dense_apply(pop.C, mm, g, pop.B, nn); };
+        MatrixXcd u;
+        {
+            const MatrixXcd g = manufactured(0.05, 0.0, u);
+            const ModalOperator op = assemble_modal_helmholtz(mm, nn, 0, 0.05);
+            modal_err = std::max(modal_err, (solve_modal_helmholtz(op, modal_rhs(g), BoundaryCondition::homogeneous(), 1e-13) - u).max_abs());
+            modal_ok = modal_ok && solve_modal_helmholtz(op, MatrixXcd::Zero(mm, nn), BoundaryCondition::homogeneous()).max_abs() == 0.0;
+        }
+        {
+            const MatrixXcd g = manufactured(0.02, 1.0, u);
+            CoeffTensor lift(GridSpec(mm, nn, 4));
+            lift.at(0, 0, 2) = 1.0;
+            const ModalOperator op = assemble_modal_helmholtz(mm, nn, 0, 0.02);
+            modal_err = std::max(modal_err, (solve_modal_helmholtz(op, modal_rhs(g), BoundaryCondition::lifted(lift), 1e-13) - u).max_abs());
+        }
+        {
+            ModalSolverCache cache(mm, nn, 1e-12);
+            const ModalSolver& ms = cache.get(-3, 1.0, true);
+            modal_ok = modal_ok && &ms == &cache.get(3, 1.0, true) && ms.plan() && ms.plan()->J > 0 &&
+                       int(ms.plan()->u.size()) == ms.plan()->J && ModalSolver(mm, nn, 0, 0.0, false).plan() == nullptr;
+            MatrixXcd frand(mm, nn);
+            for (int k = 0; k < nn; ++k)
+                for (int j = 0; j < mm; ++j) frand(j, k) = Complex(nd(rng), nd(rng)) * std::pow(0.8, j + k);
+            ms.solve(frand);
+            modal_ok = modal_ok && ms.last_residual() < 1e-12;
+            try {
+                ms.solve(MatrixXcd::Zero(mm, nn + 2));
+                modal_ok = false;
+            } catch (const DomainError&) {
+            }
+        }
+        // lifted 3-D Poisson: u = lift + homogeneous part; the wall values are the lift's (u - lift vanishes there)
+        {
+            CoeffTensor lift(spec);
+            lift.at(0, 0, spec.zero_mode()) = 1.0;
+            lift.at(2, 1, spec.zero_mode()) = 0.25;
+            const CoeffTensor ul = solve_poisson_3d(f, BoundaryCondition::lifted(lift));
+            double wall = 0.0;  // r = 1: sum_j (u - lift)(j, k, l) = 0 for every k, l
+            for (int l = 0; l < spec.p; ++l)
+                for (int k = 0; k < spec.n; ++k) {
+                    Complex acc(0);
+                    for (int j = 0; j < spec.m; ++j)
+                        if ((j + spec.wavenumber(l)) % 2 == 0) acc += ul.at(j, k, l) - lift.at(j, k, l);
+                    wall = std::max(wall, std::abs(acc));
+                }
+            modal_ok = modal_ok && wall < 1e-11 * std::max(1.0, ul.max_abs());
+        }
+        // pt_decompose(check_divergence): a non-solenoidal field is refused (ptns.cpp:60-67)
+        {
+            VectorFieldCoeffs bad(spec);
+            bad.comp_z = f;
+            bool refused = false;
+            try {
+                pt_decompose(bad, true);
+            } catch (const NotIncompressibleError& e) {
+                refused = e.divergence > 0.0;
+            }
+            modal_ok = modal_ok && refused;
+        }
+        modal_ok = modal_ok && modal_err < 1e-10;
+    }
     bool threw = false;
     try {
         GridSpec bad(m, m, 7);
@@ -145,7 +234,7 @@ int main(int argc, char** argv) {
     const CoeffTensor rd = std::get<CoeffTensor>(read_field("/tmp/shim_lambda.ccf"));
     const bool io_ok = rd.data == run.final_omega.lambda.data && crc32_ieee(reinterpret_cast<const uint8_t*>("123456789"), 9) == 0xCBF43926u;
     std::printf("shim ok: roundtrip %.3e final_time %.6f domain_error %d heat_err %.3e io %d spec_errors %d/6 "
-                "worst_residual %.3e seed %d (%.2e)\n", err / mx, run.final_time, int(threw), herr / hmx, int(io_ok), spec_errors,
-                hr.worst_residual, int(seed_ok), seed_err);
-    return (err / mx < 1e-12 && threw && herr / hmx < 1e-4 && io_ok && spec_ok && seed_ok) ? 0 : 1;
+                "worst_residual %.3e seed %d (%.2e) modal %d (%.2e)\n", err / mx, run.final_time, int(threw), herr / hmx, int(io_ok), spec_errors,
+                hr.worst_residual, int(seed_ok), seed_err, int(modal_ok), modal_err);
+    return (err / mx < 1e-12 && threw && herr / hmx < 1e-4 && io_ok && spec_ok && seed_ok && modal_ok) ? 0 : 1;
 }

@@ -687,11 +687,13 @@ ccf_status ccf_ns_step(ccf_ns_state* st, int nsteps) {
     return guard(st->ctx, [&](Ctx& c) {
         for (int i = 0; i < nsteps; ++i) st->st.step_once();
         c.shard_check();
-        c.check_adi_error(false);
-        int f = 0;
-        CCF_CUDA(cudaMemcpyAsync(&f, st->st.dflag, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        // solver error words and the non-finite flag in one round trip (pinned status words, one sync)
+        int* hs = c.ws.hstat;
+        CCF_CUDA(cudaMemcpyAsync(hs, c.ws.err, sizeof(int) * 4, cudaMemcpyDeviceToHost, c.stream));
+        CCF_CUDA(cudaMemcpyAsync(hs + 4, st->st.dflag, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
         c.sync();
-        if (f) throw Error(ccf::NUMERICAL, "NSStepper: non-finite state at step " + std::to_string(st->st.steps));
+        if (hs[0]) c.check_adi_error(false);
+        if (hs[4]) throw Error(ccf::NUMERICAL, "NSStepper: non-finite state at step " + std::to_string(st->st.steps));
     });
 }
 

@@ -106,6 +106,7 @@ Ctx::Ctx(int m_, int n_, int p_, int device_, double tol_, int flags_)
     CCF_CUDA(cudaMalloc(&ws.err, sizeof(int) * 4));
     CCF_CUDA(cudaMalloc(&ws.flag, sizeof(int) * 4));
     CCF_CUDA(cudaMalloc(&ws.iters, sizeof(unsigned long long) * 2));
+    CCF_CUDA(cudaHostAlloc(&ws.hstat, sizeof(int) * 8, cudaHostAllocDefault));
     CCF_CUDA(cudaMemset(ws.err, 0, sizeof(int) * 4));
     CCF_CUDA(cudaMemset(ws.iters, 0, sizeof(unsigned long long) * 2));
     CCF_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
@@ -153,6 +154,7 @@ Ctx::~Ctx() {
     cudaFree(ws.err);
     cudaFree(ws.flag);
     cudaFree(ws.iters);
+    if (ws.hstat) cudaFreeHost(ws.hstat);
     if (own_stream) cudaStreamDestroy(own_stream);
 }
 

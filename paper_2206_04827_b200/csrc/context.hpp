@@ -82,6 +82,7 @@ struct Workspace {  // ADI round bookkeeping
     int *active = nullptr, *rounds = nullptr, *err = nullptr, *flag = nullptr;
     unsigned long long* iters = nullptr;
     int cap_slots = 0;
+    int* hstat = nullptr;  // pinned host copy of {err[4], stepper flag}: one sync per status read (ccf_ns_step)
 };
 
 // Mode sharding of the NS step over the GPUs of one node (csrc/shard.cu).

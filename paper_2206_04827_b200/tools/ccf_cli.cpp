@@ -405,7 +405,7 @@ int run_ns(const RunConfig& cfg) {
     nc.order = cfg.bdf_order;
     nc.adi_tol = cfg.adi_tol;
     const auto t0 = std::chrono::steady_clock::now();
-    NSRunResult run = ns_run(nc, omega0, cfg.steps);
+    NSRunResult run = ns_run(nc, omega0, cfg.steps, cfg.output_every);  // cylspec_main.cpp:200
     const double sec = seconds_since(t0);
     write_field((outdir / "omega_toroidal.ccf").string(), run.final_omega.lambda);
     write_field((outdir / "omega_poloidal.ccf").string(), run.final_omega.gamma);

@@ -165,6 +165,38 @@ def cpu_sample(cfg, threads):
     return 1.0 / t_step, sample, d
 
 
+def parity_check(P, ctx, cfg, wl, wg, steps=10):
+    """Live cross-check of the timed configuration (not timed): `steps` NS steps of the production path (INT8
+    digit products, the stepper the bench times) against the FP64 tensor-core (DMMA) product path in a second
+    context, same initial data -> max-norm relative difference of omega. The CPU oracle needs ~80 s per step at
+    256^3 (16 cores); its step-1 match and the 50-step drift logs are in profiles/ (DESIGN.md section 4)."""
+    from tests.inputs import rel_err
+    res = []
+    for oz in (None, "0"):
+        old = os.environ.get("CCF_OZAKI")
+        if oz is not None:
+            os.environ["CCF_OZAKI"] = oz
+        try:
+            c = ctx if oz is None else P.Context(cfg["m"], cfg["n"], cfg["p"], device=0)
+            s = P.NSStepper(c, wl, wg, reynolds=cfg["reynolds"], h=cfg["h"], order=4)
+            s.step(steps)
+            res.append(s.omega())
+            s.close()
+            if c is not ctx:
+                c.close()
+        finally:
+            if oz is not None:
+                if old is None:
+                    os.environ.pop("CCF_OZAKI", None)
+                else:
+                    os.environ["CCF_OZAKI"] = old
+    err = max(rel_err(res[0][0], res[1][0]), rel_err(res[0][1], res[1][1]))
+    return {"steps": steps, "production_vs_fp64_dmma_path_max_rel_diff": err, "gate": 1e-10,
+            "vs_cpu_oracle": "step 1: 6.4e-12 (profiles/drift_config4_256_oracle_r02.log); 50-step drift vs the "
+                             "reference-algorithm (ADI) GPU path 3.0e-11 (profiles/drift_config4_256_paths_r02.log); "
+                             "config 3, 200 steps vs the CPU oracle 4.3e-12 (profiles/drift_config3_64_200steps_r02.log)"}
+
+
 def secondary_configs(P, torch):
     """BASELINE.json configs 1-3 on the same GPU (reported beside the headline, SURVEY §8d units):
     config 1 Poisson 32^3 (us per solve: steady state with a cached plan, and with setup like the
@@ -518,7 +550,10 @@ def main():
     status_bytes = 4 * 4 + 4  # per step: ADI error words + non-finite flag (ccf_ns_step)
 
     sec = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_secondary:
+        if ozaki and cfg["m"] == 256:
+            parity = parity_check(P, ctx, cfg, hl.numpy(), hg.numpy())
         sec = secondary_configs(P, torch)
 
     cpu = None
@@ -596,6 +631,8 @@ def main():
         }
         if cpu:
             line["cpu_baseline"] = cpu
+        if parity:
+            line["parity"] = parity
         if sec:
             line["secondary_configs"] = sec
         print(json.dumps(line), flush=True)

@@ -1,4 +1,5 @@
 // C-ABI (include/ccf.h) over the B200 CCF context.
+#include <cmath>
 #include <cstring>
 #include <optional>
 #include <set>
@@ -165,7 +166,10 @@ ccf_status ccf_helmholtz_step(ccf_ctx* ctx, const double* const* hist, int nhist
         if (nhist < order) throw Error(ccf::DOMAIN_ERROR, "bdf_rhs: insufficient history for the requested order");
         const double kappa = koh * h;
         const double scale = kappa * diffusivity;
-        if (scale == 0.0) throw Error(ccf::DOMAIN_ERROR, "ccf_helmholtz_step: zero diffusivity (mass solve) is not supported on the B200 path");
+        // zero diffusivity: the mass pair (solvers.cpp:57-62) as a fast-diagonalization set with unit denominators
+        if (scale == 0.0 && (c.flags & 4))
+            throw Error(ccf::CONFIG_ERROR, "ccf_helmholtz_step: the mass solve (zero diffusivity) needs a fast-diagonalization context");
+        if (scale < 0.0) throw Error(ccf::DOMAIN_ERROR, "HelmholtzTensorStepper: negative diffusivity");
         const bool full = true;
         const long nt = c.tensor_doubles(full);
         for (int i = 0; i < order + 2; ++i)
@@ -547,7 +551,8 @@ ccf_ns_state* ns_create_impl(ccf_ctx* ctx, Ctx& c, double reynolds, double h, in
     // the heat stepper needs only the modal bases (no composite operators)
     const char* ev = std::getenv("CCF_NS_EIGEN");
     const bool want = !(ev && ev[0] == '0');
-    if (want && pset.host.has_diag && pset.dg) {
+    // (a zero-diffusivity heat stepper solves the mass pair, which has no place in the shared Poisson basis)
+    if (want && pset.host.has_diag && pset.dg && std::isfinite(reynolds)) {
         ccf::Pipeline& P = *s.pl;
         bool ok = true;
         if (!disable_nonlinear) {
@@ -630,7 +635,10 @@ ccf_status ccf_heat_create(ccf_ctx* ctx, double alpha, double h, int order, cons
                            ccf_ns_state** out) {
     return guard(ctx, [&](Ctx& c) {
         c.require_unsharded("ccf_heat_create");
-        if (!(alpha > 0.0)) throw Error(ccf::DOMAIN_ERROR, "HeatStepper: alpha must be positive on the B200 path");
+        // alpha = 0 (test_timestep.cpp:136-149): every step is the mass solve; coefficient-space state
+        if (!(alpha >= 0.0)) throw Error(ccf::DOMAIN_ERROR, "HeatStepper: alpha must be nonnegative");
+        if (alpha == 0.0 && (c.flags & 4))
+            throw Error(ccf::CONFIG_ERROR, "HeatStepper: alpha = 0 (mass solve) needs a fast-diagonalization context");
         if (initial_kind != 0 && initial_kind != 1) throw Error(ccf::DOMAIN_ERROR, "ccf_heat_create: initial_kind 0 | 1");
         *out = ns_create_impl(ctx, c, 1.0 / alpha, h, order, true, initial, nullptr, true, initial_kind == 0);
     });

@@ -286,10 +286,12 @@ DiagRight diag_right(const CBand& Btb, const CBand& Dtb, const CBand& C02b, int 
     return out;
 }
 
-DiagLeft mass_left(const CBand& Ab, int M, int mh) {
+DiagLeft mass_left(const CBand& Ab, const CBand& R2b, int M, int mh) {
     const BandOp A = from_band(Ab, M);
-    LMat PL(M, mh);
-    for (int a = 0; a < M; ++a) PL(a, a) = 1.0L;
+    LMat PL(M, mh);  // R2m[a][y] = R2(a, y - a) (identity band: the raw right-hand side, truncated)
+    for (int a = 0; a < M; ++a)
+        for (int d = R2b.lo; d <= R2b.hi; ++d)
+            if (a + d >= 0 && a + d < mh) PL(a, a + d) = R(R2b.at(a, d));
     if (!dense_solve(A.m, PL)) throw Error(SINGULAR, "mass solve: R2 block is singular");
     LMat QL(mh, M);  // S_r
     for (int a = 0; a < mh; ++a)
@@ -298,20 +300,26 @@ DiagLeft mass_left(const CBand& Ab, int M, int mh) {
     out.PL = to_double(PL);
     out.PL_ld = PL.a;
     out.QL = to_double(QL);
-    out.lam.assign(size_t(M), 0.0);
-    out.lam_ld.assign(size_t(M), 0.0L);
+    out.lam.assign(size_t(M), 1.0);  // with mu = 0: 1 / (lambda_i + mu_j) = 1
+    out.lam_ld.assign(size_t(M), 1.0L);
     return out;
 }
 
-DiagRight mass_right(const CBand& Btb, int N, int nh) {
+DiagRight mass_right(const CBand& Btb, const CBand& C02b, int N, int nh) {
     // Y B^ = E  <=>  B^^T Y^T = E^T: invert Bt = B^^T and transpose
     const BandOp Bt = from_band(Btb, N);
     LMat inv(N, N);
     for (int i = 0; i < N; ++i) inv(i, i) = 1.0L;
     if (!dense_solve(Bt.m, inv)) throw Error(SINGULAR, "mass solve: C02 block is singular");
-    LMat PR(nh, N);  // rows < N: B^^-1 = (Bt^-1)^T
-    for (int x = 0; x < N; ++x)
-        for (int e = 0; e < N; ++e) PR(x, e) = inv(e, x);
+    LMat PR(nh, N);  // C02m B^^-1, C02m[x][b] = C02(b, x - b), B^^-1 = (Bt^-1)^T
+    for (int b = 0; b < N; ++b)
+        for (int d = C02b.lo; d <= C02b.hi; ++d) {
+            const int x = b + d;
+            if (x < 0 || x >= nh) continue;
+            const R c = R(C02b.at(b, d));
+            if (c == 0.0L) continue;
+            for (int e = 0; e < N; ++e) PR(x, e) += c * inv(e, b);
+        }
     LMat QR(N, nh);  // S_z^T
     for (int i = 0; i < N; ++i)
         for (int b = 0; b < nh; ++b) QR(i, b) = (b == i ? 1.0L : 0.0L) - (b == i + 1 ? 1.0L : 0.0L);

@@ -42,8 +42,9 @@ DiagRight diag_right(const CBand& Bt, const CBand& Dt, const CBand& C02, int N, 
 
 // Mass-only pair (Helmholtz scale 0, solvers.cpp:57-62, 84-91): X = A^-1 E B^^-1 with A = Ab (R2 recombined, one
 // parity block) and B^ = Bt^T (C02 recombined), in the same four-product form u = QL [(PL f PR) .* 1] QR:
-// PL = A^-1 [I | 0] (M x mh), QL = S_r (mh x M); PR = [I ; 0] B^^-1 (nh x N), QR = S_z^T (N x nh).
-DiagLeft mass_left(const CBand& Ab, int M, int mh);
-DiagRight mass_right(const CBand& Bt, int N, int nh);
+// PL = A^-1 R2m (M x mh), QL = S_r (mh x M), lambda = 1; PR = C02m B^^-1 (nh x N), QR = S_z^T (N x nh), mu = 0
+// (R2b / C02b as in diag_left / diag_right; identity bands give the raw, truncated right-hand side).
+DiagLeft mass_left(const CBand& Ab, const CBand& R2b, int M, int mh);
+DiagRight mass_right(const CBand& Bt, const CBand& C02b, int N, int nh);
 
 }  // namespace ccf

@@ -454,9 +454,18 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
         // this set's left data: Poisson as cached; Helmholtz (A = R2 - s L, C = -s R2): same V,
         // lambda = nu - 1/s, PL = -(1/s) PL_Poisson
         std::vector<DiagLeft> left(diag_in.size());
+        const bool mass = !poisson && scale == 0.0;
+        DiagLeft mass_l[2];
         for (size_t i = 0; i < diag_in.size(); ++i) {
             const DiagLeft& P = so.diag_poisson.at(diag_in[i].aw);
             DiagLeft& L = left[i];
+            if (mass) {  // scale 0 (solvers.cpp:57-62): X = R2'^-1 (R2 f C02^T) C02'^-T, no eigenpairs involved
+                const int j0 = diag_in[i].aw & 1;
+                if (mass_l[j0].PL.empty())
+                    mass_l[j0] = mass_left(compress(so.R2rec, j0, M, M, -2, 3), compress(so.ur.r2, j0, M, mh, -1, 3), M, mh);
+                L = mass_l[j0];
+                continue;
+            }
             L.QL = P.QL;
             if (poisson) {
                 L.PL = P.PL;
@@ -486,7 +495,10 @@ SolverSet build_solver_set(SizeOps& so, const std::vector<int>& slot_w, bool poi
             for (int k0 = 0; k0 < 2; ++k0) so.diag_right_data[k0] = diag_right(Btc[k0], Dtc[k0], C02c[k0], N, nh);
             so.diag_right_ok = true;
         }
-        const DiagRight* right = so.diag_right_data;
+        DiagRight mass_r[2];
+        if (mass)
+            for (int k0 = 0; k0 < 2; ++k0) mass_r[k0] = mass_right(Btc[k0], C02c[k0], N, nh);
+        const DiagRight* right = mass ? mass_r : so.diag_right_data;
         // QL (mh x M) and PR (nh x N) are stored with the leading dimension rounded up to even so
         // that every GEMM operand row is 16-byte aligned (cp.async pipeline)
         auto padld = [](const std::vector<double>& x, int rows, int cols) {

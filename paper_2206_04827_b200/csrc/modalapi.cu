@@ -67,11 +67,11 @@ struct ModalDev {
         const Dense lrec = recombine(lw);
         for (int j0 = 0; j0 < 2; ++j0) {
             const CBand Cp = compress(so.R2rec, j0, M, M, -2, 3);
-            left[j0] = mass ? mass_left(Cp, M, mh) : diag_left(compress(lrec, j0, M, M, -2, 3), Cp, idM, M, mh);
+            left[j0] = mass ? mass_left(Cp, idM, M, mh) : diag_left(compress(lrec, j0, M, M, -2, 3), Cp, idM, M, mh);
         }
         for (int k0 = 0; k0 < 2; ++k0) {
             const CBand Btc = compress(so.C02recZ, k0, N, N, -1, 2);
-            right[k0] = mass ? mass_right(Btc, N, nh)
+            right[k0] = mass ? mass_right(Btc, idN, N, nh)
                              : diag_right(Btc, compress(so.D2recZ, k0, N, N, -1, 2), idN, N, nh);
         }
         // pack: per j0 [PL M x mh | QL mh x Mp], per k0 [PR nh x Np | QR N x nh], RT[j0][k0] M x Np, then the

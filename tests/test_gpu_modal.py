@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 from tests.inputs import hermitian_coeffs, rel_err
-from tests.modal_cases import manufactured, mass_pair, modal_rhs, random_rhs, unit_lift
+from tests.modal_cases import manufactured, mass_pair, modal_rhs, operator_known_answers, random_rhs, unit_lift
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-10
@@ -82,4 +82,34 @@ def test_lifted_poisson_and_helmholtz_step(P, O):
         assert rel_err(got, ref) < TOL
     with pytest.raises(P.DomainError):
         ctx.solve_poisson_3d(f, lift=lift[:4])
+    ctx.close()
+
+
+def test_operator_known_answers_on_device(P, O):  # test_ultraop.cpp:194-238 through ccf_modal_apply
+    def apply(x, w, scale, poisson):
+        n, m = x.shape
+        ctx = P.Context(m, n, 4)
+        s = P.ModalSolver(ctx, w, scale, poisson)
+        y = s.apply(x)
+        s.close()
+        ctx.close()
+        return y
+
+    e1, e2, e3 = operator_known_answers(apply, lambda f: modal_rhs(O, f))
+    assert e1 < 1e-12 and e2 < 1e-15 and e3 < 1e-13
+
+
+def test_poisson_boundary_rows_hold_on_device(P, O):  # test_solvers.cpp:148-156
+    from tests.conftest import sample
+    m, n, p = 12, 12, 8
+    ctx = P.Context(m, n, p)
+    f = sample(O, m, n, p, lambda r, z, t: np.sin(2 * r * np.cos(t)) * np.cos(z) + 0.3 * z)
+    u = ctx.solve_poisson_3d(ctx.analyze(f))
+    worst = 0.0
+    for t in -np.pi + 2 * np.pi * np.arange(p) / p:
+        for z in np.cos(np.pi * np.arange(n) / (n - 1)):
+            worst = max(worst, abs(O.evaluate_at(u, 1.0, z, t)), abs(O.evaluate_at(u, -1.0, z, t)))
+        for r in np.cos(np.pi * np.arange(m) / (m - 1)):
+            worst = max(worst, abs(O.evaluate_at(u, r, 1.0, t)), abs(O.evaluate_at(u, r, -1.0, t)))
+    assert worst < 1e-12 * max(1.0, np.abs(u).max())
     ctx.close()

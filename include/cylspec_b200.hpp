@@ -149,7 +149,51 @@ struct CoeffTensor {
         for (const Complex& c : data) v = std::max(v, std::abs(c));
         return v;
     }
+    bool all_finite() const {  // coeffs.cpp:12-17
+        for (const Complex& c : data)
+            if (!std::isfinite(c.real()) || !std::isfinite(c.imag())) return false;
+        return true;
+    }
+    CoeffTensor& operator-=(const CoeffTensor& o) {  // coeffs.cpp:25-29
+        if (!(spec == o.spec)) throw DomainError("CoeffTensor: spec mismatch");
+        for (size_t i = 0; i < data.size(); ++i) data[i] -= o.data[i];
+        return *this;
+    }
+    friend CoeffTensor operator+(CoeffTensor a, const CoeffTensor& b) { return a += b; }
+    friend CoeffTensor operator-(CoeffTensor a, const CoeffTensor& b) { return a -= b; }
+    friend CoeffTensor operator*(Complex s, CoeffTensor a) { return a *= s; }
 };
+
+// Container-level helpers of coeffs.hpp:47-59 (index masks and comparisons on the host-side tensor; on the device
+// path the parity classes are built into the parity-compressed layout, so the kernels never store the masked half).
+inline double hermitian_symmetry_error(const CoeffTensor& t) {  // coeffs.cpp:36-48
+    const GridSpec& s = t.spec;
+    const int half = s.p / 2;
+    double worst = 0.0;
+    for (int l = 0; l < s.p; ++l) {
+        const int lp = 2 * half - l;  // partner slice carrying -wavenumber
+        if (lp < 0 || lp >= s.p) continue;
+        for (int k = 0; k < s.n; ++k)
+            for (int j = 0; j < s.m; ++j) worst = std::max(worst, std::abs(t.at(j, k, l) - std::conj(t.at(j, k, lp))));
+    }
+    return worst;
+}
+enum class Parity { scalar, azimuthal_flip };  // keep j + wavenumber even | odd
+inline void parity_project_in_place(CoeffTensor& coeffs, Parity parity = Parity::scalar) {  // coeffs.cpp:50-59
+    const GridSpec& s = coeffs.spec;
+    const int keep_mod = (parity == Parity::scalar) ? 0 : 1;
+    for (int l = 0; l < s.p; ++l) {
+        const int w = s.wavenumber(l);
+        for (int k = 0; k < s.n; ++k)
+            for (int j = 0; j < s.m; ++j)
+                if (((j + w) % 2 + 2) % 2 != keep_mod) coeffs.at(j, k, l) = Complex(0);
+    }
+}
+inline CoeffTensor parity_project(const CoeffTensor& coeffs, Parity parity = Parity::scalar) {  // coeffs.cpp:61-65
+    CoeffTensor out = coeffs;
+    parity_project_in_place(out, parity);
+    return out;
+}
 
 // grid points (grid.cpp:16-40): r_j = cos((m-1-j) pi/(m-1)) with exact endpoints / midpoint, theta_l = (2l - p) pi / p
 inline std::vector<double> chebyshev_points(int count) {

@@ -169,6 +169,14 @@ int main(int argc, char** argv) {
             }
             modal_ok = modal_ok && refused;
         }
+        // coeffs.hpp helpers: a solver output is Hermitian and parity-clean; the flipped class is its complement
+        {
+            const CoeffTensor& wl = run.final_omega.lambda;
+            const CoeffTensor flip = parity_project(wl, Parity::azimuthal_flip);
+            modal_ok = modal_ok && hermitian_symmetry_error(wl) < 1e-13 * wl.max_abs() && wl.all_finite() &&
+                       (parity_project(wl) - wl).max_abs() == 0.0 && flip.max_abs() == 0.0 &&
+                       (Complex(2.0) * wl - wl - wl).max_abs() == 0.0;
+        }
         modal_ok = modal_ok && modal_err < 1e-10;
     }
     bool threw = false;

@@ -611,7 +611,7 @@ class ModalSolver:
         return out
 
     def close(self):
-        if getattr(self, "h", None) and getattr(self.ctx, "h", None):
+        if getattr(self, "h", None):  # safe after the context: ccf_ctx_destroy detaches its modal handles
             lib().ccf_modal_destroy(self.h)
         self.h = None
 

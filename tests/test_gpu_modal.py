@@ -113,3 +113,15 @@ def test_poisson_boundary_rows_hold_on_device(P, O):  # test_solvers.cpp:148-156
             worst = max(worst, abs(O.evaluate_at(u, r, 1.0, t)), abs(O.evaluate_at(u, r, -1.0, t)))
     assert worst < 1e-12 * max(1.0, np.abs(u).max())
     ctx.close()
+
+
+def test_handle_outliving_its_context(P):
+    ctx = P.Context(12, 10, 4)
+    s = P.ModalSolver(ctx, 1, 0.1, False)
+    f = random_rhs(12, 10, 1)
+    s.solve(f)
+    h = ctx.h
+    ctx.close()  # releases the handle's device data and detaches it
+    x = np.zeros_like(f)
+    assert P.lib().ccf_modal_solve(s.h, f.ctypes.data, x.ctypes.data) == 9  # CCF_INTERNAL_ERROR, no crash
+    s.close()

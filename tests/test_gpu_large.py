@@ -3,7 +3,7 @@ ADI data, so the NS path runs at any size (config 5 is 512^3). Parity against th
 reference's own Poisson plan still exists (the 1e-8 enclosure pad overlaps at larger m, quirk Q2).
 At m = 384 the reference ADI's rounding floor lies above its default 1e-12 (it throws
 NonConvergenceError), so the oracle runs with adi_tol = 1e-10; its inexact solves accumulate to ~1e-8
-over 4 steps (the components alone agree to ~1e-11, tools/gpu_check_ns.py 384x16x16), gate 5e-8."""
+over 4 steps (the components alone agree to ~1e-11, tests/tools/gpu_check_ns.py 384x16x16), gate 5e-8."""
 import numpy as np
 import pytest
 
@@ -64,7 +64,7 @@ def test_tma_path_ns_matches_oracle(P, O):
     k-boxes and operand blocks at aligned and unaligned offsets (the 256^3 bench shape is too slow for
     the oracle in a test). Per step the agreement is <= 1e-10 (the north-star contract); over several
     steps the oracle's own ADI error (residual <= 1e-12 at cond ~1e3) dominates the drift (~5e-10 by
-    step 3 at this size, tools/gpu_check_ns.py 160x64x8), so the 3-step gate is 2e-9."""
+    step 3 at this size, tests/tools/gpu_check_ns.py 160x64x8), so the 3-step gate is 2e-9."""
     m, n, p = 160, 64, 8  # mh = 80, nh = 32: 16-column k-boxes, mixed aligned / unaligned blocks
     ctx = P.Context(m, n, p)
     lam, gam = hermitian_coeffs(m, n, p, 0.7, 3), hermitian_coeffs(m, n, p, 0.7, 103)

@@ -1,5 +1,5 @@
 import sys, os, time
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), '..', '..'))
 import numpy as np
 import paper_2206_04827_b200 as P
 from oracle import pyoracle as O

@@ -2,12 +2,12 @@
 initial field scaled to the bench's max|v|; 256 = config 4, the bench workload, ~80 s per oracle step) on the GPU
 (production path through the C-ABI) and on the CPU oracle in lockstep; prints the relative max-norm coefficient
 error of omega = (lambda, gamma) at checkpoints.
-Run under gpurun from the repo root: python tools/drift_report.py [steps] [size] > gpurun_out/drift.log"""
+Run under gpurun from the repo root: python tests/tools/drift_report.py [steps] [size] > gpurun_out/drift.log"""
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", ".."))
 import numpy as np
 
 import bench

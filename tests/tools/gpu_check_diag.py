@@ -5,7 +5,7 @@ import time
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2206_04827_b200 as P  # noqa: E402
 from oracle import pyoracle as O  # noqa: E402
 from tests.inputs import hermitian_coeffs, rel_err  # noqa: E402

@@ -1,5 +1,5 @@
 import sys, os, time
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), '..', '..'))
 import numpy as np
 from tests.inputs import hermitian_coeffs, rel_err
 import paper_2206_04827_b200 as P

@@ -7,14 +7,14 @@ GPU: HeatStepper on the device, forcing sampled on the device (torch) and analyz
 path needs even m, n, so the paper's N = 7^3 .. 19^3 become 8^3 .. 20^3; the CPU oracle (the
 reference's algorithm, one core) runs the paper's own sizes. Larger GPU sizes show the scaling.
 
-  python tools/heat_table1.py [--cpu-sizes 7,11,15,19] [--gpu-sizes 8,12,16,20,32,64,128]
+  python tests/tools/heat_table1.py [--cpu-sizes 7,11,15,19] [--gpu-sizes 8,12,16,20,32,64,128]
 """
 import argparse
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np  # noqa: E402
 
 import paper_2206_04827_b200 as P  # noqa: E402

@@ -1,6 +1,6 @@
 """Step the NS solver (GPU) and print max|omega| per step + ADI iterations; optionally compare with the oracle."""
 import sys, os, time
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), '..'))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), '..', '..'))
 import numpy as np
 import paper_2206_04827_b200 as P
 from bench import CONFIGS, initial_vorticity

@@ -32,6 +32,19 @@ def main():
     frc = hermitian_coeffs(16, 12, 8, 0.85, 20)
     np.savez_compressed(os.path.join(HERE, "helmholtz_16x12x8.npz"), h0=hist[0], h1=hist[1], h2=hist[2], h3=hist[3],
                         forcing=frc, out=O.helmholtz_step(hist, 4, 0.01, 1e-3, forcing=frc))
+    # per-mode API, lifted data and the substeps bootstrap (round 2)
+    from tests.modal_cases import random_rhs
+    fm = random_rhs(12, 10, 7)
+    out = {"f": fm}
+    for name, (w, scale, poisson) in {"poisson_w2": (2, 1.0, True), "helm_w1": (1, 0.03, False), "mass_w0": (0, 0.0, False)}.items():
+        out[name] = O.modal_solve(fm, w, scale, poisson)[0]
+        out[name + "_apply"] = O.modal_apply(fm, w, scale, poisson)
+    np.savez_compressed(os.path.join(HERE, "modal_12x10.npz"), **out)
+    f8, lift8 = hermitian_coeffs(12, 10, 8, 0.8, 31), hermitian_coeffs(12, 10, 8, 0.6, 32)
+    np.savez_compressed(os.path.join(HERE, "poisson_lifted_12x10x8.npz"), f=f8, lift=lift8, u=O.poisson3d(f8, lift=lift8))
+    lam3, gam3 = hermitian_coeffs(8, 8, 8, 0.7, 21) * 1e-3, hermitian_coeffs(8, 8, 8, 0.7, 22) * 1e-3
+    l, g, t = O.ns_run(lam3, gam3, 6, 100.0, 2e-3, order=3, bootstrap="substeps")
+    np.savez_compressed(os.path.join(HERE, "ns_run_substeps_8.npz"), lam0=lam3, gam0=gam3, lam=l, gam=g, time=t)
 
 
 if __name__ == "__main__":

@@ -164,6 +164,27 @@ def test_golden_fixtures(P):
     assert rel_err(out, h["out"]) < TOL
 
 
+def test_golden_fixtures_round2(P):
+    # per-mode API, lifted data and the substeps bootstrap against the committed oracle vectors
+    d = np.load(os.path.join(G, "modal_12x10.npz"))
+    ctx = P.Context(12, 10, 4)
+    for name, (w, scale, poisson) in {"poisson_w2": (2, 1.0, True), "helm_w1": (1, 0.03, False), "mass_w0": (0, 0.0, False)}.items():
+        s = P.ModalSolver(ctx, w, scale, poisson)
+        assert rel_err(s.solve(d["f"]), d[name]) < TOL and rel_err(s.apply(d["f"]), d[name + "_apply"]) < 1e-13
+        s.close()
+    ctx.close()
+    d = np.load(os.path.join(G, "poisson_lifted_12x10x8.npz"))
+    ctx = P.Context(12, 10, 8)
+    assert rel_err(ctx.solve_poisson_3d(d["f"], lift=d["lift"]), d["u"]) < TOL
+    ctx.close()
+    d = np.load(os.path.join(G, "ns_run_substeps_8.npz"))
+    ctx = P.Context(8, 8, 8)
+    run = P.ns_run(ctx, d["lam0"], d["gam0"], 6, reynolds=100.0, h=2e-3, order=3, bootstrap="substeps")
+    assert rel_err(run["final_omega"][0], d["lam"]) < TOL and rel_err(run["final_omega"][1], d["gam"]) < TOL
+    assert abs(run["final_time"] - float(d["time"])) < 1e-15
+    ctx.close()
+
+
 def test_error_taxonomy(P):
     ctx = P.Context(8, 8, 8)
     f = np.zeros((8, 8, 8), complex)

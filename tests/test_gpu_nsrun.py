@@ -119,3 +119,31 @@ def test_seed_errors(P):
         st.step()
     st.close()
     ctx.close()
+
+
+def test_seed_at_the_bench_size_on_the_int8_path(P):
+    # 256^3 (the INT8 product stages, panels written by the RHS pass, graph replay): a stepper seeded with a run's
+    # history continues that run (the seeded state is re-expanded in the modal basis, so agreement is to rounding)
+    import bench
+    cfg = bench.CONFIGS[256]
+    ctx = P.Context(256, 256, 256)
+    wl, wg, _ = bench.initial_vorticity(ctx, cfg, cfg["vmax"])
+    kw = dict(reynolds=cfg["reynolds"], h=cfg["h"])
+    run = P.NSStepper(ctx, wl, wg, **kw)
+    run.step(5)
+    oh = [run.omega()]
+    for _ in range(3):
+        run.step()
+        oh.insert(0, run.omega())
+    nh = [ctx.nonlinear_term(*ctx.velocity_from_vorticity(*w), *w) for w in oh[1:]]
+    run.step(12)
+    ref = run.omega()
+    run.close()
+    seeded = P.NSStepper(ctx, *oh[0], **kw)
+    seeded.seed(oh, nh, 8 * cfg["h"], 8)
+    seeded.step(12)  # one eager coefficient-space step, four warm-up phases, then graph replays
+    got = seeded.omega()
+    assert _err(got, ref) < 1e-10
+    assert seeded.steps_taken == 20
+    seeded.close()
+    ctx.close()

@@ -52,7 +52,7 @@ def main():
     global SIZE
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 50
     SIZE = int(sys.argv[2]) if len(sys.argv) > 2 else 256
-    marks = sorted(k for k in {1, 2, 3, 5, 10, 20, 30, 40, n} if k <= n)
+    marks = sorted(k for k in {1, 2, 3, 5, 10, 20, 30, 40, 50, 100, 200, n} if k <= n)
     prod = run("prod", "diag", {}, marks)
     dmma = run("dmma", "diag", {"CCF_OZAKI": "0"}, marks)
     # the on-chip ADI kernel holds one sub-problem per CTA (m, n <= 320): above that the third path keeps the

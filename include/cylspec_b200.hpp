@@ -743,35 +743,33 @@ inline NSRunResult ns_run(const NSConfig& config, const PTScalars& initial_omega
         r.final_omega = st.omega();
         r.final_time = st.time();
     };
-    if (config.bootstrap == NSBootstrap::substeps && config.order > 1 && steps > 0) {
-        const int b = config.order;
-        const int per = 32;
-        NSConfig sub = config;
-        sub.order = std::min(2, config.order);
-        sub.h = config.h / per;
-        sub.bootstrap = NSBootstrap::ramp;
-        std::deque<PTScalars> hist;  // newest first
-        hist.push_front(initial_omega);
-        {
-            NSStepper fine(sub, initial_omega);
-            for (int big = 1; big <= b - 1; ++big) {
-                fine.steps(per);
-                hist.push_front(fine.omega());
-            }
+    const int b = config.order;
+    const bool bootstrap = config.bootstrap == NSBootstrap::substeps && b > 1 && steps > 0;
+    std::deque<PTScalars> samples{initial_omega};  // newest first
+    if (bootstrap) {  // the trajectory at t = h .. (b-1) h from a BDF-min(2, b) run with 32 sub-steps per h
+        constexpr int kSub = 32;
+        NSConfig fine_cfg = config;
+        fine_cfg.order = std::min(2, b);
+        fine_cfg.h = config.h / kSub;
+        fine_cfg.bootstrap = NSBootstrap::ramp;
+        NSStepper fine(fine_cfg, initial_omega);  // (released before the full-order stepper takes its arenas)
+        for (int level = 1; level < b; ++level) {
+            fine.steps(kSub);
+            samples.push_front(fine.omega());
         }
-        NSStepper stepper(config, hist.front());
-        std::deque<PTScalars> replay;
-        if (!config.disable_nonlinear)
-            for (int i = int(hist.size()) - 1; i >= 1; --i) {
-                const PTScalars v = velocity_from_vorticity(hist[size_t(i)], config.adi_tol);
-                replay.push_front(nonlinear_term(v, hist[size_t(i)], config.dealias_two_thirds));
-            }
-        stepper.seed(hist, replay, (b - 1) * config.h, b - 1);
-        advance(stepper, b - 1);
-        return r;
     }
-    NSStepper stepper(config, initial_omega);
-    advance(stepper, 0);
+    NSStepper full(config, samples.front());
+    int done = 0;
+    if (bootstrap) {
+        std::deque<PTScalars> nl;  // N of samples[1..], newest first: the explicit extrapolation's old time levels
+        if (!config.disable_nonlinear)
+            for (size_t i = 1; i < samples.size(); ++i)
+                nl.push_back(nonlinear_term(velocity_from_vorticity(samples[i], config.adi_tol), samples[i],
+                                            config.dealias_two_thirds));
+        done = b - 1;
+        full.seed(samples, nl, done * config.h, done);
+    }
+    advance(full, done);
     return r;
 }
 

@@ -710,37 +710,39 @@ void NSStepper::step() {  // ptns.cpp:217-267
     ++steps_;
 }
 
-PT ns_run(const NSConfig& cfg, const PT& omega0, int steps, bool substeps, double* final_time) {  // ptns.cpp:269-324
-    if (substeps && cfg.order > 1 && steps > 0) {
-        const int b = cfg.order, per = 32;
-        NSConfig sub = cfg;
-        sub.order = std::min(2, cfg.order);
-        sub.h = cfg.h / per;
-        NSStepper fine(sub, omega0);
-        std::deque<PT> hist;  // newest first
-        hist.push_front(omega0);
-        for (int big = 1; big <= b - 1; ++big) {
-            for (int s = 0; s < per; ++s) fine.step();
-            hist.push_front(fine.omega());
+// Restatement of ns_run (ptns.cpp:269-324). Ramp start: step the full-order stepper from omega0. Substeps start
+// (:272-311): sample a BDF-min(2, b) run with 32 sub-steps per h at t = h .. (b-1) h, rebuild the nonlinear terms
+// of the older samples, seed the full-order stepper with both histories at steps_taken = b - 1, and finish the run.
+PT ns_run(const NSConfig& cfg, const PT& omega0, int steps, bool substeps, double* final_time) {
+    const int b = cfg.order;
+    const bool bootstrap = substeps && b > 1 && steps > 0;
+    std::deque<PT> samples{omega0};  // newest first
+    if (bootstrap) {
+        constexpr int kSub = 32;
+        NSConfig fine_cfg = cfg;
+        fine_cfg.order = std::min(2, b);
+        fine_cfg.h = cfg.h / kSub;
+        NSStepper fine(fine_cfg, omega0);
+        for (int level = 1; level < b; ++level) {
+            for (int q = 0; q < kSub; ++q) fine.step();
+            samples.push_front(fine.omega());
         }
-        NSStepper stepper(cfg, hist.front());
-        std::deque<PT> replay;
+    }
+    NSStepper full(cfg, samples.front());
+    int done = 0;
+    if (bootstrap) {
+        std::deque<PT> nl;  // N of samples[1..], newest first
         if (!cfg.disable_nonlinear) {
             ModalSolverCache cache(cfg.spec.m, cfg.spec.n, cfg.tol);
-            for (int i = int(hist.size()) - 1; i >= 1; --i) {
-                const PT v = velocity_from_vorticity(hist[size_t(i)], cache);
-                replay.push_front(nonlinear_term(v, hist[size_t(i)], cfg.dealias));
-            }
+            for (size_t i = 1; i < samples.size(); ++i)
+                nl.push_back(nonlinear_term(velocity_from_vorticity(samples[i], cache), samples[i], cfg.dealias));
         }
-        stepper.seed(hist, replay, (b - 1) * cfg.h, b - 1);
-        for (int s = b - 1; s < steps; ++s) stepper.step();
-        if (final_time) *final_time = stepper.time();
-        return stepper.omega();
+        done = b - 1;
+        full.seed(samples, nl, done * cfg.h, done);
     }
-    NSStepper stepper(cfg, omega0);
-    for (int s = 0; s < steps; ++s) stepper.step();
-    if (final_time) *final_time = stepper.time();
-    return stepper.omega();
+    for (int s = done; s < steps; ++s) full.step();
+    if (final_time) *final_time = full.time();
+    return full.omega();
 }
 
 }  // namespace oracle

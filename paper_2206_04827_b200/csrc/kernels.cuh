@@ -121,6 +121,7 @@ struct ThetaCross {
     const double* in[6];
     double* out[3];
     const double2* tw;
+    const double2* twfull;  // p twiddles exp(-2 pi i q / p): the dense-DFT path of theta_cross_kernel (p not 2^k)
     // mode sharding (csrc/shard.cu): this launch covers rows row0 + blockIdx.y; slot s is read from
     // and written to the exchange buffer of its owning rank q (sb[q] <= s < sb[q+1]), rdelta[q]
     // doubles away from the local one (peer memory over NVLink); world == 1: local, delta 0

@@ -761,19 +761,22 @@ bool Pipeline::theta_quad_ok() const {
 
 void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
     const Geo& g = c.gh;
-    if (tp.logp < 0) throw Error(DOMAIN_ERROR, "ccf: the fused theta kernel needs p to be a power of two");
-    ThetaCross t{};
+    ThetaCross t{};  // (p not a power of two: the generic kernel's dense-DFT path)
     t.g = g;
     t.logp = tp.logp;
     if (g.n % 2) throw Error(DOMAIN_ERROR, "ccf: the z-parity split value layout needs even n");
     int tj = 8;  // points per CTA (pairs of +-z)
-    while (tj > 2 && size_t(3) * tj * g.p * sizeof(double2) > 100 * 1024) tj /= 2;
+    const size_t nbuf = tp.logp < 0 ? 2 : 1;  // the dense-DFT path transforms out of place
+    while (tj > 2 && nbuf * 3 * tj * g.p * sizeof(double2) > 100 * 1024) tj /= 2;
+    if (nbuf * 3 * tj * g.p * sizeof(double2) > 200 * 1024)
+        throw Error(DOMAIN_ERROR, "ccf: p too large for the theta kernel's shared-memory tile");
     t.tj = tj;
     for (int i = 0; i < 6; ++i) t.in[i] = v6[i];
     for (int i = 0; i < 3; ++i) t.out[i] = a3[i];
     t.vquad = val_quad_ ? 1 : 0;
     val_quad_ = false;
     t.tw = reinterpret_cast<const double2*>(tp.tw.p);
+    t.twfull = reinterpret_cast<const double2*>(tp.twfull.p);
     // mode sharding: this rank's rows of every slot, each slot in its owner's exchange buffer
     const Shard& sh = c.sh;
     t.row0 = sh.r_lo;
@@ -820,7 +823,7 @@ void Pipeline::theta_cross(const double* const* v6, double* const* a3) {
         const dim3 grid(unsigned((g.nh + np - 1) / np), unsigned(g.mh));
         theta_cross256_kernel<<<grid, theta_cross256_threads(), theta_cross256_smem(), c.stream>>>(t);
     } else {
-        const size_t smem = size_t(3) * tj * g.p * sizeof(double2);
+        const size_t smem = nbuf * 3 * tj * g.p * sizeof(double2);
         const dim3 grid(unsigned((g.nh + tj / 2 - 1) / (tj / 2)), rows);
         theta_cross_kernel<<<grid, 256, smem, c.stream>>>(t);
     }

@@ -546,7 +546,30 @@ __device__ void fft_pow2_block(double2* __restrict__ d, int cnt, int P, int logP
     }
 }
 
-__device__ __forceinline__ int bitrev(int x, int logP) { return __brev(unsigned(x)) >> (32 - logP); }
+__device__ __forceinline__ int bitrev(int x, int logP) { return logP < 0 ? x : int(__brev(unsigned(x)) >> (32 - logP)); }
+
+// Dense DFT of `cnt` complex arrays of length P (any P) from src to dst, natural order both sides:
+// dst[k] = sum_j src[j] exp(sign 2 pi i j k / P); twf[q] = exp(-2 pi i q / P). The fallback for p that is not a
+// power of two (the reference's FFTW plans take any even p, transform.cpp:19-60): O(P^2) per pencil.
+__device__ void dft_dense_block(const double2* __restrict__ src, double2* __restrict__ dst, int cnt, int P,
+                                const double2* __restrict__ twf, int sign) {
+    for (int i = threadIdx.x; i < cnt * P; i += blockDim.x) {
+        const int arr = i / P, k = i % P;
+        const double2* x = src + arr * P;
+        double re = 0.0, im = 0.0;
+        int q = 0;  // j k mod P
+        for (int j = 0; j < P; ++j) {
+            double2 w = twf[q];
+            if (sign > 0) w.y = -w.y;
+            re = fma(x[j].x, w.x, fma(-x[j].y, w.y, re));
+            im = fma(x[j].x, w.y, fma(x[j].y, w.x, im));
+            q += k;
+            if (q >= P) q -= P;
+        }
+        dst[i] = make_double2(re, im);
+    }
+    __syncthreads();
+}
 
 }  // namespace
 
@@ -554,7 +577,8 @@ __device__ __forceinline__ int bitrev(int x, int logP) { return __brev(unsigned(
 // in[0..5] = (v_r, v_theta, v_z, w_r, w_theta, w_z), out[0..2] = (a_r, a_theta, a_z),
 // all in the (r,z)-value / theta-half-spectrum layout [slot][plane][jr][E | O] (z-parity split
 // values: position i < nh holds E_i, i + nh holds O_i, f(+-z_{nh+i}) = E_i +- O_i).
-// Generic path (any power-of-two p): one CTA per (jr, tile of TJ/2 positions = TJ points).
+// Generic path: one CTA per (jr, tile of TJ/2 positions = TJ points); shared-memory radix-2 FFTs for a
+// power-of-two p, dense DFTs (second buffer behind the first) for any other even p (logp < 0).
 __global__ void theta_cross_kernel(ThetaCross t) {
     extern __shared__ double2 sd[];
     const Geo& g = t.g;
@@ -608,7 +632,14 @@ __global__ void theta_cross_kernel(ThetaCross t) {
         Z[(pr * TJ + jl) * P + bitrev(tt, logP)] = z;
     }
     __syncthreads();
-    fft_pow2_block(Z, 3 * TJ, P, logP, tw, +1);
+    double2* Z2 = sd + 3 * TJ * P;  // (dense-DFT path only)
+    if (logP >= 0) {
+        fft_pow2_block(Z, 3 * TJ, P, logP, tw, +1);
+    } else {
+        dft_dense_block(Z, Z2, 3 * TJ, P, t.twfull, +1);
+        for (int e = threadIdx.x; e < 3 * TJ * P; e += blockDim.x) Z[e] = Z2[e];
+        __syncthreads();
+    }
     // ---- pointwise cross product a = v x w (ptns.cpp:127-132); repack (a_r + i a_t), (a_z + 0 i)
     for (int e = threadIdx.x; e < TJ * P; e += blockDim.x) {
         const int jl = e / P, l = e % P;
@@ -635,7 +666,13 @@ __global__ void theta_cross_kernel(ThetaCross t) {
         }
     }
     __syncthreads();
-    fft_pow2_block(Z, 2 * TJ, P, logP, tw, -1);
+    if (logP >= 0) {
+        fft_pow2_block(Z, 2 * TJ, P, logP, tw, -1);
+    } else {  // (bitrev is the identity: the permutation above moved nothing)
+        dft_dense_block(Z, Z2, 2 * TJ, P, t.twfull, -1);
+        for (int e = threadIdx.x; e < 2 * TJ * P; e += blockDim.x) Z[e] = Z2[e];
+        __syncthreads();
+    }
     // ---- unpack X_a = (Z[t] + conj Z[P-t]) / 2, X_b = (Z[t] - conj Z[P-t]) / (2i); c_w = (-1)^w X[w mod P] / P
     const double invp = 1.0 / double(P);
     const int TP = TJ / 2;

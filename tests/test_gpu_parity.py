@@ -164,6 +164,23 @@ def test_golden_fixtures(P):
     assert rel_err(out, h["out"]) < TOL
 
 
+@pytest.mark.parametrize("size", [(16, 16, 12), (12, 10, 6), (16, 12, 20)], ids=lambda s: "x".join(map(str, s)))
+def test_ns_any_even_p(P, O, size):
+    # p that is not a power of two (the reference's FFTW plans take any even p): the theta stage runs dense DFTs
+    m, n, p = size
+    ctx = P.Context(m, n, p)
+    lam, gam = hermitian_coeffs(m, n, p, 0.7, 1) * 1e-2, hermitian_coeffs(m, n, p, 0.7, 2) * 1e-2
+    st, ons = P.NSStepper(ctx, lam, gam, reynolds=100.0, h=1e-3), O.NSStepper(lam, gam, 100.0, 1e-3)
+    st.step(7)
+    ons.step(7)
+    (l, g), (rl, rg) = st.omega(), ons.omega()
+    assert max(rel_err(l, rl), rel_err(g, rg)) < TOL
+    got, ref = ctx.nonlinear_term(gam, lam, lam, gam), O.nonlinear(gam, lam, lam, gam)
+    assert max(rel_err(got[0], ref[0]), rel_err(got[1], ref[1])) < TOL
+    st.close()
+    ctx.close()
+
+
 def test_golden_fixtures_round2(P):
     # per-mode API, lifted data and the substeps bootstrap against the committed oracle vectors
     d = np.load(os.path.join(G, "modal_12x10.npz"))
